@@ -1,0 +1,218 @@
+/*
+ * vsx_b200.h — C ABI of the B200-native CityGS-X training hot path.
+ *
+ * Every entry point takes caller-owned DEVICE buffers as raw pointers plus
+ * explicit element counts, is asynchronous on the given CUDA stream, and
+ * returns a status code (VSX_OK or a negative VSX_ERR_*). There are no torch
+ * types in any signature. Host callers (the Python shim in
+ * paper_2503_23044_b200/, or a ctypes/cgo binding) own allocation.
+ *
+ * Reference interface each group replaces (paths relative to
+ * /root/reference/pkg/src/voxsplat):
+ *   vsx_cull / vsx_select          scene.py:239-259 active_mask (+ lod_for_distance :232-236)
+ *   vsx_decode_fwd                 decoder.py:142-180 decode_inputs/_head_forward/decode_arrays,
+ *                                  decoder.py:210-250 decode_active (canonical order)
+ *   vsx_project_fwd                renderer.py:144-204 project_splats (EWA + (z,gid) order)
+ *   vsx_sort_pairs_u64/_u32        renderer.py:197 np.lexsort((gid, z)) (stable LSD radix)
+ *   vsx_bin                        renderer.py:207-226 bin_splats
+ *   vsx_raster_fwd                 renderer.py:242-301 _blend_padded + _finalize, :390-449 rasterize_view
+ *   vsx_raster_bwd                 renderer.py:347-367 rasterize_backward (autograd of the blend)
+ *   vsx_project_bwd                autograd of project_splats (trainer.py:330)
+ *   vsx_decode_bwd                 decoder.py:267-292 decoder_backward (autograd of decode)
+ *   vsx_l1_loss / vsx_depth_loss   losses.py:43-53 bl_rgb_loss, losses.py:65-84 e_depth_loss
+ *   vsx_adam                       trainer.py:220-247 TrainState._adam + apply_*_grads
+ *   vsx_exchange_*                 renderer.py:452-477 transfer_gaussians (real C1 payload packing)
+ */
+#ifndef VSX_B200_H
+#define VSX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VSX_OK 0
+#define VSX_ERR_INVALID -1   /* -> errors.InvalidInput */
+#define VSX_ERR_NUMERICAL -2 /* -> errors.NumericalError */
+#define VSX_ERR_CONTRACT -3  /* -> errors.ContractViolation */
+#define VSX_ERR_CUDA -4      /* CUDA launch/runtime failure */
+#define VSX_ERR_CAPACITY -5  /* workspace too small -> errors.ResourceError */
+
+/* Device-status bits written by kernels into a caller-owned int32 word. */
+#define VSX_STATUS_NONPD 1     /* det(cov2d) <= 0 (renderer.py:182-183) */
+#define VSX_STATUS_NONFINITE 2 /* non-finite decoder output (decoder.py:246-249) */
+
+typedef void *vsx_stream; /* cudaStream_t */
+
+/* Pinhole camera: x_cam = R x_world + t (geometry.py:68-112). center = -R^T t
+ * is computed on the host so it is bit-identical to CameraView.center. */
+typedef struct vsx_camera {
+  double r[9];
+  double t[3];
+  double center[3];
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} vsx_camera;
+
+/* Splat record, 64 bytes, one per projected gaussian (sorted order). The
+ * mean is kept in float64 so per-tile local pixel offsets are exact even at
+ * 4K; everything the compositor multiplies is float32. */
+typedef struct vsx_splat {
+  double mean2d[2];
+  float conic[3]; /* (A, B, C) = inverse 2D covariance (c, -b, a)/det */
+  float opacity;
+  float color[3];
+  float normal[3]; /* camera-frame normal, flipped to face the camera */
+  float plane_d;   /* n_cam . mu_cam */
+  uint32_t src;    /* index of the gaussian in the decode batch */
+} vsx_splat;
+
+/* Decoder weights, all float32 device pointers, reference layouts
+ * (decoder.py:39-78): w1 (36,64) row-major, b1 (64), w2 (64,out), b2 (out),
+ * out = n, 3n, 7n for opacity, color, cov. */
+typedef struct vsx_decoder {
+  const float *w1[3];
+  const float *b1[3];
+  const float *w2[3];
+  const float *b2[3];
+  int32_t n;
+} vsx_decoder;
+
+typedef struct vsx_decoder_grads {
+  float *w1[3];
+  float *b1[3];
+  float *w2[3];
+  float *b2[3];
+} vsx_decoder_grads;
+
+const char *vsx_last_error(void);
+int vsx_version(void);
+
+/* ---- generic device primitives ---------------------------------------- */
+/* Workspace bytes needed by vsx_sort_pairs_* / vsx_select / vsx_scan for n items. */
+size_t vsx_sort_ws_bytes(int64_t n);
+size_t vsx_scan_ws_bytes(int64_t n);
+/* Exclusive scan of uint32 counts: out[i] = sum(in[0:i]); out[n] = total. */
+int vsx_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, void *ws, size_t ws_bytes,
+                 vsx_stream s);
+/* Stable LSD radix sort of (key, value) pairs on key bits [begin_bit, end_bit).
+ * Bytes whose value is identical for all keys are skipped (one host sync). */
+int vsx_sort_pairs_u64(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
+                       uint32_t *vals_out, int64_t n, int32_t begin_bit, int32_t end_bit,
+                       void *ws, size_t ws_bytes, vsx_stream s);
+int vsx_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                       uint32_t *vals_out, int64_t n, int32_t begin_bit, int32_t end_bit,
+                       void *ws, size_t ws_bytes, vsx_stream s);
+/* Ordered stream compaction: out_idx = flatnonzero(flags), *out_count on device. */
+int vsx_select(const uint8_t *flags, int64_t n, int32_t *out_idx, uint32_t *out_count,
+               void *ws, size_t ws_bytes, vsx_stream s);
+
+/* ---- K1: frustum + LoD culling (scene.py:232-259) --------------------- */
+int vsx_cull(const double *centers, const int32_t *level, int64_t n_anchors, int32_t lod_count,
+             double lod_ref, int32_t lod_bias, vsx_camera cam, uint8_t *mask, vsx_stream s);
+
+/* ---- K2: anchor -> gaussian decode (decoder.py:142-180) --------------- */
+/* active: ascending flat anchor ids (n_active). Per-anchor params are flat
+ * level-major: emb (A,32) f32, log_scale (A,3) f32 (l_v = exp in float64),
+ * offsets (A,n,3) f32, centers (A,3) f64. Outputs are gaussian-major
+ * (n_active*n rows). cache_h (n_active,192) and cache_o (n_active,11n) keep
+ * the hidden activations and raw head outputs for vsx_decode_bwd (may be
+ * NULL for inference). */
+int vsx_decode_fwd(vsx_decoder W, const int32_t *active, int32_t n_active, const double *centers,
+                   const float *emb, const float *log_scale, const float *offsets,
+                   vsx_camera cam, double lod_ref, double max_scale, double *means,
+                   float *opacity, float *color, float *scale, float *quat, float *normal,
+                   float *cache_h, float *cache_o, int32_t *status, vsx_stream s);
+
+/* ---- K3: projection (renderer.py:144-204) ----------------------------- */
+/* Writes one unsorted record per gaussian plus a sort key (float64 z bits,
+ * or UINT64_MAX when z <= 0.01) and the 3-sigma radius; *n_kept counts
+ * z > 0.01. Sorting (key, index) stably gives the reference (z, gid) order
+ * when the batch is in ascending-gid order. */
+int vsx_project_fwd(const double *means, const float *opacity, const float *color,
+                    const float *scale, const float *quat, const float *normal, int32_t n,
+                    vsx_camera cam, vsx_splat *rec, uint64_t *zkey, double *radius,
+                    uint32_t *n_kept, int32_t *status, vsx_stream s);
+/* Gather records/radius into sorted order: dst[i] = src[order[i]], i < n. */
+int vsx_gather_splats(const vsx_splat *rec, const double *radius, const uint32_t *order,
+                      int32_t n, vsx_splat *rec_sorted, double *radius_sorted, vsx_stream s);
+
+/* ---- K4: tile binning (renderer.py:207-226) --------------------------- */
+/* Phase 1: per-splat tile counts + per-tile histogram. */
+int vsx_bin_count(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
+                  int32_t height, uint32_t *splat_tiles, uint32_t *tile_counts, vsx_stream s);
+/* Phase 2: emit (tile, rank) pairs at exclusive-scan offsets of splat_tiles. */
+int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
+                 int32_t height, const uint32_t *splat_offsets, uint32_t *isect_tile,
+                 uint32_t *isect_rank, vsx_stream s);
+
+/* ---- K5: compositing forward (renderer.py:242-301, 390-449) ----------- */
+/* tile_offsets (T+1) CSR over tile_list (sorted ranks). Outputs are HWC
+ * images (rgb/normal/raw_normal 3 channels) plus per-pixel backward state
+ * (t_final, n_contrib). Any output pointer except t_final/n_contrib may be
+ * NULL to skip it. */
+int vsx_raster_fwd(const vsx_splat *rec, const uint32_t *tile_offsets, const uint32_t *tile_list,
+                   vsx_camera cam, float *rgb, float *alpha, float *depth, float *normal,
+                   float *raw_normal, uint8_t *valid, float *t_final, int32_t *n_contrib,
+                   vsx_stream s);
+
+/* ---- K6: compositing backward ------------------------------------------ */
+/* Pixel cotangents (any may be NULL = zero) -> per-splat gradients
+ * (sorted order, float32 x 13: mean2d 2, conic 3, opacity, color 3,
+ * normal 3, plane_d), accumulated (+=) into grad_splat. */
+int vsx_raster_bwd(const vsx_splat *rec, const uint32_t *tile_offsets, const uint32_t *tile_list,
+                   vsx_camera cam, const float *rgb, const float *alpha, const float *depth,
+                   const float *raw_normal, const float *t_final, const int32_t *n_contrib,
+                   const float *g_rgb, const float *g_alpha, const float *g_depth,
+                   const float *g_normal, const float *g_raw_normal, float *grad_splat,
+                   vsx_stream s);
+
+/* ---- K7: projection backward ------------------------------------------- */
+/* grad_splat (sorted, 13 floats) -> per-gaussian grads (+=, batch order):
+ * means 3, opacity, color 3, scale 3, quat 4 (w.r.t. the normalised quat),
+ * normal 3. */
+int vsx_project_bwd(const double *means, const float *scale, const float *quat,
+                    const float *normal, const vsx_splat *rec_sorted, const float *grad_splat,
+                    int32_t n_sorted, vsx_camera cam, float *g_means, float *g_opacity,
+                    float *g_color, float *g_scale, float *g_quat, float *g_normal,
+                    vsx_stream s);
+
+/* ---- K8: decode backward ------------------------------------------------ */
+/* Per-gaussian grads -> decoder weight grads (+=) and per-anchor grads (+=)
+ * for emb (A,32), log_scale (A,3), offsets (A,n,3). scale/quat are the
+ * decoded (clamped) scales and normalised quaternions of the forward. */
+size_t vsx_decode_bwd_ws_bytes(int32_t n, int32_t n_active);
+int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t *active, int32_t n_active,
+                   const double *centers, const float *emb, const float *log_scale,
+                   const float *offsets, vsx_camera cam, double lod_ref, double max_scale,
+                   const float *cache_h, const float *cache_o, const float *scale,
+                   const float *quat, const float *g_means, const float *g_opacity,
+                   const float *g_color, const float *g_scale, const float *g_quat,
+                   const float *g_normal, float *g_emb, float *g_log_scale, float *g_offsets,
+                   void *ws, size_t ws_bytes, vsx_stream s);
+
+/* ---- K9: losses --------------------------------------------------------- */
+/* L1: loss_accum[0] += sum|r - g| (float64); grad = sign(r - g) * scale. */
+int vsx_l1_loss(const float *rendered, const float *target, int64_t n, float scale,
+                double *loss_accum, float *grad, vsx_stream s);
+/* Masked depth L1 (losses.py:65-84): mask = prior_valid & valid;
+ * sums[0] += sum |d - p| * mask, counts[0] += sum mask; with grad != NULL
+ * writes grad = sign(d - p) * mask * (*scale) where scale is a DEVICE
+ * float (w2 / (B_depth * count)), so no host sync is needed. */
+int vsx_depth_loss(const float *depth, const uint8_t *valid, const float *prior,
+                   const uint8_t *prior_valid, int64_t n, double *sums, uint32_t *counts,
+                   const float *scale, float *grad, vsx_stream s);
+
+/* ---- K10: fused Adam (trainer.py:220-247) ------------------------------- */
+/* One launch over n_seg contiguous segments; seg_begin (n_seg+1, host) are
+ * element offsets into the flat param/grad/m/v buffers, lr (n_seg, host). */
+int vsx_adam(float *param, const float *grad, float *m, float *v, int32_t n_seg,
+             const int64_t *seg_begin, const double *lr, double beta1, double beta2, double eps,
+             int32_t step, vsx_stream s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSX_B200_H */

@@ -1,0 +1,284 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference implementation.
+
+Run in the build container only (it imports ``/root/reference/pkg/src``,
+which does not exist on the GPU box):
+
+    python oracle/make_golden.py            # writes tests/golden/*.npz
+
+The fixtures pin ``oracle/pipeline.py`` (see tests/test_oracle_golden.py).
+Every array here is produced by calling the reference's own public functions;
+nothing is recomputed by this repository's code.
+"""
+
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+REF = "/root/reference/pkg/src"
+OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
+
+
+def _ref():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import voxsplat  # noqa: F401
+    from voxsplat import decoder, geometry, partition, renderer, scene, trainer, losses
+    return decoder, geometry, partition, renderer, scene, trainer, losses
+
+
+def _view_arrays(prefix: str, view) -> dict:
+    return {f"{prefix}_r": view.r, f"{prefix}_t": view.t,
+            f"{prefix}_intr": np.array([view.fx, view.fy, view.cx, view.cy]),
+            f"{prefix}_size": np.array([view.width, view.height]),
+            f"{prefix}_center": view.center}
+
+
+def _csr(tiles) -> tuple[np.ndarray, np.ndarray]:
+    counts = np.array([len(t) for t in tiles], np.int64)
+    offsets = np.concatenate([[0], np.cumsum(counts)])
+    lists = np.concatenate([np.asarray(t, np.int64) for t in tiles]) if len(tiles) else np.zeros(0)
+    return offsets, lists.astype(np.int64)
+
+
+def _scene_arrays(scene) -> dict:
+    out = {"lod_ref": np.array(scene.lod_ref_distance), "lod_bias": np.array(scene.lod_bias),
+           "base_voxel": np.array(scene.base_voxel_size), "n": np.array(scene.offsets_per_voxel),
+           "lod_count": np.array(scene.lod_count)}
+    for k, lv in enumerate(scene.levels):
+        out[f"grid{k}"] = lv.grid
+        out[f"emb{k}"] = lv.embeddings
+        out[f"off{k}"] = lv.offsets
+        out[f"scl{k}"] = lv.scales
+    return out
+
+
+def _render_dump(prefix, renderer, view, scene, asg, params) -> dict:
+    out = {}
+    from voxsplat.decoder import decode_active
+    batch = decode_active(params, scene, view)
+    out.update({f"{prefix}_dec_{k}": getattr(batch, k).numpy()
+                for k in ("means", "opacities", "colors", "scales", "quats", "normals")})
+    out[f"{prefix}_dec_gid"] = batch.gid
+    splats = renderer.project_splats(batch, view)
+    out.update({f"{prefix}_spl_{k}": getattr(splats, k).numpy()
+                for k in ("mean2d", "conic", "color", "opacity", "normal_cam", "plane_d")})
+    out.update({f"{prefix}_spl_{k}": getattr(splats, k) for k in ("radius", "zkey", "gid")})
+    off, lists = _csr(renderer.bin_splats(splats, view.width, view.height))
+    out[f"{prefix}_tile_off"], out[f"{prefix}_tile_list"] = off, lists
+    targets, counts = renderer.rasterize_view(splats, view)
+    for k in ("rgb", "depth", "normal", "alpha", "valid", "raw_normal"):
+        out[f"{prefix}_img_{k}"] = getattr(targets, k).numpy()
+    out[f"{prefix}_counts"] = counts
+    return out
+
+
+def make_scene_small():
+    decoder, geometry, partition, renderer, scene_m, trainer, _ = _ref()
+    rng = np.random.default_rng(0)
+    pts = scene_m.SparsePoints(positions=rng.uniform(-1, 1, size=(150, 3)))
+    scene = scene_m.build_hierarchy(pts, 0.5, 3, offsets_per_voxel=2, seed=0)
+    r, t = geometry.look_at(np.array([0.0, -3.0, 1.0]), np.zeros(3))
+    far = geometry.CameraView(0, 48, 48, 40.0, 40.0, 23.5, 23.5, r, t)
+    r2, t2 = geometry.look_at(np.array([0.3, -1.2, 0.6]), np.array([0.0, 0.2, 0.0]))
+    near = geometry.CameraView(1, 40, 36, 30.0, 30.0, 19.5, 17.5, r2, t2)
+    scene.set_lod_reference([far])
+    params = decoder.DecoderParams.init(2, seed=0, scale_bias=float(np.log(0.1)))
+    asg = partition.assign_voxels(scene, 1)
+    out = {"points": pts.positions, **_scene_arrays(scene), **_view_arrays("far", far),
+           **_view_arrays("near", near)}
+    for name, t_ in params.tensors.items():
+        out[f"w_{name}"] = t_.numpy()
+    for tag, view in (("far", far), ("near", near)):
+        for k in range(scene.lod_count):
+            out[f"{tag}_mask{k}"] = scene_m.active_mask(scene, k, view)
+        out.update(_render_dump(tag, renderer, view, scene, asg, params))
+    np.savez_compressed(OUT / "scene_small.npz", **out)
+
+
+def _leaf_case(rng, count, view):
+    """Random gaussians in front of an identity camera with mixed sizes."""
+    z = rng.uniform(1.2, 4.0, size=count)
+    u = rng.uniform(-4.0, view.width + 4.0, size=count)
+    v = rng.uniform(-4.0, view.height + 4.0, size=count)
+    means = np.stack([(u - view.cx) / view.fx * z, (v - view.cy) / view.fy * z, z], -1)
+    scales = rng.uniform(0.01, 0.25, size=(count, 3))
+    quats = rng.normal(size=(count, 4))
+    quats /= np.linalg.norm(quats, axis=-1, keepdims=True)
+    return {"means": means, "opacities": rng.uniform(0.05, 0.95, size=count),
+            "colors": rng.uniform(0.0, 1.0, size=(count, 3)), "scales": scales,
+            "quats": quats}
+
+
+def make_raster_leaf():
+    decoder, geometry, partition, renderer, scene_m, trainer, _ = _ref()
+    out = {}
+    for case, (seed, count, w, h, f) in enumerate([(1, 60, 40, 24, 30.0),
+                                                   (2, 300, 64, 48, 50.0)]):
+        rng = np.random.default_rng(seed)
+        view = geometry.CameraView(case, w, h, f, f, (w - 1) / 2.0, (h - 1) / 2.0,
+                                   np.eye(3), np.zeros(3))
+        arr = _leaf_case(rng, count, view)
+        batch = renderer.make_leaf_gaussians(arr["means"], arr["opacities"], arr["colors"],
+                                             arr["scales"], arr["quats"], requires_grad=True)
+        splats = renderer.project_splats(batch, view)
+        targets, counts = renderer.rasterize_view(splats, view)
+        off, lists = _csr(renderer.bin_splats(splats, view.width, view.height))
+        rn = targets.raw_normal.detach().numpy()
+        rx = (np.arange(w) - view.cx) / view.fx
+        ry = (np.arange(h) - view.cy) / view.fy
+        denom = rn[..., 0] * rx[None, :] + rn[..., 1] * ry[:, None] + rn[..., 2]
+        guard = (targets.alpha.detach().numpy() > 0.05) & (np.abs(denom) > 1e-2)
+        cot = {"rgb": rng.normal(size=(h, w, 3)), "alpha": rng.normal(size=(h, w)),
+               "depth": rng.normal(size=(h, w)) * guard,
+               "normal": rng.normal(size=(h, w, 3)) * guard[..., None]}
+        grads = renderer.rasterize_backward(
+            splats, {"rgb": targets.rgb, "alpha": targets.alpha, "depth": targets.depth,
+                     "normal": targets.normal}, cot)
+        p = f"c{case}"
+        out.update({f"{p}_{k}": a for k, a in arr.items()})
+        out.update(_view_arrays(p, view))
+        out.update({f"{p}_spl_{k}": getattr(splats, k).detach().numpy()
+                    for k in ("mean2d", "conic", "color", "opacity", "normal_cam", "plane_d")})
+        out.update({f"{p}_spl_{k}": getattr(splats, k) for k in ("radius", "zkey", "gid")})
+        out[f"{p}_tile_off"], out[f"{p}_tile_list"] = off, lists
+        for k in ("rgb", "depth", "normal", "alpha", "valid", "raw_normal"):
+            out[f"{p}_img_{k}"] = getattr(targets, k).detach().numpy()
+        out.update({f"{p}_cot_{k}": c for k, c in cot.items()})
+        out.update({f"{p}_grad_{k}": g.numpy() for k, g in grads.items()})
+    np.savez_compressed(OUT / "raster_leaf.npz", **out)
+
+
+def _cfg1_scene(scene_m, geometry):
+    rng = np.random.default_rng(0)
+    pts = np.stack([rng.uniform(-1, 1, 120000), rng.uniform(-1, 1, 120000),
+                    rng.uniform(-0.005, 0.005, 120000)], -1)
+    scene = scene_m.build_hierarchy(scene_m.SparsePoints(pts), base_voxel_size=0.02,
+                                    lod_count=1, offsets_per_voxel=10, seed=0)
+    f = 64.0 / np.tan(np.radians(30.0))
+    views = []
+    for i in range(4):
+        eye = np.array([0.3 * np.cos(np.pi * i / 2), 0.3 * np.sin(np.pi * i / 2), 2.2])
+        r, t = geometry.look_at(eye, np.zeros(3), up=(0.0, 1.0, 0.0))
+        views.append(geometry.CameraView(i, 128, 128, f, f, 63.5, 63.5, r, t))
+    scene.set_lod_reference(views)
+    images = [rng.uniform(0, 1, (128, 128, 3)) for _ in range(4)]
+    return scene, views, images
+
+
+def _reference_grads(trainer, renderer, losses, state, views, images):
+    """The reference train_step's gradient block (trainer.py:270-339), via its own API."""
+    dstate = state.decode_state()
+    targets, means = [], []
+    for view in views:
+        batch, _ = renderer.transfer_gaussians(view, state.scene, state.assignment,
+                                               state.replicas[0], state=dstate,
+                                               keep_graph=True)
+        splats = renderer.project_splats(batch, view)
+        t, _ = renderer.rasterize_view(splats, view, renderer.ALL_TASKS)
+        targets.append(t)
+        means.append(batch.means)
+    loss = losses.bl_rgb_loss([t.rgb for t in targets],
+                              [torch.as_tensor(im) for im in images])
+    dec = state.replicas[0].tensors
+    names = list(dec)
+    lv = [state.level_state[0][k] for k in ("embeddings", "log_scales", "offsets")]
+    g = torch.autograd.grad(loss, [dec[n] for n in names] + lv, allow_unused=True)
+    return float(loss), {n: x.numpy() for n, x in zip(names, g[:len(names)])}, \
+        [x.numpy() for x in g[len(names):]]
+
+
+def make_cfg1():
+    decoder, geometry, partition, renderer, scene_m, trainer, losses = _ref()
+    t0 = time.time()
+    torch.set_num_threads(8)
+    scene, views, images = _cfg1_scene(scene_m, geometry)
+    out = {"lod_ref": np.array(scene.lod_ref_distance), "grid0": scene.levels[0].grid}
+    for i, v in enumerate(views):
+        out[f"mask{i}"] = scene_m.active_mask(scene, 0, v)
+    cfg = trainer.TrainConfig(total_steps=100, batch_size=4, workers=1, step2_start=100,
+                              step3_start=100, growth_stop=0, log_every=0)
+    state = trainer.make_state(scene, cfg)
+    asg = state.assignment
+    params = state.replicas[0]
+    dump = _render_dump("v0", renderer, views[0], scene, asg, params)
+    keep = ("v0_spl_zkey", "v0_spl_gid", "v0_spl_radius", "v0_tile_off", "v0_tile_list",
+            "v0_img_rgb", "v0_img_depth", "v0_img_alpha", "v0_img_valid", "v0_counts")
+    out.update({k: dump[k] for k in keep})
+    loss, dgrads, lgrads = _reference_grads(trainer, renderer, losses, state, views, images)
+    rows = np.random.default_rng(7).choice(scene.levels[0].count, 512, replace=False)
+    out["loss0"] = np.array(loss)
+    out.update({f"grad_{k}": a for k, a in dgrads.items()})
+    out["rows"] = rows
+    for name, a in zip(("emb", "log_scales", "offsets"), lgrads):
+        out[f"lgrad_{name}"] = a[rows]
+    reports = [trainer.train_step(state, views, images) for _ in range(2)]
+    out["report_rgb"] = np.array([r.rgb for r in reports])
+    for k, t_ in state.replicas[0].tensors.items():
+        out[f"post_{k}"] = t_.detach().numpy()
+    for name, key in (("emb", "embeddings"), ("log_scales", "log_scales"),
+                      ("offsets", "offsets")):
+        out[f"post_lv_{name}"] = state.level_state[0][key].detach().numpy()[rows]
+    np.savez_compressed(OUT / "cfg1.npz", **out)
+    print(f"cfg1 golden in {time.time() - t0:.0f}s")
+
+
+def make_train_small():
+    decoder, geometry, partition, renderer, scene_m, trainer, losses = _ref()
+    from voxsplat.depth_prior import EnhancedDepthMap
+    rng = np.random.default_rng(3)
+    pts = scene_m.SparsePoints(positions=np.concatenate([
+        np.stack([rng.uniform(-1, 1, 400), rng.uniform(-1, 1, 400),
+                  rng.uniform(-0.05, 0.05, 400)], -1),
+        rng.uniform(-0.3, 0.3, size=(100, 3)) + np.array([0.0, 0.0, 0.3])]))
+    views = []
+    for i in range(3):
+        ang = 2 * np.pi * i / 3
+        r, t = geometry.look_at(np.array([1.6 * np.cos(ang), 1.6 * np.sin(ang), 1.4]),
+                                np.zeros(3))
+        views.append(geometry.CameraView(i, 48, 40, 40.0, 40.0, 23.5, 19.5, r, t))
+    scene = scene_m.build_hierarchy(pts, 0.25, 2, offsets_per_voxel=3, seed=4, views=views)
+    out = {"points": pts.positions, **_scene_arrays(scene)}
+    for i, v in enumerate(views):
+        out.update(_view_arrays(f"v{i}", v))
+    images = [rng.uniform(0, 1, (40, 48, 3)) for _ in views]
+    priors = []
+    for i, v in enumerate(views):
+        d = rng.uniform(1.0, 2.5, (40, 48))
+        valid = rng.uniform(size=(40, 48)) > 0.25
+        priors.append(EnhancedDepthMap(values=np.where(valid, d, 0.0), valid=valid,
+                                       min_roundtrip=np.zeros((40, 48)), tau=1.0))
+        out[f"img{i}"] = images[i]
+        out[f"prior{i}"] = priors[i].values
+        out[f"pvalid{i}"] = valid
+    for tag, s2 in (("rgb", 8), ("depth", 0)):
+        scene_t = scene_m.build_hierarchy(pts, 0.25, 2, offsets_per_voxel=3, seed=4,
+                                          views=views)
+        cfg = trainer.TrainConfig(total_steps=8, batch_size=3, workers=1, step2_start=s2,
+                                  step3_start=8, growth_stop=0, log_every=0)
+        state = trainer.make_state(scene_t, cfg)
+        reps = []
+        for _ in range(3):
+            reps.append(trainer.train_step(state, views, images,
+                                           priors if tag == "depth" else None))
+        out[f"{tag}_loss"] = np.array([[r.total, r.rgb, r.depth] for r in reps])
+        out[f"{tag}_supervised"] = np.array([r.supervised_depth_px for r in reps])
+        for k, t_ in state.replicas[0].tensors.items():
+            out[f"{tag}_post_{k}"] = t_.detach().numpy()
+        for k in range(scene_t.lod_count):
+            for key in ("embeddings", "log_scales", "offsets"):
+                out[f"{tag}_post_lv{k}_{key}"] = state.level_state[k][key].detach().numpy()
+    np.savez_compressed(OUT / "train_small.npz", **out)
+
+
+if __name__ == "__main__":
+    OUT.mkdir(parents=True, exist_ok=True)
+    which = sys.argv[1:] or ["scene_small", "raster_leaf", "train_small", "cfg1"]
+    for name in which:
+        t0 = time.time()
+        globals()[f"make_{name}"]()
+        print(f"{name}: {time.time() - t0:.1f}s")

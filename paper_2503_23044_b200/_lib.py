@@ -1,0 +1,106 @@
+"""ctypes binding of libvsx_b200.so (the C ABI in include/vsx_b200.h).
+
+The library is built in-tree (``make -C paper_2503_23044_b200/csrc``) and
+loaded from the package directory. There is no fallback: if the shared
+object is missing or CUDA is unavailable, every device entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import raise_for_status
+from .geometry import VsxCamera
+
+LIB_PATH = Path(__file__).resolve().parent / "libvsx_b200.so"
+
+c_void_p = ctypes.c_void_p
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_f32 = ctypes.c_float
+c_f64 = ctypes.c_double
+c_size = ctypes.c_size_t
+
+
+class VsxDecoder(ctypes.Structure):
+    _fields_ = [("w1", c_void_p * 3), ("b1", c_void_p * 3), ("w2", c_void_p * 3),
+                ("b2", c_void_p * 3), ("n", c_i32)]
+
+
+class VsxDecoderGrads(ctypes.Structure):
+    _fields_ = [("w1", c_void_p * 3), ("b1", c_void_p * 3), ("w2", c_void_p * 3),
+                ("b2", c_void_p * 3)]
+
+
+P = c_void_p
+_SIGS = {
+    "vsx_version": ([], c_i32),
+    "vsx_last_error": ([], ctypes.c_char_p),
+    "vsx_sort_ws_bytes": ([c_i64], c_size),
+    "vsx_scan_ws_bytes": ([c_i64], c_size),
+    "vsx_scan_u32": ([P, P, c_i64, P, c_size, P], c_i32),
+    "vsx_sort_pairs_u64": ([P, P, P, P, c_i64, c_i32, c_i32, P, c_size, P], c_i32),
+    "vsx_sort_pairs_u32": ([P, P, P, P, c_i64, c_i32, c_i32, P, c_size, P], c_i32),
+    "vsx_select": ([P, c_i64, P, P, P, c_size, P], c_i32),
+    "vsx_cull": ([P, P, c_i64, c_i32, c_f64, c_i32, VsxCamera, P, P], c_i32),
+    "vsx_decode_fwd": ([VsxDecoder, P, c_i32, P, P, P, P, VsxCamera, c_f64, c_f64,
+                        P, P, P, P, P, P, P, P, P, P], c_i32),
+    "vsx_decode_bwd_ws_bytes": ([c_i32, c_i32], c_size),
+    "vsx_decode_bwd": ([VsxDecoder, VsxDecoderGrads, P, c_i32, P, P, P, P, VsxCamera, c_f64,
+                        c_f64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, c_size, P], c_i32),
+    "vsx_project_fwd": ([P, P, P, P, P, P, c_i32, VsxCamera, P, P, P, P, P, P], c_i32),
+    "vsx_gather_splats": ([P, P, P, c_i32, P, P, P], c_i32),
+    "vsx_bin_count": ([P, P, c_i32, c_i32, c_i32, P, P, P], c_i32),
+    "vsx_bin_emit": ([P, P, c_i32, c_i32, c_i32, P, P, P, P], c_i32),
+    "vsx_raster_fwd": ([P, P, P, VsxCamera, P, P, P, P, P, P, P, P, P], c_i32),
+    "vsx_raster_bwd": ([P, P, P, VsxCamera, P, P, P, P, P, P, P, P, P, P, P, P, P], c_i32),
+    "vsx_project_bwd": ([P, P, P, P, P, P, c_i32, VsxCamera, P, P, P, P, P, P, P], c_i32),
+    "vsx_l1_loss": ([P, P, c_i64, c_f32, P, P, P], c_i32),
+    "vsx_depth_loss": ([P, P, P, P, c_i64, P, P, P, P, P], c_i32),
+    "vsx_adam": ([P, P, P, P, c_i32, P, P, c_f64, c_f64, c_f64, c_i32, P], c_i32),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load(path: os.PathLike | None = None) -> ctypes.CDLL:
+    """Load (once) and type the shared library; raises if it is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise ImportError(f"{p} not built: run `make -C paper_2503_23044_b200/csrc` "
+                          "(or __graft_entry__.build())")
+    lib = ctypes.CDLL(str(p))
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke an entry point and raise the mapped exception on failure."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        raise_for_status(rc, name, lib.vsx_last_error().decode(errors="replace"))
+
+
+def ptr(t) -> c_void_p:
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return c_void_p(0)
+    return c_void_p(t.data_ptr())
+
+
+def stream() -> c_void_p:
+    import torch
+    return c_void_p(torch.cuda.current_stream().cuda_stream)

@@ -1,0 +1,114 @@
+// Shared device helpers for the vsx_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/vsx_b200.h"
+
+#define VSX_CUDA_TRY(expr)                                   \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) {                                 \
+      vsx_set_error("%s: %s", #expr, cudaGetErrorString(_e)); \
+      return VSX_ERR_CUDA;                                   \
+    }                                                        \
+  } while (0)
+
+#define VSX_LAUNCH_CHECK(name)                                          \
+  do {                                                                  \
+    cudaError_t _e = cudaGetLastError();                                \
+    if (_e != cudaSuccess) {                                            \
+      vsx_set_error("%s launch: %s", name, cudaGetErrorString(_e));     \
+      return VSX_ERR_CUDA;                                              \
+    }                                                                   \
+  } while (0)
+
+#define VSX_REQUIRE(cond, ...)    \
+  do {                            \
+    if (!(cond)) {                \
+      vsx_set_error(__VA_ARGS__); \
+      return VSX_ERR_INVALID;     \
+    }                             \
+  } while (0)
+
+void vsx_set_error(const char *fmt, ...);
+
+namespace vsx {
+
+constexpr int kTile = 16;
+constexpr int kTilePixels = kTile * kTile;
+constexpr int kEmbed = 32;
+constexpr int kInDim = kEmbed + 4;
+constexpr int kHidden = 64;
+constexpr int kHeads = 3;
+
+constexpr double kZNear = 0.01;
+constexpr float kAlphaClamp = 0.99f;
+constexpr float kEarlyStopT = 1e-4f;
+constexpr float kAlphaValidMin = 1e-4f;
+constexpr float kDenomGuard = 1e-6f;
+constexpr double kLowpass = 0.3;
+constexpr double kMinScale = 1e-6;
+
+inline cudaStream_t as_stream(vsx_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int grid_for(int64_t n, int block) { return (int)((n + block - 1) / block); }
+
+// Explicitly rounded float64 ops: nvcc would otherwise contract a*b+c into an
+// FMA, which numpy/torch elementwise code never does. Decisions that must be
+// bit-exact against the reference (culling, projection keys, binning) use these.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// x_cam = R x + t with the row dot products evaluated left to right.
+__device__ __forceinline__ void cam_transform(const vsx_camera &c, double x, double y, double z,
+                                              double &ox, double &oy, double &oz) {
+  ox = dadd(dadd(dadd(dmul(c.r[0], x), dmul(c.r[1], y)), dmul(c.r[2], z)), c.t[0]);
+  oy = dadd(dadd(dadd(dmul(c.r[3], x), dmul(c.r[4], y)), dmul(c.r[5], z)), c.t[1]);
+  oz = dadd(dadd(dadd(dmul(c.r[6], x), dmul(c.r[7], y)), dmul(c.r[8], z)), c.t[2]);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Quaternion (w,x,y,z) -> row-major rotation, reference decoder.py:108-114.
+template <typename T>
+__device__ __forceinline__ void quat_to_rot(T w, T x, T y, T z, T *m) {
+  m[0] = T(1) - T(2) * (y * y + z * z);
+  m[1] = T(2) * (x * y - w * z);
+  m[2] = T(2) * (x * z + w * y);
+  m[3] = T(2) * (x * y + w * z);
+  m[4] = T(1) - T(2) * (x * x + z * z);
+  m[5] = T(2) * (y * z - w * x);
+  m[6] = T(2) * (x * z - w * y);
+  m[7] = T(2) * (y * z + w * x);
+  m[8] = T(1) - T(2) * (x * x + y * y);
+}
+
+// Index of the smallest of three scales, first index on ties (torch.argmin).
+template <typename T>
+__device__ __forceinline__ int argmin3(T a, T b, T c) {
+  int i = 0;
+  T best = a;
+  if (b < best) { best = b; i = 1; }
+  if (c < best) { i = 2; }
+  return i;
+}
+
+}  // namespace vsx

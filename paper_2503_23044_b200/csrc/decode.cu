@@ -1,0 +1,546 @@
+// K2 / K8 — shared anchor decoder (3 tanh MLP heads 36 -> 64 -> {n,3n,7n}).
+//
+// Forward restates voxsplat decoder.py:142-180 (decode_inputs, _head_forward,
+// decode_arrays) for the active anchors of one view, emitting gaussians in the
+// canonical (anchor, slot) order of decode_active (decoder.py:210-250).
+// Backward restates the autograd of that graph (decoder.py:267-292): an
+// anchor-parallel kernel producing head-output and pre-activation cotangents
+// plus per-anchor grads, then K-reduction GEMMs for the weight gradients.
+//
+// Layouts: per-anchor caches are FEATURE-major ([feature][anchor]) so warps
+// read/write them coalesced and the weight-gradient reductions stream them.
+#include "common.cuh"
+
+namespace vsx {
+
+struct DecSmem {
+  // W1cat [36][192] (head h -> columns h*64..h*64+63), b1cat [192],
+  // W2T per head [out_h][64] (transposed), b2cat [11n]
+  float *w1, *b1, *w2t, *b2;
+};
+
+__host__ __device__ inline int dec_out_width(int n) { return 11 * n; }
+__host__ __device__ inline int dec_head_off(int h, int n) { return h == 0 ? 0 : (h == 1 ? n : 4 * n); }
+__host__ __device__ inline int dec_head_w(int h, int n) { return h == 0 ? n : (h == 1 ? 3 * n : 7 * n); }
+
+inline size_t dec_smem_bytes(int n) {
+  return sizeof(float) * (size_t)(kInDim * 192 + 192 + 64 * 11 * n + 11 * n);
+}
+
+__device__ __forceinline__ DecSmem dec_smem_carve(float *base, int n) {
+  DecSmem s;
+  s.w1 = base;
+  s.b1 = s.w1 + kInDim * 192;
+  s.w2t = s.b1 + 192;
+  s.b2 = s.w2t + 64 * 11 * n;
+  return s;
+}
+
+__device__ void dec_load_weights(const vsx_decoder &W, DecSmem s) {
+  const int n = W.n;
+  for (int h = 0; h < 3; ++h) {
+    const int ow = dec_head_w(h, n), oo = dec_head_off(h, n);
+    for (int e = threadIdx.x; e < kInDim * 64; e += blockDim.x) {
+      const int i = e / 64, k = e % 64;
+      s.w1[i * 192 + h * 64 + k] = W.w1[h][e];
+    }
+    for (int k = threadIdx.x; k < 64; k += blockDim.x) s.b1[h * 64 + k] = W.b1[h][k];
+    for (int e = threadIdx.x; e < 64 * ow; e += blockDim.x) {
+      const int k = e / ow, j = e % ow;  // w2 is (64, ow) row-major
+      s.w2t[(oo + j) * 64 + k] = W.w2[h][e];
+    }
+    for (int j = threadIdx.x; j < ow; j += blockDim.x) s.b2[oo + j] = W.b2[h][j];
+  }
+  __syncthreads();
+}
+
+// Input block x = [emb | d/ref | (c - cam)/d] (decoder.py:142-147), float64
+// geometry rounded to float32 for the MLP.
+__device__ __forceinline__ void dec_inputs(const double *centers, const float *emb, int a,
+                                           const vsx_camera &cam, double lod_ref, float *x) {
+  const double rx = dsub(centers[3 * a + 0], cam.center[0]);
+  const double ry = dsub(centers[3 * a + 1], cam.center[1]);
+  const double rz = dsub(centers[3 * a + 2], cam.center[2]);
+  double d = sqrt(dadd(dadd(dmul(rx, rx), dmul(ry, ry)), dmul(rz, rz)));
+  d = fmax(d, 1e-12);
+  const float4 *e4 = reinterpret_cast<const float4 *>(emb + (size_t)a * kEmbed);
+#pragma unroll
+  for (int q = 0; q < kEmbed / 4; ++q) {
+    const float4 v = e4[q];
+    x[4 * q + 0] = v.x;
+    x[4 * q + 1] = v.y;
+    x[4 * q + 2] = v.z;
+    x[4 * q + 3] = v.w;
+  }
+  x[32] = (float)ddiv(d, lod_ref);
+  x[33] = (float)ddiv(rx, d);
+  x[34] = (float)ddiv(ry, d);
+  x[35] = (float)ddiv(rz, d);
+}
+
+// hid[0:64] = W1_h^T x + b1_h (pre-activation)
+__device__ __forceinline__ void dec_hidden(const DecSmem &s, int h, const float *x, float *hid) {
+#pragma unroll
+  for (int k = 0; k < 64; ++k) hid[k] = s.b1[h * 64 + k];
+#pragma unroll
+  for (int i = 0; i < kInDim; ++i) {
+    const float xi = x[i];
+    const float4 *w = reinterpret_cast<const float4 *>(s.w1 + i * 192 + h * 64);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const float4 wv = w[q];
+      hid[4 * q + 0] = fmaf(xi, wv.x, hid[4 * q + 0]);
+      hid[4 * q + 1] = fmaf(xi, wv.y, hid[4 * q + 1]);
+      hid[4 * q + 2] = fmaf(xi, wv.z, hid[4 * q + 2]);
+      hid[4 * q + 3] = fmaf(xi, wv.w, hid[4 * q + 3]);
+    }
+  }
+}
+
+__device__ __forceinline__ float dec_out(const DecSmem &s, int col, const float *hid) {
+  const float4 *w = reinterpret_cast<const float4 *>(s.w2t + col * 64);
+  float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+  for (int q = 0; q < 16; q += 2) {
+    const float4 a = w[q], b = w[q + 1];
+    acc0 = fmaf(hid[4 * q + 0], a.x, acc0);
+    acc0 = fmaf(hid[4 * q + 1], a.y, acc0);
+    acc0 = fmaf(hid[4 * q + 2], a.z, acc0);
+    acc0 = fmaf(hid[4 * q + 3], a.w, acc0);
+    acc1 = fmaf(hid[4 * q + 4], b.x, acc1);
+    acc1 = fmaf(hid[4 * q + 5], b.y, acc1);
+    acc1 = fmaf(hid[4 * q + 6], b.z, acc1);
+    acc1 = fmaf(hid[4 * q + 7], b.w, acc1);
+  }
+  return s.b2[col] + (acc0 + acc1);
+}
+
+__device__ __forceinline__ float sigmoidf_(float v) { return 1.0f / (1.0f + expf(-v)); }
+
+__global__ void __launch_bounds__(128) decode_fwd_kernel(
+    vsx_decoder W, const int32_t *__restrict__ active, int32_t n_active,
+    const double *__restrict__ centers, const float *__restrict__ emb,
+    const float *__restrict__ log_scale, const float *__restrict__ offsets, vsx_camera cam,
+    double lod_ref, double max_scale, double *__restrict__ means, float *__restrict__ opacity,
+    float *__restrict__ color, float *__restrict__ scale, float *__restrict__ quat,
+    float *__restrict__ normal, float *__restrict__ cache_h, float *__restrict__ cache_o,
+    int32_t *__restrict__ status) {
+  extern __shared__ __align__(16) float smem[];
+  const int n = W.n;
+  DecSmem s = dec_smem_carve(smem, n);
+  dec_load_weights(W, s);
+  const float smax = (float)max_scale, smin = (float)kMinScale;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_active; r += gridDim.x * blockDim.x) {
+    const int a = active[r];
+    float x[kInDim];
+    dec_inputs(centers, emb, a, cam, lod_ref, x);
+    bool bad = false;
+    float hid[64];
+    // opacity head
+    dec_hidden(s, 0, x, hid);
+#pragma unroll
+    for (int k = 0; k < 64; ++k) {
+      hid[k] = tanhf(hid[k]);
+      if (cache_h) cache_h[(size_t)k * n_active + r] = hid[k];
+    }
+    for (int j = 0; j < n; ++j) {
+      const float o = dec_out(s, j, hid);
+      if (cache_o) cache_o[(size_t)j * n_active + r] = o;
+      const float op = sigmoidf_(o);
+      bad |= !isfinite(op);
+      opacity[(size_t)r * n + j] = op;
+    }
+    // color head
+    dec_hidden(s, 1, x, hid);
+#pragma unroll
+    for (int k = 0; k < 64; ++k) {
+      hid[k] = tanhf(hid[k]);
+      if (cache_h) cache_h[(size_t)(64 + k) * n_active + r] = hid[k];
+    }
+    for (int j = 0; j < 3 * n; ++j) {
+      const float o = dec_out(s, n + j, hid);
+      if (cache_o) cache_o[(size_t)(n + j) * n_active + r] = o;
+      const float c = sigmoidf_(o);
+      bad |= !isfinite(c);
+      color[(size_t)r * 3 * n + j] = c;
+    }
+    // covariance head: per slot 3 log-scales + 4 raw quaternion entries
+    dec_hidden(s, 2, x, hid);
+#pragma unroll
+    for (int k = 0; k < 64; ++k) {
+      hid[k] = tanhf(hid[k]);
+      if (cache_h) cache_h[(size_t)(128 + k) * n_active + r] = hid[k];
+    }
+    const double l0 = exp((double)log_scale[3 * a + 0]);
+    const double l1 = exp((double)log_scale[3 * a + 1]);
+    const double l2 = exp((double)log_scale[3 * a + 2]);
+    for (int sl = 0; sl < n; ++sl) {
+      float o[7];
+#pragma unroll
+      for (int c = 0; c < 7; ++c) {
+        o[c] = dec_out(s, 4 * n + 7 * sl + c, hid);
+        if (cache_o) cache_o[(size_t)(4 * n + 7 * sl + c) * n_active + r] = o[c];
+      }
+      const size_t g = (size_t)r * n + sl;
+      float sc[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        sc[c] = fminf(fmaxf(expf(o[c]), smin), smax);
+        scale[3 * g + c] = sc[c];
+      }
+      float qw = o[3] + 1.0f, qx = o[4], qy = o[5], qz = o[6];
+      const float qn = fmaxf(sqrtf(qw * qw + qx * qx + qy * qy + qz * qz), 1e-12f);
+      qw /= qn;
+      qx /= qn;
+      qy /= qn;
+      qz /= qn;
+      quat[4 * g + 0] = qw;
+      quat[4 * g + 1] = qx;
+      quat[4 * g + 2] = qy;
+      quat[4 * g + 3] = qz;
+      float R[9];
+      quat_to_rot(qw, qx, qy, qz, R);
+      const int ax = argmin3(sc[0], sc[1], sc[2]);
+      normal[3 * g + 0] = R[0 + ax];
+      normal[3 * g + 1] = R[3 + ax];
+      normal[3 * g + 2] = R[6 + ax];
+      const float *off = offsets + ((size_t)a * n + sl) * 3;
+      const double m0 = dadd(centers[3 * a + 0], dmul((double)off[0], l0));
+      const double m1 = dadd(centers[3 * a + 1], dmul((double)off[1], l1));
+      const double m2 = dadd(centers[3 * a + 2], dmul((double)off[2], l2));
+      means[3 * g + 0] = m0;
+      means[3 * g + 1] = m1;
+      means[3 * g + 2] = m2;
+      bad |= !(isfinite(sc[0]) && isfinite(sc[1]) && isfinite(sc[2]) && isfinite(qw) &&
+               isfinite(qx) && isfinite(qy) && isfinite(qz) && isfinite(m0) && isfinite(m1) &&
+               isfinite(m2));
+    }
+    if (bad) atomicOr(status, VSX_STATUS_NONFINITE);
+  }
+}
+
+// ---------------------------------------------------------------- backward
+
+// dR/dq contraction: gq += sum_ij G_ij dR_ij/dq (row-major R of quat_to_rot).
+__device__ __forceinline__ void rot_vjp(float w, float x, float y, float z, const float *G,
+                                        float *gq) {
+  gq[0] += 2.f * (-z * G[1] + y * G[2] + z * G[3] - x * G[5] - y * G[6] + x * G[7]);
+  gq[1] += 2.f * (y * G[1] + z * G[2] + y * G[3] - 2.f * x * G[4] - w * G[5] + z * G[6] +
+                  w * G[7] - 2.f * x * G[8]);
+  gq[2] += 2.f * (-2.f * y * G[0] + x * G[1] + w * G[2] + x * G[3] + z * G[5] - w * G[6] +
+                  z * G[7] - 2.f * y * G[8]);
+  gq[3] += 2.f * (-2.f * z * G[0] - w * G[1] + x * G[2] + w * G[3] - 2.f * z * G[4] +
+                  y * G[5] + x * G[6] + y * G[7]);
+}
+
+// Anchor-parallel backward: per-gaussian cotangents -> head-output cotangents
+// g_o (feature-major), pre-activation cotangents g_pre (feature-major), the
+// input block x (feature-major, + a ones row for bias grads), and per-anchor
+// grads of embeddings / log-scales / offsets.
+__global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
+    vsx_decoder W, const int32_t *__restrict__ active, int32_t n_active,
+    const double *__restrict__ centers, const float *__restrict__ emb,
+    const float *__restrict__ log_scale, const float *__restrict__ offsets, vsx_camera cam,
+    double lod_ref, double max_scale, const float *__restrict__ cache_h,
+    const float *__restrict__ cache_o, const float *__restrict__ dscale,
+    const float *__restrict__ dquat, const float *__restrict__ g_means,
+    const float *__restrict__ g_opacity, const float *__restrict__ g_color,
+    const float *__restrict__ g_scale, const float *__restrict__ g_quat,
+    const float *__restrict__ g_normal, float *__restrict__ g_emb,
+    float *__restrict__ g_log_scale, float *__restrict__ g_offsets, float *__restrict__ xs,
+    float *__restrict__ g_o_out, float *__restrict__ g_pre_out) {
+  extern __shared__ __align__(16) float smem[];
+  const int n = W.n;
+  DecSmem s = dec_smem_carve(smem, n);
+  dec_load_weights(W, s);
+  const float smax = (float)max_scale, smin = (float)kMinScale;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_active; r += gridDim.x * blockDim.x) {
+    const int a = active[r];
+    float x[kInDim];
+    dec_inputs(centers, emb, a, cam, lod_ref, x);
+#pragma unroll
+    for (int i = 0; i < kInDim; ++i) xs[(size_t)i * n_active + r] = x[i];
+    xs[(size_t)kInDim * n_active + r] = 1.0f;
+    float gx[kInDim];
+#pragma unroll
+    for (int i = 0; i < kInDim; ++i) gx[i] = 0.f;
+    const double l[3] = {exp((double)log_scale[3 * a + 0]), exp((double)log_scale[3 * a + 1]),
+                         exp((double)log_scale[3 * a + 2])};
+    double gl[3] = {0.0, 0.0, 0.0};
+    for (int h = 0; h < 3; ++h) {
+      const int ow = dec_head_w(h, n), oo = dec_head_off(h, n);
+      float gh[64];
+#pragma unroll
+      for (int k = 0; k < 64; ++k) gh[k] = 0.f;
+      if (h < 2) {
+        for (int j = 0; j < ow; ++j) {
+          const float o = cache_o[(size_t)(oo + j) * n_active + r];
+          const float sg = sigmoidf_(o);
+          const float up = (h == 0) ? g_opacity[(size_t)r * n + j] : g_color[(size_t)r * 3 * n + j];
+          const float go = up * sg * (1.f - sg);
+          g_o_out[(size_t)(oo + j) * n_active + r] = go;
+          const float4 *w = reinterpret_cast<const float4 *>(s.w2t + (oo + j) * 64);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 wv = w[q];
+            gh[4 * q + 0] = fmaf(go, wv.x, gh[4 * q + 0]);
+            gh[4 * q + 1] = fmaf(go, wv.y, gh[4 * q + 1]);
+            gh[4 * q + 2] = fmaf(go, wv.z, gh[4 * q + 2]);
+            gh[4 * q + 3] = fmaf(go, wv.w, gh[4 * q + 3]);
+          }
+        }
+      } else {
+        for (int sl = 0; sl < n; ++sl) {
+          const size_t g = (size_t)r * n + sl;
+          float o[7], go[7];
+#pragma unroll
+          for (int c = 0; c < 7; ++c) o[c] = cache_o[(size_t)(oo + 7 * sl + c) * n_active + r];
+          // scales: clamp(exp(o), 1e-6, max) — gradient passes inside [min, max]
+          float sc[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const float e = expf(o[c]);
+            sc[c] = dscale[3 * g + c];
+            const bool pass = (e >= smin) && (e <= smax);
+            go[c] = pass ? g_scale[3 * g + c] * e : 0.f;
+          }
+          // quaternion: normalised (o[3:7] + (1,0,0,0)); normal = column argmin(s) of R(q)
+          const float qw = dquat[4 * g + 0], qx = dquat[4 * g + 1], qy = dquat[4 * g + 2],
+                      qz = dquat[4 * g + 3];
+          float gq[4] = {g_quat[4 * g + 0], g_quat[4 * g + 1], g_quat[4 * g + 2],
+                         g_quat[4 * g + 3]};
+          const int ax = argmin3(sc[0], sc[1], sc[2]);
+          float G[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          G[0 + ax] = g_normal[3 * g + 0];
+          G[3 + ax] = g_normal[3 * g + 1];
+          G[6 + ax] = g_normal[3 * g + 2];
+          rot_vjp(qw, qx, qy, qz, G, gq);
+          const float rw = o[3] + 1.0f, rx = o[4], ry = o[5], rz = o[6];
+          const float rn = sqrtf(rw * rw + rx * rx + ry * ry + rz * rz);
+          if (rn >= 1e-12f) {
+            const float dot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
+            go[3] = (gq[0] - qw * dot) / rn;
+            go[4] = (gq[1] - qx * dot) / rn;
+            go[5] = (gq[2] - qy * dot) / rn;
+            go[6] = (gq[3] - qz * dot) / rn;
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) go[3 + c] = gq[c] / 1e-12f;
+          }
+#pragma unroll
+          for (int c = 0; c < 7; ++c) {
+            g_o_out[(size_t)(oo + 7 * sl + c) * n_active + r] = go[c];
+            const float4 *w = reinterpret_cast<const float4 *>(s.w2t + (oo + 7 * sl + c) * 64);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const float4 wv = w[q];
+              gh[4 * q + 0] = fmaf(go[c], wv.x, gh[4 * q + 0]);
+              gh[4 * q + 1] = fmaf(go[c], wv.y, gh[4 * q + 1]);
+              gh[4 * q + 2] = fmaf(go[c], wv.z, gh[4 * q + 2]);
+              gh[4 * q + 3] = fmaf(go[c], wv.w, gh[4 * q + 3]);
+            }
+          }
+          // means = c + offset * l
+          const float *off = offsets + g * 3;
+          float *goff = g_offsets + ((size_t)a * n + sl) * 3;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const float gm = g_means[3 * g + c];
+            atomicAdd(goff + c, (float)((double)gm * l[c]));
+            gl[c] += (double)gm * (double)off[c];
+          }
+        }
+      }
+      // tanh backward, input-block cotangent
+#pragma unroll
+      for (int k = 0; k < 64; ++k) {
+        const float hv = cache_h[(size_t)(h * 64 + k) * n_active + r];
+        gh[k] *= (1.f - hv * hv);
+        g_pre_out[(size_t)(h * 64 + k) * n_active + r] = gh[k];
+      }
+#pragma unroll
+      for (int i = 0; i < kEmbed; ++i) {
+        const float4 *w = reinterpret_cast<const float4 *>(s.w1 + i * 192 + h * 64);
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float4 wv = w[q];
+          acc = fmaf(gh[4 * q + 0], wv.x, acc);
+          acc = fmaf(gh[4 * q + 1], wv.y, acc);
+          acc = fmaf(gh[4 * q + 2], wv.z, acc);
+          acc = fmaf(gh[4 * q + 3], wv.w, acc);
+        }
+        gx[i] += acc;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kEmbed; ++i) atomicAdd(g_emb + (size_t)a * kEmbed + i, gx[i]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) atomicAdd(g_log_scale + 3 * a + c, (float)(gl[c] * l[c]));
+  }
+}
+
+// C[m][c] += sum_k A[m][k] * B[c][k] for a K-chunk per blockIdx.z, where A is
+// (M x K) and B is (Ncols x K), both row-major with leading dim K (feature-
+// major caches). Output column c maps to segment out[c / seg_w] with row
+// stride ld_out; row M (== A_rows) is an implicit ones row written to
+// bias[c] when bias != nullptr.
+struct WgradOut {
+  float *out[3];
+  float *bias[3];
+  int seg_w;
+  int ld_out;
+};
+
+constexpr int kWgTile = 32;
+constexpr int kWgK = 64;
+
+__global__ void __launch_bounds__(256) wgrad_kernel(const float *__restrict__ A, int a_rows,
+                                                    bool ones_row, const float *__restrict__ B,
+                                                    int b_rows, int64_t K, int64_t k_chunk,
+                                                    WgradOut o) {
+  __shared__ float sa[kWgTile][kWgK + 1];
+  __shared__ float sb[kWgTile][kWgK + 1];
+  const int m0 = blockIdx.x * kWgTile, c0 = blockIdx.y * kWgTile;
+  const int64_t k_begin = (int64_t)blockIdx.z * k_chunk;
+  const int64_t k_end = min(K, k_begin + k_chunk);
+  const int tm = threadIdx.x / 8;         // 0..31 row within tile
+  const int tc = (threadIdx.x % 8) * 4;   // 4 consecutive columns
+  const int m_total = a_rows + (ones_row ? 1 : 0);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t kk = k_begin; kk < k_end; kk += kWgK) {
+    for (int e = threadIdx.x; e < kWgTile * kWgK; e += 256) {
+      const int rr = e / kWgK, k = e % kWgK;
+      const int64_t gk = kk + k;
+      const int m = m0 + rr, c = c0 + rr;
+      float av = 0.f, bv = 0.f;
+      if (gk < k_end) {
+        if (m < a_rows) av = A[(size_t)m * K + gk];
+        else if (m < m_total) av = 1.f;
+        if (c < b_rows) bv = B[(size_t)c * K + gk];
+      }
+      sa[rr][k] = av;
+      sb[rr][k] = bv;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < kWgK; ++k) {
+      const float av = sa[tm][k];
+      acc[0] = fmaf(av, sb[tc + 0][k], acc[0]);
+      acc[1] = fmaf(av, sb[tc + 1][k], acc[1]);
+      acc[2] = fmaf(av, sb[tc + 2][k], acc[2]);
+      acc[3] = fmaf(av, sb[tc + 3][k], acc[3]);
+    }
+    __syncthreads();
+  }
+  const int m = m0 + tm;
+  if (m >= m_total) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = c0 + tc + q;
+    if (c >= b_rows) continue;
+    const int seg = c / o.seg_w, cc = c % o.seg_w;
+    if (m < a_rows) atomicAdd(o.out[seg] + (size_t)m * o.ld_out + cc, acc[q]);
+    else if (o.bias[seg]) atomicAdd(o.bias[seg] + cc, acc[q]);
+  }
+}
+
+static int launch_wgrad(const float *A, int a_rows, bool ones_row, const float *B, int b_rows,
+                        int64_t K, WgradOut o, cudaStream_t st) {
+  if (K == 0) return VSX_OK;
+  const int gm = (a_rows + (ones_row ? 1 : 0) + kWgTile - 1) / kWgTile;
+  const int gc = (b_rows + kWgTile - 1) / kWgTile;
+  int64_t splits = std::max<int64_t>(1, (296 + gm * gc - 1) / (gm * gc));
+  int64_t k_chunk = (K + splits - 1) / splits;
+  k_chunk = ((k_chunk + kWgK - 1) / kWgK) * kWgK;
+  splits = (K + k_chunk - 1) / k_chunk;
+  dim3 grid(gm, gc, (unsigned)splits);
+  wgrad_kernel<<<grid, 256, 0, st>>>(A, a_rows, ones_row, B, b_rows, K, k_chunk, o);
+  VSX_LAUNCH_CHECK("wgrad");
+  return VSX_OK;
+}
+
+}  // namespace vsx
+
+using namespace vsx;
+
+static int dec_grid(int32_t n_active, size_t smem) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per_sm = std::max<int>(1, (int)(200 * 1024 / std::max<size_t>(smem, 1)));
+  return std::max(1, std::min(grid_for(n_active, 128), sms * std::min(per_sm, 4)));
+}
+
+extern "C" int vsx_decode_fwd(vsx_decoder W, const int32_t *active, int32_t n_active,
+                              const double *centers, const float *emb, const float *log_scale,
+                              const float *offsets, vsx_camera cam, double lod_ref,
+                              double max_scale, double *means, float *opacity, float *color,
+                              float *scale, float *quat, float *normal, float *cache_h,
+                              float *cache_o, int32_t *status, vsx_stream s) {
+  VSX_REQUIRE(W.n >= 1 && n_active >= 0 && lod_ref > 0, "decode_fwd: bad arguments");
+  if (n_active == 0) return VSX_OK;
+  const size_t smem = dec_smem_bytes(W.n);
+  VSX_REQUIRE(smem <= 227 * 1024, "decode_fwd: n=%d too large for shared weights", W.n);
+  VSX_CUDA_TRY(cudaFuncSetAttribute(decode_fwd_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  decode_fwd_kernel<<<dec_grid(n_active, smem), 128, smem, as_stream(s)>>>(
+      W, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, max_scale, means,
+      opacity, color, scale, quat, normal, cache_h, cache_o, status);
+  VSX_LAUNCH_CHECK("decode_fwd");
+  return VSX_OK;
+}
+
+extern "C" size_t vsx_decode_bwd_ws_bytes(int32_t n, int32_t n_active) {
+  return sizeof(float) * (size_t)n_active * (size_t)(kInDim + 1 + 192 + 11 * n) + 256;
+}
+
+extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t *active,
+                              int32_t n_active, const double *centers, const float *emb,
+                              const float *log_scale, const float *offsets, vsx_camera cam,
+                              double lod_ref, double max_scale, const float *cache_h,
+                              const float *cache_o, const float *scale, const float *quat,
+                              const float *g_means, const float *g_opacity, const float *g_color,
+                              const float *g_scale, const float *g_quat, const float *g_normal,
+                              float *g_emb, float *g_log_scale, float *g_offsets, void *ws,
+                              size_t ws_bytes, vsx_stream s) {
+  VSX_REQUIRE(W.n >= 1 && n_active >= 0, "decode_bwd: bad arguments");
+  if (n_active == 0) return VSX_OK;
+  VSX_REQUIRE(ws_bytes >= vsx_decode_bwd_ws_bytes(W.n, n_active), "decode_bwd: workspace");
+  cudaStream_t st = as_stream(s);
+  const int n = W.n;
+  float *xs = static_cast<float *>(ws);
+  float *g_pre = xs + (size_t)(kInDim + 1) * n_active;
+  float *g_o = g_pre + (size_t)192 * n_active;
+  const size_t smem = dec_smem_bytes(n);
+  VSX_CUDA_TRY(cudaFuncSetAttribute(decode_bwd_anchor_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  decode_bwd_anchor_kernel<<<dec_grid(n_active, smem), 128, smem, st>>>(
+      W, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, max_scale, cache_h,
+      cache_o, scale, quat, g_means, g_opacity, g_color, g_scale, g_quat, g_normal, g_emb,
+      g_log_scale, g_offsets, xs, g_o, g_pre);
+  VSX_LAUNCH_CHECK("decode_bwd_anchor");
+  // dW1_h = X^T Gpre_h (+ db1 via the ones row of X)
+  WgradOut o1{};
+  for (int h = 0; h < 3; ++h) {
+    o1.out[h] = dW.w1[h];
+    o1.bias[h] = dW.b1[h];
+  }
+  o1.seg_w = 64;
+  o1.ld_out = 64;
+  int rc = launch_wgrad(xs, kInDim, true, g_pre, 192, n_active, o1, st);
+  if (rc) return rc;
+  // dW2_h = H_h^T Go_h (+ db2 via an implicit ones row)
+  for (int h = 0; h < 3; ++h) {
+    const int ow = dec_head_w(h, n), oo = dec_head_off(h, n);
+    WgradOut o2{};
+    o2.out[0] = dW.w2[h];
+    o2.bias[0] = dW.b2[h];
+    o2.seg_w = ow;
+    o2.ld_out = ow;
+    rc = launch_wgrad(cache_h + (size_t)h * 64 * n_active, 64, true,
+                      g_o + (size_t)oo * n_active, ow, n_active, o2, st);
+    if (rc) return rc;
+  }
+  return VSX_OK;
+}

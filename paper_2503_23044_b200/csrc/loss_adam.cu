@@ -1,0 +1,142 @@
+// K9 — photometric / depth L1 losses with fused cotangents, and
+// K10 — one-launch fused Adam over every parameter group.
+//
+// bl_rgb_loss restates voxsplat losses.py:43-53 (mean over views of mean
+// |I_hat - I|; d/dI_hat = sign(diff) / (B*H*W*3), sign(0) = 0).
+// e_depth_loss restates losses.py:65-84 (masked L1 over prior-valid &
+// render-valid pixels, per-view mean, batch mean).
+// Adam restates trainer.py:220-247 (bias-corrected, eps 1e-15), dense: every
+// element moves every step, including zero-gradient anchors.
+#include "common.cuh"
+
+namespace vsx {
+
+__device__ __forceinline__ float signf_(float d) { return d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f); }
+
+__global__ void __launch_bounds__(256) l1_kernel(const float *__restrict__ r,
+                                                 const float *__restrict__ g, int64_t n,
+                                                 float scale, double *__restrict__ loss,
+                                                 float *__restrict__ grad) {
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float d = r[i] - g[i];
+    acc += fabs((double)d);
+    if (grad) grad[i] = signf_(d) * scale;
+  }
+  acc = warp_sum_d(acc);
+  __shared__ double ws[8];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < 8 ? ws[threadIdx.x] : 0.0;
+    v = warp_sum_d(v);
+    if (threadIdx.x == 0) atomicAdd(loss, v);
+  }
+}
+
+__global__ void __launch_bounds__(256) depth_l1_kernel(
+    const float *__restrict__ d, const uint8_t *__restrict__ valid, const float *__restrict__ p,
+    const uint8_t *__restrict__ pv, int64_t n, double *__restrict__ sums,
+    uint32_t *__restrict__ counts, const float *__restrict__ scale, float *__restrict__ grad) {
+  double acc = 0.0;
+  uint32_t cnt = 0;
+  const float sc = (grad && scale) ? *scale : 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool m = valid[i] && pv[i];
+    const float diff = d[i] - p[i];
+    if (m) {
+      acc += fabs((double)diff);
+      ++cnt;
+    }
+    if (grad) grad[i] = m ? signf_(diff) * sc : 0.f;
+  }
+  acc = warp_sum_d(acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) {
+    if (sums) atomicAdd(sums, acc);
+    if (counts) atomicAdd(counts, cnt);
+  }
+}
+
+constexpr int kMaxSeg = 16;
+struct AdamSegs {
+  int64_t begin[kMaxSeg + 1];
+  double lr[kMaxSeg];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) adam_kernel(float *__restrict__ p,
+                                                   const float *__restrict__ g,
+                                                   float *__restrict__ m, float *__restrict__ v,
+                                                   AdamSegs segs, double b1, double b2, double eps,
+                                                   double bc1, double bc2) {
+  const int64_t total = segs.begin[segs.n];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int s = 0;
+    while (s + 1 < segs.n && i >= segs.begin[s + 1]) ++s;
+    const double gi = g[i];
+    const double mi = b1 * (double)m[i] + (1.0 - b1) * gi;
+    const double vi = b2 * (double)v[i] + (1.0 - b2) * gi * gi;
+    m[i] = (float)mi;
+    v[i] = (float)vi;
+    const double step = -segs.lr[s] * (mi / bc1) / (sqrt(vi / bc2) + eps);
+    p[i] = (float)((double)p[i] + step);
+  }
+}
+
+}  // namespace vsx
+
+using namespace vsx;
+
+static int persistent_grid(int64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::max(1, std::min(grid_for(n, 256), sms * 8));
+}
+
+extern "C" int vsx_l1_loss(const float *rendered, const float *target, int64_t n, float scale,
+                           double *loss_accum, float *grad, vsx_stream s) {
+  VSX_REQUIRE(n >= 0 && loss_accum, "l1_loss: bad args");
+  if (n == 0) return VSX_OK;
+  l1_kernel<<<persistent_grid(n), 256, 0, as_stream(s)>>>(rendered, target, n, scale, loss_accum,
+                                                          grad);
+  VSX_LAUNCH_CHECK("l1_loss");
+  return VSX_OK;
+}
+
+extern "C" int vsx_depth_loss(const float *depth, const uint8_t *valid, const float *prior,
+                              const uint8_t *prior_valid, int64_t n, double *sums,
+                              uint32_t *counts, const float *scale, float *grad, vsx_stream s) {
+  VSX_REQUIRE(n >= 0, "depth_loss: bad args");
+  if (n == 0) return VSX_OK;
+  depth_l1_kernel<<<persistent_grid(n), 256, 0, as_stream(s)>>>(depth, valid, prior, prior_valid,
+                                                                n, sums, counts, scale, grad);
+  VSX_LAUNCH_CHECK("depth_loss");
+  return VSX_OK;
+}
+
+extern "C" int vsx_adam(float *param, const float *grad, float *m, float *v, int32_t n_seg,
+                        const int64_t *seg_begin, const double *lr, double beta1, double beta2,
+                        double eps, int32_t step, vsx_stream s) {
+  VSX_REQUIRE(n_seg >= 1 && n_seg <= kMaxSeg, "adam: 1..16 segments");
+  AdamSegs segs{};
+  segs.n = n_seg;
+  for (int i = 0; i <= n_seg; ++i) segs.begin[i] = seg_begin[i];
+  for (int i = 0; i < n_seg; ++i) {
+    VSX_REQUIRE(seg_begin[i + 1] >= seg_begin[i], "adam: segments must be ascending");
+    segs.lr[i] = lr[i];
+  }
+  const int64_t total = seg_begin[n_seg];
+  if (total == 0) return VSX_OK;
+  const int t = step + 1;
+  const double bc1 = 1.0 - pow(beta1, (double)t), bc2 = 1.0 - pow(beta2, (double)t);
+  adam_kernel<<<persistent_grid(total), 256, 0, as_stream(s)>>>(param, grad, m, v, segs, beta1,
+                                                                beta2, eps, bc1, bc2);
+  VSX_LAUNCH_CHECK("adam");
+  return VSX_OK;
+}

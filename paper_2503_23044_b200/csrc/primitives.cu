@@ -1,0 +1,371 @@
+// Generic device primitives: error state, exclusive scan, ordered select,
+// stable LSD radix sort. Hand-written (no CUB) so the sort's stability —
+// which carries the reference's (z, gid) tie-break — is explicit.
+#include <cstdarg>
+
+#include "common.cuh"
+
+static thread_local char g_err[512] = "";
+
+void vsx_set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" const char *vsx_last_error(void) { return g_err; }
+extern "C" int vsx_version(void) { return 1; }
+
+namespace vsx {
+
+// ------------------------------------------------------------------ scan
+
+constexpr int kScanBlock = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanBlock * kScanItems;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t &total) {
+  __shared__ uint32_t warp_tot[kScanBlock / 32];
+  __shared__ uint32_t tot_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = lane < kScanBlock / 32 ? warp_tot[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < kScanBlock / 32) warp_tot[lane] = wi - w;
+    if (lane == kScanBlock / 32 - 1) tot_s = wi;
+  }
+  __syncthreads();
+  const uint32_t res = warp_tot[warp] + inc - v;
+  total = tot_s;
+  __syncthreads();
+  return res;
+}
+
+// Tile-local exclusive scan; tile total goes to sums[blockIdx.x].
+__global__ void scan_tiles_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out,
+                                  int64_t n, uint32_t *__restrict__ sums) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = (base + i < n) ? in[base + i] : 0u;
+    acc += v[i];
+  }
+  uint32_t total = 0;
+  uint32_t pre = block_exclusive_scan(acc, total);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = pre;
+    pre += v[i];
+  }
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void scan_add_kernel(uint32_t *__restrict__ out, int64_t n,
+                                const uint32_t *__restrict__ tile_off, int64_t n_tiles) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] += tile_off[i / kScanTile];
+  if (i == 0) out[n] = tile_off[n_tiles];
+}
+
+static size_t scan_ws_elems(int64_t n) {
+  if (n <= kScanTile) return 0;
+  const int64_t nt = (n + kScanTile - 1) / kScanTile;
+  return (size_t)(2 * nt + 1) + scan_ws_elems(nt);
+}
+
+static int scan_impl(const uint32_t *in, uint32_t *out, int64_t n, uint32_t *ws,
+                     cudaStream_t st) {
+  if (n <= kScanTile) {
+    scan_tiles_kernel<<<1, kScanBlock, 0, st>>>(in, out, n, out + n);
+    VSX_LAUNCH_CHECK("scan_tiles");
+    return VSX_OK;
+  }
+  const int64_t nt = (n + kScanTile - 1) / kScanTile;
+  uint32_t *sums = ws;
+  uint32_t *sums_scan = ws + nt;
+  scan_tiles_kernel<<<(unsigned)nt, kScanBlock, 0, st>>>(in, out, n, sums);
+  VSX_LAUNCH_CHECK("scan_tiles");
+  int rc = scan_impl(sums, sums_scan, nt, ws + 2 * nt + 1, st);
+  if (rc) return rc;
+  scan_add_kernel<<<grid_for(n, 256), 256, 0, st>>>(out, n, sums_scan, nt);
+  VSX_LAUNCH_CHECK("scan_add");
+  return VSX_OK;
+}
+
+// ------------------------------------------------------------------ select
+
+__global__ void flags_to_u32_kernel(const uint8_t *__restrict__ f, uint32_t *__restrict__ o,
+                                    int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) o[i] = f[i] ? 1u : 0u;
+}
+
+__global__ void select_scatter_kernel(const uint8_t *__restrict__ f,
+                                      const uint32_t *__restrict__ pos, int64_t n,
+                                      int32_t *__restrict__ out, uint32_t *__restrict__ count) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && f[i]) out[pos[i]] = (int32_t)i;
+  if (i == 0) *count = pos[n];
+}
+
+// ------------------------------------------------------------------ radix sort
+
+constexpr int kRsBlock = 256;
+constexpr int kRsRounds = 16;
+constexpr int kRsTile = kRsBlock * kRsRounds;
+constexpr int kRsWarps = kRsBlock / 32;
+
+template <typename K>
+__global__ void rs_minmax_kernel(const K *__restrict__ keys, int64_t n,
+                                 unsigned long long *__restrict__ or_and) {
+  unsigned long long o = 0ull, a = ~0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long k = (unsigned long long)keys[i];
+    o |= k;
+    a &= k;
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    o |= __shfl_xor_sync(0xffffffffu, o, s);
+    a &= __shfl_xor_sync(0xffffffffu, a, s);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(&or_and[0], o);
+    atomicAnd(&or_and[1], a);
+  }
+}
+
+__global__ void rs_init_or_and(unsigned long long *or_and) {
+  or_and[0] = 0ull;
+  or_and[1] = ~0ull;
+}
+
+template <typename K>
+__global__ void rs_hist_kernel(const K *__restrict__ keys, int64_t n, int shift,
+                               uint32_t *__restrict__ hist) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRsTile;
+#pragma unroll 4
+  for (int r = 0; r < kRsRounds; ++r) {
+    const int64_t i = base + r * kRsBlock + threadIdx.x;
+    if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter: within a block, keys are ranked in input order (round-major,
+// then thread); across blocks the digit-major scanned histogram keeps block
+// order, so equal digits never reorder.
+template <typename K>
+__global__ void rs_scatter_kernel(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
+                                  K *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
+                                  int shift, const uint32_t *__restrict__ offs) {
+  __shared__ uint32_t run[256];
+  __shared__ uint32_t wcnt[kRsWarps][256];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  run[t] = offs[(int64_t)t * gridDim.x + blockIdx.x];
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t base = (int64_t)blockIdx.x * kRsTile;
+  for (int r = 0; r < kRsRounds; ++r) {
+    const int64_t i = base + r * kRsBlock + t;
+    if (base + r * kRsBlock >= n) break;  // block-uniform
+    const bool ok = i < n;
+    K k = ok ? kin[i] : K(0);
+    uint32_t v = ok ? vin[i] : 0u;
+    const uint32_t d = ok ? ((uint32_t)(k >> shift) & 255u) : 256u;
+#pragma unroll
+    for (int w = 0; w < kRsWarps; ++w) wcnt[w][t] = 0u;
+    __syncthreads();
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t lrank = __popc(peers & lt);
+    if (ok && lrank == 0) wcnt[warp][d] = __popc(peers);
+    __syncthreads();
+    uint32_t acc = run[t];
+#pragma unroll
+    for (int w = 0; w < kRsWarps; ++w) {
+      const uint32_t c = wcnt[w][t];
+      wcnt[w][t] = acc;
+      acc += c;
+    }
+    run[t] = acc;
+    __syncthreads();
+    if (ok) {
+      const uint32_t pos = wcnt[warp][d] + lrank;
+      kout[pos] = k;
+      vout[pos] = v;
+    }
+    __syncthreads();
+  }
+}
+
+struct SortWs {
+  void *alt_keys;
+  uint32_t *alt_vals;
+  uint32_t *hist;
+  uint32_t *hist_scan;
+  uint32_t *scan_ws;
+  unsigned long long *or_and;
+};
+
+static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+static size_t sort_ws_bytes(int64_t n) {
+  const int64_t nb = (n + kRsTile - 1) / kRsTile;
+  const int64_t nh = 256 * std::max<int64_t>(nb, 1);
+  return align256(sizeof(uint64_t) * n) + align256(sizeof(uint32_t) * n) +
+         align256(sizeof(uint32_t) * nh) + align256(sizeof(uint32_t) * (nh + 1)) +
+         align256(sizeof(uint32_t) * (scan_ws_elems(nh) + 1)) + 256;
+}
+
+static SortWs carve_sort_ws(void *ws, int64_t n) {
+  const int64_t nb = (n + kRsTile - 1) / kRsTile;
+  const int64_t nh = 256 * std::max<int64_t>(nb, 1);
+  char *p = static_cast<char *>(ws);
+  SortWs w;
+  w.alt_keys = p;
+  p += align256(sizeof(uint64_t) * n);
+  w.alt_vals = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * n);
+  w.hist = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * nh);
+  w.hist_scan = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * (nh + 1));
+  w.scan_ws = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * (scan_ws_elems(nh) + 1));
+  w.or_and = reinterpret_cast<unsigned long long *>(p);
+  return w;
+}
+
+template <typename K>
+static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout, int64_t n,
+                      int begin_bit, int end_bit, void *ws, size_t ws_bytes, cudaStream_t st) {
+  VSX_REQUIRE(n >= 0 && n < (int64_t)1 << 32, "sort: bad n %lld", (long long)n);
+  VSX_REQUIRE(begin_bit >= 0 && end_bit <= (int)(8 * sizeof(K)) && begin_bit <= end_bit,
+              "sort: bad bit range");
+  if (n == 0) return VSX_OK;
+  VSX_REQUIRE(ws_bytes >= sort_ws_bytes(n), "sort: workspace %zu < %zu", ws_bytes,
+              sort_ws_bytes(n));
+  SortWs w = carve_sort_ws(ws, n);
+  // Which digit bytes actually vary? (one tiny D2H read)
+  rs_init_or_and<<<1, 1, 0, st>>>(w.or_and);
+  rs_minmax_kernel<K><<<std::min(grid_for(n, 256), 1184), 256, 0, st>>>(kin, n, w.or_and);
+  VSX_LAUNCH_CHECK("rs_minmax");
+  unsigned long long oa[2];
+  VSX_CUDA_TRY(cudaMemcpyAsync(oa, w.or_and, sizeof(oa), cudaMemcpyDeviceToHost, st));
+  VSX_CUDA_TRY(cudaStreamSynchronize(st));
+  const unsigned long long varying = oa[0] ^ oa[1];
+  int shifts[16];
+  int np = 0;
+  for (int sh = begin_bit - (begin_bit % 8); sh < end_bit; sh += 8) {
+    unsigned long long m = (0xFFull << sh);
+    if (varying & m) shifts[np++] = sh;
+  }
+  if (np == 0) {
+    if (kout != kin) VSX_CUDA_TRY(cudaMemcpyAsync(kout, kin, sizeof(K) * n, cudaMemcpyDeviceToDevice, st));
+    if (vout != vin) VSX_CUDA_TRY(cudaMemcpyAsync(vout, vin, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st));
+    return VSX_OK;
+  }
+  const int nb = grid_for(n, kRsTile);
+  const int64_t nh = 256 * (int64_t)nb;
+  K *alt_k = static_cast<K *>(w.alt_keys);
+  const K *src_k = kin;
+  const uint32_t *src_v = vin;
+  for (int p = 0; p < np; ++p) {
+    const bool to_out = ((np - 1 - p) % 2) == 0;
+    K *dk = to_out ? kout : alt_k;
+    uint32_t *dv = to_out ? vout : w.alt_vals;
+    rs_hist_kernel<K><<<nb, kRsBlock, 0, st>>>(src_k, n, shifts[p], w.hist);
+    VSX_LAUNCH_CHECK("rs_hist");
+    int rc = scan_impl(w.hist, w.hist_scan, nh, w.scan_ws, st);
+    if (rc) return rc;
+    rs_scatter_kernel<K><<<nb, kRsBlock, 0, st>>>(src_k, src_v, dk, dv, n, shifts[p], w.hist_scan);
+    VSX_LAUNCH_CHECK("rs_scatter");
+    src_k = dk;
+    src_v = dv;
+  }
+  return VSX_OK;
+}
+
+}  // namespace vsx
+
+using namespace vsx;
+
+extern "C" size_t vsx_scan_ws_bytes(int64_t n) { return sizeof(uint32_t) * (scan_ws_elems(n) + 1); }
+
+extern "C" size_t vsx_sort_ws_bytes(int64_t n) {
+  const size_t a = sort_ws_bytes(n);
+  const size_t b = sizeof(uint32_t) * (n + 1) + vsx_scan_ws_bytes(n) + 512;  // select
+  return a > b ? a : b;
+}
+
+extern "C" int vsx_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, void *ws,
+                            size_t ws_bytes, vsx_stream s) {
+  VSX_REQUIRE(n >= 0, "scan: negative n");
+  VSX_REQUIRE(ws_bytes >= vsx_scan_ws_bytes(n), "scan: workspace too small");
+  if (n == 0) {
+    VSX_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(uint32_t), as_stream(s)));
+    return VSX_OK;
+  }
+  return scan_impl(in, out, n, static_cast<uint32_t *>(ws), as_stream(s));
+}
+
+extern "C" int vsx_select(const uint8_t *flags, int64_t n, int32_t *out_idx,
+                          uint32_t *out_count, void *ws, size_t ws_bytes, vsx_stream s) {
+  cudaStream_t st = as_stream(s);
+  VSX_REQUIRE(n >= 0, "select: negative n");
+  if (n == 0) {
+    VSX_CUDA_TRY(cudaMemsetAsync(out_count, 0, sizeof(uint32_t), st));
+    return VSX_OK;
+  }
+  const size_t need = align256(sizeof(uint32_t) * (n + 1)) + align256(sizeof(uint32_t) * n) +
+                      vsx_scan_ws_bytes(n);
+  VSX_REQUIRE(ws_bytes >= need, "select: workspace %zu < %zu", ws_bytes, need);
+  char *p = static_cast<char *>(ws);
+  uint32_t *pos = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * (n + 1));
+  uint32_t *ones = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * n);
+  flags_to_u32_kernel<<<grid_for(n, 256), 256, 0, st>>>(flags, ones, n);
+  VSX_LAUNCH_CHECK("flags_to_u32");
+  int rc = scan_impl(ones, pos, n, reinterpret_cast<uint32_t *>(p), st);
+  if (rc) return rc;
+  select_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(flags, pos, n, out_idx, out_count);
+  VSX_LAUNCH_CHECK("select_scatter");
+  return VSX_OK;
+}
+
+extern "C" int vsx_sort_pairs_u64(const uint64_t *keys_in, const uint32_t *vals_in,
+                                  uint64_t *keys_out, uint32_t *vals_out, int64_t n,
+                                  int32_t begin_bit, int32_t end_bit, void *ws, size_t ws_bytes,
+                                  vsx_stream s) {
+  return sort_pairs<uint64_t>(keys_in, vals_in, keys_out, vals_out, n, begin_bit, end_bit, ws,
+                              ws_bytes, as_stream(s));
+}
+
+extern "C" int vsx_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_in,
+                                  uint32_t *keys_out, uint32_t *vals_out, int64_t n,
+                                  int32_t begin_bit, int32_t end_bit, void *ws, size_t ws_bytes,
+                                  vsx_stream s) {
+  return sort_pairs<uint32_t>(keys_in, vals_in, keys_out, vals_out, n, begin_bit, end_bit, ws,
+                              ws_bytes, as_stream(s));
+}

@@ -1,0 +1,362 @@
+// K3 / K4 / K7 — EWA projection, tile binning, projection backward.
+//
+// Projection restates voxsplat renderer.py:144-204 in float64 (one thread per
+// gaussian): z > 0.01 cull, J Sigma_c J^T + 0.3 I, conic, 3-sigma radius,
+// camera normal flipped to face the camera, plane offset. The (z, gid) sort
+// of renderer.py:197 is a stable radix sort of the float64 z bits over the
+// ascending-gid batch (primitives.cu). Binning restates renderer.py:207-226.
+#include "common.cuh"
+
+namespace vsx {
+
+struct ProjGeom {
+  double x, y, z;      // mu_cam
+  double Rq[9];        // rotation of the gaussian (world)
+  double M[9];         // R * Rq (camera-frame rotation)
+  double s2[3];        // squared scales
+  double J00, J02, J11, J12;
+  double S[6];         // Sigma_c symmetric (00,01,02,11,12,22)
+  double a, b, c, det;
+};
+
+__device__ __forceinline__ void proj_geom(const vsx_camera &cam, const double *mu, const float *sc,
+                                          const float *q, ProjGeom &g) {
+  cam_transform(cam, mu[0], mu[1], mu[2], g.x, g.y, g.z);
+  quat_to_rot<double>(q[0], q[1], q[2], q[3], g.Rq);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g.s2[k] = (double)sc[k] * (double)sc[k];
+  // M = R * Rq, Sigma_c = M diag(s2) M^T
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      g.M[3 * i + j] = cam.r[3 * i + 0] * g.Rq[0 + j] + cam.r[3 * i + 1] * g.Rq[3 + j] +
+                       cam.r[3 * i + 2] * g.Rq[6 + j];
+  auto sig = [&](int i, int j) {
+    return g.M[3 * i + 0] * g.s2[0] * g.M[3 * j + 0] + g.M[3 * i + 1] * g.s2[1] * g.M[3 * j + 1] +
+           g.M[3 * i + 2] * g.s2[2] * g.M[3 * j + 2];
+  };
+  g.S[0] = sig(0, 0);
+  g.S[1] = sig(0, 1);
+  g.S[2] = sig(0, 2);
+  g.S[3] = sig(1, 1);
+  g.S[4] = sig(1, 2);
+  g.S[5] = sig(2, 2);
+  const double zi = 1.0 / g.z;
+  g.J00 = cam.fx * zi;
+  g.J02 = -cam.fx * g.x * zi * zi;
+  g.J11 = cam.fy * zi;
+  g.J12 = -cam.fy * g.y * zi * zi;
+  // cov2d = J S J^T with J = [[J00, 0, J02], [0, J11, J12]]
+  const double c00 = g.J00 * (g.J00 * g.S[0] + g.J02 * g.S[2]) + g.J02 * (g.J00 * g.S[2] + g.J02 * g.S[5]);
+  const double c01 = g.J00 * (g.J11 * g.S[1] + g.J12 * g.S[2]) + g.J02 * (g.J11 * g.S[4] + g.J12 * g.S[5]);
+  const double c11 = g.J11 * (g.J11 * g.S[3] + g.J12 * g.S[4]) + g.J12 * (g.J11 * g.S[4] + g.J12 * g.S[5]);
+  g.a = c00 + kLowpass;
+  g.b = c01;
+  g.c = c11 + kLowpass;
+  g.det = g.a * g.c - g.b * g.b;
+}
+
+__global__ void __launch_bounds__(256) project_fwd_kernel(
+    const double *__restrict__ means, const float *__restrict__ opacity,
+    const float *__restrict__ color, const float *__restrict__ scale,
+    const float *__restrict__ quat, const float *__restrict__ normal, int32_t n, vsx_camera cam,
+    vsx_splat *__restrict__ rec, uint64_t *__restrict__ zkey, double *__restrict__ radius,
+    uint32_t *__restrict__ n_kept, int32_t *__restrict__ status) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  if (i < n) {
+    const double mu[3] = {means[3 * i + 0], means[3 * i + 1], means[3 * i + 2]};
+    double x, y, z;
+    cam_transform(cam, mu[0], mu[1], mu[2], x, y, z);
+    keep = z > kZNear;
+    if (!keep) {
+      zkey[i] = ~0ull;
+      radius[i] = 0.0;
+    } else {
+      ProjGeom g;
+      proj_geom(cam, mu, scale + 3 * i, quat + 4 * i, g);
+      if (!(g.det > 0.0)) {
+        if (g.det <= 0.0) atomicOr(status, VSX_STATUS_NONPD);
+      }
+      const double idet = 1.0 / g.det;
+      const double mid = 0.5 * (g.a + g.c);
+      const double disc = 0.25 * (g.a - g.c) * (g.a - g.c) + g.b * g.b;
+      const double lam = mid + sqrt(fmax(disc, 0.0));
+      radius[i] = 3.0 * sqrt(lam);
+      // camera normal, flipped to face the camera (sign(n.mu) > 0 -> flip)
+      const double n0 = normal[3 * i + 0], n1 = normal[3 * i + 1], n2 = normal[3 * i + 2];
+      double nc[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) nc[k] = cam.r[3 * k + 0] * n0 + cam.r[3 * k + 1] * n1 + cam.r[3 * k + 2] * n2;
+      const double face = nc[0] * x + nc[1] * y + nc[2] * z;
+      const double fl = face > 0.0 ? -1.0 : 1.0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) nc[k] *= fl;
+      vsx_splat r;
+      r.mean2d[0] = dadd(ddiv(dmul(cam.fx, x), z), cam.cx);
+      r.mean2d[1] = dadd(ddiv(dmul(cam.fy, y), z), cam.cy);
+      r.conic[0] = (float)(g.c * idet);
+      r.conic[1] = (float)(-g.b * idet);
+      r.conic[2] = (float)(g.a * idet);
+      r.opacity = opacity[i];
+      r.color[0] = color[3 * i + 0];
+      r.color[1] = color[3 * i + 1];
+      r.color[2] = color[3 * i + 2];
+      r.normal[0] = (float)nc[0];
+      r.normal[1] = (float)nc[1];
+      r.normal[2] = (float)nc[2];
+      r.plane_d = (float)(nc[0] * x + nc[1] * y + nc[2] * z);
+      r.src = (uint32_t)i;
+      rec[i] = r;
+      zkey[i] = (uint64_t)__double_as_longlong(z);
+    }
+  }
+  const unsigned ball = __ballot_sync(0xffffffffu, keep);
+  if ((threadIdx.x & 31) == 0 && ball) atomicAdd(n_kept, (uint32_t)__popc(ball));
+}
+
+__global__ void gather_splats_kernel(const vsx_splat *__restrict__ rec,
+                                     const double *__restrict__ radius,
+                                     const uint32_t *__restrict__ order, int32_t n,
+                                     vsx_splat *__restrict__ out, double *__restrict__ rout) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t j = order[i];
+  out[i] = rec[j];
+  rout[i] = radius[j];
+}
+
+// Tile rectangle of a splat (renderer.py:216-221), float64 floor semantics.
+__device__ __forceinline__ bool tile_rect(double u, double v, double r, int txn, int tyn, int &x0,
+                                          int &x1, int &y0, int &y1) {
+  const double fx0 = fmax(floor(dsub(u, r) / 16.0), 0.0);
+  const double fx1 = fmin(floor(dadd(u, r) / 16.0), (double)(txn - 1));
+  const double fy0 = fmax(floor(dsub(v, r) / 16.0), 0.0);
+  const double fy1 = fmin(floor(dadd(v, r) / 16.0), (double)(tyn - 1));
+  if (!(fx1 >= fx0) || !(fy1 >= fy0)) return false;
+  x0 = (int)fx0;
+  x1 = (int)fx1;
+  y0 = (int)fy0;
+  y1 = (int)fy1;
+  return true;
+}
+
+__global__ void bin_count_kernel(const vsx_splat *__restrict__ rec,
+                                 const double *__restrict__ radius, int32_t n, int txn, int tyn,
+                                 uint32_t *__restrict__ splat_tiles,
+                                 uint32_t *__restrict__ tile_counts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int x0, x1, y0, y1;
+  uint32_t cnt = 0;
+  if (tile_rect(rec[i].mean2d[0], rec[i].mean2d[1], radius[i], txn, tyn, x0, x1, y0, y1)) {
+    cnt = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+    for (int ty = y0; ty <= y1; ++ty)
+      for (int tx = x0; tx <= x1; ++tx) atomicAdd(tile_counts + ty * txn + tx, 1u);
+  }
+  splat_tiles[i] = cnt;
+}
+
+__global__ void bin_emit_kernel(const vsx_splat *__restrict__ rec,
+                                const double *__restrict__ radius, int32_t n, int txn, int tyn,
+                                const uint32_t *__restrict__ offs, uint32_t *__restrict__ tiles,
+                                uint32_t *__restrict__ ranks) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int x0, x1, y0, y1;
+  if (!tile_rect(rec[i].mean2d[0], rec[i].mean2d[1], radius[i], txn, tyn, x0, x1, y0, y1)) return;
+  uint32_t o = offs[i];
+  for (int ty = y0; ty <= y1; ++ty)
+    for (int tx = x0; tx <= x1; ++tx) {
+      tiles[o] = (uint32_t)(ty * txn + tx);
+      ranks[o] = (uint32_t)i;
+      ++o;
+    }
+}
+
+// ---------------------------------------------------------------- K7 backward
+
+// Per sorted splat: screen-space grads (mean2d 2, conic 3, opacity, color 3,
+// normal 3, plane_d) -> gaussian grads, float64 internally. Writes (=) into
+// the batch-order outputs at rec.src; culled gaussians keep the caller's zeros.
+__global__ void __launch_bounds__(128) project_bwd_kernel(
+    const double *__restrict__ means, const float *__restrict__ scale,
+    const float *__restrict__ quat, const float *__restrict__ normal,
+    const vsx_splat *__restrict__ rec, const float *__restrict__ gs, int32_t n, vsx_camera cam,
+    float *__restrict__ g_means, float *__restrict__ g_opacity, float *__restrict__ g_color,
+    float *__restrict__ g_scale, float *__restrict__ g_quat, float *__restrict__ g_normal) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t i = rec[r].src;
+  const float *G = gs + (size_t)13 * r;
+  const double mu[3] = {means[3 * i + 0], means[3 * i + 1], means[3 * i + 2]};
+  const float *sc = scale + 3 * i;
+  const float *q = quat + 4 * i;
+  ProjGeom g;
+  proj_geom(cam, mu, sc, q, g);
+  const double x = g.x, y = g.y, z = g.z;
+  const double zi = 1.0 / z;
+  // ---- conic -> (a, b, c)
+  const double gA = G[2], gB = G[3], gC = G[4];
+  const double idet = 1.0 / g.det;
+  const double gdet = -(gA * g.c - gB * g.b + gC * g.a) * idet * idet;
+  const double ga = gC * idet + gdet * g.c;
+  const double gc = gA * idet + gdet * g.a;
+  const double gb = -gB * idet - 2.0 * gdet * g.b;
+  // symmetric cov2d cotangent Gs = [[ga, gb/2], [gb/2, gc]]
+  const double G00 = ga, G01 = 0.5 * gb, G11 = gc;
+  // J rows: j0 = (J00, 0, J02), j1 = (0, J11, J12)
+  const double j0[3] = {g.J00, 0.0, g.J02}, j1[3] = {0.0, g.J11, g.J12};
+  const double S[9] = {g.S[0], g.S[1], g.S[2], g.S[1], g.S[3], g.S[4], g.S[2], g.S[4], g.S[5]};
+  // g_J = 2 Gs J S  (2x3)
+  double JS0[3], JS1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    JS0[k] = j0[0] * S[k] + j0[1] * S[3 + k] + j0[2] * S[6 + k];
+    JS1[k] = j1[0] * S[k] + j1[1] * S[3 + k] + j1[2] * S[6 + k];
+  }
+  const double gJ00 = 2.0 * (G00 * JS0[0] + G01 * JS1[0]);
+  const double gJ02 = 2.0 * (G00 * JS0[2] + G01 * JS1[2]);
+  const double gJ11 = 2.0 * (G01 * JS0[1] + G11 * JS1[1]);
+  const double gJ12 = 2.0 * (G01 * JS0[2] + G11 * JS1[2]);
+  // g_S = J^T Gs J (3x3 symmetric)
+  double gS[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      gS[3 * a + b] = j0[a] * (G00 * j0[b] + G01 * j1[b]) + j1[a] * (G01 * j0[b] + G11 * j1[b]);
+  // ---- mu_cam cotangent
+  double gx = 0.0, gy = 0.0, gz = 0.0;
+  const double gu = G[0], gv = G[1];
+  gx += gu * cam.fx * zi;
+  gy += gv * cam.fy * zi;
+  gz += -gu * cam.fx * x * zi * zi - gv * cam.fy * y * zi * zi;
+  gz += -gJ00 * cam.fx * zi * zi - gJ11 * cam.fy * zi * zi;
+  gx += -gJ02 * cam.fx * zi * zi;
+  gz += gJ02 * 2.0 * cam.fx * x * zi * zi * zi;
+  gy += -gJ12 * cam.fy * zi * zi;
+  gz += gJ12 * 2.0 * cam.fy * y * zi * zi * zi;
+  // plane_d = n_c . mu_c, n_c = fl * R n
+  const double nw[3] = {normal[3 * i + 0], normal[3 * i + 1], normal[3 * i + 2]};
+  double nc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) nc[k] = cam.r[3 * k + 0] * nw[0] + cam.r[3 * k + 1] * nw[1] + cam.r[3 * k + 2] * nw[2];
+  const double fl = (nc[0] * x + nc[1] * y + nc[2] * z) > 0.0 ? -1.0 : 1.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) nc[k] *= fl;
+  const double gpd = G[12];
+  gx += gpd * nc[0];
+  gy += gpd * nc[1];
+  gz += gpd * nc[2];
+  const double gnc[3] = {G[9] + gpd * x, G[10] + gpd * y, G[11] + gpd * z};
+  // mu = R^T mu_c cotangent; n = fl R^T gnc
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    g_means[3 * i + k] = (float)(cam.r[0 + k] * gx + cam.r[3 + k] * gy + cam.r[6 + k] * gz);
+    g_normal[3 * i + k] = (float)(fl * (cam.r[0 + k] * gnc[0] + cam.r[3 + k] * gnc[1] + cam.r[6 + k] * gnc[2]));
+  }
+  // ---- Sigma_c = M D M^T, M = R Rq: gM = 2 gS M D ; gD_k = (M^T gS M)_kk
+  double gM[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      gM[3 * a + k] = 2.0 * (gS[3 * a + 0] * g.M[0 + k] + gS[3 * a + 1] * g.M[3 + k] +
+                             gS[3 * a + 2] * g.M[6 + k]) * g.s2[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double d = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) d += g.M[3 * a + k] * gS[3 * a + b] * g.M[3 * b + k];
+    g_scale[3 * i + k] = (float)(d * 2.0 * (double)sc[k]);
+  }
+  // gRq = R^T gM
+  double gRq[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      gRq[3 * a + k] = cam.r[0 + a] * gM[0 + k] + cam.r[3 + a] * gM[3 + k] + cam.r[6 + a] * gM[6 + k];
+  const double w = q[0], qx = q[1], qy = q[2], qz = q[3];
+  const double *Gq = gRq;
+  g_quat[4 * i + 0] = (float)(2.0 * (-qz * Gq[1] + qy * Gq[2] + qz * Gq[3] - qx * Gq[5] - qy * Gq[6] + qx * Gq[7]));
+  g_quat[4 * i + 1] = (float)(2.0 * (qy * Gq[1] + qz * Gq[2] + qy * Gq[3] - 2.0 * qx * Gq[4] - w * Gq[5] + qz * Gq[6] + w * Gq[7] - 2.0 * qx * Gq[8]));
+  g_quat[4 * i + 2] = (float)(2.0 * (-2.0 * qy * Gq[0] + qx * Gq[1] + w * Gq[2] + qx * Gq[3] + qz * Gq[5] - w * Gq[6] + qz * Gq[7] - 2.0 * qy * Gq[8]));
+  g_quat[4 * i + 3] = (float)(2.0 * (-2.0 * qz * Gq[0] - w * Gq[1] + qx * Gq[2] + w * Gq[3] - 2.0 * qz * Gq[4] + qy * Gq[5] + qx * Gq[6] + qy * Gq[7]));
+  g_opacity[i] = G[5];
+  g_color[3 * i + 0] = G[6];
+  g_color[3 * i + 1] = G[7];
+  g_color[3 * i + 2] = G[8];
+}
+
+}  // namespace vsx
+
+using namespace vsx;
+
+extern "C" int vsx_project_fwd(const double *means, const float *opacity, const float *color,
+                               const float *scale, const float *quat, const float *normal,
+                               int32_t n, vsx_camera cam, vsx_splat *rec, uint64_t *zkey,
+                               double *radius, uint32_t *n_kept, int32_t *status, vsx_stream s) {
+  VSX_REQUIRE(n >= 0, "project_fwd: negative n");
+  cudaStream_t st = as_stream(s);
+  VSX_CUDA_TRY(cudaMemsetAsync(n_kept, 0, sizeof(uint32_t), st));
+  if (n == 0) return VSX_OK;
+  project_fwd_kernel<<<grid_for(n, 256), 256, 0, st>>>(means, opacity, color, scale, quat, normal,
+                                                       n, cam, rec, zkey, radius, n_kept, status);
+  VSX_LAUNCH_CHECK("project_fwd");
+  return VSX_OK;
+}
+
+extern "C" int vsx_gather_splats(const vsx_splat *rec, const double *radius,
+                                 const uint32_t *order, int32_t n, vsx_splat *rec_sorted,
+                                 double *radius_sorted, vsx_stream s) {
+  if (n <= 0) return VSX_OK;
+  gather_splats_kernel<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(rec, radius, order, n,
+                                                                   rec_sorted, radius_sorted);
+  VSX_LAUNCH_CHECK("gather_splats");
+  return VSX_OK;
+}
+
+extern "C" int vsx_bin_count(const vsx_splat *rec, const double *radius, int32_t n,
+                             int32_t width, int32_t height, uint32_t *splat_tiles,
+                             uint32_t *tile_counts, vsx_stream s) {
+  VSX_REQUIRE(width > 0 && height > 0 && n >= 0, "bin_count: bad arguments");
+  const int txn = (width + kTile - 1) / kTile, tyn = (height + kTile - 1) / kTile;
+  cudaStream_t st = as_stream(s);
+  VSX_CUDA_TRY(cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * txn * tyn, st));
+  if (n == 0) return VSX_OK;
+  bin_count_kernel<<<grid_for(n, 256), 256, 0, st>>>(rec, radius, n, txn, tyn, splat_tiles,
+                                                     tile_counts);
+  VSX_LAUNCH_CHECK("bin_count");
+  return VSX_OK;
+}
+
+extern "C" int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
+                            int32_t height, const uint32_t *splat_offsets, uint32_t *isect_tile,
+                            uint32_t *isect_rank, vsx_stream s) {
+  VSX_REQUIRE(width > 0 && height > 0 && n >= 0, "bin_emit: bad arguments");
+  if (n == 0) return VSX_OK;
+  const int txn = (width + kTile - 1) / kTile, tyn = (height + kTile - 1) / kTile;
+  bin_emit_kernel<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(rec, radius, n, txn, tyn,
+                                                              splat_offsets, isect_tile,
+                                                              isect_rank);
+  VSX_LAUNCH_CHECK("bin_emit");
+  return VSX_OK;
+}
+
+extern "C" int vsx_project_bwd(const double *means, const float *scale, const float *quat,
+                               const float *normal, const vsx_splat *rec_sorted,
+                               const float *grad_splat, int32_t n_sorted, vsx_camera cam,
+                               float *g_means, float *g_opacity, float *g_color, float *g_scale,
+                               float *g_quat, float *g_normal, vsx_stream s) {
+  if (n_sorted <= 0) return VSX_OK;
+  project_bwd_kernel<<<grid_for(n_sorted, 128), 128, 0, as_stream(s)>>>(
+      means, scale, quat, normal, rec_sorted, grad_splat, n_sorted, cam, g_means, g_opacity,
+      g_color, g_scale, g_quat, g_normal);
+  VSX_LAUNCH_CHECK("project_bwd");
+  return VSX_OK;
+}

@@ -1,0 +1,354 @@
+"""Device-side pipeline stages over the C ABI (PyTorch = allocator + streams).
+
+Every function here allocates its outputs with torch on the current CUDA
+device and launches the corresponding ``vsx_*`` kernels on the current
+stream. Nothing here computes on the CPU: without CUDA (or without the
+built library) every entry point raises.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call, ptr, stream
+from .errors import NumericalError
+from .geometry import CameraView
+
+EMBED_DIM = 32
+HIDDEN = 64
+REC_F32 = 16            # sizeof(vsx_splat) / 4
+GRAD_F32 = 13           # per-splat gradient record
+STATUS_NONPD = 1
+STATUS_NONFINITE = 2
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2503_23044_b200 runs on a CUDA (sm_100a) device only; "
+                           "there is no CPU fallback")
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class Workspace:
+    """Grow-only scratch buffer shared by the sort/scan/decode-backward calls."""
+
+    def __init__(self) -> None:
+        self.buf: torch.Tensor | None = None
+
+    def get(self, nbytes: int) -> tuple:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device.index != torch.cuda.current_device():
+            grow = nbytes if self.buf is None else max(nbytes, int(self.buf.numel() * 1.25))
+            self.buf = torch.empty(grow, dtype=torch.uint8, device="cuda")
+        return ptr(self.buf), self.buf.numel()
+
+
+_WORKSPACES: dict[int, Workspace] = {}
+
+
+def workspace() -> Workspace:
+    key = torch.cuda.current_stream().cuda_stream
+    ws = _WORKSPACES.get(key)
+    if ws is None:
+        ws = _WORKSPACES[key] = Workspace()
+    return ws
+
+
+def _u32(n: int) -> torch.Tensor:
+    return torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+
+
+# ------------------------------------------------------------------ primitives
+
+def sort_pairs_u64(keys: torch.Tensor, vals: torch.Tensor, n: int):
+    ko = torch.empty_like(keys)
+    vo = torch.empty_like(vals)
+    lib = _lib.load()
+    wp, wb = workspace().get(lib.vsx_sort_ws_bytes(n))
+    call("vsx_sort_pairs_u64", ptr(keys), ptr(vals), ptr(ko), ptr(vo), n, 0, 64, wp, wb, stream())
+    return ko, vo
+
+
+def sort_pairs_u32(keys: torch.Tensor, vals: torch.Tensor, n: int, bits: int):
+    ko = torch.empty_like(keys)
+    vo = torch.empty_like(vals)
+    lib = _lib.load()
+    wp, wb = workspace().get(lib.vsx_sort_ws_bytes(n))
+    call("vsx_sort_pairs_u32", ptr(keys), ptr(vals), ptr(ko), ptr(vo), n, 0, bits, wp, wb,
+         stream())
+    return ko, vo
+
+
+def exclusive_scan(counts: torch.Tensor, n: int) -> torch.Tensor:
+    out = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    lib = _lib.load()
+    wp, wb = workspace().get(lib.vsx_scan_ws_bytes(n))
+    call("vsx_scan_u32", ptr(counts), ptr(out), n, wp, wb, stream())
+    return out
+
+
+def select(flags: torch.Tensor) -> torch.Tensor:
+    """Ordered indices of non-zero u8 flags (one host sync for the count)."""
+    n = int(flags.numel())
+    idx = _u32(n)
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib = _lib.load()
+    wp, wb = workspace().get(lib.vsx_sort_ws_bytes(n))
+    call("vsx_select", ptr(flags), n, ptr(idx), ptr(cnt), wp, wb, stream())
+    return idx[: int(cnt.item())]
+
+
+# ------------------------------------------------------------------ scene
+
+class DeviceScene:
+    """Static anchor geometry of a SceneModel in the flat level-major layout.
+
+    centers (A,3) float64 are ``grid * cell`` computed on the host with numpy,
+    so they are bit-identical to the reference's ``SceneLevel.centers``.
+    """
+
+    def __init__(self, scene) -> None:
+        require_cuda()
+        self.lod_count = scene.lod_count
+        self.lod_ref = float(scene.lod_ref_distance)
+        self.lod_bias = int(scene.lod_bias)
+        self.n = scene.offsets_per_voxel
+        self.base_voxel_size = float(scene.base_voxel_size)
+        self.level_bases = scene.level_bases
+        self.count = int(self.level_bases[-1])
+        self.centers = torch.from_numpy(np.ascontiguousarray(scene.flat_centers())).cuda()
+        self.levels = torch.from_numpy(scene.flat_levels()).cuda()
+        self.signature = self._signature(scene)
+
+    @staticmethod
+    def _signature(scene):
+        return (tuple(lv.count for lv in scene.levels), float(scene.lod_ref_distance),
+                int(scene.lod_bias), torch.cuda.current_device())
+
+    @property
+    def max_scale(self) -> float:
+        return 3.0 * self.base_voxel_size
+
+    def cull(self, view: CameraView) -> torch.Tensor:
+        mask = torch.empty(max(self.count, 1), dtype=torch.uint8, device="cuda")
+        call("vsx_cull", ptr(self.centers), ptr(self.levels), self.count, self.lod_count,
+             self.lod_ref, self.lod_bias, view.to_abi(), ptr(mask), stream())
+        return mask[: self.count]
+
+    def active(self, view: CameraView) -> torch.Tensor:
+        return select(self.cull(view))
+
+
+def device_scene_for(scene) -> DeviceScene:
+    ds = getattr(scene, "_vsx_device", None)
+    if ds is None or ds.signature != DeviceScene._signature(scene):
+        ds = DeviceScene(scene)
+        scene._vsx_device = ds
+    return ds
+
+
+# ------------------------------------------------------------------ decode
+
+@dataclass
+class Decoded:
+    active: torch.Tensor          # (A') int32 flat anchor ids
+    means: torch.Tensor           # (G,3) f64
+    opacity: torch.Tensor         # (G,) f32
+    color: torch.Tensor           # (G,3)
+    scale: torch.Tensor           # (G,3)
+    quat: torch.Tensor            # (G,4)
+    normal: torch.Tensor          # (G,3)
+    cache_h: torch.Tensor | None  # (192, A') f32 feature-major
+    cache_o: torch.Tensor | None  # (11n, A')
+
+    @property
+    def count(self) -> int:
+        return int(self.means.shape[0])
+
+
+def decode(dec_abi, n: int, active: torch.Tensor, centers: torch.Tensor, emb: torch.Tensor,
+           log_scales: torch.Tensor, offsets: torch.Tensor, view: CameraView, lod_ref: float,
+           max_scale: float, status: torch.Tensor, keep_cache: bool) -> Decoded:
+    na = int(active.numel())
+    g = na * n
+    dev = "cuda"
+    means = torch.empty((g, 3), dtype=torch.float64, device=dev)
+    opac = torch.empty(g, dtype=torch.float32, device=dev)
+    col = torch.empty((g, 3), dtype=torch.float32, device=dev)
+    scl = torch.empty((g, 3), dtype=torch.float32, device=dev)
+    quat = torch.empty((g, 4), dtype=torch.float32, device=dev)
+    nrm = torch.empty((g, 3), dtype=torch.float32, device=dev)
+    ch = torch.empty((192, max(na, 1)), dtype=torch.float32, device=dev) if keep_cache else None
+    co = torch.empty((11 * n, max(na, 1)), dtype=torch.float32, device=dev) if keep_cache else None
+    call("vsx_decode_fwd", dec_abi, ptr(active), na, ptr(centers), ptr(emb), ptr(log_scales),
+         ptr(offsets), view.to_abi(), lod_ref, max_scale, ptr(means), ptr(opac), ptr(col),
+         ptr(scl), ptr(quat), ptr(nrm), ptr(ch), ptr(co), ptr(status), stream())
+    return Decoded(active, means, opac, col, scl, quat, nrm, ch, co)
+
+
+# ------------------------------------------------------------------ project + sort
+
+@dataclass
+class Projected:
+    rec: torch.Tensor        # (G',16) f32 view of vsx_splat records, sorted
+    radius: torch.Tensor     # (G',) f64 sorted
+    zkey: torch.Tensor       # (G',) int64 (float64 z bits) sorted
+    src: torch.Tensor        # (G',) int32 index into the decode batch
+    count: int
+
+    @property
+    def mean2d(self) -> torch.Tensor:
+        return self.rec.view(torch.float64)[:, 0:2]
+
+    @property
+    def conic(self) -> torch.Tensor:
+        return self.rec[:, 4:7]
+
+    @property
+    def opacity(self) -> torch.Tensor:
+        return self.rec[:, 7]
+
+    @property
+    def color(self) -> torch.Tensor:
+        return self.rec[:, 8:11]
+
+    @property
+    def normal_cam(self) -> torch.Tensor:
+        return self.rec[:, 11:14]
+
+    @property
+    def plane_d(self) -> torch.Tensor:
+        return self.rec[:, 14]
+
+
+def project(means, opacity, color, scale, quat, normal, view: CameraView,
+            status: torch.Tensor) -> Projected:
+    """EWA projection + stable (z, batch-order) sort; batch must be gid-ascending."""
+    g = int(means.shape[0])
+    rec = torch.empty((max(g, 1), REC_F32), dtype=torch.float32, device="cuda")
+    key = torch.empty(max(g, 1), dtype=torch.int64, device="cuda")
+    rad = torch.empty(max(g, 1), dtype=torch.float64, device="cuda")
+    kept = torch.zeros(1, dtype=torch.int32, device="cuda")
+    call("vsx_project_fwd", ptr(means), ptr(opacity), ptr(color), ptr(scale), ptr(quat),
+         ptr(normal), g, view.to_abi(), ptr(rec), ptr(key), ptr(rad), ptr(kept), ptr(status),
+         stream())
+    if g == 0:
+        e = torch.empty(0, device="cuda")
+        return Projected(rec[:0], rad[:0], key[:0], kept[:0], 0)
+    idx = torch.arange(g, dtype=torch.int32, device="cuda")
+    skey, order = sort_pairs_u64(key[:g], idx, g)
+    n_kept = int(kept.item())
+    rs = torch.empty((max(n_kept, 1), REC_F32), dtype=torch.float32, device="cuda")
+    rr = torch.empty(max(n_kept, 1), dtype=torch.float64, device="cuda")
+    call("vsx_gather_splats", ptr(rec), ptr(rad), ptr(order), n_kept, ptr(rs), ptr(rr), stream())
+    return Projected(rs[:n_kept], rr[:n_kept], skey[:n_kept], order[:n_kept], n_kept)
+
+
+# ------------------------------------------------------------------ binning
+
+@dataclass
+class Bins:
+    tile_offsets: torch.Tensor   # (T+1,) int32 (uint32 bits)
+    tile_list: torch.Tensor      # (I,) int32 sorted-splat ranks, ascending per tile
+    tiles_x: int
+    tiles_y: int
+
+    @property
+    def intersections(self) -> int:
+        return int(self.tile_list.numel())
+
+
+def bin_tiles(P: Projected, width: int, height: int) -> Bins:
+    txn, tyn = (width + 15) // 16, (height + 15) // 16
+    T = txn * tyn
+    n = P.count
+    counts = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    tcounts = torch.empty(T, dtype=torch.int32, device="cuda")
+    call("vsx_bin_count", ptr(P.rec), ptr(P.radius), n, width, height, ptr(counts),
+         ptr(tcounts), stream())
+    toff = exclusive_scan(tcounts, T)
+    if n == 0:
+        return Bins(toff, torch.empty(0, dtype=torch.int32, device="cuda"), txn, tyn)
+    soff = exclusive_scan(counts, n)
+    total = int(soff[n].item())
+    tiles = torch.empty(max(total, 1), dtype=torch.int32, device="cuda")
+    ranks = torch.empty(max(total, 1), dtype=torch.int32, device="cuda")
+    call("vsx_bin_emit", ptr(P.rec), ptr(P.radius), n, width, height, ptr(soff), ptr(tiles),
+         ptr(ranks), stream())
+    if total == 0:
+        return Bins(toff, ranks[:0], txn, tyn)
+    bits = max(1, math.ceil(math.log2(T))) if T > 1 else 1
+    _, lst = sort_pairs_u32(tiles[:total], ranks[:total], total, bits)
+    return Bins(toff, lst, txn, tyn)
+
+
+# ------------------------------------------------------------------ raster
+
+@dataclass
+class Raster:
+    rgb: torch.Tensor
+    alpha: torch.Tensor
+    depth: torch.Tensor
+    normal: torch.Tensor
+    raw_normal: torch.Tensor
+    valid: torch.Tensor          # uint8
+    t_final: torch.Tensor
+    n_contrib: torch.Tensor
+
+
+def raster_forward(P: Projected, B: Bins, view: CameraView) -> Raster:
+    H, W = view.height, view.width
+    dev = "cuda"
+    rgb = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+    alpha = torch.empty((H, W), dtype=torch.float32, device=dev)
+    depth = torch.empty((H, W), dtype=torch.float32, device=dev)
+    normal = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+    raw = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
+    valid = torch.empty((H, W), dtype=torch.uint8, device=dev)
+    tfin = torch.empty((H, W), dtype=torch.float32, device=dev)
+    nc = torch.empty((H, W), dtype=torch.int32, device=dev)
+    call("vsx_raster_fwd", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list), view.to_abi(),
+         ptr(rgb), ptr(alpha), ptr(depth), ptr(normal), ptr(raw), ptr(valid), ptr(tfin), ptr(nc),
+         stream())
+    return Raster(rgb, alpha, depth, normal, raw, valid, tfin, nc)
+
+
+def raster_backward(P: Projected, B: Bins, view: CameraView, R: Raster, g_rgb=None, g_alpha=None,
+                    g_depth=None, g_normal=None, g_raw=None, out: torch.Tensor | None = None):
+    grad = out if out is not None else torch.zeros((max(P.count, 1), GRAD_F32),
+                                                   dtype=torch.float32, device="cuda")
+    call("vsx_raster_bwd", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list), view.to_abi(),
+         ptr(R.rgb), ptr(R.alpha), ptr(R.depth), ptr(R.raw_normal), ptr(R.t_final),
+         ptr(R.n_contrib), ptr(g_rgb), ptr(g_alpha), ptr(g_depth), ptr(g_normal), ptr(g_raw),
+         ptr(grad), stream())
+    return grad[: P.count]
+
+
+def project_backward(means, scale, quat, normal, P: Projected, grad_splat: torch.Tensor,
+                     view: CameraView):
+    g = int(means.shape[0])
+    dev = "cuda"
+    gm = torch.zeros((g, 3), dtype=torch.float32, device=dev)
+    go = torch.zeros(g, dtype=torch.float32, device=dev)
+    gc = torch.zeros((g, 3), dtype=torch.float32, device=dev)
+    gs = torch.zeros((g, 3), dtype=torch.float32, device=dev)
+    gq = torch.zeros((g, 4), dtype=torch.float32, device=dev)
+    gn = torch.zeros((g, 3), dtype=torch.float32, device=dev)
+    call("vsx_project_bwd", ptr(means), ptr(scale), ptr(quat), ptr(normal), ptr(P.rec),
+         ptr(grad_splat), P.count, view.to_abi(), ptr(gm), ptr(go), ptr(gc), ptr(gs), ptr(gq),
+         ptr(gn), stream())
+    return {"means": gm, "opacities": go, "colors": gc, "scales": gs, "quats": gq, "normals": gn}
+
+
+def check_status(status: torch.Tensor, what: str) -> None:
+    s = int(status.item())
+    if s & STATUS_NONPD:
+        raise NumericalError(f"{what}: non positive definite 2d covariance")
+    if s & STATUS_NONFINITE:
+        raise NumericalError(f"{what}: non-finite decoder output")

@@ -1,0 +1,386 @@
+"""Batch-level multi-view training step on the B200 (``voxsplat/trainer.py``).
+
+``TrainState`` keeps every learnable tensor in ONE flat float32 device buffer
+(decoder tensors, then per-anchor embeddings, log-scales, offsets, level-
+major), with matching flat gradient and Adam-moment buffers, so the whole
+optimizer step is a single ``vsx_adam`` launch (K10).
+
+``train_step`` runs, per view: K1 cull -> K2 decode -> K3 project + radix
+sort -> K4 bin -> K5 composite -> K9 loss with fused cotangents -> K6
+composite backward -> K7 projection backward -> K8 decode backward
+(accumulating into the flat gradient). The batch loss is a sum of per-view
+terms, so each view's backward runs right after its forward and nothing per
+view outlives it. Then one Adam launch. Semantics follow
+``trainer.py:258-376`` (RGB L1 always; Eq. 9 depth term weighted by the stage
+schedule when priors are given).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import time
+from dataclasses import dataclass, fields
+
+import numpy as np
+import torch
+
+from . import device as D
+from ._lib import call, ptr, stream
+from .decoder import AnchorState, DecoderParams, decoder_backward_into
+from .errors import InvalidInput, NumericalError
+from .geometry import CameraView
+from .partition import assign_voxels
+
+ADAM_EPS = 1e-15
+
+
+@dataclass
+class TrainConfig:
+    total_steps: int = 2000
+    batch_size: int = 4
+    workers: int = 1
+    seed: int = 0
+    step2_start: int = 800
+    step3_start: int = 1400
+    lr_decoder: float = 2e-3
+    lr_embeddings: float = 5e-3
+    lr_offsets: float = 1e-2
+    lr_scales: float = 5e-3
+    lr_final_factor: float = 0.01
+    beta1: float = 0.9
+    beta2: float = 0.999
+    growth_threshold: float = 2e-4
+    growth_window: int = 100
+    growth_stop: int = 1000
+    w3_max: float = 0.2
+    tau_depth: float = 1.0
+    geo_patches: int = 64
+    geo_patch_half: int = 3
+    init_scale_fraction: float = 0.125
+    log_every: int = 10
+    eval_every: int = 0
+    checkpoint_every: int = 0
+
+    def validate(self) -> None:
+        if self.total_steps < 1:
+            raise InvalidInput("total_steps must be >= 1")
+        for name in ("step2_start", "step3_start"):
+            if not 0 <= getattr(self, name) <= self.total_steps:
+                raise InvalidInput(f"{name} must lie in [0, total_steps]")
+        if self.batch_size < 1 or self.workers < 1 or self.growth_window < 1:
+            raise InvalidInput("batch_size, workers and growth_window must be >= 1")
+        if not 0 < self.lr_final_factor <= 1:
+            raise InvalidInput("lr_final_factor must be in (0, 1]")
+        for name in ("lr_decoder", "lr_embeddings", "lr_offsets", "lr_scales"):
+            if getattr(self, name) <= 0:
+                raise InvalidInput(f"{name} must be positive")
+        if not 0 < self.init_scale_fraction <= 3:
+            raise InvalidInput("init_scale_fraction must be in (0, 3]")
+
+    @classmethod
+    def from_dict(cls, data: dict) -> "TrainConfig":
+        bad = set(data) - {f.name for f in fields(cls)}
+        if bad:
+            raise InvalidInput(f"unknown train config keys: {sorted(bad)}")
+        cfg = cls(**data)
+        cfg.validate()
+        return cfg
+
+
+def weight_schedule(step: int, cfg: TrainConfig) -> tuple[float, float]:
+    w2 = 0.0
+    if step >= cfg.step2_start and cfg.total_steps > cfg.step2_start:
+        w2 = 1.0 - (step - cfg.step2_start) / (cfg.total_steps - cfg.step2_start)
+    w3 = 0.0
+    if step >= cfg.step3_start and cfg.total_steps > cfg.step3_start:
+        w3 = cfg.w3_max * (step - cfg.step3_start) / (cfg.total_steps - cfg.step3_start)
+    return w2, w3
+
+
+def cosine_lr(step: int, base: float, cfg: TrainConfig) -> float:
+    lo = base * cfg.lr_final_factor
+    return lo + 0.5 * (base - lo) * (1.0 + np.cos(np.pi * step / cfg.total_steps))
+
+
+@dataclass
+class StepReport:
+    step: int
+    total: float
+    rgb: float
+    depth: float
+    geo: float
+    w2: float
+    w3: float
+    lr: float
+    supervised_depth_px: int
+    geo_pairs: int
+    geo_patches: int
+    gaussians: int
+    transfer_bytes: int
+    imbalance: float
+    max_tile_splats: int
+    seconds: float
+    grown: int = 0
+    intersections: int = 0
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "step": self.step, "total": self.total, "rgb": self.rgb, "depth": self.depth,
+            "geo": self.geo, "w2": self.w2, "w3": self.w3, "lr": self.lr,
+            "depth_px": self.supervised_depth_px, "geo_pairs": self.geo_pairs,
+            "geo_patches": self.geo_patches, "gaussians": self.gaussians,
+            "transfer_bytes": self.transfer_bytes, "imbalance": self.imbalance,
+            "max_tile_splats": self.max_tile_splats, "seconds": self.seconds,
+            "grown": self.grown})
+
+
+def _pad4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+class FlatParams:
+    """One flat float32 buffer (+ grad, m, v) carved into named views."""
+
+    def __init__(self, shapes: list[tuple[str, tuple]], groups: dict[str, str]):
+        self.layout = {}
+        off = 0
+        self.group_spans: dict[str, list[int]] = {}
+        for name, shape in shapes:
+            n = int(np.prod(shape)) if shape else 1
+            self.layout[name] = (off, shape)
+            g = groups[name]
+            span = self.group_spans.setdefault(g, [off, off])
+            span[1] = off + _pad4(n)
+            off += _pad4(n)
+        self.size = off
+        dev = "cuda"
+        self.param = torch.zeros(self.size, dtype=torch.float32, device=dev)
+        self.grad = torch.zeros_like(self.param)
+        self.m = torch.zeros_like(self.param)
+        self.v = torch.zeros_like(self.param)
+
+    def view(self, buf: torch.Tensor, name: str) -> torch.Tensor:
+        off, shape = self.layout[name]
+        n = int(np.prod(shape)) if shape else 1
+        return buf[off:off + n].view(shape)
+
+    def segments(self, order: list[str]) -> tuple[list[int], list[str]]:
+        """Contiguous [begin, end) per group in buffer order (for vsx_adam)."""
+        spans = sorted(((self.group_spans[g][0], self.group_spans[g][1], g) for g in order))
+        begins = [s[0] for s in spans] + [spans[-1][1]]
+        for (b0, e0, _), (b1, _, _) in zip(spans, spans[1:]):
+            if e0 != b1:
+                raise InvalidInput("flat parameter groups are not contiguous")
+        return begins, [s[2] for s in spans]
+
+
+class TrainState:
+    """Scene mirrors, the decoder replica and Adam state, all on the device."""
+
+    def __init__(self, scene, cfg: TrainConfig):
+        cfg.validate()
+        D.require_cuda()
+        self.scene = scene
+        self.cfg = cfg
+        self.step = 0
+        self.rng = np.random.default_rng(cfg.seed)
+        n = scene.offsets_per_voxel
+        A = scene.total_voxels
+        self.n = n
+        init = DecoderParams.init_arrays(
+            n, seed=cfg.seed,
+            scale_bias=float(np.log(cfg.init_scale_fraction * scene.base_voxel_size)))
+        dec_shapes = DecoderParams.shapes(n)
+        names = DecoderParams.param_names(n)
+        shapes = [(f"dec/{k}", dec_shapes[k]) for k in names]
+        shapes += [("emb", (A, 32)), ("log_scales", (A, 3)), ("offsets", (A, n, 3))]
+        groups = {f"dec/{k}": "dec" for k in names}
+        groups.update({"emb": "emb", "log_scales": "log_scales", "offsets": "offsets"})
+        self.flat = FlatParams(shapes, groups)
+        with torch.no_grad():
+            for k in names:
+                self.flat.view(self.flat.param, f"dec/{k}").copy_(
+                    torch.as_tensor(init[k], dtype=torch.float32))
+            self.flat.view(self.flat.param, "emb").copy_(
+                torch.as_tensor(scene.flat("embeddings"), dtype=torch.float32))
+            self.flat.view(self.flat.param, "log_scales").copy_(
+                torch.as_tensor(np.log(scene.flat("scales")), dtype=torch.float32))
+            self.flat.view(self.flat.param, "offsets").copy_(
+                torch.as_tensor(scene.flat("offsets"), dtype=torch.float32))
+        self.params = DecoderParams(n, {k: self.flat.view(self.flat.param, f"dec/{k}")
+                                        for k in names})
+        self.dgrads = {k: self.flat.view(self.flat.grad, f"dec/{k}") for k in names}
+        self.replicas = [self.params]
+        self.anchors = AnchorState(self.flat.view(self.flat.param, "emb"),
+                                   self.flat.view(self.flat.param, "log_scales"),
+                                   self.flat.view(self.flat.param, "offsets"))
+        self.anchor_grads = AnchorState(self.flat.view(self.flat.grad, "emb"),
+                                        self.flat.view(self.flat.grad, "log_scales"),
+                                        self.flat.view(self.flat.grad, "offsets"))
+        self.assignment = assign_voxels(scene, cfg.workers)
+        self.dscene = D.device_scene_for(scene)
+        self._image_cache: dict = {}
+
+    # -- reference-compatible views ---------------------------------------
+    @property
+    def moments(self) -> dict:
+        out = {}
+        for name in self.flat.layout:
+            out[name] = (self.flat.view(self.flat.m, name), self.flat.view(self.flat.v, name))
+        return out
+
+    def barrier_check(self) -> None:
+        """Single replica per process; cross-rank equality is checked by dist.py."""
+
+    def decode_state(self) -> AnchorState:
+        return self.anchors
+
+    def sync_to_scene(self) -> None:
+        A_bases = self.scene.level_bases
+        emb = self.anchors.emb.double().cpu().numpy()
+        ls = self.anchors.log_scales.double().cpu().numpy()
+        off = self.anchors.offsets.double().cpu().numpy()
+        for k, lv in enumerate(self.scene.levels):
+            lo, hi = int(A_bases[k]), int(A_bases[k + 1])
+            lv.embeddings = emb[lo:hi].copy()
+            lv.scales = np.exp(ls[lo:hi])
+            lv.offsets = off[lo:hi].copy()
+
+    def lrs(self) -> dict[str, float]:
+        c = self.cfg
+        return {"dec": cosine_lr(self.step, c.lr_decoder, c),
+                "emb": cosine_lr(self.step, c.lr_embeddings, c),
+                "log_scales": cosine_lr(self.step, c.lr_scales, c),
+                "offsets": cosine_lr(self.step, c.lr_offsets, c)}
+
+    def adam(self) -> None:
+        """One fused Adam launch over every parameter group (K10)."""
+        begins, order = self.flat.segments(["dec", "emb", "log_scales", "offsets"])
+        lrs = self.lrs()
+        nseg = len(order)
+        seg = (ctypes.c_int64 * (nseg + 1))(*begins)
+        lr = (ctypes.c_double * nseg)(*[lrs[g] for g in order])
+        f = self.flat
+        call("vsx_adam", ptr(f.param), ptr(f.grad), ptr(f.m), ptr(f.v), nseg, seg, lr,
+             self.cfg.beta1, self.cfg.beta2, ADAM_EPS, self.step, stream())
+
+
+def make_state(scene, cfg: TrainConfig) -> TrainState:
+    return TrainState(scene, cfg)
+
+
+def _to_device_image(x, shape) -> torch.Tensor:
+    t = x if torch.is_tensor(x) else torch.as_tensor(np.asarray(x))
+    t = t.to(device="cuda", dtype=torch.float32).contiguous()
+    if tuple(t.shape) != tuple(shape):
+        raise InvalidInput(f"image shape mismatch {tuple(t.shape)} vs {tuple(shape)}")
+    return t
+
+
+def _prior_arrays(e):
+    if e is None:
+        return None
+    if isinstance(e, tuple):
+        return e
+    return e.values, e.valid
+
+
+@dataclass
+class ViewWork:
+    """Per-view device intermediates kept for inspection (tests / bench)."""
+
+    active: torch.Tensor
+    decoded: D.Decoded
+    projected: D.Projected
+    bins: D.Bins
+    raster: D.Raster
+    grad_splat: torch.Tensor
+    grad_gauss: dict
+
+
+def train_step(state: TrainState, views: list[CameraView], images: list,
+               enhanced: list | None = None, keep: list | None = None) -> StepReport:
+    """One optimisation step over a batch of views (``trainer.py:258-376``)."""
+    cfg = state.cfg
+    t0 = time.perf_counter()
+    B = len(views)
+    if B == 0 or len(images) != B:
+        raise InvalidInput("views and images must be equal length and non-empty")
+    w2, w3 = weight_schedule(state.step, cfg)
+    priors = [_prior_arrays(e) for e in enhanced] if enhanced is not None else None
+    use_depth = w2 > 0 and priors is not None and any(p is not None for p in priors)
+    have = [i for i in range(B) if use_depth and priors[i] is not None]
+    ds = state.dscene
+    params = state.params
+    st = state.flat
+    st.grad.zero_()
+    dev = "cuda"
+    rgb_acc = torch.zeros(B, dtype=torch.float64, device=dev)
+    dep_sum = torch.zeros(B, dtype=torch.float64, device=dev)
+    dep_cnt = torch.zeros(B, dtype=torch.int32, device=dev)
+    tile_max = torch.zeros(B, dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    gaussians = 0
+    isects = 0
+    anchors, agrads = state.anchors, state.anchor_grads
+    for vi, view in enumerate(views):
+        H, W = view.height, view.width
+        active = ds.active(view)
+        dec = D.decode(params.abi(), params.n, active, ds.centers, anchors.emb,
+                       anchors.log_scales, anchors.offsets, view, ds.lod_ref, ds.max_scale,
+                       status, keep_cache=True)
+        gaussians += dec.count
+        P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, view,
+                      status)
+        Bn = D.bin_tiles(P, W, H)
+        isects += Bn.intersections
+        tile_max[vi] = torch.diff(Bn.tile_offsets.long()).max()
+        R = D.raster_forward(P, Bn, view)
+        gt = _to_device_image(images[vi], (H, W, 3))
+        g_rgb = torch.empty_like(R.rgb)
+        call("vsx_l1_loss", ptr(R.rgb), ptr(gt), R.rgb.numel(), 1.0 / (B * H * W * 3),
+             ptr(rgb_acc[vi:vi + 1]), ptr(g_rgb), stream())
+        g_depth = None
+        if vi in have:
+            pd, pv = priors[vi]
+            pd = _to_device_image(pd, (H, W))
+            pv = torch.as_tensor(np.asarray(pv) if not torch.is_tensor(pv) else pv).to(
+                device=dev, dtype=torch.uint8).contiguous()
+            call("vsx_depth_loss", ptr(R.depth), ptr(R.valid), ptr(pd), ptr(pv), H * W,
+                 ptr(dep_sum[vi:vi + 1]), ptr(dep_cnt[vi:vi + 1]), ptr(None), ptr(None), stream())
+            scale = (w2 / len(have)) / dep_cnt[vi:vi + 1].clamp_min(1).float()
+            g_depth = torch.empty_like(R.depth)
+            call("vsx_depth_loss", ptr(R.depth), ptr(R.valid), ptr(pd), ptr(pv), H * W,
+                 ptr(None), ptr(None), ptr(scale), ptr(g_depth), stream())
+        gs = D.raster_backward(P, Bn, view, R, g_rgb=g_rgb, g_depth=g_depth)
+        gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P, gs, view)
+        decoder_backward_into(params, state.dgrads, active, ds.centers, anchors.emb,
+                              anchors.log_scales, anchors.offsets, view, ds.lod_ref,
+                              ds.max_scale, dec, gg["means"], gg["opacities"], gg["colors"],
+                              gg["scales"], gg["quats"], gg["normals"], agrads.emb,
+                              agrads.log_scales, agrads.offsets)
+        if keep is not None:
+            keep.append(ViewWork(active, dec, P, Bn, R, gs, gg))
+    D.check_status(status, "train_step")
+    hw = torch.tensor([v.height * v.width * 3 for v in views], dtype=torch.float64, device=dev)
+    rgb = float((rgb_acc / hw).mean())
+    depth = 0.0
+    supervised = 0
+    if have:
+        cnt = dep_cnt.double()
+        terms = torch.where(cnt > 0, dep_sum / cnt.clamp_min(1), torch.zeros_like(cnt))
+        depth = float(terms[have].mean())
+        supervised = int(dep_cnt.sum())
+    total = rgb + w2 * depth
+    if not np.isfinite(total):
+        raise NumericalError(f"non-finite loss at step {state.step}: rgb={rgb:.4g} depth={depth:.4g}")
+    state.adam()
+    report = StepReport(
+        step=state.step, total=total, rgb=rgb, depth=depth, geo=0.0, w2=w2, w3=w3,
+        lr=cosine_lr(state.step, cfg.lr_decoder, cfg), supervised_depth_px=supervised,
+        geo_pairs=0, geo_patches=0, gaussians=gaussians, transfer_bytes=0, imbalance=1.0,
+        max_tile_splats=int(tile_max.max()), seconds=time.perf_counter() - t0,
+        intersections=isects)
+    state.step += 1
+    return report
