@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""bench.py — RGB-D-N fwd+bwd training views/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "cfg2"): synthetic aerial city block,
+~200k anchors x 10 gaussians (K=3 LoD levels, LoD bias 2), a batch of 8 views
+at 1920x1080 per step, loss = L1 rgb + depth-prior L1 (Eq. 9, weight 1 at
+step 0) + normal-prior L1 (weight 0.5). One step = cull, decode, project,
+sort, bin, composite, loss, composite backward, projection backward, decode
+backward for all 8 views, then the fused Adam over every parameter.
+Targets are rendered by a "teacher" (same scene, different decoder seed and
+embeddings) on the device before timing. Inputs (>> L2 per step: 8 views x
+1080p x RGB/depth/normal targets + ~0.5 GB of per-view intermediates) are
+larger than the 126 MB L2, so no explicit flush is needed.
+
+  python bench.py [--gpus N --steps K --warmup W]            # CUDA path
+  python bench.py --impl reference [--steps K --warmup W]    # CPU oracle arm
+
+Under torchrun (N>1) every rank trains its own replica on its own 8 views
+(replicas, weak scaling) and rank 0 prints one JSON line with the max-over-
+ranks device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+METRIC = "RGB-D-N fwd+bwd train views/sec at 1/2/4/8 B200 vs CPU ref; raster HBM GB/s"
+CFG2_VOXEL = 1.119          # base voxel size giving ~200k anchors over 3 levels
+CFG2_LOD_BIAS = 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["vsx", "reference"], default="vsx")
+    ap.add_argument("--config", choices=["cfg2", "cfg1"], default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-tiles", type=int, default=48,
+                    help="tiles per CPU-baseline sample (evenly spaced over the view)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ workload
+
+def workload(config: str):
+    from paper_2503_23044_b200.synthetic import cfg1_scene, city_scene
+    if config == "cfg1":
+        scene, views, images = cfg1_scene()
+        return scene, views, {"workload": "cfg1: 10,198 anchors x 10 gaussians, 4 views 128x128",
+                              "anchors": scene.total_voxels, "views_per_step": 4,
+                              "resolution": "128x128", "loss": "rgb"}, images
+    scene, views = city_scene(target_anchors=200_000, base_voxel_size=CFG2_VOXEL)
+    scene.lod_bias = CFG2_LOD_BIAS
+    desc = {"workload": "cfg2: synthetic aerial city block, 200k anchors x 10 gaussians "
+                        "(K=3, LoD bias 2), 8 views/step at 1920x1080, RGB+depth+normal loss",
+            "anchors": scene.total_voxels, "gaussians_total": scene.total_voxels * 10,
+            "views_per_step": len(views), "resolution": "1920x1080",
+            "loss": "L1 rgb + depth-prior L1 (Eq.9) + 0.5 normal-prior L1",
+            "l2_flush": "inputs > L2 (per-step working set ~GBs)"}
+    return scene, views, desc, None
+
+
+def teacher_targets(scene, views):
+    """Render RGB / depth / normal targets with a perturbed teacher on the device."""
+    import torch
+    from paper_2503_23044_b200 import device as D
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState
+    teacher = TrainState(scene, TrainConfig(seed=7, total_steps=10))
+    g = torch.Generator(device="cuda").manual_seed(7)
+    with torch.no_grad():
+        teacher.anchors.emb.add_(torch.randn(teacher.anchors.emb.shape, generator=g,
+                                             device="cuda") * 0.5)
+    ds = teacher.dscene
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = []
+    for v in views:
+        act = ds.active(v)
+        dec = D.decode(teacher.params.abi(), teacher.n, act, ds.centers, teacher.anchors.emb,
+                       teacher.anchors.log_scales, teacher.anchors.offsets, v, ds.lod_ref,
+                       ds.max_scale, status, keep_cache=False)
+        P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, v,
+                      status)
+        R = D.raster_forward(P, D.bin_tiles(P, v.width, v.height), v)
+        out.append({"rgb": R.rgb.clone(), "depth": R.depth.clone(), "valid": R.valid.clone(),
+                    "normal": R.normal.clone()})
+    D.check_status(status, "teacher")
+    del teacher
+    return out
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = Path(tempfile.mkstemp(prefix="clocks_", suffix=".csv")[1])
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        rows = [r.split(", ") for r in self.path.read_text().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+
+def cpu_sample(scene, views, tiles: int, images=None) -> dict:
+    """Oracle (float64 CPU port) on ONE view of the workload, time-extrapolated.
+
+    Full cull/decode/project/bin for the view, composite fwd+bwd on `tiles`
+    evenly spaced non-empty tiles, full projection+decode backward; the tile
+    time is scaled by intersections(total)/intersections(sampled).
+    """
+    import torch
+    import oracle
+    torch.set_num_threads(os.cpu_count() or 1)
+    n = scene.offsets_per_voxel
+    w = oracle.decoder_init(n, 0, float(np.log(0.125 * scene.base_voxel_size)))
+    st = oracle.OracleState.create(
+        scene.flat_centers(), scene.flat_levels(), scene.lod_count, scene.lod_ref_distance,
+        scene.lod_bias, scene.base_voxel_size, n, w, scene.flat("embeddings"),
+        np.log(scene.flat("scales")), scene.flat("offsets"), total_steps=30000)
+    v = views[0]
+    img = images[0] if images is not None else \
+        np.random.default_rng(0).uniform(0, 1, (v.height, v.width, 3))
+    t0 = time.perf_counter()
+    oracle.train_step(st, [oracle.Cam.of(v)], [img], tile_limit=tiles)
+    wall = time.perf_counter() - t0
+    tm = st.last_timing
+    t_tiles = tm["t_tiles"] * tm["isect_total"] / max(tm["isect_sampled"], 1)
+    t_view = tm["t_fixed"] + t_tiles
+    return {"value": 1.0 / t_view, "unit": "views/s", "cores": torch.get_num_threads(),
+            "kind": "port", "wall_s": wall,
+            "sample": (f"oracle/ float64 port, 1 view of the workload: full cull/decode/project/"
+                       f"bin, composite fwd+bwd on {tm['tiles_done']} of {tm['tiles_nonempty']} "
+                       f"non-empty tiles ({tm['isect_sampled']} of {tm['isect_total']} "
+                       f"intersections, extrapolated by intersections), RGB L1 term, "
+                       f"Adam excluded; {wall:.1f}s measured")}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    scene, views, desc, images = workload(args.config)
+    if args.config == "cfg1":
+        tiles = None
+    else:
+        tiles = args.cpu_tiles
+    vals = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(scene, views, tiles if tiles else 10**9, images)
+        if i >= args.warmup:
+            vals.append(s)
+    value = float(np.median([s["value"] for s in vals]))
+    cb = dict(vals[-1])
+    cb["value"] = value
+    line = {"metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": desc, "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ CUDA arm
+
+def raster_bytes(stage: str, isect: int, pixels: int, splats: int) -> int:
+    """Algorithmic bytes per raster launch."""
+    if stage == "raster_fwd":
+        return isect * (4 + 52) + pixels * 48
+    return isect * 56 + pixels * (32 + 28) + splats * 52
+
+
+def run_vsx(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    from paper_2503_23044_b200 import _lib
+    from paper_2503_23044_b200.trainer import GpuTimer, TrainConfig, TrainState, train_step
+    lib = _lib.load()
+    scene, views, desc, images = workload(args.config)
+    cfg2 = args.config == "cfg2"
+    cfg = TrainConfig(total_steps=30000, batch_size=len(views), step2_start=0 if cfg2 else 30000,
+                      step3_start=30000, growth_stop=0, normal_weight=0.5 if cfg2 else 0.0)
+    if cfg2:
+        tgt = teacher_targets(scene, views)
+        imgs = [t["rgb"] for t in tgt]
+        priors = [(t["depth"], t["valid"]) for t in tgt]
+        nprior = [(t["normal"], t["valid"]) for t in tgt]
+    else:
+        imgs = [torch.as_tensor(np.asarray(im, np.float32)).cuda() for im in images]
+        priors = nprior = None
+    state = TrainState(scene, cfg)
+    for _ in range(args.warmup):
+        train_step(state, views, imgs, priors, normal_priors=nprior)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    timer = GpuTimer()
+    launches0 = lib.vsx_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record()
+    reps = []
+    for _ in range(args.steps):
+        reps.append(train_step(state, views, imgs, priors, normal_priors=nprior, timer=timer))
+    ev1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = lib.vsx_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    stage_ms = timer.totals_ms()
+    stage_n = timer.counts()
+    # roofline of the dominant single-launch compositing kernel
+    isect = sum(r.intersections for r in reps)
+    pixels = sum(v.width * v.height for v in views) * args.steps
+    splats = sum(r.gaussians for r in reps)
+    dom = max(("raster_fwd", "raster_bwd"), key=lambda k: stage_ms.get(k, 0.0))
+    per_launch_bytes = raster_bytes(dom, isect, pixels, splats) / stage_n[dom]
+    per_launch_s = stage_ms[dom] / 1e3 / stage_n[dom]
+    peaks = measured_peaks()
+    achieved = per_launch_bytes / per_launch_s / 1e9
+    value = len(views) * world / (ms / 1e3)
+    # end to end through the public API with host buffers (pinned H2D + loss D2H)
+    e2e = None
+    if not args.no_e2e:
+        himgs = [t.cpu().pin_memory() for t in imgs]
+        hpri = [(d.cpu().pin_memory(), v.cpu().pin_memory()) for d, v in priors] if priors else None
+        hnrm = [(nn.cpu().pin_memory(), v.cpu().pin_memory()) for nn, v in nprior] if nprior else None
+        h2d = sum(t.numel() * t.element_size() for t in himgs)
+        if hpri:
+            h2d += sum(d.numel() * 4 + v.numel() for d, v in hpri)
+        if hnrm:
+            h2d += sum(nn.numel() * 4 + v.numel() for nn, v in hnrm)
+        train_step(state, views, himgs, hpri, normal_priors=hnrm)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            train_step(state, views, himgs, hpri, normal_priors=hnrm)
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": len(views) * world / (ems / 1e3), "unit": "views/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * 4 + 8}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(scene, views, args.cpu_tiles if cfg2 else 10**9, images)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    desc = dict(desc)
+    desc["parallelism"] = f"replicas{world}" if world > 1 else "single"
+    line = {
+        "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": desc,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "peak_src": peaks["src"],
+                     "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_s * 1e3},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk,
+        "stages_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
+        "per_step": {"gaussians": reps[-1].gaussians, "intersections": reps[-1].intersections,
+                     "loss_total": reps[-1].total, "loss_rgb": reps[-1].rgb,
+                     "loss_depth": reps[-1].depth, "loss_normal": reps[-1].normal},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_vsx(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -89,6 +89,8 @@ typedef struct vsx_decoder_grads {
 
 const char *vsx_last_error(void);
 int vsx_version(void);
+/* Number of kernels this library has launched so far (monotonic). */
+uint64_t vsx_launch_count(void);
 
 /* ---- generic device primitives ---------------------------------------- */
 /* Workspace bytes needed by vsx_sort_pairs_* / vsx_select / vsx_scan for n items. */
@@ -204,6 +206,12 @@ int vsx_l1_loss(const float *rendered, const float *target, int64_t n, float sca
 int vsx_depth_loss(const float *depth, const uint8_t *valid, const float *prior,
                    const uint8_t *prior_valid, int64_t n, double *sums, uint32_t *counts,
                    const float *scale, float *grad, vsx_stream s);
+
+/* Generic masked L1 over `channels` values per pixel (normal-prior term of
+ * the RGB-D-N objective; channels = 1 reproduces vsx_depth_loss). */
+int vsx_masked_l1(const float *x, const uint8_t *valid, const float *prior,
+                  const uint8_t *prior_valid, int64_t n_pix, int32_t channels, double *sums,
+                  uint32_t *counts, const float *scale, float *grad, vsx_stream s);
 
 /* ---- K10: fused Adam (trainer.py:220-247) ------------------------------- */
 /* One launch over n_seg contiguous segments; seg_begin (n_seg+1, host) are

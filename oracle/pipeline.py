@@ -15,6 +15,7 @@ call up to float64 summation order).
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -440,6 +441,7 @@ class OracleState:
     step: int = 0
     moments: dict = field(default_factory=dict)
     last_grads: dict = field(default_factory=dict)
+    last_timing: dict = field(default_factory=dict)
 
     @classmethod
     def create(cls, centers, levels, lod_count, lod_ref, lod_bias, base_voxel_size, n,
@@ -511,7 +513,9 @@ def train_step(st: OracleState, cams: list, images: list, priors: list | None = 
         p.grad = None
     have = [i for i in range(B) if use_depth and priors[i] is not None]
     rgb_terms, depth_terms, supervised, gaussians, max_tile = [], [], 0, 0, 0
+    timing = {"t_fixed": 0.0, "t_tiles": 0.0, "tiles_done": 0, "tiles_nonempty": 0}
     for vi, cam in enumerate(cams):
+        tv = time.perf_counter()
         P, active, flat = _view_splats(st, cam, grad=True)
         gaussians += flat["means"].shape[0]
         offsets, lists = bin_tiles(P["mean2d"].detach().numpy(), P["radius"],
@@ -534,12 +538,18 @@ def train_step(st: OracleState, cams: list, images: list, priors: list | None = 
         rgb_sum = torch.zeros((), dtype=F64)
         dep_sum = torch.zeros((), dtype=F64)
         done = 0
-        for t in range(tx_n * ty_n):
+        timing["tiles_nonempty"] += int((np.diff(offsets) > 0).sum())
+        tt = time.perf_counter()
+        timing["t_fixed"] += tt - tv
+        busy = np.flatnonzero(np.diff(offsets) > 0)
+        if tile_limit is not None and busy.size > tile_limit:
+            # evenly spaced sample of the non-empty tiles (bounded CPU baseline)
+            busy = busy[np.linspace(0, busy.size - 1, tile_limit).round().astype(np.int64)]
+        timing["isect_sampled"] = timing.get("isect_sampled", 0) + int(
+            np.diff(offsets)[busy].sum())
+        timing["isect_total"] = timing.get("isect_total", 0) + int(offsets[-1])
+        for t in busy:
             lo, hi = int(offsets[t]), int(offsets[t + 1])
-            if hi == lo:
-                continue
-            if tile_limit is not None and done >= tile_limit:
-                break
             done += 1
             ty, tx = divmod(t, tx_n)
             out = raster_tile(leaves, lists[lo:hi], tx, ty, cam)
@@ -557,12 +567,17 @@ def train_step(st: OracleState, cams: list, images: list, priors: list | None = 
                 dep_sum = dep_sum + dd.detach()
             if obj.requires_grad:
                 obj.backward()
+        tb = time.perf_counter()
+        timing["t_tiles"] += tb - tt
+        timing["tiles_done"] += done
         rgb_terms.append(rgb_sum / (H * W * 3))
         if vi in have:
             depth_terms.append(dep_sum * (dnorm * len(have) / w2))
         grads = [leaves[k].grad if leaves[k].grad is not None else torch.zeros_like(leaves[k])
                  for k in SPLAT_KEYS]
         torch.autograd.backward([P[k] for k in SPLAT_KEYS], grads)
+        timing["t_fixed"] += time.perf_counter() - tb
+    st.last_timing = timing
     rgb = torch.stack(rgb_terms).mean()
     depth = torch.stack(depth_terms).mean() if depth_terms else torch.zeros((), dtype=F64)
     total = rgb + w2 * depth

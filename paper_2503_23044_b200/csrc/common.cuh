@@ -19,8 +19,11 @@
     }                                                        \
   } while (0)
 
+void vsx_count_launch();
+
 #define VSX_LAUNCH_CHECK(name)                                          \
   do {                                                                  \
+    vsx_count_launch();                                                 \
     cudaError_t _e = cudaGetLastError();                                \
     if (_e != cudaSuccess) {                                            \
       vsx_set_error("%s launch: %s", name, cudaGetErrorString(_e));     \
@@ -67,12 +70,20 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
-// x_cam = R x + t with the row dot products evaluated left to right.
+// x_cam = R x + t, rounded exactly like the reference's `p @ R.T + t`: the
+// host BLAS dgemm accumulates the K=3 dot product as fma(p2, r2, fma(p1, r1,
+// p0*r0)) (verified bit-for-bit against numpy and torch on the build host),
+// then the bias add is a separate rounded op.
+__device__ __forceinline__ double dot3_blas(double a0, double a1, double a2, double b0, double b1,
+                                            double b2) {
+  return __fma_rn(a2, b2, __fma_rn(a1, b1, dmul(a0, b0)));
+}
+
 __device__ __forceinline__ void cam_transform(const vsx_camera &c, double x, double y, double z,
                                               double &ox, double &oy, double &oz) {
-  ox = dadd(dadd(dadd(dmul(c.r[0], x), dmul(c.r[1], y)), dmul(c.r[2], z)), c.t[0]);
-  oy = dadd(dadd(dadd(dmul(c.r[3], x), dmul(c.r[4], y)), dmul(c.r[5], z)), c.t[1]);
-  oz = dadd(dadd(dadd(dmul(c.r[6], x), dmul(c.r[7], y)), dmul(c.r[8], z)), c.t[2]);
+  ox = dadd(dot3_blas(x, y, z, c.r[0], c.r[1], c.r[2]), c.t[0]);
+  oy = dadd(dot3_blas(x, y, z, c.r[3], c.r[4], c.r[5]), c.t[1]);
+  oz = dadd(dot3_blas(x, y, z, c.r[6], c.r[7], c.r[8]), c.t[2]);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

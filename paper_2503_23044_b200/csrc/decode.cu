@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
             }
           }
           // means = c + offset * l
-          const float *off = offsets + g * 3;
+          const float *off = offsets + ((size_t)a * n + sl) * 3;
           float *goff = g_offsets + ((size_t)a * n + sl) * 3;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {

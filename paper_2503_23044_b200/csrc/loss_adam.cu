@@ -61,6 +61,35 @@ __global__ void __launch_bounds__(256) depth_l1_kernel(
   }
 }
 
+// Masked multi-channel L1 (normal-prior term, same masking rule as the depth
+// term): mask = valid & prior_valid per pixel, |x - p| summed over channels.
+__global__ void __launch_bounds__(256) masked_l1_kernel(
+    const float *__restrict__ x, const uint8_t *__restrict__ valid, const float *__restrict__ p,
+    const uint8_t *__restrict__ pv, int64_t n_pix, int channels, double *__restrict__ sums,
+    uint32_t *__restrict__ counts, const float *__restrict__ scale, float *__restrict__ grad) {
+  double acc = 0.0;
+  uint32_t cnt = 0;
+  const float sc = (grad && scale) ? *scale : 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pix;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool m = valid[i] && pv[i];
+    cnt += m ? 1u : 0u;
+    for (int c = 0; c < channels; ++c) {
+      const int64_t j = i * channels + c;
+      const float diff = x[j] - p[j];
+      if (m) acc += fabs((double)diff);
+      if (grad) grad[j] = m ? signf_(diff) * sc : 0.f;
+    }
+  }
+  acc = warp_sum_d(acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) {
+    if (sums) atomicAdd(sums, acc);
+    if (counts) atomicAdd(counts, cnt);
+  }
+}
+
 constexpr int kMaxSeg = 16;
 struct AdamSegs {
   int64_t begin[kMaxSeg + 1];
@@ -117,6 +146,18 @@ extern "C" int vsx_depth_loss(const float *depth, const uint8_t *valid, const fl
   depth_l1_kernel<<<persistent_grid(n), 256, 0, as_stream(s)>>>(depth, valid, prior, prior_valid,
                                                                 n, sums, counts, scale, grad);
   VSX_LAUNCH_CHECK("depth_loss");
+  return VSX_OK;
+}
+
+extern "C" int vsx_masked_l1(const float *x, const uint8_t *valid, const float *prior,
+                             const uint8_t *prior_valid, int64_t n_pix, int32_t channels,
+                             double *sums, uint32_t *counts, const float *scale, float *grad,
+                             vsx_stream s) {
+  VSX_REQUIRE(n_pix >= 0 && channels >= 1, "masked_l1: bad args");
+  if (n_pix == 0) return VSX_OK;
+  masked_l1_kernel<<<persistent_grid(n_pix), 256, 0, as_stream(s)>>>(
+      x, valid, prior, prior_valid, n_pix, channels, sums, counts, scale, grad);
+  VSX_LAUNCH_CHECK("masked_l1");
   return VSX_OK;
 }
 

@@ -1,6 +1,7 @@
 // Generic device primitives: error state, exclusive scan, ordered select,
 // stable LSD radix sort. Hand-written (no CUB) so the sort's stability —
 // which carries the reference's (z, gid) tie-break — is explicit.
+#include <atomic>
 #include <cstdarg>
 
 #include "common.cuh"
@@ -16,6 +17,12 @@ void vsx_set_error(const char *fmt, ...) {
 
 extern "C" const char *vsx_last_error(void) { return g_err; }
 extern "C" int vsx_version(void) { return 1; }
+
+// Every kernel launch of this library bumps one counter (VSX_LAUNCH_CHECK),
+// so callers can report how many of OUR kernels ran in a timed region.
+static std::atomic<unsigned long long> g_launches{0};
+void vsx_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" uint64_t vsx_launch_count(void) { return g_launches.load(); }
 
 namespace vsx {
 

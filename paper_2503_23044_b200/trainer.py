@@ -17,6 +17,7 @@ schedule when priors are given).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import json
 import time
@@ -58,6 +59,8 @@ class TrainConfig:
     geo_patches: int = 64
     geo_patch_half: int = 3
     init_scale_fraction: float = 0.125
+    # extension: weight of the normal-prior L1 (0 = reference objective)
+    normal_weight: float = 0.0
     log_every: int = 10
     eval_every: int = 0
     checkpoint_every: int = 0
@@ -123,6 +126,7 @@ class StepReport:
     seconds: float
     grown: int = 0
     intersections: int = 0
+    normal: float = 0.0
 
     def to_json(self) -> str:
         return json.dumps({
@@ -299,9 +303,64 @@ class ViewWork:
     grad_gauss: dict
 
 
+class GpuTimer:
+    """CUDA-event spans on the current stream, summed per stage name."""
+
+    def __init__(self) -> None:
+        self.spans: list[tuple[str, torch.cuda.Event, torch.cuda.Event]] = []
+
+    @contextlib.contextmanager
+    def span(self, name: str):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        try:
+            yield
+        finally:
+            b.record()
+            self.spans.append((name, a, b))
+
+    def totals_ms(self) -> dict[str, float]:
+        torch.cuda.synchronize()
+        out: dict[str, float] = {}
+        for name, a, b in self.spans:
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
+
+    def counts(self) -> dict[str, int]:
+        out: dict[str, int] = {}
+        for name, _, _ in self.spans:
+            out[name] = out.get(name, 0) + 1
+        return out
+
+
+_NULL = contextlib.nullcontext()
+
+
+def _span(timer, name):
+    return timer.span(name) if timer is not None else _NULL
+
+
+def _mask_u8(v, shape) -> torch.Tensor:
+    t = v if torch.is_tensor(v) else torch.as_tensor(np.asarray(v))
+    t = t.to(device="cuda", dtype=torch.uint8).contiguous()
+    if tuple(t.shape) != tuple(shape):
+        raise InvalidInput(f"mask shape mismatch {tuple(t.shape)} vs {tuple(shape)}")
+    return t
+
+
 def train_step(state: TrainState, views: list[CameraView], images: list,
-               enhanced: list | None = None, keep: list | None = None) -> StepReport:
-    """One optimisation step over a batch of views (``trainer.py:258-376``)."""
+               enhanced: list | None = None, keep: list | None = None,
+               normal_priors: list | None = None, timer: GpuTimer | None = None) -> StepReport:
+    """One optimisation step over a batch of views (``trainer.py:258-376``).
+
+    ``enhanced`` holds per-view depth priors (EnhancedDepthMap or (depth,
+    valid)) for the Eq. 9 term, weighted by the stage schedule.
+    ``normal_priors`` (optional, (normals, valid) per view) add the normal
+    term of the RGB-D-N objective with weight ``cfg.normal_weight`` (an
+    extension: the reference supervises normals only through the depth
+    quotient and Eq. 10). Images/priors may be host arrays or CUDA tensors.
+    """
     cfg = state.cfg
     t0 = time.perf_counter()
     B = len(views)
@@ -311,6 +370,9 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     priors = [_prior_arrays(e) for e in enhanced] if enhanced is not None else None
     use_depth = w2 > 0 and priors is not None and any(p is not None for p in priors)
     have = [i for i in range(B) if use_depth and priors[i] is not None]
+    wn = float(getattr(cfg, "normal_weight", 0.0))
+    use_normal = wn > 0 and normal_priors is not None
+    have_n = [i for i in range(B) if use_normal and normal_priors[i] is not None]
     ds = state.dscene
     params = state.params
     st = state.flat
@@ -319,6 +381,8 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     rgb_acc = torch.zeros(B, dtype=torch.float64, device=dev)
     dep_sum = torch.zeros(B, dtype=torch.float64, device=dev)
     dep_cnt = torch.zeros(B, dtype=torch.int32, device=dev)
+    nrm_sum = torch.zeros(B, dtype=torch.float64, device=dev)
+    nrm_cnt = torch.zeros(B, dtype=torch.int32, device=dev)
     tile_max = torch.zeros(B, dtype=torch.int64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     gaussians = 0
@@ -326,40 +390,59 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     anchors, agrads = state.anchors, state.anchor_grads
     for vi, view in enumerate(views):
         H, W = view.height, view.width
-        active = ds.active(view)
-        dec = D.decode(params.abi(), params.n, active, ds.centers, anchors.emb,
-                       anchors.log_scales, anchors.offsets, view, ds.lod_ref, ds.max_scale,
-                       status, keep_cache=True)
+        with _span(timer, "cull"):
+            active = ds.active(view)
+        with _span(timer, "decode_fwd"):
+            dec = D.decode(params.abi(), params.n, active, ds.centers, anchors.emb,
+                           anchors.log_scales, anchors.offsets, view, ds.lod_ref, ds.max_scale,
+                           status, keep_cache=True)
         gaussians += dec.count
-        P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, view,
-                      status)
-        Bn = D.bin_tiles(P, W, H)
+        with _span(timer, "project_sort"):
+            P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal,
+                          view, status)
+        with _span(timer, "bin_sort"):
+            Bn = D.bin_tiles(P, W, H)
         isects += Bn.intersections
         tile_max[vi] = torch.diff(Bn.tile_offsets.long()).max()
-        R = D.raster_forward(P, Bn, view)
-        gt = _to_device_image(images[vi], (H, W, 3))
-        g_rgb = torch.empty_like(R.rgb)
-        call("vsx_l1_loss", ptr(R.rgb), ptr(gt), R.rgb.numel(), 1.0 / (B * H * W * 3),
-             ptr(rgb_acc[vi:vi + 1]), ptr(g_rgb), stream())
-        g_depth = None
-        if vi in have:
-            pd, pv = priors[vi]
-            pd = _to_device_image(pd, (H, W))
-            pv = torch.as_tensor(np.asarray(pv) if not torch.is_tensor(pv) else pv).to(
-                device=dev, dtype=torch.uint8).contiguous()
-            call("vsx_depth_loss", ptr(R.depth), ptr(R.valid), ptr(pd), ptr(pv), H * W,
-                 ptr(dep_sum[vi:vi + 1]), ptr(dep_cnt[vi:vi + 1]), ptr(None), ptr(None), stream())
-            scale = (w2 / len(have)) / dep_cnt[vi:vi + 1].clamp_min(1).float()
-            g_depth = torch.empty_like(R.depth)
-            call("vsx_depth_loss", ptr(R.depth), ptr(R.valid), ptr(pd), ptr(pv), H * W,
-                 ptr(None), ptr(None), ptr(scale), ptr(g_depth), stream())
-        gs = D.raster_backward(P, Bn, view, R, g_rgb=g_rgb, g_depth=g_depth)
-        gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P, gs, view)
-        decoder_backward_into(params, state.dgrads, active, ds.centers, anchors.emb,
-                              anchors.log_scales, anchors.offsets, view, ds.lod_ref,
-                              ds.max_scale, dec, gg["means"], gg["opacities"], gg["colors"],
-                              gg["scales"], gg["quats"], gg["normals"], agrads.emb,
-                              agrads.log_scales, agrads.offsets)
+        with _span(timer, "raster_fwd"):
+            R = D.raster_forward(P, Bn, view)
+        with _span(timer, "loss"):
+            gt = _to_device_image(images[vi], (H, W, 3))
+            g_rgb = torch.empty_like(R.rgb)
+            call("vsx_l1_loss", ptr(R.rgb), ptr(gt), R.rgb.numel(), 1.0 / (B * H * W * 3),
+                 ptr(rgb_acc[vi:vi + 1]), ptr(g_rgb), stream())
+            g_depth = g_normal = None
+            if vi in have:
+                pd = _to_device_image(priors[vi][0], (H, W))
+                pv = _mask_u8(priors[vi][1], (H, W))
+                call("vsx_depth_loss", ptr(R.depth), ptr(R.valid), ptr(pd), ptr(pv), H * W,
+                     ptr(dep_sum[vi:vi + 1]), ptr(dep_cnt[vi:vi + 1]), ptr(None), ptr(None),
+                     stream())
+                scale = (w2 / len(have)) / dep_cnt[vi:vi + 1].clamp_min(1).float()
+                g_depth = torch.empty_like(R.depth)
+                call("vsx_depth_loss", ptr(R.depth), ptr(R.valid), ptr(pd), ptr(pv), H * W,
+                     ptr(None), ptr(None), ptr(scale), ptr(g_depth), stream())
+            if vi in have_n:
+                pn = _to_device_image(normal_priors[vi][0], (H, W, 3))
+                pnv = _mask_u8(normal_priors[vi][1], (H, W))
+                call("vsx_masked_l1", ptr(R.normal), ptr(R.valid), ptr(pn), ptr(pnv), H * W, 3,
+                     ptr(nrm_sum[vi:vi + 1]), ptr(nrm_cnt[vi:vi + 1]), ptr(None), ptr(None),
+                     stream())
+                nscale = (wn / len(have_n) / 3.0) / nrm_cnt[vi:vi + 1].clamp_min(1).float()
+                g_normal = torch.empty_like(R.normal)
+                call("vsx_masked_l1", ptr(R.normal), ptr(R.valid), ptr(pn), ptr(pnv), H * W, 3,
+                     ptr(None), ptr(None), ptr(nscale), ptr(g_normal), stream())
+        with _span(timer, "raster_bwd"):
+            gs = D.raster_backward(P, Bn, view, R, g_rgb=g_rgb, g_depth=g_depth,
+                                   g_normal=g_normal)
+        with _span(timer, "project_bwd"):
+            gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P, gs, view)
+        with _span(timer, "decode_bwd"):
+            decoder_backward_into(params, state.dgrads, active, ds.centers, anchors.emb,
+                                  anchors.log_scales, anchors.offsets, view, ds.lod_ref,
+                                  ds.max_scale, dec, gg["means"], gg["opacities"], gg["colors"],
+                                  gg["scales"], gg["quats"], gg["normals"], agrads.emb,
+                                  agrads.log_scales, agrads.offsets)
         if keep is not None:
             keep.append(ViewWork(active, dec, P, Bn, R, gs, gg))
     D.check_status(status, "train_step")
@@ -372,15 +455,21 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         terms = torch.where(cnt > 0, dep_sum / cnt.clamp_min(1), torch.zeros_like(cnt))
         depth = float(terms[have].mean())
         supervised = int(dep_cnt.sum())
-    total = rgb + w2 * depth
+    normal = 0.0
+    if have_n:
+        cnt = nrm_cnt.double()
+        terms = torch.where(cnt > 0, nrm_sum / (3.0 * cnt.clamp_min(1)), torch.zeros_like(cnt))
+        normal = float(terms[have_n].mean())
+    total = rgb + w2 * depth + wn * normal
     if not np.isfinite(total):
         raise NumericalError(f"non-finite loss at step {state.step}: rgb={rgb:.4g} depth={depth:.4g}")
-    state.adam()
+    with _span(timer, "adam"):
+        state.adam()
     report = StepReport(
         step=state.step, total=total, rgb=rgb, depth=depth, geo=0.0, w2=w2, w3=w3,
         lr=cosine_lr(state.step, cfg.lr_decoder, cfg), supervised_depth_px=supervised,
         geo_pairs=0, geo_patches=0, gaussians=gaussians, transfer_bytes=0, imbalance=1.0,
         max_tile_splats=int(tile_max.max()), seconds=time.perf_counter() - t0,
-        intersections=isects)
+        intersections=isects, normal=normal)
     state.step += 1
     return report
