@@ -88,7 +88,8 @@ def teacher_targets(scene, views):
     import torch
     from paper_2503_23044_b200 import device as D
     from paper_2503_23044_b200.trainer import TrainConfig, TrainState
-    teacher = TrainState(scene, TrainConfig(seed=7, total_steps=10))
+    teacher = TrainState(scene, TrainConfig(seed=7, total_steps=10, step2_start=10,
+                                                step3_start=10, growth_stop=0))
     g = torch.Generator(device="cuda").manual_seed(7)
     with torch.no_grad():
         teacher.anchors.emb.add_(torch.randn(teacher.anchors.emb.shape, generator=g,
