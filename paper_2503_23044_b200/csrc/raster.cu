@@ -11,35 +11,21 @@
 // Backward walks each tile back to front from the per-pixel live count,
 // recovering T_k = T_{k+1} / (1 - alpha_k) from the stored final
 // transmittance (the stable direction; see SURVEY.md §7 backward note).
-#include "common.cuh"
+// It is split per chunk of kBC splats into
+//   phase 1 (thread = pixel): the sequential back-to-front recursion, writing
+//            the two per-(pixel, splat) scalars w = alpha*T and
+//            q = dL/d(alpha_unclamped) * exp(power) to shared memory;
+//   phase 2 (warp = splats, lane = pixels): per-splat sums over the tile's 256
+//            pixels in registers, one warp reduction per splat and chunk, and
+//            13 float atomics per (splat, tile) into the per-splat gradient.
+// This replaces a 13-value warp reduction per (splat, warp) — the v1 kernel,
+// kept below for A/B — which made the backward shuffle/atomic bound.
+#include "raster_common.cuh"
 
 namespace vsx {
 
 constexpr int kChunk = 256;
-
-struct PixRay {
-  float rx, ry;
-};
-
-__device__ __forceinline__ PixRay pixel_ray(const vsx_camera &cam, int px, int py) {
-  PixRay r;
-  r.rx = (float)(((double)px - cam.cx) / cam.fx);
-  r.ry = (float)(((double)py - cam.cy) / cam.fy);
-  return r;
-}
-
-__device__ __noinline__ float denom_of(const float *rn, PixRay ray) {
-  return __fadd_rn(__fadd_rn(__fmul_rn(rn[0], ray.rx), __fmul_rn(rn[1], ray.ry)), rn[2]);
-}
-
-// Stage one splat record into shared memory in tile-local float coordinates.
-__device__ __forceinline__ void stage_splat(const vsx_splat &s, double ox, double oy, float4 &p0,
-                                            float4 &p1, float4 &p2, float4 &p3) {
-  p0 = make_float4((float)(s.mean2d[0] - ox), (float)(s.mean2d[1] - oy), s.conic[0], s.conic[1]);
-  p1 = make_float4(s.conic[2], s.opacity, s.plane_d, 0.f);
-  p2 = make_float4(s.color[0], s.color[1], s.color[2], 0.f);
-  p3 = make_float4(s.normal[0], s.normal[1], s.normal[2], 0.f);
-}
+constexpr int kBC = 32;  // backward splat chunk
 
 __global__ void __launch_bounds__(256) raster_fwd_kernel(
     const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
@@ -93,9 +79,8 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
   }
   if (!inside) return;
   const size_t p = (size_t)py * cam.width + px;
-  const float rn[3] = {n0, n1, n2};
   const PixRay ray = pixel_ray(cam, px, py);
-  const float den = denom_of(rn, ray);
+  const float den = denom_of(n0, n1, n2, ray);
   const bool covered = acc >= kAlphaValidMin;
   const bool valid = covered && fabsf(den) >= kDenomGuard;
   if (out_rgb) {
@@ -121,14 +106,135 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
   out_nc[p] = nc;
 }
 
-__global__ void __launch_bounds__(256) raster_bwd_kernel(
-    const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
-    const uint32_t *__restrict__ tile_list, vsx_camera cam, const float *__restrict__ in_alpha,
-    const float *__restrict__ in_depth, const float *__restrict__ in_raw,
-    const float *__restrict__ in_T, const int32_t *__restrict__ in_nc,
-    const float *__restrict__ g_rgb, const float *__restrict__ g_alpha,
-    const float *__restrict__ g_depth, const float *__restrict__ g_normal,
-    const float *__restrict__ g_raw, float *__restrict__ grad) {
+struct BwdArgs {
+  const vsx_splat *rec;
+  const uint32_t *tile_off;
+  const uint32_t *tile_list;
+  const float *alpha, *depth, *raw, *T, *g_rgb, *g_alpha, *g_depth, *g_normal, *g_raw;
+  const int32_t *nc;
+  float *grad;
+};
+
+// ---------------------------------------------------------------- backward v2
+
+__global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera cam) {
+  __shared__ float4 s0[kBC], s1[kBC], s2[kBC], s3[kBC];
+  __shared__ uint32_t s_rank[kBC];
+  extern __shared__ float2 s_wq[];                // (w, q) per (splat, pixel): [kBC][256]
+  __shared__ float4 s_ga[kTilePixels], s_gb[kTilePixels];  // pixel cotangents
+  __shared__ int s_max;
+  const int txn = gridDim.x;
+  const int tile = blockIdx.y * txn + blockIdx.x;
+  const int t = threadIdx.x;
+  const int lx = t & 15, ly = t >> 4;
+  const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
+  const bool inside = px < cam.width && py < cam.height;
+  const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
+  const uint32_t begin = a.tile_off[tile];
+  const float fx = (float)lx, fy = (float)ly;
+  const int lane = t & 31, warp = t >> 5;
+  if (t == 0) s_max = 0;
+  __syncthreads();
+  int nc = 0;
+  float T = 1.f;
+  PixCot c{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (inside) {
+    const size_t p = (size_t)py * cam.width + px;
+    nc = a.nc[p];
+    T = a.T[p];
+    c = pixel_cotangent(cam, px, py, p, a.alpha, a.depth, a.raw, a.g_rgb, a.g_alpha, a.g_depth,
+                        a.g_normal, a.g_raw);
+    if (nc > 0) atomicMax(&s_max, nc);
+  }
+  s_ga[t] = make_float4(c.gA, c.gC0, c.gC1, c.gC2);
+  s_gb[t] = make_float4(c.gR0, c.gR1, c.gR2, c.gD);
+  __syncthreads();
+  const uint32_t stop = begin + (uint32_t)s_max;
+  float S = 0.f;  // sum over later live splats of s_i * w_i
+  for (uint32_t ce = stop; ce > begin;) {
+    const uint32_t cs = ce > begin + kBC ? ce - kBC : begin;
+    const int cnt = (int)(ce - cs);
+    if (t < cnt) {
+      const uint32_t r = a.tile_list[cs + t];
+      s_rank[t] = r;
+      stage_splat(a.rec[r], ox, oy, s0[t], s1[t], s2[t], s3[t]);
+    }
+    __syncthreads();
+    // ---- phase 1: per-pixel back-to-front recursion
+    const int kbase = (int)(cs - begin);
+    for (int j = cnt - 1; j >= 0; --j) {
+      float2 wq = make_float2(0.f, 0.f);
+      if (kbase + j < nc) {
+        const float4 p0 = s0[j], p1 = s1[j], p2 = s2[j], p3 = s3[j];
+        const float dx = fx - p0.x, dy = fy - p0.y;
+        const float power = -0.5f * (p0.z * dx * dx + 2.0f * p0.w * dx * dy + p1.x * dy * dy);
+        const float e = __expf(fminf(power, 0.f));
+        const float at = p1.y * e;
+        const float alpha = fminf(at, kAlphaClamp);
+        const float rom = __frcp_rn(1.f - alpha);
+        const float Tk = T * rom;
+        const float w = alpha * Tk;
+        const float sk = c.gA + c.gC0 * p2.x + c.gC1 * p2.y + c.gC2 * p2.z + c.gR0 * p3.x +
+                         c.gR1 * p3.y + c.gR2 * p3.z + c.gD * p1.z;
+        const float da = Tk * sk - S * rom;
+        S = fmaf(sk, w, S);
+        T = Tk;
+        // power <= 0 for a positive-definite conic; where rounding makes it
+        // slightly positive the clamped branch's zero d/dpower differs from
+        // dat*e*op only by terms of order dx, dy ~ 0 (phase 2 multiplies them).
+        const float dat = at <= kAlphaClamp ? da : 0.f;
+        wq = make_float2(w, dat * e);
+      }
+      s_wq[j * kTilePixels + t] = wq;
+    }
+    __syncthreads();
+    // ---- phase 2: warp w sums splats j = w, w+8, ... over all 256 pixels
+    for (int j = warp; j < cnt; j += 8) {
+      const float4 p0 = s0[j], p1 = s1[j];
+      const float op = p1.y;
+      float g[13];
+#pragma unroll
+      for (int q = 0; q < 13; ++q) g[q] = 0.f;
+#pragma unroll 2
+      for (int i = 0; i < kTilePixels / 32; ++i) {
+        const int pix = lane + 32 * i;
+        const float2 wq = s_wq[j * kTilePixels + pix];
+        if (wq.x == 0.f && wq.y == 0.f) continue;
+        const float4 ga = s_ga[pix], gb = s_gb[pix];
+        const float dx = (float)(pix & 15) - p0.x, dy = (float)(pix >> 4) - p0.y;
+        const float qe = wq.y;        // dL/d(alpha~) * e
+        const float dp = qe * op;     // dL/dpower
+        g[0] = fmaf(dp, p0.z * dx + p0.w * dy, g[0]);
+        g[1] = fmaf(dp, p0.w * dx + p1.x * dy, g[1]);
+        g[2] = fmaf(-0.5f * dp, dx * dx, g[2]);
+        g[3] = fmaf(-dp, dx * dy, g[3]);
+        g[4] = fmaf(-0.5f * dp, dy * dy, g[4]);
+        g[5] += qe;
+        g[6] = fmaf(wq.x, ga.y, g[6]);
+        g[7] = fmaf(wq.x, ga.z, g[7]);
+        g[8] = fmaf(wq.x, ga.w, g[8]);
+        g[9] = fmaf(wq.x, gb.x, g[9]);
+        g[10] = fmaf(wq.x, gb.y, g[10]);
+        g[11] = fmaf(wq.x, gb.z, g[11]);
+        g[12] = fmaf(wq.x, gb.w, g[12]);
+      }
+#pragma unroll
+      for (int q = 0; q < 13; ++q) g[q] = warp_sum(g[q]);
+      if (lane < 13) {
+        float v = g[0];
+#pragma unroll
+        for (int q = 1; q < 13; ++q) v = (lane == q) ? g[q] : v;
+        if (v != 0.f) atomicAdd(a.grad + (size_t)13 * s_rank[j] + lane, v);
+      }
+    }
+    __syncthreads();
+    ce = cs;
+  }
+}
+
+// ---------------------------------------------------------------- backward v1 (A/B)
+
+__global__ void __launch_bounds__(256) raster_bwd_v1_kernel(BwdArgs a, vsx_camera cam) {
   __shared__ float4 s0[kChunk], s1[kChunk], s2[kChunk], s3[kChunk];
   __shared__ uint32_t s_rank[kChunk];
   __shared__ int s_max;
@@ -138,72 +244,33 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
   const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
   const bool inside = px < cam.width && py < cam.height;
   const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
-  const uint32_t begin = tile_off[tile], end = tile_off[tile + 1];
+  const uint32_t begin = a.tile_off[tile];
   const float fx = (float)lx, fy = (float)ly;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) s_max = 0;
   __syncthreads();
-  // ---- per-pixel cotangent of the blended channels (finalize backward)
   int nc = 0;
   float T = 1.f;
-  float gA = 0.f, gC0 = 0.f, gC1 = 0.f, gC2 = 0.f, gR0 = 0.f, gR1 = 0.f, gR2 = 0.f, gD = 0.f;
+  PixCot c{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (inside) {
     const size_t p = (size_t)py * cam.width + px;
-    nc = in_nc[p];
-    T = in_T[p];
-    const float acc = in_alpha[p];
-    const float rn[3] = {in_raw[3 * p + 0], in_raw[3 * p + 1], in_raw[3 * p + 2]};
-    const PixRay ray = pixel_ray(cam, px, py);
-    const float den = denom_of(rn, ray);
-    const bool covered = acc >= kAlphaValidMin;
-    const bool valid = covered && fabsf(den) >= kDenomGuard;
-    if (g_alpha) gA = g_alpha[p];
-    if (g_rgb) {
-      gC0 = g_rgb[3 * p + 0];
-      gC1 = g_rgb[3 * p + 1];
-      gC2 = g_rgb[3 * p + 2];
-    }
-    if (g_depth && valid) {
-      const float gd = g_depth[p];
-      const float depth = in_depth[p];
-      gD = gd / den;
-      const float gden = -gd * depth / den;
-      gR0 += gden * ray.rx;
-      gR1 += gden * ray.ry;
-      gR2 += gden;
-    }
-    if (g_raw) {
-      gR0 += g_raw[3 * p + 0];
-      gR1 += g_raw[3 * p + 1];
-      gR2 += g_raw[3 * p + 2];
-    }
-    if (g_normal && covered) {
-      const float gn0 = g_normal[3 * p + 0], gn1 = g_normal[3 * p + 1], gn2 = g_normal[3 * p + 2];
-      const float len = sqrtf(rn[0] * rn[0] + rn[1] * rn[1] + rn[2] * rn[2]);
-      if (len >= 1e-12f) {
-        const float il = 1.f / len;
-        const float dot = (rn[0] * gn0 + rn[1] * gn1 + rn[2] * gn2) * il * il;
-        gR0 += (gn0 - rn[0] * dot) * il;
-        gR1 += (gn1 - rn[1] * dot) * il;
-        gR2 += (gn2 - rn[2] * dot) * il;
-      } else {
-        gR0 += gn0 * 1e12f;
-        gR1 += gn1 * 1e12f;
-        gR2 += gn2 * 1e12f;
-      }
-    }
+    nc = a.nc[p];
+    T = a.T[p];
+    c = pixel_cotangent(cam, px, py, p, a.alpha, a.depth, a.raw, a.g_rgb, a.g_alpha, a.g_depth,
+                        a.g_normal, a.g_raw);
     atomicMax(&s_max, nc);
   }
   __syncthreads();
   const uint32_t stop = begin + (uint32_t)s_max;
-  float S = 0.f;  // sum over later live splats of s_i * w_i
+  float S = 0.f;
   for (uint32_t ce = stop; ce > begin;) {
     const uint32_t cs = ce > begin + kChunk ? ce - kChunk : begin;
     const uint32_t idx = cs + threadIdx.x;
     if (idx < ce) {
-      const uint32_t r = tile_list[idx];
+      const uint32_t r = a.tile_list[idx];
       s_rank[threadIdx.x] = r;
-      stage_splat(rec[r], ox, oy, s0[threadIdx.x], s1[threadIdx.x], s2[threadIdx.x], s3[threadIdx.x]);
+      stage_splat(a.rec[r], ox, oy, s0[threadIdx.x], s1[threadIdx.x], s2[threadIdx.x],
+                  s3[threadIdx.x]);
     }
     __syncthreads();
     for (int j = (int)(ce - cs) - 1; j >= 0; --j) {
@@ -222,18 +289,18 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
         const float om = 1.f - alpha;
         const float Tk = T / om;
         const float w = alpha * Tk;
-        const float sk = gA + gC0 * p2.x + gC1 * p2.y + gC2 * p2.z + gR0 * p3.x + gR1 * p3.y +
-                         gR2 * p3.z + gD * p1.z;
+        const float sk = c.gA + c.gC0 * p2.x + c.gC1 * p2.y + c.gC2 * p2.z + c.gR0 * p3.x +
+                         c.gR1 * p3.y + c.gR2 * p3.z + c.gD * p1.z;
         const float da = Tk * sk - S / om;
         S = fmaf(sk, w, S);
         T = Tk;
-        g[6] = w * gC0;
-        g[7] = w * gC1;
-        g[8] = w * gC2;
-        g[9] = w * gR0;
-        g[10] = w * gR1;
-        g[11] = w * gR2;
-        g[12] = w * gD;
+        g[6] = w * c.gC0;
+        g[7] = w * c.gC1;
+        g[8] = w * c.gC2;
+        g[9] = w * c.gR0;
+        g[10] = w * c.gR1;
+        g[11] = w * c.gR2;
+        g[12] = w * c.gD;
         const float dat = at <= kAlphaClamp ? da : 0.f;
         g[5] = dat * e;
         const float dp = power <= 0.f ? dat * p1.y * e : 0.f;
@@ -247,7 +314,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(
 #pragma unroll
         for (int q = 0; q < 13; ++q) g[q] = warp_sum(g[q]);
         if (lane == 0) {
-          float *dst = grad + (size_t)13 * s_rank[j];
+          float *dst = a.grad + (size_t)13 * s_rank[j];
 #pragma unroll
           for (int q = 0; q < 13; ++q) atomicAdd(dst + q, g[q]);
         }
@@ -287,10 +354,21 @@ extern "C" int vsx_raster_bwd(const vsx_splat *rec, const uint32_t *tile_offsets
               "raster_bwd: bad args");
   VSX_REQUIRE(!g_depth || depth, "raster_bwd: depth cotangent needs the depth image");
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
-  raster_bwd_kernel<<<grid, 256, 0, as_stream(s)>>>(rec, tile_offsets, tile_list, cam, alpha,
-                                                    depth, raw_normal, t_final, n_contrib, g_rgb,
-                                                    g_alpha, g_depth, g_normal, g_raw_normal,
-                                                    grad_splat);
+  BwdArgs a{rec, tile_offsets, tile_list, alpha, depth, raw_normal, t_final, g_rgb, g_alpha,
+            g_depth, g_normal, g_raw_normal, n_contrib, grad_splat};
+  static const bool v1 = getenv("VSX_RASTER_BWD_V1") != nullptr;
+  if (v1) {
+    raster_bwd_v1_kernel<<<grid, 256, 0, as_stream(s)>>>(a, cam);
+  } else {
+    const int smem = (int)(sizeof(float2) * kBC * kTilePixels);
+    static bool attr = false;
+    if (!attr) {
+      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    raster_bwd_kernel<<<grid, 256, smem, as_stream(s)>>>(a, cam);
+  }
   VSX_LAUNCH_CHECK("raster_bwd");
   return VSX_OK;
 }

@@ -1,0 +1,94 @@
+// Shared pieces of the compositing forward (K5) and backward (K6) kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace vsx {
+
+struct PixRay {
+  float rx, ry;
+};
+
+// ((u - cx)/fx, (v - cy)/fy) of an integer pixel centre (renderer.py:274-275).
+__device__ __forceinline__ PixRay pixel_ray(const vsx_camera &cam, int px, int py) {
+  PixRay r;
+  r.rx = (float)(((double)px - cam.cx) / cam.fx);
+  r.ry = (float)(((double)py - cam.cy) / cam.fy);
+  return r;
+}
+
+// Depth-quotient denominator raw_normal . ray, identically rounded in the
+// forward and the backward (no FMA contraction) so validity decisions agree.
+__device__ __forceinline__ float denom_of(float n0, float n1, float n2, PixRay ray) {
+  return __fadd_rn(__fadd_rn(__fmul_rn(n0, ray.rx), __fmul_rn(n1, ray.ry)), n2);
+}
+
+// One splat record in tile-local float coordinates: p0 = (mx, my, A, B),
+// p1 = (C, opacity, plane_d, -), p2 = color, p3 = camera normal.
+__device__ __forceinline__ void stage_splat(const vsx_splat &s, double ox, double oy, float4 &p0,
+                                            float4 &p1, float4 &p2, float4 &p3) {
+  p0 = make_float4((float)(s.mean2d[0] - ox), (float)(s.mean2d[1] - oy), s.conic[0], s.conic[1]);
+  p1 = make_float4(s.conic[2], s.opacity, s.plane_d, 0.f);
+  p2 = make_float4(s.color[0], s.color[1], s.color[2], 0.f);
+  p3 = make_float4(s.normal[0], s.normal[1], s.normal[2], 0.f);
+}
+
+// Cotangent of the 8 blended channels of one pixel (finalize backward,
+// renderer.py:282-301): alpha, rgb, raw normal (incl. depth-quotient and
+// normal-renormalisation terms) and the plane-offset sum.
+struct PixCot {
+  float gA, gC0, gC1, gC2, gR0, gR1, gR2, gD;
+};
+
+__device__ __forceinline__ PixCot pixel_cotangent(
+    const vsx_camera &cam, int px, int py, size_t p, const float *__restrict__ in_alpha,
+    const float *__restrict__ in_depth, const float *__restrict__ in_raw,
+    const float *__restrict__ g_rgb, const float *__restrict__ g_alpha,
+    const float *__restrict__ g_depth, const float *__restrict__ g_normal,
+    const float *__restrict__ g_raw) {
+  PixCot c{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const float acc = in_alpha[p];
+  const float n0 = in_raw[3 * p + 0], n1 = in_raw[3 * p + 1], n2 = in_raw[3 * p + 2];
+  const PixRay ray = pixel_ray(cam, px, py);
+  const float den = denom_of(n0, n1, n2, ray);
+  const bool covered = acc >= kAlphaValidMin;
+  const bool valid = covered && fabsf(den) >= kDenomGuard;
+  if (g_alpha) c.gA = g_alpha[p];
+  if (g_rgb) {
+    c.gC0 = g_rgb[3 * p + 0];
+    c.gC1 = g_rgb[3 * p + 1];
+    c.gC2 = g_rgb[3 * p + 2];
+  }
+  if (g_depth && valid) {
+    const float gd = g_depth[p];
+    const float depth = in_depth[p];
+    c.gD = gd / den;
+    const float gden = -gd * depth / den;
+    c.gR0 += gden * ray.rx;
+    c.gR1 += gden * ray.ry;
+    c.gR2 += gden;
+  }
+  if (g_raw) {
+    c.gR0 += g_raw[3 * p + 0];
+    c.gR1 += g_raw[3 * p + 1];
+    c.gR2 += g_raw[3 * p + 2];
+  }
+  if (g_normal && covered) {
+    const float gn0 = g_normal[3 * p + 0], gn1 = g_normal[3 * p + 1], gn2 = g_normal[3 * p + 2];
+    const float len = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
+    if (len >= 1e-12f) {
+      const float il = 1.f / len;
+      const float dot = (n0 * gn0 + n1 * gn1 + n2 * gn2) * il * il;
+      c.gR0 += (gn0 - n0 * dot) * il;
+      c.gR1 += (gn1 - n1 * dot) * il;
+      c.gR2 += (gn2 - n2 * dot) * il;
+    } else {
+      c.gR0 += gn0 * 1e12f;
+      c.gR1 += gn1 * 1e12f;
+      c.gR2 += gn2 * 1e12f;
+    }
+  }
+  return c;
+}
+
+}  // namespace vsx
