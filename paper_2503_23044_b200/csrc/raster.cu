@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
       const float4 p0 = s0[j], p1 = s1[j];
       const float dx = fx - p0.x, dy = fy - p0.y;
       const float power = -0.5f * (p0.z * dx * dx + 2.0f * p0.w * dx * dy + p1.x * dy * dy);
+      nc = (int32_t)(cs - begin) + j + 1;
       const float alpha = fminf(p1.y * __expf(fminf(power, 0.f)), kAlphaClamp);
       const float w = alpha * T;
       const float4 p2 = s2[j], p3 = s3[j];
@@ -74,7 +75,6 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
       n2 = fmaf(w, p3.z, n2);
       dist = fmaf(w, p1.z, dist);
       T = T * (1.f - alpha);
-      nc = (int32_t)(cs - begin) + j + 1;
     }
   }
   if (!inside) return;
@@ -117,6 +117,7 @@ struct BwdArgs {
 
 // ---------------------------------------------------------------- backward v2
 
+template <int NS>
 __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera cam) {
   __shared__ float4 s0[kBC], s1[kBC], s2[kBC], s3[kBC];
   __shared__ uint32_t s_rank[kBC];
@@ -164,10 +165,11 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera c
     const int kbase = (int)(cs - begin);
     for (int j = cnt - 1; j >= 0; --j) {
       float2 wq = make_float2(0.f, 0.f);
+      const float4 p0 = s0[j], p1 = s1[j];
+      const float dx = fx - p0.x, dy = fy - p0.y;
+      const float power = -0.5f * (p0.z * dx * dx + 2.0f * p0.w * dx * dy + p1.x * dy * dy);
       if (kbase + j < nc) {
-        const float4 p0 = s0[j], p1 = s1[j], p2 = s2[j], p3 = s3[j];
-        const float dx = fx - p0.x, dy = fy - p0.y;
-        const float power = -0.5f * (p0.z * dx * dx + 2.0f * p0.w * dx * dy + p1.x * dy * dy);
+        const float4 p2 = s2[j], p3 = s3[j];
         const float e = __expf(fminf(power, 0.f));
         const float at = p1.y * e;
         const float alpha = fminf(at, kAlphaClamp);
@@ -188,43 +190,73 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera c
       s_wq[j * kTilePixels + t] = wq;
     }
     __syncthreads();
-    // ---- phase 2: warp w sums splats j = w, w+8, ... over all 256 pixels
-    for (int j = warp; j < cnt; j += 8) {
-      const float4 p0 = s0[j], p1 = s1[j];
-      const float op = p1.y;
-      float g[13];
+    // ---- phase 2: warp w owns splats j = w + 8s (s < 4); lanes stride the 256
+    // pixels. Per splat it accumulates 7 colour/normal/plane sums sum_p w*G(p)
+    // and 6 pixel moments of q about the tile centre (1, x, y, x^2, xy, y^2);
+    // the conic/mean/opacity gradients are polynomials of those moments.
+    for (int jb = warp; jb < cnt; jb += 8 * NS) {
+      float acc[NS][13];
 #pragma unroll
-      for (int q = 0; q < 13; ++q) g[q] = 0.f;
-#pragma unroll 2
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int q = 0; q < 13; ++q) acc[s][q] = 0.f;
+#pragma unroll 1
       for (int i = 0; i < kTilePixels / 32; ++i) {
         const int pix = lane + 32 * i;
-        const float2 wq = s_wq[j * kTilePixels + pix];
-        if (wq.x == 0.f && wq.y == 0.f) continue;
         const float4 ga = s_ga[pix], gb = s_gb[pix];
-        const float dx = (float)(pix & 15) - p0.x, dy = (float)(pix >> 4) - p0.y;
-        const float qe = wq.y;        // dL/d(alpha~) * e
-        const float dp = qe * op;     // dL/dpower
-        g[0] = fmaf(dp, p0.z * dx + p0.w * dy, g[0]);
-        g[1] = fmaf(dp, p0.w * dx + p1.x * dy, g[1]);
-        g[2] = fmaf(-0.5f * dp, dx * dx, g[2]);
-        g[3] = fmaf(-dp, dx * dy, g[3]);
-        g[4] = fmaf(-0.5f * dp, dy * dy, g[4]);
-        g[5] += qe;
-        g[6] = fmaf(wq.x, ga.y, g[6]);
-        g[7] = fmaf(wq.x, ga.z, g[7]);
-        g[8] = fmaf(wq.x, ga.w, g[8]);
-        g[9] = fmaf(wq.x, gb.x, g[9]);
-        g[10] = fmaf(wq.x, gb.y, g[10]);
-        g[11] = fmaf(wq.x, gb.z, g[11]);
-        g[12] = fmaf(wq.x, gb.w, g[12]);
+        const float xc = (float)(pix & 15) - 7.5f, yc = (float)(pix >> 4) - 7.5f;
+        const float xx = xc * xc, xy = xc * yc, yy = yc * yc;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const int j = jb + 8 * s;
+          if (j < cnt) {
+            const float2 wq = s_wq[j * kTilePixels + pix];
+            acc[s][0] = fmaf(wq.x, ga.y, acc[s][0]);
+            acc[s][1] = fmaf(wq.x, ga.z, acc[s][1]);
+            acc[s][2] = fmaf(wq.x, ga.w, acc[s][2]);
+            acc[s][3] = fmaf(wq.x, gb.x, acc[s][3]);
+            acc[s][4] = fmaf(wq.x, gb.y, acc[s][4]);
+            acc[s][5] = fmaf(wq.x, gb.z, acc[s][5]);
+            acc[s][6] = fmaf(wq.x, gb.w, acc[s][6]);
+            acc[s][7] += wq.y;
+            acc[s][8] = fmaf(wq.y, xc, acc[s][8]);
+            acc[s][9] = fmaf(wq.y, yc, acc[s][9]);
+            acc[s][10] = fmaf(wq.y, xx, acc[s][10]);
+            acc[s][11] = fmaf(wq.y, xy, acc[s][11]);
+            acc[s][12] = fmaf(wq.y, yy, acc[s][12]);
+          }
+        }
       }
 #pragma unroll
-      for (int q = 0; q < 13; ++q) g[q] = warp_sum(g[q]);
-      if (lane < 13) {
-        float v = g[0];
+      for (int s = 0; s < NS; ++s) {
+        const int j = jb + 8 * s;
+        if (j >= cnt) break;  // warp-uniform
 #pragma unroll
-        for (int q = 1; q < 13; ++q) v = (lane == q) ? g[q] : v;
-        if (v != 0.f) atomicAdd(a.grad + (size_t)13 * s_rank[j] + lane, v);
+        for (int q = 0; q < 13; ++q) acc[s][q] = warp_sum(acc[s][q]);
+        const float4 p0 = s0[j], p1 = s1[j];
+        const float op = p1.y, A = p0.z, B = p0.w, C = p1.x;
+        const float mx = p0.x - 7.5f, my = p0.y - 7.5f;
+        const float Q1 = acc[s][7];
+        const float sx = acc[s][8] - mx * Q1;                 // sum q dx
+        const float sy = acc[s][9] - my * Q1;                 // sum q dy
+        const float sxx = acc[s][10] - 2.f * mx * acc[s][8] + mx * mx * Q1;
+        const float sxy = acc[s][11] - mx * acc[s][9] - my * acc[s][8] + mx * my * Q1;
+        const float syy = acc[s][12] - 2.f * my * acc[s][9] + my * my * Q1;
+        float g[13];
+        g[0] = op * (A * sx + B * sy);
+        g[1] = op * (B * sx + C * sy);
+        g[2] = -0.5f * op * sxx;
+        g[3] = -op * sxy;
+        g[4] = -0.5f * op * syy;
+        g[5] = Q1;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) g[6 + q] = acc[s][q];
+        if (lane < 13) {
+          float v = g[0];
+#pragma unroll
+          for (int q = 1; q < 13; ++q) v = (lane == q) ? g[q] : v;
+          if (v != 0.f) atomicAdd(a.grad + (size_t)13 * s_rank[j] + lane, v);
+        }
       }
     }
     __syncthreads();
@@ -356,18 +388,31 @@ extern "C" int vsx_raster_bwd(const vsx_splat *rec, const uint32_t *tile_offsets
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
   BwdArgs a{rec, tile_offsets, tile_list, alpha, depth, raw_normal, t_final, g_rgb, g_alpha,
             g_depth, g_normal, g_raw_normal, n_contrib, grad_splat};
-  static const bool v1 = getenv("VSX_RASTER_BWD_V1") != nullptr;
-  if (v1) {
+  // VSX_RASTER_BWD selects an implementation for A/B timing: "v1" (per-warp
+  // reductions) or the two-phase kernel with 1/2/4 splats per phase-2 pass.
+  static const char *sel = getenv("VSX_RASTER_BWD");
+  static const int ns = sel ? atoi(sel) : 2;
+  if (sel && sel[0] == 'v') {
     raster_bwd_v1_kernel<<<grid, 256, 0, as_stream(s)>>>(a, cam);
   } else {
     const int smem = (int)(sizeof(float2) * kBC * kTilePixels);
     static bool attr = false;
     if (!attr) {
-      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel,
+      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<1>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<4>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr = true;
     }
-    raster_bwd_kernel<<<grid, 256, smem, as_stream(s)>>>(a, cam);
+    if (ns == 4) {
+      raster_bwd_kernel<4><<<grid, 256, smem, as_stream(s)>>>(a, cam);
+    } else if (ns == 1) {
+      raster_bwd_kernel<1><<<grid, 256, smem, as_stream(s)>>>(a, cam);
+    } else {
+      raster_bwd_kernel<2><<<grid, 256, smem, as_stream(s)>>>(a, cam);
+    }
   }
   VSX_LAUNCH_CHECK("raster_bwd");
   return VSX_OK;
