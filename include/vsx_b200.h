@@ -100,13 +100,15 @@ size_t vsx_scan_ws_bytes(int64_t n);
 int vsx_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, void *ws, size_t ws_bytes,
                  vsx_stream s);
 /* Stable LSD radix sort of (key, value) pairs on key bits [begin_bit, end_bit).
- * Bytes whose value is identical for all keys are skipped (one host sync). */
+ * flags & VSX_SORT_SKIP_CONSTANT: first reduce OR/AND of the keys and skip
+ * 8-bit digits that are identical for every key (costs one host sync). */
+#define VSX_SORT_SKIP_CONSTANT 1
 int vsx_sort_pairs_u64(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
                        uint32_t *vals_out, int64_t n, int32_t begin_bit, int32_t end_bit,
-                       void *ws, size_t ws_bytes, vsx_stream s);
+                       int32_t flags, void *ws, size_t ws_bytes, vsx_stream s);
 int vsx_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                        uint32_t *vals_out, int64_t n, int32_t begin_bit, int32_t end_bit,
-                       void *ws, size_t ws_bytes, vsx_stream s);
+                       int32_t flags, void *ws, size_t ws_bytes, vsx_stream s);
 /* Ordered stream compaction: out_idx = flatnonzero(flags), *out_count on device. */
 int vsx_select(const uint8_t *flags, int64_t n, int32_t *out_idx, uint32_t *out_count,
                void *ws, size_t ws_bytes, vsx_stream s);
@@ -142,13 +144,19 @@ int vsx_gather_splats(const vsx_splat *rec, const double *radius, const uint32_t
                       int32_t n, vsx_splat *rec_sorted, double *radius_sorted, vsx_stream s);
 
 /* ---- K4: tile binning (renderer.py:207-226) --------------------------- */
-/* Phase 1: per-splat tile counts + per-tile histogram. */
+/* Phase 1: per-splat tile counts (+ per-tile histogram when tile_counts is
+ * not NULL; the training path derives tile ranges from the sorted keys
+ * instead and passes NULL). */
 int vsx_bin_count(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
                   int32_t height, uint32_t *splat_tiles, uint32_t *tile_counts, vsx_stream s);
 /* Phase 2: emit (tile, rank) pairs at exclusive-scan offsets of splat_tiles. */
 int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
                  int32_t height, const uint32_t *splat_offsets, uint32_t *isect_tile,
                  uint32_t *isect_rank, vsx_stream s);
+/* Phase 3: CSR tile offsets (num_tiles+1) from the tile-sorted keys
+ * (lower_bound per tile; no atomics). */
+int vsx_tile_ranges(const uint32_t *sorted_tiles, int64_t n, int32_t num_tiles,
+                    uint32_t *tile_offsets, vsx_stream s);
 
 /* ---- K5: compositing forward (renderer.py:242-301, 390-449) ----------- */
 /* tile_offsets (T+1) CSR over tile_list (sorted ranks). Outputs are HWC

@@ -182,15 +182,28 @@ __global__ void rs_hist_kernel(const K *__restrict__ keys, int64_t n, int shift,
 
 // Stable scatter: within a block, keys are ranked in input order (round-major,
 // then thread); across blocks the digit-major scanned histogram keeps block
-// order, so equal digits never reorder.
+// order, so equal digits never reorder. Keys are first placed digit-grouped
+// in shared memory, then written out so that consecutive threads store
+// consecutive addresses of each digit bucket (coalesced stores).
 template <typename K>
-__global__ void rs_scatter_kernel(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
-                                  K *__restrict__ kout, uint32_t *__restrict__ vout, int64_t n,
-                                  int shift, const uint32_t *__restrict__ offs) {
+__global__ void __launch_bounds__(kRsBlock) rs_scatter_kernel(
+    const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
+    uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ offs,
+    const uint32_t *__restrict__ hist) {
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  K *sk = reinterpret_cast<K *>(rs_smem);
+  uint32_t *sv = reinterpret_cast<uint32_t *>(sk + kRsTile);
   __shared__ uint32_t run[256];
+  __shared__ uint32_t lstart[256];
+  __shared__ uint32_t gbase[256];
   __shared__ uint32_t wcnt[kRsWarps][256];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  run[t] = offs[(int64_t)t * gridDim.x + blockIdx.x];
+  const int64_t cell = (int64_t)t * gridDim.x + blockIdx.x;
+  gbase[t] = offs[cell];
+  uint32_t tot = 0;
+  const uint32_t ls = block_exclusive_scan(hist[cell], tot);
+  lstart[t] = ls;
+  run[t] = ls;
   const unsigned lt = (1u << lane) - 1u;
   const int64_t base = (int64_t)blockIdx.x * kRsTile;
   for (int r = 0; r < kRsRounds; ++r) {
@@ -217,11 +230,19 @@ __global__ void rs_scatter_kernel(const K *__restrict__ kin, const uint32_t *__r
     run[t] = acc;
     __syncthreads();
     if (ok) {
-      const uint32_t pos = wcnt[warp][d] + lrank;
-      kout[pos] = k;
-      vout[pos] = v;
+      const uint32_t pos = wcnt[warp][d] + lrank;  // block-local, digit-grouped
+      sk[pos] = k;
+      sv[pos] = v;
     }
     __syncthreads();
+  }
+  const int nvalid = (int)min((int64_t)kRsTile, n - base);
+  for (int s = t; s < nvalid; s += kRsBlock) {
+    const K k = sk[s];
+    const uint32_t d = (uint32_t)(k >> shift) & 255u;
+    const uint32_t pos = gbase[d] + (uint32_t)s - lstart[d];
+    kout[pos] = k;
+    vout[pos] = sv[s];
   }
 }
 
@@ -265,7 +286,8 @@ static SortWs carve_sort_ws(void *ws, int64_t n) {
 
 template <typename K>
 static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout, int64_t n,
-                      int begin_bit, int end_bit, void *ws, size_t ws_bytes, cudaStream_t st) {
+                      int begin_bit, int end_bit, int flags, void *ws, size_t ws_bytes,
+                      cudaStream_t st) {
   VSX_REQUIRE(n >= 0 && n < (int64_t)1 << 32, "sort: bad n %lld", (long long)n);
   VSX_REQUIRE(begin_bit >= 0 && end_bit <= (int)(8 * sizeof(K)) && begin_bit <= end_bit,
               "sort: bad bit range");
@@ -273,14 +295,28 @@ static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout
   VSX_REQUIRE(ws_bytes >= sort_ws_bytes(n), "sort: workspace %zu < %zu", ws_bytes,
               sort_ws_bytes(n));
   SortWs w = carve_sort_ws(ws, n);
-  // Which digit bytes actually vary? (one tiny D2H read)
-  rs_init_or_and<<<1, 1, 0, st>>>(w.or_and);
-  rs_minmax_kernel<K><<<std::min(grid_for(n, 256), 1184), 256, 0, st>>>(kin, n, w.or_and);
-  VSX_LAUNCH_CHECK("rs_minmax");
-  unsigned long long oa[2];
-  VSX_CUDA_TRY(cudaMemcpyAsync(oa, w.or_and, sizeof(oa), cudaMemcpyDeviceToHost, st));
-  VSX_CUDA_TRY(cudaStreamSynchronize(st));
-  const unsigned long long varying = oa[0] ^ oa[1];
+  static bool attr = false;
+  const int smem = (int)((sizeof(K) + sizeof(uint32_t)) * kRsTile);
+  if (!attr) {
+    VSX_CUDA_TRY(cudaFuncSetAttribute(rs_scatter_kernel<uint64_t>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(12 * kRsTile)));
+    VSX_CUDA_TRY(cudaFuncSetAttribute(rs_scatter_kernel<uint32_t>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(8 * kRsTile)));
+    attr = true;
+  }
+  unsigned long long varying = ~0ull;
+  if (flags & VSX_SORT_SKIP_CONSTANT) {
+    // Which digit bytes actually vary? (one tiny D2H read)
+    rs_init_or_and<<<1, 1, 0, st>>>(w.or_and);
+    rs_minmax_kernel<K><<<std::min(grid_for(n, 256), 1184), 256, 0, st>>>(kin, n, w.or_and);
+    VSX_LAUNCH_CHECK("rs_minmax");
+    unsigned long long oa[2];
+    VSX_CUDA_TRY(cudaMemcpyAsync(oa, w.or_and, sizeof(oa), cudaMemcpyDeviceToHost, st));
+    VSX_CUDA_TRY(cudaStreamSynchronize(st));
+    varying = oa[0] ^ oa[1];
+  }
   int shifts[16];
   int np = 0;
   for (int sh = begin_bit - (begin_bit % 8); sh < end_bit; sh += 8) {
@@ -305,7 +341,8 @@ static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout
     VSX_LAUNCH_CHECK("rs_hist");
     int rc = scan_impl(w.hist, w.hist_scan, nh, w.scan_ws, st);
     if (rc) return rc;
-    rs_scatter_kernel<K><<<nb, kRsBlock, 0, st>>>(src_k, src_v, dk, dv, n, shifts[p], w.hist_scan);
+    rs_scatter_kernel<K><<<nb, kRsBlock, smem, st>>>(src_k, src_v, dk, dv, n, shifts[p],
+                                                    w.hist_scan, w.hist);
     VSX_LAUNCH_CHECK("rs_scatter");
     src_k = dk;
     src_v = dv;
@@ -363,16 +400,16 @@ extern "C" int vsx_select(const uint8_t *flags, int64_t n, int32_t *out_idx,
 
 extern "C" int vsx_sort_pairs_u64(const uint64_t *keys_in, const uint32_t *vals_in,
                                   uint64_t *keys_out, uint32_t *vals_out, int64_t n,
-                                  int32_t begin_bit, int32_t end_bit, void *ws, size_t ws_bytes,
-                                  vsx_stream s) {
-  return sort_pairs<uint64_t>(keys_in, vals_in, keys_out, vals_out, n, begin_bit, end_bit, ws,
-                              ws_bytes, as_stream(s));
+                                  int32_t begin_bit, int32_t end_bit, int32_t flags, void *ws,
+                                  size_t ws_bytes, vsx_stream s) {
+  return sort_pairs<uint64_t>(keys_in, vals_in, keys_out, vals_out, n, begin_bit, end_bit, flags,
+                              ws, ws_bytes, as_stream(s));
 }
 
 extern "C" int vsx_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_in,
                                   uint32_t *keys_out, uint32_t *vals_out, int64_t n,
-                                  int32_t begin_bit, int32_t end_bit, void *ws, size_t ws_bytes,
-                                  vsx_stream s) {
-  return sort_pairs<uint32_t>(keys_in, vals_in, keys_out, vals_out, n, begin_bit, end_bit, ws,
-                              ws_bytes, as_stream(s));
+                                  int32_t begin_bit, int32_t end_bit, int32_t flags, void *ws,
+                                  size_t ws_bytes, vsx_stream s) {
+  return sort_pairs<uint32_t>(keys_in, vals_in, keys_out, vals_out, n, begin_bit, end_bit, flags,
+                              ws, ws_bytes, as_stream(s));
 }

@@ -152,10 +152,25 @@ __global__ void bin_count_kernel(const vsx_splat *__restrict__ rec,
   uint32_t cnt = 0;
   if (tile_rect(rec[i].mean2d[0], rec[i].mean2d[1], radius[i], txn, tyn, x0, x1, y0, y1)) {
     cnt = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
-    for (int ty = y0; ty <= y1; ++ty)
-      for (int tx = x0; tx <= x1; ++tx) atomicAdd(tile_counts + ty * txn + tx, 1u);
+    if (tile_counts)
+      for (int ty = y0; ty <= y1; ++ty)
+        for (int tx = x0; tx <= x1; ++tx) atomicAdd(tile_counts + ty * txn + tx, 1u);
   }
   splat_tiles[i] = cnt;
+}
+
+// tile_off[t] = lower_bound(sorted_tiles, t), tile_off[T] = n.
+__global__ void tile_ranges_kernel(const uint32_t *__restrict__ keys, int64_t n, int T,
+                                   uint32_t *__restrict__ tile_off) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > T) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < (uint32_t)t) lo = mid + 1;
+    else hi = mid;
+  }
+  tile_off[t] = (uint32_t)(t == T ? n : lo);
 }
 
 __global__ void bin_emit_kernel(const vsx_splat *__restrict__ rec,
@@ -327,7 +342,7 @@ extern "C" int vsx_bin_count(const vsx_splat *rec, const double *radius, int32_t
   VSX_REQUIRE(width > 0 && height > 0 && n >= 0, "bin_count: bad arguments");
   const int txn = (width + kTile - 1) / kTile, tyn = (height + kTile - 1) / kTile;
   cudaStream_t st = as_stream(s);
-  VSX_CUDA_TRY(cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * txn * tyn, st));
+  if (tile_counts) VSX_CUDA_TRY(cudaMemsetAsync(tile_counts, 0, sizeof(uint32_t) * txn * tyn, st));
   if (n == 0) return VSX_OK;
   bin_count_kernel<<<grid_for(n, 256), 256, 0, st>>>(rec, radius, n, txn, tyn, splat_tiles,
                                                      tile_counts);
@@ -345,6 +360,15 @@ extern "C" int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t 
                                                               splat_offsets, isect_tile,
                                                               isect_rank);
   VSX_LAUNCH_CHECK("bin_emit");
+  return VSX_OK;
+}
+
+extern "C" int vsx_tile_ranges(const uint32_t *sorted_tiles, int64_t n, int32_t num_tiles,
+                               uint32_t *tile_offsets, vsx_stream s) {
+  VSX_REQUIRE(n >= 0 && num_tiles >= 1, "tile_ranges: bad args");
+  tile_ranges_kernel<<<grid_for(num_tiles + 1, 256), 256, 0, as_stream(s)>>>(
+      sorted_tiles, n, num_tiles, tile_offsets);
+  VSX_LAUNCH_CHECK("tile_ranges");
   return VSX_OK;
 }
 

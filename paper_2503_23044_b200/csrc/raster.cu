@@ -18,8 +18,8 @@
 //   phase 2 (warp = splats, lane = pixels): per-splat sums over the tile's 256
 //            pixels in registers, one warp reduction per splat and chunk, and
 //            13 float atomics per (splat, tile) into the per-splat gradient.
-// This replaces a 13-value warp reduction per (splat, warp) — the v1 kernel,
-// kept below for A/B — which made the backward shuffle/atomic bound.
+// This replaces a 13-value warp reduction per (splat, warp) (round-1 v1, see
+// profiles/r01_raster_bwd_v1_ncu.txt), which made the backward LSU-bound.
 #include "raster_common.cuh"
 
 namespace vsx {
@@ -54,27 +54,28 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
     }
     __syncthreads();
     const int cnt = (int)min((uint32_t)kChunk, end - cs);
-    for (int j = 0; j < cnt && !done; ++j) {
-      if (T < kEarlyStopT) {
-        done = true;
-        break;
+    if (!done) {
+      int j = 0;
+#pragma unroll 4
+      for (; j < cnt; ++j) {
+        if (T < kEarlyStopT) break;  // T_prev < 1e-4: this and every later splat is dead
+        const float4 p0 = s0[j], p1 = s1[j];
+        float e, at;
+        const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
+        const float w = alpha * T;
+        const float4 p2 = s2[j], p3 = s3[j];
+        acc += w;
+        c0 = fmaf(w, p2.x, c0);
+        c1 = fmaf(w, p2.y, c1);
+        c2 = fmaf(w, p2.z, c2);
+        n0 = fmaf(w, p3.x, n0);
+        n1 = fmaf(w, p3.y, n1);
+        n2 = fmaf(w, p3.z, n2);
+        dist = fmaf(w, p1.z, dist);
+        T = __fmaf_rn(-alpha, T, T);
       }
-      const float4 p0 = s0[j], p1 = s1[j];
-      const float dx = fx - p0.x, dy = fy - p0.y;
-      const float power = -0.5f * (p0.z * dx * dx + 2.0f * p0.w * dx * dy + p1.x * dy * dy);
-      nc = (int32_t)(cs - begin) + j + 1;
-      const float alpha = fminf(p1.y * __expf(fminf(power, 0.f)), kAlphaClamp);
-      const float w = alpha * T;
-      const float4 p2 = s2[j], p3 = s3[j];
-      acc += w;
-      c0 = fmaf(w, p2.x, c0);
-      c1 = fmaf(w, p2.y, c1);
-      c2 = fmaf(w, p2.z, c2);
-      n0 = fmaf(w, p3.x, n0);
-      n1 = fmaf(w, p3.y, n1);
-      n2 = fmaf(w, p3.z, n2);
-      dist = fmaf(w, p1.z, dist);
-      T = T * (1.f - alpha);
+      nc = (int32_t)(cs - begin) + j;
+      done = j < cnt;
     }
   }
   if (!inside) return;
@@ -163,16 +164,17 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera c
     __syncthreads();
     // ---- phase 1: per-pixel back-to-front recursion
     const int kbase = (int)(cs - begin);
-    for (int j = cnt - 1; j >= 0; --j) {
-      float2 wq = make_float2(0.f, 0.f);
-      const float4 p0 = s0[j], p1 = s1[j];
-      const float dx = fx - p0.x, dy = fy - p0.y;
-      const float power = -0.5f * (p0.z * dx * dx + 2.0f * p0.w * dx * dy + p1.x * dy * dy);
-      if (kbase + j < nc) {
+    // live splats of this pixel in the chunk are j < nc - kbase
+    const int jlive = min(cnt, nc - kbase);
+    for (int j = cnt - 1; j >= max(jlive, 0); --j) s_wq[j * kTilePixels + t] = make_float2(0.f, 0.f);
+#pragma unroll 2
+    for (int j = jlive - 1; j >= 0; --j) {
+      float2 wq;
+      {
+        const float4 p0 = s0[j], p1 = s1[j];
         const float4 p2 = s2[j], p3 = s3[j];
-        const float e = __expf(fminf(power, 0.f));
-        const float at = p1.y * e;
-        const float alpha = fminf(at, kAlphaClamp);
+        float e, at;
+        const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
         const float rom = __frcp_rn(1.f - alpha);
         const float Tk = T * rom;
         const float w = alpha * Tk;
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera c
 #pragma unroll
         for (int q = 0; q < 13; ++q) acc[s][q] = warp_sum(acc[s][q]);
         const float4 p0 = s0[j], p1 = s1[j];
-        const float op = p1.y, A = p0.z, B = p0.w, C = p1.x;
+        const float op = p1.y, A = p1.w, B = s2[j].w, C = s3[j].w;
         const float mx = p0.x - 7.5f, my = p0.y - 7.5f;
         const float Q1 = acc[s][7];
         const float sx = acc[s][8] - mx * Q1;                 // sum q dx
@@ -256,99 +258,6 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera c
 #pragma unroll
           for (int q = 1; q < 13; ++q) v = (lane == q) ? g[q] : v;
           if (v != 0.f) atomicAdd(a.grad + (size_t)13 * s_rank[j] + lane, v);
-        }
-      }
-    }
-    __syncthreads();
-    ce = cs;
-  }
-}
-
-// ---------------------------------------------------------------- backward v1 (A/B)
-
-__global__ void __launch_bounds__(256) raster_bwd_v1_kernel(BwdArgs a, vsx_camera cam) {
-  __shared__ float4 s0[kChunk], s1[kChunk], s2[kChunk], s3[kChunk];
-  __shared__ uint32_t s_rank[kChunk];
-  __shared__ int s_max;
-  const int txn = gridDim.x;
-  const int tile = blockIdx.y * txn + blockIdx.x;
-  const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
-  const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
-  const bool inside = px < cam.width && py < cam.height;
-  const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
-  const uint32_t begin = a.tile_off[tile];
-  const float fx = (float)lx, fy = (float)ly;
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) s_max = 0;
-  __syncthreads();
-  int nc = 0;
-  float T = 1.f;
-  PixCot c{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  if (inside) {
-    const size_t p = (size_t)py * cam.width + px;
-    nc = a.nc[p];
-    T = a.T[p];
-    c = pixel_cotangent(cam, px, py, p, a.alpha, a.depth, a.raw, a.g_rgb, a.g_alpha, a.g_depth,
-                        a.g_normal, a.g_raw);
-    atomicMax(&s_max, nc);
-  }
-  __syncthreads();
-  const uint32_t stop = begin + (uint32_t)s_max;
-  float S = 0.f;
-  for (uint32_t ce = stop; ce > begin;) {
-    const uint32_t cs = ce > begin + kChunk ? ce - kChunk : begin;
-    const uint32_t idx = cs + threadIdx.x;
-    if (idx < ce) {
-      const uint32_t r = a.tile_list[idx];
-      s_rank[threadIdx.x] = r;
-      stage_splat(a.rec[r], ox, oy, s0[threadIdx.x], s1[threadIdx.x], s2[threadIdx.x],
-                  s3[threadIdx.x]);
-    }
-    __syncthreads();
-    for (int j = (int)(ce - cs) - 1; j >= 0; --j) {
-      const int k = (int)(cs - begin) + j;
-      const bool live = k < nc;
-      float g[13];
-#pragma unroll
-      for (int q = 0; q < 13; ++q) g[q] = 0.f;
-      if (live) {
-        const float4 p0 = s0[j], p1 = s1[j], p2 = s2[j], p3 = s3[j];
-        const float dx = fx - p0.x, dy = fy - p0.y;
-        const float power = -0.5f * (p0.z * dx * dx + 2.0f * p0.w * dx * dy + p1.x * dy * dy);
-        const float e = __expf(fminf(power, 0.f));
-        const float at = p1.y * e;
-        const float alpha = fminf(at, kAlphaClamp);
-        const float om = 1.f - alpha;
-        const float Tk = T / om;
-        const float w = alpha * Tk;
-        const float sk = c.gA + c.gC0 * p2.x + c.gC1 * p2.y + c.gC2 * p2.z + c.gR0 * p3.x +
-                         c.gR1 * p3.y + c.gR2 * p3.z + c.gD * p1.z;
-        const float da = Tk * sk - S / om;
-        S = fmaf(sk, w, S);
-        T = Tk;
-        g[6] = w * c.gC0;
-        g[7] = w * c.gC1;
-        g[8] = w * c.gC2;
-        g[9] = w * c.gR0;
-        g[10] = w * c.gR1;
-        g[11] = w * c.gR2;
-        g[12] = w * c.gD;
-        const float dat = at <= kAlphaClamp ? da : 0.f;
-        g[5] = dat * e;
-        const float dp = power <= 0.f ? dat * p1.y * e : 0.f;
-        g[2] = -0.5f * dp * dx * dx;
-        g[3] = -dp * dx * dy;
-        g[4] = -0.5f * dp * dy * dy;
-        g[0] = dp * (p0.z * dx + p0.w * dy);
-        g[1] = dp * (p0.w * dx + p1.x * dy);
-      }
-      if (__any_sync(0xffffffffu, live)) {
-#pragma unroll
-        for (int q = 0; q < 13; ++q) g[q] = warp_sum(g[q]);
-        if (lane == 0) {
-          float *dst = a.grad + (size_t)13 * s_rank[j];
-#pragma unroll
-          for (int q = 0; q < 13; ++q) atomicAdd(dst + q, g[q]);
         }
       }
     }
@@ -392,9 +301,7 @@ extern "C" int vsx_raster_bwd(const vsx_splat *rec, const uint32_t *tile_offsets
   // reductions) or the two-phase kernel with 1/2/4 splats per phase-2 pass.
   static const char *sel = getenv("VSX_RASTER_BWD");
   static const int ns = sel ? atoi(sel) : 2;
-  if (sel && sel[0] == 'v') {
-    raster_bwd_v1_kernel<<<grid, 256, 0, as_stream(s)>>>(a, cam);
-  } else {
+  {
     const int smem = (int)(sizeof(float2) * kBC * kTilePixels);
     static bool attr = false;
     if (!attr) {

@@ -23,14 +23,40 @@ __device__ __forceinline__ float denom_of(float n0, float n1, float n2, PixRay r
   return __fadd_rn(__fadd_rn(__fmul_rn(n0, ray.rx), __fmul_rn(n1, ray.ry)), n2);
 }
 
-// One splat record in tile-local float coordinates: p0 = (mx, my, A, B),
-// p1 = (C, opacity, plane_d, -), p2 = color, p3 = camera normal.
+// One splat record staged in tile-local float coordinates:
+//   p0 = (mx, my, A2, B2)      A2 = -log2(e)/2 * A, B2 = -log2(e) * B
+//   p1 = (C2, opacity, plane_d, A)   C2 = -log2(e)/2 * C
+//   p2 = (r, g, b, B)
+//   p3 = (nx, ny, nz, C)
+// so that power * log2(e) = dx*(A2*dx + B2*dy) + C2*dy^2 feeds ex2 directly,
+// while the unscaled conic (A, B, C) stays available for the gradients.
+constexpr float kLog2e = 1.4426950408889634f;
+
 __device__ __forceinline__ void stage_splat(const vsx_splat &s, double ox, double oy, float4 &p0,
                                             float4 &p1, float4 &p2, float4 &p3) {
-  p0 = make_float4((float)(s.mean2d[0] - ox), (float)(s.mean2d[1] - oy), s.conic[0], s.conic[1]);
-  p1 = make_float4(s.conic[2], s.opacity, s.plane_d, 0.f);
-  p2 = make_float4(s.color[0], s.color[1], s.color[2], 0.f);
-  p3 = make_float4(s.normal[0], s.normal[1], s.normal[2], 0.f);
+  p0 = make_float4((float)(s.mean2d[0] - ox), (float)(s.mean2d[1] - oy),
+                   (-0.5f * kLog2e) * s.conic[0], (-kLog2e) * s.conic[1]);
+  p1 = make_float4((-0.5f * kLog2e) * s.conic[2], s.opacity, s.plane_d, s.conic[0]);
+  p2 = make_float4(s.color[0], s.color[1], s.color[2], s.conic[1]);
+  p3 = make_float4(s.normal[0], s.normal[1], s.normal[2], s.conic[2]);
+}
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Gaussian falloff e = exp(min(power, 0)) and alpha = min(o * e, 0.99) for a
+// pixel offset (dx, dy). Explicitly rounded so the forward and the backward
+// recompute bit-identical alphas (the backward divides T by 1 - alpha).
+__device__ __forceinline__ float splat_alpha(const float4 &p0, const float4 &p1, float dx,
+                                             float dy, float &e, float &at) {
+  const float q = __fmaf_rn(p0.z, dx, __fmul_rn(p0.w, dy));
+  const float p2 = __fmaf_rn(q, dx, __fmul_rn(__fmul_rn(p1.x, dy), dy));
+  e = ex2_ftz(fminf(p2, 0.f));
+  at = __fmul_rn(p1.y, e);
+  return fminf(at, 0.99f);
 }
 
 // Cotangent of the 8 blended channels of one pixel (finalize backward,

@@ -66,22 +66,27 @@ def _u32(n: int) -> torch.Tensor:
 
 # ------------------------------------------------------------------ primitives
 
-def sort_pairs_u64(keys: torch.Tensor, vals: torch.Tensor, n: int):
+SORT_SKIP_CONSTANT = 1
+
+
+def sort_pairs_u64(keys: torch.Tensor, vals: torch.Tensor, n: int, skip_constant: bool = True):
     ko = torch.empty_like(keys)
     vo = torch.empty_like(vals)
     lib = _lib.load()
     wp, wb = workspace().get(lib.vsx_sort_ws_bytes(n))
-    call("vsx_sort_pairs_u64", ptr(keys), ptr(vals), ptr(ko), ptr(vo), n, 0, 64, wp, wb, stream())
+    call("vsx_sort_pairs_u64", ptr(keys), ptr(vals), ptr(ko), ptr(vo), n, 0, 64,
+         SORT_SKIP_CONSTANT if skip_constant else 0, wp, wb, stream())
     return ko, vo
 
 
-def sort_pairs_u32(keys: torch.Tensor, vals: torch.Tensor, n: int, bits: int):
+def sort_pairs_u32(keys: torch.Tensor, vals: torch.Tensor, n: int, bits: int,
+                   skip_constant: bool = False):
     ko = torch.empty_like(keys)
     vo = torch.empty_like(vals)
     lib = _lib.load()
     wp, wb = workspace().get(lib.vsx_sort_ws_bytes(n))
-    call("vsx_sort_pairs_u32", ptr(keys), ptr(vals), ptr(ko), ptr(vo), n, 0, bits, wp, wb,
-         stream())
+    call("vsx_sort_pairs_u32", ptr(keys), ptr(vals), ptr(ko), ptr(vo), n, 0, bits,
+         SORT_SKIP_CONSTANT if skip_constant else 0, wp, wb, stream())
     return ko, vo
 
 
@@ -268,23 +273,25 @@ def bin_tiles(P: Projected, width: int, height: int) -> Bins:
     txn, tyn = (width + 15) // 16, (height + 15) // 16
     T = txn * tyn
     n = P.count
-    counts = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
-    tcounts = torch.empty(T, dtype=torch.int32, device="cuda")
-    call("vsx_bin_count", ptr(P.rec), ptr(P.radius), n, width, height, ptr(counts),
-         ptr(tcounts), stream())
-    toff = exclusive_scan(tcounts, T)
     if n == 0:
-        return Bins(toff, torch.empty(0, dtype=torch.int32, device="cuda"), txn, tyn)
+        return Bins(torch.zeros(T + 1, dtype=torch.int32, device="cuda"),
+                    torch.empty(0, dtype=torch.int32, device="cuda"), txn, tyn)
+    counts = torch.empty(n, dtype=torch.int32, device="cuda")
+    call("vsx_bin_count", ptr(P.rec), ptr(P.radius), n, width, height, ptr(counts), ptr(None),
+         stream())
     soff = exclusive_scan(counts, n)
     total = int(soff[n].item())
-    tiles = torch.empty(max(total, 1), dtype=torch.int32, device="cuda")
-    ranks = torch.empty(max(total, 1), dtype=torch.int32, device="cuda")
+    if total == 0:
+        return Bins(torch.zeros(T + 1, dtype=torch.int32, device="cuda"),
+                    torch.empty(0, dtype=torch.int32, device="cuda"), txn, tyn)
+    tiles = torch.empty(total, dtype=torch.int32, device="cuda")
+    ranks = torch.empty(total, dtype=torch.int32, device="cuda")
     call("vsx_bin_emit", ptr(P.rec), ptr(P.radius), n, width, height, ptr(soff), ptr(tiles),
          ptr(ranks), stream())
-    if total == 0:
-        return Bins(toff, ranks[:0], txn, tyn)
     bits = max(1, math.ceil(math.log2(T))) if T > 1 else 1
-    _, lst = sort_pairs_u32(tiles[:total], ranks[:total], total, bits)
+    skeys, lst = sort_pairs_u32(tiles, ranks, total, bits)
+    toff = torch.empty(T + 1, dtype=torch.int32, device="cuda")
+    call("vsx_tile_ranges", ptr(skeys), total, T, ptr(toff), stream())
     return Bins(toff, lst, txn, tyn)
 
 
