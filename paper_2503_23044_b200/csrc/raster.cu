@@ -25,7 +25,7 @@
 namespace vsx {
 
 constexpr int kChunk = 256;
-constexpr int kBC = 32;  // backward splat chunk
+constexpr int kBCMax = 32;  // largest backward splat chunk
 
 __global__ void __launch_bounds__(256) raster_fwd_kernel(
     const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
@@ -118,8 +118,9 @@ struct BwdArgs {
 
 // ---------------------------------------------------------------- backward v2
 
-template <int NS>
-__global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera cam) {
+template <int NS, int kBC>
+__global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
+    raster_bwd_kernel(BwdArgs a, vsx_camera cam) {
   __shared__ float4 s0[kBC], s1[kBC], s2[kBC], s3[kBC];
   __shared__ uint32_t s_rank[kBC];
   extern __shared__ float2 s_wq[];                // (w, q) per (splat, pixel): [kBC][256]
@@ -166,7 +167,8 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera c
     const int kbase = (int)(cs - begin);
     // live splats of this pixel in the chunk are j < nc - kbase
     const int jlive = min(cnt, nc - kbase);
-    for (int j = cnt - 1; j >= max(jlive, 0); --j) s_wq[j * kTilePixels + t] = make_float2(0.f, 0.f);
+    // dead (and, in a partial chunk, padding) rows carry zeros into phase 2
+    for (int j = kBC - 1; j >= max(jlive, 0); --j) s_wq[j * kTilePixels + t] = make_float2(0.f, 0.f);
 #pragma unroll 2
     for (int j = jlive - 1; j >= 0; --j) {
       float2 wq;
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera c
         const float4 p2 = s2[j], p3 = s3[j];
         float e, at;
         const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
-        const float rom = __frcp_rn(1.f - alpha);
+        const float rom = rcp_ftz(1.f - alpha);
         const float Tk = T * rom;
         const float w = alpha * Tk;
         const float sk = c.gA + c.gC0 * p2.x + c.gC1 * p2.y + c.gC2 * p2.z + c.gR0 * p3.x +
@@ -202,16 +204,18 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdArgs a, vsx_camera c
       for (int s = 0; s < NS; ++s)
 #pragma unroll
         for (int q = 0; q < 13; ++q) acc[s][q] = 0.f;
-#pragma unroll 1
+      // pix = lane + 32 i: x = lane & 15 is fixed per lane, y = (lane >> 4) + 2 i
+      const float xc = (float)(lane & 15) - 7.5f, xx = xc * xc;
+#pragma unroll 2
       for (int i = 0; i < kTilePixels / 32; ++i) {
         const int pix = lane + 32 * i;
         const float4 ga = s_ga[pix], gb = s_gb[pix];
-        const float xc = (float)(pix & 15) - 7.5f, yc = (float)(pix >> 4) - 7.5f;
-        const float xx = xc * xc, xy = xc * yc, yy = yc * yc;
+        const float yc = (float)((lane >> 4) + 2 * i) - 7.5f;
+        const float xy = xc * yc, yy = yc * yc;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-          const int j = jb + 8 * s;
-          if (j < cnt) {
+          const int j = jb + 8 * s;  // rows >= cnt are zero-padded by phase 1
+          {
             const float2 wq = s_wq[j * kTilePixels + pix];
             acc[s][0] = fmaf(wq.x, ga.y, acc[s][0]);
             acc[s][1] = fmaf(wq.x, ga.z, acc[s][1]);
@@ -297,29 +301,32 @@ extern "C" int vsx_raster_bwd(const vsx_splat *rec, const uint32_t *tile_offsets
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
   BwdArgs a{rec, tile_offsets, tile_list, alpha, depth, raw_normal, t_final, g_rgb, g_alpha,
             g_depth, g_normal, g_raw_normal, n_contrib, grad_splat};
-  // VSX_RASTER_BWD selects an implementation for A/B timing: "v1" (per-warp
-  // reductions) or the two-phase kernel with 1/2/4 splats per phase-2 pass.
-  static const char *sel = getenv("VSX_RASTER_BWD");
-  static const int ns = sel ? atoi(sel) : 2;
-  {
-    const int smem = (int)(sizeof(float2) * kBC * kTilePixels);
-    static bool attr = false;
-    if (!attr) {
-      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<1>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<4>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
-    if (ns == 4) {
-      raster_bwd_kernel<4><<<grid, 256, smem, as_stream(s)>>>(a, cam);
-    } else if (ns == 1) {
-      raster_bwd_kernel<1><<<grid, 256, smem, as_stream(s)>>>(a, cam);
-    } else {
-      raster_bwd_kernel<2><<<grid, 256, smem, as_stream(s)>>>(a, cam);
-    }
+  // VSX_RASTER_BWD="NS,BC" selects the phase-2 splats-per-pass and the splat
+  // chunk for A/B timing (default 2,32).
+  static int ns = 2, bc = 32;
+  static bool attr = false;
+  if (!attr) {
+    if (const char *sel = getenv("VSX_RASTER_BWD")) sscanf(sel, "%d,%d", &ns, &bc);
+    const int s32 = (int)(sizeof(float2) * 32 * kTilePixels);
+    const int s16 = (int)(sizeof(float2) * 16 * kTilePixels);
+    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<1, 16>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, s16));
+    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<2, 16>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, s16));
+    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<1, 32>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
+    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<2, 32>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
+    attr = true;
+  }
+  const int smem = (int)(sizeof(float2) * bc * kTilePixels);
+  cudaStream_t st = as_stream(s);
+  if (bc == 16) {
+    if (ns == 1) raster_bwd_kernel<1, 16><<<grid, 256, smem, st>>>(a, cam);
+    else raster_bwd_kernel<2, 16><<<grid, 256, smem, st>>>(a, cam);
+  } else {
+    if (ns == 1) raster_bwd_kernel<1, 32><<<grid, 256, smem, st>>>(a, cam);
+    else raster_bwd_kernel<2, 32><<<grid, 256, smem, st>>>(a, cam);
   }
   VSX_LAUNCH_CHECK("raster_bwd");
   return VSX_OK;

@@ -41,6 +41,12 @@ __device__ __forceinline__ void stage_splat(const vsx_splat &s, double ox, doubl
   p3 = make_float4(s.normal[0], s.normal[1], s.normal[2], s.conic[2]);
 }
 
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float ex2_ftz(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
