@@ -130,6 +130,18 @@ int vsx_decode_fwd(vsx_decoder W, const int32_t *active, int32_t n_active, const
                    float *opacity, float *color, float *scale, float *quat, float *normal,
                    float *cache_h, float *cache_o, int32_t *status, vsx_stream s);
 
+/* Tensor-core (tcgen05, 3xTF32) variant of vsx_decode_fwd. `img` is the
+ * decoder weight image built by vsx_decoder_image (vsx_decoder_image_floats(n)
+ * floats) after every weight update. Supported for n <= 13. */
+size_t vsx_decoder_image_floats(int32_t n);
+int vsx_decoder_image(vsx_decoder W, float *img, vsx_stream s);
+int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t *active, int32_t n_active,
+                      const double *centers, const float *emb, const float *log_scale,
+                      const float *offsets, vsx_camera cam, double lod_ref, double max_scale,
+                      double *means, float *opacity, float *color, float *scale, float *quat,
+                      float *normal, float *cache_h, float *cache_o, int32_t *status,
+                      vsx_stream s);
+
 /* ---- K3: projection (renderer.py:144-204) ----------------------------- */
 /* Writes one unsorted record per gaussian plus a sort key (float64 z bits,
  * or UINT64_MAX when z <= 0.01) and the 3-sigma radius; *n_kept counts
@@ -227,6 +239,12 @@ int vsx_masked_l1(const float *x, const uint8_t *valid, const float *prior,
 int vsx_adam(float *param, const float *grad, float *m, float *v, int32_t n_seg,
              const int64_t *seg_begin, const double *lr, double beta1, double beta2, double eps,
              int32_t step, vsx_stream s);
+
+/* ---- diagnostics --------------------------------------------------------- */
+/* tcgen05 self-test: D[128 x N] = A[128 x K] . B[N x K]^T, kind::tf32 from
+ * shared memory into TMEM (three != 0: 3xTF32 split). */
+int vsx_umma_selftest(const float *A, const float *B, float *D, int32_t N, int32_t K,
+                      int32_t three, vsx_stream s);
 
 #ifdef __cplusplus
 }

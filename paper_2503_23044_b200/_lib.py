@@ -63,6 +63,11 @@ _SIGS = {
     "vsx_adam": ([P, P, P, P, c_i32, P, P, c_f64, c_f64, c_f64, c_i32, P], c_i32),
     "vsx_masked_l1": ([P, P, P, P, c_i64, c_i32, P, P, P, P, P], c_i32),
     "vsx_launch_count": ([], ctypes.c_uint64),
+    "vsx_umma_selftest": ([P, P, P, c_i32, c_i32, c_i32, P], c_i32),
+    "vsx_decoder_image_floats": ([c_i32], c_size),
+    "vsx_decoder_image": ([VsxDecoder, P, P], c_i32),
+    "vsx_decode_fwd_tc": ([VsxDecoder, P, P, c_i32, P, P, P, P, VsxCamera, c_f64, c_f64,
+                           P, P, P, P, P, P, P, P, P, P], c_i32),
 }
 
 EXPORTED = tuple(_SIGS)

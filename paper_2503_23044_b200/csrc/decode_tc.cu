@@ -1,0 +1,362 @@
+// K2 on the 5th-gen tensor cores: the anchor decoder MLP with tcgen05.
+//
+// Same math as decode.cu (voxsplat decoder.py:142-180) but the two GEMMs per
+// head run as kind::tf32 MMAs from shared memory into TMEM, with a 3xTF32
+// split (hi*hi + lo*hi + hi*lo) so the result keeps fp32 accuracy (single
+// TF32 misses the 1e-4 image bound, SURVEY §7 hard part 4):
+//   GEMM1  Hpre[128 x 64] = [x | 1] [128 x 40] . [W1_h ; b1_h]^T   (bias folded in K)
+//   GEMM2  O   [128 x Nh] = tanh(Hpre) [128 x 64] . W2_h^T         (+ b2 in the epilogue)
+// One CTA (4 warps, thread = anchor row) loops persistently over tiles of 128
+// active anchors; warp 0 lane 0 issues the MMAs; the epilogue reads TMEM with
+// tcgen05.ld (warp w owns lanes 32w..32w+31) and applies the activations.
+//
+// Weights are pre-split once per optimizer step by decoder_image_kernel into
+// the exact shared-memory image (hi/lo tiles in the K-major interleaved
+// layout of umma.cuh), so tiles only copy them.
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace vsx {
+
+constexpr int kTcK1 = 40;   // 36 inputs + bias column + zero pad (multiple of 8)
+constexpr int kTcK2 = 64;   // hidden width
+constexpr int kTcRows = 128;
+
+__host__ __device__ inline int pad16(int x) { return (x + 15) / 16 * 16; }
+
+struct TcDims {
+  int n;          // gaussians per anchor
+  int np[3];      // padded head widths (multiples of 16)
+  int row0[3];    // row offset of each head inside the W2 image
+  int np_total;
+};
+
+__host__ __device__ inline TcDims tc_dims(int n) {
+  TcDims d;
+  d.n = n;
+  d.np[0] = pad16(n);
+  d.np[1] = pad16(3 * n);
+  d.np[2] = pad16(7 * n);
+  d.row0[0] = 0;
+  d.row0[1] = d.np[0];
+  d.row0[2] = d.np[0] + d.np[1];
+  d.np_total = d.np[0] + d.np[1] + d.np[2];
+  return d;
+}
+
+// Floats of the weight image: 3 heads x (hi, lo) x [64 x 40] + (hi, lo) x [NP x 64].
+__host__ __device__ inline size_t tc_image_floats(int n) {
+  return (size_t)3 * 2 * 64 * kTcK1 + (size_t)2 * tc_dims(n).np_total * kTcK2;
+}
+
+__global__ void decoder_image_kernel(vsx_decoder W, float *__restrict__ img) {
+  const TcDims d = tc_dims(W.n);
+  const int w1_tile = 64 * kTcK1;
+  const int total1 = 3 * 64 * kTcK1;
+  const int total2 = d.np_total * kTcK2;
+  float *w2img = img + 3 * 2 * w1_tile;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total1 + total2;
+       e += gridDim.x * blockDim.x) {
+    if (e < total1) {
+      const int h = e / w1_tile, rem = e % w1_tile, n = rem / kTcK1, k = rem % kTcK1;
+      float v = 0.f;
+      if (k < kInDim) v = W.w1[h][k * 64 + n];
+      else if (k == kInDim) v = W.b1[h][n];
+      float hi, lo;
+      umma::split_tf32(v, hi, lo);
+      float *base = img + (size_t)h * 2 * w1_tile;
+      const uint32_t off = umma::kmajor_offset(n, k, kTcK1) / 4;
+      base[off] = hi;
+      base[w1_tile + off] = lo;
+    } else {
+      const int e2 = e - total1, row = e2 / kTcK2, k = e2 % kTcK2;
+      int h = 2;
+      if (row < d.row0[1]) h = 0;
+      else if (row < d.row0[2]) h = 1;
+      const int j = row - d.row0[h];
+      const int width = (h == 0 ? 1 : (h == 1 ? 3 : 7)) * d.n;
+      const float v = j < width ? W.w2[h][k * width + j] : 0.f;
+      float hi, lo;
+      umma::split_tf32(v, hi, lo);
+      const uint32_t off = umma::kmajor_offset(row, k, kTcK2) / 4;
+      w2img[off] = hi;
+      w2img[(size_t)d.np_total * kTcK2 + off] = lo;
+    }
+  }
+}
+
+__device__ __forceinline__ float sigm(float v) { return 1.0f / (1.0f + expf(-v)); }
+
+struct TcSmem {
+  float *x_hi, *x_lo, *w1_hi, *w1_lo, *h_hi, *h_lo, *w2_hi, *w2_lo;
+};
+
+__device__ __forceinline__ void st_split4(float *hi_base, float *lo_base, uint32_t off_bytes,
+                                          float a, float b, float c, float d) {
+  float4 h, l;
+  umma::split_tf32(a, h.x, l.x);
+  umma::split_tf32(b, h.y, l.y);
+  umma::split_tf32(c, h.z, l.z);
+  umma::split_tf32(d, h.w, l.w);
+  *reinterpret_cast<float4 *>(reinterpret_cast<char *>(hi_base) + off_bytes) = h;
+  *reinterpret_cast<float4 *>(reinterpret_cast<char *>(lo_base) + off_bytes) = l;
+}
+
+// 3xTF32 chain D (+)= A . B^T over K (in 8-element MMA steps).
+__device__ __forceinline__ void mma3(uint32_t d, const float *a_hi, const float *a_lo,
+                                     const float *b_hi, const float *b_lo, int K, uint32_t id) {
+  const uint32_t ah = umma::smem_addr(a_hi), al = umma::smem_addr(a_lo);
+  const uint32_t bh = umma::smem_addr(b_hi), bl = umma::smem_addr(b_lo);
+  for (int s = 0; s < K / 8; ++s) {
+    const uint32_t off = (uint32_t)s * 256;
+    umma::mma_tf32(d, umma::desc_kmajor(ah + off, K), umma::desc_kmajor(bh + off, K), id, s > 0);
+    umma::mma_tf32(d, umma::desc_kmajor(al + off, K), umma::desc_kmajor(bh + off, K), id, true);
+    umma::mma_tf32(d, umma::desc_kmajor(ah + off, K), umma::desc_kmajor(bl + off, K), id, true);
+  }
+}
+
+__global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
+    vsx_decoder W, const float *__restrict__ img, const int32_t *__restrict__ active,
+    int32_t n_active, const double *__restrict__ centers, const float *__restrict__ emb,
+    const float *__restrict__ log_scale, const float *__restrict__ offsets, vsx_camera cam,
+    double lod_ref, double max_scale, double *__restrict__ means, float *__restrict__ opacity,
+    float *__restrict__ color, float *__restrict__ scale, float *__restrict__ quat,
+    float *__restrict__ normal, float *__restrict__ cache_h, float *__restrict__ cache_o,
+    int32_t *__restrict__ status) {
+  extern __shared__ __align__(1024) float tsm[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tslot;
+  const int n = W.n;
+  const TcDims dims = tc_dims(n);
+  TcSmem s;
+  s.x_hi = tsm;
+  s.x_lo = s.x_hi + kTcRows * kTcK1;
+  s.w1_hi = s.x_lo + kTcRows * kTcK1;
+  s.w1_lo = s.w1_hi + 64 * kTcK1;
+  s.h_hi = s.w1_lo + 64 * kTcK1;
+  s.h_lo = s.h_hi + kTcRows * kTcK2;
+  s.w2_hi = s.h_lo + kTcRows * kTcK2;
+  s.w2_lo = s.w2_hi + dims.np_total * kTcK2;
+  const int t = threadIdx.x, warp = t >> 5;
+  // resident W2 image (hi and lo back to back, same as the global image)
+  {
+    const float4 *src = reinterpret_cast<const float4 *>(img + 3 * 2 * 64 * kTcK1);
+    float4 *dst = reinterpret_cast<float4 *>(s.w2_hi);
+    const int n4 = 2 * dims.np_total * kTcK2 / 4;
+    for (int i = t; i < n4; i += 128) dst[i] = src[i];
+  }
+  if (warp == 0) umma::tmem_alloc(&tslot, 256);
+  if (t == 0) umma::mbar_init(&mbar, 1);
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tbase = tslot;
+  const uint32_t lane = (uint32_t)(warp * 32) << 16;
+  const uint32_t d1 = tbase, d2 = tbase + 64;
+  uint32_t phase = 0;
+  const float smax = (float)max_scale, smin = (float)kMinScale;
+  const int n_tiles = (n_active + kTcRows - 1) / kTcRows;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int r = tile * kTcRows + t;
+    const bool valid = r < n_active;
+    const int a = valid ? active[r] : 0;
+    // ---- input block (decoder.py:142-147) + bias column, split into X tiles
+    {
+      float x[kTcK1];
+#pragma unroll
+      for (int i = 0; i < kTcK1; ++i) x[i] = 0.f;
+      if (valid) {
+        const double rx = dsub(centers[3 * a + 0], cam.center[0]);
+        const double ry = dsub(centers[3 * a + 1], cam.center[1]);
+        const double rz = dsub(centers[3 * a + 2], cam.center[2]);
+        const double dd = fmax(sqrt(dadd(dadd(dmul(rx, rx), dmul(ry, ry)), dmul(rz, rz))), 1e-12);
+        const float4 *e4 = reinterpret_cast<const float4 *>(emb + (size_t)a * kEmbed);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = e4[q];
+          x[4 * q] = v.x;
+          x[4 * q + 1] = v.y;
+          x[4 * q + 2] = v.z;
+          x[4 * q + 3] = v.w;
+        }
+        x[32] = (float)ddiv(dd, lod_ref);
+        x[33] = (float)ddiv(rx, dd);
+        x[34] = (float)ddiv(ry, dd);
+        x[35] = (float)ddiv(rz, dd);
+        x[36] = 1.f;
+      }
+#pragma unroll
+      for (int q = 0; q < kTcK1 / 4; ++q)
+        st_split4(s.x_hi, s.x_lo, umma::kmajor_offset(t, 4 * q, kTcK1), x[4 * q], x[4 * q + 1],
+                  x[4 * q + 2], x[4 * q + 3]);
+    }
+    bool bad = false;
+    const double l0 = valid ? exp((double)log_scale[3 * a + 0]) : 1.0;
+    const double l1 = valid ? exp((double)log_scale[3 * a + 1]) : 1.0;
+    const double l2 = valid ? exp((double)log_scale[3 * a + 2]) : 1.0;
+    for (int h = 0; h < 3; ++h) {
+      // W1_h image -> smem
+      {
+        const float4 *src = reinterpret_cast<const float4 *>(img + (size_t)h * 2 * 64 * kTcK1);
+        float4 *dst = reinterpret_cast<float4 *>(s.w1_hi);
+        for (int i = t; i < 2 * 64 * kTcK1 / 4; i += 128) dst[i] = src[i];
+      }
+      umma::fence_async_smem();
+      umma::fence_before_sync();
+      __syncthreads();
+      umma::fence_after_sync();
+      if (t == 0) {
+        mma3(d1, s.x_hi, s.x_lo, s.w1_hi, s.w1_lo, kTcK1, umma::idesc_tf32(128, 64));
+        umma::commit(&mbar);
+      }
+      umma::mbar_wait(&mbar, phase);
+      phase ^= 1u;
+      umma::fence_after_sync();
+      // hidden activations -> cache + H tiles
+#pragma unroll
+      for (int c = 0; c < 64; c += 16) {
+        float v[16];
+        umma::tmem_ld16(d1 + lane + (uint32_t)c, v);
+        umma::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          v[i] = tanhf(v[i]);
+          if (valid && cache_h) cache_h[(size_t)(h * 64 + c + i) * n_active + r] = v[i];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          st_split4(s.h_hi, s.h_lo, umma::kmajor_offset(t, c + 4 * q, kTcK2), v[4 * q],
+                    v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      umma::fence_async_smem();
+      umma::fence_before_sync();
+      __syncthreads();
+      umma::fence_after_sync();
+      if (t == 0) {
+        const int off = dims.row0[h] * kTcK2;  // row offset (multiple of 16 rows)
+        mma3(d2, s.h_hi, s.h_lo, s.w2_hi + off, s.w2_lo + off, kTcK2,
+             umma::idesc_tf32(128, dims.np[h]));
+        umma::commit(&mbar);
+      }
+      umma::mbar_wait(&mbar, phase);
+      phase ^= 1u;
+      umma::fence_after_sync();
+      const int width = (h == 0 ? 1 : (h == 1 ? 3 : 7)) * n;
+      const int oo = h == 0 ? 0 : (h == 1 ? n : 4 * n);
+      if (h < 2) {
+        for (int c = 0; c < dims.np[h]; c += 16) {
+          float v[16];
+          umma::tmem_ld16(d2 + lane + (uint32_t)c, v);
+          umma::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int j = c + i;
+            if (valid && j < width) {
+              const float o = v[i] + W.b2[h][j];
+              if (cache_o) cache_o[(size_t)(oo + j) * n_active + r] = o;
+              const float sg = sigm(o);
+              bad |= !isfinite(sg);
+              if (h == 0) opacity[(size_t)r * n + j] = sg;
+              else color[(size_t)r * 3 * n + j] = sg;
+            }
+          }
+        }
+      } else {
+        for (int sl = 0; sl < n; ++sl) {
+          float o[16];
+          umma::tmem_ld16(d2 + lane + (uint32_t)(7 * sl), o);  // columns 7sl .. 7sl+15
+          umma::tmem_ld_wait();
+          if (!valid) continue;
+#pragma unroll
+          for (int c = 0; c < 7; ++c) {
+            o[c] += W.b2[2][7 * sl + c];
+            if (cache_o) cache_o[(size_t)(oo + 7 * sl + c) * n_active + r] = o[c];
+          }
+          const size_t g = (size_t)r * n + sl;
+          float sc[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            sc[c] = fminf(fmaxf(expf(o[c]), smin), smax);
+            scale[3 * g + c] = sc[c];
+          }
+          float qw = o[3] + 1.0f, qx = o[4], qy = o[5], qz = o[6];
+          const float qn = fmaxf(sqrtf(qw * qw + qx * qx + qy * qy + qz * qz), 1e-12f);
+          qw /= qn;
+          qx /= qn;
+          qy /= qn;
+          qz /= qn;
+          quat[4 * g + 0] = qw;
+          quat[4 * g + 1] = qx;
+          quat[4 * g + 2] = qy;
+          quat[4 * g + 3] = qz;
+          float R[9];
+          quat_to_rot(qw, qx, qy, qz, R);
+          const int ax = argmin3(sc[0], sc[1], sc[2]);
+          normal[3 * g + 0] = R[0 + ax];
+          normal[3 * g + 1] = R[3 + ax];
+          normal[3 * g + 2] = R[6 + ax];
+          const float *off = offsets + ((size_t)a * n + sl) * 3;
+          const double m0 = dadd(centers[3 * a + 0], dmul((double)off[0], l0));
+          const double m1 = dadd(centers[3 * a + 1], dmul((double)off[1], l1));
+          const double m2 = dadd(centers[3 * a + 2], dmul((double)off[2], l2));
+          means[3 * g + 0] = m0;
+          means[3 * g + 1] = m1;
+          means[3 * g + 2] = m2;
+          bad |= !(isfinite(sc[0]) && isfinite(sc[1]) && isfinite(sc[2]) && isfinite(qw) &&
+                   isfinite(qx) && isfinite(qy) && isfinite(qz) && isfinite(m0) &&
+                   isfinite(m1) && isfinite(m2));
+        }
+      }
+      umma::fence_before_sync();
+    }
+    if (bad) atomicOr(status, VSX_STATUS_NONFINITE);
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tbase, 256);
+}
+
+size_t tc_smem_bytes(int n) {
+  const TcDims d = tc_dims(n);
+  return sizeof(float) * ((size_t)2 * kTcRows * kTcK1 + 2 * 64 * kTcK1 + 2 * kTcRows * kTcK2 +
+                          (size_t)2 * d.np_total * kTcK2);
+}
+
+bool tc_supported(int n) { return n >= 1 && tc_smem_bytes(n) <= 220 * 1024 && 7 * n + 16 <= 176; }
+
+}  // namespace vsx
+
+using namespace vsx;
+
+extern "C" size_t vsx_decoder_image_floats(int32_t n) { return tc_image_floats(n); }
+
+extern "C" int vsx_decoder_image(vsx_decoder W, float *img, vsx_stream s) {
+  VSX_REQUIRE(W.n >= 1, "decoder_image: bad n");
+  decoder_image_kernel<<<64, 256, 0, as_stream(s)>>>(W, img);
+  VSX_LAUNCH_CHECK("decoder_image");
+  return VSX_OK;
+}
+
+extern "C" int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t *active,
+                                 int32_t n_active, const double *centers, const float *emb,
+                                 const float *log_scale, const float *offsets, vsx_camera cam,
+                                 double lod_ref, double max_scale, double *means, float *opacity,
+                                 float *color, float *scale, float *quat, float *normal,
+                                 float *cache_h, float *cache_o, int32_t *status, vsx_stream s) {
+  VSX_REQUIRE(W.n >= 1 && n_active >= 0 && lod_ref > 0, "decode_fwd_tc: bad arguments");
+  VSX_REQUIRE(tc_supported(W.n), "decode_fwd_tc: n=%d not supported by the tensor-core path",
+              W.n);
+  if (n_active == 0) return VSX_OK;
+  const size_t smem = tc_smem_bytes(W.n);
+  VSX_CUDA_TRY(cudaFuncSetAttribute(decode_fwd_tc_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = (n_active + kTcRows - 1) / kTcRows;
+  decode_fwd_tc_kernel<<<std::min(tiles, sms), 128, smem, as_stream(s)>>>(
+      W, img, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, max_scale, means,
+      opacity, color, scale, quat, normal, cache_h, cache_o, status);
+  VSX_LAUNCH_CHECK("decode_fwd_tc");
+  return VSX_OK;
+}

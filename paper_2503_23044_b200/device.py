@@ -191,10 +191,31 @@ def decode(dec_abi, n: int, active: torch.Tensor, centers: torch.Tensor, emb: to
     nrm = torch.empty((g, 3), dtype=torch.float32, device=dev)
     ch = torch.empty((192, max(na, 1)), dtype=torch.float32, device=dev) if keep_cache else None
     co = torch.empty((11 * n, max(na, 1)), dtype=torch.float32, device=dev) if keep_cache else None
-    call("vsx_decode_fwd", dec_abi, ptr(active), na, ptr(centers), ptr(emb), ptr(log_scales),
-         ptr(offsets), view.to_abi(), lod_ref, max_scale, ptr(means), ptr(opac), ptr(col),
-         ptr(scl), ptr(quat), ptr(nrm), ptr(ch), ptr(co), ptr(status), stream())
+    if use_tensor_cores(n):
+        img = decoder_image(dec_abi, n)
+        call("vsx_decode_fwd_tc", dec_abi, ptr(img), ptr(active), na, ptr(centers), ptr(emb),
+             ptr(log_scales), ptr(offsets), view.to_abi(), lod_ref, max_scale, ptr(means),
+             ptr(opac), ptr(col), ptr(scl), ptr(quat), ptr(nrm), ptr(ch), ptr(co), ptr(status),
+             stream())
+    else:
+        call("vsx_decode_fwd", dec_abi, ptr(active), na, ptr(centers), ptr(emb), ptr(log_scales),
+             ptr(offsets), view.to_abi(), lod_ref, max_scale, ptr(means), ptr(opac), ptr(col),
+             ptr(scl), ptr(quat), ptr(nrm), ptr(ch), ptr(co), ptr(status), stream())
     return Decoded(active, means, opac, col, scl, quat, nrm, ch, co)
+
+
+def use_tensor_cores(n: int) -> bool:
+    """tcgen05 decoder for n <= 13 unless VSX_DECODE_TC=0 (FFMA kernel, for A/B)."""
+    import os
+    return n <= 13 and os.environ.get("VSX_DECODE_TC", "1") != "0"
+
+
+def decoder_image(dec_abi, n: int) -> torch.Tensor:
+    """3xTF32 hi/lo weight image in the tensor-core shared-memory layout."""
+    lib = _lib.load()
+    img = torch.empty(int(lib.vsx_decoder_image_floats(n)), dtype=torch.float32, device="cuda")
+    call("vsx_decoder_image", dec_abi, ptr(img), stream())
+    return img
 
 
 # ------------------------------------------------------------------ project + sort
