@@ -460,6 +460,9 @@ static int launch_wgrad(const float *A, int a_rows, bool ones_row, const float *
   return VSX_OK;
 }
 
+int decoder_wgrad_tc(const float *g_o, const float *cache_h, const float *g_pre, const float *xs,
+                     int64_t K, int n, vsx_decoder_grads dW, cudaStream_t st);
+
 }  // namespace vsx
 
 using namespace vsx;
@@ -520,6 +523,12 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
       cache_o, scale, quat, g_means, g_opacity, g_color, g_scale, g_quat, g_normal, g_emb,
       g_log_scale, g_offsets, xs, g_o, g_pre);
   VSX_LAUNCH_CHECK("decode_bwd_anchor");
+  static const bool use_tc = [] {
+    const char *e = getenv("VSX_DECODE_TC");
+    return !(e && e[0] == '0');
+  }();
+  if (use_tc && 11 * n <= 128)  // tensor-core weight gradients (decode_tc.cu)
+    return decoder_wgrad_tc(g_o, cache_h, g_pre, xs, n_active, n, dW, st);
   // dW1_h = X^T Gpre_h (+ db1 via the ones row of X)
   WgradOut o1{};
   for (int h = 0; h < 3; ++h) {

@@ -316,6 +316,184 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
   if (warp == 0) umma::tmem_dealloc(tbase, 256);
 }
 
+// ---------------------------------------------------------------- weight gradients
+//
+// All decoder weight gradients of one view as two K-split tcgen05 GEMMs over
+// the active anchors (K), reading the feature-major caches directly (a row
+// of each cache is contiguous along K, i.e. a K-major operand):
+//   C1[j][n] = sum_r dO[r][j] * [H | 1][r][n]   M = 11n outputs (pad 128), N = 192 + 1 (pad 208)
+//              -> dW2_h[n][j] (diagonal head blocks) and db2 (ones column)
+//   C2[m][i] = sum_r dPre[r][m] * [X | 1][r][i] M = 192 hidden (two 128 tiles), N = 37 (pad 48)
+//              -> dW1_h[i][m] and db1 (ones column)
+// Each CTA accumulates its K-chunks in TMEM and adds its partial result to
+// the global gradients with one atomicAdd per element at the end.
+
+constexpr int kWgKc = 32;    // anchors per stage (4 MMA k-steps)
+constexpr int kWgN1 = 208;   // 192 hidden + ones row, padded to 16
+constexpr int kWgN2 = 48;    // 36 inputs + ones row, padded to 16
+
+struct WgSmem {
+  float *a1_hi, *a1_lo, *b1_hi, *b1_lo, *a2_hi, *a2_lo, *b2_hi, *b2_lo;
+};
+
+inline size_t wg_smem_bytes() {
+  return sizeof(float) * (size_t)2 * kWgKc * (128 + kWgN1 + 256 + kWgN2);
+}
+
+// Stage rows [0, rows) of a feature-major [rows_valid x K] matrix, anchors
+// [k0, k0 + 32), into a hi/lo K-major tile of `rows` rows. Rows >= rows_valid
+// read `ones_row` (1.0 when == that row index) or zero.
+__device__ __forceinline__ void wg_stage(float *hi, float *lo, const float *__restrict__ src,
+                                         int rows, int rows_valid, int ones_row, int64_t K,
+                                         int64_t k0) {
+  const int quads = rows * (kWgKc / 4);
+  for (int e = threadIdx.x; e < quads; e += blockDim.x) {
+    const int r = e / (kWgKc / 4), q = e % (kWgKc / 4);
+    const int64_t k = k0 + 4 * q;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (r < rows_valid) {
+      const float *p = src + (size_t)r * K + k;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = (k + i < K) ? p[i] : 0.f;
+    } else if (r == ones_row) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = (k + i < K) ? 1.f : 0.f;
+    }
+    st_split4(hi, lo, umma::kmajor_offset(r, 4 * q, kWgKc), v[0], v[1], v[2], v[3]);
+  }
+}
+
+__global__ void __launch_bounds__(128, 1) decoder_wgrad_tc_kernel(
+    const float *__restrict__ g_o, const float *__restrict__ cache_h,
+    const float *__restrict__ g_pre, const float *__restrict__ xs, int64_t K, int n,
+    vsx_decoder_grads dW) {
+  extern __shared__ __align__(1024) float wsm[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tslot;
+  WgSmem s;
+  s.a1_hi = wsm;
+  s.a1_lo = s.a1_hi + 128 * kWgKc;
+  s.b1_hi = s.a1_lo + 128 * kWgKc;
+  s.b1_lo = s.b1_hi + kWgN1 * kWgKc;
+  s.a2_hi = s.b1_lo + kWgN1 * kWgKc;
+  s.a2_lo = s.a2_hi + 256 * kWgKc;
+  s.b2_hi = s.a2_lo + 256 * kWgKc;
+  s.b2_lo = s.b2_hi + kWgN2 * kWgKc;
+  const int t = threadIdx.x, warp = t >> 5;
+  const int nout = 11 * n;
+  if (warp == 0) umma::tmem_alloc(&tslot, 512);
+  if (t == 0) umma::mbar_init(&mbar, 1);
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tbase = tslot;
+  const uint32_t c1 = tbase, c2a = tbase + kWgN1, c2b = tbase + kWgN1 + kWgN2;
+  uint32_t phase = 0;
+  const int64_t nchunks = (K + kWgKc - 1) / kWgKc;
+  bool first = true;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t k0 = ch * kWgKc;
+    wg_stage(s.a1_hi, s.a1_lo, g_o, 128, nout, -1, K, k0);
+    wg_stage(s.b1_hi, s.b1_lo, cache_h, kWgN1, 192, 192, K, k0);
+    wg_stage(s.a2_hi, s.a2_lo, g_pre, 256, 192, -1, K, k0);
+    wg_stage(s.b2_hi, s.b2_lo, xs, kWgN2, kInDim + 1, -1, K, k0);  // xs row 36 = ones
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    if (t == 0) {
+      const uint32_t i1 = umma::idesc_tf32(128, kWgN1), i2 = umma::idesc_tf32(128, kWgN2);
+      const uint32_t a1h = umma::smem_addr(s.a1_hi), a1l = umma::smem_addr(s.a1_lo);
+      const uint32_t b1h = umma::smem_addr(s.b1_hi), b1l = umma::smem_addr(s.b1_lo);
+      const uint32_t a2h = umma::smem_addr(s.a2_hi), a2l = umma::smem_addr(s.a2_lo);
+      const uint32_t b2h = umma::smem_addr(s.b2_hi), b2l = umma::smem_addr(s.b2_lo);
+      const uint32_t tile2 = 128 * kWgKc * 4;  // second 128-row tile of A2
+      for (int st = 0; st < kWgKc / 8; ++st) {
+        const uint32_t o = (uint32_t)st * 256;
+        const bool acc0 = !(first && st == 0);
+        using umma::desc_kmajor;
+        umma::mma_tf32(c1, desc_kmajor(a1h + o, kWgKc), desc_kmajor(b1h + o, kWgKc), i1, acc0);
+        umma::mma_tf32(c1, desc_kmajor(a1l + o, kWgKc), desc_kmajor(b1h + o, kWgKc), i1, true);
+        umma::mma_tf32(c1, desc_kmajor(a1h + o, kWgKc), desc_kmajor(b1l + o, kWgKc), i1, true);
+        for (int mt = 0; mt < 2; ++mt) {
+          const uint32_t d = mt ? c2b : c2a, ao = mt ? tile2 : 0u;
+          umma::mma_tf32(d, desc_kmajor(a2h + ao + o, kWgKc), desc_kmajor(b2h + o, kWgKc), i2,
+                         acc0);
+          umma::mma_tf32(d, desc_kmajor(a2l + ao + o, kWgKc), desc_kmajor(b2h + o, kWgKc), i2,
+                         true);
+          umma::mma_tf32(d, desc_kmajor(a2h + ao + o, kWgKc), desc_kmajor(b2l + o, kWgKc), i2,
+                         true);
+        }
+      }
+      umma::commit(&mbar);
+    }
+    umma::mbar_wait(&mbar, phase);
+    phase ^= 1u;
+    umma::fence_after_sync();
+    first = false;
+  }
+  if (!first) {
+    const uint32_t lane = (uint32_t)(warp * 32) << 16;
+    // C1 row t = output j: head blocks of dW2 and db2
+    const int j = t;
+    int h = 2;
+    if (j < n) h = 0;
+    else if (j < 4 * n) h = 1;
+    const int oo = h == 0 ? 0 : (h == 1 ? n : 4 * n);
+    const int width = (h == 0 ? 1 : (h == 1 ? 3 : 7)) * n;
+    for (int c = 0; c < kWgN1; c += 16) {
+      float v[16];
+      umma::tmem_ld16(c1 + lane + (uint32_t)c, v);
+      umma::tmem_ld_wait();
+      if (j >= nout) continue;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int col = c + i;
+        if (col >= h * 64 && col < h * 64 + 64)
+          atomicAdd(dW.w2[h] + (size_t)(col - h * 64) * width + (j - oo), v[i]);
+        else if (col == 192)
+          atomicAdd(dW.b2[h] + (j - oo), v[i]);
+      }
+    }
+    // C2 rows = hidden m (two tiles): dW1_h[i][m] and db1 (ones column 36)
+    for (int mt = 0; mt < 2; ++mt) {
+      const int m = mt * 128 + t;
+      for (int c = 0; c < kWgN2; c += 16) {
+        float v[16];
+        umma::tmem_ld16((mt ? c2b : c2a) + lane + (uint32_t)c, v);
+        umma::tmem_ld_wait();
+        if (m >= 192) continue;
+        const int hh = m / 64, mm = m % 64;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int col = c + i;
+          if (col < kInDim) atomicAdd(dW.w1[hh] + (size_t)col * 64 + mm, v[i]);
+          else if (col == kInDim) atomicAdd(dW.b1[hh] + mm, v[i]);
+        }
+      }
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tbase, 512);
+}
+
+int decoder_wgrad_tc(const float *g_o, const float *cache_h, const float *g_pre, const float *xs,
+                     int64_t K, int n, vsx_decoder_grads dW, cudaStream_t st) {
+  if (K == 0) return VSX_OK;
+  const size_t smem = wg_smem_bytes();
+  VSX_CUDA_TRY(cudaFuncSetAttribute(decoder_wgrad_tc_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t chunks = (K + kWgKc - 1) / kWgKc;
+  decoder_wgrad_tc_kernel<<<(int)std::min<int64_t>(chunks, sms), 128, smem, st>>>(
+      g_o, cache_h, g_pre, xs, K, n, dW);
+  VSX_LAUNCH_CHECK("decoder_wgrad_tc");
+  return VSX_OK;
+}
+
 size_t tc_smem_bytes(int n) {
   const TcDims d = tc_dims(n);
   return sizeof(float) * ((size_t)2 * kTcRows * kTcK1 + 2 * 64 * kTcK1 + 2 * kTcRows * kTcK2 +
