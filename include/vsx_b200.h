@@ -180,6 +180,36 @@ int vsx_raster_fwd(const vsx_splat *rec, const uint32_t *tile_offsets, const uin
                    float *raw_normal, uint8_t *valid, float *t_final, int32_t *n_contrib,
                    vsx_stream s);
 
+/* Fused training objective of one view (K9 folded into K5/K6):
+ *   L = rgb_scale * sum|rgb - gt|                              (losses.py:43-53)
+ *     + depth_weight  * sum_mask |depth - prior| / count_depth  (losses.py:65-84)
+ *     + normal_weight * sum_mask |normal - prior_n| / count_normal
+ * with mask = render-valid & prior-valid. The forward accumulates the raw
+ * sums (sums[0..2], float64) and counts (counts[0..1]); the backward forms
+ * the pixel cotangents on the fly from the same inputs. Unused priors NULL. */
+typedef struct vsx_loss_desc {
+  const float *gt_rgb;
+  const float *prior_depth;
+  const uint8_t *prior_depth_valid;
+  const float *prior_normal;
+  const uint8_t *prior_normal_valid;
+  float rgb_scale;
+  float depth_weight;
+  float normal_weight;
+  double *sums;
+  uint32_t *counts;
+} vsx_loss_desc;
+
+int vsx_raster_fwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,
+                        const uint32_t *tile_list, vsx_camera cam, float *rgb, float *alpha,
+                        float *depth, float *normal, float *raw_normal, uint8_t *valid,
+                        float *t_final, int32_t *n_contrib, vsx_loss_desc loss, vsx_stream s);
+int vsx_raster_bwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,
+                        const uint32_t *tile_list, vsx_camera cam, const float *rgb,
+                        const float *alpha, const float *depth, const float *normal,
+                        const float *raw_normal, const float *t_final, const int32_t *n_contrib,
+                        vsx_loss_desc loss, float *grad_splat, vsx_stream s);
+
 /* ---- K6: compositing backward ------------------------------------------ */
 /* Pixel cotangents (any may be NULL = zero) -> per-splat gradients
  * (sorted order, float32 x 13: mean2d 2, conic 3, opacity, color 3,

@@ -34,6 +34,16 @@ class VsxDecoderGrads(ctypes.Structure):
                 ("b2", c_void_p * 3)]
 
 
+class VsxLossDesc(ctypes.Structure):
+    """Mirror of vsx_loss_desc (fused RGB-D-N objective of one view)."""
+
+    _fields_ = [("gt_rgb", c_void_p), ("prior_depth", c_void_p),
+                ("prior_depth_valid", c_void_p), ("prior_normal", c_void_p),
+                ("prior_normal_valid", c_void_p), ("rgb_scale", c_f32),
+                ("depth_weight", c_f32), ("normal_weight", c_f32), ("sums", c_void_p),
+                ("counts", c_void_p)]
+
+
 P = c_void_p
 _SIGS = {
     "vsx_version": ([], c_i32),
@@ -64,6 +74,10 @@ _SIGS = {
     "vsx_masked_l1": ([P, P, P, P, c_i64, c_i32, P, P, P, P, P], c_i32),
     "vsx_launch_count": ([], ctypes.c_uint64),
     "vsx_umma_selftest": ([P, P, P, c_i32, c_i32, c_i32, P], c_i32),
+    "vsx_raster_fwd_loss": ([P, P, P, VsxCamera, P, P, P, P, P, P, P, P, VsxLossDesc, P],
+                            c_i32),
+    "vsx_raster_bwd_loss": ([P, P, P, VsxCamera, P, P, P, P, P, P, P, VsxLossDesc, P, P],
+                            c_i32),
     "vsx_decoder_image_floats": ([c_i32], c_size),
     "vsx_decoder_image": ([VsxDecoder, P, P], c_i32),
     "vsx_decode_fwd_tc": ([VsxDecoder, P, P, c_i32, P, P, P, P, VsxCamera, c_f64, c_f64,

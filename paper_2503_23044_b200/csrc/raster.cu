@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
     const uint32_t *__restrict__ tile_list, vsx_camera cam, float *__restrict__ out_rgb,
     float *__restrict__ out_alpha, float *__restrict__ out_depth, float *__restrict__ out_normal,
     float *__restrict__ out_raw, uint8_t *__restrict__ out_valid, float *__restrict__ out_T,
-    int32_t *__restrict__ out_nc) {
+    int32_t *__restrict__ out_nc, vsx_loss_desc L) {
   __shared__ float4 s0[kChunk], s1[kChunk], s2[kChunk], s3[kChunk];
   const int txn = gridDim.x;
   const int tile = blockIdx.y * txn + blockIdx.x;
@@ -78,33 +78,71 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
       done = j < cnt;
     }
   }
-  if (!inside) return;
-  const size_t p = (size_t)py * cam.width + px;
-  const PixRay ray = pixel_ray(cam, px, py);
-  const float den = denom_of(n0, n1, n2, ray);
-  const bool covered = acc >= kAlphaValidMin;
-  const bool valid = covered && fabsf(den) >= kDenomGuard;
-  if (out_rgb) {
-    out_rgb[3 * p + 0] = c0;
-    out_rgb[3 * p + 1] = c1;
-    out_rgb[3 * p + 2] = c2;
-  }
-  if (out_alpha) out_alpha[p] = acc;
-  if (out_depth) out_depth[p] = valid ? dist / den : 0.f;
-  if (out_raw) {
-    out_raw[3 * p + 0] = n0;
-    out_raw[3 * p + 1] = n1;
-    out_raw[3 * p + 2] = n2;
-  }
-  if (out_normal) {
+  // loss partial sums (fused K9): rgb |d|, masked depth |d|, masked normal |d|
+  double l_rgb = 0.0, l_dep = 0.0, l_nrm = 0.0;
+  uint32_t c_dep = 0, c_nrm = 0;
+  if (inside) {
+    const size_t p = (size_t)py * cam.width + px;
+    const PixRay ray = pixel_ray(cam, px, py);
+    const float den = denom_of(n0, n1, n2, ray);
+    const bool covered = acc >= kAlphaValidMin;
+    const bool valid = covered && fabsf(den) >= kDenomGuard;
+    const float depth = valid ? dist / den : 0.f;
     const float nn = fmaxf(sqrtf(n0 * n0 + n1 * n1 + n2 * n2), 1e-12f);
-    out_normal[3 * p + 0] = covered ? n0 / nn : 0.f;
-    out_normal[3 * p + 1] = covered ? n1 / nn : 0.f;
-    out_normal[3 * p + 2] = covered ? n2 / nn : 0.f;
+    const float nx = covered ? n0 / nn : 0.f, ny = covered ? n1 / nn : 0.f,
+                nz = covered ? n2 / nn : 0.f;
+    if (out_rgb) {
+      out_rgb[3 * p + 0] = c0;
+      out_rgb[3 * p + 1] = c1;
+      out_rgb[3 * p + 2] = c2;
+    }
+    if (out_alpha) out_alpha[p] = acc;
+    if (out_depth) out_depth[p] = depth;
+    if (out_raw) {
+      out_raw[3 * p + 0] = n0;
+      out_raw[3 * p + 1] = n1;
+      out_raw[3 * p + 2] = n2;
+    }
+    if (out_normal) {
+      out_normal[3 * p + 0] = nx;
+      out_normal[3 * p + 1] = ny;
+      out_normal[3 * p + 2] = nz;
+    }
+    if (out_valid) out_valid[p] = valid ? 1 : 0;
+    out_T[p] = T;
+    out_nc[p] = nc;
+    if (L.gt_rgb) {
+      l_rgb = fabs((double)(c0 - L.gt_rgb[3 * p + 0])) + fabs((double)(c1 - L.gt_rgb[3 * p + 1])) +
+              fabs((double)(c2 - L.gt_rgb[3 * p + 2]));
+      if (L.prior_depth && valid && L.prior_depth_valid[p]) {
+        l_dep = fabs((double)(depth - L.prior_depth[p]));
+        c_dep = 1;
+      }
+      if (L.prior_normal && valid && L.prior_normal_valid[p]) {
+        l_nrm = fabs((double)(nx - L.prior_normal[3 * p + 0])) +
+                fabs((double)(ny - L.prior_normal[3 * p + 1])) +
+                fabs((double)(nz - L.prior_normal[3 * p + 2]));
+        c_nrm = 1;
+      }
+    }
   }
-  if (out_valid) out_valid[p] = valid ? 1 : 0;
-  out_T[p] = T;
-  out_nc[p] = nc;
+  if (L.gt_rgb) {  // block-uniform
+    l_rgb = warp_sum_d(l_rgb);
+    l_dep = warp_sum_d(l_dep);
+    l_nrm = warp_sum_d(l_nrm);
+    const unsigned bd = __ballot_sync(0xffffffffu, c_dep), bn = __ballot_sync(0xffffffffu, c_nrm);
+    if ((threadIdx.x & 31) == 0) {
+      if (l_rgb != 0.0) atomicAdd(L.sums + 0, l_rgb);
+      if (bd) {
+        atomicAdd(L.sums + 1, l_dep);
+        atomicAdd(L.counts + 0, (uint32_t)__popc(bd));
+      }
+      if (bn) {
+        atomicAdd(L.sums + 2, l_nrm);
+        atomicAdd(L.counts + 1, (uint32_t)__popc(bn));
+      }
+    }
+  }
 }
 
 struct BwdArgs {
@@ -114,6 +152,8 @@ struct BwdArgs {
   const float *alpha, *depth, *raw, *T, *g_rgb, *g_alpha, *g_depth, *g_normal, *g_raw;
   const int32_t *nc;
   float *grad;
+  const float *rgb, *normal;  // forward outputs (fused-loss mode)
+  vsx_loss_desc L;            // L.gt_rgb != NULL: cotangents from the fused objective
 };
 
 // ---------------------------------------------------------------- backward v2
@@ -145,8 +185,11 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
     const size_t p = (size_t)py * cam.width + px;
     nc = a.nc[p];
     T = a.T[p];
-    c = pixel_cotangent(cam, px, py, p, a.alpha, a.depth, a.raw, a.g_rgb, a.g_alpha, a.g_depth,
-                        a.g_normal, a.g_raw);
+    if (a.L.gt_rgb)
+      c = pixel_cotangent_loss(cam, px, py, p, a.alpha, a.rgb, a.depth, a.normal, a.raw, a.L);
+    else
+      c = pixel_cotangent(cam, px, py, p, a.alpha, a.depth, a.raw, a.g_rgb, a.g_alpha, a.g_depth,
+                          a.g_normal, a.g_raw);
     if (nc > 0) atomicMax(&s_max, nc);
   }
   s_ga[t] = make_float4(c.gA, c.gC0, c.gC1, c.gC2);
@@ -270,37 +313,8 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
   }
 }
 
-}  // namespace vsx
-
-using namespace vsx;
-
-extern "C" int vsx_raster_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
-                              const uint32_t *tile_list, vsx_camera cam, float *rgb,
-                              float *alpha, float *depth, float *normal, float *raw_normal,
-                              uint8_t *valid, float *t_final, int32_t *n_contrib,
-                              vsx_stream s) {
-  VSX_REQUIRE(cam.width > 0 && cam.height > 0 && t_final && n_contrib, "raster_fwd: bad args");
+static int launch_bwd(const BwdArgs &a, const vsx_camera &cam, cudaStream_t st) {
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
-  raster_fwd_kernel<<<grid, 256, 0, as_stream(s)>>>(rec, tile_offsets, tile_list, cam, rgb, alpha,
-                                                    depth, normal, raw_normal, valid, t_final,
-                                                    n_contrib);
-  VSX_LAUNCH_CHECK("raster_fwd");
-  return VSX_OK;
-}
-
-extern "C" int vsx_raster_bwd(const vsx_splat *rec, const uint32_t *tile_offsets,
-                              const uint32_t *tile_list, vsx_camera cam, const float *rgb,
-                              const float *alpha, const float *depth, const float *raw_normal,
-                              const float *t_final, const int32_t *n_contrib, const float *g_rgb,
-                              const float *g_alpha, const float *g_depth, const float *g_normal,
-                              const float *g_raw_normal, float *grad_splat, vsx_stream s) {
-  (void)rgb;
-  VSX_REQUIRE(cam.width > 0 && cam.height > 0 && alpha && raw_normal && t_final && n_contrib,
-              "raster_bwd: bad args");
-  VSX_REQUIRE(!g_depth || depth, "raster_bwd: depth cotangent needs the depth image");
-  dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
-  BwdArgs a{rec, tile_offsets, tile_list, alpha, depth, raw_normal, t_final, g_rgb, g_alpha,
-            g_depth, g_normal, g_raw_normal, n_contrib, grad_splat};
   // VSX_RASTER_BWD="NS,BC" selects the phase-2 splats-per-pass and the splat
   // chunk for A/B timing (default 2,32).
   static int ns = 2, bc = 32;
@@ -320,7 +334,6 @@ extern "C" int vsx_raster_bwd(const vsx_splat *rec, const uint32_t *tile_offsets
     attr = true;
   }
   const int smem = (int)(sizeof(float2) * bc * kTilePixels);
-  cudaStream_t st = as_stream(s);
   if (bc == 16) {
     if (ns == 1) raster_bwd_kernel<1, 16><<<grid, 256, smem, st>>>(a, cam);
     else raster_bwd_kernel<2, 16><<<grid, 256, smem, st>>>(a, cam);
@@ -330,4 +343,70 @@ extern "C" int vsx_raster_bwd(const vsx_splat *rec, const uint32_t *tile_offsets
   }
   VSX_LAUNCH_CHECK("raster_bwd");
   return VSX_OK;
+}
+
+static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
+                      const uint32_t *tile_list, const vsx_camera &cam, float *rgb, float *alpha,
+                      float *depth, float *normal, float *raw_normal, uint8_t *valid,
+                      float *t_final, int32_t *n_contrib, const vsx_loss_desc &L,
+                      cudaStream_t st) {
+  VSX_REQUIRE(cam.width > 0 && cam.height > 0 && t_final && n_contrib, "raster_fwd: bad args");
+  dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
+  raster_fwd_kernel<<<grid, 256, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha, depth,
+                                          normal, raw_normal, valid, t_final, n_contrib, L);
+  VSX_LAUNCH_CHECK("raster_fwd");
+  return VSX_OK;
+}
+
+}  // namespace vsx
+
+using namespace vsx;
+
+extern "C" int vsx_raster_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
+                              const uint32_t *tile_list, vsx_camera cam, float *rgb,
+                              float *alpha, float *depth, float *normal, float *raw_normal,
+                              uint8_t *valid, float *t_final, int32_t *n_contrib,
+                              vsx_stream s) {
+  vsx_loss_desc none{};
+  return launch_fwd(rec, tile_offsets, tile_list, cam, rgb, alpha, depth, normal, raw_normal,
+                    valid, t_final, n_contrib, none, as_stream(s));
+}
+
+extern "C" int vsx_raster_fwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,
+                                   const uint32_t *tile_list, vsx_camera cam, float *rgb,
+                                   float *alpha, float *depth, float *normal, float *raw_normal,
+                                   uint8_t *valid, float *t_final, int32_t *n_contrib,
+                                   vsx_loss_desc loss, vsx_stream s) {
+  VSX_REQUIRE(loss.gt_rgb && loss.sums && loss.counts, "raster_fwd_loss: gt_rgb/sums/counts");
+  VSX_REQUIRE(rgb && depth && normal && valid, "raster_fwd_loss: needs rgb/depth/normal/valid");
+  return launch_fwd(rec, tile_offsets, tile_list, cam, rgb, alpha, depth, normal, raw_normal,
+                    valid, t_final, n_contrib, loss, as_stream(s));
+}
+
+extern "C" int vsx_raster_bwd(const vsx_splat *rec, const uint32_t *tile_offsets,
+                              const uint32_t *tile_list, vsx_camera cam, const float *rgb,
+                              const float *alpha, const float *depth, const float *raw_normal,
+                              const float *t_final, const int32_t *n_contrib, const float *g_rgb,
+                              const float *g_alpha, const float *g_depth, const float *g_normal,
+                              const float *g_raw_normal, float *grad_splat, vsx_stream s) {
+  VSX_REQUIRE(cam.width > 0 && cam.height > 0 && alpha && raw_normal && t_final && n_contrib,
+              "raster_bwd: bad args");
+  VSX_REQUIRE(!g_depth || depth, "raster_bwd: depth cotangent needs the depth image");
+  BwdArgs a{rec, tile_offsets, tile_list, alpha, depth, raw_normal, t_final, g_rgb, g_alpha,
+            g_depth, g_normal, g_raw_normal, n_contrib, grad_splat, rgb, nullptr, {}};
+  return launch_bwd(a, cam, as_stream(s));
+}
+
+extern "C" int vsx_raster_bwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,
+                                   const uint32_t *tile_list, vsx_camera cam, const float *rgb,
+                                   const float *alpha, const float *depth, const float *normal,
+                                   const float *raw_normal, const float *t_final,
+                                   const int32_t *n_contrib, vsx_loss_desc loss,
+                                   float *grad_splat, vsx_stream s) {
+  VSX_REQUIRE(cam.width > 0 && cam.height > 0 && rgb && alpha && depth && normal && raw_normal &&
+                  t_final && n_contrib && loss.gt_rgb && loss.counts,
+              "raster_bwd_loss: bad args");
+  BwdArgs a{rec, tile_offsets, tile_list, alpha, depth, raw_normal, t_final, nullptr, nullptr,
+            nullptr, nullptr, nullptr, n_contrib, grad_splat, rgb, normal, loss};
+  return launch_bwd(a, cam, as_stream(s));
 }

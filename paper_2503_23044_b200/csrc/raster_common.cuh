@@ -123,4 +123,54 @@ __device__ __forceinline__ PixCot pixel_cotangent(
   return c;
 }
 
+__device__ __forceinline__ float sgn(float d) { return d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f); }
+
+// Cotangents of the fused RGB-D-N objective (vsx_loss_desc) for one pixel,
+// chained through the finalize backward exactly like pixel_cotangent.
+__device__ __forceinline__ PixCot pixel_cotangent_loss(
+    const vsx_camera &cam, int px, int py, size_t p, const float *__restrict__ in_alpha,
+    const float *__restrict__ in_rgb, const float *__restrict__ in_depth,
+    const float *__restrict__ in_normal, const float *__restrict__ in_raw,
+    const vsx_loss_desc &L) {
+  PixCot c{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const float acc = in_alpha[p];
+  const float n0 = in_raw[3 * p + 0], n1 = in_raw[3 * p + 1], n2 = in_raw[3 * p + 2];
+  const PixRay ray = pixel_ray(cam, px, py);
+  const float den = denom_of(n0, n1, n2, ray);
+  const bool covered = acc >= kAlphaValidMin;
+  const bool valid = covered && fabsf(den) >= kDenomGuard;
+  c.gC0 = sgn(in_rgb[3 * p + 0] - L.gt_rgb[3 * p + 0]) * L.rgb_scale;
+  c.gC1 = sgn(in_rgb[3 * p + 1] - L.gt_rgb[3 * p + 1]) * L.rgb_scale;
+  c.gC2 = sgn(in_rgb[3 * p + 2] - L.gt_rgb[3 * p + 2]) * L.rgb_scale;
+  if (L.prior_depth && valid && L.prior_depth_valid[p]) {
+    const float depth = in_depth[p];
+    const float gd = sgn(depth - L.prior_depth[p]) * L.depth_weight /
+                     (float)max(L.counts[0], 1u);
+    c.gD = gd / den;
+    const float gden = -gd * depth / den;
+    c.gR0 += gden * ray.rx;
+    c.gR1 += gden * ray.ry;
+    c.gR2 += gden;
+  }
+  if (L.prior_normal && valid && L.prior_normal_valid[p]) {
+    const float sc = L.normal_weight / (float)max(L.counts[1], 1u);
+    const float gn0 = sgn(in_normal[3 * p + 0] - L.prior_normal[3 * p + 0]) * sc;
+    const float gn1 = sgn(in_normal[3 * p + 1] - L.prior_normal[3 * p + 1]) * sc;
+    const float gn2 = sgn(in_normal[3 * p + 2] - L.prior_normal[3 * p + 2]) * sc;
+    const float len = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
+    if (len >= 1e-12f) {
+      const float il = 1.f / len;
+      const float dot = (n0 * gn0 + n1 * gn1 + n2 * gn2) * il * il;
+      c.gR0 += (gn0 - n0 * dot) * il;
+      c.gR1 += (gn1 - n1 * dot) * il;
+      c.gR2 += (gn2 - n2 * dot) * il;
+    } else {
+      c.gR0 += gn0 * 1e12f;
+      c.gR1 += gn1 * 1e12f;
+      c.gR2 += gn2 * 1e12f;
+    }
+  }
+  return c;
+}
+
 }  // namespace vsx

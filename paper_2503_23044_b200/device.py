@@ -330,7 +330,8 @@ class Raster:
     n_contrib: torch.Tensor
 
 
-def raster_forward(P: Projected, B: Bins, view: CameraView) -> Raster:
+def raster_forward(P: Projected, B: Bins, view: CameraView, loss=None) -> Raster:
+    """K5; with a VsxLossDesc the fused objective's sums/counts are accumulated too."""
     H, W = view.height, view.width
     dev = "cuda"
     rgb = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
@@ -341,16 +342,28 @@ def raster_forward(P: Projected, B: Bins, view: CameraView) -> Raster:
     valid = torch.empty((H, W), dtype=torch.uint8, device=dev)
     tfin = torch.empty((H, W), dtype=torch.float32, device=dev)
     nc = torch.empty((H, W), dtype=torch.int32, device=dev)
-    call("vsx_raster_fwd", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list), view.to_abi(),
-         ptr(rgb), ptr(alpha), ptr(depth), ptr(normal), ptr(raw), ptr(valid), ptr(tfin), ptr(nc),
-         stream())
+    if loss is None:
+        call("vsx_raster_fwd", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list), view.to_abi(),
+             ptr(rgb), ptr(alpha), ptr(depth), ptr(normal), ptr(raw), ptr(valid), ptr(tfin),
+             ptr(nc), stream())
+    else:
+        call("vsx_raster_fwd_loss", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list),
+             view.to_abi(), ptr(rgb), ptr(alpha), ptr(depth), ptr(normal), ptr(raw), ptr(valid),
+             ptr(tfin), ptr(nc), loss, stream())
     return Raster(rgb, alpha, depth, normal, raw, valid, tfin, nc)
 
 
 def raster_backward(P: Projected, B: Bins, view: CameraView, R: Raster, g_rgb=None, g_alpha=None,
-                    g_depth=None, g_normal=None, g_raw=None, out: torch.Tensor | None = None):
+                    g_depth=None, g_normal=None, g_raw=None, out: torch.Tensor | None = None,
+                    loss=None):
+    """K6 from explicit pixel cotangents, or (loss=VsxLossDesc) from the fused objective."""
     grad = out if out is not None else torch.zeros((max(P.count, 1), GRAD_F32),
                                                    dtype=torch.float32, device="cuda")
+    if loss is not None:
+        call("vsx_raster_bwd_loss", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list),
+             view.to_abi(), ptr(R.rgb), ptr(R.alpha), ptr(R.depth), ptr(R.normal),
+             ptr(R.raw_normal), ptr(R.t_final), ptr(R.n_contrib), loss, ptr(grad), stream())
+        return grad[: P.count]
     call("vsx_raster_bwd", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list), view.to_abi(),
          ptr(R.rgb), ptr(R.alpha), ptr(R.depth), ptr(R.raw_normal), ptr(R.t_final),
          ptr(R.n_contrib), ptr(g_rgb), ptr(g_alpha), ptr(g_depth), ptr(g_normal), ptr(g_raw),

@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import device as D
-from ._lib import call, ptr, stream
+from ._lib import VsxLossDesc, call, ptr, stream
 from .decoder import AnchorState, DecoderParams, decoder_backward_into
 from .errors import InvalidInput, NumericalError
 from .geometry import CameraView
@@ -378,11 +378,10 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     st = state.flat
     st.grad.zero_()
     dev = "cuda"
-    rgb_acc = torch.zeros(B, dtype=torch.float64, device=dev)
-    dep_sum = torch.zeros(B, dtype=torch.float64, device=dev)
-    dep_cnt = torch.zeros(B, dtype=torch.int32, device=dev)
-    nrm_sum = torch.zeros(B, dtype=torch.float64, device=dev)
-    nrm_cnt = torch.zeros(B, dtype=torch.int32, device=dev)
+    sums = torch.zeros((B, 3), dtype=torch.float64, device=dev)     # rgb, depth, normal |d|
+    counts = torch.zeros((B, 2), dtype=torch.int32, device=dev)     # depth px, normal px
+    rgb_acc, dep_sum, nrm_sum = sums[:, 0], sums[:, 1], sums[:, 2]
+    dep_cnt, nrm_cnt = counts[:, 0], counts[:, 1]
     tile_max = torch.zeros(B, dtype=torch.int64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     gaussians = 0
@@ -404,37 +403,27 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             Bn = D.bin_tiles(P, W, H)
         isects += Bn.intersections
         tile_max[vi] = torch.diff(Bn.tile_offsets.long()).max()
+        # fused objective (K9 inside K5/K6): loss sums in the forward epilogue,
+        # cotangents formed on the fly in the backward
+        gt = _to_device_image(images[vi], (H, W, 3))
+        pd = pv = pn = pnv = None
+        if vi in have:
+            pd = _to_device_image(priors[vi][0], (H, W))
+            pv = _mask_u8(priors[vi][1], (H, W))
+        if vi in have_n:
+            pn = _to_device_image(normal_priors[vi][0], (H, W, 3))
+            pnv = _mask_u8(normal_priors[vi][1], (H, W))
+        loss = VsxLossDesc(
+            gt_rgb=gt.data_ptr(), prior_depth=ptr(pd).value, prior_depth_valid=ptr(pv).value,
+            prior_normal=ptr(pn).value, prior_normal_valid=ptr(pnv).value,
+            rgb_scale=1.0 / (B * H * W * 3),
+            depth_weight=(w2 / len(have)) if vi in have else 0.0,
+            normal_weight=(wn / len(have_n) / 3.0) if vi in have_n else 0.0,
+            sums=sums[vi].data_ptr(), counts=counts[vi].data_ptr())
         with _span(timer, "raster_fwd"):
-            R = D.raster_forward(P, Bn, view)
-        with _span(timer, "loss"):
-            gt = _to_device_image(images[vi], (H, W, 3))
-            g_rgb = torch.empty_like(R.rgb)
-            call("vsx_l1_loss", ptr(R.rgb), ptr(gt), R.rgb.numel(), 1.0 / (B * H * W * 3),
-                 ptr(rgb_acc[vi:vi + 1]), ptr(g_rgb), stream())
-            g_depth = g_normal = None
-            if vi in have:
-                pd = _to_device_image(priors[vi][0], (H, W))
-                pv = _mask_u8(priors[vi][1], (H, W))
-                call("vsx_depth_loss", ptr(R.depth), ptr(R.valid), ptr(pd), ptr(pv), H * W,
-                     ptr(dep_sum[vi:vi + 1]), ptr(dep_cnt[vi:vi + 1]), ptr(None), ptr(None),
-                     stream())
-                scale = (w2 / len(have)) / dep_cnt[vi:vi + 1].clamp_min(1).float()
-                g_depth = torch.empty_like(R.depth)
-                call("vsx_depth_loss", ptr(R.depth), ptr(R.valid), ptr(pd), ptr(pv), H * W,
-                     ptr(None), ptr(None), ptr(scale), ptr(g_depth), stream())
-            if vi in have_n:
-                pn = _to_device_image(normal_priors[vi][0], (H, W, 3))
-                pnv = _mask_u8(normal_priors[vi][1], (H, W))
-                call("vsx_masked_l1", ptr(R.normal), ptr(R.valid), ptr(pn), ptr(pnv), H * W, 3,
-                     ptr(nrm_sum[vi:vi + 1]), ptr(nrm_cnt[vi:vi + 1]), ptr(None), ptr(None),
-                     stream())
-                nscale = (wn / len(have_n) / 3.0) / nrm_cnt[vi:vi + 1].clamp_min(1).float()
-                g_normal = torch.empty_like(R.normal)
-                call("vsx_masked_l1", ptr(R.normal), ptr(R.valid), ptr(pn), ptr(pnv), H * W, 3,
-                     ptr(None), ptr(None), ptr(nscale), ptr(g_normal), stream())
+            R = D.raster_forward(P, Bn, view, loss=loss)
         with _span(timer, "raster_bwd"):
-            gs = D.raster_backward(P, Bn, view, R, g_rgb=g_rgb, g_depth=g_depth,
-                                   g_normal=g_normal)
+            gs = D.raster_backward(P, Bn, view, R, loss=loss)
         with _span(timer, "project_bwd"):
             gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P, gs, view)
         with _span(timer, "decode_bwd"):
