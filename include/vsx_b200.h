@@ -109,6 +109,12 @@ int vsx_sort_pairs_u64(const uint64_t *keys_in, const uint32_t *vals_in, uint64_
 int vsx_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                        uint32_t *vals_out, int64_t n, int32_t begin_bit, int32_t end_bit,
                        int32_t flags, void *ws, size_t ws_bytes, vsx_stream s);
+/* order = np.lexsort((gid, z)) for positive float64 z (renderer.py:197), used
+ * by a renderer rank to merge splat segments received from several owners:
+ * stable radix sort on the z bits, then runs of equal z reordered by gid. */
+size_t vsx_sort_z_gid_ws_bytes(int64_t n);
+int vsx_sort_z_gid(const double *z, const int64_t *gid, uint32_t *order, int64_t n, void *ws,
+                   size_t ws_bytes, vsx_stream s);
 /* Ordered stream compaction: out_idx = flatnonzero(flags), *out_count on device. */
 int vsx_select(const uint8_t *flags, int64_t n, int32_t *out_idx, uint32_t *out_count,
                void *ws, size_t ws_bytes, vsx_stream s);

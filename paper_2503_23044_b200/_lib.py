@@ -54,6 +54,8 @@ _SIGS = {
     "vsx_sort_pairs_u64": ([P, P, P, P, c_i64, c_i32, c_i32, c_i32, P, c_size, P], c_i32),
     "vsx_sort_pairs_u32": ([P, P, P, P, c_i64, c_i32, c_i32, c_i32, P, c_size, P], c_i32),
     "vsx_tile_ranges": ([P, c_i64, c_i32, P, P], c_i32),
+    "vsx_sort_z_gid_ws_bytes": ([c_i64], c_size),
+    "vsx_sort_z_gid": ([P, P, P, c_i64, P, c_size, P], c_i32),
     "vsx_select": ([P, c_i64, P, P, P, c_size, P], c_i32),
     "vsx_cull": ([P, P, c_i64, c_i32, c_f64, c_i32, VsxCamera, P, P], c_i32),
     "vsx_decode_fwd": ([VsxDecoder, P, c_i32, P, P, P, P, VsxCamera, c_f64, c_f64,

@@ -350,9 +350,60 @@ static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout
   return VSX_OK;
 }
 
+__global__ void iota_kernel(uint32_t *__restrict__ v, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (uint32_t)i;
+}
+
+// After a stable sort by z, runs of equal z keep input order; reorder each
+// run by gid so the result is lexsort((gid, z)) (renderer.py:197). Runs are
+// almost always length 1, so one thread per run start suffices.
+__global__ void fix_ties_kernel(const uint64_t *__restrict__ keys, const int64_t *__restrict__ gid,
+                                uint32_t *__restrict__ order, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || (i > 0 && keys[i] == keys[i - 1])) return;
+  int64_t j = i + 1;
+  while (j < n && keys[j] == keys[i]) ++j;
+  for (int64_t a = i + 1; a < j; ++a) {
+    const uint32_t o = order[a];
+    const int64_t g = gid[o];
+    int64_t b = a - 1;
+    while (b >= i && gid[order[b]] > g) {
+      order[b + 1] = order[b];
+      --b;
+    }
+    order[b + 1] = o;
+  }
+}
+
 }  // namespace vsx
 
 using namespace vsx;
+
+extern "C" int vsx_sort_z_gid(const double *z, const int64_t *gid, uint32_t *order, int64_t n,
+                              void *ws, size_t ws_bytes, vsx_stream s) {
+  cudaStream_t st = as_stream(s);
+  if (n <= 0) return VSX_OK;
+  const size_t extra = align256(sizeof(uint64_t) * n) + align256(sizeof(uint32_t) * n);
+  VSX_REQUIRE(ws_bytes >= extra + sort_ws_bytes(n), "sort_z_gid: workspace too small");
+  char *p = static_cast<char *>(ws);
+  uint64_t *keys_out = reinterpret_cast<uint64_t *>(p);
+  p += align256(sizeof(uint64_t) * n);
+  uint32_t *iota = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * n);
+  iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(iota, n);
+  VSX_LAUNCH_CHECK("iota");
+  int rc = sort_pairs<uint64_t>(reinterpret_cast<const uint64_t *>(z), iota, keys_out, order, n,
+                                0, 64, VSX_SORT_SKIP_CONSTANT, p, ws_bytes - extra, st);
+  if (rc) return rc;
+  fix_ties_kernel<<<grid_for(n, 256), 256, 0, st>>>(keys_out, gid, order, n);
+  VSX_LAUNCH_CHECK("fix_ties");
+  return VSX_OK;
+}
+
+extern "C" size_t vsx_sort_z_gid_ws_bytes(int64_t n) {
+  return align256(sizeof(uint64_t) * n) + align256(sizeof(uint32_t) * n) + sort_ws_bytes(n);
+}
 
 extern "C" size_t vsx_scan_ws_bytes(int64_t n) { return sizeof(uint32_t) * (scan_ws_elems(n) + 1); }
 

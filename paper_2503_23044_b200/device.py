@@ -90,6 +90,19 @@ def sort_pairs_u32(keys: torch.Tensor, vals: torch.Tensor, n: int, bits: int,
     return ko, vo
 
 
+def sort_z_gid(z: torch.Tensor, gid: torch.Tensor) -> torch.Tensor:
+    """Permutation = lexsort((gid, z)) of positive float64 z (int64 on device)."""
+    n = int(z.numel())
+    order = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    if n == 0:
+        return order[:0].long()
+    lib = _lib.load()
+    wp, wb = workspace().get(lib.vsx_sort_z_gid_ws_bytes(n))
+    call("vsx_sort_z_gid", ptr(z.contiguous()), ptr(gid.contiguous()), ptr(order), n, wp, wb,
+         stream())
+    return order.long()
+
+
 def exclusive_scan(counts: torch.Tensor, n: int) -> torch.Tensor:
     out = torch.empty(n + 1, dtype=torch.int32, device="cuda")
     lib = _lib.load()

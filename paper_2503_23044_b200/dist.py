@@ -1,0 +1,313 @@
+"""Multi-GPU training step: anchors sharded by the paper's Eq. 3, splats exchanged.
+
+One process per GPU. Each rank owns the anchors with ``i mod M == rank`` per
+level (``partition.assign_voxels``, reference ``partition.py:43-52``) and, for
+EVERY view of the batch, culls/decodes/projects only those anchors. View ``v``
+is rendered by rank ``v mod M``. Per step:
+
+* **C1 forward** (``exchange_splats``): an all-to-all of the projected splat
+  payloads (64-byte record + float64 z, radius and int64 gid per splat) from
+  the owners to each view's renderer. The reference only accounts these bytes
+  (``renderer.py:452-477``); here they really move (NCCL over NVLink).
+* The renderer merges the segments, restores the exact reference order
+  ``lexsort((gid, z))`` (stable z sort + gid tie fix), bins, composites, and
+  back-propagates the fused loss to per-splat gradients (13 floats).
+* **C1 backward** (``return_grads``): the reverse all-to-all sends each owner
+  the gradients of its own splats, which then runs projection and decode
+  backward locally. Anchor gradients and their Adam stay owner-local.
+* **C2**: an all-reduce SUM of the decoder gradient (the reference sums over
+  all views and anchors in one autograd call, ``trainer.py:330``), then the
+  replicated decoder Adam keeps every replica bit-identical.
+
+The compute is behind a small backend interface so the routing is testable
+without GPUs: ``CudaShardBackend`` (below) drives the sm_100a kernels;
+``oracle.shard.OracleShardBackend`` (test infrastructure) drives the float64
+oracle, and ``tests/test_dist_gloo.py`` checks a 2-rank gloo run against the
+single-process oracle step.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .errors import ProtocolError
+
+
+@dataclass
+class SplatPayload:
+    """Projected splats of one (rank, view): rows aligned across the tensors."""
+
+    rec: torch.Tensor     # (n, R) record words (R = 16 float32 on CUDA)
+    z: torch.Tensor       # (n,) float64 camera depth (sort key)
+    radius: torch.Tensor  # (n,) float64 3-sigma radius (binning)
+    gid: torch.Tensor     # (n,) int64 global gaussian id (tie break)
+
+    @property
+    def count(self) -> int:
+        return int(self.z.shape[0])
+
+    @staticmethod
+    def cat(parts: list["SplatPayload"], like: "SplatPayload") -> "SplatPayload":
+        if not parts:
+            return SplatPayload(like.rec[:0], like.z[:0], like.radius[:0], like.gid[:0])
+        return SplatPayload(torch.cat([p.rec for p in parts]), torch.cat([p.z for p in parts]),
+                            torch.cat([p.radius for p in parts]),
+                            torch.cat([p.gid for p in parts]))
+
+
+def renderer_of(view_index: int, world: int) -> int:
+    return view_index % world
+
+
+def _a2a(x: torch.Tensor, in_splits: list[int], out_splits: list[int], group=None):
+    out = torch.empty((sum(out_splits),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    dist.all_to_all_single(out, x.contiguous(), out_splits, in_splits, group=group)
+    return out
+
+
+@dataclass
+class ExchangePlan:
+    """Per-(source rank, view) row counts of one step's C1 exchange."""
+
+    counts: np.ndarray        # (world, B): rows rank q contributes to view v
+    rank: int
+    world: int
+
+    def views_of(self, r: int) -> list[int]:
+        return [v for v in range(self.counts.shape[1]) if renderer_of(v, self.world) == r]
+
+    def send_splits(self) -> list[int]:
+        return [int(self.counts[self.rank, self.views_of(r)].sum()) for r in range(self.world)]
+
+    def recv_splits(self) -> list[int]:
+        mine = self.views_of(self.rank)
+        return [int(self.counts[q, mine].sum()) for q in range(self.world)]
+
+
+def exchange_splats(payloads: list[SplatPayload], rank: int, world: int, group=None):
+    """C1 forward: route every view's payload rows to its renderer rank.
+
+    Returns (plan, merged) where merged[v] (for the views this rank renders)
+    is the concatenation of all ranks' rows in source-rank order, plus the
+    per-source row offsets inside it.
+    """
+    B = len(payloads)
+    dev = payloads[0].z.device
+    mine_counts = torch.tensor([p.count for p in payloads], dtype=torch.int64, device=dev)
+    gathered = [torch.zeros_like(mine_counts) for _ in range(world)]
+    dist.all_gather(gathered, mine_counts, group=group)
+    plan = ExchangePlan(torch.stack(gathered).cpu().numpy(), rank, world)
+    send_parts = [payloads[v] for r in range(world) for v in plan.views_of(r)]
+    send = SplatPayload.cat(send_parts, payloads[0])
+    ins, outs = plan.send_splits(), plan.recv_splits()
+    recv = SplatPayload(_a2a(send.rec, ins, outs, group), _a2a(send.z, ins, outs, group),
+                        _a2a(send.radius, ins, outs, group), _a2a(send.gid, ins, outs, group))
+    # split the received block per (source, view) and regroup per view
+    mine = plan.views_of(rank)
+    merged: dict[int, tuple[SplatPayload, list[int]]] = {}
+    pieces: dict[int, list[SplatPayload]] = {v: [] for v in mine}
+    off = 0
+    for q in range(world):
+        for v in mine:
+            c = int(plan.counts[q, v])
+            pieces[v].append(SplatPayload(recv.rec[off:off + c], recv.z[off:off + c],
+                                          recv.radius[off:off + c], recv.gid[off:off + c]))
+            off += c
+    for v in mine:
+        seg = [0] + list(np.cumsum([int(plan.counts[q, v]) for q in range(world)]))
+        merged[v] = (SplatPayload.cat(pieces[v], payloads[0]), seg)
+    return plan, merged
+
+
+def return_grads(plan: ExchangePlan, grads: dict[int, torch.Tensor], like: torch.Tensor,
+                 group=None) -> list[torch.Tensor]:
+    """C1 backward: send each source its rows' gradients; returns per-view grads
+    aligned with this rank's own payloads."""
+    rank, world = plan.rank, plan.world
+    mine = plan.views_of(rank)
+    blocks = []
+    for q in range(world):
+        for v in mine:
+            g = grads[v]
+            seg = np.concatenate([[0], np.cumsum(plan.counts[:, v])])
+            blocks.append(g[int(seg[q]):int(seg[q + 1])])
+    send = torch.cat(blocks) if blocks else like[:0]
+    recv = _a2a(send, plan.recv_splits(), plan.send_splits(), group)
+    out: list[torch.Tensor | None] = [None] * plan.counts.shape[1]
+    off = 0
+    for r in range(world):
+        for v in plan.views_of(r):
+            c = int(plan.counts[rank, v])
+            out[v] = recv[off:off + c]
+            off += c
+    return out
+
+
+def sharded_train_step(backend, views, images, priors=None, normal_priors=None, group=None):
+    """One sharded step; returns the global loss terms (same on every rank)."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    B = len(views)
+    backend.begin_step(views)
+    payloads = [backend.forward_shard(v, views[v]) for v in range(B)]
+    plan, merged = exchange_splats(payloads, rank, world, group)
+    grads = {}
+    for v, (payload, seg) in merged.items():
+        grads[v] = backend.render(v, views[v], payload, images[v],
+                                  None if priors is None else priors[v],
+                                  None if normal_priors is None else normal_priors[v])
+    back = return_grads(plan, grads, backend.grad_like(), group)
+    for v in range(B):
+        backend.backward_shard(v, views[v], back[v])
+    dist.all_reduce(backend.decoder_grad(), op=dist.ReduceOp.SUM, group=group)
+    losses = backend.loss_terms()              # (B, 5): rgb, depth, normal sums; counts
+    dist.all_reduce(losses, op=dist.ReduceOp.SUM, group=group)
+    report = backend.finish_step(losses)
+    check_replicas(backend.decoder_checksum(), group)
+    return report
+
+
+def check_replicas(checksum: torch.Tensor, group=None) -> None:
+    """Decoder replicas must stay bit-identical (reference trainer.py:204-207)."""
+    lo, hi = checksum.clone(), checksum.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    if not torch.equal(lo, hi):
+        raise ProtocolError("decoder replicas diverged across ranks")
+
+
+# ------------------------------------------------------------------ CUDA backend
+
+class CudaShardBackend:
+    """Drives the sm_100a kernels for one rank of the sharded step."""
+
+    def __init__(self, state, rank: int, world: int):
+        from . import device as D
+        self.D = D
+        self.state = state
+        self.rank, self.world = rank, world
+        owner = torch.as_tensor(state.assignment.flat_owner() if world == state.cfg.workers
+                                else np.concatenate([np.arange(lv.count) % world
+                                                     for lv in state.scene.levels]))
+        self.owned = (owner == rank).to(torch.uint8).cuda()
+        self.work: dict = {}
+        self.timer = None     # optional trainer.GpuTimer for per-kernel spans
+        self.isects = 0
+
+    def begin_step(self, views) -> None:
+        st = self.state
+        st.flat.grad.zero_()
+        B = len(views)
+        self.B = B
+        self._hw = np.array([v.height * v.width * 3 for v in views], dtype=np.float64)
+        self.sums = torch.zeros((B, 3), dtype=torch.float64, device="cuda")
+        self.counts = torch.zeros((B, 2), dtype=torch.int32, device="cuda")
+        self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.work.clear()
+        self.gaussians = 0
+        self.isects = 0
+
+    def grad_like(self) -> torch.Tensor:
+        return torch.zeros((0, self.D.GRAD_F32), dtype=torch.float32, device="cuda")
+
+    def forward_shard(self, v: int, view) -> SplatPayload:
+        D, st = self.D, self.state
+        ds = st.dscene
+        mask = ds.cull(view)
+        active = D.select(mask & self.owned)
+        an = st.anchors
+        dec = D.decode(st.params.abi(), st.n, active, ds.centers, an.emb, an.log_scales,
+                       an.offsets, view, ds.lod_ref, ds.max_scale, self.status, keep_cache=True)
+        self.gaussians += dec.count
+        P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, view,
+                      self.status)
+        src = P.src.long()
+        gid = active.long()[src // st.n] * st.n + src % st.n
+        self.work[v] = (active, dec, P)
+        return SplatPayload(P.rec, P.zkey.view(torch.float64), P.radius, gid)
+
+    def render(self, v: int, view, payload: SplatPayload, image, prior, nprior) -> torch.Tensor:
+        from ._lib import VsxLossDesc, ptr
+        D, st = self.D, self.state
+        from .trainer import _mask_u8, _prior_arrays, _to_device_image, weight_schedule
+        n = payload.count
+        H, W = view.height, view.width
+        order = D.sort_z_gid(payload.z, payload.gid)
+        P = D.Projected(payload.rec[order].contiguous(), payload.radius[order].contiguous(),
+                        payload.z[order].view(torch.int64), order.int(), n)
+        Bn = D.bin_tiles(P, W, H)
+        w2, _ = weight_schedule(st.step, st.cfg)
+        wn = float(getattr(st.cfg, "normal_weight", 0.0))
+        gt = _to_device_image(image, (H, W, 3))
+        pd = pv = pn = pnv = None
+        if prior is not None and w2 > 0:
+            d_, m_ = _prior_arrays(prior)
+            pd, pv = _to_device_image(d_, (H, W)), _mask_u8(m_, (H, W))
+        if nprior is not None and wn > 0:
+            pn, pnv = _to_device_image(nprior[0], (H, W, 3)), _mask_u8(nprior[1], (H, W))
+        # every view carries the same kind of priors in the bench; the global
+        # per-term normaliser is the batch size (reference losses.py:84)
+        loss = VsxLossDesc(gt_rgb=gt.data_ptr(), prior_depth=ptr(pd).value,
+                           prior_depth_valid=ptr(pv).value, prior_normal=ptr(pn).value,
+                           prior_normal_valid=ptr(pnv).value, rgb_scale=1.0 / (self.B * H * W * 3),
+                           depth_weight=w2 / self.B if pd is not None else 0.0,
+                           normal_weight=wn / self.B / 3.0 if pn is not None else 0.0,
+                           sums=self.sums[v].data_ptr(), counts=self.counts[v].data_ptr())
+        from .trainer import _span
+        self.isects += Bn.intersections
+        with _span(self.timer, "raster_fwd"):
+            R = D.raster_forward(P, Bn, view, loss=loss)
+        with _span(self.timer, "raster_bwd"):
+            gs = D.raster_backward(P, Bn, view, R, loss=loss)
+        merged = torch.empty_like(gs)
+        merged[order] = gs
+        return merged
+
+    def backward_shard(self, v: int, view, grads: torch.Tensor) -> None:
+        from .decoder import decoder_backward_into
+        D, st = self.D, self.state
+        ds = st.dscene
+        active, dec, P = self.work[v]
+        gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P,
+                                grads.contiguous(), view)
+        an, ag = st.anchors, st.anchor_grads
+        decoder_backward_into(st.params, st.dgrads, active, ds.centers, an.emb, an.log_scales,
+                              an.offsets, view, ds.lod_ref, ds.max_scale, dec, gg["means"],
+                              gg["opacities"], gg["colors"], gg["scales"], gg["quats"],
+                              gg["normals"], ag.emb, ag.log_scales, ag.offsets)
+
+    def decoder_grad(self) -> torch.Tensor:
+        st = self.state
+        lo, hi = st.flat.group_spans["dec"]
+        return st.flat.grad[lo:hi]
+
+    def loss_terms(self) -> torch.Tensor:
+        return torch.cat([self.sums, self.counts.double()], dim=1)
+
+    def finish_step(self, losses: torch.Tensor) -> dict:
+        from .errors import NumericalError
+        from .trainer import weight_schedule
+        st = self.state
+        self.D.check_status(self.status, "sharded train_step")
+        w2, _ = weight_schedule(st.step, st.cfg)
+        L = losses.cpu().numpy()
+        hw = self._hw
+        rgb = float(np.mean(L[:, 0] / hw))
+        dcnt, ncnt = L[:, 3], L[:, 4]
+        depth = float(np.mean(np.where(dcnt > 0, L[:, 1] / np.maximum(dcnt, 1), 0.0)))
+        normal = float(np.mean(np.where(ncnt > 0, L[:, 2] / (3 * np.maximum(ncnt, 1)), 0.0)))
+        total = rgb + w2 * depth + float(getattr(st.cfg, "normal_weight", 0.0)) * normal
+        if not np.isfinite(total):
+            raise NumericalError(f"non-finite loss at step {st.step}")
+        st.adam()
+        st.step += 1
+        return {"total": total, "rgb": rgb, "depth": depth, "normal": normal,
+                "gaussians": self.gaussians}
+
+    def decoder_checksum(self) -> torch.Tensor:
+        g = self.state.flat
+        lo, hi = g.group_spans["dec"]
+        return g.param[lo:hi].view(torch.int32).long().sum().reshape(1)

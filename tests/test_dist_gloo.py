@@ -1,0 +1,135 @@
+"""Multi-rank (gloo, CPU) tests of the sharded step's C1/C2 routing.
+
+* exchange round trip: every renderer receives exactly the rows of its views
+  from every owner, in source-rank order, and the reverse exchange returns
+  each owner the gradients of its own rows;
+* end to end: 2 gloo ranks running ``dist.sharded_train_step`` with the
+  float64 oracle backend reproduce the single-process oracle train step
+  (itself pinned to the reference) for the anchors each rank owns and for the
+  replicated decoder.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import golden_view, load_golden
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _init(rank, world, port):
+    dist.init_process_group("gloo", rank=rank, world_size=world,
+                            init_method=f"tcp://127.0.0.1:{port}")
+    torch.set_num_threads(1)
+
+
+def _exchange_worker(rank, world, port, out):
+    from paper_2503_23044_b200.dist import SplatPayload, exchange_splats, return_grads
+    _init(rank, world, port)
+    B = 5
+    rng = np.random.default_rng(rank)
+    payloads = []
+    for v in range(B):
+        n = int(rng.integers(0, 6)) if (v + rank) % 3 else 0
+        gid = torch.tensor([rank * 1000 + v * 100 + i for i in range(n)], dtype=torch.int64)
+        rec = gid.double().unsqueeze(-1).repeat(1, 4)
+        payloads.append(SplatPayload(rec, gid.double(), gid.double() * 2, gid))
+    plan, merged = exchange_splats(payloads, rank, world)
+    ok = True
+    grads = {}
+    for v, (p, seg) in merged.items():
+        expect = []
+        for q in range(world):
+            expect += [q * 1000 + v * 100 + i for i in range(int(plan.counts[q, v]))]
+        ok &= p.gid.tolist() == expect and len(seg) == world + 1 and seg[-1] == len(expect)
+        grads[v] = p.rec[:, :2] * -1.0
+    back = return_grads(plan, grads, torch.zeros((0, 2), dtype=torch.float64))
+    for v in range(B):
+        ok &= torch.equal(back[v], payloads[v].rec[:, :2] * -1.0)
+    torch.save({"ok": bool(ok)}, os.path.join(out, f"r{rank}.pt"))
+    dist.destroy_process_group()
+
+
+def test_exchange_round_trip_two_ranks():
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as out:
+        mp.spawn(_exchange_worker, args=(2, port, out), nprocs=2, join=True)
+        for r in range(2):
+            assert torch.load(os.path.join(out, f"r{r}.pt"))["ok"]
+
+
+def _small_state(d):
+    import oracle
+    K = int(d["lod_count"])
+    base = float(d["base_voxel"])
+    centers = np.concatenate([d[f"grid{k}"].astype(np.float64) * (base / 2.0 ** k)
+                              for k in range(K)])
+    levels = np.concatenate([np.full(d[f"grid{k}"].shape[0], k) for k in range(K)])
+    n = int(d["n"])
+    w = oracle.decoder_init(n, 0, float(np.log(0.125 * base)))
+    return oracle.OracleState.create(
+        centers, levels, K, float(d["lod_ref"]), int(d["lod_bias"]), base, n, w,
+        np.concatenate([d[f"emb{k}"] for k in range(K)]),
+        np.log(np.concatenate([d[f"scl{k}"] for k in range(K)])),
+        np.concatenate([d[f"off{k}"] for k in range(K)]), total_steps=8, step2_start=0,
+        step3_start=8)
+
+
+def _sharded_worker(rank, world, port, out):
+    from oracle.shard import OracleShardBackend
+    from paper_2503_23044_b200.dist import sharded_train_step
+    _init(rank, world, port)
+    d = load_golden("train_small")
+    views = [golden_view(d, f"v{i}", i) for i in range(3)]
+    images = [d[f"img{i}"] for i in range(3)]
+    priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
+    st = _small_state(d)
+    be = OracleShardBackend(st, rank, world)
+    reps = [sharded_train_step(be, views, images, priors) for _ in range(2)]
+    torch.save({"reps": reps, "owned": be.owned,
+                "weights": {k: v.numpy() for k, v in st.weights.items()},
+                "emb": st.emb.numpy(), "offsets": st.offsets.numpy(),
+                "log_scales": st.log_scales.numpy()}, os.path.join(out, f"r{rank}.pt"))
+    dist.destroy_process_group()
+
+
+@pytest.mark.slow
+def test_sharded_step_two_ranks_matches_single_process_oracle():
+    import oracle
+    port = _free_port()
+    d = load_golden("train_small")
+    views = [golden_view(d, f"v{i}", i) for i in range(3)]
+    images = [d[f"img{i}"] for i in range(3)]
+    priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
+    ref = _small_state(d)
+    cams = [oracle.Cam.of(v) for v in views]
+    ref_reps = [oracle.train_step(ref, cams, images, priors) for _ in range(2)]
+    with tempfile.TemporaryDirectory() as out:
+        mp.spawn(_sharded_worker, args=(2, port, out), nprocs=2, join=True)
+        res = [torch.load(os.path.join(out, f"r{r}.pt"), weights_only=False) for r in range(2)]
+    for r in res:
+        for s in range(2):
+            assert r["reps"][s]["rgb"] == pytest.approx(ref_reps[s]["rgb"], rel=1e-10)
+            assert r["reps"][s]["depth"] == pytest.approx(ref_reps[s]["depth"], rel=1e-9)
+        for k, w in r["weights"].items():
+            np.testing.assert_allclose(w, ref.weights[k].numpy(), rtol=1e-9, atol=1e-13)
+        own = r["owned"]
+        for name in ("emb", "offsets", "log_scales"):
+            np.testing.assert_allclose(r[name][own], getattr(ref, name).numpy()[own],
+                                       rtol=1e-9, atol=1e-13)
+    assert np.array_equal(res[0]["owned"], ~res[1]["owned"])

@@ -1,0 +1,59 @@
+"""The sharded (C1/C2) CUDA path on one GPU: a world-size-1 NCCL group runs the
+same exchange code paths (all-to-all, merge + lexsort((gid, z)), reverse
+all-to-all, decoder all-reduce) and must reproduce ``train_step``."""
+
+from __future__ import annotations
+
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+from conftest import golden_scene, golden_view
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl_world1():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{port}")
+    yield
+    dist.destroy_process_group()
+
+
+def test_sort_z_gid_is_lexsort():
+    from paper_2503_23044_b200 import device as D
+    rng = np.random.default_rng(0)
+    z = np.round(rng.uniform(1, 2, 50000), 3)           # many exact ties
+    gid = rng.permutation(50000).astype(np.int64)
+    order = D.sort_z_gid(torch.as_tensor(z).cuda(), torch.as_tensor(gid).cuda()).cpu().numpy()
+    np.testing.assert_array_equal(order, np.lexsort((gid, z)))
+
+
+def test_sharded_step_world1_matches_train_step(nccl_world1, train_small):
+    from paper_2503_23044_b200.dist import CudaShardBackend, sharded_train_step
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step
+    d = train_small
+    views = [golden_view(d, f"v{i}", i) for i in range(3)]
+    images = [d[f"img{i}"] for i in range(3)]
+    priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
+    cfg = dict(total_steps=8, batch_size=3, step2_start=0, step3_start=8, growth_stop=0)
+    a = TrainState(golden_scene(d), TrainConfig(**cfg))
+    b = TrainState(golden_scene(d), TrainConfig(**cfg))
+    be = CudaShardBackend(b, 0, 1)
+    for _ in range(2):
+        ra = train_step(a, views, images, priors)
+        rb = sharded_train_step(be, views, images, priors)
+        assert rb["rgb"] == pytest.approx(ra.rgb, rel=1e-6)
+        assert rb["depth"] == pytest.approx(ra.depth, rel=1e-5)
+    pa, pb = a.flat.param.cpu().numpy(), b.flat.param.cpu().numpy()
+    bad = np.abs(pa - pb) > 1e-5 * np.maximum(np.abs(pa), np.abs(pb)) + 1e-7
+    assert bad.mean() < 1e-3, bad.sum()
