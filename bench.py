@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--config", choices=["cfg2", "cfg1"], default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU sharded step even at one rank (testing)")
     ap.add_argument("--cpu-tiles", type=int, default=48,
                     help="tiles per CPU-baseline sample (evenly spaced over the view)")
     return ap.parse_args()
@@ -234,9 +236,13 @@ def raster_bytes(stage: str, isect: int, pixels: int, splats: int) -> int:
 def run_vsx(args):
     import torch
     world, rank, local = dist_env()
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         import torch.distributed as dist
         torch.cuda.set_device(local)
+        if "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0",
+                              WORLD_SIZE="1")
         dist.init_process_group("nccl")
     else:
         torch.cuda.set_device(0)
@@ -261,7 +267,7 @@ def run_vsx(args):
         imgs = [torch.as_tensor(np.asarray(im, np.float32)).cuda() for im in images]
         priors = nprior = None
     state = TrainState(scene, cfg)
-    if world > 1:
+    if sharded:
         from paper_2503_23044_b200.dist import CudaShardBackend, sharded_train_step
         backend = CudaShardBackend(state, rank, world)
 
@@ -371,7 +377,7 @@ def run_vsx(args):
                      "loss_depth": reps[-1]["depth"], "loss_normal": reps[-1]["normal"]},
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 
