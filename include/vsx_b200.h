@@ -127,9 +127,9 @@ int vsx_cull(const double *centers, const int32_t *level, int64_t n_anchors, int
 /* active: ascending flat anchor ids (n_active). Per-anchor params are flat
  * level-major: emb (A,32) f32, log_scale (A,3) f32 (l_v = exp in float64),
  * offsets (A,n,3) f32, centers (A,3) f64. Outputs are gaussian-major
- * (n_active*n rows). cache_h (n_active,192) and cache_o (n_active,11n) keep
- * the hidden activations and raw head outputs for vsx_decode_bwd (may be
- * NULL for inference). */
+ * (n_active*n rows). cache_h [192][ld] and cache_o [11n][ld] (feature-major,
+ * ld = n_active rounded up to a multiple of 4) keep the hidden activations
+ * and raw head outputs for vsx_decode_bwd (may be NULL for inference). */
 int vsx_decode_fwd(vsx_decoder W, const int32_t *active, int32_t n_active, const double *centers,
                    const float *emb, const float *log_scale, const float *offsets,
                    vsx_camera cam, double lod_ref, double max_scale, double *means,

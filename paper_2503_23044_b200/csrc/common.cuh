@@ -62,6 +62,12 @@ inline cudaStream_t as_stream(vsx_stream s) { return reinterpret_cast<cudaStream
 
 inline int grid_for(int64_t n, int block) { return (int)((n + block - 1) / block); }
 
+// Row stride of the feature-major decoder caches ([rows][ld], anchors along a
+// row): padded to 4 floats so rows are 16-byte aligned for vector loads.
+__host__ __device__ __forceinline__ size_t cache_ld(int64_t n_active) {
+  return (size_t)((n_active + 3) & ~int64_t(3));
+}
+
 // Explicitly rounded float64 ops: nvcc would otherwise contract a*b+c into an
 // FMA, which numpy/torch elementwise code never does. Decisions that must be
 // bit-exact against the reference (culling, projection keys, binning) use these.

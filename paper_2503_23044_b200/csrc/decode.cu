@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(128) decode_fwd_kernel(
   DecSmem s = dec_smem_carve(smem, n);
   dec_load_weights(W, s);
   const float smax = (float)max_scale, smin = (float)kMinScale;
+  const size_t ld = cache_ld(n_active);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_active; r += gridDim.x * blockDim.x) {
     const int a = active[r];
     float x[kInDim];
@@ -141,11 +142,11 @@ __global__ void __launch_bounds__(128) decode_fwd_kernel(
 #pragma unroll
     for (int k = 0; k < 64; ++k) {
       hid[k] = tanhf(hid[k]);
-      if (cache_h) cache_h[(size_t)k * n_active + r] = hid[k];
+      if (cache_h) cache_h[(size_t)k * ld + r] = hid[k];
     }
     for (int j = 0; j < n; ++j) {
       const float o = dec_out(s, j, hid);
-      if (cache_o) cache_o[(size_t)j * n_active + r] = o;
+      if (cache_o) cache_o[(size_t)j * ld + r] = o;
       const float op = sigmoidf_(o);
       bad |= !isfinite(op);
       opacity[(size_t)r * n + j] = op;
@@ -155,11 +156,11 @@ __global__ void __launch_bounds__(128) decode_fwd_kernel(
 #pragma unroll
     for (int k = 0; k < 64; ++k) {
       hid[k] = tanhf(hid[k]);
-      if (cache_h) cache_h[(size_t)(64 + k) * n_active + r] = hid[k];
+      if (cache_h) cache_h[(size_t)(64 + k) * ld + r] = hid[k];
     }
     for (int j = 0; j < 3 * n; ++j) {
       const float o = dec_out(s, n + j, hid);
-      if (cache_o) cache_o[(size_t)(n + j) * n_active + r] = o;
+      if (cache_o) cache_o[(size_t)(n + j) * ld + r] = o;
       const float c = sigmoidf_(o);
       bad |= !isfinite(c);
       color[(size_t)r * 3 * n + j] = c;
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(128) decode_fwd_kernel(
 #pragma unroll
     for (int k = 0; k < 64; ++k) {
       hid[k] = tanhf(hid[k]);
-      if (cache_h) cache_h[(size_t)(128 + k) * n_active + r] = hid[k];
+      if (cache_h) cache_h[(size_t)(128 + k) * ld + r] = hid[k];
     }
     const double l0 = exp((double)log_scale[3 * a + 0]);
     const double l1 = exp((double)log_scale[3 * a + 1]);
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(128) decode_fwd_kernel(
 #pragma unroll
       for (int c = 0; c < 7; ++c) {
         o[c] = dec_out(s, 4 * n + 7 * sl + c, hid);
-        if (cache_o) cache_o[(size_t)(4 * n + 7 * sl + c) * n_active + r] = o[c];
+        if (cache_o) cache_o[(size_t)(4 * n + 7 * sl + c) * ld + r] = o[c];
       }
       const size_t g = (size_t)r * n + sl;
       float sc[3];
@@ -254,13 +255,14 @@ __global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
   DecSmem s = dec_smem_carve(smem, n);
   dec_load_weights(W, s);
   const float smax = (float)max_scale, smin = (float)kMinScale;
+  const size_t ld = cache_ld(n_active);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_active; r += gridDim.x * blockDim.x) {
     const int a = active[r];
     float x[kInDim];
     dec_inputs(centers, emb, a, cam, lod_ref, x);
 #pragma unroll
-    for (int i = 0; i < kInDim; ++i) xs[(size_t)i * n_active + r] = x[i];
-    xs[(size_t)kInDim * n_active + r] = 1.0f;
+    for (int i = 0; i < kInDim; ++i) xs[(size_t)i * ld + r] = x[i];
+    xs[(size_t)kInDim * ld + r] = 1.0f;
     float gx[kInDim];
 #pragma unroll
     for (int i = 0; i < kInDim; ++i) gx[i] = 0.f;
@@ -274,11 +276,11 @@ __global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
       for (int k = 0; k < 64; ++k) gh[k] = 0.f;
       if (h < 2) {
         for (int j = 0; j < ow; ++j) {
-          const float o = cache_o[(size_t)(oo + j) * n_active + r];
+          const float o = cache_o[(size_t)(oo + j) * ld + r];
           const float sg = sigmoidf_(o);
           const float up = (h == 0) ? g_opacity[(size_t)r * n + j] : g_color[(size_t)r * 3 * n + j];
           const float go = up * sg * (1.f - sg);
-          g_o_out[(size_t)(oo + j) * n_active + r] = go;
+          g_o_out[(size_t)(oo + j) * ld + r] = go;
           const float4 *w = reinterpret_cast<const float4 *>(s.w2t + (oo + j) * 64);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
           const size_t g = (size_t)r * n + sl;
           float o[7], go[7];
 #pragma unroll
-          for (int c = 0; c < 7; ++c) o[c] = cache_o[(size_t)(oo + 7 * sl + c) * n_active + r];
+          for (int c = 0; c < 7; ++c) o[c] = cache_o[(size_t)(oo + 7 * sl + c) * ld + r];
           // scales: clamp(exp(o), 1e-6, max) — gradient passes inside [min, max]
           float sc[3];
 #pragma unroll
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
           }
 #pragma unroll
           for (int c = 0; c < 7; ++c) {
-            g_o_out[(size_t)(oo + 7 * sl + c) * n_active + r] = go[c];
+            g_o_out[(size_t)(oo + 7 * sl + c) * ld + r] = go[c];
             const float4 *w = reinterpret_cast<const float4 *>(s.w2t + (oo + 7 * sl + c) * 64);
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
@@ -354,9 +356,9 @@ __global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
       // tanh backward, input-block cotangent
 #pragma unroll
       for (int k = 0; k < 64; ++k) {
-        const float hv = cache_h[(size_t)(h * 64 + k) * n_active + r];
+        const float hv = cache_h[(size_t)(h * 64 + k) * ld + r];
         gh[k] *= (1.f - hv * hv);
-        g_pre_out[(size_t)(h * 64 + k) * n_active + r] = gh[k];
+        g_pre_out[(size_t)(h * 64 + k) * ld + r] = gh[k];
       }
 #pragma unroll
       for (int i = 0; i < kEmbed; ++i) {
@@ -398,7 +400,7 @@ constexpr int kWgK = 64;
 __global__ void __launch_bounds__(256) wgrad_kernel(const float *__restrict__ A, int a_rows,
                                                     bool ones_row, const float *__restrict__ B,
                                                     int b_rows, int64_t K, int64_t k_chunk,
-                                                    WgradOut o) {
+                                                    size_t ld, WgradOut o) {
   __shared__ float sa[kWgTile][kWgK + 1];
   __shared__ float sb[kWgTile][kWgK + 1];
   const int m0 = blockIdx.x * kWgTile, c0 = blockIdx.y * kWgTile;
@@ -415,9 +417,9 @@ __global__ void __launch_bounds__(256) wgrad_kernel(const float *__restrict__ A,
       const int m = m0 + rr, c = c0 + rr;
       float av = 0.f, bv = 0.f;
       if (gk < k_end) {
-        if (m < a_rows) av = A[(size_t)m * K + gk];
+        if (m < a_rows) av = A[(size_t)m * ld + gk];
         else if (m < m_total) av = 1.f;
-        if (c < b_rows) bv = B[(size_t)c * K + gk];
+        if (c < b_rows) bv = B[(size_t)c * ld + gk];
       }
       sa[rr][k] = av;
       sb[rr][k] = bv;
@@ -446,7 +448,7 @@ __global__ void __launch_bounds__(256) wgrad_kernel(const float *__restrict__ A,
 }
 
 static int launch_wgrad(const float *A, int a_rows, bool ones_row, const float *B, int b_rows,
-                        int64_t K, WgradOut o, cudaStream_t st) {
+                        int64_t K, size_t ld, WgradOut o, cudaStream_t st) {
   if (K == 0) return VSX_OK;
   const int gm = (a_rows + (ones_row ? 1 : 0) + kWgTile - 1) / kWgTile;
   const int gc = (b_rows + kWgTile - 1) / kWgTile;
@@ -455,13 +457,13 @@ static int launch_wgrad(const float *A, int a_rows, bool ones_row, const float *
   k_chunk = ((k_chunk + kWgK - 1) / kWgK) * kWgK;
   splits = (K + k_chunk - 1) / k_chunk;
   dim3 grid(gm, gc, (unsigned)splits);
-  wgrad_kernel<<<grid, 256, 0, st>>>(A, a_rows, ones_row, B, b_rows, K, k_chunk, o);
+  wgrad_kernel<<<grid, 256, 0, st>>>(A, a_rows, ones_row, B, b_rows, K, k_chunk, ld, o);
   VSX_LAUNCH_CHECK("wgrad");
   return VSX_OK;
 }
 
 int decoder_wgrad_tc(const float *g_o, const float *cache_h, const float *g_pre, const float *xs,
-                     int64_t K, int n, vsx_decoder_grads dW, cudaStream_t st);
+                     int64_t K, size_t ld, int n, vsx_decoder_grads dW, cudaStream_t st);
 
 }  // namespace vsx
 
@@ -495,7 +497,7 @@ extern "C" int vsx_decode_fwd(vsx_decoder W, const int32_t *active, int32_t n_ac
 }
 
 extern "C" size_t vsx_decode_bwd_ws_bytes(int32_t n, int32_t n_active) {
-  return sizeof(float) * (size_t)n_active * (size_t)(kInDim + 1 + 192 + 11 * n) + 256;
+  return sizeof(float) * cache_ld(n_active) * (size_t)(kInDim + 1 + 192 + 11 * n) + 256;
 }
 
 extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t *active,
@@ -512,9 +514,10 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
   VSX_REQUIRE(ws_bytes >= vsx_decode_bwd_ws_bytes(W.n, n_active), "decode_bwd: workspace");
   cudaStream_t st = as_stream(s);
   const int n = W.n;
+  const size_t ld = cache_ld(n_active);
   float *xs = static_cast<float *>(ws);
-  float *g_pre = xs + (size_t)(kInDim + 1) * n_active;
-  float *g_o = g_pre + (size_t)192 * n_active;
+  float *g_pre = xs + (size_t)(kInDim + 1) * ld;
+  float *g_o = g_pre + (size_t)192 * ld;
   const size_t smem = dec_smem_bytes(n);
   VSX_CUDA_TRY(cudaFuncSetAttribute(decode_bwd_anchor_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -528,7 +531,7 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
     return !(e && e[0] == '0');
   }();
   if (use_tc && 11 * n <= 128)  // tensor-core weight gradients (decode_tc.cu)
-    return decoder_wgrad_tc(g_o, cache_h, g_pre, xs, n_active, n, dW, st);
+    return decoder_wgrad_tc(g_o, cache_h, g_pre, xs, n_active, ld, n, dW, st);
   // dW1_h = X^T Gpre_h (+ db1 via the ones row of X)
   WgradOut o1{};
   for (int h = 0; h < 3; ++h) {
@@ -537,7 +540,7 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
   }
   o1.seg_w = 64;
   o1.ld_out = 64;
-  int rc = launch_wgrad(xs, kInDim, true, g_pre, 192, n_active, o1, st);
+  int rc = launch_wgrad(xs, kInDim, true, g_pre, 192, n_active, ld, o1, st);
   if (rc) return rc;
   // dW2_h = H_h^T Go_h (+ db2 via an implicit ones row)
   for (int h = 0; h < 3; ++h) {
@@ -547,8 +550,8 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
     o2.bias[0] = dW.b2[h];
     o2.seg_w = ow;
     o2.ld_out = ow;
-    rc = launch_wgrad(cache_h + (size_t)h * 64 * n_active, 64, true,
-                      g_o + (size_t)oo * n_active, ow, n_active, o2, st);
+    rc = launch_wgrad(cache_h + (size_t)h * 64 * ld, 64, true, g_o + (size_t)oo * ld, ow,
+                      n_active, ld, o2, st);
     if (rc) return rc;
   }
   return VSX_OK;

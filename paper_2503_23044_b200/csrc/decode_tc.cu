@@ -115,7 +115,10 @@ __device__ __forceinline__ void mma3(uint32_t d, const float *a_hi, const float 
   }
 }
 
-__global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
+// Two warpgroups (256 threads): both own TMEM lanes 0-127 (thread row =
+// tid % 128) and split every epilogue's columns / slots between them, which
+// halves the serial per-thread epilogue chains that bound this kernel.
+__global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
     vsx_decoder W, const float *__restrict__ img, const int32_t *__restrict__ active,
     int32_t n_active, const double *__restrict__ centers, const float *__restrict__ emb,
     const float *__restrict__ log_scale, const float *__restrict__ offsets, vsx_camera cam,
@@ -137,16 +140,16 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
   s.h_lo = s.h_hi + kTcRows * kTcK2;
   s.w2_hi = s.h_lo + kTcRows * kTcK2;
   s.w2_lo = s.w2_hi + dims.np_total * kTcK2;
-  const int t = threadIdx.x, warp = t >> 5;
+  const int tid = threadIdx.x, t = tid & 127, wg = tid >> 7, warp = (tid >> 5) & 3;
   // resident W2 image (hi and lo back to back, same as the global image)
   {
     const float4 *src = reinterpret_cast<const float4 *>(img + 3 * 2 * 64 * kTcK1);
     float4 *dst = reinterpret_cast<float4 *>(s.w2_hi);
     const int n4 = 2 * dims.np_total * kTcK2 / 4;
-    for (int i = t; i < n4; i += 128) dst[i] = src[i];
+    for (int i = tid; i < n4; i += 256) dst[i] = src[i];
   }
-  if (warp == 0) umma::tmem_alloc(&tslot, 256);
-  if (t == 0) umma::mbar_init(&mbar, 1);
+  if (tid < 32) umma::tmem_alloc(&tslot, 256);
+  if (tid == 0) umma::mbar_init(&mbar, 1);
   umma::fence_before_sync();
   __syncthreads();
   umma::fence_after_sync();
@@ -156,12 +159,13 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
   uint32_t phase = 0;
   const float smax = (float)max_scale, smin = (float)kMinScale;
   const int n_tiles = (n_active + kTcRows - 1) / kTcRows;
+  const size_t ld = cache_ld(n_active);
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int r = tile * kTcRows + t;
     const bool valid = r < n_active;
     const int a = valid ? active[r] : 0;
     // ---- input block (decoder.py:142-147) + bias column, split into X tiles
-    {
+    if (wg == 0) {
       float x[kTcK1];
 #pragma unroll
       for (int i = 0; i < kTcK1; ++i) x[i] = 0.f;
@@ -199,29 +203,29 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
       {
         const float4 *src = reinterpret_cast<const float4 *>(img + (size_t)h * 2 * 64 * kTcK1);
         float4 *dst = reinterpret_cast<float4 *>(s.w1_hi);
-        for (int i = t; i < 2 * 64 * kTcK1 / 4; i += 128) dst[i] = src[i];
+        for (int i = tid; i < 2 * 64 * kTcK1 / 4; i += 256) dst[i] = src[i];
       }
       umma::fence_async_smem();
       umma::fence_before_sync();
       __syncthreads();
       umma::fence_after_sync();
-      if (t == 0) {
+      if (tid == 0) {
         mma3(d1, s.x_hi, s.x_lo, s.w1_hi, s.w1_lo, kTcK1, umma::idesc_tf32(128, 64));
         umma::commit(&mbar);
       }
       umma::mbar_wait(&mbar, phase);
       phase ^= 1u;
       umma::fence_after_sync();
-      // hidden activations -> cache + H tiles
+      // hidden activations -> cache + H tiles (warpgroup wg: columns 32wg..32wg+31)
 #pragma unroll
-      for (int c = 0; c < 64; c += 16) {
+      for (int c = 32 * wg; c < 32 * wg + 32; c += 16) {
         float v[16];
         umma::tmem_ld16(d1 + lane + (uint32_t)c, v);
         umma::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           v[i] = tanhf(v[i]);
-          if (valid && cache_h) cache_h[(size_t)(h * 64 + c + i) * n_active + r] = v[i];
+          if (valid && cache_h) cache_h[(size_t)(h * 64 + c + i) * ld + r] = v[i];
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
       umma::fence_before_sync();
       __syncthreads();
       umma::fence_after_sync();
-      if (t == 0) {
+      if (tid == 0) {
         const int off = dims.row0[h] * kTcK2;  // row offset (multiple of 16 rows)
         mma3(d2, s.h_hi, s.h_lo, s.w2_hi + off, s.w2_lo + off, kTcK2,
              umma::idesc_tf32(128, dims.np[h]));
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
       const int width = (h == 0 ? 1 : (h == 1 ? 3 : 7)) * n;
       const int oo = h == 0 ? 0 : (h == 1 ? n : 4 * n);
       if (h < 2) {
-        for (int c = 0; c < dims.np[h]; c += 16) {
+        for (int c = 16 * wg; c < dims.np[h]; c += 32) {
           float v[16];
           umma::tmem_ld16(d2 + lane + (uint32_t)c, v);
           umma::tmem_ld_wait();
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
             const int j = c + i;
             if (valid && j < width) {
               const float o = v[i] + W.b2[h][j];
-              if (cache_o) cache_o[(size_t)(oo + j) * n_active + r] = o;
+              if (cache_o) cache_o[(size_t)(oo + j) * ld + r] = o;
               const float sg = sigm(o);
               bad |= !isfinite(sg);
               if (h == 0) opacity[(size_t)r * n + j] = sg;
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
           }
         }
       } else {
-        for (int sl = 0; sl < n; ++sl) {
+        for (int sl = wg; sl < n; sl += 2) {
           float o[16];
           umma::tmem_ld16(d2 + lane + (uint32_t)(7 * sl), o);  // columns 7sl .. 7sl+15
           umma::tmem_ld_wait();
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
 #pragma unroll
           for (int c = 0; c < 7; ++c) {
             o[c] += W.b2[2][7 * sl + c];
-            if (cache_o) cache_o[(size_t)(oo + 7 * sl + c) * n_active + r] = o[c];
+            if (cache_o) cache_o[(size_t)(oo + 7 * sl + c) * ld + r] = o[c];
           }
           const size_t g = (size_t)r * n + sl;
           float sc[3];
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(128, 1) decode_fwd_tc_kernel(
   }
   umma::fence_before_sync();
   __syncthreads();
-  if (warp == 0) umma::tmem_dealloc(tbase, 256);
+  if (tid < 32) umma::tmem_dealloc(tbase, 256);
 }
 
 // ---------------------------------------------------------------- weight gradients
@@ -345,16 +349,24 @@ inline size_t wg_smem_bytes() {
 // read `ones_row` (1.0 when == that row index) or zero.
 __device__ __forceinline__ void wg_stage(float *hi, float *lo, const float *__restrict__ src,
                                          int rows, int rows_valid, int ones_row, int64_t K,
-                                         int64_t k0) {
+                                         size_t ld, int64_t k0) {
   const int quads = rows * (kWgKc / 4);
   for (int e = threadIdx.x; e < quads; e += blockDim.x) {
     const int r = e / (kWgKc / 4), q = e % (kWgKc / 4);
     const int64_t k = k0 + 4 * q;
     float v[4] = {0.f, 0.f, 0.f, 0.f};
     if (r < rows_valid) {
-      const float *p = src + (size_t)r * K + k;
+      const float *p = src + (size_t)r * ld + k;
+      if (k + 3 < K) {  // rows are 16-byte aligned (ld % 4 == 0)
+        const float4 f = __ldg(reinterpret_cast<const float4 *>(p));
+        v[0] = f.x;
+        v[1] = f.y;
+        v[2] = f.z;
+        v[3] = f.w;
+      } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = (k + i < K) ? p[i] : 0.f;
+        for (int i = 0; i < 4; ++i) v[i] = (k + i < K) ? p[i] : 0.f;
+      }
     } else if (r == ones_row) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) v[i] = (k + i < K) ? 1.f : 0.f;
@@ -365,7 +377,7 @@ __device__ __forceinline__ void wg_stage(float *hi, float *lo, const float *__re
 
 __global__ void __launch_bounds__(128, 1) decoder_wgrad_tc_kernel(
     const float *__restrict__ g_o, const float *__restrict__ cache_h,
-    const float *__restrict__ g_pre, const float *__restrict__ xs, int64_t K, int n,
+    const float *__restrict__ g_pre, const float *__restrict__ xs, int64_t K, size_t ld, int n,
     vsx_decoder_grads dW) {
   extern __shared__ __align__(1024) float wsm[];
   __shared__ uint64_t mbar;
@@ -393,10 +405,10 @@ __global__ void __launch_bounds__(128, 1) decoder_wgrad_tc_kernel(
   bool first = true;
   for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const int64_t k0 = ch * kWgKc;
-    wg_stage(s.a1_hi, s.a1_lo, g_o, 128, nout, -1, K, k0);
-    wg_stage(s.b1_hi, s.b1_lo, cache_h, kWgN1, 192, 192, K, k0);
-    wg_stage(s.a2_hi, s.a2_lo, g_pre, 256, 192, -1, K, k0);
-    wg_stage(s.b2_hi, s.b2_lo, xs, kWgN2, kInDim + 1, -1, K, k0);  // xs row 36 = ones
+    wg_stage(s.a1_hi, s.a1_lo, g_o, 128, nout, -1, K, ld, k0);
+    wg_stage(s.b1_hi, s.b1_lo, cache_h, kWgN1, 192, 192, K, ld, k0);
+    wg_stage(s.a2_hi, s.a2_lo, g_pre, 256, 192, -1, K, ld, k0);
+    wg_stage(s.b2_hi, s.b2_lo, xs, kWgN2, kInDim + 1, -1, K, ld, k0);  // xs row 36 = ones
     umma::fence_async_smem();
     umma::fence_before_sync();
     __syncthreads();
@@ -479,7 +491,7 @@ __global__ void __launch_bounds__(128, 1) decoder_wgrad_tc_kernel(
 }
 
 int decoder_wgrad_tc(const float *g_o, const float *cache_h, const float *g_pre, const float *xs,
-                     int64_t K, int n, vsx_decoder_grads dW, cudaStream_t st) {
+                     int64_t K, size_t ld, int n, vsx_decoder_grads dW, cudaStream_t st) {
   if (K == 0) return VSX_OK;
   const size_t smem = wg_smem_bytes();
   VSX_CUDA_TRY(cudaFuncSetAttribute(decoder_wgrad_tc_kernel,
@@ -489,7 +501,7 @@ int decoder_wgrad_tc(const float *g_o, const float *cache_h, const float *g_pre,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t chunks = (K + kWgKc - 1) / kWgKc;
   decoder_wgrad_tc_kernel<<<(int)std::min<int64_t>(chunks, sms), 128, smem, st>>>(
-      g_o, cache_h, g_pre, xs, K, n, dW);
+      g_o, cache_h, g_pre, xs, K, ld, n, dW);
   VSX_LAUNCH_CHECK("decoder_wgrad_tc");
   return VSX_OK;
 }
@@ -532,7 +544,7 @@ extern "C" int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = (n_active + kTcRows - 1) / kTcRows;
-  decode_fwd_tc_kernel<<<std::min(tiles, sms), 128, smem, as_stream(s)>>>(
+  decode_fwd_tc_kernel<<<std::min(tiles, sms), 256, smem, as_stream(s)>>>(
       W, img, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, max_scale, means,
       opacity, color, scale, quat, normal, cache_h, cache_o, status);
   VSX_LAUNCH_CHECK("decode_fwd_tc");

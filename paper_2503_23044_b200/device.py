@@ -202,8 +202,9 @@ def decode(dec_abi, n: int, active: torch.Tensor, centers: torch.Tensor, emb: to
     scl = torch.empty((g, 3), dtype=torch.float32, device=dev)
     quat = torch.empty((g, 4), dtype=torch.float32, device=dev)
     nrm = torch.empty((g, 3), dtype=torch.float32, device=dev)
-    ch = torch.empty((192, max(na, 1)), dtype=torch.float32, device=dev) if keep_cache else None
-    co = torch.empty((11 * n, max(na, 1)), dtype=torch.float32, device=dev) if keep_cache else None
+    ld = max((na + 3) // 4 * 4, 4)     # cache_ld() of common.cuh: 16-byte aligned rows
+    ch = torch.empty((192, ld), dtype=torch.float32, device=dev) if keep_cache else None
+    co = torch.empty((11 * n, ld), dtype=torch.float32, device=dev) if keep_cache else None
     if use_tensor_cores(n):
         img = decoder_image(dec_abi, n)
         call("vsx_decode_fwd_tc", dec_abi, ptr(img), ptr(active), na, ptr(centers), ptr(emb),
