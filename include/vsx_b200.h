@@ -109,6 +109,13 @@ int vsx_sort_pairs_u64(const uint64_t *keys_in, const uint32_t *vals_in, uint64_
 int vsx_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
                        uint32_t *vals_out, int64_t n, int32_t begin_bit, int32_t end_bit,
                        int32_t flags, void *ws, size_t ws_bytes, vsx_stream s);
+/* Stable order of projected splats by their float64 z keys (vsx_project_fwd
+ * zkey; UINT64_MAX = culled, sorted last) without sorting 64-bit keys: a
+ * 4-pass sort on a round-toward-zero float32 proxy, then runs of equal proxy
+ * re-sorted by the exact key (ties by index). No host synchronisation. */
+size_t vsx_sort_splats_ws_bytes(int64_t n);
+int vsx_sort_splats_z(const uint64_t *zkey, int64_t n, uint32_t *order, void *ws,
+                      size_t ws_bytes, vsx_stream s);
 /* order = np.lexsort((gid, z)) for positive float64 z (renderer.py:197), used
  * by a renderer rank to merge splat segments received from several owners:
  * stable radix sort on the z bits, then runs of equal z reordered by gid. */

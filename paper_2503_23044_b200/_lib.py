@@ -54,6 +54,8 @@ _SIGS = {
     "vsx_sort_pairs_u64": ([P, P, P, P, c_i64, c_i32, c_i32, c_i32, P, c_size, P], c_i32),
     "vsx_sort_pairs_u32": ([P, P, P, P, c_i64, c_i32, c_i32, c_i32, P, c_size, P], c_i32),
     "vsx_tile_ranges": ([P, c_i64, c_i32, P, P], c_i32),
+    "vsx_sort_splats_ws_bytes": ([c_i64], c_size),
+    "vsx_sort_splats_z": ([P, c_i64, P, P, c_size, P], c_i32),
     "vsx_sort_z_gid_ws_bytes": ([c_i64], c_size),
     "vsx_sort_z_gid": ([P, P, P, c_i64, P, c_size, P], c_i32),
     "vsx_select": ([P, c_i64, P, P, P, c_size, P], c_i32),

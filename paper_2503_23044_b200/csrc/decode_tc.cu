@@ -351,27 +351,38 @@ __device__ __forceinline__ void wg_stage(float *hi, float *lo, const float *__re
                                          int rows, int rows_valid, int ones_row, int64_t K,
                                          size_t ld, int64_t k0) {
   const int quads = rows * (kWgKc / 4);
-  for (int e = threadIdx.x; e < quads; e += blockDim.x) {
-    const int r = e / (kWgKc / 4), q = e % (kWgKc / 4);
-    const int64_t k = k0 + 4 * q;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (r < rows_valid) {
-      const float *p = src + (size_t)r * ld + k;
-      if (k + 3 < K) {  // rows are 16-byte aligned (ld % 4 == 0)
-        const float4 f = __ldg(reinterpret_cast<const float4 *>(p));
-        v[0] = f.x;
-        v[1] = f.y;
-        v[2] = f.z;
-        v[3] = f.w;
-      } else {
+  constexpr int kU = 8;  // float4 loads in flight per thread
+  for (int base = threadIdx.x; base < quads; base += kU * blockDim.x) {
+    float4 v[kU];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = (k + i < K) ? p[i] : 0.f;
+    for (int u = 0; u < kU; ++u) {
+      const int e = base + u * blockDim.x;
+      const int r = e / (kWgKc / 4), q = e % (kWgKc / 4);
+      const int64_t k = k0 + 4 * q;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < quads && r < rows_valid) {
+        const float *p = src + (size_t)r * ld + k;
+        if (k + 3 < K) {  // rows are 16-byte aligned (ld % 4 == 0)
+          v[u] = __ldg(reinterpret_cast<const float4 *>(p));
+        } else {
+          v[u].x = (k + 0 < K) ? p[0] : 0.f;
+          v[u].y = (k + 1 < K) ? p[1] : 0.f;
+          v[u].z = (k + 2 < K) ? p[2] : 0.f;
+          v[u].w = (k + 3 < K) ? p[3] : 0.f;
+        }
+      } else if (e < quads && r == ones_row) {
+        v[u] = make_float4(k < K ? 1.f : 0.f, k + 1 < K ? 1.f : 0.f, k + 2 < K ? 1.f : 0.f,
+                           k + 3 < K ? 1.f : 0.f);
       }
-    } else if (r == ones_row) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = (k + i < K) ? 1.f : 0.f;
     }
-    st_split4(hi, lo, umma::kmajor_offset(r, 4 * q, kWgKc), v[0], v[1], v[2], v[3]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = base + u * blockDim.x;
+      if (e < quads) {
+        const int r = e / (kWgKc / 4), q = e % (kWgKc / 4);
+        st_split4(hi, lo, umma::kmajor_offset(r, 4 * q, kWgKc), v[u].x, v[u].y, v[u].z, v[u].w);
+      }
+    }
   }
 }
 

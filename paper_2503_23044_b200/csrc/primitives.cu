@@ -376,9 +376,68 @@ __global__ void fix_ties_kernel(const uint64_t *__restrict__ keys, const int64_t
   }
 }
 
+// 32-bit monotone proxy of a positive float64 z: round toward zero to float32
+// (order-preserving, never reverses two keys); ~0 marks culled entries.
+__global__ void z_proxy_kernel(const uint64_t *__restrict__ zkey, int64_t n,
+                               uint32_t *__restrict__ k32) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = zkey[i];
+  k32[i] = (k == ~0ull) ? 0xFFFFFFFFu : __float_as_uint(__double2float_rz(__longlong_as_double((long long)k)));
+}
+
+// Runs of equal 32-bit proxies (float32 collisions) are re-sorted by the exact
+// float64 key, ties by index: the final order is the stable float64 order.
+__global__ void fix_proxy_runs_kernel(const uint32_t *__restrict__ k32,
+                                      const uint64_t *__restrict__ zkey,
+                                      uint32_t *__restrict__ order, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || (i > 0 && k32[i] == k32[i - 1])) return;
+  int64_t j = i + 1;
+  while (j < n && k32[j] == k32[i]) ++j;
+  for (int64_t a = i + 1; a < j; ++a) {
+    const uint32_t o = order[a];
+    const uint64_t z = zkey[o];
+    int64_t b = a - 1;
+    while (b >= i && (zkey[order[b]] > z || (zkey[order[b]] == z && order[b] > o))) {
+      order[b + 1] = order[b];
+      --b;
+    }
+    order[b + 1] = o;
+  }
+}
+
 }  // namespace vsx
 
 using namespace vsx;
+
+extern "C" size_t vsx_sort_splats_ws_bytes(int64_t n) {
+  return 2 * align256(sizeof(uint32_t) * n) + align256(sizeof(uint32_t) * n) + sort_ws_bytes(n);
+}
+
+extern "C" int vsx_sort_splats_z(const uint64_t *zkey, int64_t n, uint32_t *order, void *ws,
+                                 size_t ws_bytes, vsx_stream s) {
+  cudaStream_t st = as_stream(s);
+  if (n <= 0) return VSX_OK;
+  VSX_REQUIRE(ws_bytes >= vsx_sort_splats_ws_bytes(n), "sort_splats_z: workspace too small");
+  char *p = static_cast<char *>(ws);
+  uint32_t *k32 = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * n);
+  uint32_t *k32s = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * n);
+  uint32_t *iota = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * n);
+  z_proxy_kernel<<<grid_for(n, 256), 256, 0, st>>>(zkey, n, k32);
+  VSX_LAUNCH_CHECK("z_proxy");
+  iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(iota, n);
+  VSX_LAUNCH_CHECK("iota");
+  int rc = sort_pairs<uint32_t>(k32, iota, k32s, order, n, 0, 32, 0, p,
+                                ws_bytes - 3 * align256(sizeof(uint32_t) * n), st);
+  if (rc) return rc;
+  fix_proxy_runs_kernel<<<grid_for(n, 256), 256, 0, st>>>(k32s, zkey, order, n);
+  VSX_LAUNCH_CHECK("fix_proxy_runs");
+  return VSX_OK;
+}
 
 extern "C" int vsx_sort_z_gid(const double *z, const int64_t *gid, uint32_t *order, int64_t n,
                               void *ws, size_t ws_bytes, vsx_stream s) {

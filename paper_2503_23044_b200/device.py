@@ -281,13 +281,26 @@ def project(means, opacity, color, scale, quat, normal, view: CameraView,
     if g == 0:
         e = torch.empty(0, device="cuda")
         return Projected(rec[:0], rad[:0], key[:0], kept[:0], 0)
-    idx = torch.arange(g, dtype=torch.int32, device="cuda")
-    skey, order = sort_pairs_u64(key[:g], idx, g)
+    order = sort_splats_z(key[:g], g)
     n_kept = int(kept.item())
+    return gather_projected(rec, key, rad, order, n_kept)
+
+
+def sort_splats_z(key: torch.Tensor, g: int) -> torch.Tensor:
+    """Stable order by the float64 z bits (proxy sort + exact run fix-up, no sync)."""
+    order = torch.empty(max(g, 1), dtype=torch.int32, device="cuda")
+    lib = _lib.load()
+    wp, wb = workspace().get(lib.vsx_sort_splats_ws_bytes(g))
+    call("vsx_sort_splats_z", ptr(key), g, ptr(order), wp, wb, stream())
+    return order[:g]
+
+
+def gather_projected(rec, key, rad, order, n_kept: int) -> "Projected":
     rs = torch.empty((max(n_kept, 1), REC_F32), dtype=torch.float32, device="cuda")
     rr = torch.empty(max(n_kept, 1), dtype=torch.float64, device="cuda")
     call("vsx_gather_splats", ptr(rec), ptr(rad), ptr(order), n_kept, ptr(rs), ptr(rr), stream())
-    return Projected(rs[:n_kept], rr[:n_kept], skey[:n_kept], order[:n_kept], n_kept)
+    skey = key[order[:n_kept].long()]
+    return Projected(rs[:n_kept], rr[:n_kept], skey, order[:n_kept], n_kept)
 
 
 # ------------------------------------------------------------------ binning
