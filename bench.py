@@ -116,6 +116,66 @@ def teacher_targets(scene, views):
 
 # ------------------------------------------------------------------ clocks
 
+class NvmlClockSampler:
+    """SM clock + clock-event reasons sampled in-process (NVML) every 100 ms.
+
+    NVML is initialised at construction (before warm-up) so its start-up cost
+    never lands in the timed region; the sampling thread only runs while the
+    timed steps run. Falls back to ClockSampler (nvidia-smi) if NVML fails.
+    """
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
+               ("hw_power_brake_slowdown", 0x80))
+
+    def __init__(self, gpu: int):
+        import threading
+        import pynvml
+        import torch
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(gpu)
+        try:
+            self.h = pynvml.nvmlDeviceGetHandleByUUID("GPU-" + str(p.uuid))
+        except Exception:
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        self.rows: list[tuple[float, int]] = []
+        self.ev = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _sample(self):
+        nv = self.nv
+        self.rows.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                          int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+
+    def _run(self):
+        while True:
+            self._sample()
+            if self.ev.wait(0.1):
+                break
+
+    def start(self):
+        self.th.start()
+
+    def stop(self) -> dict:
+        self.ev.set()
+        self.th.join()
+        self._sample()
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for _, bits in self.rows for n, b in self.REASONS if bits & b})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "src": "nvml"}
+
+
+def clock_sampler(gpu: int):
+    try:
+        return NvmlClockSampler(gpu)
+    except Exception:
+        return ClockSampler(gpu)
+
+
 class ClockSampler:
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -280,12 +340,12 @@ def run_vsx(args):
             r = train_step(state, views, im, pr, normal_priors=npr, timer=timer)
             return {"gaussians": r.gaussians, "intersections": r.intersections, "total": r.total,
                     "rgb": r.rgb, "depth": r.depth, "normal": r.normal}
+    clocks = clock_sampler(local)
     for _ in range(args.warmup):
         step(imgs, priors, nprior)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
     clocks.start()
     timer = GpuTimer()
     launches0 = lib.vsx_launch_count()

@@ -20,6 +20,11 @@
 //            13 float atomics per (splat, tile) into the per-splat gradient.
 // This replaces a 13-value warp reduction per (splat, warp) (round-1 v1, see
 // profiles/r01_raster_bwd_v1_ncu.txt), which made the backward LSU-bound.
+// v3 (raster_bwd_tc_kernel, the default) moves both dot-product-shaped parts
+// onto the tensor cores (mma.sync tf32, 3xTF32 split): the per-(pixel, splat)
+// cotangent dot s = F[p] . P[j] before phase 1, and phase 2's per-splat sums,
+// which are two [kBC x 256] x [256 x 8] GEMMs. Records are prefetched one
+// chunk ahead with cp.async. VSX_RASTER_BWD="NS,BC" with NS > 0 selects v2.
 #include "raster_common.cuh"
 
 namespace vsx {
@@ -313,14 +318,349 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
   }
 }
 
+// ------------------------------------------------------- backward v3 (tensor)
+//
+// Phase 2 of v2 is two small GEMMs per chunk of kBC splats:
+//   Gsum[j][f] = sum_p W[j][p] * Gw[p][f]   f = (rgb, raw normal, plane) cotangents
+//   Mom[j][m]  = sum_p Q[j][p] * Mq[p][m]   m = (1, x, y, x^2, xy, y^2) about the centre
+// run here on the tensor cores with mma.sync m16n8k8 tf32 (A = the w / q
+// planes written by phase 1, B = per-tile constants). Precision is kept at
+// fp32 level with the 3xTF32 split (a_hi b_hi + a_hi b_lo + a_lo b_hi) for
+// Gw; Mq holds multiples of 1/4 below 64, exact in tf32, so q needs only
+// a_hi + a_lo. Warps split (m-tile, plane, k-range); the KSPLIT partial sums
+// meet in shared memory and one 8-lane group per splat forms its 13
+// gradients (same polynomials as v2) and issues the atomics.
+constexpr int kPlaneStride = kTilePixels + 4;  // 4 mod 32: conflict-free A fragments
+
+__device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (&a)[4],
+                                                 uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void copy_splat_async(vsx_splat *dst, const vsx_splat *src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * k),
+                 "l"(reinterpret_cast<const char *>(src) + 16 * k)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// tf32 by truncation: one LOP3 (cvt.rna.tf32 is a 4-instruction sequence on
+// sm_100a). With x = hi + (x - hi), the dropped bits of lo cost < 2^-21 |x|.
+__device__ __forceinline__ uint32_t tf32_bits(float x) {
+  return __float_as_uint(x) & 0xffffe000u;
+}
+
+// pixel moment m of tile pixel p (x, y about the tile centre)
+__device__ __forceinline__ float pixel_moment(int p, int m) {
+  const float xc = (float)(p & 15) - 7.5f, yc = (float)(p >> 4) - 7.5f;
+  switch (m) {
+    case 0: return 1.f;
+    case 1: return xc;
+    case 2: return yc;
+    case 3: return xc * xc;
+    case 4: return xc * yc;
+    case 5: return yc * yc;
+    default: return 0.f;
+  }
+}
+
+template <int kBC>
+__global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
+    raster_bwd_tc_kernel(BwdArgs a, vsx_camera cam) {
+  constexpr int kMT = kBC / 16;          // m-tiles per chunk
+  constexpr int kSplit = 8 / (2 * kMT);  // k-range split across warps
+  constexpr int kKS = 32 / kSplit;       // k-steps (8 pixels) per warp
+  __shared__ float4 s0[2][kBC], s1[2][kBC], s2[2][kBC], s3[2][kBC];
+  __shared__ float4 s_ph[2][kBC][4];  // P B fragments per (splat, lane&3): hi b0, hi b1, lo b0, lo b1
+  __shared__ uint32_t s_rank[2][kBC];
+  __shared__ float4 s_bw[32][32];  // Gw B fragments per (k-step, lane): hi b0, hi b1, lo b0, lo b1
+  __shared__ float2 s_bq[32][32];  // Mq B fragments per (k-step, lane)
+  __shared__ float s_red[kSplit][kBC][24];
+  __shared__ __align__(16) vsx_splat s_raw[2][kBC];
+  __shared__ int s_max;
+  extern __shared__ float s_plane[];  // w plane [kBC][kPlaneStride], then q plane
+  const int txn = gridDim.x;
+  const int tile = blockIdx.y * txn + blockIdx.x;
+  const int t = threadIdx.x;
+  const int lx = t & 15, ly = t >> 4;
+  const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
+  const bool inside = px < cam.width && py < cam.height;
+  const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
+  const uint32_t begin = a.tile_off[tile];
+  const float fx = (float)lx, fy = (float)ly;
+  const int lane = t & 31, warp = t >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  if (t == 0) s_max = 0;
+  int nc = 0;
+  float T = 1.f;
+  PixCot c{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (inside) {
+    const size_t p = (size_t)py * cam.width + px;
+    nc = a.nc[p];
+    T = a.T[p];
+    if (a.L.gt_rgb)
+      c = pixel_cotangent_loss(cam, px, py, p, a.alpha, a.rgb, a.depth, a.normal, a.raw, a.L);
+    else
+      c = pixel_cotangent(cam, px, py, p, a.alpha, a.depth, a.raw, a.g_rgb, a.g_alpha, a.g_depth,
+                          a.g_normal, a.g_raw);
+  }
+  // per-tile B fragments: Gw[p][f] staged through the (not yet used) w plane
+  {
+    float *gw = s_plane + t * 9;
+    gw[0] = c.gC0; gw[1] = c.gC1; gw[2] = c.gC2; gw[3] = c.gR0;
+    gw[4] = c.gR1; gw[5] = c.gR2; gw[6] = c.gD; gw[7] = c.gA;
+  }
+  __syncthreads();
+  if (inside && nc > 0) atomicMax(&s_max, nc);
+  // F A fragments (pixel rows of this warp x the 8 pixel cotangents), split
+  uint32_t fhi[2][4], flo[2][4];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int pix = 32 * warp + 16 * m + g + 8 * (r & 1), f = tq + 4 * (r >> 1);
+      const float v = s_plane[pix * 9 + f];
+      fhi[m][r] = tf32_bits(v);
+      flo[m][r] = tf32_bits(v - __uint_as_float(fhi[m][r]));
+    }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = t + 256 * i, ks = idx >> 5, ln = idx & 31;
+    const int f = ln >> 2, p0 = 8 * ks + (ln & 3), p1 = p0 + 4;
+    const float v0 = f < 7 ? s_plane[p0 * 9 + f] : 0.f, v1 = f < 7 ? s_plane[p1 * 9 + f] : 0.f;
+    const float h0 = __uint_as_float(tf32_bits(v0)), h1 = __uint_as_float(tf32_bits(v1));
+    s_bw[ks][ln] = make_float4(h0, h1, __uint_as_float(tf32_bits(v0 - h0)),
+                               __uint_as_float(tf32_bits(v1 - h1)));
+    s_bq[ks][ln] = make_float2(pixel_moment(p0, f), pixel_moment(p1, f));
+  }
+  __syncthreads();
+  const uint32_t stop = begin + (uint32_t)s_max;
+  float S = 0.f;  // sum over later live splats of s_i * w_i
+  float *wpl = s_plane, *qpl = s_plane + kBC * kPlaneStride;
+  // phase-2 role of this warp
+  const int mt = warp % kMT, plane = (warp / kMT) & 1, kr = warp / (2 * kMT);
+  int buf = 0;
+  // Record prefetch: the raw 64-byte records of chunk i+1 are copied
+  // (cp.async) into s_raw while chunk i is processed, and the tile-list ranks
+  // of chunk i+2 are loaded into a register, so neither dependent global load
+  // sits in front of a barrier. Thread t always owns slot t.
+  auto chunk_lo = [&](uint32_t e) { return e > begin + kBC ? e - kBC : begin; };
+  uint32_t rr = 0;  // rank of slot t in the chunk whose copy is in flight
+  uint32_t nr = 0;  // rank of slot t in the chunk after it
+  {
+    const uint32_t cs = chunk_lo(stop);
+    if (stop > begin && t < (int)(stop - cs)) {
+      rr = a.tile_list[cs + t];
+      copy_splat_async(&s_raw[0][t], a.rec + rr);
+    }
+    cp_async_commit();
+    const uint32_t cs2 = chunk_lo(cs);
+    if (cs > begin && t < (int)(cs - cs2)) nr = a.tile_list[cs2 + t];
+  }
+  for (uint32_t ce = stop; ce > begin; buf ^= 1) {
+    const uint32_t cs = chunk_lo(ce);
+    const int cnt = (int)(ce - cs);
+    cp_async_wait_all();
+    if (t < cnt) {
+      s_rank[buf][t] = rr;
+      const vsx_splat &sp = s_raw[buf][t];
+      stage_splat(sp, ox, oy, s0[buf][t], s1[buf][t], s2[buf][t], s3[buf][t]);
+      const float pv[8] = {sp.color[0], sp.color[1], sp.color[2], sp.normal[0],
+                           sp.normal[1], sp.normal[2], sp.plane_d, 1.f};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float h0 = __uint_as_float(tf32_bits(pv[k])), h1 = __uint_as_float(tf32_bits(pv[k + 4]));
+        s_ph[buf][t][k] = make_float4(h0, h1, __uint_as_float(tf32_bits(pv[k] - h0)),
+                                      __uint_as_float(tf32_bits(pv[k + 4] - h1)));
+      }
+    }
+    {
+      const uint32_t cs2 = chunk_lo(cs);
+      if (cs > begin && t < (int)(cs - cs2)) {
+        rr = nr;
+        copy_splat_async(&s_raw[buf ^ 1][t], a.rec + nr);
+      }
+      cp_async_commit();
+      const uint32_t cs3 = chunk_lo(cs2);
+      if (cs2 > begin && t < (int)(cs2 - cs3)) nr = a.tile_list[cs3 + t];
+    }
+    __syncthreads();
+    // ---- phase 0: sk[j][p] = F[p] . P[j] for this warp's 32 pixels on the
+    // tensor cores (3xTF32), written into the q plane that phase 1 overwrites
+    // in place with q (same thread, same slot)
+#pragma unroll
+    for (int nt = 0; nt < kBC / 8; ++nt) {
+      const float4 b = s_ph[buf][8 * nt + g][tq];
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        mma_m16n8k8_tf32(d, flo[m], __float_as_uint(b.x), __float_as_uint(b.y));
+        mma_m16n8k8_tf32(d, fhi[m], __float_as_uint(b.z), __float_as_uint(b.w));
+        mma_m16n8k8_tf32(d, fhi[m], __float_as_uint(b.x), __float_as_uint(b.y));
+        float *o = qpl + (8 * nt + 2 * tq) * kPlaneStride + 32 * warp + 16 * m + g;
+        o[0] = d[0];
+        o[kPlaneStride] = d[1];
+        o[8] = d[2];
+        o[kPlaneStride + 8] = d[3];
+      }
+    }
+    __syncwarp();
+    // ---- phase 1: per-pixel back-to-front recursion (as v2)
+    const int kbase = (int)(cs - begin);
+    const int jlive = min(cnt, nc - kbase);
+    for (int j = cnt - 1; j >= max(jlive, 0); --j) {
+      wpl[j * kPlaneStride + t] = 0.f;
+      qpl[j * kPlaneStride + t] = 0.f;
+    }
+    // batches of 4: the alphas (the long dependent part) are independent
+    // across splats; only T and S are carried, one FMUL / FFMA each
+    int j = jlive - 1;
+    for (; j >= 3; j -= 4) {
+      float al[4], ee[4], aa[4], rm[4], sk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 p0 = s0[buf][j - u], p1 = s1[buf][j - u];
+        al[u] = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, ee[u], aa[u]);
+        rm[u] = rcp_ftz(1.f - al[u]);
+        sk[u] = qpl[(j - u) * kPlaneStride + t];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float Tk = T * rm[u];
+        const float w = al[u] * Tk;
+        const float da = Tk * sk[u] - S * rm[u];
+        S = fmaf(sk[u], w, S);
+        T = Tk;
+        wpl[(j - u) * kPlaneStride + t] = w;
+        qpl[(j - u) * kPlaneStride + t] = (aa[u] <= kAlphaClamp ? da : 0.f) * ee[u];
+      }
+    }
+    for (; j >= 0; --j) {
+      const float4 p0 = s0[buf][j], p1 = s1[buf][j];
+      float e, at;
+      const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
+      const float rom = rcp_ftz(1.f - alpha);
+      const float Tk = T * rom;
+      const float w = alpha * Tk;
+      const float sk = qpl[j * kPlaneStride + t];
+      const float da = Tk * sk - S * rom;
+      S = fmaf(sk, w, S);
+      T = Tk;
+      const float dat = at <= kAlphaClamp ? da : 0.f;
+      wpl[j * kPlaneStride + t] = w;
+      qpl[j * kPlaneStride + t] = dat * e;
+    }
+    __syncthreads();
+    // ---- phase 2: tensor-core sums over this warp's k-range
+    {
+      const float *A = (plane ? qpl : wpl) + (16 * mt + g) * kPlaneStride + tq;
+      // independent accumulators per split term and k-step parity: the HMMA
+      // chains overlap instead of serialising on one accumulator
+      float d[4] = {0.f, 0.f, 0.f, 0.f}, e1[4] = {0.f, 0.f, 0.f, 0.f},
+            e2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int kk = 0; kk < kKS; ++kk) {
+        float (&D0)[4] = d;
+        float (&D1)[4] = e1;
+        float (&D2)[4] = e2;
+        const int ks = kr * kKS + kk;
+        const float x0 = A[8 * ks], x1 = A[8 * kPlaneStride + 8 * ks], x2 = A[8 * ks + 4],
+                    x3 = A[8 * kPlaneStride + 8 * ks + 4];
+        uint32_t hi[4], lo[4];
+        hi[0] = tf32_bits(x0);
+        hi[1] = tf32_bits(x1);
+        hi[2] = tf32_bits(x2);
+        hi[3] = tf32_bits(x3);
+        lo[0] = tf32_bits(x0 - __uint_as_float(hi[0]));
+        lo[1] = tf32_bits(x1 - __uint_as_float(hi[1]));
+        lo[2] = tf32_bits(x2 - __uint_as_float(hi[2]));
+        lo[3] = tf32_bits(x3 - __uint_as_float(hi[3]));
+        if (plane == 0) {
+          const float4 b = s_bw[ks][lane];
+          mma_m16n8k8_tf32(D1, lo, __float_as_uint(b.x), __float_as_uint(b.y));
+          mma_m16n8k8_tf32(D2, hi, __float_as_uint(b.z), __float_as_uint(b.w));
+          mma_m16n8k8_tf32(D0, hi, __float_as_uint(b.x), __float_as_uint(b.y));
+        } else {
+          const float2 b = s_bq[ks][lane];
+          mma_m16n8k8_tf32(D1, lo, __float_as_uint(b.x), __float_as_uint(b.y));
+          mma_m16n8k8_tf32(D0, hi, __float_as_uint(b.x), __float_as_uint(b.y));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d[k] = (e1[k] + e2[k]) + d[k];
+      float *red = &s_red[kr][16 * mt + g][8 * plane + 2 * tq];
+      *reinterpret_cast<float2 *>(red) = make_float2(d[0], d[1]);
+      *reinterpret_cast<float2 *>(red + 8 * 24) = make_float2(d[2], d[3]);
+    }
+    __syncthreads();
+    // ---- epilogue: 8 lanes per splat, lane part holds features 2part, 2part+1
+    if (t < 8 * kBC) {
+      const int j = t >> 3, part = t & 7;
+      float2 v = *reinterpret_cast<const float2 *>(&s_red[0][j][2 * part]);
+#pragma unroll
+      for (int k = 1; k < kSplit; ++k) {
+        const float2 u = *reinterpret_cast<const float2 *>(&s_red[k][j][2 * part]);
+        v.x += u.x;
+        v.y += u.y;
+      }
+      // moments: part 4 = (1, x), 5 = (y, xx), 6 = (xy, yy)
+      const float m2 = __shfl_down_sync(0xffffffffu, v.x, 1), m3 = __shfl_down_sync(0xffffffffu, v.y, 1);
+      const float m4 = __shfl_down_sync(0xffffffffu, v.x, 2), m5 = __shfl_down_sync(0xffffffffu, v.y, 2);
+      if (j < cnt) {
+        float* gp = a.grad + (size_t)13 * s_rank[buf][j];
+        if (part < 4) {
+          if (v.x != 0.f) atomicAdd(gp + 6 + 2 * part, v.x);
+          if (part < 3 && v.y != 0.f) atomicAdd(gp + 7 + 2 * part, v.y);
+        } else if (part == 4) {
+          const float4 p0 = s0[buf][j], p1 = s1[buf][j];
+          const float op = p1.y, A = p1.w, B = s2[buf][j].w, C = s3[buf][j].w;
+          const float mx = p0.x - 7.5f, my = p0.y - 7.5f;
+          const float Q1 = v.x, X = v.y, Y = m2, XX = m3, XY = m4, YY = m5;
+          const float sx = X - mx * Q1, sy = Y - my * Q1;
+          const float sxx = XX - 2.f * mx * X + mx * mx * Q1;
+          const float sxy = XY - mx * Y - my * X + mx * my * Q1;
+          const float syy = YY - 2.f * my * Y + my * my * Q1;
+          const float g0 = op * (A * sx + B * sy), g1 = op * (B * sx + C * sy);
+          const float g2 = -0.5f * op * sxx, g3 = -op * sxy, g4 = -0.5f * op * syy;
+          if (g0 != 0.f) atomicAdd(gp + 0, g0);
+          if (g1 != 0.f) atomicAdd(gp + 1, g1);
+          if (g2 != 0.f) atomicAdd(gp + 2, g2);
+          if (g3 != 0.f) atomicAdd(gp + 3, g3);
+          if (g4 != 0.f) atomicAdd(gp + 4, g4);
+          if (Q1 != 0.f) atomicAdd(gp + 5, Q1);
+        }
+      }
+    }
+    ce = cs;
+  }
+}
+
 static int launch_bwd(const BwdArgs &a, const vsx_camera &cam, cudaStream_t st) {
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
-  // VSX_RASTER_BWD="NS,BC" selects the phase-2 splats-per-pass and the splat
-  // chunk for A/B timing (default 2,32).
-  static int ns = 2, bc = 32;
+  // VSX_RASTER_BWD="NS,BC" selects the v2 (FFMA) phase-2 splats-per-pass and
+  // splat chunk for A/B timing; NS = 0 (default) is the tensor-core v3 with
+  // chunk BC (default 16).
+  static int ns = 0, bc = 16;
   static bool attr = false;
   if (!attr) {
     if (const char *sel = getenv("VSX_RASTER_BWD")) sscanf(sel, "%d,%d", &ns, &bc);
+    const int p32 = (int)(sizeof(float) * 2 * 32 * kPlaneStride);
+    const int p16 = (int)(sizeof(float) * 2 * 16 * kPlaneStride);
+    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_tc_kernel<32>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, p32));
+    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_tc_kernel<16>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, p16));
     const int s32 = (int)(sizeof(float2) * 32 * kTilePixels);
     const int s16 = (int)(sizeof(float2) * 16 * kTilePixels);
     VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<1, 16>,
@@ -332,6 +672,13 @@ static int launch_bwd(const BwdArgs &a, const vsx_camera &cam, cudaStream_t st) 
     VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<2, 32>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
     attr = true;
+  }
+  if (ns == 0) {
+    const int smem = (int)(sizeof(float) * 2 * bc * kPlaneStride);
+    if (bc == 16) raster_bwd_tc_kernel<16><<<grid, 256, smem, st>>>(a, cam);
+    else raster_bwd_tc_kernel<32><<<grid, 256, smem, st>>>(a, cam);
+    VSX_LAUNCH_CHECK("raster_bwd");
+    return VSX_OK;
   }
   const int smem = (int)(sizeof(float2) * bc * kTilePixels);
   if (bc == 16) {

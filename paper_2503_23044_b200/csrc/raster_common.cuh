@@ -41,6 +41,18 @@ __device__ __forceinline__ void stage_splat(const vsx_splat &s, double ox, doubl
   p3 = make_float4(s.normal[0], s.normal[1], s.normal[2], s.conic[2]);
 }
 
+// 64-byte record as four 16-byte loads (rec is cudaMalloc'd, 64 B stride).
+__device__ __forceinline__ vsx_splat load_splat(const vsx_splat *__restrict__ rec, uint32_t i) {
+  union {
+    float4 v[4];
+    vsx_splat s;
+  } u;
+  const float4 *p = reinterpret_cast<const float4 *>(rec + i);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) u.v[k] = __ldg(p + k);
+  return u.s;
+}
+
 __device__ __forceinline__ float rcp_ftz(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
