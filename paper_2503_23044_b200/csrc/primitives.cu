@@ -133,11 +133,6 @@ __global__ void select_scatter_kernel(const uint8_t *__restrict__ f,
 
 // ------------------------------------------------------------------ radix sort
 
-constexpr int kRsBlock = 256;
-constexpr int kRsRounds = 16;
-constexpr int kRsTile = kRsBlock * kRsRounds;
-constexpr int kRsWarps = kRsBlock / 32;
-
 template <typename K>
 __global__ void rs_minmax_kernel(const K *__restrict__ keys, int64_t n,
                                  unsigned long long *__restrict__ or_and) {
@@ -164,122 +159,256 @@ __global__ void rs_init_or_and(unsigned long long *or_and) {
   or_and[1] = ~0ull;
 }
 
-template <typename K>
-__global__ void rs_hist_kernel(const K *__restrict__ keys, int64_t n, int shift,
-                               uint32_t *__restrict__ hist) {
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kRsTile;
-#pragma unroll 4
-  for (int r = 0; r < kRsRounds; ++r) {
-    const int64_t i = base + r * kRsBlock + threadIdx.x;
-    if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & 255u], 1u);
+// ------------------------------------------------ single-pass (onesweep) passes
+//
+// One kernel per 8-bit digit pass. Each CTA takes the next tile index from an
+// atomic counter (so every lower tile has started and will finish), ranks its
+// 4096 keys with warp-private digit counters (match_any, no CTA barriers in
+// the ranking loop), publishes its per-digit counts, and obtains the exclusive
+// per-digit prefix of all earlier tiles by decoupled look-back on a
+// (flag:2 | count:30) status word per (tile, digit). A single histogram kernel
+// up front supplies the global digit totals of every pass. Launches per sort:
+// memset + histogram + one per pass (the older multi-kernel LSD sort needed
+// histogram + 3-level scan + scatter per pass).
+
+constexpr int kOsBlock = 256;
+constexpr int kOsItems = 16;
+constexpr int kOsTile = kOsBlock * kOsItems;  // 4096 keys, 512 per warp
+constexpr int kOsWarps = kOsBlock / 32;
+constexpr uint32_t kOsAgg = 1u << 30, kOsPre = 2u << 30, kOsMask = kOsAgg - 1u;
+
+struct OsShifts {
+  int s[16];
+  int np;
+};
+
+// Lanes of the warp holding the same 8-bit digit as this lane (8 ballots;
+// cheaper and more predictable than MATCH.ANY), restricted to `valid`.
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, unsigned valid) {
+  unsigned m = valid;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+    m &= ((d >> b) & 1u) ? bal : ~bal;
   }
-  __syncthreads();
-  hist[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
+  return m;
 }
 
-// Stable scatter: within a block, keys are ranked in input order (round-major,
-// then thread); across blocks the digit-major scanned histogram keeps block
-// order, so equal digits never reorder. Keys are first placed digit-grouped
-// in shared memory, then written out so that consecutive threads store
-// consecutive addresses of each digit bucket (coalesced stores).
+// Global digit histograms of every pass in one read. Each thread takes 16
+// consecutive keys and run-length merges equal digits before its shared
+// atomic: emitted (tile, rank) keys come in long runs of equal high digits,
+// which would otherwise serialise on one shared-memory address.
 template <typename K>
-__global__ void __launch_bounds__(kRsBlock) rs_scatter_kernel(
-    const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
-    uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ offs,
-    const uint32_t *__restrict__ hist) {
-  extern __shared__ __align__(16) unsigned char rs_smem[];
-  K *sk = reinterpret_cast<K *>(rs_smem);
-  uint32_t *sv = reinterpret_cast<uint32_t *>(sk + kRsTile);
-  __shared__ uint32_t run[256];
-  __shared__ uint32_t lstart[256];
-  __shared__ uint32_t gbase[256];
-  __shared__ uint32_t wcnt[kRsWarps][256];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int64_t cell = (int64_t)t * gridDim.x + blockIdx.x;
-  gbase[t] = offs[cell];
-  uint32_t tot = 0;
-  const uint32_t ls = block_exclusive_scan(hist[cell], tot);
-  lstart[t] = ls;
-  run[t] = ls;
-  const unsigned lt = (1u << lane) - 1u;
-  const int64_t base = (int64_t)blockIdx.x * kRsTile;
-  for (int r = 0; r < kRsRounds; ++r) {
-    const int64_t i = base + r * kRsBlock + t;
-    if (base + r * kRsBlock >= n) break;  // block-uniform
-    const bool ok = i < n;
-    K k = ok ? kin[i] : K(0);
-    uint32_t v = ok ? vin[i] : 0u;
-    const uint32_t d = ok ? ((uint32_t)(k >> shift) & 255u) : 256u;
+__global__ void __launch_bounds__(256) os_hist_kernel(const K *__restrict__ keys, int64_t n,
+                                                      OsShifts sh, uint32_t *__restrict__ gh) {
+  constexpr int kPer = 16;
+  __shared__ uint32_t h[8][256];
+  for (int p = 0; p < sh.np; ++p) h[p][threadIdx.x] = 0u;
+  __syncthreads();
+  for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kPer; b0 < n;
+       b0 += (int64_t)gridDim.x * blockDim.x * kPer) {
+    K kk[kPer];
 #pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) wcnt[w][t] = 0u;
-    __syncthreads();
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t lrank = __popc(peers & lt);
-    if (ok && lrank == 0) wcnt[warp][d] = __popc(peers);
-    __syncthreads();
-    uint32_t acc = run[t];
+    for (int j = 0; j < kPer; ++j) kk[j] = b0 + j < n ? keys[b0 + j] : K(0);
+    const int m = (int)min((int64_t)kPer, n - b0);
+    for (int p = 0; p < sh.np; ++p) {
+      uint32_t cur = (uint32_t)(kk[0] >> sh.s[p]) & 255u, c = 1;
 #pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) {
-      const uint32_t c = wcnt[w][t];
-      wcnt[w][t] = acc;
-      acc += c;
+      for (int j = 1; j < kPer; ++j) {
+        if (j < m) {
+          const uint32_t d = (uint32_t)(kk[j] >> sh.s[p]) & 255u;
+          if (d == cur) {
+            ++c;
+          } else {
+            atomicAdd(&h[p][cur], c);
+            cur = d;
+            c = 1;
+          }
+        }
+      }
+      atomicAdd(&h[p][cur], c);
     }
-    run[t] = acc;
-    __syncthreads();
-    if (ok) {
-      const uint32_t pos = wcnt[warp][d] + lrank;  // block-local, digit-grouped
-      sk[pos] = k;
-      sv[pos] = v;
+  }
+  __syncthreads();
+  for (int p = 0; p < sh.np; ++p) {
+    const uint32_t c = h[p][threadIdx.x];
+    if (c) atomicAdd(&gh[p * 256 + threadIdx.x], c);
+  }
+}
+
+// The look-back words carry their own payload (flag | count), so relaxed
+// (L2-coherent) accesses suffice: no other data is published through them.
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(uint32_t *p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kOsBlock) os_pass_kernel(
+    const K *__restrict__ kin, const uint32_t *__restrict__ vin, K *__restrict__ kout,
+    uint32_t *__restrict__ vout, int64_t n, int shift, const uint32_t *__restrict__ gh,
+    uint32_t *__restrict__ status, uint32_t *__restrict__ counter) {
+  // input tile and digit-grouped output tile live in separate buffers, so
+  // keys / values are never held in registers across the ranking
+  extern __shared__ __align__(16) unsigned char os_smem[];
+  K *sk = reinterpret_cast<K *>(os_smem);
+  K *ok_ = sk + kOsTile;
+  uint32_t *sv = reinterpret_cast<uint32_t *>(ok_ + kOsTile);
+  uint32_t *ov = sv + kOsTile;
+  __shared__ uint32_t whist[kOsWarps][256];
+  __shared__ uint32_t s_lstart[256], s_dst[256];
+  __shared__ uint32_t s_bid;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) s_bid = atomicAdd(counter, 1u);
+#pragma unroll
+  for (int w = 0; w < kOsWarps; ++w) whist[w][t] = 0u;
+  __syncthreads();
+  const uint32_t bid = s_bid;
+  const int64_t base = (int64_t)bid * kOsTile;
+  const unsigned lt = (1u << lane) - 1u;
+  const int nvalid = (int)min((int64_t)kOsTile, n - base);
+  // ---- stage the tile with 16-byte loads, all in flight at once
+  {
+    const bool vec = nvalid == kOsTile &&
+                     ((reinterpret_cast<uintptr_t>(kin) | reinterpret_cast<uintptr_t>(vin)) & 15) == 0;
+    if (vec) {
+      constexpr int kKV = kOsTile * (int)sizeof(K) / 16 / kOsBlock;  // uint4 per thread
+      constexpr int kVV = kOsTile * 4 / 16 / kOsBlock;
+      const uint4 *gk = reinterpret_cast<const uint4 *>(kin + base);
+      const uint4 *gv = reinterpret_cast<const uint4 *>(vin + base);
+      uint4 bk[kKV], bv[kVV];
+#pragma unroll
+      for (int q = 0; q < kKV; ++q) bk[q] = __ldg(gk + q * kOsBlock + t);
+#pragma unroll
+      for (int q = 0; q < kVV; ++q) bv[q] = __ldg(gv + q * kOsBlock + t);
+#pragma unroll
+      for (int q = 0; q < kKV; ++q) reinterpret_cast<uint4 *>(sk)[q * kOsBlock + t] = bk[q];
+#pragma unroll
+      for (int q = 0; q < kVV; ++q) reinterpret_cast<uint4 *>(sv)[q * kOsBlock + t] = bv[q];
+    } else {
+      for (int s = t; s < nvalid; s += kOsBlock) {
+        sk[s] = kin[base + s];
+        sv[s] = vin[base + s];
+      }
     }
     __syncthreads();
   }
-  const int nvalid = (int)min((int64_t)kRsTile, n - base);
-  for (int s = t; s < nvalid; s += kRsBlock) {
-    const K k = sk[s];
-    const uint32_t d = (uint32_t)(k >> shift) & 255u;
-    const uint32_t pos = gbase[d] + (uint32_t)s - lstart[d];
-    kout[pos] = k;
-    vout[pos] = sv[s];
+  // ---- warp-private ranking, keys in input order (warp, round, lane)
+  uint32_t rk[kOsItems];
+#pragma unroll
+  for (int r = 0; r < kOsItems; ++r) {
+    const int s = warp * (32 * kOsItems) + r * 32 + lane;
+    const bool ok = s < nvalid;
+    const uint32_t d = ok ? ((uint32_t)(sk[s] >> shift) & 255u) : 0u;
+    const unsigned peers = digit_peers(d, __ballot_sync(0xffffffffu, ok));
+    uint32_t cur = 0;
+    if (ok) cur = whist[warp][d];
+    __syncwarp();
+    if (ok && (peers & lt) == 0u) whist[warp][d] = cur + __popc(peers);
+    __syncwarp();
+    rk[r] = cur + __popc(peers & lt);
+  }
+  __syncthreads();
+  // ---- thread t = digit t: per-warp offsets, tile count, publish aggregate
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int w = 0; w < kOsWarps; ++w) {
+    const uint32_t c = whist[w][t];
+    whist[w][t] = cnt;
+    cnt += c;
+  }
+  uint32_t *my = status + (size_t)bid * 256 + t;
+  st_relaxed_u32(my, (bid == 0 ? kOsPre : kOsAgg) | cnt);
+  uint32_t tot = 0;
+  const uint32_t lstart = block_exclusive_scan(cnt, tot);
+  const uint32_t gstart = block_exclusive_scan(gh[t], tot);
+  s_lstart[t] = lstart;
+  // ---- decoupled look-back over earlier tiles (per digit)
+  // A window of 8 predecessors is read per step (independent loads in
+  // flight), consumed nearest-first up to the first inclusive prefix or the
+  // first tile that has not published yet (re-read next step).
+  uint32_t excl = 0;
+  if (bid > 0) {
+    int64_t p = (int64_t)bid - 1;
+    while (true) {
+      uint32_t w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        w[j] = p - j >= 0 ? ld_relaxed_u32(status + (size_t)(p - j) * 256 + t) : kOsPre;
+      int used = 0;
+      bool done = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (!done && used == j && w[j] != 0u) {
+          excl += w[j] & kOsMask;
+          ++used;
+          done = (w[j] & kOsPre) != 0u;
+        }
+      }
+      if (done) break;
+      p -= used;
+    }
+    st_relaxed_u32(my, kOsPre | (excl + cnt));
+  }
+  s_dst[t] = gstart + excl - lstart;
+  __syncthreads();
+  // ---- place keys digit-grouped in the output tile, then coalesced stores
+#pragma unroll
+  for (int r = 0; r < kOsItems; ++r) {
+    const int s = warp * (32 * kOsItems) + r * 32 + lane;
+    if (s < nvalid) {
+      const K kk = sk[s];
+      const uint32_t d = (uint32_t)(kk >> shift) & 255u;
+      const uint32_t pos = s_lstart[d] + whist[warp][d] + rk[r];
+      ok_[pos] = kk;
+      ov[pos] = sv[s];
+    }
+  }
+  __syncthreads();
+  for (int s = t; s < nvalid; s += kOsBlock) {
+    const K kk = ok_[s];
+    const uint32_t pos = s_dst[(uint32_t)(kk >> shift) & 255u] + (uint32_t)s;
+    kout[pos] = kk;
+    vout[pos] = ov[s];
   }
 }
 
 struct SortWs {
   void *alt_keys;
   uint32_t *alt_vals;
-  uint32_t *hist;
-  uint32_t *hist_scan;
-  uint32_t *scan_ws;
+  uint32_t *gh;       // [16][256] global digit histograms
+  uint32_t *status;   // [nb][256] look-back words, per pass
+  uint32_t *counter;  // [16] tile-index counters
   unsigned long long *or_and;
 };
 
 static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
+static int64_t os_tiles(int64_t n) { return std::max<int64_t>((n + kOsTile - 1) / kOsTile, 1); }
+
 static size_t sort_ws_bytes(int64_t n) {
-  const int64_t nb = (n + kRsTile - 1) / kRsTile;
-  const int64_t nh = 256 * std::max<int64_t>(nb, 1);
   return align256(sizeof(uint64_t) * n) + align256(sizeof(uint32_t) * n) +
-         align256(sizeof(uint32_t) * nh) + align256(sizeof(uint32_t) * (nh + 1)) +
-         align256(sizeof(uint32_t) * (scan_ws_elems(nh) + 1)) + 256;
+         align256(sizeof(uint32_t) * 16 * 256) + align256(sizeof(uint32_t) * 256 * os_tiles(n)) +
+         align256(sizeof(uint32_t) * 16) + 256;
 }
 
 static SortWs carve_sort_ws(void *ws, int64_t n) {
-  const int64_t nb = (n + kRsTile - 1) / kRsTile;
-  const int64_t nh = 256 * std::max<int64_t>(nb, 1);
   char *p = static_cast<char *>(ws);
   SortWs w;
   w.alt_keys = p;
   p += align256(sizeof(uint64_t) * n);
   w.alt_vals = reinterpret_cast<uint32_t *>(p);
   p += align256(sizeof(uint32_t) * n);
-  w.hist = reinterpret_cast<uint32_t *>(p);
-  p += align256(sizeof(uint32_t) * nh);
-  w.hist_scan = reinterpret_cast<uint32_t *>(p);
-  p += align256(sizeof(uint32_t) * (nh + 1));
-  w.scan_ws = reinterpret_cast<uint32_t *>(p);
-  p += align256(sizeof(uint32_t) * (scan_ws_elems(nh) + 1));
+  w.gh = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * 16 * 256);
+  w.status = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * 256 * os_tiles(n));
+  w.counter = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * 16);
   w.or_and = reinterpret_cast<unsigned long long *>(p);
   return w;
 }
@@ -288,7 +417,7 @@ template <typename K>
 static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout, int64_t n,
                       int begin_bit, int end_bit, int flags, void *ws, size_t ws_bytes,
                       cudaStream_t st) {
-  VSX_REQUIRE(n >= 0 && n < (int64_t)1 << 32, "sort: bad n %lld", (long long)n);
+  VSX_REQUIRE(n >= 0 && n < (int64_t)1 << 30, "sort: bad n %lld", (long long)n);
   VSX_REQUIRE(begin_bit >= 0 && end_bit <= (int)(8 * sizeof(K)) && begin_bit <= end_bit,
               "sort: bad bit range");
   if (n == 0) return VSX_OK;
@@ -296,14 +425,14 @@ static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout
               sort_ws_bytes(n));
   SortWs w = carve_sort_ws(ws, n);
   static bool attr = false;
-  const int smem = (int)((sizeof(K) + sizeof(uint32_t)) * kRsTile);
+  const int smem = (int)(2 * (sizeof(K) + sizeof(uint32_t)) * kOsTile);
   if (!attr) {
-    VSX_CUDA_TRY(cudaFuncSetAttribute(rs_scatter_kernel<uint64_t>,
+    VSX_CUDA_TRY(cudaFuncSetAttribute(os_pass_kernel<uint64_t>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(12 * kRsTile)));
-    VSX_CUDA_TRY(cudaFuncSetAttribute(rs_scatter_kernel<uint32_t>,
+                                      (int)(24 * kOsTile)));
+    VSX_CUDA_TRY(cudaFuncSetAttribute(os_pass_kernel<uint32_t>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(8 * kRsTile)));
+                                      (int)(16 * kOsTile)));
     attr = true;
   }
   unsigned long long varying = ~0ull;
@@ -328,22 +457,28 @@ static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout
     if (vout != vin) VSX_CUDA_TRY(cudaMemcpyAsync(vout, vin, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st));
     return VSX_OK;
   }
-  const int nb = grid_for(n, kRsTile);
-  const int64_t nh = 256 * (int64_t)nb;
+  const int64_t nb = os_tiles(n);
   K *alt_k = static_cast<K *>(w.alt_keys);
   const K *src_k = kin;
   const uint32_t *src_v = vin;
+  OsShifts sh{};
+  sh.np = np;
+  for (int p = 0; p < np; ++p) sh.s[p] = shifts[p];
+  // gh and the counters are contiguous: one memset clears both
+  VSX_CUDA_TRY(cudaMemsetAsync(w.gh, 0, sizeof(uint32_t) * 16 * 256, st));
+  VSX_CUDA_TRY(cudaMemsetAsync(w.counter, 0, sizeof(uint32_t) * 16, st));
+  os_hist_kernel<K><<<(unsigned)std::min<int64_t>(grid_for(n, 256), 8 * 148), 256, 0, st>>>(
+      kin, n, sh, w.gh);
+  VSX_LAUNCH_CHECK("os_hist");
   for (int p = 0; p < np; ++p) {
     const bool to_out = ((np - 1 - p) % 2) == 0;
     K *dk = to_out ? kout : alt_k;
     uint32_t *dv = to_out ? vout : w.alt_vals;
-    rs_hist_kernel<K><<<nb, kRsBlock, 0, st>>>(src_k, n, shifts[p], w.hist);
-    VSX_LAUNCH_CHECK("rs_hist");
-    int rc = scan_impl(w.hist, w.hist_scan, nh, w.scan_ws, st);
-    if (rc) return rc;
-    rs_scatter_kernel<K><<<nb, kRsBlock, smem, st>>>(src_k, src_v, dk, dv, n, shifts[p],
-                                                    w.hist_scan, w.hist);
-    VSX_LAUNCH_CHECK("rs_scatter");
+    VSX_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(uint32_t) * 256 * nb, st));
+    os_pass_kernel<K><<<(unsigned)nb, kOsBlock, smem, st>>>(src_k, src_v, dk, dv, n, shifts[p],
+                                                          w.gh + 256 * p, w.status,
+                                                          w.counter + p);
+    VSX_LAUNCH_CHECK("os_pass");
     src_k = dk;
     src_v = dv;
   }

@@ -54,16 +54,43 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
     if (__syncthreads_count(!done) == 0) break;
     const uint32_t idx = cs + threadIdx.x;
     if (idx < end) {
-      const vsx_splat sp = rec[tile_list[idx]];
+      const vsx_splat sp = load_splat(rec, tile_list[idx]);
       stage_splat(sp, ox, oy, s0[threadIdx.x], s1[threadIdx.x], s2[threadIdx.x], s3[threadIdx.x]);
     }
     __syncthreads();
     const int cnt = (int)min((uint32_t)kChunk, end - cs);
     if (!done) {
-      int j = 0;
-#pragma unroll 4
-      for (; j < cnt; ++j) {
-        if (T < kEarlyStopT) break;  // T_prev < 1e-4: this and every later splat is dead
+      // batches of 4 independent alphas, then the sequential blend; T only
+      // decreases, so "live" (T_prev >= 1e-4) holds for a prefix of the chunk
+      int j = 0, live = 0;
+      for (; j + 4 <= cnt && T >= kEarlyStopT; j += 4) {
+        float al[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 p0 = s0[j + u], p1 = s1[j + u];
+          float e, at;
+          al[u] = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (T >= kEarlyStopT) {
+            const float w = al[u] * T;
+            const float4 p2 = s2[j + u], p3 = s3[j + u];
+            const float pd = s1[j + u].z;
+            acc += w;
+            c0 = fmaf(w, p2.x, c0);
+            c1 = fmaf(w, p2.y, c1);
+            c2 = fmaf(w, p2.z, c2);
+            n0 = fmaf(w, p3.x, n0);
+            n1 = fmaf(w, p3.y, n1);
+            n2 = fmaf(w, p3.z, n2);
+            dist = fmaf(w, pd, dist);
+            T = __fmaf_rn(-al[u], T, T);
+            ++live;
+          }
+        }
+      }
+      for (; j < cnt && T >= kEarlyStopT; ++j) {
         const float4 p0 = s0[j], p1 = s1[j];
         float e, at;
         const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
@@ -78,9 +105,10 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
         n2 = fmaf(w, p3.z, n2);
         dist = fmaf(w, p1.z, dist);
         T = __fmaf_rn(-alpha, T, T);
+        ++live;
       }
-      nc = (int32_t)(cs - begin) + j;
-      done = j < cnt;
+      nc = (int32_t)(cs - begin) + live;
+      done = T < kEarlyStopT;
     }
   }
   // loss partial sums (fused K9): rgb |d|, masked depth |d|, masked normal |d|
