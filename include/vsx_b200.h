@@ -145,7 +145,9 @@ int vsx_decode_fwd(vsx_decoder W, const int32_t *active, int32_t n_active, const
 
 /* Tensor-core (tcgen05, 3xTF32) variant of vsx_decode_fwd. `img` is the
  * decoder weight image built by vsx_decoder_image (vsx_decoder_image_floats(n)
- * floats) after every weight update. Supported for n <= 13. */
+ * floats) after every weight update. Supported for n <= 13. cache_o is
+ * required here (the per-gaussian activations read the raw head outputs back
+ * from it); cache_h may be NULL. */
 size_t vsx_decoder_image_floats(int32_t n);
 int vsx_decoder_image(vsx_decoder W, float *img, vsx_stream s);
 int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t *active, int32_t n_active,

@@ -234,123 +234,137 @@ __device__ __forceinline__ void rot_vjp(float w, float x, float y, float z, cons
                   y * G[5] + x * G[6] + y * G[7]);
 }
 
-// Anchor-parallel backward: per-gaussian cotangents -> head-output cotangents
-// g_o (feature-major), pre-activation cotangents g_pre (feature-major), the
-// input block x (feature-major, + a ones row for bias grads), and per-anchor
-// grads of embeddings / log-scales / offsets.
-__global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
-    vsx_decoder W, const int32_t *__restrict__ active, int32_t n_active,
-    const double *__restrict__ centers, const float *__restrict__ emb,
-    const float *__restrict__ log_scale, const float *__restrict__ offsets, vsx_camera cam,
-    double lod_ref, double max_scale, const float *__restrict__ cache_h,
+// Backward, part 1 (gaussian-parallel): per-gaussian cotangents -> head-output
+// cotangents g_o (feature-major, row = head output column) and the offsets
+// grads. Thread index = sl * n_active + r, so every g_o row is written
+// coalesced; the per-gaussian inputs are read with stride n (L2-resident).
+__global__ void __launch_bounds__(256) decode_bwd_gauss_kernel(
+    int n, const int32_t *__restrict__ active, int32_t n_active,
+    const float *__restrict__ log_scale, const float *__restrict__ offsets, double max_scale,
     const float *__restrict__ cache_o, const float *__restrict__ dscale,
     const float *__restrict__ dquat, const float *__restrict__ g_means,
     const float *__restrict__ g_opacity, const float *__restrict__ g_color,
     const float *__restrict__ g_scale, const float *__restrict__ g_quat,
-    const float *__restrict__ g_normal, float *__restrict__ g_emb,
-    float *__restrict__ g_log_scale, float *__restrict__ g_offsets, float *__restrict__ xs,
-    float *__restrict__ g_o_out, float *__restrict__ g_pre_out) {
+    const float *__restrict__ g_normal, float *__restrict__ g_offsets,
+    float *__restrict__ g_o_out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n_active * n) return;
+  const int sl = (int)(idx / n_active), r = (int)(idx % n_active);
+  const size_t ld = cache_ld(n_active);
+  const size_t g = (size_t)r * n + sl;
+  const float smax = (float)max_scale, smin = (float)kMinScale;
+  {
+    const float sg = sigmoidf_(cache_o[(size_t)sl * ld + r]);
+    g_o_out[(size_t)sl * ld + r] = g_opacity[g] * sg * (1.f - sg);
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int j = n + 3 * sl + c;
+    const float sg = sigmoidf_(cache_o[(size_t)j * ld + r]);
+    g_o_out[(size_t)j * ld + r] = g_color[3 * g + c] * sg * (1.f - sg);
+  }
+  const int oo = 4 * n + 7 * sl;
+  float o[7], go[7];
+#pragma unroll
+  for (int c = 0; c < 7; ++c) o[c] = cache_o[(size_t)(oo + c) * ld + r];
+  // scales: clamp(exp(o), 1e-6, max) — gradient passes inside [min, max]
+  float sc[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float e = expf(o[c]);
+    sc[c] = dscale[3 * g + c];
+    const bool pass = (e >= smin) && (e <= smax);
+    go[c] = pass ? g_scale[3 * g + c] * e : 0.f;
+  }
+  // quaternion: normalised (o[3:7] + (1,0,0,0)); normal = column argmin(s) of R(q)
+  const float qw = dquat[4 * g + 0], qx = dquat[4 * g + 1], qy = dquat[4 * g + 2],
+              qz = dquat[4 * g + 3];
+  float gq[4] = {g_quat[4 * g + 0], g_quat[4 * g + 1], g_quat[4 * g + 2], g_quat[4 * g + 3]};
+  const int ax = argmin3(sc[0], sc[1], sc[2]);
+  float G[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  G[0 + ax] = g_normal[3 * g + 0];
+  G[3 + ax] = g_normal[3 * g + 1];
+  G[6 + ax] = g_normal[3 * g + 2];
+  rot_vjp(qw, qx, qy, qz, G, gq);
+  const float rw = o[3] + 1.0f, rx = o[4], ry = o[5], rz = o[6];
+  const float rn = sqrtf(rw * rw + rx * rx + ry * ry + rz * rz);
+  if (rn >= 1e-12f) {
+    const float dot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
+    go[3] = (gq[0] - qw * dot) / rn;
+    go[4] = (gq[1] - qx * dot) / rn;
+    go[5] = (gq[2] - qy * dot) / rn;
+    go[6] = (gq[3] - qz * dot) / rn;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) go[3 + c] = gq[c] / 1e-12f;
+  }
+#pragma unroll
+  for (int c = 0; c < 7; ++c) g_o_out[(size_t)(oo + c) * ld + r] = go[c];
+  // means = c + offset * l  (each (anchor, slot) appears once per view)
+  const int a = active[r];
+  float *goff = g_offsets + ((size_t)a * n + sl) * 3;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double l = exp((double)log_scale[3 * a + c]);
+    atomicAdd(goff + c, (float)((double)g_means[3 * g + c] * l));
+  }
+}
+
+// Backward, part 2 (anchor-parallel): g_h = W2_h^T g_o, tanh backward ->
+// g_pre (feature-major), embedding grads W1^T g_pre, log-scale grads, and the
+// input block x (feature-major + a ones row) for the weight gradients.
+__global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
+    vsx_decoder W, const int32_t *__restrict__ active, int32_t n_active,
+    const double *__restrict__ centers, const float *__restrict__ emb,
+    const float *__restrict__ log_scale, const float *__restrict__ offsets, vsx_camera cam,
+    double lod_ref, const float *__restrict__ cache_h, const float *__restrict__ g_means,
+    const float *__restrict__ g_o, float *__restrict__ g_emb, float *__restrict__ g_log_scale,
+    float *__restrict__ xs, float *__restrict__ g_pre_out) {
   extern __shared__ __align__(16) float smem[];
   const int n = W.n;
   DecSmem s = dec_smem_carve(smem, n);
   dec_load_weights(W, s);
-  const float smax = (float)max_scale, smin = (float)kMinScale;
   const size_t ld = cache_ld(n_active);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_active; r += gridDim.x * blockDim.x) {
     const int a = active[r];
-    float x[kInDim];
-    dec_inputs(centers, emb, a, cam, lod_ref, x);
+    {
+      float x[kInDim];
+      dec_inputs(centers, emb, a, cam, lod_ref, x);
 #pragma unroll
-    for (int i = 0; i < kInDim; ++i) xs[(size_t)i * ld + r] = x[i];
-    xs[(size_t)kInDim * ld + r] = 1.0f;
-    float gx[kInDim];
+      for (int i = 0; i < kInDim; ++i) xs[(size_t)i * ld + r] = x[i];
+      xs[(size_t)kInDim * ld + r] = 1.0f;
+    }
+    // log-scale grads: sum over the anchor's slots of g_mean * offset
+    {
+      double gl[3] = {0.0, 0.0, 0.0};
+      for (int sl = 0; sl < n; ++sl) {
+        const size_t g = (size_t)r * n + sl;
+        const float *off = offsets + ((size_t)a * n + sl) * 3;
 #pragma unroll
-    for (int i = 0; i < kInDim; ++i) gx[i] = 0.f;
-    const double l[3] = {exp((double)log_scale[3 * a + 0]), exp((double)log_scale[3 * a + 1]),
-                         exp((double)log_scale[3 * a + 2])};
-    double gl[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c < 3; ++c) gl[c] += (double)g_means[3 * g + c] * (double)off[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        atomicAdd(g_log_scale + 3 * a + c, (float)(gl[c] * exp((double)log_scale[3 * a + c])));
+    }
+    float gx[kEmbed];
+#pragma unroll
+    for (int i = 0; i < kEmbed; ++i) gx[i] = 0.f;
     for (int h = 0; h < 3; ++h) {
       const int ow = dec_head_w(h, n), oo = dec_head_off(h, n);
       float gh[64];
 #pragma unroll
       for (int k = 0; k < 64; ++k) gh[k] = 0.f;
-      if (h < 2) {
-        for (int j = 0; j < ow; ++j) {
-          const float o = cache_o[(size_t)(oo + j) * ld + r];
-          const float sg = sigmoidf_(o);
-          const float up = (h == 0) ? g_opacity[(size_t)r * n + j] : g_color[(size_t)r * 3 * n + j];
-          const float go = up * sg * (1.f - sg);
-          g_o_out[(size_t)(oo + j) * ld + r] = go;
-          const float4 *w = reinterpret_cast<const float4 *>(s.w2t + (oo + j) * 64);
+      for (int j = 0; j < ow; ++j) {
+        const float go = g_o[(size_t)(oo + j) * ld + r];
+        const float4 *w = reinterpret_cast<const float4 *>(s.w2t + (oo + j) * 64);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 wv = w[q];
-            gh[4 * q + 0] = fmaf(go, wv.x, gh[4 * q + 0]);
-            gh[4 * q + 1] = fmaf(go, wv.y, gh[4 * q + 1]);
-            gh[4 * q + 2] = fmaf(go, wv.z, gh[4 * q + 2]);
-            gh[4 * q + 3] = fmaf(go, wv.w, gh[4 * q + 3]);
-          }
-        }
-      } else {
-        for (int sl = 0; sl < n; ++sl) {
-          const size_t g = (size_t)r * n + sl;
-          float o[7], go[7];
-#pragma unroll
-          for (int c = 0; c < 7; ++c) o[c] = cache_o[(size_t)(oo + 7 * sl + c) * ld + r];
-          // scales: clamp(exp(o), 1e-6, max) — gradient passes inside [min, max]
-          float sc[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const float e = expf(o[c]);
-            sc[c] = dscale[3 * g + c];
-            const bool pass = (e >= smin) && (e <= smax);
-            go[c] = pass ? g_scale[3 * g + c] * e : 0.f;
-          }
-          // quaternion: normalised (o[3:7] + (1,0,0,0)); normal = column argmin(s) of R(q)
-          const float qw = dquat[4 * g + 0], qx = dquat[4 * g + 1], qy = dquat[4 * g + 2],
-                      qz = dquat[4 * g + 3];
-          float gq[4] = {g_quat[4 * g + 0], g_quat[4 * g + 1], g_quat[4 * g + 2],
-                         g_quat[4 * g + 3]};
-          const int ax = argmin3(sc[0], sc[1], sc[2]);
-          float G[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          G[0 + ax] = g_normal[3 * g + 0];
-          G[3 + ax] = g_normal[3 * g + 1];
-          G[6 + ax] = g_normal[3 * g + 2];
-          rot_vjp(qw, qx, qy, qz, G, gq);
-          const float rw = o[3] + 1.0f, rx = o[4], ry = o[5], rz = o[6];
-          const float rn = sqrtf(rw * rw + rx * rx + ry * ry + rz * rz);
-          if (rn >= 1e-12f) {
-            const float dot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
-            go[3] = (gq[0] - qw * dot) / rn;
-            go[4] = (gq[1] - qx * dot) / rn;
-            go[5] = (gq[2] - qy * dot) / rn;
-            go[6] = (gq[3] - qz * dot) / rn;
-          } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) go[3 + c] = gq[c] / 1e-12f;
-          }
-#pragma unroll
-          for (int c = 0; c < 7; ++c) {
-            g_o_out[(size_t)(oo + 7 * sl + c) * ld + r] = go[c];
-            const float4 *w = reinterpret_cast<const float4 *>(s.w2t + (oo + 7 * sl + c) * 64);
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const float4 wv = w[q];
-              gh[4 * q + 0] = fmaf(go[c], wv.x, gh[4 * q + 0]);
-              gh[4 * q + 1] = fmaf(go[c], wv.y, gh[4 * q + 1]);
-              gh[4 * q + 2] = fmaf(go[c], wv.z, gh[4 * q + 2]);
-              gh[4 * q + 3] = fmaf(go[c], wv.w, gh[4 * q + 3]);
-            }
-          }
-          // means = c + offset * l
-          const float *off = offsets + ((size_t)a * n + sl) * 3;
-          float *goff = g_offsets + ((size_t)a * n + sl) * 3;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const float gm = g_means[3 * g + c];
-            atomicAdd(goff + c, (float)((double)gm * l[c]));
-            gl[c] += (double)gm * (double)off[c];
-          }
+        for (int q = 0; q < 16; ++q) {
+          const float4 wv = w[q];
+          gh[4 * q + 0] = fmaf(go, wv.x, gh[4 * q + 0]);
+          gh[4 * q + 1] = fmaf(go, wv.y, gh[4 * q + 1]);
+          gh[4 * q + 2] = fmaf(go, wv.z, gh[4 * q + 2]);
+          gh[4 * q + 3] = fmaf(go, wv.w, gh[4 * q + 3]);
         }
       }
       // tanh backward, input-block cotangent
@@ -377,8 +391,214 @@ __global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
     }
 #pragma unroll
     for (int i = 0; i < kEmbed; ++i) atomicAdd(g_emb + (size_t)a * kEmbed + i, gx[i]);
+  }
+}
+
+// ------------------------------------------------- anchor backward on mma.sync
+//
+// The anchor part of the backward is two small GEMMs per anchor tile:
+//   g_h  [16 x 64] = g_o_h [16 x ow_h] . W2_h^T         per head (block diagonal)
+//   g_x  [16 x 32] = sum_h (g_h (.) (1 - h^2)) [16 x 64] . W1_h[0:32]^T
+// One warp owns 16 anchors and runs both on the tensor cores with
+// mma.sync.m16n8k8 tf32, 3xTF32 split (fp32-level accuracy). The second GEMM
+// consumes the first's accumulators directly as its A operand: the C
+// fragment of an n-tile (columns 2t, 2t+1) is the A fragment of a k-step whose
+// K positions (t, t+4) are mapped to hidden units (2t, 2t+1) — the W1 image is
+// laid out with that permutation. Weights live in shared memory as
+// fragment-ordered hi/lo images (decoder_bwd_image_kernel), one float4 per
+// (k-step, n-tile, lane).
+
+__host__ __device__ inline int dbw_ks(int h, int n) { return (dec_head_w(h, n) + 7) / 8; }
+__host__ __device__ inline int dbw_ks_total(int n) { return dbw_ks(0, n) + dbw_ks(1, n) + dbw_ks(2, n); }
+__host__ __device__ inline size_t dbw_w2_floats(int n) { return (size_t)dbw_ks_total(n) * 8 * 32 * 4; }
+constexpr size_t kDbwW1Floats = (size_t)24 * 4 * 32 * 4;
+__host__ __device__ inline size_t dbw_image_floats(int n) { return dbw_w2_floats(n) + kDbwW1Floats; }
+
+__device__ __forceinline__ void split_rna(float v, float &hi, float &lo) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+  hi = __uint_as_float(h);
+  uint32_t l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(v - hi));
+  lo = __uint_as_float(l);
+}
+
+__global__ void decoder_bwd_image_kernel(vsx_decoder W, float4 *__restrict__ img) {
+  const int n = W.n;
+  const int kst = dbw_ks_total(n);
+  const int e_w2 = kst * 8 * 32;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < e_w2 + 24 * 4 * 32;
+       e += gridDim.x * blockDim.x) {
+    float v0, v1;
+    if (e < e_w2) {
+      const int lane = e & 31, nt = (e >> 5) & 7, ksg = e >> 8;
+      int h = 0, ks = ksg;
+      while (ks >= dbw_ks(h, n)) ks -= dbw_ks(h++, n);
+      const int ow = dec_head_w(h, n);
+      const int g = lane >> 2, t = lane & 3;
+      const int hid = nt * 8 + g, j0 = ks * 8 + t, j1 = j0 + 4;  // B[k=j][n=hidden]
+      v0 = j0 < ow ? W.w2[h][hid * ow + j0] : 0.f;
+      v1 = j1 < ow ? W.w2[h][hid * ow + j1] : 0.f;
+    } else {
+      const int e2 = e - e_w2;
+      const int lane = e2 & 31, nt = (e2 >> 5) & 3, ks = e2 >> 7;  // ks over 192 hidden
+      const int g = lane >> 2, t = lane & 3;
+      const int i = nt * 8 + g;                                  // embedding input
+      const int hid0 = ks * 8 + 2 * t, hid1 = hid0 + 1;          // K positions t, t+4
+      v0 = W.w1[hid0 / 64][i * 64 + hid0 % 64];
+      v1 = W.w1[hid1 / 64][i * 64 + hid1 % 64];
+    }
+    float h0, l0, h1, l1;
+    split_rna(v0, h0, l0);
+    split_rna(v1, h1, l1);
+    img[e] = make_float4(h0, h1, l0, l1);
+  }
+}
+
+__device__ __forceinline__ void mma_tf32_16x8x8(float (&d)[4], uint32_t a0, uint32_t a1,
+                                                uint32_t a2, uint32_t a3, uint32_t b0,
+                                                uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// d += a . b with a = (ah + al), b = (bh + bl): al.bh + ah.bl + ah.bh
+__device__ __forceinline__ void mma3x(float (&d)[4], const uint32_t (&ah)[4],
+                                      const uint32_t (&al)[4], float4 b) {
+  const uint32_t bh0 = __float_as_uint(b.x), bh1 = __float_as_uint(b.y);
+  const uint32_t bl0 = __float_as_uint(b.z), bl1 = __float_as_uint(b.w);
+  mma_tf32_16x8x8(d, al[0], al[1], al[2], al[3], bh0, bh1);
+  mma_tf32_16x8x8(d, ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+  mma_tf32_16x8x8(d, ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+}
+
+__device__ __forceinline__ void split_trunc(float v, uint32_t &hi, uint32_t &lo) {
+  hi = __float_as_uint(v) & 0xffffe000u;
+  lo = __float_as_uint(v - __uint_as_float(hi));
+}
+
+constexpr int kDbwWarps = 8;
+
+__global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kernel(
+    int n, const float4 *__restrict__ img, const int32_t *__restrict__ active, int32_t n_active,
+    const double *__restrict__ centers, const float *__restrict__ emb,
+    const float *__restrict__ log_scale, const float *__restrict__ offsets, vsx_camera cam,
+    double lod_ref, const float *__restrict__ cache_h, const float *__restrict__ g_means,
+    const float *__restrict__ g_o, float *__restrict__ g_emb, float *__restrict__ g_log_scale,
+    float *__restrict__ xs, float *__restrict__ g_pre_out) {
+  extern __shared__ __align__(16) float4 dimg[];
+  const int kst = dbw_ks_total(n);
+  const int nimg = (int)(dbw_image_floats(n) / 4);
+  for (int e = threadIdx.x; e < nimg; e += blockDim.x) dimg[e] = img[e];
+  __syncthreads();
+  const float4 *w2i = dimg, *w1i = dimg + kst * 8 * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const size_t ld = cache_ld(n_active);
+  const int n_tiles = (n_active + 15) / 16;
+  for (int tile = blockIdx.x * kDbwWarps + warp; tile < n_tiles; tile += gridDim.x * kDbwWarps) {
+    const int r0 = tile * 16;
+    // ---- per-anchor scalar work: lanes 0-15 write the input block, 16-31 the log-scale grads
+    {
+      const int r = r0 + (lane & 15);
+      if (r < n_active) {
+        const int a = active[r];
+        if (lane < 16) {
+          float x[kInDim];
+          dec_inputs(centers, emb, a, cam, lod_ref, x);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) atomicAdd(g_log_scale + 3 * a + c, (float)(gl[c] * l[c]));
+          for (int i = 0; i < kInDim; ++i) xs[(size_t)i * ld + r] = x[i];
+          xs[(size_t)kInDim * ld + r] = 1.0f;
+        } else {
+          double gl[3] = {0.0, 0.0, 0.0};
+          for (int sl = 0; sl < n; ++sl) {
+            const size_t gg = (size_t)r * n + sl;
+            const float *off = offsets + ((size_t)a * n + sl) * 3;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) gl[c] += (double)g_means[3 * gg + c] * (double)off[c];
+          }
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            atomicAdd(g_log_scale + 3 * a + c, (float)(gl[c] * exp((double)log_scale[3 * a + c])));
+        }
+      }
+    }
+    const int ra = r0 + g, rb = r0 + g + 8;
+    const bool va = ra < n_active, vb = rb < n_active;
+    float dx[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dx[q][0] = dx[q][1] = dx[q][2] = dx[q][3] = 0.f;
+    int ksg = 0;
+    for (int h = 0; h < 3; ++h) {
+      const int ow = dec_head_w(h, n), oo = dec_head_off(h, n), nks = dbw_ks(h, n);
+      float c[8][4];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = c[q][2] = c[q][3] = 0.f;
+      for (int ks = 0; ks < nks; ++ks, ++ksg) {
+        const int j0 = ks * 8 + t, j1 = j0 + 4;
+        const float a0 = (va && j0 < ow) ? g_o[(size_t)(oo + j0) * ld + ra] : 0.f;
+        const float a1 = (vb && j0 < ow) ? g_o[(size_t)(oo + j0) * ld + rb] : 0.f;
+        const float a2 = (va && j1 < ow) ? g_o[(size_t)(oo + j1) * ld + ra] : 0.f;
+        const float a3 = (vb && j1 < ow) ? g_o[(size_t)(oo + j1) * ld + rb] : 0.f;
+        uint32_t ah[4], al[4];
+        split_trunc(a0, ah[0], al[0]);
+        split_trunc(a1, ah[1], al[1]);
+        split_trunc(a2, ah[2], al[2]);
+        split_trunc(a3, ah[3], al[3]);
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) mma3x(c[nt], ah, al, w2i[(ksg * 8 + nt) * 32 + lane]);
+      }
+      // tanh backward -> g_pre (stored), then the W1 GEMM over this head's 8 k-steps
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const int k0 = h * 64 + nt * 8 + 2 * t;
+        const float *h0 = cache_h + (size_t)k0 * ld, *h1 = h0 + ld;
+        float *p0 = g_pre_out + (size_t)k0 * ld, *p1 = p0 + ld;
+        if (va) {
+          const float x0 = h0[ra], x1 = h1[ra];
+          c[nt][0] *= 1.f - x0 * x0;
+          c[nt][1] *= 1.f - x1 * x1;
+          p0[ra] = c[nt][0];
+          p1[ra] = c[nt][1];
+        } else {
+          c[nt][0] = c[nt][1] = 0.f;
+        }
+        if (vb) {
+          const float x0 = h0[rb], x1 = h1[rb];
+          c[nt][2] *= 1.f - x0 * x0;
+          c[nt][3] *= 1.f - x1 * x1;
+          p0[rb] = c[nt][2];
+          p1[rb] = c[nt][3];
+        } else {
+          c[nt][2] = c[nt][3] = 0.f;
+        }
+        // A fragment of k-step (h, nt): positions (t, t+4) = hidden (2t, 2t+1)
+        uint32_t ah[4], al[4];
+        split_trunc(c[nt][0], ah[0], al[0]);  // (row g,   k t)
+        split_trunc(c[nt][2], ah[1], al[1]);  // (row g+8, k t)
+        split_trunc(c[nt][1], ah[2], al[2]);  // (row g,   k t+4)
+        split_trunc(c[nt][3], ah[3], al[3]);  // (row g+8, k t+4)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mma3x(dx[q], ah, al, w1i[((h * 8 + nt) * 4 + q) * 32 + lane]);
+      }
+    }
+    // ---- embedding grads: D fragment (anchor g / g+8, input 8q + 2t, +1)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i0 = q * 8 + 2 * t;
+      if (va) {
+        float *ge = g_emb + (size_t)active[ra] * kEmbed + i0;
+        atomicAdd(ge, dx[q][0]);
+        atomicAdd(ge + 1, dx[q][1]);
+      }
+      if (vb) {
+        float *ge = g_emb + (size_t)active[rb] * kEmbed + i0;
+        atomicAdd(ge, dx[q][2]);
+        atomicAdd(ge + 1, dx[q][3]);
+      }
+    }
   }
 }
 
@@ -497,7 +717,9 @@ extern "C" int vsx_decode_fwd(vsx_decoder W, const int32_t *active, int32_t n_ac
 }
 
 extern "C" size_t vsx_decode_bwd_ws_bytes(int32_t n, int32_t n_active) {
-  return sizeof(float) * cache_ld(n_active) * (size_t)(kInDim + 1 + 192 + 11 * n) + 256;
+  // xs [37][ld] + g_pre [192][ld] + g_o [11n][ld] + the mma weight image
+  return sizeof(float) * cache_ld(n_active) * (size_t)(kInDim + 1 + 192 + 11 * n) +
+         sizeof(float) * dbw_image_floats(n) + 256;
 }
 
 extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t *active,
@@ -518,18 +740,41 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
   float *xs = static_cast<float *>(ws);
   float *g_pre = xs + (size_t)(kInDim + 1) * ld;
   float *g_o = g_pre + (size_t)192 * ld;
-  const size_t smem = dec_smem_bytes(n);
-  VSX_CUDA_TRY(cudaFuncSetAttribute(decode_bwd_anchor_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  decode_bwd_anchor_kernel<<<dec_grid(n_active, smem), 128, smem, st>>>(
-      W, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, max_scale, cache_h,
-      cache_o, scale, quat, g_means, g_opacity, g_color, g_scale, g_quat, g_normal, g_emb,
-      g_log_scale, g_offsets, xs, g_o, g_pre);
-  VSX_LAUNCH_CHECK("decode_bwd_anchor");
+  const int64_t ng = (int64_t)n_active * n;
+  decode_bwd_gauss_kernel<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(
+      n, active, n_active, log_scale, offsets, max_scale, cache_o, scale, quat, g_means,
+      g_opacity, g_color, g_scale, g_quat, g_normal, g_offsets, g_o);
+  VSX_LAUNCH_CHECK("decode_bwd_gauss");
   static const bool use_tc = [] {
     const char *e = getenv("VSX_DECODE_TC");
     return !(e && e[0] == '0');
   }();
+  if (use_tc) {  // anchor GEMMs on mma.sync (tensor cores)
+    float4 *dimg = reinterpret_cast<float4 *>(g_o + (size_t)11 * n * ld);
+    decoder_bwd_image_kernel<<<32, 256, 0, st>>>(W, dimg);
+    VSX_LAUNCH_CHECK("decoder_bwd_image");
+    const size_t smem = sizeof(float) * dbw_image_floats(n);
+    VSX_REQUIRE(smem <= 113 * 1024, "decode_bwd: n=%d too large for the mma weight image", n);
+    VSX_CUDA_TRY(cudaFuncSetAttribute(decode_bwd_anchor_mma_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int warps_needed = (n_active + 15) / 16;
+    const int grid = std::max(1, std::min(2 * sms, (warps_needed + kDbwWarps - 1) / kDbwWarps));
+    decode_bwd_anchor_mma_kernel<<<grid, kDbwWarps * 32, smem, st>>>(
+        n, dimg, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, cache_h,
+        g_means, g_o, g_emb, g_log_scale, xs, g_pre);
+    VSX_LAUNCH_CHECK("decode_bwd_anchor_mma");
+  } else {
+    const size_t smem = dec_smem_bytes(n);
+    VSX_CUDA_TRY(cudaFuncSetAttribute(decode_bwd_anchor_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    decode_bwd_anchor_kernel<<<dec_grid(n_active, smem), 128, smem, st>>>(
+        W, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, cache_h, g_means, g_o,
+        g_emb, g_log_scale, xs, g_pre);
+    VSX_LAUNCH_CHECK("decode_bwd_anchor");
+  }
   if (use_tc && 11 * n <= 128)  // tensor-core weight gradients (decode_tc.cu)
     return decoder_wgrad_tc(g_o, cache_h, g_pre, xs, n_active, ld, n, dW, st);
   // dW1_h = X^T Gpre_h (+ db1 via the ones row of X)

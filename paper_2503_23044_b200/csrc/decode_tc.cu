@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
   extern __shared__ __align__(1024) float tsm[];
   __shared__ uint64_t mbar;
   __shared__ uint32_t tslot;
+  __shared__ float s_b2[11 * 13];
   const int n = W.n;
   const TcDims dims = tc_dims(n);
   TcSmem s;
@@ -148,6 +149,8 @@ __global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
     const int n4 = 2 * dims.np_total * kTcK2 / 4;
     for (int i = tid; i < n4; i += 256) dst[i] = src[i];
   }
+  for (int j = tid; j < 11 * n; j += 256)
+    s_b2[j] = j < n ? W.b2[0][j] : (j < 4 * n ? W.b2[1][j - n] : W.b2[2][j - 4 * n]);
   if (tid < 32) umma::tmem_alloc(&tslot, 256);
   if (tid == 0) umma::mbar_init(&mbar, 1);
   umma::fence_before_sync();
@@ -157,7 +160,6 @@ __global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
   const uint32_t lane = (uint32_t)(warp * 32) << 16;
   const uint32_t d1 = tbase, d2 = tbase + 64;
   uint32_t phase = 0;
-  const float smax = (float)max_scale, smin = (float)kMinScale;
   const int n_tiles = (n_active + kTcRows - 1) / kTcRows;
   const size_t ld = cache_ld(n_active);
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -194,10 +196,6 @@ __global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
         st_split4(s.x_hi, s.x_lo, umma::kmajor_offset(t, 4 * q, kTcK1), x[4 * q], x[4 * q + 1],
                   x[4 * q + 2], x[4 * q + 3]);
     }
-    bool bad = false;
-    const double l0 = valid ? exp((double)log_scale[3 * a + 0]) : 1.0;
-    const double l1 = valid ? exp((double)log_scale[3 * a + 1]) : 1.0;
-    const double l2 = valid ? exp((double)log_scale[3 * a + 2]) : 1.0;
     for (int h = 0; h < 3; ++h) {
       // W1_h image -> smem
       {
@@ -245,79 +243,92 @@ __global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
       umma::mbar_wait(&mbar, phase);
       phase ^= 1u;
       umma::fence_after_sync();
+      // raw head outputs (+ b2) -> cache_o; the per-gaussian activations run
+      // in decode_gauss_kernel with one thread per gaussian
       const int width = (h == 0 ? 1 : (h == 1 ? 3 : 7)) * n;
       const int oo = h == 0 ? 0 : (h == 1 ? n : 4 * n);
-      if (h < 2) {
-        for (int c = 16 * wg; c < dims.np[h]; c += 32) {
-          float v[16];
-          umma::tmem_ld16(d2 + lane + (uint32_t)c, v);
-          umma::tmem_ld_wait();
+      for (int c = 16 * wg; c < dims.np[h]; c += 32) {
+        float v[16];
+        umma::tmem_ld16(d2 + lane + (uint32_t)c, v);
+        umma::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int j = c + i;
-            if (valid && j < width) {
-              const float o = v[i] + W.b2[h][j];
-              if (cache_o) cache_o[(size_t)(oo + j) * ld + r] = o;
-              const float sg = sigm(o);
-              bad |= !isfinite(sg);
-              if (h == 0) opacity[(size_t)r * n + j] = sg;
-              else color[(size_t)r * 3 * n + j] = sg;
-            }
-          }
-        }
-      } else {
-        for (int sl = wg; sl < n; sl += 2) {
-          float o[16];
-          umma::tmem_ld16(d2 + lane + (uint32_t)(7 * sl), o);  // columns 7sl .. 7sl+15
-          umma::tmem_ld_wait();
-          if (!valid) continue;
-#pragma unroll
-          for (int c = 0; c < 7; ++c) {
-            o[c] += W.b2[2][7 * sl + c];
-            if (cache_o) cache_o[(size_t)(oo + 7 * sl + c) * ld + r] = o[c];
-          }
-          const size_t g = (size_t)r * n + sl;
-          float sc[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            sc[c] = fminf(fmaxf(expf(o[c]), smin), smax);
-            scale[3 * g + c] = sc[c];
-          }
-          float qw = o[3] + 1.0f, qx = o[4], qy = o[5], qz = o[6];
-          const float qn = fmaxf(sqrtf(qw * qw + qx * qx + qy * qy + qz * qz), 1e-12f);
-          qw /= qn;
-          qx /= qn;
-          qy /= qn;
-          qz /= qn;
-          quat[4 * g + 0] = qw;
-          quat[4 * g + 1] = qx;
-          quat[4 * g + 2] = qy;
-          quat[4 * g + 3] = qz;
-          float R[9];
-          quat_to_rot(qw, qx, qy, qz, R);
-          const int ax = argmin3(sc[0], sc[1], sc[2]);
-          normal[3 * g + 0] = R[0 + ax];
-          normal[3 * g + 1] = R[3 + ax];
-          normal[3 * g + 2] = R[6 + ax];
-          const float *off = offsets + ((size_t)a * n + sl) * 3;
-          const double m0 = dadd(centers[3 * a + 0], dmul((double)off[0], l0));
-          const double m1 = dadd(centers[3 * a + 1], dmul((double)off[1], l1));
-          const double m2 = dadd(centers[3 * a + 2], dmul((double)off[2], l2));
-          means[3 * g + 0] = m0;
-          means[3 * g + 1] = m1;
-          means[3 * g + 2] = m2;
-          bad |= !(isfinite(sc[0]) && isfinite(sc[1]) && isfinite(sc[2]) && isfinite(qw) &&
-                   isfinite(qx) && isfinite(qy) && isfinite(qz) && isfinite(m0) &&
-                   isfinite(m1) && isfinite(m2));
+        for (int i = 0; i < 16; ++i) {
+          const int j = c + i;
+          if (valid && j < width) cache_o[(size_t)(oo + j) * ld + r] = v[i] + s_b2[oo + j];
         }
       }
       umma::fence_before_sync();
     }
-    if (bad) atomicOr(status, VSX_STATUS_NONFINITE);
   }
   umma::fence_before_sync();
   __syncthreads();
   if (tid < 32) umma::tmem_dealloc(tbase, 256);
+}
+
+// Per-gaussian activations of the decoded heads (decoder.py:160-180), one
+// thread per gaussian g = r * n + sl (coalesced output rows), reading the raw
+// outputs from the feature-major cache_o written by decode_fwd_tc_kernel.
+__global__ void __launch_bounds__(256) decode_gauss_kernel(
+    int n, const int32_t *__restrict__ active, int32_t n_active, const double *__restrict__ centers,
+    const float *__restrict__ log_scale, const float *__restrict__ offsets, double max_scale,
+    const float *__restrict__ cache_o, double *__restrict__ means, float *__restrict__ opacity,
+    float *__restrict__ color, float *__restrict__ scale, float *__restrict__ quat,
+    float *__restrict__ normal, int32_t *__restrict__ status) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)n_active * n;
+  bool bad = false;
+  if (g < total) {
+    const int r = (int)(g / n), sl = (int)(g % n);
+    const int a = active[r];
+    const size_t ld = cache_ld(n_active);
+    const float *col = cache_o + r;
+    const float op = sigm(col[(size_t)sl * ld]);
+    opacity[g] = op;
+    bad |= !isfinite(op);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float v = sigm(col[(size_t)(n + 3 * sl + c) * ld]);
+      color[3 * g + c] = v;
+      bad |= !isfinite(v);
+    }
+    float o[7];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) o[c] = col[(size_t)(4 * n + 7 * sl + c) * ld];
+    const float smax = (float)max_scale, smin = (float)kMinScale;
+    float sc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      sc[c] = fminf(fmaxf(expf(o[c]), smin), smax);
+      scale[3 * g + c] = sc[c];
+    }
+    float qw = o[3] + 1.0f, qx = o[4], qy = o[5], qz = o[6];
+    const float qn = fmaxf(sqrtf(qw * qw + qx * qx + qy * qy + qz * qz), 1e-12f);
+    qw /= qn;
+    qx /= qn;
+    qy /= qn;
+    qz /= qn;
+    quat[4 * g + 0] = qw;
+    quat[4 * g + 1] = qx;
+    quat[4 * g + 2] = qy;
+    quat[4 * g + 3] = qz;
+    float R[9];
+    quat_to_rot(qw, qx, qy, qz, R);
+    const int ax = argmin3(sc[0], sc[1], sc[2]);
+    normal[3 * g + 0] = R[0 + ax];
+    normal[3 * g + 1] = R[3 + ax];
+    normal[3 * g + 2] = R[6 + ax];
+    const float *off = offsets + ((size_t)a * n + sl) * 3;
+    const double m0 = dadd(centers[3 * a + 0], dmul((double)off[0], exp((double)log_scale[3 * a + 0])));
+    const double m1 = dadd(centers[3 * a + 1], dmul((double)off[1], exp((double)log_scale[3 * a + 1])));
+    const double m2 = dadd(centers[3 * a + 2], dmul((double)off[2], exp((double)log_scale[3 * a + 2])));
+    means[3 * g + 0] = m0;
+    means[3 * g + 1] = m1;
+    means[3 * g + 2] = m2;
+    bad |= !(isfinite(sc[0]) && isfinite(sc[1]) && isfinite(sc[2]) && isfinite(qw) &&
+             isfinite(qx) && isfinite(qy) && isfinite(qz) && isfinite(m0) && isfinite(m1) &&
+             isfinite(m2));
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(status, VSX_STATUS_NONFINITE);
 }
 
 // ---------------------------------------------------------------- weight gradients
@@ -330,9 +341,10 @@ __global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
 //   C2[m][i] = sum_r dPre[r][m] * [X | 1][r][i] M = 192 hidden (two 128 tiles), N = 37 (pad 48)
 //              -> dW1_h[i][m] and db1 (ones column)
 // Each CTA accumulates its K-chunks in TMEM and adds its partial result to
-// the global gradients with one atomicAdd per element at the end.
+// the global gradients with one atomicAdd per element at the end. Stages are
+// double-buffered: 8 warps split/stage chunk i+1 while the MMAs of chunk i run.
 
-constexpr int kWgKc = 32;    // anchors per stage (4 MMA k-steps)
+constexpr int kWgKc = 16;    // anchors per stage (2 MMA k-steps)
 constexpr int kWgN1 = 208;   // 192 hidden + ones row, padded to 16
 constexpr int kWgN2 = 48;    // 36 inputs + ones row, padded to 16
 
@@ -340,9 +352,9 @@ struct WgSmem {
   float *a1_hi, *a1_lo, *b1_hi, *b1_lo, *a2_hi, *a2_lo, *b2_hi, *b2_lo;
 };
 
-inline size_t wg_smem_bytes() {
-  return sizeof(float) * (size_t)2 * kWgKc * (128 + kWgN1 + 256 + kWgN2);
-}
+constexpr int kWgStageFloats = 2 * kWgKc * (128 + kWgN1 + 256 + kWgN2);
+
+inline size_t wg_smem_bytes() { return sizeof(float) * (size_t)2 * kWgStageFloats; }
 
 // Stage rows [0, rows) of a feature-major [rows_valid x K] matrix, anchors
 // [k0, k0 + 32), into a hi/lo K-major tile of `rows` rows. Rows >= rows_valid
@@ -386,15 +398,9 @@ __device__ __forceinline__ void wg_stage(float *hi, float *lo, const float *__re
   }
 }
 
-__global__ void __launch_bounds__(128, 1) decoder_wgrad_tc_kernel(
-    const float *__restrict__ g_o, const float *__restrict__ cache_h,
-    const float *__restrict__ g_pre, const float *__restrict__ xs, int64_t K, size_t ld, int n,
-    vsx_decoder_grads dW) {
-  extern __shared__ __align__(1024) float wsm[];
-  __shared__ uint64_t mbar;
-  __shared__ uint32_t tslot;
+__device__ __forceinline__ WgSmem wg_carve(float *base) {
   WgSmem s;
-  s.a1_hi = wsm;
+  s.a1_hi = base;
   s.a1_lo = s.a1_hi + 128 * kWgKc;
   s.b1_hi = s.a1_lo + 128 * kWgKc;
   s.b1_lo = s.b1_hi + kWgN1 * kWgKc;
@@ -402,28 +408,45 @@ __global__ void __launch_bounds__(128, 1) decoder_wgrad_tc_kernel(
   s.a2_lo = s.a2_hi + 256 * kWgKc;
   s.b2_hi = s.a2_lo + 256 * kWgKc;
   s.b2_lo = s.b2_hi + kWgN2 * kWgKc;
+  return s;
+}
+
+__device__ __forceinline__ void wg_stage_all(const WgSmem &s, const float *g_o,
+                                             const float *cache_h, const float *g_pre,
+                                             const float *xs, int nout, int64_t K, size_t ld,
+                                             int64_t k0) {
+  wg_stage(s.a1_hi, s.a1_lo, g_o, 128, nout, -1, K, ld, k0);
+  wg_stage(s.b1_hi, s.b1_lo, cache_h, kWgN1, 192, 192, K, ld, k0);
+  wg_stage(s.a2_hi, s.a2_lo, g_pre, 256, 192, -1, K, ld, k0);
+  wg_stage(s.b2_hi, s.b2_lo, xs, kWgN2, kInDim + 1, -1, K, ld, k0);  // xs row 36 = ones
+}
+
+__global__ void __launch_bounds__(256, 1) decoder_wgrad_tc_kernel(
+    const float *__restrict__ g_o, const float *__restrict__ cache_h,
+    const float *__restrict__ g_pre, const float *__restrict__ xs, int64_t K, size_t ld, int n,
+    vsx_decoder_grads dW) {
+  extern __shared__ __align__(1024) float wsm[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tslot;
+  const WgSmem sb[2] = {wg_carve(wsm), wg_carve(wsm + kWgStageFloats)};
   const int t = threadIdx.x, warp = t >> 5;
   const int nout = 11 * n;
   if (warp == 0) umma::tmem_alloc(&tslot, 512);
   if (t == 0) umma::mbar_init(&mbar, 1);
+  const int64_t nchunks = (K + kWgKc - 1) / kWgKc;
+  if ((int64_t)blockIdx.x < nchunks)
+    wg_stage_all(sb[0], g_o, cache_h, g_pre, xs, nout, K, ld, (int64_t)blockIdx.x * kWgKc);
+  umma::fence_async_smem();
   umma::fence_before_sync();
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tbase = tslot;
   const uint32_t c1 = tbase, c2a = tbase + kWgN1, c2b = tbase + kWgN1 + kWgN2;
   uint32_t phase = 0;
-  const int64_t nchunks = (K + kWgKc - 1) / kWgKc;
   bool first = true;
-  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const int64_t k0 = ch * kWgKc;
-    wg_stage(s.a1_hi, s.a1_lo, g_o, 128, nout, -1, K, ld, k0);
-    wg_stage(s.b1_hi, s.b1_lo, cache_h, kWgN1, 192, 192, K, ld, k0);
-    wg_stage(s.a2_hi, s.a2_lo, g_pre, 256, 192, -1, K, ld, k0);
-    wg_stage(s.b2_hi, s.b2_lo, xs, kWgN2, kInDim + 1, -1, K, ld, k0);  // xs row 36 = ones
-    umma::fence_async_smem();
-    umma::fence_before_sync();
-    __syncthreads();
-    umma::fence_after_sync();
+  int buf = 0;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, buf ^= 1) {
+    const WgSmem &s = sb[buf];
     if (t == 0) {
       const uint32_t i1 = umma::idesc_tf32(128, kWgN1), i2 = umma::idesc_tf32(128, kWgN2);
       const uint32_t a1h = umma::smem_addr(s.a1_hi), a1l = umma::smem_addr(s.a1_lo);
@@ -450,12 +473,18 @@ __global__ void __launch_bounds__(128, 1) decoder_wgrad_tc_kernel(
       }
       umma::commit(&mbar);
     }
+    // stage the next chunk into the other buffer while the MMAs run
+    const int64_t nx = ch + gridDim.x;
+    if (nx < nchunks) wg_stage_all(sb[buf ^ 1], g_o, cache_h, g_pre, xs, nout, K, ld, nx * kWgKc);
     umma::mbar_wait(&mbar, phase);
     phase ^= 1u;
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
     umma::fence_after_sync();
     first = false;
   }
-  if (!first) {
+  if (!first && t < 128) {  // TMEM lanes 0-127 belong to warps 0-3
     const uint32_t lane = (uint32_t)(warp * 32) << 16;
     // C1 row t = output j: head blocks of dW2 and db2
     const int j = t;
@@ -511,7 +540,7 @@ int decoder_wgrad_tc(const float *g_o, const float *cache_h, const float *g_pre,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t chunks = (K + kWgKc - 1) / kWgKc;
-  decoder_wgrad_tc_kernel<<<(int)std::min<int64_t>(chunks, sms), 128, smem, st>>>(
+  decoder_wgrad_tc_kernel<<<(int)std::min<int64_t>(chunks, sms), 256, smem, st>>>(
       g_o, cache_h, g_pre, xs, K, ld, n, dW);
   VSX_LAUNCH_CHECK("decoder_wgrad_tc");
   return VSX_OK;
@@ -545,6 +574,7 @@ extern "C" int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t 
                                  float *color, float *scale, float *quat, float *normal,
                                  float *cache_h, float *cache_o, int32_t *status, vsx_stream s) {
   VSX_REQUIRE(W.n >= 1 && n_active >= 0 && lod_ref > 0, "decode_fwd_tc: bad arguments");
+  VSX_REQUIRE(cache_o, "decode_fwd_tc: cache_o is required (the activations read it back)");
   VSX_REQUIRE(tc_supported(W.n), "decode_fwd_tc: n=%d not supported by the tensor-core path",
               W.n);
   if (n_active == 0) return VSX_OK;
@@ -559,5 +589,10 @@ extern "C" int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t 
       W, img, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, max_scale, means,
       opacity, color, scale, quat, normal, cache_h, cache_o, status);
   VSX_LAUNCH_CHECK("decode_fwd_tc");
+  const int64_t total = (int64_t)n_active * W.n;
+  decode_gauss_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(s)>>>(
+      W.n, active, n_active, centers, log_scale, offsets, max_scale, cache_o, means, opacity, color,
+      scale, quat, normal, status);
+  VSX_LAUNCH_CHECK("decode_gauss");
   return VSX_OK;
 }

@@ -203,9 +203,11 @@ def decode(dec_abi, n: int, active: torch.Tensor, centers: torch.Tensor, emb: to
     quat = torch.empty((g, 4), dtype=torch.float32, device=dev)
     nrm = torch.empty((g, 3), dtype=torch.float32, device=dev)
     ld = max((na + 3) // 4 * 4, 4)     # cache_ld() of common.cuh: 16-byte aligned rows
+    tc = use_tensor_cores(n)
     ch = torch.empty((192, ld), dtype=torch.float32, device=dev) if keep_cache else None
-    co = torch.empty((11 * n, ld), dtype=torch.float32, device=dev) if keep_cache else None
-    if use_tensor_cores(n):
+    # the tensor-core path always stages the raw head outputs in cache_o
+    co = torch.empty((11 * n, ld), dtype=torch.float32, device=dev) if keep_cache or tc else None
+    if tc:
         img = decoder_image(dec_abi, n)
         call("vsx_decode_fwd_tc", dec_abi, ptr(img), ptr(active), na, ptr(centers), ptr(emb),
              ptr(log_scales), ptr(offsets), view.to_abi(), lod_ref, max_scale, ptr(means),

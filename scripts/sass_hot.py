@@ -14,6 +14,8 @@ ia, isrc, ismp, iex = (h.index("Address"), h.index("Source"),
 stall_cols = [i for i, k in enumerate(h) if k.startswith("stall_")]
 recs = []
 for r in rows[2:]:
+    if r and r[0] == "Kernel Name":
+        break  # only the first kernel of a multi-kernel page
     if len(r) <= iex:
         continue
     smp = float(r[ismp] or 0)
