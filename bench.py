@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU sharded step even at one rank (testing)")
-    ap.add_argument("--cpu-tiles", type=int, default=48,
+    ap.add_argument("--cpu-tiles", type=int, default=400,
                     help="tiles per CPU-baseline sample (evenly spaced over the view)")
     return ap.parse_args()
 
@@ -214,6 +214,15 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture, or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return int(json.loads(p.read_text())[kernel]["bytes"])
+    except Exception:
+        return None
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -339,7 +348,8 @@ def run_vsx(args):
         def step(im, pr, npr, timer=None):
             r = train_step(state, views, im, pr, normal_priors=npr, timer=timer)
             return {"gaussians": r.gaussians, "intersections": r.intersections, "total": r.total,
-                    "rgb": r.rgb, "depth": r.depth, "normal": r.normal}
+                    "rgb": r.rgb, "depth": r.depth, "normal": r.normal,
+                    "live_pairs": r.live_pairs}
     clocks = clock_sampler(local)
     for _ in range(args.warmup):
         step(imgs, priors, nprior)
@@ -371,6 +381,7 @@ def run_vsx(args):
     isect = sum(r["intersections"] for r in reps)
     pixels = sum(v.width * v.height for v in views) * args.steps // world
     splats = sum(r["gaussians"] for r in reps)
+    live_pairs = sum(r.get("live_pairs", 0) for r in reps)
     dom = max(("raster_fwd", "raster_bwd"), key=lambda k: stage_ms.get(k, 0.0))
     per_launch_bytes = raster_bytes(dom, isect, pixels, splats) / stage_n[dom]
     per_launch_s = stage_ms[dom] / 1e3 / stage_n[dom]
@@ -425,14 +436,19 @@ def run_vsx(args):
         "data": "synthetic", "config": desc,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(dom),
                      "peak_src": peaks["src"],
-                     "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_s * 1e3},
+                     "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_s * 1e3,
+                     # the compositor is issue-bound, not HBM-bound: composited
+                     # (pixel, splat) pairs per second of the dominant kernel
+                     "live_pairs_per_launch": live_pairs / max(stage_n[dom], 1),
+                     "pairs_per_s": live_pairs / max(stage_n[dom], 1) / per_launch_s},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk,
         "stages_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
         "per_step": {"gaussians": reps[-1]["gaussians"],
                      "intersections": reps[-1]["intersections"],
+                     "live_pairs": reps[-1].get("live_pairs"),
                      "loss_total": reps[-1]["total"], "loss_rgb": reps[-1]["rgb"],
                      "loss_depth": reps[-1]["depth"], "loss_normal": reps[-1]["normal"]},
     }

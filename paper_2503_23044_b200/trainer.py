@@ -127,6 +127,7 @@ class StepReport:
     grown: int = 0
     intersections: int = 0
     normal: float = 0.0
+    live_pairs: int = 0     # (pixel, splat) pairs composited = sum of per-pixel live counts
 
     def to_json(self) -> str:
         return json.dumps({
@@ -276,7 +277,7 @@ def make_state(scene, cfg: TrainConfig) -> TrainState:
 
 def _to_device_image(x, shape) -> torch.Tensor:
     t = x if torch.is_tensor(x) else torch.as_tensor(np.asarray(x))
-    t = t.to(device="cuda", dtype=torch.float32).contiguous()
+    t = t.to(device="cuda", dtype=torch.float32, non_blocking=True).contiguous()
     if tuple(t.shape) != tuple(shape):
         raise InvalidInput(f"image shape mismatch {tuple(t.shape)} vs {tuple(shape)}")
     return t
@@ -343,10 +344,54 @@ def _span(timer, name):
 
 def _mask_u8(v, shape) -> torch.Tensor:
     t = v if torch.is_tensor(v) else torch.as_tensor(np.asarray(v))
-    t = t.to(device="cuda", dtype=torch.uint8).contiguous()
+    t = t.to(device="cuda", dtype=torch.uint8, non_blocking=True).contiguous()
     if tuple(t.shape) != tuple(shape):
         raise InvalidInput(f"mask shape mismatch {tuple(t.shape)} vs {tuple(shape)}")
     return t
+
+
+_COPY_STREAM = None
+
+
+class _InputStager:
+    """Per-view targets/priors moved to the device on a copy stream.
+
+    All host->device copies of the step are issued up front (non-blocking
+    from pinned host memory), one event per view; view v's compute waits only
+    for its own inputs, so the copies of later views overlap the compute of
+    earlier ones. CUDA inputs pass through untouched.
+    """
+
+    def __init__(self, views, images, priors, have, normal_priors, have_n):
+        global _COPY_STREAM
+        if _COPY_STREAM is None:
+            _COPY_STREAM = torch.cuda.Stream()
+        cur = torch.cuda.current_stream()
+        cs = _COPY_STREAM
+        cs.wait_stream(cur)
+        self.items, self.events = [], []
+        with torch.cuda.stream(cs):
+            for vi, view in enumerate(views):
+                H, W = view.height, view.width
+                gt = _to_device_image(images[vi], (H, W, 3))
+                pd = pv = pn = pnv = None
+                if vi in have:
+                    pd = _to_device_image(priors[vi][0], (H, W))
+                    pv = _mask_u8(priors[vi][1], (H, W))
+                if vi in have_n:
+                    pn = _to_device_image(normal_priors[vi][0], (H, W, 3))
+                    pnv = _mask_u8(normal_priors[vi][1], (H, W))
+                for t in (gt, pd, pv, pn, pnv):
+                    if t is not None:
+                        t.record_stream(cur)  # freed only after the compute stream used it
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                self.items.append((gt, pd, pv, pn, pnv))
+                self.events.append(ev)
+
+    def get(self, vi):
+        torch.cuda.current_stream().wait_event(self.events[vi])
+        return self.items[vi]
 
 
 def train_step(state: TrainState, views: list[CameraView], images: list,
@@ -383,10 +428,12 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     rgb_acc, dep_sum, nrm_sum = sums[:, 0], sums[:, 1], sums[:, 2]
     dep_cnt, nrm_cnt = counts[:, 0], counts[:, 1]
     tile_max = torch.zeros(B, dtype=torch.int64, device=dev)
+    live = torch.zeros((), dtype=torch.int64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     gaussians = 0
     isects = 0
     anchors, agrads = state.anchors, state.anchor_grads
+    stager = _InputStager(views, images, priors, have, normal_priors, have_n)
     for vi, view in enumerate(views):
         H, W = view.height, view.width
         with _span(timer, "cull"):
@@ -405,14 +452,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         tile_max[vi] = torch.diff(Bn.tile_offsets.long()).max()
         # fused objective (K9 inside K5/K6): loss sums in the forward epilogue,
         # cotangents formed on the fly in the backward
-        gt = _to_device_image(images[vi], (H, W, 3))
-        pd = pv = pn = pnv = None
-        if vi in have:
-            pd = _to_device_image(priors[vi][0], (H, W))
-            pv = _mask_u8(priors[vi][1], (H, W))
-        if vi in have_n:
-            pn = _to_device_image(normal_priors[vi][0], (H, W, 3))
-            pnv = _mask_u8(normal_priors[vi][1], (H, W))
+        gt, pd, pv, pn, pnv = stager.get(vi)
         loss = VsxLossDesc(
             gt_rgb=gt.data_ptr(), prior_depth=ptr(pd).value, prior_depth_valid=ptr(pv).value,
             prior_normal=ptr(pn).value, prior_normal_valid=ptr(pnv).value,
@@ -422,6 +462,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             sums=sums[vi].data_ptr(), counts=counts[vi].data_ptr())
         with _span(timer, "raster_fwd"):
             R = D.raster_forward(P, Bn, view, loss=loss)
+        live += R.n_contrib.sum()
         with _span(timer, "raster_bwd"):
             gs = D.raster_backward(P, Bn, view, R, loss=loss)
         with _span(timer, "project_bwd"):
@@ -459,6 +500,6 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         lr=cosine_lr(state.step, cfg.lr_decoder, cfg), supervised_depth_px=supervised,
         geo_pairs=0, geo_patches=0, gaussians=gaussians, transfer_bytes=0, imbalance=1.0,
         max_tile_splats=int(tile_max.max()), seconds=time.perf_counter() - t0,
-        intersections=isects, normal=normal)
+        intersections=isects, normal=normal, live_pairs=int(live))
     state.step += 1
     return report
