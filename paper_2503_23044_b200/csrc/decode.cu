@@ -602,6 +602,207 @@ __global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kerne
   }
 }
 
+// ----------------------------------------------- weight gradients on mma.sync
+//
+// dW2_h[k][j] = sum_r H_h[r][k] g_o[r][j] (+ db2 via a ones column) and
+// dW1_h[i][k] = sum_r X[r][i] g_pre[r][k] (+ db1 via the ones row of X) as one
+// K-split GEMM over the active anchors (K). Each CTA streams its K-chunks of
+// the four feature-major operands into shared memory with cp.async (two
+// stages, 16 anchors each) and its 8 warps own 144 output tiles (m16n8), 18
+// each, accumulated in registers with mma.sync tf32 3xTF32. Per-CTA partial
+// tiles go to a buffer that one reduction kernel folds into the gradients
+// (no atomics). Head blocks of g_o are padded to 16 rows so every m-tile
+// belongs to one head.
+
+__host__ __device__ inline int wm_pad16(int x) { return (x + 15) / 16 * 16; }
+
+constexpr int kWmKc = 16;       // anchors per stage
+constexpr int kWmStride = 20;   // floats per staged row (bank-conflict-free fragments)
+constexpr int kWmGo = 128;      // padded g_o rows (n <= 10: 16 + 32 + 80)
+constexpr int kWmH = 200;       // cache_h rows + ones row (192) + zero rows
+constexpr int kWmGp = 192;      // g_pre rows
+constexpr int kWmX = 48;        // xs rows (36 = ones) + zero rows
+constexpr int kWmRows = kWmGo + kWmH + kWmGp + kWmX;
+constexpr int kWmStageFloats = kWmRows * kWmStride;
+constexpr int kWmTiles = 144;
+constexpr int kWmMaxCtas = 320;
+
+__host__ __device__ inline bool wm_supported(int n) {
+  return wm_pad16(n) + wm_pad16(3 * n) + wm_pad16(7 * n) <= kWmGo;
+}
+
+__device__ __forceinline__ void cp_async16_zfill(float *dst, const float *src, int bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256, 2) decoder_wgrad_mma_kernel(
+    const float *__restrict__ g_o, const float *__restrict__ cache_h,
+    const float *__restrict__ g_pre, const float *__restrict__ xs, int64_t K, size_t ld, int n,
+    float *__restrict__ partial) {
+  extern __shared__ __align__(16) float wms[];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int np0 = wm_pad16(n), np1 = wm_pad16(3 * n);
+  const int go_row0[3] = {0, np0, np0 + np1};
+  const int oo[3] = {0, n, 4 * n};
+  // zero both stages once (padding rows are never written again)
+  for (int e = t; e < 2 * kWmStageFloats; e += 256) wms[e] = 0.f;
+  __syncthreads();
+  const int64_t nchunks = (K + kWmKc - 1) / kWmKc;
+  auto stage_ptr = [&](int s) { return wms + s * kWmStageFloats; };
+  // issue the copies of chunk c into stage s
+  auto issue = [&](int64_t c, int s) {
+    float *base = stage_ptr(s);
+    const int64_t k0 = c * kWmKc;
+    const int valid_rows = 11 * n + 192 + 192 + (kInDim + 1);
+    for (int e = t; e < valid_rows * 4; e += 256) {
+      const int row = e >> 2, q = e & 3;
+      const float *src;
+      int dst_row;
+      if (row < 11 * n) {
+        const int h = row < n ? 0 : (row < 4 * n ? 1 : 2);
+        src = g_o + (size_t)row * ld;
+        dst_row = go_row0[h] + (row - oo[h]);
+      } else if (row < 11 * n + 192) {
+        const int r = row - 11 * n;
+        src = cache_h + (size_t)r * ld;
+        dst_row = kWmGo + r;
+      } else if (row < 11 * n + 384) {
+        const int r = row - 11 * n - 192;
+        src = g_pre + (size_t)r * ld;
+        dst_row = kWmGo + kWmH + r;
+      } else {
+        const int r = row - 11 * n - 384;
+        src = xs + (size_t)r * ld;
+        dst_row = kWmGo + kWmH + kWmGp + r;
+      }
+      const int64_t k = k0 + 4 * q;
+      const int bytes = (int)max((int64_t)0, min((int64_t)16, (K - k) * 4));
+      cp_async16_zfill(base + dst_row * kWmStride + 4 * q, src + (bytes > 0 ? k : 0), bytes);
+    }
+  };
+  float acc[18][4];
+#pragma unroll
+  for (int q = 0; q < 18; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+  int s = 0;
+  if ((int64_t)blockIdx.x < nchunks) issue(blockIdx.x, 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, s ^= 1) {
+    const int64_t nx = c + gridDim.x;
+    if (nx < nchunks) issue(nx, s ^ 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    float *base = stage_ptr(s);
+    if (t < kWmKc) base[(kWmGo + 192) * kWmStride + t] = (c * kWmKc + t < K) ? 1.f : 0.f;
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kWmKc; kk += 8) {
+      const int col = kk + tq;
+      if (warp < 4) {
+        // dW2: m-tiles 2w, 2w+1 over padded g_o rows; n-tiles 0..7 = head
+        // hidden units, 8 = ones column (db2)
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int mt = 2 * warp + mi;
+          const int h = mt * 16 < go_row0[1] ? 0 : (mt * 16 < go_row0[2] ? 1 : 2);
+          const float *A = base + (mt * 16 + g) * kWmStride + col;
+          uint32_t ah[4], al[4];
+          split_trunc(A[0], ah[0], al[0]);
+          split_trunc(A[8 * kWmStride], ah[1], al[1]);
+          split_trunc(A[4], ah[2], al[2]);
+          split_trunc(A[8 * kWmStride + 4], ah[3], al[3]);
+#pragma unroll
+          for (int nt = 0; nt < 9; ++nt) {
+            const int hrow = nt < 8 ? h * 64 + nt * 8 + g : 192 + g;
+            const float *Bp = base + (kWmGo + hrow) * kWmStride + col;
+            uint32_t bh0, bl0, bh1, bl1;
+            split_trunc(Bp[0], bh0, bl0);
+            split_trunc(Bp[4], bh1, bl1);
+            float (&d)[4] = acc[mi * 9 + nt];
+            mma_tf32_16x8x8(d, al[0], al[1], al[2], al[3], bh0, bh1);
+            mma_tf32_16x8x8(d, ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+            mma_tf32_16x8x8(d, ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+          }
+        }
+      } else {
+        // dW1: m-tiles 0..2 over xs rows; n-tiles 6(w-4) .. +5 over g_pre rows
+        uint32_t ah[3][4], al[3][4];
+#pragma unroll
+        for (int mt = 0; mt < 3; ++mt) {
+          const float *A = base + (kWmGo + kWmH + kWmGp + mt * 16 + g) * kWmStride + col;
+          split_trunc(A[0], ah[mt][0], al[mt][0]);
+          split_trunc(A[8 * kWmStride], ah[mt][1], al[mt][1]);
+          split_trunc(A[4], ah[mt][2], al[mt][2]);
+          split_trunc(A[8 * kWmStride + 4], ah[mt][3], al[mt][3]);
+        }
+#pragma unroll
+        for (int ni = 0; ni < 6; ++ni) {
+          const int nt = 6 * (warp - 4) + ni;
+          const float *Bp = base + (kWmGo + kWmH + nt * 8 + g) * kWmStride + col;
+          uint32_t bh0, bl0, bh1, bl1;
+          split_trunc(Bp[0], bh0, bl0);
+          split_trunc(Bp[4], bh1, bl1);
+#pragma unroll
+          for (int mt = 0; mt < 3; ++mt) {
+            float (&d)[4] = acc[mt * 6 + ni];
+            mma_tf32_16x8x8(d, al[mt][0], al[mt][1], al[mt][2], al[mt][3], bh0, bh1);
+            mma_tf32_16x8x8(d, ah[mt][0], ah[mt][1], ah[mt][2], ah[mt][3], bl0, bl1);
+            mma_tf32_16x8x8(d, ah[mt][0], ah[mt][1], ah[mt][2], ah[mt][3], bh0, bh1);
+          }
+        }
+      }
+    }
+    __syncthreads();  // the stage is overwritten by the copies issued next iteration
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  // partial tiles in fragment order: tile index = dW2 mt*9+nt | 72 + dW1 mt*24+nt
+  float4 *out = reinterpret_cast<float4 *>(partial) + (size_t)blockIdx.x * kWmTiles * 32;
+#pragma unroll
+  for (int q = 0; q < 18; ++q) {
+    int tile;
+    if (warp < 4) tile = (2 * warp + q / 9) * 9 + q % 9;
+    else tile = 72 + (q / 6) * 24 + 6 * (warp - 4) + q % 6;
+    out[tile * 32 + lane] = make_float4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+  }
+}
+
+// blockIdx.y = slice of the CTA partials (kWmSlices slices, 8-way atomics)
+constexpr int kWmSlices = 8;
+
+__global__ void decoder_wgrad_reduce_kernel(const float *__restrict__ partial, int ctas, int n,
+                                            vsx_decoder_grads dW) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (tile, lane, e)
+  if (idx >= kWmTiles * 128) return;
+  const int per = (ctas + kWmSlices - 1) / kWmSlices;
+  const int c0 = blockIdx.y * per, c1 = min(ctas, c0 + per);
+  if (c0 >= c1) return;
+  float sum = 0.f;
+  for (int c = c0; c < c1; ++c) sum += partial[(size_t)c * kWmTiles * 128 + idx];
+  const int tile = idx >> 7, lane = (idx >> 2) & 31, e = idx & 3;
+  const int g = lane >> 2, tq = lane & 3;
+  const int row_in = g + 8 * (e >> 1), col_in = 2 * tq + (e & 1);
+  if (tile < 72) {
+    const int mt = tile / 9, nt = tile % 9;
+    const int np0 = wm_pad16(n), np1 = wm_pad16(3 * n);
+    const int row = mt * 16 + row_in;
+    const int h = row < np0 ? 0 : (row < np0 + np1 ? 1 : 2);
+    const int jh = row - (h == 0 ? 0 : (h == 1 ? np0 : np0 + np1));
+    const int owh = h == 0 ? n : (h == 1 ? 3 * n : 7 * n);
+    if (jh >= owh) return;
+    const int col = nt * 8 + col_in;
+    if (nt < 8) atomicAdd(dW.w2[h] + (size_t)col * owh + jh, sum);
+    else if (col == 64) atomicAdd(dW.b2[h] + jh, sum);
+  } else {
+    const int tt = tile - 72, mt = tt / 24, nt = tt % 24;
+    const int i = mt * 16 + row_in, col = nt * 8 + col_in;
+    const int h = col / 64, hh = col % 64;
+    if (i < kInDim) atomicAdd(dW.w1[h] + (size_t)i * 64 + hh, sum);
+    else if (i == kInDim) atomicAdd(dW.b1[h] + hh, sum);
+  }
+}
+
 // C[m][c] += sum_k A[m][k] * B[c][k] for a K-chunk per blockIdx.z, where A is
 // (M x K) and B is (Ncols x K), both row-major with leading dim K (feature-
 // major caches). Output column c maps to segment out[c / seg_w] with row
@@ -719,7 +920,8 @@ extern "C" int vsx_decode_fwd(vsx_decoder W, const int32_t *active, int32_t n_ac
 extern "C" size_t vsx_decode_bwd_ws_bytes(int32_t n, int32_t n_active) {
   // xs [37][ld] + g_pre [192][ld] + g_o [11n][ld] + the mma weight image
   return sizeof(float) * cache_ld(n_active) * (size_t)(kInDim + 1 + 192 + 11 * n) +
-         sizeof(float) * dbw_image_floats(n) + 256;
+         sizeof(float) * dbw_image_floats(n) + sizeof(float) * (size_t)kWmMaxCtas * kWmTiles * 128 +
+         256;
 }
 
 extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t *active,
@@ -774,6 +976,29 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
         W, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, cache_h, g_means, g_o,
         g_emb, g_log_scale, xs, g_pre);
     VSX_LAUNCH_CHECK("decode_bwd_anchor");
+  }
+  static const int wg_impl = [] {
+    const char *e = getenv("VSX_WGRAD");  // "tc" = tcgen05 version (A/B)
+    return (e && e[0] == 't') ? 1 : 0;
+  }();
+  if (use_tc && wg_impl == 0 && wm_supported(n)) {  // mma.sync K-split + reduction
+    float *partial = reinterpret_cast<float *>(
+        reinterpret_cast<char *>(g_o + (size_t)11 * n * ld) + sizeof(float) * dbw_image_floats(n));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nchunks = (n_active + kWmKc - 1) / kWmKc;
+    const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(2 * sms, kWmMaxCtas), nchunks));
+    const size_t smem = sizeof(float) * 2 * kWmStageFloats;
+    VSX_CUDA_TRY(cudaFuncSetAttribute(decoder_wgrad_mma_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    decoder_wgrad_mma_kernel<<<ctas, 256, smem, st>>>(g_o, cache_h, g_pre, xs, n_active, ld, n,
+                                                       partial);
+    VSX_LAUNCH_CHECK("decoder_wgrad_mma");
+    decoder_wgrad_reduce_kernel<<<dim3((kWmTiles * 128 + 255) / 256, kWmSlices), 256, 0, st>>>(
+        partial, ctas, n, dW);
+    VSX_LAUNCH_CHECK("decoder_wgrad_reduce");
+    return VSX_OK;
   }
   if (use_tc && 11 * n <= 128)  // tensor-core weight gradients (decode_tc.cu)
     return decoder_wgrad_tc(g_o, cache_h, g_pre, xs, n_active, ld, n, dW, st);

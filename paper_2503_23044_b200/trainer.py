@@ -351,6 +351,30 @@ def _mask_u8(v, shape) -> torch.Tensor:
 
 
 _COPY_STREAM = None
+_FRONT_STREAM = None
+
+
+def _front_stream() -> torch.cuda.Stream:
+    global _FRONT_STREAM
+    if _FRONT_STREAM is None:
+        _FRONT_STREAM = torch.cuda.Stream(priority=-1)  # ahead of the compositor's CTAs
+    return _FRONT_STREAM
+
+
+_TAIL_STREAM = None
+
+
+def _tail_stream() -> torch.cuda.Stream:
+    global _TAIL_STREAM
+    if _TAIL_STREAM is None:
+        _TAIL_STREAM = torch.cuda.Stream()
+    return _TAIL_STREAM
+
+
+def _pipeline_enabled() -> bool:
+    """VSX_PIPELINE=0 runs every view's stages back to back on one stream (A/B)."""
+    import os
+    return os.environ.get("VSX_PIPELINE", "1") != "0"
 
 
 class _InputStager:
@@ -434,22 +458,48 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     isects = 0
     anchors, agrads = state.anchors, state.anchor_grads
     stager = _InputStager(views, images, priors, have, normal_priors, have_n)
+    main = torch.cuda.current_stream()
+    # Three-stream software pipeline over the views: the front end of view v+1
+    # (cull, decode, project + sort, binning: small, latency-bound kernels and
+    # the host reads of their counts) runs on a high-priority side stream, and
+    # the projection/decoder backward of view v-1 on a tail stream, while the
+    # compositor of view v runs on the main stream. Per-view
+    # device buffers stay referenced until the end-of-step sync, so the caching
+    # allocator never recycles a side-stream block the main stream still reads.
+    fs = _front_stream() if _pipeline_enabled() else main
+    ts = _tail_stream() if _pipeline_enabled() else main
+    fs.wait_stream(main)
+    ts.wait_stream(main)
+    hold = []
+    fronts = {}
+
+    def front(vi):
+        view = views[vi]
+        with torch.cuda.stream(fs):
+            with _span(timer, "cull"):
+                active = ds.active(view)
+            with _span(timer, "decode_fwd"):
+                dec = D.decode(params.abi(), params.n, active, ds.centers, anchors.emb,
+                               anchors.log_scales, anchors.offsets, view, ds.lod_ref,
+                               ds.max_scale, status, keep_cache=True)
+            with _span(timer, "project_sort"):
+                P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal,
+                              view, status)
+            with _span(timer, "bin_sort"):
+                Bn = D.bin_tiles(P, view.width, view.height)
+            tile_max[vi] = torch.diff(Bn.tile_offsets.long()).max()
+            ev = torch.cuda.Event()
+            ev.record(fs)
+        fronts[vi] = (active, dec, P, Bn, ev)
+
+    front(0)
     for vi, view in enumerate(views):
         H, W = view.height, view.width
-        with _span(timer, "cull"):
-            active = ds.active(view)
-        with _span(timer, "decode_fwd"):
-            dec = D.decode(params.abi(), params.n, active, ds.centers, anchors.emb,
-                           anchors.log_scales, anchors.offsets, view, ds.lod_ref, ds.max_scale,
-                           status, keep_cache=True)
+        active, dec, P, Bn, ev = fronts.pop(vi)
+        hold.append((active, dec, P, Bn))
+        main.wait_event(ev)
         gaussians += dec.count
-        with _span(timer, "project_sort"):
-            P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal,
-                          view, status)
-        with _span(timer, "bin_sort"):
-            Bn = D.bin_tiles(P, W, H)
         isects += Bn.intersections
-        tile_max[vi] = torch.diff(Bn.tile_offsets.long()).max()
         # fused objective (K9 inside K5/K6): loss sums in the forward epilogue,
         # cotangents formed on the fly in the backward
         gt, pd, pv, pn, pnv = stager.get(vi)
@@ -465,16 +515,28 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         live += R.n_contrib.sum()
         with _span(timer, "raster_bwd"):
             gs = D.raster_backward(P, Bn, view, R, loss=loss)
-        with _span(timer, "project_bwd"):
-            gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P, gs, view)
-        with _span(timer, "decode_bwd"):
-            decoder_backward_into(params, state.dgrads, active, ds.centers, anchors.emb,
-                                  anchors.log_scales, anchors.offsets, view, ds.lod_ref,
-                                  ds.max_scale, dec, gg["means"], gg["opacities"], gg["colors"],
-                                  gg["scales"], gg["quats"], gg["normals"], agrads.emb,
-                                  agrads.log_scales, agrads.offsets)
+        # projection + decoder backward of this view run on the tail stream,
+        # overlapping the next view's compositor; they are the only writers
+        # of the parameter gradients, so one stream keeps them ordered
+        if ts is not main:
+            ts.wait_stream(main)
+        with torch.cuda.stream(ts):
+            with _span(timer, "project_bwd"):
+                gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P, gs, view)
+            with _span(timer, "decode_bwd"):
+                decoder_backward_into(params, state.dgrads, active, ds.centers, anchors.emb,
+                                      anchors.log_scales, anchors.offsets, view, ds.lod_ref,
+                                      ds.max_scale, dec, gg["means"], gg["opacities"],
+                                      gg["colors"], gg["scales"], gg["quats"], gg["normals"],
+                                      agrads.emb, agrads.log_scales, agrads.offsets)
+        hold.append((R, gs, gg))
         if keep is not None:
             keep.append(ViewWork(active, dec, P, Bn, R, gs, gg))
+        # the next view's front end is issued after this view's back end is
+        # queued, so it overlaps it on the GPU
+        if vi + 1 < B:
+            front(vi + 1)
+    main.wait_stream(ts)
     D.check_status(status, "train_step")
     hw = torch.tensor([v.height * v.width * 3 for v in views], dtype=torch.float64, device=dev)
     rgb = float((rgb_acc / hw).mean())
@@ -495,6 +557,8 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         raise NumericalError(f"non-finite loss at step {state.step}: rgb={rgb:.4g} depth={depth:.4g}")
     with _span(timer, "adam"):
         state.adam()
+    torch.cuda.current_stream().synchronize()
+    del hold
     report = StepReport(
         step=state.step, total=total, rgb=rgb, depth=depth, geo=0.0, w2=w2, w3=w3,
         lr=cosine_lr(state.step, cfg.lr_decoder, cfg), supervised_depth_px=supervised,
