@@ -602,6 +602,193 @@ __global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kerne
   }
 }
 
+// ------------------------------------------------------- forward on mma.sync
+//
+// GEMM1 (per head)  Hpre[16 x 64] = [x | 1 | 0][16 x 40] . [W1_h ; b1_h ; 0]
+// GEMM2 (per head)  O   [16 x ow] = tanh(Hpre)[16 x 64] . W2_h      (+ b2)
+// One warp owns 16 anchors; the GEMM1 accumulators feed GEMM2 directly as
+// its A operand (same K permutation as the backward's W1 image). Writes the
+// feature-major caches (hidden activations, raw head outputs + b2); the
+// per-gaussian activations run in decode_gauss_kernel.
+
+__host__ __device__ inline int dfw_nt2(int h, int n) { return (dec_head_w(h, n) + 7) / 8; }
+__host__ __device__ inline int dfw_nt2_total(int n) { return dfw_nt2(0, n) + dfw_nt2(1, n) + dfw_nt2(2, n); }
+constexpr size_t kDfwW1Floats = (size_t)3 * 5 * 8 * 32 * 4;
+__host__ __device__ inline size_t dfw_image_floats(int n) {
+  return kDfwW1Floats + (size_t)8 * dfw_nt2_total(n) * 32 * 4;
+}
+__host__ __device__ inline bool dfw_supported(int n) { return dfw_nt2(2, n) <= 9; }
+
+__global__ void decoder_fwd_image_kernel(vsx_decoder W, float4 *__restrict__ img) {
+  const int n = W.n;
+  const int e_w1 = 3 * 5 * 8 * 32;
+  const int e_w2 = 8 * dfw_nt2_total(n) * 32;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < e_w1 + e_w2;
+       e += gridDim.x * blockDim.x) {
+    const int lane = e & 31, g = lane >> 2, t = lane & 3;
+    float v0, v1;
+    if (e < e_w1) {
+      const int nt = (e >> 5) & 7, ks = (e >> 8) % 5, h = (e >> 8) / 5;
+      const int hid = nt * 8 + g;
+      auto w1v = [&](int k) {
+        if (k < kInDim) return W.w1[h][k * 64 + hid];
+        if (k == kInDim) return W.b1[h][hid];
+        return 0.f;
+      };
+      v0 = w1v(ks * 8 + t);
+      v1 = w1v(ks * 8 + t + 4);
+    } else {
+      int e2 = e - e_w1;
+      int h = 0;
+      while (e2 >= 8 * dfw_nt2(h, n) * 32) e2 -= 8 * dfw_nt2(h++, n) * 32;
+      const int nt2h = dfw_nt2(h, n), ow = dec_head_w(h, n);
+      const int nt2 = (e2 >> 5) % nt2h, kk = (e2 >> 5) / nt2h;
+      const int j = nt2 * 8 + g;
+      const int hid0 = kk * 8 + 2 * t, hid1 = hid0 + 1;  // K positions t, t+4
+      v0 = j < ow ? W.w2[h][hid0 * ow + j] : 0.f;
+      v1 = j < ow ? W.w2[h][hid1 * ow + j] : 0.f;
+    }
+    float h0, l0, h1, l1;
+    split_rna(v0, h0, l0);
+    split_rna(v1, h1, l1);
+    img[e] = make_float4(h0, h1, l0, l1);
+  }
+}
+
+constexpr int kDfwWarps = 16;
+
+__global__ void __launch_bounds__(kDfwWarps * 32, 1) decode_fwd_mma_kernel(
+    vsx_decoder W, const float4 *__restrict__ img, const int32_t *__restrict__ active,
+    int32_t n_active, const double *__restrict__ centers, const float *__restrict__ emb,
+    vsx_camera cam, double lod_ref, float *__restrict__ cache_h, float *__restrict__ cache_o) {
+  extern __shared__ __align__(16) float4 fimg[];
+  __shared__ float s_b2[11 * 10];
+  const int n = W.n;
+  const int nimg = (int)(dfw_image_floats(n) / 4);
+  for (int e = threadIdx.x; e < nimg; e += blockDim.x) fimg[e] = img[e];
+  for (int j = threadIdx.x; j < 11 * n; j += blockDim.x)
+    s_b2[j] = j < n ? W.b2[0][j] : (j < 4 * n ? W.b2[1][j - n] : W.b2[2][j - 4 * n]);
+  __syncthreads();
+  const float4 *w1i = fimg, *w2i = fimg + 3 * 5 * 8 * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const size_t ld = cache_ld(n_active);
+  const int n_tiles = (n_active + 15) / 16;
+  for (int tile = blockIdx.x * kDfwWarps + warp; tile < n_tiles; tile += gridDim.x * kDfwWarps) {
+    const int r0 = tile * 16, ra = r0 + g, rb = r0 + g + 8;
+    const bool va = ra < n_active, vb = rb < n_active;
+    const int aa = va ? active[ra] : 0, ab = vb ? active[rb] : 0;
+    // X fragments (raw): xa[ks] = {X[ra][8ks+t], X[rb][8ks+t], X[ra][8ks+t+4], X[rb][8ks+t+4]}
+    float xa[5][4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      xa[ks][0] = va ? emb[(size_t)aa * kEmbed + 8 * ks + t] : 0.f;
+      xa[ks][1] = vb ? emb[(size_t)ab * kEmbed + 8 * ks + t] : 0.f;
+      xa[ks][2] = va ? emb[(size_t)aa * kEmbed + 8 * ks + t + 4] : 0.f;
+      xa[ks][3] = vb ? emb[(size_t)ab * kEmbed + 8 * ks + t + 4] : 0.f;
+    }
+    // columns 32..35 = (d/ref, (c - cam)/d) (decoder.py:142-147, float64), 36 = bias
+    auto derived = [&](int a, bool v) {
+      if (!v) return 0.f;
+      const double rx = dsub(centers[3 * a + 0], cam.center[0]);
+      const double ry = dsub(centers[3 * a + 1], cam.center[1]);
+      const double rz = dsub(centers[3 * a + 2], cam.center[2]);
+      const double d = fmax(sqrt(dadd(dadd(dmul(rx, rx), dmul(ry, ry)), dmul(rz, rz))), 1e-12);
+      const double num = t == 0 ? d : (t == 1 ? rx : (t == 2 ? ry : rz));
+      return (float)ddiv(num, t == 0 ? lod_ref : d);
+    };
+    xa[4][0] = derived(aa, va);
+    xa[4][1] = derived(ab, vb);
+    xa[4][2] = (t == 0 && va) ? 1.f : 0.f;
+    xa[4][3] = (t == 0 && vb) ? 1.f : 0.f;
+    int w2off = 0;
+    for (int h = 0; h < 3; ++h) {
+      const int nt2h = dfw_nt2(h, n), ow = dec_head_w(h, n), oo = dec_head_off(h, n);
+      float c[8][4];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = c[q][2] = c[q][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < 5; ++ks) {
+        uint32_t ah[4], al[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split_trunc(xa[ks][e], ah[e], al[e]);
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) mma3x(c[nt], ah, al, w1i[((h * 5 + ks) * 8 + nt) * 32 + lane]);
+      }
+      float o[9][4];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) o[q][0] = o[q][1] = o[q][2] = o[q][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const float v0 = tanhf(c[kk][0]), v1 = tanhf(c[kk][1]);
+        const float v2 = tanhf(c[kk][2]), v3 = tanhf(c[kk][3]);
+        if (cache_h) {
+          const int k0 = h * 64 + kk * 8 + 2 * t;
+          float *h0 = cache_h + (size_t)k0 * ld, *h1 = h0 + ld;
+          if (va) {
+            h0[ra] = v0;
+            h1[ra] = v1;
+          }
+          if (vb) {
+            h0[rb] = v2;
+            h1[rb] = v3;
+          }
+        }
+        uint32_t ah[4], al[4];
+        split_trunc(v0, ah[0], al[0]);  // (row g,   k t)   = hidden 2t
+        split_trunc(v2, ah[1], al[1]);  // (row g+8, k t)
+        split_trunc(v1, ah[2], al[2]);  // (row g,   k t+4) = hidden 2t+1
+        split_trunc(v3, ah[3], al[3]);  // (row g+8, k t+4)
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+          if (q < nt2h) mma3x(o[q], ah, al, w2i[(w2off + kk * nt2h + q) * 32 + lane]);
+      }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        if (q >= nt2h) break;
+        const int j0 = q * 8 + 2 * t;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = j0 + e;
+          if (j >= ow) continue;
+          float *col = cache_o + (size_t)(oo + j) * ld;
+          if (va) col[ra] = o[q][e] + s_b2[oo + j];
+          if (vb) col[rb] = o[q][2 + e] + s_b2[oo + j];
+        }
+      }
+      w2off += 8 * nt2h;
+    }
+  }
+}
+
+size_t decoder_fwd_image_floats(int n) { return dfw_image_floats(n); }
+
+int decoder_fwd_image(vsx_decoder W, float *img, cudaStream_t st) {
+  decoder_fwd_image_kernel<<<32, 256, 0, st>>>(W, reinterpret_cast<float4 *>(img));
+  VSX_LAUNCH_CHECK("decoder_fwd_image");
+  return VSX_OK;
+}
+
+// Returns 1 (not launched) when n is outside the mma path's register budget.
+int decode_fwd_mma(vsx_decoder W, const float *img, const int32_t *active, int32_t n_active,
+                   const double *centers, const float *emb, vsx_camera cam, double lod_ref,
+                   float *cache_h, float *cache_o, cudaStream_t st) {
+  if (!dfw_supported(W.n) || 11 * W.n > 110) return 1;
+  const size_t smem = sizeof(float) * dfw_image_floats(W.n);
+  VSX_CUDA_TRY(cudaFuncSetAttribute(decode_fwd_mma_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = (n_active + 15) / 16;
+  const int grid = std::max(1, std::min(sms, (tiles + kDfwWarps - 1) / kDfwWarps));
+  decode_fwd_mma_kernel<<<grid, kDfwWarps * 32, smem, st>>>(
+      W, reinterpret_cast<const float4 *>(img), active, n_active, centers, emb, cam, lod_ref,
+      cache_h, cache_o);
+  VSX_LAUNCH_CHECK("decode_fwd_mma");
+  return VSX_OK;
+}
+
 // ----------------------------------------------- weight gradients on mma.sync
 //
 // dW2_h[k][j] = sum_r H_h[r][k] g_o[r][j] (+ db2 via a ones column) and

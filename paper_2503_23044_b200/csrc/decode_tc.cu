@@ -558,13 +558,27 @@ bool tc_supported(int n) { return n >= 1 && tc_smem_bytes(n) <= 220 * 1024 && 7 
 
 using namespace vsx;
 
-extern "C" size_t vsx_decoder_image_floats(int32_t n) { return tc_image_floats(n); }
+namespace vsx {
+size_t decoder_fwd_image_floats(int n);
+int decoder_fwd_image(vsx_decoder W, float *img, cudaStream_t st);
+int decode_fwd_mma(vsx_decoder W, const float *img, const int32_t *active, int32_t n_active,
+                   const double *centers, const float *emb, vsx_camera cam, double lod_ref,
+                   float *cache_h, float *cache_o, cudaStream_t st);
+}  // namespace vsx
+
+// The image holds both weight layouts: the tcgen05 shared-memory tiles, then
+// (16-byte aligned) the mma.sync fragment image of decode_fwd_mma.
+static size_t mma_image_offset(int n) { return (tc_image_floats(n) + 3) / 4 * 4; }
+
+extern "C" size_t vsx_decoder_image_floats(int32_t n) {
+  return mma_image_offset(n) + decoder_fwd_image_floats(n);
+}
 
 extern "C" int vsx_decoder_image(vsx_decoder W, float *img, vsx_stream s) {
   VSX_REQUIRE(W.n >= 1, "decoder_image: bad n");
   decoder_image_kernel<<<64, 256, 0, as_stream(s)>>>(W, img);
   VSX_LAUNCH_CHECK("decoder_image");
-  return VSX_OK;
+  return decoder_fwd_image(W, img + mma_image_offset(W.n), as_stream(s));
 }
 
 extern "C" int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t *active,
@@ -578,17 +592,30 @@ extern "C" int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t 
   VSX_REQUIRE(tc_supported(W.n), "decode_fwd_tc: n=%d not supported by the tensor-core path",
               W.n);
   if (n_active == 0) return VSX_OK;
-  const size_t smem = tc_smem_bytes(W.n);
-  VSX_CUDA_TRY(cudaFuncSetAttribute(decode_fwd_tc_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = (n_active + kTcRows - 1) / kTcRows;
-  decode_fwd_tc_kernel<<<std::min(tiles, sms), 256, smem, as_stream(s)>>>(
-      W, img, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, max_scale, means,
-      opacity, color, scale, quat, normal, cache_h, cache_o, status);
-  VSX_LAUNCH_CHECK("decode_fwd_tc");
+  // VSX_DECODE_FWD=tcgen05 selects the tcgen05 MLP (A/B); default is the
+  // warp-per-16-anchors mma.sync kernel (falls back for large n)
+  static const bool use_tcgen05 = [] {
+    const char *e = getenv("VSX_DECODE_FWD");
+    return e && e[0] == 't';
+  }();
+  int rc = 1;
+  if (!use_tcgen05)
+    rc = decode_fwd_mma(W, img + mma_image_offset(W.n), active, n_active, centers, emb, cam,
+                        lod_ref, cache_h, cache_o, as_stream(s));
+  if (rc < 0) return rc;
+  if (rc == 1) {
+    const size_t smem = tc_smem_bytes(W.n);
+    VSX_CUDA_TRY(cudaFuncSetAttribute(decode_fwd_tc_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = (n_active + kTcRows - 1) / kTcRows;
+    decode_fwd_tc_kernel<<<std::min(tiles, sms), 256, smem, as_stream(s)>>>(
+        W, img, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, max_scale,
+        means, opacity, color, scale, quat, normal, cache_h, cache_o, status);
+    VSX_LAUNCH_CHECK("decode_fwd_tc");
+  }
   const int64_t total = (int64_t)n_active * W.n;
   decode_gauss_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(s)>>>(
       W.n, active, n_active, centers, log_scale, offsets, max_scale, cache_o, means, opacity, color,
