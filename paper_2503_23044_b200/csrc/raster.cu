@@ -32,6 +32,87 @@ namespace vsx {
 constexpr int kChunk = 256;
 constexpr int kBCMax = 32;  // largest backward splat chunk
 
+// Per-pixel finalize (renderer.py:282-301) + fused loss partial sums (K9),
+// shared by both forward kernels. Block-uniform in L.gt_rgb.
+__device__ __forceinline__ void fwd_epilogue(const vsx_camera &cam, bool inside, int px, int py,
+                                             float acc, float c0, float c1, float c2, float n0,
+                                             float n1, float n2, float dist, float T, int32_t nc,
+                                             float *__restrict__ out_rgb,
+                                             float *__restrict__ out_alpha,
+                                             float *__restrict__ out_depth,
+                                             float *__restrict__ out_normal,
+                                             float *__restrict__ out_raw,
+                                             uint8_t *__restrict__ out_valid,
+                                             float *__restrict__ out_T,
+                                             int32_t *__restrict__ out_nc,
+                                             const vsx_loss_desc &L) {
+  // loss partial sums (fused K9): rgb |d|, masked depth |d|, masked normal |d|
+  double l_rgb = 0.0, l_dep = 0.0, l_nrm = 0.0;
+  uint32_t c_dep = 0, c_nrm = 0;
+  if (inside) {
+    const size_t p = (size_t)py * cam.width + px;
+    const PixRay ray = pixel_ray(cam, px, py);
+    const float den = denom_of(n0, n1, n2, ray);
+    const bool covered = acc >= kAlphaValidMin;
+    const bool valid = covered && fabsf(den) >= kDenomGuard;
+    const float depth = valid ? dist / den : 0.f;
+    const float nn = fmaxf(sqrtf(n0 * n0 + n1 * n1 + n2 * n2), 1e-12f);
+    const float nx = covered ? n0 / nn : 0.f, ny = covered ? n1 / nn : 0.f,
+                nz = covered ? n2 / nn : 0.f;
+    if (out_rgb) {
+      out_rgb[3 * p + 0] = c0;
+      out_rgb[3 * p + 1] = c1;
+      out_rgb[3 * p + 2] = c2;
+    }
+    if (out_alpha) out_alpha[p] = acc;
+    if (out_depth) out_depth[p] = depth;
+    if (out_raw) {
+      out_raw[3 * p + 0] = n0;
+      out_raw[3 * p + 1] = n1;
+      out_raw[3 * p + 2] = n2;
+    }
+    if (out_normal) {
+      out_normal[3 * p + 0] = nx;
+      out_normal[3 * p + 1] = ny;
+      out_normal[3 * p + 2] = nz;
+    }
+    if (out_valid) out_valid[p] = valid ? 1 : 0;
+    out_T[p] = T;
+    out_nc[p] = nc;
+    if (L.gt_rgb) {
+      l_rgb = fabs((double)(c0 - L.gt_rgb[3 * p + 0])) + fabs((double)(c1 - L.gt_rgb[3 * p + 1])) +
+              fabs((double)(c2 - L.gt_rgb[3 * p + 2]));
+      if (L.prior_depth && valid && L.prior_depth_valid[p]) {
+        l_dep = fabs((double)(depth - L.prior_depth[p]));
+        c_dep = 1;
+      }
+      if (L.prior_normal && valid && L.prior_normal_valid[p]) {
+        l_nrm = fabs((double)(nx - L.prior_normal[3 * p + 0])) +
+                fabs((double)(ny - L.prior_normal[3 * p + 1])) +
+                fabs((double)(nz - L.prior_normal[3 * p + 2]));
+        c_nrm = 1;
+      }
+    }
+  }
+  if (L.gt_rgb) {  // block-uniform
+    l_rgb = warp_sum_d(l_rgb);
+    l_dep = warp_sum_d(l_dep);
+    l_nrm = warp_sum_d(l_nrm);
+    const unsigned bd = __ballot_sync(0xffffffffu, c_dep), bn = __ballot_sync(0xffffffffu, c_nrm);
+    if ((threadIdx.x & 31) == 0) {
+      if (l_rgb != 0.0) atomicAdd(L.sums + 0, l_rgb);
+      if (bd) {
+        atomicAdd(L.sums + 1, l_dep);
+        atomicAdd(L.counts + 0, (uint32_t)__popc(bd));
+      }
+      if (bn) {
+        atomicAdd(L.sums + 2, l_nrm);
+        atomicAdd(L.counts + 1, (uint32_t)__popc(bn));
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) raster_fwd_kernel(
     const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
     const uint32_t *__restrict__ tile_list, vsx_camera cam, float *__restrict__ out_rgb,
@@ -111,71 +192,188 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
       done = T < kEarlyStopT;
     }
   }
-  // loss partial sums (fused K9): rgb |d|, masked depth |d|, masked normal |d|
-  double l_rgb = 0.0, l_dep = 0.0, l_nrm = 0.0;
-  uint32_t c_dep = 0, c_nrm = 0;
-  if (inside) {
-    const size_t p = (size_t)py * cam.width + px;
-    const PixRay ray = pixel_ray(cam, px, py);
-    const float den = denom_of(n0, n1, n2, ray);
-    const bool covered = acc >= kAlphaValidMin;
-    const bool valid = covered && fabsf(den) >= kDenomGuard;
-    const float depth = valid ? dist / den : 0.f;
-    const float nn = fmaxf(sqrtf(n0 * n0 + n1 * n1 + n2 * n2), 1e-12f);
-    const float nx = covered ? n0 / nn : 0.f, ny = covered ? n1 / nn : 0.f,
-                nz = covered ? n2 / nn : 0.f;
-    if (out_rgb) {
-      out_rgb[3 * p + 0] = c0;
-      out_rgb[3 * p + 1] = c1;
-      out_rgb[3 * p + 2] = c2;
-    }
-    if (out_alpha) out_alpha[p] = acc;
-    if (out_depth) out_depth[p] = depth;
-    if (out_raw) {
-      out_raw[3 * p + 0] = n0;
-      out_raw[3 * p + 1] = n1;
-      out_raw[3 * p + 2] = n2;
-    }
-    if (out_normal) {
-      out_normal[3 * p + 0] = nx;
-      out_normal[3 * p + 1] = ny;
-      out_normal[3 * p + 2] = nz;
-    }
-    if (out_valid) out_valid[p] = valid ? 1 : 0;
-    out_T[p] = T;
-    out_nc[p] = nc;
-    if (L.gt_rgb) {
-      l_rgb = fabs((double)(c0 - L.gt_rgb[3 * p + 0])) + fabs((double)(c1 - L.gt_rgb[3 * p + 1])) +
-              fabs((double)(c2 - L.gt_rgb[3 * p + 2]));
-      if (L.prior_depth && valid && L.prior_depth_valid[p]) {
-        l_dep = fabs((double)(depth - L.prior_depth[p]));
-        c_dep = 1;
+  fwd_epilogue(cam, inside, px, py, acc, c0, c1, c2, n0, n1, n2, dist, T, nc, out_rgb, out_alpha,
+               out_depth, out_normal, out_raw, out_valid, out_T, out_nc, L);
+}
+
+__device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (&a)[4],
+                                                 uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void copy_splat_async(vsx_splat *dst, const vsx_splat *src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * k),
+                 "l"(reinterpret_cast<const char *>(src) + 16 * k)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// tf32 by truncation: one LOP3 (cvt.rna.tf32 is a 4-instruction sequence on
+// sm_100a). With x = hi + (x - hi), the dropped bits of lo cost < 2^-21 |x|.
+__device__ __forceinline__ uint32_t tf32_bits(float x) {
+  return __float_as_uint(x) & 0xffffe000u;
+}
+
+// ------------------------------------------------------ forward v2 (tensor)
+//
+// The blend sums rgb, raw normal, plane offset and alpha are an [px x splat] .
+// [splat x 8] product once the per-(pixel, splat) weights w = alpha*T are
+// known. Each warp owns 32 pixels and walks the staged chunk of 256 splats in
+// sub-chunks of 32: lanes run the sequential transmittance recursion and
+// write w into a warp-private shared plane (0 once the pixel is dead), then
+// the warp accumulates the 8 channels with mma.sync m16n8k8 tf32 (3xTF32)
+// into register accumulators. Staged per splat: the alpha parameters and the
+// channel vector (r, g, b, nx, ny, nz, plane_d, 1) pre-split hi/lo.
+constexpr int kFwSub = 32;                 // splats per warp sub-chunk
+constexpr int kFwPlane = kFwSub * 36;      // floats per warp plane ([splat][36])
+
+__global__ void __launch_bounds__(256, 3) raster_fwd_tc_kernel(
+    const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
+    const uint32_t *__restrict__ tile_list, vsx_camera cam, float *__restrict__ out_rgb,
+    float *__restrict__ out_alpha, float *__restrict__ out_depth, float *__restrict__ out_normal,
+    float *__restrict__ out_raw, uint8_t *__restrict__ out_valid, float *__restrict__ out_T,
+    int32_t *__restrict__ out_nc, vsx_loss_desc L) {
+  __shared__ float4 s0[kChunk];
+  __shared__ float2 s1[kChunk];
+  __shared__ float s_phi[kChunk * 8], s_plo[kChunk * 8];
+  extern __shared__ float s_w[];  // 8 warp planes of kFwPlane floats
+  const int txn = gridDim.x;
+  const int tile = blockIdx.y * txn + blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  // pixel of this thread: warp w owns pixels 32w .. 32w+31 (rows 2w, 2w+1)
+  const int lx = t & 15, ly = t >> 4;
+  const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
+  const bool inside = px < cam.width && py < cam.height;
+  const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
+  const uint32_t begin = tile_off[tile], end = tile_off[tile + 1];
+  const float fx = (float)lx, fy = (float)ly;
+  float *wpl = s_w + warp * kFwPlane;
+  float T = 1.f;
+  int32_t nc = 0;
+  bool done = !inside;
+  float acc[2][4];  // C fragments: m-tile m = pixels 16m..16m+15 of the warp, channels
+#pragma unroll
+  for (int m = 0; m < 2; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+  for (uint32_t cs = begin; cs < end; cs += kChunk) {
+    if (__syncthreads_count(!done) == 0) break;
+    const uint32_t idx = cs + t;
+    if (idx < end) {
+      const vsx_splat sp = load_splat(rec, tile_list[idx]);
+      s0[t] = make_float4((float)(sp.mean2d[0] - ox), (float)(sp.mean2d[1] - oy),
+                          (-0.5f * kLog2e) * sp.conic[0], (-kLog2e) * sp.conic[1]);
+      s1[t] = make_float2((-0.5f * kLog2e) * sp.conic[2], sp.opacity);
+      const float pv[8] = {sp.color[0], sp.color[1], sp.color[2], sp.normal[0],
+                           sp.normal[1], sp.normal[2], sp.plane_d, 1.f};
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float hi = __uint_as_float(tf32_bits(pv[c]));
+        s_phi[t * 8 + c] = hi;
+        s_plo[t * 8 + c] = __uint_as_float(tf32_bits(pv[c] - hi));
       }
-      if (L.prior_normal && valid && L.prior_normal_valid[p]) {
-        l_nrm = fabs((double)(nx - L.prior_normal[3 * p + 0])) +
-                fabs((double)(ny - L.prior_normal[3 * p + 1])) +
-                fabs((double)(nz - L.prior_normal[3 * p + 2]));
-        c_nrm = 1;
+    }
+    __syncthreads();
+    const int cnt = (int)min((uint32_t)kChunk, end - cs);
+    for (int sb = 0; sb < cnt; sb += kFwSub) {
+      if (!__any_sync(0xffffffffu, !done)) break;  // warp-uniform
+      const int m = min(kFwSub, cnt - sb);
+      // ---- sequential weights of this sub-chunk (dead pixels write 0)
+      int j = 0;
+      for (; j + 4 <= m; j += 4) {
+        float al[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 p0 = s0[sb + j + u];
+          const float2 p1 = s1[sb + j + u];
+          float e, at;
+          al[u] = splat_alpha(p0, make_float4(p1.x, p1.y, 0.f, 0.f), fx - p0.x, fy - p0.y, e, at);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float w = 0.f;
+          if (!done) {
+            if (T >= kEarlyStopT) {
+              w = al[u] * T;
+              T = __fmaf_rn(-al[u], T, T);
+              ++nc;
+            } else {
+              done = true;
+            }
+          }
+          wpl[(j + u) * 36 + lane] = w;
+        }
       }
+      for (; j < m; ++j) {
+        const float4 p0 = s0[sb + j];
+        const float2 p1 = s1[sb + j];
+        float e, at;
+        const float alpha =
+            splat_alpha(p0, make_float4(p1.x, p1.y, 0.f, 0.f), fx - p0.x, fy - p0.y, e, at);
+        float w = 0.f;
+        if (!done) {
+          if (T >= kEarlyStopT) {
+            w = alpha * T;
+            T = __fmaf_rn(-alpha, T, T);
+            ++nc;
+          } else {
+            done = true;
+          }
+        }
+        wpl[j * 36 + lane] = w;
+      }
+      for (; j < kFwSub; ++j) wpl[j * 36 + lane] = 0.f;  // ragged last sub-chunk
+      __syncwarp();
+      // ---- channel sums on the tensor cores: C[px][ch] += W[px][j] . P[j][ch]
+#pragma unroll
+      for (int ks = 0; ks < kFwSub / 8; ++ks) {
+        const int jr = sb + ks * 8 + tq;  // staged splat row of b0 (b1: +4)
+        const bool ok0 = ks * 8 + tq < m, ok1 = ks * 8 + tq + 4 < m;
+        const uint32_t bh0 = ok0 ? __float_as_uint(s_phi[jr * 8 + g]) : 0u;
+        const uint32_t bl0 = ok0 ? __float_as_uint(s_plo[jr * 8 + g]) : 0u;
+        const uint32_t bh1 = ok1 ? __float_as_uint(s_phi[(jr + 4) * 8 + g]) : 0u;
+        const uint32_t bl1 = ok1 ? __float_as_uint(s_plo[(jr + 4) * 8 + g]) : 0u;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const float *A = wpl + (ks * 8 + tq) * 36 + 16 * mt + g;
+          const float a0 = A[0], a1 = A[8], a2 = A[4 * 36], a3 = A[4 * 36 + 8];
+          const uint32_t ah[4] = {tf32_bits(a0), tf32_bits(a1), tf32_bits(a2), tf32_bits(a3)};
+          const uint32_t alo[4] = {tf32_bits(a0 - __uint_as_float(ah[0])),
+                                   tf32_bits(a1 - __uint_as_float(ah[1])),
+                                   tf32_bits(a2 - __uint_as_float(ah[2])),
+                                   tf32_bits(a3 - __uint_as_float(ah[3]))};
+          mma_m16n8k8_tf32(acc[mt], alo, bh0, bh1);
+          mma_m16n8k8_tf32(acc[mt], ah, bl0, bl1);
+          mma_m16n8k8_tf32(acc[mt], ah, bh0, bh1);
+        }
+      }
+      __syncwarp();
     }
   }
-  if (L.gt_rgb) {  // block-uniform
-    l_rgb = warp_sum_d(l_rgb);
-    l_dep = warp_sum_d(l_dep);
-    l_nrm = warp_sum_d(l_nrm);
-    const unsigned bd = __ballot_sync(0xffffffffu, c_dep), bn = __ballot_sync(0xffffffffu, c_nrm);
-    if ((threadIdx.x & 31) == 0) {
-      if (l_rgb != 0.0) atomicAdd(L.sums + 0, l_rgb);
-      if (bd) {
-        atomicAdd(L.sums + 1, l_dep);
-        atomicAdd(L.counts + 0, (uint32_t)__popc(bd));
-      }
-      if (bn) {
-        atomicAdd(L.sums + 2, l_nrm);
-        atomicAdd(L.counts + 1, (uint32_t)__popc(bn));
-      }
-    }
+  // ---- C fragments -> per-pixel channels through the warp's plane
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    float *o = wpl + (16 * mt + g) * 9 + 2 * tq;
+    o[0] = acc[mt][0];
+    o[1] = acc[mt][1];
+    o[8 * 9] = acc[mt][2];
+    o[8 * 9 + 1] = acc[mt][3];
   }
+  __syncwarp();
+  const float *ch = wpl + lane * 9;
+  fwd_epilogue(cam, inside, px, py, ch[7], ch[0], ch[1], ch[2], ch[3], ch[4], ch[5], ch[6], T, nc,
+               out_rgb, out_alpha, out_depth, out_normal, out_raw, out_valid, out_T, out_nc, L);
 }
 
 struct BwdArgs {
@@ -359,35 +557,6 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
 // meet in shared memory and one 8-lane group per splat forms its 13
 // gradients (same polynomials as v2) and issues the atomics.
 constexpr int kPlaneStride = kTilePixels + 4;  // 4 mod 32: conflict-free A fragments
-
-__device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (&a)[4],
-                                                 uint32_t b0, uint32_t b1) {
-  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ void copy_splat_async(vsx_splat *dst, const vsx_splat *src) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * k),
-                 "l"(reinterpret_cast<const char *>(src) + 16 * k)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-// tf32 by truncation: one LOP3 (cvt.rna.tf32 is a 4-instruction sequence on
-// sm_100a). With x = hi + (x - hi), the dropped bits of lo cost < 2^-21 |x|.
-__device__ __forceinline__ uint32_t tf32_bits(float x) {
-  return __float_as_uint(x) & 0xffffe000u;
-}
 
 // pixel moment m of tile pixel p (x, y about the tile centre)
 __device__ __forceinline__ float pixel_moment(int p, int m) {
@@ -727,8 +896,28 @@ static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
                       cudaStream_t st) {
   VSX_REQUIRE(cam.width > 0 && cam.height > 0 && t_final && n_contrib, "raster_fwd: bad args");
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
-  raster_fwd_kernel<<<grid, 256, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha, depth,
-                                          normal, raw_normal, valid, t_final, n_contrib, L);
+  // VSX_RASTER_FWD=tc selects the tensor-core-accumulation forward (A/B: it
+  // measured 6.0 vs 5.7 ms/step on cfg2 — the forward is bound by the alpha
+  // recursion, not by the 8 accumulation FMAs it removes)
+  static const bool tc = [] {
+    const char *e = getenv("VSX_RASTER_FWD");
+    return e && e[0] == 't';
+  }();
+  if (tc) {
+    const int smem = (int)(sizeof(float) * 8 * kFwPlane);
+    static bool attr = false;
+    if (!attr) {
+      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_fwd_tc_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    raster_fwd_tc_kernel<<<grid, 256, smem, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha,
+                                                  depth, normal, raw_normal, valid, t_final,
+                                                  n_contrib, L);
+  }
+  else
+    raster_fwd_kernel<<<grid, 256, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha, depth,
+                                            normal, raw_normal, valid, t_final, n_contrib, L);
   VSX_LAUNCH_CHECK("raster_fwd");
   return VSX_OK;
 }
