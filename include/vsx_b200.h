@@ -285,6 +285,29 @@ int vsx_adam(float *param, const float *grad, float *m, float *v, int32_t n_seg,
              const int64_t *seg_begin, const double *lr, double beta1, double beta2, double eps,
              int32_t step, vsx_stream s);
 
+/* ---- f1: depth-prior precompute (depth_prior.py:85-214) ------------------ */
+/* float64 device maps (H, W) row-major with uint8 validity. Replaces the
+ * numpy passes of fit_scale_shift (:85-110; the 2x2 normal equations and the
+ * MAD refit stay on the host), apply_scale_shift (:132-140),
+ * reprojection_error (:143-187) and enhance (:205-214). */
+/* Per point: camera z, and the bilinearly sampled raw depth when the point
+ * projects in front (z > 1e-9) inside [0, W-1] x [0, H-1]; ok = 0 (not
+ * projected), 1 (projected, some touched texel invalid), 2 (sampled). */
+int vsx_prior_sample(const double *points, int64_t n, vsx_camera cam, const double *depth,
+                     const uint8_t *valid, double *raw, double *z, uint8_t *ok, vsx_stream s);
+/* metric = scale * raw + shift where valid (NULL: finite and > 0) and the
+ * result is finite and > 0; 0 elsewhere. */
+int vsx_apply_scale_shift(const double *raw, const uint8_t *valid, int64_t n, double scale,
+                          double shift, double *out, uint8_t *out_valid, vsx_stream s);
+/* Pixel round-trip error src -> ref -> src for every valid source pixel
+ * (+inf where the chain breaks); accumulate_min != 0 min-combines into err. */
+int vsx_reprojection_error(const double *src, const uint8_t *src_valid, vsx_camera view_src,
+                           const double *ref, const uint8_t *ref_valid, vsx_camera view_ref,
+                           double *err, int32_t accumulate_min, vsx_stream s);
+/* Enhanced prior: keep valid source pixels with min round trip <= tau. */
+int vsx_enhance_finalize(const double *src, const uint8_t *src_valid, const double *emin,
+                         double tau, int64_t n, double *out, uint8_t *out_valid, vsx_stream s);
+
 /* ---- diagnostics --------------------------------------------------------- */
 /* tcgen05 self-test: D[128 x N] = A[128 x K] . B[N x K]^T, kind::tf32 from
  * shared memory into TMEM (three != 0: 3xTF32 split). */

@@ -275,9 +275,63 @@ def make_train_small():
     np.savez_compressed(OUT / "train_small.npz", **out)
 
 
+def make_depth_prior():
+    """f1 prior precompute: three aerial views of the ground plane z = 0 with
+    raw relative depth maps (planted affine + noise, a corrupted stripe in view
+    0) and sparse plane points; outputs of the reference's fit_scale_shift,
+    apply_scale_shift, select_neighbors, reprojection_error and enhance."""
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    from voxsplat import depth_prior as dp
+    from voxsplat.geometry import CameraView, look_at
+    rng = np.random.default_rng(11)
+    W, H, f = 64, 48, 55.0
+    eyes = [(0.0, -4.0, 6.0), (1.0, -4.2, 6.1), (-1.2, -3.8, 5.9)]
+    views = []
+    for i, e in enumerate(eyes):
+        r, t = look_at(np.array(e), np.array([0.1 * i, 0.5, 0.0]))
+        views.append(CameraView(view_id=i, width=W, height=H, fx=f, fy=f, cx=(W - 1) / 2.0,
+                                cy=(H - 1) / 2.0, r=r, t=t))
+    uu, vv = np.meshgrid(np.arange(W, dtype=np.float64), np.arange(H, dtype=np.float64))
+    raws, metrics = [], []
+    st = [(0.8, 0.3), (1.25, -0.2), (0.6, 0.45)]
+    for i, v in enumerate(views):
+        d = np.stack([(uu - v.cx) / v.fx, (vv - v.cy) / v.fy, np.ones_like(uu)], -1)
+        dw = d @ v.r                      # camera ray -> world direction (r rows = axes)
+        c = v.center
+        metric = -c[2] / dw[..., 2]       # camera z of the plane hit (ray has unit cam z)
+        s, b = st[i]
+        raw = (metric - b) / s + rng.normal(0.0, 1e-3, metric.shape)
+        if i == 0:
+            raw[30:34, :] *= 1.3          # corrupted stripe
+        raws.append(raw)
+        metrics.append(metric)
+    pts = np.stack([rng.uniform(-3, 3, 400), rng.uniform(-2, 3, 400), np.zeros(400)], -1)
+    out = {"raw0": raws[0], "raw1": raws[1], "raw2": raws[2], "points": pts,
+           "metric0": metrics[0]}
+    for i, v in enumerate(views):
+        out.update(_view_arrays(f"v{i}", v))
+    aligned = []
+    for i, v in enumerate(views):
+        fit = dp.fit_scale_shift(raws[i], v, pts)
+        out[f"fit{i}"] = np.array([fit.scale, fit.shift, fit.samples, fit.inliers], np.float64)
+        al = dp.apply_scale_shift(raws[i], fit)
+        aligned.append(al)
+        out[f"aligned{i}_values"] = al.values
+        out[f"aligned{i}_valid"] = al.valid
+    nb0 = dp.select_neighbors(views, 0)
+    out["neighbors0"] = np.array(nb0, np.int64)
+    out["err01"] = dp.reprojection_error(aligned[0], views[0], aligned[1], views[1])
+    enh = dp.enhance(aligned[0], views[0], [(aligned[j], views[j]) for j in nb0], tau=1.0)
+    out["enh0_values"] = enh.values
+    out["enh0_valid"] = enh.valid
+    out["enh0_min_roundtrip"] = enh.min_roundtrip
+    np.savez_compressed(OUT / "depth_prior.npz", **out)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    which = sys.argv[1:] or ["scene_small", "raster_leaf", "train_small", "cfg1"]
+    which = sys.argv[1:] or ["scene_small", "raster_leaf", "train_small", "cfg1", "depth_prior"]
     for name in which:
         t0 = time.time()
         globals()[f"make_{name}"]()

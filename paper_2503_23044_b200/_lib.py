@@ -86,6 +86,10 @@ _SIGS = {
     "vsx_decoder_image": ([VsxDecoder, P, P], c_i32),
     "vsx_decode_fwd_tc": ([VsxDecoder, P, P, c_i32, P, P, P, P, VsxCamera, c_f64, c_f64,
                            P, P, P, P, P, P, P, P, P, P], c_i32),
+    "vsx_prior_sample": ([P, c_i64, VsxCamera, P, P, P, P, P, P], c_i32),
+    "vsx_apply_scale_shift": ([P, P, c_i64, c_f64, c_f64, P, P, P], c_i32),
+    "vsx_reprojection_error": ([P, P, VsxCamera, P, P, VsxCamera, P, c_i32, P], c_i32),
+    "vsx_enhance_finalize": ([P, P, P, c_f64, c_i64, P, P, P], c_i32),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -44,6 +44,14 @@ class ContractViolation(VoxsplatError):
     """An ordering/shape contract between pipeline stages was broken."""
 
 
+class InsufficientData(VoxsplatError):
+    """Too few samples for a fit (reference errors.py:44)."""
+
+
+class DegenerateFit(VoxsplatError):
+    """A fit has no unique / admissible solution (reference errors.py:48)."""
+
+
 # Status codes shared with include/vsx_b200.h (VSX_OK ... VSX_ERR_CUDA).
 VSX_OK = 0
 VSX_ERR_INVALID = -1
