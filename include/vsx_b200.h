@@ -22,6 +22,11 @@
  *   vsx_l1_loss / vsx_depth_loss   losses.py:43-53 bl_rgb_loss, losses.py:65-84 e_depth_loss
  *   vsx_adam                       trainer.py:220-247 TrainState._adam + apply_*_grads
  *   vsx_exchange_*                 renderer.py:452-477 transfer_gaussians (real C1 payload packing)
+ *   vsx_prior_sample / vsx_apply_scale_shift / vsx_reprojection_error / vsx_enhance_finalize
+ *                                  depth_prior.py:85-214 (fit_scale_shift, apply_scale_shift,
+ *                                  reprojection_error, enhance)
+ *   vsx_ncc_patches / vsx_ncc_scatter
+ *                                  losses.py:98-287 compute_homography .. bl_geo_loss (Eq. 10)
  */
 #ifndef VSX_B200_H
 #define VSX_B200_H
@@ -213,6 +218,12 @@ typedef struct vsx_loss_desc {
   float normal_weight;
   double *sums;
   uint32_t *counts;
+  /* optional additional cotangents of the rendered rgb (H,W,3), normal
+   * (H,W,3) and depth (H,W) images (e.g. the NCC term, vsx_ncc_scatter);
+   * NULL when absent. Used by vsx_raster_bwd_loss only. */
+  const float *extra_rgb;
+  const float *extra_normal;
+  const float *extra_depth;
 } vsx_loss_desc;
 
 int vsx_raster_fwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,
@@ -307,6 +318,38 @@ int vsx_reprojection_error(const double *src, const uint8_t *src_valid, vsx_came
 /* Enhanced prior: keep valid source pixels with min round trip <= tau. */
 int vsx_enhance_finalize(const double *src, const uint8_t *src_valid, const double *emin,
                          double tau, int64_t n, double *out, uint8_t *out_valid, vsx_stream s);
+
+/* ---- f2: multi-view patch NCC loss, Eq. 10 (losses.py:98-287) ----------- */
+/* Relative pose (R_rel = R_ref R_src^T, t_rel = t_ref - R_rel t_src, row-major)
+ * and both intrinsics of a (reference, source) pair (losses.py:118-128). */
+typedef struct vsx_ncc_geom {
+  double r_rel[9];
+  double t_rel[3];
+  double src_fx, src_fy, src_cx, src_cy;
+  double ref_fx, ref_fy, ref_cx, ref_cy;
+} vsx_ncc_geom;
+
+/* Per patch centre (int32 (u, v) pairs chosen by the host's stratified draw,
+ * losses.py:184-206): term = 1 - NCC of the (2h+1)^2 source grayscale patch
+ * against the reference grayscale warped by the plane homography of the
+ * rendered source normal/depth at the centre; status 0 plane rejected,
+ * 1 warp outside the reference, 2 used; the per-patch gradients of the term
+ * w.r.t. the patch pixels' grayscale, the centre normal and the centre depth.
+ * pair_sum / pair_used get the pair's sum of terms and used count, and
+ * pairs_used (device counter) is incremented when the pair used a patch. */
+int vsx_ncc_patches(const float *src_rgb, const float *src_normal, const float *src_depth,
+                    int32_t src_width, int32_t src_height, const float *ref_rgb,
+                    int32_t ref_width, int32_t ref_height, vsx_ncc_geom geom,
+                    const int32_t *centers, int32_t n_patches, int32_t half, double *term,
+                    uint8_t *status, double *g_patch, double *g_normal, double *g_depth,
+                    double *pair_sum, int32_t *pair_used, int32_t *pairs_used, vsx_stream s);
+/* Adds upstream / (pairs_used * pair_used) times the per-patch gradients into
+ * the source cotangent images g_rgb (H,W,3), g_normal (H,W,3), g_depth (H,W). */
+int vsx_ncc_scatter(const int32_t *centers, int32_t n_patches, int32_t half, int32_t src_width,
+                    const uint8_t *status, const double *g_patch, const double *g_normal,
+                    const double *g_depth, const int32_t *pair_used, const int32_t *pairs_used,
+                    double upstream, float *g_rgb, float *g_normal_img, float *g_depth_img,
+                    vsx_stream s);
 
 /* ---- diagnostics --------------------------------------------------------- */
 /* tcgen05 self-test: D[128 x N] = A[128 x K] . B[N x K]^T, kind::tf32 from

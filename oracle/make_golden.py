@@ -255,11 +255,13 @@ def make_train_small():
         out[f"img{i}"] = images[i]
         out[f"prior{i}"] = priors[i].values
         out[f"pvalid{i}"] = valid
-    for tag, s2 in (("rgb", 8), ("depth", 0)):
+    # "geo": the Eq. 10 NCC term ramps in from step 0 (w3 = 0.025, 0.05 at
+    # steps 1, 2); the three views give one (reference, source) pair
+    for tag, s2, s3 in (("rgb", 8, 8), ("depth", 0, 8), ("geo", 8, 0)):
         scene_t = scene_m.build_hierarchy(pts, 0.25, 2, offsets_per_voxel=3, seed=4,
                                           views=views)
         cfg = trainer.TrainConfig(total_steps=8, batch_size=3, workers=1, step2_start=s2,
-                                  step3_start=8, growth_stop=0, log_every=0)
+                                  step3_start=s3, growth_stop=0, log_every=0)
         state = trainer.make_state(scene_t, cfg)
         reps = []
         for _ in range(3):
@@ -267,6 +269,7 @@ def make_train_small():
                                            priors if tag == "depth" else None))
         out[f"{tag}_loss"] = np.array([[r.total, r.rgb, r.depth] for r in reps])
         out[f"{tag}_supervised"] = np.array([r.supervised_depth_px for r in reps])
+        out[f"{tag}_geo"] = np.array([[r.geo, r.w3, r.geo_pairs, r.geo_patches] for r in reps])
         for k, t_ in state.replicas[0].tensors.items():
             out[f"{tag}_post_{k}"] = t_.detach().numpy()
         for k in range(scene_t.lod_count):
@@ -329,9 +332,72 @@ def make_depth_prior():
     np.savez_compressed(OUT / "depth_prior.npz", **out)
 
 
+def make_geo_loss():
+    """f2 Eq. 10: the reference's own render targets of two coplanar textured
+    sheets (the layout of its geo FD test, helpers.py:256-300) for two texture
+    phases, bl_geo_loss values / stats with a seeded rng, and the gradients of
+    the loss w.r.t. the source view's rendered rgb, normal and depth; plus
+    reference picks of _stratified_centers on random candidate sets."""
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    tests_dir = str(Path(REF).parent / "tests")
+    if tests_dir not in sys.path:
+        sys.path.insert(0, tests_dir)
+    import helpers as H
+    from voxsplat import losses as L
+    from voxsplat.geometry import CameraView
+    from voxsplat.renderer import make_leaf_gaussians, project_splats, rasterize_view
+    out = {}
+    for case, (phase_b, tilt) in enumerate([(4.0, (0.05, -0.08)), (1.0, (-0.1, 0.07))]):
+        normal = np.array([tilt[0], tilt[1], 1.0])
+        point = np.array([0.0, 0.0, 2.2])
+        src_view = CameraView(view_id=0, width=24, height=24, fx=30.0, fy=30.0, cx=11.5, cy=11.5,
+                              r=np.eye(3), t=np.zeros(3))
+        ref_view = CameraView(view_id=1, width=40, height=40, fx=30.0, fy=30.0, cx=19.5,
+                              cy=19.5, r=np.eye(3), t=-np.array([0.06, 0.04, 0.0]))
+        targets = []
+        for view, phase in ((ref_view, phase_b), (src_view, 1.0)):
+            arrays = H.plane_gaussian_arrays(normal, point, extent=2.0, spacing=0.18)
+            arrays["colors"] = H._smooth_colors(arrays["means"], phase)
+            batch = make_leaf_gaussians(arrays["means"], arrays["opacities"], arrays["colors"],
+                                        arrays["scales"], arrays["quats"], requires_grad=True)
+            t, _ = rasterize_view(project_splats(batch, view), view)
+            targets.append(t)
+        views = [ref_view, src_view]
+        val, stats = L.bl_geo_loss(targets, views, np.random.default_rng(case), patch_count=16)
+        src = targets[1]
+        g = torch.autograd.grad(val, [src.rgb, src.normal, src.depth], allow_unused=True)
+        p = f"c{case}_"
+        for k, t in zip(("ref", "src"), targets):
+            for f in ("rgb", "normal", "depth", "alpha"):
+                out[p + f"{k}_{f}"] = getattr(t, f).detach().numpy()
+            out[p + f"{k}_valid"] = t.valid.numpy()
+        out.update(_view_arrays(p + "vref", ref_view))
+        out.update(_view_arrays(p + "vsrc", src_view))
+        out[p + "loss"] = np.array(float(val))
+        out[p + "stats"] = np.array([stats.pairs_used, stats.patches_used,
+                                     stats.patches_rejected])
+        for name, gg, like in zip(("g_rgb", "g_normal", "g_depth"), g,
+                                  (src.rgb, src.normal, src.depth)):
+            out[p + name] = (gg if gg is not None else torch.zeros_like(like)).detach().numpy()
+    rng = np.random.default_rng(5)
+    for k in range(4):
+        n = int(rng.integers(20, 400))
+        w, h = int(rng.integers(16, 80)), int(rng.integers(16, 80))
+        cu = rng.integers(0, w, n).astype(np.float64)
+        cv = rng.integers(0, h, n).astype(np.float64)
+        cnt = int(rng.integers(4, 70))
+        out[f"strat{k}_in"] = np.concatenate([cu, cv])
+        out[f"strat{k}_args"] = np.array([w, h, cnt, 100 + k])
+        out[f"strat{k}_out"] = L._stratified_centers(cu, cv, w, h, cnt,
+                                                     np.random.default_rng(100 + k))
+    np.savez_compressed(OUT / "geo_loss.npz", **out)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
-    which = sys.argv[1:] or ["scene_small", "raster_leaf", "train_small", "cfg1", "depth_prior"]
+    which = sys.argv[1:] or ["scene_small", "raster_leaf", "train_small", "cfg1", "depth_prior",
+                             "geo_loss"]
     for name in which:
         t0 = time.time()
         globals()[f"make_{name}"]()

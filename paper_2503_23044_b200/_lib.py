@@ -41,7 +41,16 @@ class VsxLossDesc(ctypes.Structure):
                 ("prior_depth_valid", c_void_p), ("prior_normal", c_void_p),
                 ("prior_normal_valid", c_void_p), ("rgb_scale", c_f32),
                 ("depth_weight", c_f32), ("normal_weight", c_f32), ("sums", c_void_p),
-                ("counts", c_void_p)]
+                ("counts", c_void_p), ("extra_rgb", c_void_p), ("extra_normal", c_void_p),
+                ("extra_depth", c_void_p)]
+
+
+class VsxNccGeom(ctypes.Structure):
+    """Mirror of vsx_ncc_geom (relative pose + both intrinsics of a view pair)."""
+
+    _fields_ = [("r_rel", c_f64 * 9), ("t_rel", c_f64 * 3),
+                ("src_fx", c_f64), ("src_fy", c_f64), ("src_cx", c_f64), ("src_cy", c_f64),
+                ("ref_fx", c_f64), ("ref_fy", c_f64), ("ref_cx", c_f64), ("ref_cy", c_f64)]
 
 
 P = c_void_p
@@ -90,6 +99,9 @@ _SIGS = {
     "vsx_apply_scale_shift": ([P, P, c_i64, c_f64, c_f64, P, P, P], c_i32),
     "vsx_reprojection_error": ([P, P, VsxCamera, P, P, VsxCamera, P, c_i32, P], c_i32),
     "vsx_enhance_finalize": ([P, P, P, c_f64, c_i64, P, P, P], c_i32),
+    "vsx_ncc_patches": ([P, P, P, c_i32, c_i32, P, c_i32, c_i32, VsxNccGeom, P, c_i32, c_i32,
+                         P, P, P, P, P, P, P, P, P], c_i32),
+    "vsx_ncc_scatter": ([P, c_i32, c_i32, c_i32, P, P, P, P, P, P, c_f64, P, P, P, P], c_i32),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -154,21 +154,37 @@ __device__ __forceinline__ PixCot pixel_cotangent_loss(
   c.gC0 = sgn(in_rgb[3 * p + 0] - L.gt_rgb[3 * p + 0]) * L.rgb_scale;
   c.gC1 = sgn(in_rgb[3 * p + 1] - L.gt_rgb[3 * p + 1]) * L.rgb_scale;
   c.gC2 = sgn(in_rgb[3 * p + 2] - L.gt_rgb[3 * p + 2]) * L.rgb_scale;
-  if (L.prior_depth && valid && L.prior_depth_valid[p]) {
+  if (L.extra_rgb) {
+    c.gC0 += L.extra_rgb[3 * p + 0];
+    c.gC1 += L.extra_rgb[3 * p + 1];
+    c.gC2 += L.extra_rgb[3 * p + 2];
+  }
+  float gd = 0.f;  // cotangent of the output depth (defined where valid)
+  if (L.prior_depth && valid && L.prior_depth_valid[p])
+    gd = sgn(in_depth[p] - L.prior_depth[p]) * L.depth_weight / (float)max(L.counts[0], 1u);
+  if (L.extra_depth && valid) gd += L.extra_depth[p];
+  if (gd != 0.f) {
     const float depth = in_depth[p];
-    const float gd = sgn(depth - L.prior_depth[p]) * L.depth_weight /
-                     (float)max(L.counts[0], 1u);
     c.gD = gd / den;
     const float gden = -gd * depth / den;
     c.gR0 += gden * ray.rx;
     c.gR1 += gden * ray.ry;
     c.gR2 += gden;
   }
+  // cotangent of the output (normalised) normal, defined where covered
+  float gn0 = 0.f, gn1 = 0.f, gn2 = 0.f;
   if (L.prior_normal && valid && L.prior_normal_valid[p]) {
     const float sc = L.normal_weight / (float)max(L.counts[1], 1u);
-    const float gn0 = sgn(in_normal[3 * p + 0] - L.prior_normal[3 * p + 0]) * sc;
-    const float gn1 = sgn(in_normal[3 * p + 1] - L.prior_normal[3 * p + 1]) * sc;
-    const float gn2 = sgn(in_normal[3 * p + 2] - L.prior_normal[3 * p + 2]) * sc;
+    gn0 = sgn(in_normal[3 * p + 0] - L.prior_normal[3 * p + 0]) * sc;
+    gn1 = sgn(in_normal[3 * p + 1] - L.prior_normal[3 * p + 1]) * sc;
+    gn2 = sgn(in_normal[3 * p + 2] - L.prior_normal[3 * p + 2]) * sc;
+  }
+  if (L.extra_normal && covered) {
+    gn0 += L.extra_normal[3 * p + 0];
+    gn1 += L.extra_normal[3 * p + 1];
+    gn2 += L.extra_normal[3 * p + 2];
+  }
+  if (gn0 != 0.f || gn1 != 0.f || gn2 != 0.f) {
     const float len = sqrtf(n0 * n0 + n1 * n1 + n2 * n2);
     if (len >= 1e-12f) {
       const float il = 1.f / len;

@@ -18,6 +18,7 @@ schedule when priors are given).
 from __future__ import annotations
 
 import contextlib
+from types import SimpleNamespace
 import ctypes
 import json
 import time
@@ -492,27 +493,31 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             ev.record(fs)
         fronts[vi] = (active, dec, P, Bn, ev)
 
-    front(0)
-    for vi, view in enumerate(views):
-        H, W = view.height, view.width
+    def loss_desc(vi, extra=None):
+        view = views[vi]
+        gt, pd, pv, pn, pnv = stager.get(vi)
+        ex_rgb, ex_nrm, ex_dep = extra if extra is not None else (None, None, None)
+        return VsxLossDesc(
+            gt_rgb=gt.data_ptr(), prior_depth=ptr(pd).value, prior_depth_valid=ptr(pv).value,
+            prior_normal=ptr(pn).value, prior_normal_valid=ptr(pnv).value,
+            rgb_scale=1.0 / (B * view.height * view.width * 3),
+            depth_weight=(w2 / len(have)) if vi in have else 0.0,
+            normal_weight=(wn / len(have_n) / 3.0) if vi in have_n else 0.0,
+            sums=sums[vi].data_ptr(), counts=counts[vi].data_ptr(),
+            extra_rgb=ptr(ex_rgb).value, extra_normal=ptr(ex_nrm).value,
+            extra_depth=ptr(ex_dep).value)
+
+    def take_front(vi):
+        nonlocal gaussians, isects
         active, dec, P, Bn, ev = fronts.pop(vi)
         hold.append((active, dec, P, Bn))
         main.wait_event(ev)
         gaussians += dec.count
         isects += Bn.intersections
-        # fused objective (K9 inside K5/K6): loss sums in the forward epilogue,
-        # cotangents formed on the fly in the backward
-        gt, pd, pv, pn, pnv = stager.get(vi)
-        loss = VsxLossDesc(
-            gt_rgb=gt.data_ptr(), prior_depth=ptr(pd).value, prior_depth_valid=ptr(pv).value,
-            prior_normal=ptr(pn).value, prior_normal_valid=ptr(pnv).value,
-            rgb_scale=1.0 / (B * H * W * 3),
-            depth_weight=(w2 / len(have)) if vi in have else 0.0,
-            normal_weight=(wn / len(have_n) / 3.0) if vi in have_n else 0.0,
-            sums=sums[vi].data_ptr(), counts=counts[vi].data_ptr())
-        with _span(timer, "raster_fwd"):
-            R = D.raster_forward(P, Bn, view, loss=loss)
-        live += R.n_contrib.sum()
+        return active, dec, P, Bn
+
+    def backward(vi, active, dec, P, Bn, R, loss):
+        view = views[vi]
         with _span(timer, "raster_bwd"):
             gs = D.raster_backward(P, Bn, view, R, loss=loss)
         # projection + decoder backward of this view run on the tail stream,
@@ -532,10 +537,52 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         hold.append((R, gs, gg))
         if keep is not None:
             keep.append(ViewWork(active, dec, P, Bn, R, gs, gg))
-        # the next view's front end is issued after this view's back end is
-        # queued, so it overlaps it on the GPU
-        if vi + 1 < B:
-            front(vi + 1)
+
+    geo_val, geo_pairs, geo_patches = 0.0, 0, 0
+    use_geo = w3 > 0 and B >= 2
+    front(0)
+    if not use_geo:
+        for vi in range(B):
+            active, dec, P, Bn = take_front(vi)
+            # fused objective (K9 inside K5/K6): loss sums in the forward
+            # epilogue, cotangents formed on the fly in the backward
+            loss = loss_desc(vi)
+            with _span(timer, "raster_fwd"):
+                R = D.raster_forward(P, Bn, views[vi], loss=loss)
+            live += R.n_contrib.sum()
+            backward(vi, active, dec, P, Bn, R, loss)
+            # the next view's front end is issued after this view's back end
+            # is queued, so it overlaps it on the GPU
+            if vi + 1 < B:
+                front(vi + 1)
+    else:
+        # Eq. 10 couples view pairs (losses.py:199-287, trainer.py:309-315):
+        # every view is composited first, the NCC cotangents of the source
+        # views are formed on the device, then each view runs its backward
+        # with them added to the fused objective's cotangents.
+        fwd = []
+        for vi in range(B):
+            active, dec, P, Bn = take_front(vi)
+            loss = loss_desc(vi)
+            with _span(timer, "raster_fwd"):
+                R = D.raster_forward(P, Bn, views[vi], loss=loss)
+            live += R.n_contrib.sum()
+            fwd.append((active, dec, P, Bn, R))
+            if vi + 1 < B:
+                front(vi + 1)
+        from .losses import geo_loss_cotangents
+        tg = [SimpleNamespace(rgb=f[4].rgb, normal=f[4].normal, depth=f[4].depth,
+                              alpha=f[4].alpha, valid=f[4].valid) for f in fwd]
+        with _span(timer, "geo_ncc"):
+            g_loss, gstats, cot = geo_loss_cotangents(tg, views, state.rng,
+                                                      patch_count=cfg.geo_patches,
+                                                      half=cfg.geo_patch_half, upstream=w3)
+        geo_val = float(g_loss)
+        geo_pairs, geo_patches = gstats.pairs_used, gstats.patches_used
+        hold.append(cot)
+        for vi in range(B):
+            active, dec, P, Bn, R = fwd[vi]
+            backward(vi, active, dec, P, Bn, R, loss_desc(vi, cot.get(vi)))
     main.wait_stream(ts)
     D.check_status(status, "train_step")
     hw = torch.tensor([v.height * v.width * 3 for v in views], dtype=torch.float64, device=dev)
@@ -552,7 +599,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         cnt = nrm_cnt.double()
         terms = torch.where(cnt > 0, nrm_sum / (3.0 * cnt.clamp_min(1)), torch.zeros_like(cnt))
         normal = float(terms[have_n].mean())
-    total = rgb + w2 * depth + wn * normal
+    total = rgb + w2 * depth + wn * normal + w3 * geo_val
     if not np.isfinite(total):
         raise NumericalError(f"non-finite loss at step {state.step}: rgb={rgb:.4g} depth={depth:.4g}")
     with _span(timer, "adam"):
@@ -560,9 +607,10 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     torch.cuda.current_stream().synchronize()
     del hold
     report = StepReport(
-        step=state.step, total=total, rgb=rgb, depth=depth, geo=0.0, w2=w2, w3=w3,
+        step=state.step, total=total, rgb=rgb, depth=depth, geo=geo_val, w2=w2, w3=w3,
         lr=cosine_lr(state.step, cfg.lr_decoder, cfg), supervised_depth_px=supervised,
-        geo_pairs=0, geo_patches=0, gaussians=gaussians, transfer_bytes=0, imbalance=1.0,
+        geo_pairs=geo_pairs, geo_patches=geo_patches, gaussians=gaussians, transfer_bytes=0,
+        imbalance=1.0,
         max_tile_splats=int(tile_max.max()), seconds=time.perf_counter() - t0,
         intersections=isects, normal=normal, live_pairs=int(live))
     state.step += 1

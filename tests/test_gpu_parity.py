@@ -355,3 +355,34 @@ def test_cfg1_forward_vs_reference_and_oracle(cfg1_case, cfg1_golden):
     moved = int((gid_dev[src] != d["v0_spl_gid"]).sum())
     assert moved <= 0.01 * src.size, moved
     assert rep.rgb == pytest.approx(float(d["report_rgb"][0]), rel=1e-4)
+
+
+def test_train_steps_with_ncc_term_match_reference(train_small):
+    """3 device steps with the Eq. 10 NCC term ramping in (w3 > 0 at steps 1,
+    2) vs the reference's own log and post-step parameters."""
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step
+    d = train_small
+    scene = golden_scene(d)
+    views = [golden_view(d, f"v{i}", i) for i in range(3)]
+    images = [d[f"img{i}"] for i in range(3)]
+    state = TrainState(scene, TrainConfig(total_steps=8, batch_size=3, step2_start=8,
+                                          step3_start=0, growth_stop=0))
+    for s in range(3):
+        rep = train_step(state, views, images)
+        ref = d["geo_loss"][s]
+        g = d["geo_geo"][s]
+        assert (rep.w3, rep.geo_pairs, rep.geo_patches) == (g[1], int(g[2]), int(g[3]))
+        assert rep.geo == pytest.approx(g[0], rel=1e-3, abs=1e-6)
+        np.testing.assert_allclose([rep.total, rep.rgb], ref[:2], rtol=2e-4, atol=1e-6)
+    names = [k[len("geo_post_"):] for k in d if k.startswith("geo_post_") and "_lv" not in k]
+    for name in names:
+        got = state.flat.view(state.flat.param, f"dec/{name}").detach().cpu().numpy()
+        ok, worst, nbad = rel_close(got, d[f"geo_post_{name}"], 1e-3, 1e-6)
+        assert nbad / got.size <= 5e-3, f"{name}: {nbad}/{got.size} off, worst {worst:.3g}"
+    for key, flat in (("embeddings", "emb"), ("log_scales", "log_scales"),
+                      ("offsets", "offsets")):
+        ref = np.concatenate([d[f"geo_post_lv{k}_{key}"].reshape(-1)
+                              for k in range(int(d["lod_count"]))])
+        got = state.flat.view(state.flat.param, flat).detach().cpu().numpy().reshape(-1)
+        ok, worst, nbad = rel_close(got, ref, 1e-3, 1e-6)
+        assert nbad / got.size <= 5e-3, f"{key}: {nbad}/{got.size} off, worst {worst:.3g}"
