@@ -278,6 +278,45 @@ def make_train_small():
     np.savez_compressed(OUT / "train_small.npz", **out)
 
 
+def make_growth():
+    """f3 anchor growth (trainer.py:341-349, 379-454): the train_small scene,
+    two reference train steps (growth accumulators), grow_anchors, one more
+    step on the grown scene."""
+    decoder, geometry, partition, renderer, scene_m, trainer, losses = _ref()
+    d = np.load(OUT / "train_small.npz")
+    pts = scene_m.SparsePoints(positions=d["points"])
+    views = []
+    for i in range(3):
+        views.append(geometry.CameraView(i, int(d[f"v{i}_size"][0]), int(d[f"v{i}_size"][1]),
+                                         *[float(x) for x in d[f"v{i}_intr"]],
+                                         d[f"v{i}_r"], d[f"v{i}_t"]))
+    images = [d[f"img{i}"] for i in range(3)]
+    scene = scene_m.build_hierarchy(pts, 0.25, 2, offsets_per_voxel=3, seed=4, views=views)
+    cfg = trainer.TrainConfig(total_steps=8, batch_size=3, workers=1, step2_start=8,
+                              step3_start=8, growth_stop=8, growth_threshold=7.35e-4,
+                              log_every=0)
+    state = trainer.make_state(scene, cfg)
+    out = {}
+    for _ in range(2):
+        trainer.train_step(state, views, images)
+    for k in range(scene.lod_count):
+        out[f"grow_sum{k}"] = state.grow_sum[k].copy()
+        out[f"grow_cnt{k}"] = state.grow_cnt[k].copy()
+    out["grown"] = np.array(trainer.grow_anchors(state))
+    out["events"] = np.array([[e["level"], e["added"], e["parents"]] for e in state.grow_events])
+    for k, lv in enumerate(scene.levels):
+        out[f"grid{k}"] = lv.grid
+        out[f"owner{k}"] = lv.owner
+    rep = trainer.train_step(state, views, images)
+    out["post_loss"] = np.array([rep.total, rep.rgb])
+    for k, t_ in state.replicas[0].tensors.items():
+        out[f"post_{k}"] = t_.detach().numpy()
+    for k in range(scene.lod_count):
+        for key in ("embeddings", "log_scales", "offsets"):
+            out[f"post_lv{k}_{key}"] = state.level_state[k][key].detach().numpy()
+    np.savez_compressed(OUT / "growth.npz", **out)
+
+
 def make_depth_prior():
     """f1 prior precompute: three aerial views of the ground plane z = 0 with
     raw relative depth maps (planted affine + noise, a corrupted stripe in view

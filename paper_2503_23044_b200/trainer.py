@@ -197,13 +197,8 @@ class TrainState:
         init = DecoderParams.init_arrays(
             n, seed=cfg.seed,
             scale_bias=float(np.log(cfg.init_scale_fraction * scene.base_voxel_size)))
-        dec_shapes = DecoderParams.shapes(n)
         names = DecoderParams.param_names(n)
-        shapes = [(f"dec/{k}", dec_shapes[k]) for k in names]
-        shapes += [("emb", (A, 32)), ("log_scales", (A, 3)), ("offsets", (A, n, 3))]
-        groups = {f"dec/{k}": "dec" for k in names}
-        groups.update({"emb": "emb", "log_scales": "log_scales", "offsets": "offsets"})
-        self.flat = FlatParams(shapes, groups)
+        self.flat = self._alloc_flat(A)
         with torch.no_grad():
             for k in names:
                 self.flat.view(self.flat.param, f"dec/{k}").copy_(
@@ -214,8 +209,30 @@ class TrainState:
                 torch.as_tensor(np.log(scene.flat("scales")), dtype=torch.float32))
             self.flat.view(self.flat.param, "offsets").copy_(
                 torch.as_tensor(scene.flat("offsets"), dtype=torch.float32))
-        self.params = DecoderParams(n, {k: self.flat.view(self.flat.param, f"dec/{k}")
-                                        for k in names})
+        self._bind_views()
+        self.assignment = assign_voxels(scene, cfg.workers)
+        self.dscene = D.device_scene_for(scene)
+        self._image_cache: dict = {}
+        # growth pressure (trainer.py:341-349): per anchor, sum and count of
+        # the decoded-position gradient norms of its gaussians (flat, level-major)
+        self.grow_sum_flat = torch.zeros(A, dtype=torch.float64, device="cuda")
+        self.grow_cnt_flat = torch.zeros(A, dtype=torch.float64, device="cuda")
+        self.grow_events: list[dict] = []
+
+    def _alloc_flat(self, A: int) -> "FlatParams":
+        n = self.n
+        dec_shapes = DecoderParams.shapes(n)
+        names = DecoderParams.param_names(n)
+        shapes = [(f"dec/{k}", dec_shapes[k]) for k in names]
+        shapes += [("emb", (A, 32)), ("log_scales", (A, 3)), ("offsets", (A, n, 3))]
+        groups = {f"dec/{k}": "dec" for k in names}
+        groups.update({"emb": "emb", "log_scales": "log_scales", "offsets": "offsets"})
+        return FlatParams(shapes, groups)
+
+    def _bind_views(self) -> None:
+        names = DecoderParams.param_names(self.n)
+        self.params = DecoderParams(self.n, {k: self.flat.view(self.flat.param, f"dec/{k}")
+                                             for k in names})
         self.dgrads = {k: self.flat.view(self.flat.grad, f"dec/{k}") for k in names}
         self.replicas = [self.params]
         self.anchors = AnchorState(self.flat.view(self.flat.param, "emb"),
@@ -224,9 +241,47 @@ class TrainState:
         self.anchor_grads = AnchorState(self.flat.view(self.flat.grad, "emb"),
                                         self.flat.view(self.flat.grad, "log_scales"),
                                         self.flat.view(self.flat.grad, "offsets"))
-        self.assignment = assign_voxels(scene, cfg.workers)
-        self.dscene = D.device_scene_for(scene)
-        self._image_cache: dict = {}
+
+    def _per_level(self, flat: torch.Tensor) -> dict:
+        b = self.scene.level_bases
+        host = flat.cpu().numpy()
+        return {k: host[int(b[k]):int(b[k + 1])].copy() for k in range(self.scene.lod_count)}
+
+    @property
+    def grow_sum(self) -> dict:
+        """Reference-shaped per-level growth sums (host copies)."""
+        return self._per_level(self.grow_sum_flat)
+
+    @property
+    def grow_cnt(self) -> dict:
+        return self._per_level(self.grow_cnt_flat)
+
+    def _insert_anchors(self, old_bases: np.ndarray, additions: dict) -> None:
+        """Re-lay the flat buffers after growth: every level keeps its rows and
+        gets its new anchors appended (level-major); new Adam moments are 0."""
+        new = self._alloc_flat(self.scene.total_voxels)
+        old = self.flat
+        nb = self.scene.level_bases
+        with torch.no_grad():
+            for name in old.layout:
+                if name.startswith("dec/"):
+                    for b_old, b_new in ((old.param, new.param), (old.m, new.m), (old.v, new.v)):
+                        new.view(b_new, name).copy_(old.view(b_old, name))
+            for name, key in (("emb", 0), ("log_scales", 1), ("offsets", 2)):
+                for k in range(self.scene.lod_count):
+                    lo, hi = int(old_bases[k]), int(old_bases[k + 1])
+                    dst = int(nb[k])
+                    for b_old, b_new in ((old.param, new.param), (old.m, new.m),
+                                         (old.v, new.v)):
+                        new.view(b_new, name)[dst:dst + hi - lo].copy_(
+                            old.view(b_old, name)[lo:hi])
+                    if k in additions:
+                        arr = torch.as_tensor(additions[k][key], dtype=torch.float32)
+                        new.view(new.param, name)[dst + hi - lo:int(nb[k + 1])].copy_(arr)
+        self.flat = new
+        self._bind_views()
+        self.dscene = D.device_scene_for(self.scene)
+        self._image_cache = {}
 
     # -- reference-compatible views ---------------------------------------
     @property
@@ -528,6 +583,11 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         with torch.cuda.stream(ts):
             with _span(timer, "project_bwd"):
                 gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P, gs, view)
+                # growth pressure: |dL/dmu| of every gaussian into its anchor
+                norms = torch.linalg.vector_norm(gg["means"].double(), dim=-1)
+                gidx = active.long().repeat_interleave(state.n)
+                state.grow_sum_flat.index_add_(0, gidx, norms)
+                state.grow_cnt_flat.index_add_(0, gidx, torch.ones_like(norms))
             with _span(timer, "decode_bwd"):
                 decoder_backward_into(params, state.dgrads, active, ds.centers, anchors.emb,
                                       anchors.log_scales, anchors.offsets, view, ds.lod_ref,
@@ -615,3 +675,70 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         intersections=isects, normal=normal, live_pairs=int(live))
     state.step += 1
     return report
+
+
+OCTANT_SIGNS = np.array([[sx, sy, sz] for sx in (-1.0, 1.0)
+                         for sy in (-1.0, 1.0) for sz in (-1.0, 1.0)])
+
+
+def grow_anchors(state: TrainState) -> int:
+    """Insert finer-level children under voxels with persistent gradient
+    strain (``trainer.py:379-454``): a level-k voxel whose mean decoded-position
+    gradient norm over the window exceeds ``growth_threshold`` gets its octant
+    cells at level k+1 (deduplicated, lattice-sorted) appended, with new
+    parameters drawn from ``state.rng`` in the reference's order. The device
+    buffers are re-laid out level-major; accumulators reset afterwards."""
+    from .scene import quantize
+    cfg, scene = state.cfg, state.scene
+    old_bases = scene.level_bases.copy()
+    gsum = state.grow_sum_flat.cpu().numpy()
+    gcnt = state.grow_cnt_flat.cpu().numpy()
+    additions: dict = {}
+    grown = 0
+    for k in range(scene.lod_count - 1):
+        lo, hi = int(old_bases[k]), int(old_bases[k + 1])
+        cnt, sm = gcnt[lo:hi], gsum[lo:hi]
+        if cnt.sum() == 0:
+            continue
+        mean = np.where(cnt > 0, sm / np.maximum(cnt, 1.0), 0.0)
+        parents = np.flatnonzero(mean > cfg.growth_threshold)
+        if parents.size == 0:
+            continue
+        child = scene.levels[k + 1]
+        cell = scene.levels[k].cell_size
+        cand = (scene.levels[k].centers[parents][:, None, :]
+                + OCTANT_SIGNS[None, :, :] * (cell / 4.0)).reshape(-1, 3)
+        grid = np.unique(quantize(cand, child.cell_size), axis=0)
+        if child.count:
+            have = {tuple(g) for g in child.grid}
+            fresh = np.array([g for g in grid if tuple(g) not in have],
+                             dtype=np.int64).reshape(-1, 3)
+        else:
+            fresh = grid
+        if fresh.size == 0:
+            continue
+        v_new = len(fresh)
+        n = scene.offsets_per_voxel
+        emb_dim = child.embeddings.shape[1]
+        new_emb = state.rng.uniform(-0.01, 0.01, size=(v_new, emb_dim))
+        new_scales = np.full((v_new, 3), child.cell_size)
+        new_offsets = state.rng.uniform(-0.5, 0.5, size=(v_new, n, 3))
+        child.grid = np.concatenate([child.grid, fresh])
+        child.embeddings = np.concatenate([child.embeddings, new_emb])
+        child.scales = np.concatenate([child.scales, new_scales])
+        child.offsets = np.concatenate([child.offsets, new_offsets])
+        child.owner = np.concatenate(
+            [child.owner, ((np.arange(v_new) + child.count - v_new) % cfg.workers).astype(np.int32)])
+        additions[k + 1] = (new_emb, np.log(new_scales), new_offsets)
+        grown += v_new
+        state.grow_events.append({"step": state.step, "level": k + 1, "added": v_new,
+                                  "parents": int(parents.size)})
+    if grown:
+        state.assignment = assign_voxels(scene, cfg.workers)
+        scene.validate()
+        state._insert_anchors(old_bases, additions)
+    A = scene.total_voxels
+    state.grow_sum_flat = torch.zeros(A, dtype=torch.float64, device="cuda")
+    state.grow_cnt_flat = torch.zeros(A, dtype=torch.float64, device="cuda")
+    return grown
+

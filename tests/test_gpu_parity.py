@@ -386,3 +386,40 @@ def test_train_steps_with_ncc_term_match_reference(train_small):
         got = state.flat.view(state.flat.param, flat).detach().cpu().numpy().reshape(-1)
         ok, worst, nbad = rel_close(got, ref, 1e-3, 1e-6)
         assert nbad / got.size <= 5e-3, f"{key}: {nbad}/{got.size} off, worst {worst:.3g}"
+
+
+def test_growth_matches_reference(train_small):
+    """f3: growth accumulators over two steps, grow_anchors (same children,
+    same RNG draws, same owners) and one step on the grown scene vs the
+    reference (trainer.py:341-349, 379-454)."""
+    from conftest import load_golden
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState, grow_anchors, train_step
+    g = load_golden("growth")
+    d = train_small
+    scene = golden_scene(d)
+    views = [golden_view(d, f"v{i}", i) for i in range(3)]
+    images = [d[f"img{i}"] for i in range(3)]
+    state = TrainState(scene, TrainConfig(total_steps=8, batch_size=3, step2_start=8,
+                                          step3_start=8, growth_stop=8,
+                                          growth_threshold=7.35e-4))
+    for _ in range(2):
+        train_step(state, views, images)
+    for k in range(scene.lod_count):
+        np.testing.assert_array_equal(state.grow_cnt[k], g[f"grow_cnt{k}"])
+        ok, worst, nbad = rel_close(state.grow_sum[k], g[f"grow_sum{k}"], 1e-3, 1e-9)
+        assert ok, f"level {k}: grow_sum worst rel {worst:.3g}"
+    assert grow_anchors(state) == int(g["grown"])
+    assert [[e["level"], e["added"], e["parents"]] for e in state.grow_events] == \
+        g["events"].tolist()
+    for k, lv in enumerate(scene.levels):
+        np.testing.assert_array_equal(lv.grid, g[f"grid{k}"])
+        np.testing.assert_array_equal(lv.owner, g[f"owner{k}"])
+    rep = train_step(state, views, images)
+    np.testing.assert_allclose([rep.total, rep.rgb], g["post_loss"], rtol=2e-4, atol=1e-6)
+    for key, flat in (("embeddings", "emb"), ("log_scales", "log_scales"),
+                      ("offsets", "offsets")):
+        ref = np.concatenate([g[f"post_lv{k}_{key}"].reshape(-1)
+                              for k in range(scene.lod_count)])
+        got = state.flat.view(state.flat.param, flat).detach().cpu().numpy().reshape(-1)
+        ok, worst, nbad = rel_close(got, ref, 1e-3, 1e-6)
+        assert nbad / got.size <= 5e-3, f"{key}: {nbad}/{got.size} off, worst {worst:.3g}"
