@@ -351,6 +351,17 @@ int vsx_ncc_scatter(const int32_t *centers, int32_t n_patches, int32_t half, int
                     double upstream, float *g_rgb, float *g_normal_img, float *g_depth_img,
                     vsx_stream s);
 
+/* ---- f4: TSDF fusion (fusion.py:102-133) --------------------------------- */
+/* Folds one depth map (float64 (H, W) + uint8 valid, device) into a dense
+ * volume: tsdf / weight are float64 device arrays of dims[0]*dims[1]*dims[2]
+ * voxels (ij-indexed, voxel (i,j,k) at origin + (i,j,k)*voxel_size); dims
+ * (3 int64) and origin (3 double) are HOST arrays. *touched (device u64) is
+ * incremented by the number of voxels updated. */
+int vsx_tsdf_integrate(double *tsdf, double *weight, const int64_t *dims, const double *origin,
+                       double voxel_size, double truncation, const double *depth,
+                       const uint8_t *valid, vsx_camera cam, unsigned long long *touched,
+                       vsx_stream s);
+
 /* ---- diagnostics --------------------------------------------------------- */
 /* tcgen05 self-test: D[128 x N] = A[128 x K] . B[N x K]^T, kind::tf32 from
  * shared memory into TMEM (three != 0: 3xTF32 split). */

@@ -317,6 +317,28 @@ def make_growth():
     np.savez_compressed(OUT / "growth.npz", **out)
 
 
+def make_fusion():
+    """f4 TSDF integration (fusion.py:102-133): a volume around the
+    depth_prior ground plane, integrated with the three aligned depth maps of
+    that fixture; per-call touched counts and the final tsdf / weight."""
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    from voxsplat.fusion import TsdfVolume
+    from voxsplat.geometry import CameraView
+    d = np.load(OUT / "depth_prior.npz")
+    vol = TsdfVolume.from_bounds([-3.0, -2.0, -0.5], [3.0, 3.0, 0.5], 0.1, 0.3)
+    touched = []
+    for i in range(3):
+        fx, fy, cx, cy = d[f"v{i}_intr"]
+        w, h = d[f"v{i}_size"]
+        view = CameraView(i, int(w), int(h), float(fx), float(fy), float(cx), float(cy),
+                          d[f"v{i}_r"], d[f"v{i}_t"])
+        touched.append(vol.integrate(d[f"aligned{i}_values"], d[f"aligned{i}_valid"], view))
+    np.savez_compressed(OUT / "fusion.npz", touched=np.array(touched), dims=np.array(vol.dims),
+                        origin=vol.origin, voxel=np.array(vol.voxel_size),
+                        trunc=np.array(vol.truncation), tsdf=vol.tsdf, weight=vol.weight)
+
+
 def make_depth_prior():
     """f1 prior precompute: three aerial views of the ground plane z = 0 with
     raw relative depth maps (planted affine + noise, a corrupted stripe in view

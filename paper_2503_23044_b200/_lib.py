@@ -102,6 +102,7 @@ _SIGS = {
     "vsx_ncc_patches": ([P, P, P, c_i32, c_i32, P, c_i32, c_i32, VsxNccGeom, P, c_i32, c_i32,
                          P, P, P, P, P, P, P, P, P], c_i32),
     "vsx_ncc_scatter": ([P, c_i32, c_i32, c_i32, P, P, P, P, P, P, c_f64, P, P, P, P], c_i32),
+    "vsx_tsdf_integrate": ([P, P, P, P, c_f64, c_f64, P, P, VsxCamera, P, P], c_i32),
 }
 
 EXPORTED = tuple(_SIGS)
