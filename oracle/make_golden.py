@@ -339,6 +339,46 @@ def make_fusion():
                         trunc=np.array(vol.truncation), tsdf=vol.tsdf, weight=vol.weight)
 
 
+def make_checkpoint():
+    """f4 .vsnap state IO (snapshot.py, trainer.py:491-522): a reference
+    checkpoint after two train steps on the train_small scene (the raw file,
+    committed), the records its own reader returns, and the reference's loss
+    and parameters after one more step from that file."""
+    decoder, geometry, partition, renderer, scene_m, trainer, losses = _ref()
+    from voxsplat import snapshot
+    d = np.load(OUT / "train_small.npz")
+    pts = scene_m.SparsePoints(positions=d["points"])
+    views = [geometry.CameraView(i, int(d[f"v{i}_size"][0]), int(d[f"v{i}_size"][1]),
+                                 *[float(x) for x in d[f"v{i}_intr"]], d[f"v{i}_r"],
+                                 d[f"v{i}_t"]) for i in range(3)]
+    images = [d[f"img{i}"] for i in range(3)]
+    scene = scene_m.build_hierarchy(pts, 0.25, 2, offsets_per_voxel=3, seed=4, views=views)
+    cfg = trainer.TrainConfig(total_steps=8, batch_size=3, workers=1, step2_start=8,
+                              step3_start=8, growth_stop=0, log_every=0)
+    state = trainer.make_state(scene, cfg)
+    for _ in range(2):
+        trainer.train_step(state, views, images)
+    path = OUT / "checkpoint.vsnap"
+    trainer.save_checkpoint(path, state)
+    data = snapshot.read_snapshot(path)
+    out = {f"{tag}:{name}": arr for tag, rec in data.items() for name, arr in rec.items()}
+    # resume: scene + decoder from the file, train records restored
+    scene2, dec2, rest = snapshot.load_scene(path)
+    st2 = trainer.make_state(scene2, cfg)
+    with torch.no_grad():
+        for k, t_ in st2.replicas[0].tensors.items():
+            t_.copy_(dec2.tensors[k])
+    trainer.restore_train_records(st2, rest["TRN1"])
+    rep = trainer.train_step(st2, views, images)
+    out["resume_loss"] = np.array([rep.total, rep.rgb, rep.step])
+    for k, t_ in st2.replicas[0].tensors.items():
+        out[f"resume_post_{k}"] = t_.detach().numpy()
+    for k in range(scene2.lod_count):
+        for key in ("embeddings", "log_scales", "offsets"):
+            out[f"resume_post_lv{k}_{key}"] = st2.level_state[k][key].detach().numpy()
+    np.savez_compressed(OUT / "checkpoint.npz", **out)
+
+
 def make_depth_prior():
     """f1 prior precompute: three aerial views of the ground plane z = 0 with
     raw relative depth maps (planted affine + noise, a corrupted stripe in view

@@ -742,3 +742,79 @@ def grow_anchors(state: TrainState) -> int:
     state.grow_cnt_flat = torch.zeros(A, dtype=torch.float64, device="cuda")
     return grown
 
+
+
+# ------------------------------------------------------------------ checkpoints
+
+_LEVEL_KEYS = (("embeddings", "emb"), ("log_scales", "log_scales"), ("offsets", "offsets"))
+
+
+def _moment_slices(state: TrainState):
+    """(reference moment name, flat buffer name, row slice) in the reference's
+    order: decoder tensors, then per level embeddings / log_scales / offsets."""
+    out = [(f"dec/{k}", f"dec/{k}", slice(None)) for k in DecoderParams.param_names(state.n)]
+    b = state.scene.level_bases
+    for k in range(state.scene.lod_count):
+        for key, flat in _LEVEL_KEYS:
+            out.append((f"lv{k}/{key}", flat, slice(int(b[k]), int(b[k + 1]))))
+    return out
+
+
+def train_records(state: TrainState) -> dict[str, np.ndarray]:
+    """Optimizer / train state as the reference's TRN1 records
+    (trainer.py:491-502): step, Adam moments (float64), growth accumulators,
+    RNG state."""
+    rec = {"meta_i": np.array([state.step, state.cfg.workers], np.int64)}
+    f = state.flat
+    for name, flat, sl in _moment_slices(state):
+        rec[f"adam/{name}/m"] = f.view(f.m, flat)[sl].double().cpu().numpy()
+        rec[f"adam/{name}/v"] = f.view(f.v, flat)[sl].double().cpu().numpy()
+    gs, gc = state.grow_sum, state.grow_cnt
+    for k in sorted(gs):
+        rec[f"grow/lv{k}/sum"] = gs[k]
+        rec[f"grow/lv{k}/cnt"] = gc[k]
+    blob = json.dumps(state.rng.bit_generator.state).encode()
+    rec["rng_state"] = np.frombuffer(blob, dtype=np.uint8).copy()
+    return rec
+
+
+def restore_train_records(state: TrainState, rec: dict) -> None:
+    """Inverse of train_records (trainer.py:505-516)."""
+    state.step = int(rec["meta_i"][0])
+    f = state.flat
+    with torch.no_grad():
+        for name, flat, sl in _moment_slices(state):
+            for buf, key in ((f.m, "m"), (f.v, "v")):
+                dst = f.view(buf, flat)[sl]
+                dst.copy_(torch.as_tensor(rec[f"adam/{name}/{key}"], dtype=torch.float32)
+                          .reshape(dst.shape))
+        b = state.scene.level_bases
+        for k in range(state.scene.lod_count):
+            lo, hi = int(b[k]), int(b[k + 1])
+            state.grow_sum_flat[lo:hi] = torch.as_tensor(rec[f"grow/lv{k}/sum"])
+            state.grow_cnt_flat[lo:hi] = torch.as_tensor(rec[f"grow/lv{k}/cnt"])
+    state.rng.bit_generator.state = json.loads(bytes(rec["rng_state"]).decode())
+
+
+def save_checkpoint(path, state: TrainState):
+    """Scene (with the trained anchor parameters), decoder and TRN1 in one
+    .vsnap file (trainer.py:519-522), readable by the reference."""
+    from .snapshot import save_scene
+    state.sync_to_scene()
+    return save_scene(path, state.scene, decoder=state.params,
+                      extra={"TRN1": train_records(state)})
+
+
+def load_checkpoint(path, cfg: TrainConfig) -> TrainState:
+    """Resume from a .vsnap written by save_checkpoint here or by the
+    reference: scene + decoder weights + (when present) optimizer state."""
+    from .snapshot import load_scene
+    scene, dec, rest = load_scene(path)
+    state = TrainState(scene, cfg)
+    if dec is not None:
+        with torch.no_grad():
+            for k, t in state.params.tensors.items():
+                t.copy_(dec.tensors[k])
+    if "TRN1" in rest:
+        restore_train_records(state, rest["TRN1"])
+    return state
