@@ -379,6 +379,36 @@ def make_checkpoint():
     np.savez_compressed(OUT / "checkpoint.npz", **out)
 
 
+def make_partition():
+    """f4 LPT/EMA scheduler (partition.py:84-207): schedules of three views
+    over 3 workers, cold and after two epochs of random measured seconds."""
+    decoder, geometry, partition, renderer, scene_m, trainer, losses = _ref()
+    rng = np.random.default_rng(21)
+    views = [geometry.CameraView(i, int(w), int(h), 50.0, 50.0, (w - 1) / 2, (h - 1) / 2,
+                                 np.eye(3), np.zeros(3))
+             for i, (w, h) in enumerate([(70, 40), (48, 48), (33, 65)])]
+    pts = scene_m.SparsePoints(positions=rng.uniform(-1, 1, size=(300, 3)))
+    scene = scene_m.build_hierarchy(pts, 0.5, 2, offsets_per_voxel=2, seed=0)
+    asg = partition.assign_voxels(scene, 3)
+    model = partition.PatchCostModel()
+    out = {"lpt_costs": rng.uniform(0, 5, 40).round(1)}
+    out["lpt_workers"] = partition.lpt_assign(out["lpt_costs"], 4)
+    for ep in range(3):
+        sch = partition.schedule_patches(views, 3, model)
+        out[f"ep{ep}_workers"] = sch.workers
+        out[f"ep{ep}_est"] = sch.est_costs
+        out[f"ep{ep}_loads"] = sch.loads()
+        meas = rng.uniform(0.0, 2e-3, len(sch.patches))
+        out[f"ep{ep}_measured"] = meas
+        st = partition.balance_report(asg, sch, meas, epoch=ep, cost_model=model)
+        out[f"ep{ep}_seconds"] = st.seconds
+        out[f"ep{ep}_stats"] = np.array([st.imbalance, st.load_fraction])
+        out[f"ep{ep}_voxels"] = st.voxel_counts
+    for k, lv in enumerate(scene.levels):
+        out[f"grid{k}"] = lv.grid
+    np.savez_compressed(OUT / "partition.npz", **out)
+
+
 def make_depth_prior():
     """f1 prior precompute: three aerial views of the ground plane z = 0 with
     raw relative depth maps (planted affine + noise, a corrupted stripe in view

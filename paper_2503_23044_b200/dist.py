@@ -76,9 +76,19 @@ class ExchangePlan:
     counts: np.ndarray        # (world, B): rows rank q contributes to view v
     rank: int
     world: int
+    renderers: np.ndarray | None = None   # (B,) renderer rank of each view
+
+    def __post_init__(self) -> None:
+        B = self.counts.shape[1]
+        if self.renderers is None:
+            self.renderers = np.array([renderer_of(v, self.world) for v in range(B)])
+        self.renderers = np.asarray(self.renderers, dtype=np.int64)
+        if self.renderers.shape != (B,) or np.any((self.renderers < 0) |
+                                                   (self.renderers >= self.world)):
+            raise ProtocolError("renderer ranks must be one valid rank per view")
 
     def views_of(self, r: int) -> list[int]:
-        return [v for v in range(self.counts.shape[1]) if renderer_of(v, self.world) == r]
+        return [v for v in range(self.counts.shape[1]) if int(self.renderers[v]) == r]
 
     def send_splits(self) -> list[int]:
         return [int(self.counts[self.rank, self.views_of(r)].sum()) for r in range(self.world)]
@@ -88,7 +98,8 @@ class ExchangePlan:
         return [int(self.counts[q, mine].sum()) for q in range(self.world)]
 
 
-def exchange_splats(payloads: list[SplatPayload], rank: int, world: int, group=None):
+def exchange_splats(payloads: list[SplatPayload], rank: int, world: int, group=None,
+                    renderers=None):
     """C1 forward: route every view's payload rows to its renderer rank.
 
     Returns (plan, merged) where merged[v] (for the views this rank renders)
@@ -100,7 +111,7 @@ def exchange_splats(payloads: list[SplatPayload], rank: int, world: int, group=N
     mine_counts = torch.tensor([p.count for p in payloads], dtype=torch.int64, device=dev)
     gathered = [torch.zeros_like(mine_counts) for _ in range(world)]
     dist.all_gather(gathered, mine_counts, group=group)
-    plan = ExchangePlan(torch.stack(gathered).cpu().numpy(), rank, world)
+    plan = ExchangePlan(torch.stack(gathered).cpu().numpy(), rank, world, renderers)
     send_parts = [payloads[v] for r in range(world) for v in plan.views_of(r)]
     send = SplatPayload.cat(send_parts, payloads[0])
     ins, outs = plan.send_splits(), plan.recv_splits()
@@ -147,18 +158,29 @@ def return_grads(plan: ExchangePlan, grads: dict[int, torch.Tensor], like: torch
     return out
 
 
-def sharded_train_step(backend, views, images, priors=None, normal_priors=None, group=None):
-    """One sharded step; returns the global loss terms (same on every rank)."""
+def sharded_train_step(backend, views, images, priors=None, normal_priors=None, group=None,
+                       scheduler=None):
+    """One sharded step; returns the global loss terms (same on every rank).
+
+    With a ``partition.ViewScheduler`` the renderer rank of every view comes
+    from LPT over the EMA of each view's measured render seconds (the
+    reference's patch scheduler, ``partition.py:84-207``, applied to whole
+    views); the per-view times are summed across ranks so every rank folds
+    identical measurements into its model and picks the same assignment.
+    """
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     B = len(views)
+    renderers = scheduler.assign(views, world) if scheduler is not None else None
     backend.begin_step(views)
     payloads = [backend.forward_shard(v, views[v]) for v in range(B)]
-    plan, merged = exchange_splats(payloads, rank, world, group)
-    grads = {}
+    plan, merged = exchange_splats(payloads, rank, world, group, renderers)
+    grads, timers = {}, {}
     for v, (payload, seg) in merged.items():
+        t0 = _Stopwatch(payload.z.device)
         grads[v] = backend.render(v, views[v], payload, images[v],
                                   None if priors is None else priors[v],
                                   None if normal_priors is None else normal_priors[v])
+        timers[v] = t0.stop()
     back = return_grads(plan, grads, backend.grad_like(), group)
     for v in range(B):
         backend.backward_shard(v, views[v], back[v])
@@ -167,7 +189,50 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
     dist.all_reduce(losses, op=dist.ReduceOp.SUM, group=group)
     report = backend.finish_step(losses)
     check_replicas(backend.decoder_checksum(), group)
+    secs = torch.zeros(B, dtype=torch.float64)
+    for v, t in timers.items():
+        secs[v] = t.seconds()
+    if dist.get_backend(group) == "nccl":
+        secs = secs.cuda()
+    dist.all_reduce(secs, op=dist.ReduceOp.SUM, group=group)
+    secs = secs.cpu().numpy()
+    per_rank = np.bincount(plan.renderers, weights=secs, minlength=world)
+    if isinstance(report, dict):
+        report["render_seconds"] = per_rank.tolist()
+        report["imbalance"] = float(per_rank.max() / per_rank.mean()) if per_rank.sum() > 0 \
+            else 1.0
+    if scheduler is not None:
+        scheduler.update(views, secs)
     return report
+
+
+class _Stopwatch:
+    """Seconds of the work issued between construction and stop(): CUDA
+    events on the current stream for device work, wall clock otherwise."""
+
+    def __init__(self, device):
+        self.cuda = getattr(device, "type", "cpu") == "cuda"
+        if self.cuda:
+            self.a = torch.cuda.Event(enable_timing=True)
+            self.b = torch.cuda.Event(enable_timing=True)
+            self.a.record()
+        else:
+            import time
+            self.t = time.perf_counter()
+
+    def stop(self) -> "_Stopwatch":
+        if self.cuda:
+            self.b.record()
+        else:
+            import time
+            self.t = time.perf_counter() - self.t
+        return self
+
+    def seconds(self) -> float:
+        if self.cuda:
+            self.b.synchronize()
+            return self.a.elapsed_time(self.b) / 1e3
+        return float(self.t)
 
 
 def check_replicas(checksum: torch.Tensor, group=None) -> None:

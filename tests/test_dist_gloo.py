@@ -90,9 +90,10 @@ def _small_state(d):
         step3_start=8)
 
 
-def _sharded_worker(rank, world, port, out):
+def _sharded_worker(rank, world, port, out, scheduled=False):
     from oracle.shard import OracleShardBackend
     from paper_2503_23044_b200.dist import sharded_train_step
+    from paper_2503_23044_b200.partition import ViewScheduler
     _init(rank, world, port)
     d = load_golden("train_small")
     views = [golden_view(d, f"v{i}", i) for i in range(3)]
@@ -100,7 +101,13 @@ def _sharded_worker(rank, world, port, out):
     priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
     st = _small_state(d)
     be = OracleShardBackend(st, rank, world)
-    reps = [sharded_train_step(be, views, images, priors) for _ in range(2)]
+    sched = None
+    if scheduled:
+        # EMA history that moves view 1 to rank 0 and views 0, 2 to rank 1
+        sched = ViewScheduler(beta=1.0)
+        sched.update(views, [1.0, 5.0, 1.0])
+        sched.update = lambda *a, **k: None  # keep the planted assignment
+    reps = [sharded_train_step(be, views, images, priors, scheduler=sched) for _ in range(2)]
     torch.save({"reps": reps, "owned": be.owned,
                 "weights": {k: v.numpy() for k, v in st.weights.items()},
                 "emb": st.emb.numpy(), "offsets": st.offsets.numpy(),
@@ -109,7 +116,8 @@ def _sharded_worker(rank, world, port, out):
 
 
 @pytest.mark.slow
-def test_sharded_step_two_ranks_matches_single_process_oracle():
+@pytest.mark.parametrize("scheduled", [False, True])
+def test_sharded_step_two_ranks_matches_single_process_oracle(scheduled):
     import oracle
     port = _free_port()
     d = load_golden("train_small")
@@ -120,7 +128,7 @@ def test_sharded_step_two_ranks_matches_single_process_oracle():
     cams = [oracle.Cam.of(v) for v in views]
     ref_reps = [oracle.train_step(ref, cams, images, priors) for _ in range(2)]
     with tempfile.TemporaryDirectory() as out:
-        mp.spawn(_sharded_worker, args=(2, port, out), nprocs=2, join=True)
+        mp.spawn(_sharded_worker, args=(2, port, out, scheduled), nprocs=2, join=True)
         res = [torch.load(os.path.join(out, f"r{r}.pt"), weights_only=False) for r in range(2)]
     for r in res:
         for s in range(2):
