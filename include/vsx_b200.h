@@ -189,6 +189,18 @@ int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t n, int32_t 
  * (lower_bound per tile; no atomics). */
 int vsx_tile_ranges(const uint32_t *sorted_tiles, int64_t n, int32_t num_tiles,
                     uint32_t *tile_offsets, vsx_stream s);
+/* Tile-major alternative to phases 2-3 (the training path): with
+ * tile_offsets = exclusive scan of vsx_bin_count's tile_counts (splat_tiles
+ * may be NULL), every covered tile's next slot (atomic cursor, num_tiles
+ * u32 scratch, zeroed here) gets the splat rank; vsx_tile_segsort then sorts
+ * each tile's ranks ascending (one CTA per tile, shared-memory bitonic sort;
+ * VSX_ERR_CAPACITY when max_len > 4096 — the caller falls back to phases
+ * 2-3). The result equals the sorted (tile, rank) lists bit for bit. */
+int vsx_bin_emit_tiles(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
+                       int32_t height, const uint32_t *tile_offsets, uint32_t *cursor,
+                       uint32_t *tile_list, vsx_stream s);
+int vsx_tile_segsort(const uint32_t *tile_offsets, int32_t num_tiles, uint32_t *tile_list,
+                     int32_t max_len, vsx_stream s);
 
 /* ---- K5: compositing forward (renderer.py:242-301, 390-449) ----------- */
 /* tile_offsets (T+1) CSR over tile_list (sorted ranks). Outputs are HWC

@@ -103,6 +103,8 @@ _SIGS = {
                          P, P, P, P, P, P, P, P, P], c_i32),
     "vsx_ncc_scatter": ([P, c_i32, c_i32, c_i32, P, P, P, P, P, P, c_f64, P, P, P, P], c_i32),
     "vsx_tsdf_integrate": ([P, P, P, P, c_f64, c_f64, P, P, VsxCamera, P, P], c_i32),
+    "vsx_bin_emit_tiles": ([P, P, c_i32, c_i32, c_i32, P, P, P, P], c_i32),
+    "vsx_tile_segsort": ([P, c_i32, P, c_i32, P], c_i32),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -156,7 +156,57 @@ __global__ void bin_count_kernel(const vsx_splat *__restrict__ rec,
       for (int ty = y0; ty <= y1; ++ty)
         for (int tx = x0; tx <= x1; ++tx) atomicAdd(tile_counts + ty * txn + tx, 1u);
   }
-  splat_tiles[i] = cnt;
+  if (splat_tiles) splat_tiles[i] = cnt;
+}
+
+// Tile-major emission: every covered tile's next free slot (atomic cursor)
+// gets the splat's rank. Order inside a tile is arbitrary here and restored
+// by tile_segsort_kernel.
+__global__ void bin_emit_tiles_kernel(const vsx_splat *__restrict__ rec,
+                                      const double *__restrict__ radius, int32_t n, int txn,
+                                      int tyn, const uint32_t *__restrict__ tile_off,
+                                      uint32_t *__restrict__ cursor,
+                                      uint32_t *__restrict__ tile_list) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int x0, x1, y0, y1;
+  if (!tile_rect(rec[i].mean2d[0], rec[i].mean2d[1], radius[i], txn, tyn, x0, x1, y0, y1)) return;
+  for (int ty = y0; ty <= y1; ++ty)
+    for (int tx = x0; tx <= x1; ++tx) {
+      const int t = ty * txn + tx;
+      tile_list[tile_off[t] + atomicAdd(cursor + t, 1u)] = (uint32_t)i;
+    }
+}
+
+// One CTA per tile: bitonic sort of the tile's ranks in shared memory (ranks
+// are unique, so ascending order is exactly the reference's emission order).
+constexpr int kSegCap = 4096;
+
+__global__ void __launch_bounds__(256) tile_segsort_kernel(const uint32_t *__restrict__ tile_off,
+                                                           uint32_t *__restrict__ tile_list) {
+  __shared__ uint32_t s[kSegCap];
+  const uint32_t b = tile_off[blockIdx.x], n = tile_off[blockIdx.x + 1] - b;
+  if (n <= 1) return;
+  uint32_t N = 2;
+  while (N < n) N <<= 1;
+  for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) s[i] = i < n ? tile_list[b + i] : 0xFFFFFFFFu;
+  __syncthreads();
+  for (uint32_t k = 2; k <= N; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const uint32_t a = s[i], c = s[l];
+          if ((a > c) == ((i & k) == 0)) {
+            s[i] = c;
+            s[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) tile_list[b + i] = s[i];
 }
 
 // tile_off[t] = lower_bound(sorted_tiles, t), tile_off[T] = n.
@@ -369,6 +419,32 @@ extern "C" int vsx_tile_ranges(const uint32_t *sorted_tiles, int64_t n, int32_t 
   tile_ranges_kernel<<<grid_for(num_tiles + 1, 256), 256, 0, as_stream(s)>>>(
       sorted_tiles, n, num_tiles, tile_offsets);
   VSX_LAUNCH_CHECK("tile_ranges");
+  return VSX_OK;
+}
+
+extern "C" int vsx_bin_emit_tiles(const vsx_splat *rec, const double *radius, int32_t n,
+                                  int32_t width, int32_t height, const uint32_t *tile_offsets,
+                                  uint32_t *cursor, uint32_t *tile_list, vsx_stream s) {
+  VSX_REQUIRE(width > 0 && height > 0 && n >= 0, "bin_emit_tiles: bad arguments");
+  const int txn = (width + kTile - 1) / kTile, tyn = (height + kTile - 1) / kTile;
+  cudaStream_t st = as_stream(s);
+  VSX_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * txn * tyn, st));
+  if (n == 0) return VSX_OK;
+  bin_emit_tiles_kernel<<<grid_for(n, 256), 256, 0, st>>>(rec, radius, n, txn, tyn, tile_offsets,
+                                                          cursor, tile_list);
+  VSX_LAUNCH_CHECK("bin_emit_tiles");
+  return VSX_OK;
+}
+
+extern "C" int vsx_tile_segsort(const uint32_t *tile_offsets, int32_t num_tiles,
+                                uint32_t *tile_list, int32_t max_len, vsx_stream s) {
+  VSX_REQUIRE(num_tiles >= 1, "tile_segsort: bad num_tiles");
+  if (max_len > kSegCap) {
+    vsx_set_error("tile_segsort: tile list of %d > %d entries", max_len, kSegCap);
+    return VSX_ERR_CAPACITY;
+  }
+  tile_segsort_kernel<<<num_tiles, 256, 0, as_stream(s)>>>(tile_offsets, tile_list);
+  VSX_LAUNCH_CHECK("tile_segsort");
   return VSX_OK;
 }
 
