@@ -303,11 +303,9 @@ __global__ void __launch_bounds__(256) decode_bwd_gauss_kernel(
   // means = c + offset * l  (each (anchor, slot) appears once per view)
   const int a = active[r];
   float *goff = g_offsets + ((size_t)a * n + sl) * 3;
+  // float32 is ample for a gradient (the forward keeps mu in float64)
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const double l = exp((double)log_scale[3 * a + c]);
-    atomicAdd(goff + c, (float)((double)g_means[3 * g + c] * l));
-  }
+  for (int c = 0; c < 3; ++c) atomicAdd(goff + c, g_means[3 * g + c] * expf(log_scale[3 * a + c]));
 }
 
 // Backward, part 2 (anchor-parallel): g_h = W2_h^T g_o, tanh backward ->

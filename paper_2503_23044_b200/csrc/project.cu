@@ -130,10 +130,11 @@ __global__ void gather_splats_kernel(const vsx_splat *__restrict__ rec,
 // Tile rectangle of a splat (renderer.py:216-221), float64 floor semantics.
 __device__ __forceinline__ bool tile_rect(double u, double v, double r, int txn, int tyn, int &x0,
                                           int &x1, int &y0, int &y1) {
-  const double fx0 = fmax(floor(dsub(u, r) / 16.0), 0.0);
-  const double fx1 = fmin(floor(dadd(u, r) / 16.0), (double)(txn - 1));
-  const double fy0 = fmax(floor(dsub(v, r) / 16.0), 0.0);
-  const double fy1 = fmin(floor(dadd(v, r) / 16.0), (double)(tyn - 1));
+  // x / 16 == x * 0.0625 exactly (power of two), without the f64 divide
+  const double fx0 = fmax(floor(dmul(dsub(u, r), 0.0625)), 0.0);
+  const double fx1 = fmin(floor(dmul(dadd(u, r), 0.0625)), (double)(txn - 1));
+  const double fy0 = fmax(floor(dmul(dsub(v, r), 0.0625)), 0.0);
+  const double fy1 = fmin(floor(dmul(dadd(v, r), 0.0625)), (double)(tyn - 1));
   if (!(fx1 >= fx0) || !(fy1 >= fy0)) return false;
   x0 = (int)fx0;
   x1 = (int)fx1;
@@ -227,17 +228,34 @@ __global__ void bin_emit_kernel(const vsx_splat *__restrict__ rec,
                                 const double *__restrict__ radius, int32_t n, int txn, int tyn,
                                 const uint32_t *__restrict__ offs, uint32_t *__restrict__ tiles,
                                 uint32_t *__restrict__ ranks) {
+  // Warp-cooperative emission: the warp walks its 32 splats in order and all
+  // lanes write one splat's row-major tile run together, so every store
+  // instruction covers consecutive addresses (a thread-per-splat loop made
+  // each lane stream its own run: one 32-byte sector per 4-byte store).
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int x0, x1, y0, y1;
-  if (!tile_rect(rec[i].mean2d[0], rec[i].mean2d[1], radius[i], txn, tyn, x0, x1, y0, y1)) return;
-  uint32_t o = offs[i];
-  for (int ty = y0; ty <= y1; ++ty)
-    for (int tx = x0; tx <= x1; ++tx) {
-      tiles[o] = (uint32_t)(ty * txn + tx);
-      ranks[o] = (uint32_t)i;
-      ++o;
+  const int lane = threadIdx.x & 31;
+  int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
+  bool ok = false;
+  uint32_t o = 0;
+  if (i < n) {
+    ok = tile_rect(rec[i].mean2d[0], rec[i].mean2d[1], radius[i], txn, tyn, x0, x1, y0, y1);
+    o = offs[i];
+  }
+  const int w = ok ? x1 - x0 + 1 : 0, h = ok ? y1 - y0 + 1 : 0;
+  const unsigned live = __ballot_sync(0xffffffffu, ok);
+  const uint32_t first = (uint32_t)(i - lane);
+  for (int sl = 0; sl < 32; ++sl) {
+    if (!((live >> sl) & 1u)) continue;  // warp-uniform
+    const int ws = __shfl_sync(0xffffffffu, w, sl), hs = __shfl_sync(0xffffffffu, h, sl);
+    const int xs = __shfl_sync(0xffffffffu, x0, sl), ys = __shfl_sync(0xffffffffu, y0, sl);
+    const uint32_t os = __shfl_sync(0xffffffffu, o, sl);
+    const int cnt = ws * hs;
+    for (int k = lane; k < cnt; k += 32) {
+      const int ty = ys + k / ws, tx = xs + k % ws;
+      tiles[os + k] = (uint32_t)(ty * txn + tx);
+      ranks[os + k] = first + (uint32_t)sl;
     }
+  }
 }
 
 // ---------------------------------------------------------------- K7 backward
@@ -408,7 +426,7 @@ extern "C" int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t 
   const int txn = (width + kTile - 1) / kTile, tyn = (height + kTile - 1) / kTile;
   bin_emit_kernel<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(rec, radius, n, txn, tyn,
                                                               splat_offsets, isect_tile,
-                                                              isect_rank);
+                                                              isect_rank);  // whole warps
   VSX_LAUNCH_CHECK("bin_emit");
   return VSX_OK;
 }
