@@ -570,6 +570,16 @@ def train_step(st: OracleState, cams: list, images: list, priors: list | None = 
         tb = time.perf_counter()
         timing["t_tiles"] += tb - tt
         timing["tiles_done"] += done
+        if tile_limit is None:
+            # tiles without splats render black (renderer.py:390-449): their
+            # pixels still count |0 - I| in the L1 term (no gradient)
+            empty = np.flatnonzero(np.diff(offsets) == 0)
+            if empty.size:
+                ey, ex = np.divmod(empty, tx_n)
+                m = np.zeros((ty_n * 16, tx_n * 16), bool)
+                for y0, x0 in zip(ey * 16, ex * 16):
+                    m[y0:y0 + 16, x0:x0 + 16] = True
+                rgb_sum = rgb_sum + gt[torch.from_numpy(m[:H, :W])].abs().sum()
         rgb_terms.append(rgb_sum / (H * W * 3))
         if vi in have:
             depth_terms.append(dep_sum * (dnorm * len(have) / w2))

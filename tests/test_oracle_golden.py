@@ -12,7 +12,7 @@ import pytest
 import torch
 
 import oracle
-from conftest import golden_scene, golden_view
+from conftest import golden_scene, golden_view, load_golden
 
 F64 = torch.float64
 
@@ -207,3 +207,34 @@ def test_oracle_cfg1_matches_reference(cfg1_golden):
     for name in ("emb", "log_scales", "offsets"):
         np.testing.assert_allclose(getattr(st, name).numpy()[rows], d[f"post_lv_{name}"],
                                    rtol=1e-7, atol=1e-12)
+
+
+@pytest.mark.slow
+def test_oracle_empty_and_ragged_views_match_reference():
+    """A ragged 37x29 view (partial tiles on both axes) next to a regular one:
+    oracle losses and decoder update vs the reference (edge_views golden)."""
+    from conftest import golden_scene, golden_view
+    from paper_2503_23044_b200.geometry import CameraView, look_at
+    d = load_golden("train_small")
+    g = load_golden("edge_views")
+    scene = golden_scene(d)
+    v0 = golden_view(d, "v0", 0)
+    r, t = look_at(np.array([0.0, 0.0, 5.0]), np.array([0.0, 0.0, 10.0]))
+    away = CameraView(7, 48, 40, 40.0, 40.0, 23.5, 19.5, r, t)
+    rr, tt = look_at(np.array([1.2, -1.1, 1.3]), np.zeros(3))
+    ragged = CameraView(8, 37, 29, 30.0, 30.0, 18.0, 14.0, rr, tt)
+    del away  # the reference itself raises on an empty view (see make_edge_views)
+    cams = [oracle.Cam.of(v) for v in (v0, ragged)]
+    images = [d["img0"], g["img_ragged"]]
+    w = oracle.decoder_init(3, 0, float(np.log(0.125 * scene.base_voxel_size)))
+    st = oracle.OracleState.create(
+        scene.flat_centers(), scene.flat_levels(), scene.lod_count, scene.lod_ref_distance,
+        scene.lod_bias, scene.base_voxel_size, 3, w, scene.flat("embeddings"),
+        np.log(scene.flat("scales")), scene.flat("offsets"), total_steps=8)
+    for s in range(2):
+        rep = oracle.train_step(st, cams, images)
+        np.testing.assert_allclose([rep["total"], rep["rgb"], rep["gaussians"]], g["loss"][s],
+                                   rtol=1e-10)
+    for name, t_ in st.weights.items():
+        np.testing.assert_allclose(t_.detach().numpy(), g[f"post_{name}"], rtol=1e-8,
+                                   atol=1e-12)
