@@ -406,6 +406,17 @@ __global__ void __launch_bounds__(128) decode_bwd_anchor_kernel(
 // fragment-ordered hi/lo images (decoder_bwd_image_kernel), one float4 per
 // (k-step, n-tile, lane).
 
+// VSX_DECODE_IMG=smem copies the mma weight images into shared memory per CTA
+// (A/B); by default fragments are read through L1, which leaves the SM's
+// shared memory to the compositor kernels running concurrently.
+inline int decode_image_in_smem() {
+  static const int v = [] {
+    const char *e = getenv("VSX_DECODE_IMG");
+    return (e && e[0] == 's') ? 1 : 0;
+  }();
+  return v;
+}
+
 __host__ __device__ inline int dbw_ks(int h, int n) { return (dec_head_w(h, n) + 7) / 8; }
 __host__ __device__ inline int dbw_ks_total(int n) { return dbw_ks(0, n) + dbw_ks(1, n) + dbw_ks(2, n); }
 __host__ __device__ inline size_t dbw_w2_floats(int n) { return (size_t)dbw_ks_total(n) * 8 * 32 * 4; }
@@ -485,13 +496,17 @@ __global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kerne
     const float *__restrict__ log_scale, const float *__restrict__ offsets, vsx_camera cam,
     double lod_ref, const float *__restrict__ cache_h, const float *__restrict__ g_means,
     const float *__restrict__ g_o, float *__restrict__ g_emb, float *__restrict__ g_log_scale,
-    float *__restrict__ xs, float *__restrict__ g_pre_out) {
+    float *__restrict__ xs, float *__restrict__ g_pre_out, int smem_img) {
   extern __shared__ __align__(16) float4 dimg[];
   const int kst = dbw_ks_total(n);
-  const int nimg = (int)(dbw_image_floats(n) / 4);
-  for (int e = threadIdx.x; e < nimg; e += blockDim.x) dimg[e] = img[e];
-  __syncthreads();
-  const float4 *w2i = dimg, *w1i = dimg + kst * 8 * 32;
+  const float4 *base = img;  // weight fragments read through L1 (shared with the compositor)
+  if (smem_img) {
+    const int nimg = (int)(dbw_image_floats(n) / 4);
+    for (int e = threadIdx.x; e < nimg; e += blockDim.x) dimg[e] = img[e];
+    __syncthreads();
+    base = dimg;
+  }
+  const float4 *w2i = base, *w1i = base + kst * 8 * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const size_t ld = cache_ld(n_active);
@@ -658,16 +673,21 @@ constexpr int kDfwWarps = 16;
 __global__ void __launch_bounds__(kDfwWarps * 32, 1) decode_fwd_mma_kernel(
     vsx_decoder W, const float4 *__restrict__ img, const int32_t *__restrict__ active,
     int32_t n_active, const double *__restrict__ centers, const float *__restrict__ emb,
-    vsx_camera cam, double lod_ref, float *__restrict__ cache_h, float *__restrict__ cache_o) {
+    vsx_camera cam, double lod_ref, float *__restrict__ cache_h, float *__restrict__ cache_o,
+    int smem_img) {
   extern __shared__ __align__(16) float4 fimg[];
   __shared__ float s_b2[11 * 10];
   const int n = W.n;
-  const int nimg = (int)(dfw_image_floats(n) / 4);
-  for (int e = threadIdx.x; e < nimg; e += blockDim.x) fimg[e] = img[e];
+  const float4 *base = img;  // weight fragments read through L1 (shared with the compositor)
+  if (smem_img) {
+    const int nimg = (int)(dfw_image_floats(n) / 4);
+    for (int e = threadIdx.x; e < nimg; e += blockDim.x) fimg[e] = img[e];
+    base = fimg;
+  }
   for (int j = threadIdx.x; j < 11 * n; j += blockDim.x)
     s_b2[j] = j < n ? W.b2[0][j] : (j < 4 * n ? W.b2[1][j - n] : W.b2[2][j - 4 * n]);
   __syncthreads();
-  const float4 *w1i = fimg, *w2i = fimg + 3 * 5 * 8 * 32;
+  const float4 *w1i = base, *w2i = base + 3 * 5 * 8 * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const size_t ld = cache_ld(n_active);
@@ -772,9 +792,11 @@ int decode_fwd_mma(vsx_decoder W, const float *img, const int32_t *active, int32
                    const double *centers, const float *emb, vsx_camera cam, double lod_ref,
                    float *cache_h, float *cache_o, cudaStream_t st) {
   if (!dfw_supported(W.n) || 11 * W.n > 110) return 1;
-  const size_t smem = sizeof(float) * dfw_image_floats(W.n);
+  const int smem_img = decode_image_in_smem();
+  const size_t smem = smem_img ? sizeof(float) * dfw_image_floats(W.n) : 0;
   VSX_CUDA_TRY(cudaFuncSetAttribute(decode_fwd_mma_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(float) * dfw_image_floats(W.n))));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -782,7 +804,7 @@ int decode_fwd_mma(vsx_decoder W, const float *img, const int32_t *active, int32
   const int grid = std::max(1, std::min(sms, (tiles + kDfwWarps - 1) / kDfwWarps));
   decode_fwd_mma_kernel<<<grid, kDfwWarps * 32, smem, st>>>(
       W, reinterpret_cast<const float4 *>(img), active, n_active, centers, emb, cam, lod_ref,
-      cache_h, cache_o);
+      cache_h, cache_o, smem_img);
   VSX_LAUNCH_CHECK("decode_fwd_mma");
   return VSX_OK;
 }
@@ -1140,10 +1162,12 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
     float4 *dimg = reinterpret_cast<float4 *>(g_o + (size_t)11 * n * ld);
     decoder_bwd_image_kernel<<<32, 256, 0, st>>>(W, dimg);
     VSX_LAUNCH_CHECK("decoder_bwd_image");
-    const size_t smem = sizeof(float) * dbw_image_floats(n);
-    VSX_REQUIRE(smem <= 113 * 1024, "decode_bwd: n=%d too large for the mma weight image", n);
+    const int smem_img = decode_image_in_smem();
+    const size_t smem_full = sizeof(float) * dbw_image_floats(n);
+    VSX_REQUIRE(smem_full <= 113 * 1024, "decode_bwd: n=%d too large for the mma weight image", n);
     VSX_CUDA_TRY(cudaFuncSetAttribute(decode_bwd_anchor_mma_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
+    const size_t smem = smem_img ? smem_full : 0;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1151,7 +1175,7 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
     const int grid = std::max(1, std::min(2 * sms, (warps_needed + kDbwWarps - 1) / kDbwWarps));
     decode_bwd_anchor_mma_kernel<<<grid, kDbwWarps * 32, smem, st>>>(
         n, dimg, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, cache_h,
-        g_means, g_o, g_emb, g_log_scale, xs, g_pre);
+        g_means, g_o, g_emb, g_log_scale, xs, g_pre, smem_img);
     VSX_LAUNCH_CHECK("decode_bwd_anchor_mma");
   } else {
     const size_t smem = dec_smem_bytes(n);
