@@ -449,3 +449,11 @@ def check_status(status: torch.Tensor, what: str) -> None:
         raise NumericalError(f"{what}: non positive definite 2d covariance")
     if s & STATUS_NONFINITE:
         raise NumericalError(f"{what}: non-finite decoder output")
+
+
+def raise_status(bits: int, what: str) -> None:
+    """check_status on an already-read status word."""
+    if bits & STATUS_NONPD:
+        raise NumericalError(f"{what}: non positive definite 2d covariance")
+    if bits & STATUS_NONFINITE:
+        raise NumericalError(f"{what}: non-finite decoder output")

@@ -213,6 +213,7 @@ class TrainState:
         self.assignment = assign_voxels(scene, cfg.workers)
         self.dscene = D.device_scene_for(scene)
         self._image_cache: dict = {}
+        self._inflight = None
         # growth pressure (trainer.py:341-349): per anchor, sum and count of
         # the decoded-position gradient norms of its gaussians (flat, level-major)
         self.grow_sum_flat = torch.zeros(A, dtype=torch.float64, device="cuda")
@@ -566,7 +567,8 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         nonlocal gaussians, isects
         active, dec, P, Bn, ev = fronts.pop(vi)
         hold.append((active, dec, P, Bn))
-        main.wait_event(ev)
+        with _span(timer, "wait_front"):   # main-stream idle time waiting for the front end
+            main.wait_event(ev)
         gaussians += dec.count
         isects += Bn.intersections
         return active, dec, P, Bn
@@ -644,35 +646,41 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             active, dec, P, Bn, R = fwd[vi]
             backward(vi, active, dec, P, Bn, R, loss_desc(vi, cot.get(vi)))
     main.wait_stream(ts)
-    D.check_status(status, "train_step")
+    # every report scalar in ONE device->host read (the only sync of the
+    # step; the non-finite check must precede Adam, trainer.py:317-321)
     hw = torch.tensor([v.height * v.width * 3 for v in views], dtype=torch.float64, device=dev)
-    rgb = float((rgb_acc / hw).mean())
-    depth = 0.0
-    supervised = 0
+    z = torch.zeros((), dtype=torch.float64, device=dev)
+    vals = [status[0].double(), (rgb_acc / hw).mean(), z, z, z, tile_max.max().double(),
+            live.double()]
     if have:
         cnt = dep_cnt.double()
         terms = torch.where(cnt > 0, dep_sum / cnt.clamp_min(1), torch.zeros_like(cnt))
-        depth = float(terms[have].mean())
-        supervised = int(dep_cnt.sum())
-    normal = 0.0
+        vals[2] = terms[have].mean()
+        vals[3] = dep_cnt.sum().double()
     if have_n:
         cnt = nrm_cnt.double()
         terms = torch.where(cnt > 0, nrm_sum / (3.0 * cnt.clamp_min(1)), torch.zeros_like(cnt))
-        normal = float(terms[have_n].mean())
+        vals[4] = terms[have_n].mean()
+    host = torch.stack(vals).cpu().numpy()
+    state._inflight = None  # the previous step's buffers are idle now
+    st_bits, rgb, depth, supervised, normal = int(host[0]), float(host[1]), float(host[2]), \
+        int(host[3]), float(host[4])
+    if st_bits:
+        D.raise_status(st_bits, "train_step")
     total = rgb + w2 * depth + wn * normal + w3 * geo_val
     if not np.isfinite(total):
         raise NumericalError(f"non-finite loss at step {state.step}: rgb={rgb:.4g} depth={depth:.4g}")
     with _span(timer, "adam"):
         state.adam()
-    torch.cuda.current_stream().synchronize()
-    del hold
+    # per-view buffers stay referenced until the next step's sync point (the
+    # GPU may still be running Adam and this step's last kernels)
+    state._inflight = hold
     report = StepReport(
         step=state.step, total=total, rgb=rgb, depth=depth, geo=geo_val, w2=w2, w3=w3,
         lr=cosine_lr(state.step, cfg.lr_decoder, cfg), supervised_depth_px=supervised,
         geo_pairs=geo_pairs, geo_patches=geo_patches, gaussians=gaussians, transfer_bytes=0,
-        imbalance=1.0,
-        max_tile_splats=int(tile_max.max()), seconds=time.perf_counter() - t0,
-        intersections=isects, normal=normal, live_pairs=int(live))
+        imbalance=1.0, max_tile_splats=int(host[5]), seconds=time.perf_counter() - t0,
+        intersections=isects, normal=normal, live_pairs=int(host[6]))
     state.step += 1
     return report
 
