@@ -68,6 +68,48 @@ __host__ __device__ __forceinline__ size_t cache_ld(int64_t n_active) {
   return (size_t)((n_active + 3) & ~int64_t(3));
 }
 
+// Gaussian-parallel decoder kernels stage the [rows x na] slice of a
+// feature-major cache (anchors r0 .. r0+na) through shared memory
+// ([rows][sp] floats). rows * na <= 11 * 256, so each of the 256 threads owns
+// at most 11 elements; all of its loads are issued before the first smem store
+// so their latencies overlap. Element e sits at row e / na, split with a float
+// reciprocal: (e + 0.5) / na is >= 0.5 / na from any integer and e < 2^12, so
+// the truncated product is the exact quotient.
+__device__ __forceinline__ int tile_row(int e, float inv_na) {
+  return __float2int_rz(((float)e + 0.5f) * inv_na);
+}
+
+__device__ __forceinline__ void stage_cache_tile(float *__restrict__ so, const float *__restrict__ src,
+                                                 size_t ld, int r0, int na, int rows, int sp) {
+  const int total = rows * na;
+  const float inv = 1.0f / (float)na;
+  float v[11];
+#pragma unroll
+  for (int i = 0; i < 11; ++i) {
+    const int e = (int)threadIdx.x + 256 * i;
+    const int row = tile_row(e, inv);
+    if (e < total) v[i] = __ldg(src + (size_t)row * ld + r0 + (e - row * na));
+  }
+#pragma unroll
+  for (int i = 0; i < 11; ++i) {
+    const int e = (int)threadIdx.x + 256 * i;
+    const int row = tile_row(e, inv);
+    if (e < total) so[row * sp + (e - row * na)] = v[i];
+  }
+}
+
+__device__ __forceinline__ void flush_cache_tile(float *__restrict__ dst, const float *__restrict__ so,
+                                                 size_t ld, int r0, int na, int rows, int sp) {
+  const int total = rows * na;
+  const float inv = 1.0f / (float)na;
+#pragma unroll
+  for (int i = 0; i < 11; ++i) {
+    const int e = (int)threadIdx.x + 256 * i;
+    const int row = tile_row(e, inv);
+    if (e < total) dst[(size_t)row * ld + r0 + (e - row * na)] = so[row * sp + (e - row * na)];
+  }
+}
+
 // Explicitly rounded float64 ops: nvcc would otherwise contract a*b+c into an
 // FMA, which numpy/torch elementwise code never does. Decisions that must be
 // bit-exact against the reference (culling, projection keys, binning) use these.

@@ -236,8 +236,11 @@ __device__ __forceinline__ void rot_vjp(float w, float x, float y, float z, cons
 
 // Backward, part 1 (gaussian-parallel): per-gaussian cotangents -> head-output
 // cotangents g_o (feature-major, row = head output column) and the offsets
-// grads. Thread index = sl * n_active + r, so every g_o row is written
-// coalesced; the per-gaussian inputs are read with stride n (L2-resident).
+// grads. A block owns floor(256 / n) whole anchors (n gaussians each, thread =
+// gaussian, so every per-gaussian array is read coalesced); the block's
+// [11n x anchors] slice of the raw head outputs is staged through shared
+// memory in, and the g_o slice out, so the feature-major rows move as
+// contiguous runs instead of one scattered 4-byte access per (gaussian, row).
 __global__ void __launch_bounds__(256) decode_bwd_gauss_kernel(
     int n, const int32_t *__restrict__ active, int32_t n_active,
     const float *__restrict__ log_scale, const float *__restrict__ offsets, double max_scale,
@@ -247,65 +250,86 @@ __global__ void __launch_bounds__(256) decode_bwd_gauss_kernel(
     const float *__restrict__ g_scale, const float *__restrict__ g_quat,
     const float *__restrict__ g_normal, float *__restrict__ g_offsets,
     float *__restrict__ g_o_out) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)n_active * n) return;
-  const int sl = (int)(idx / n_active), r = (int)(idx % n_active);
+  extern __shared__ float so[];  // [11n][ab + 1]
+  const int ab = 256 / n, sp = ab + 1;
+  const int r0 = blockIdx.x * ab;
+  const int na = min(ab, n_active - r0);
+  const int rows = 11 * n;
   const size_t ld = cache_ld(n_active);
+  const int t = threadIdx.x;
+  stage_cache_tile(so, cache_o, ld, r0, na, rows, sp);
+  __syncthreads();
+  const bool ok = t < na * n;
+  const int ra = t / n, sl = t - ra * n;  // block-local anchor, slot
+  const int r = r0 + ra;
   const size_t g = (size_t)r * n + sl;
   const float smax = (float)max_scale, smin = (float)kMinScale;
-  {
-    const float sg = sigmoidf_(cache_o[(size_t)sl * ld + r]);
-    g_o_out[(size_t)sl * ld + r] = g_opacity[g] * sg * (1.f - sg);
+  float go[11];
+  if (ok) {
+    {
+      const float sg = sigmoidf_(so[sl * sp + ra]);
+      go[0] = g_opacity[g] * sg * (1.f - sg);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float sg = sigmoidf_(so[(n + 3 * sl + c) * sp + ra]);
+      go[1 + c] = g_color[3 * g + c] * sg * (1.f - sg);
+    }
+    float o[7];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) o[c] = so[(4 * n + 7 * sl + c) * sp + ra];
+    // scales: clamp(exp(o), 1e-6, max) — gradient passes inside [min, max]
+    float sc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float e = expf(o[c]);
+      sc[c] = dscale[3 * g + c];
+      const bool pass = (e >= smin) && (e <= smax);
+      go[4 + c] = pass ? g_scale[3 * g + c] * e : 0.f;
+    }
+    // quaternion: normalised (o[3:7] + (1,0,0,0)); normal = column argmin(s) of R(q)
+    const float qw = dquat[4 * g + 0], qx = dquat[4 * g + 1], qy = dquat[4 * g + 2],
+                qz = dquat[4 * g + 3];
+    float gq[4] = {g_quat[4 * g + 0], g_quat[4 * g + 1], g_quat[4 * g + 2], g_quat[4 * g + 3]};
+    const int ax = argmin3(sc[0], sc[1], sc[2]);
+    float G[9];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {  // register selects: a dynamic index would spill G
+      const float gn = g_normal[3 * g + c];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) G[3 * c + k] = k == ax ? gn : 0.f;
+    }
+    rot_vjp(qw, qx, qy, qz, G, gq);
+    const float rw = o[3] + 1.0f, rx = o[4], ry = o[5], rz = o[6];
+    const float rn = sqrtf(rw * rw + rx * rx + ry * ry + rz * rz);
+    if (rn >= 1e-12f) {
+      const float dot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
+      go[7] = (gq[0] - qw * dot) / rn;
+      go[8] = (gq[1] - qx * dot) / rn;
+      go[9] = (gq[2] - qy * dot) / rn;
+      go[10] = (gq[3] - qz * dot) / rn;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) go[7 + c] = gq[c] / 1e-12f;
+    }
+    // means = c + offset * l  (each (anchor, slot) appears once per view);
+    // float32 is ample for a gradient (the forward keeps mu in float64)
+    const int a = active[r];
+    float *goff = g_offsets + ((size_t)a * n + sl) * 3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      atomicAdd(goff + c, g_means[3 * g + c] * expf(log_scale[3 * a + c]));
   }
+  __syncthreads();  // the tile is reused for g_o
+  if (ok) {
+    so[sl * sp + ra] = go[0];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const int j = n + 3 * sl + c;
-    const float sg = sigmoidf_(cache_o[(size_t)j * ld + r]);
-    g_o_out[(size_t)j * ld + r] = g_color[3 * g + c] * sg * (1.f - sg);
+    for (int c = 0; c < 3; ++c) so[(n + 3 * sl + c) * sp + ra] = go[1 + c];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) so[(4 * n + 7 * sl + c) * sp + ra] = go[4 + c];
   }
-  const int oo = 4 * n + 7 * sl;
-  float o[7], go[7];
-#pragma unroll
-  for (int c = 0; c < 7; ++c) o[c] = cache_o[(size_t)(oo + c) * ld + r];
-  // scales: clamp(exp(o), 1e-6, max) — gradient passes inside [min, max]
-  float sc[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const float e = expf(o[c]);
-    sc[c] = dscale[3 * g + c];
-    const bool pass = (e >= smin) && (e <= smax);
-    go[c] = pass ? g_scale[3 * g + c] * e : 0.f;
-  }
-  // quaternion: normalised (o[3:7] + (1,0,0,0)); normal = column argmin(s) of R(q)
-  const float qw = dquat[4 * g + 0], qx = dquat[4 * g + 1], qy = dquat[4 * g + 2],
-              qz = dquat[4 * g + 3];
-  float gq[4] = {g_quat[4 * g + 0], g_quat[4 * g + 1], g_quat[4 * g + 2], g_quat[4 * g + 3]};
-  const int ax = argmin3(sc[0], sc[1], sc[2]);
-  float G[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  G[0 + ax] = g_normal[3 * g + 0];
-  G[3 + ax] = g_normal[3 * g + 1];
-  G[6 + ax] = g_normal[3 * g + 2];
-  rot_vjp(qw, qx, qy, qz, G, gq);
-  const float rw = o[3] + 1.0f, rx = o[4], ry = o[5], rz = o[6];
-  const float rn = sqrtf(rw * rw + rx * rx + ry * ry + rz * rz);
-  if (rn >= 1e-12f) {
-    const float dot = qw * gq[0] + qx * gq[1] + qy * gq[2] + qz * gq[3];
-    go[3] = (gq[0] - qw * dot) / rn;
-    go[4] = (gq[1] - qx * dot) / rn;
-    go[5] = (gq[2] - qy * dot) / rn;
-    go[6] = (gq[3] - qz * dot) / rn;
-  } else {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) go[3 + c] = gq[c] / 1e-12f;
-  }
-#pragma unroll
-  for (int c = 0; c < 7; ++c) g_o_out[(size_t)(oo + c) * ld + r] = go[c];
-  // means = c + offset * l  (each (anchor, slot) appears once per view)
-  const int a = active[r];
-  float *goff = g_offsets + ((size_t)a * n + sl) * 3;
-  // float32 is ample for a gradient (the forward keeps mu in float64)
-#pragma unroll
-  for (int c = 0; c < 3; ++c) atomicAdd(goff + c, g_means[3 * g + c] * expf(log_scale[3 * a + c]));
+  __syncthreads();
+  flush_cache_tile(g_o_out, so, ld, r0, na, rows, sp);
 }
 
 // Backward, part 2 (anchor-parallel): g_h = W2_h^T g_o, tanh backward ->
@@ -1150,7 +1174,11 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
   float *g_pre = xs + (size_t)(kInDim + 1) * ld;
   float *g_o = g_pre + (size_t)192 * ld;
   const int64_t ng = (int64_t)n_active * n;
-  decode_bwd_gauss_kernel<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(
+  VSX_REQUIRE(n <= 256, "decode_bwd: n=%d > 256", n);
+  const int ab = 256 / n;
+  const size_t gsm = sizeof(float) * 11 * n * (ab + 1);
+  (void)ng;
+  decode_bwd_gauss_kernel<<<(unsigned)((n_active + ab - 1) / ab), 256, gsm, st>>>(
       n, active, n_active, log_scale, offsets, max_scale, cache_o, scale, quat, g_means,
       g_opacity, g_color, g_scale, g_quat, g_normal, g_offsets, g_o);
   VSX_LAUNCH_CHECK("decode_bwd_gauss");

@@ -266,34 +266,46 @@ __global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
 }
 
 // Per-gaussian activations of the decoded heads (decoder.py:160-180), one
-// thread per gaussian g = r * n + sl (coalesced output rows), reading the raw
-// outputs from the feature-major cache_o written by decode_fwd_tc_kernel.
+// thread per gaussian g = r * n + sl (coalesced output rows). A block owns
+// floor(256 / n) whole anchors and stages their [11n x anchors] slice of the
+// feature-major cache_o through shared memory, so the raw outputs are read as
+// contiguous row runs instead of one scattered 4-byte load per (gaussian, row).
 __global__ void __launch_bounds__(256) decode_gauss_kernel(
     int n, const int32_t *__restrict__ active, int32_t n_active, const double *__restrict__ centers,
     const float *__restrict__ log_scale, const float *__restrict__ offsets, double max_scale,
     const float *__restrict__ cache_o, double *__restrict__ means, float *__restrict__ opacity,
     float *__restrict__ color, float *__restrict__ scale, float *__restrict__ quat,
     float *__restrict__ normal, int32_t *__restrict__ status) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)n_active * n;
+  extern __shared__ float so[];  // [11n][ab + 1]
+  __shared__ double s_ls[3 * 256];  // exp(log_scale) of the block's anchors
+  const int ab = 256 / n, sp = ab + 1;
+  const int r0 = blockIdx.x * ab;
+  const int na = min(ab, n_active - r0);
+  const int rows = 11 * n;
+  const size_t ld = cache_ld(n_active);
+  const int t = threadIdx.x;
+  stage_cache_tile(so, cache_o, ld, r0, na, rows, sp);
+  for (int e = t; e < 3 * na; e += blockDim.x)
+    s_ls[e] = exp((double)log_scale[3 * active[r0 + e / 3] + e % 3]);
+  __syncthreads();
   bool bad = false;
-  if (g < total) {
-    const int r = (int)(g / n), sl = (int)(g % n);
+  if (t < na * n) {
+    const int ra = t / n, sl = t - ra * n;
+    const int r = r0 + ra;
+    const int64_t g = (int64_t)r * n + sl;
     const int a = active[r];
-    const size_t ld = cache_ld(n_active);
-    const float *col = cache_o + r;
-    const float op = sigm(col[(size_t)sl * ld]);
+    const float op = sigm(so[sl * sp + ra]);
     opacity[g] = op;
     bad |= !isfinite(op);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const float v = sigm(col[(size_t)(n + 3 * sl + c) * ld]);
+      const float v = sigm(so[(n + 3 * sl + c) * sp + ra]);
       color[3 * g + c] = v;
       bad |= !isfinite(v);
     }
     float o[7];
 #pragma unroll
-    for (int c = 0; c < 7; ++c) o[c] = col[(size_t)(4 * n + 7 * sl + c) * ld];
+    for (int c = 0; c < 7; ++c) o[c] = so[(4 * n + 7 * sl + c) * sp + ra];
     const float smax = (float)max_scale, smin = (float)kMinScale;
     float sc[3];
 #pragma unroll
@@ -314,13 +326,13 @@ __global__ void __launch_bounds__(256) decode_gauss_kernel(
     float R[9];
     quat_to_rot(qw, qx, qy, qz, R);
     const int ax = argmin3(sc[0], sc[1], sc[2]);
-    normal[3 * g + 0] = R[0 + ax];
-    normal[3 * g + 1] = R[3 + ax];
-    normal[3 * g + 2] = R[6 + ax];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)  // register selects: a dynamic index would spill R
+      normal[3 * g + c] = ax == 0 ? R[3 * c] : (ax == 1 ? R[3 * c + 1] : R[3 * c + 2]);
     const float *off = offsets + ((size_t)a * n + sl) * 3;
-    const double m0 = dadd(centers[3 * a + 0], dmul((double)off[0], exp((double)log_scale[3 * a + 0])));
-    const double m1 = dadd(centers[3 * a + 1], dmul((double)off[1], exp((double)log_scale[3 * a + 1])));
-    const double m2 = dadd(centers[3 * a + 2], dmul((double)off[2], exp((double)log_scale[3 * a + 2])));
+    const double m0 = dadd(centers[3 * a + 0], dmul((double)off[0], s_ls[3 * ra + 0]));
+    const double m1 = dadd(centers[3 * a + 1], dmul((double)off[1], s_ls[3 * ra + 1]));
+    const double m2 = dadd(centers[3 * a + 2], dmul((double)off[2], s_ls[3 * ra + 2]));
     means[3 * g + 0] = m0;
     means[3 * g + 1] = m1;
     means[3 * g + 2] = m2;
@@ -617,7 +629,11 @@ extern "C" int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t 
     VSX_LAUNCH_CHECK("decode_fwd_tc");
   }
   const int64_t total = (int64_t)n_active * W.n;
-  decode_gauss_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(s)>>>(
+  VSX_REQUIRE(W.n <= 256, "decode_fwd: n=%d > 256", W.n);
+  const int ab = 256 / W.n;
+  const size_t gsm = sizeof(float) * 11 * W.n * (ab + 1);
+  (void)total;
+  decode_gauss_kernel<<<(unsigned)((n_active + ab - 1) / ab), 256, gsm, as_stream(s)>>>(
       W.n, active, n_active, centers, log_scale, offsets, max_scale, cache_o, means, opacity, color,
       scale, quat, normal, status);
   VSX_LAUNCH_CHECK("decode_gauss");
