@@ -204,6 +204,24 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
 struct FwdPix {
   float T = 1.f, acc = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f, dist = 0.f;
   int32_t live = 0;
+  // Branch-free live test: a dead pixel (T < 1e-4) blends with alpha 0, which
+  // leaves every accumulator and T bit-identical (all staged values are finite).
+  __device__ __forceinline__ void blend_if_live(float al, const float4 &p2, const float4 &p3,
+                                                float pd) {
+    const bool lv = T >= kEarlyStopT;
+    const float m = lv ? al : 0.f;
+    const float w = m * T;
+    acc += w;
+    c0 = fmaf(w, p2.x, c0);
+    c1 = fmaf(w, p2.y, c1);
+    c2 = fmaf(w, p2.z, c2);
+    n0 = fmaf(w, p3.x, n0);
+    n1 = fmaf(w, p3.y, n1);
+    n2 = fmaf(w, p3.z, n2);
+    dist = fmaf(w, pd, dist);
+    T = __fmaf_rn(-m, T, T);
+    live += lv ? 1 : 0;
+  }
   __device__ __forceinline__ void blend(float al, const float4 &p2, const float4 &p3, float pd) {
     const float w = al * T;
     acc += w;
@@ -226,30 +244,50 @@ __device__ __forceinline__ float falloff_alpha(const float4 &p0, const float4 &p
   return fminf(__fmul_rn(p1.y, ex2_ftz(fminf(p2, 0.f))), 0.99f);
 }
 
-__global__ void __launch_bounds__(128) raster_fwd2_kernel(
+template <int PX, int U>
+__global__ void __launch_bounds__(256 / PX) raster_fwd2_kernel(
     const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
     const uint32_t *__restrict__ tile_list, vsx_camera cam, float *__restrict__ out_rgb,
     float *__restrict__ out_alpha, float *__restrict__ out_depth, float *__restrict__ out_normal,
     float *__restrict__ out_raw, uint8_t *__restrict__ out_valid, float *__restrict__ out_T,
     int32_t *__restrict__ out_nc, vsx_loss_desc L) {
+  constexpr int kThreads = 256 / PX, kRowThreads = kTile / PX;
   __shared__ float4 s0[kChunk], s1[kChunk], s2[kChunk], s3[kChunk];
   const int txn = gridDim.x;
   const int tile = blockIdx.y * txn + blockIdx.x;
-  const int lx = 2 * (threadIdx.x & 7), ly = threadIdx.x >> 3;
+  const int lx = PX * (threadIdx.x % kRowThreads), ly = threadIdx.x / kRowThreads;
   const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
-  const bool inA = px < cam.width && py < cam.height;
-  const bool inB = px + 1 < cam.width && py < cam.height;
   const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
   const uint32_t begin = tile_off[tile], end = tile_off[tile + 1];
-  const float fxA = (float)lx, fxB = (float)(lx + 1), fy = (float)ly;
-  FwdPix A, B;
-  int32_t ncA = 0, ncB = 0;
-  bool doneA = !inA, doneB = !inB;
-  for (uint32_t cs = begin; cs < end; cs += kChunk) {
-    if (__syncthreads_count(!(doneA && doneB)) == 0) break;
+  const float fy = (float)ly;
+  float fx[PX];
+  bool in[PX], done[PX];
+  int32_t nc[PX];
+  FwdPix A[PX];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = threadIdx.x + 128 * h;
+  for (int i = 0; i < PX; ++i) {
+    fx[i] = (float)(lx + i);
+    in[i] = px + i < cam.width && py < cam.height;
+    done[i] = !in[i];
+    nc[i] = 0;
+  }
+  auto all_done = [&] {
+    bool d = true;
+#pragma unroll
+    for (int i = 0; i < PX; ++i) d = d && done[i];
+    return d;
+  };
+  auto any_live = [&] {
+    bool l = false;
+#pragma unroll
+    for (int i = 0; i < PX; ++i) l = l || A[i].T >= kEarlyStopT;
+    return l;
+  };
+  for (uint32_t cs = begin; cs < end; cs += kChunk) {
+    if (__syncthreads_count(!all_done()) == 0) break;
+#pragma unroll
+    for (int h = 0; h < PX; ++h) {
+      const int k = threadIdx.x + kThreads * h;
       const uint32_t idx = cs + k;
       if (idx < end) {
         const vsx_splat sp = load_splat(rec, tile_list[idx]);
@@ -258,53 +296,56 @@ __global__ void __launch_bounds__(128) raster_fwd2_kernel(
     }
     __syncthreads();
     const int cnt = (int)min((uint32_t)kChunk, end - cs);
-    if (!(doneA && doneB)) {
-      A.live = 0;
-      B.live = 0;
-      // T only decreases, so each pixel's "live" splats are a prefix of the chunk
-      int j = 0;
-      for (; j + 2 <= cnt && (A.T >= kEarlyStopT || B.T >= kEarlyStopT); j += 2) {
-        float aA[2], aB[2];
+    if (!all_done()) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+      for (int i = 0; i < PX; ++i) A[i].live = 0;
+      // T only decreases, so each pixel's "live" splats are a prefix of the chunk
+      // batches of U splats: all U * PX alphas first (independent), then the
+      // sequential blends
+      int j = 0;
+      for (; j + U <= cnt && any_live(); j += U) {
+        float al[U][PX];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
           const float4 p0 = s0[j + u], p1 = s1[j + u];
           const float dy = fy - p0.y;
           const float cy = __fmul_rn(p0.w, dy), cyy = __fmul_rn(__fmul_rn(p1.x, dy), dy);
-          aA[u] = falloff_alpha(p0, p1, fxA - p0.x, cy, cyy);
-          aB[u] = falloff_alpha(p0, p1, fxB - p0.x, cy, cyy);
+#pragma unroll
+          for (int i = 0; i < PX; ++i) al[u][i] = falloff_alpha(p0, p1, fx[i] - p0.x, cy, cyy);
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
           const float4 p2 = s2[j + u], p3 = s3[j + u];
           const float pd = s1[j + u].z;
-          if (A.T >= kEarlyStopT) A.blend(aA[u], p2, p3, pd);
-          if (B.T >= kEarlyStopT) B.blend(aB[u], p2, p3, pd);
+#pragma unroll
+          for (int i = 0; i < PX; ++i) A[i].blend_if_live(al[u][i], p2, p3, pd);
         }
       }
-      for (; j < cnt && (A.T >= kEarlyStopT || B.T >= kEarlyStopT); ++j) {
+      for (; j < cnt && any_live(); ++j) {
         const float4 p0 = s0[j], p1 = s1[j];
         const float dy = fy - p0.y;
         const float cy = __fmul_rn(p0.w, dy), cyy = __fmul_rn(__fmul_rn(p1.x, dy), dy);
-        const float aA = falloff_alpha(p0, p1, fxA - p0.x, cy, cyy);
-        const float aB = falloff_alpha(p0, p1, fxB - p0.x, cy, cyy);
+        float al[PX];
+#pragma unroll
+        for (int i = 0; i < PX; ++i) al[i] = falloff_alpha(p0, p1, fx[i] - p0.x, cy, cyy);
         const float4 p2 = s2[j], p3 = s3[j];
-        if (A.T >= kEarlyStopT) A.blend(aA, p2, p3, p1.z);
-        if (B.T >= kEarlyStopT) B.blend(aB, p2, p3, p1.z);
+#pragma unroll
+        for (int i = 0; i < PX; ++i)
+          if (A[i].T >= kEarlyStopT) A[i].blend(al[i], p2, p3, p1.z);
       }
-      if (!doneA) {
-        ncA = (int32_t)(cs - begin) + A.live;
-        doneA = A.T < kEarlyStopT;
-      }
-      if (!doneB) {
-        ncB = (int32_t)(cs - begin) + B.live;
-        doneB = B.T < kEarlyStopT;
-      }
+#pragma unroll
+      for (int i = 0; i < PX; ++i)
+        if (!done[i]) {
+          nc[i] = (int32_t)(cs - begin) + A[i].live;
+          done[i] = A[i].T < kEarlyStopT;
+        }
     }
   }
-  fwd_epilogue(cam, inA, px, py, A.acc, A.c0, A.c1, A.c2, A.n0, A.n1, A.n2, A.dist, A.T, ncA,
-               out_rgb, out_alpha, out_depth, out_normal, out_raw, out_valid, out_T, out_nc, L);
-  fwd_epilogue(cam, inB, px + 1, py, B.acc, B.c0, B.c1, B.c2, B.n0, B.n1, B.n2, B.dist, B.T, ncB,
-               out_rgb, out_alpha, out_depth, out_normal, out_raw, out_valid, out_T, out_nc, L);
+#pragma unroll
+  for (int i = 0; i < PX; ++i)
+    fwd_epilogue(cam, in[i], px + i, py, A[i].acc, A[i].c0, A[i].c1, A[i].c2, A[i].n0, A[i].n1,
+                 A[i].n2, A[i].dist, A[i].T, nc[i], out_rgb, out_alpha, out_depth, out_normal,
+                 out_raw, out_valid, out_T, out_nc, L);
 }
 
 __device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (&a)[4],
@@ -1014,10 +1055,16 @@ static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
     const char *e = getenv("VSX_RASTER_FWD");
     return e && e[0] == 't';
   }();
-  static const bool px1 = [] {  // VSX_RASTER_FWD=1: one pixel per thread (A/B)
+  // VSX_RASTER_FWD=1|2|4: pixels per thread (A/B)
+  static const int fwd_px = [] {
     const char *e = getenv("VSX_RASTER_FWD");
-    return e && e[0] == '1';
+    return (e && (e[0] == '1' || e[0] == '4')) ? e[0] - '0' : 2;
   }();
+  static const int fwd_u = [] {  // second digit: splats per alpha batch
+    const char *e = getenv("VSX_RASTER_FWD");
+    return (e && e[0] && e[1] >= '1' && e[1] <= '8') ? e[1] - '0' : 4;
+  }();
+  const bool px1 = fwd_px == 1;
   if (tc) {
     const int smem = (int)(sizeof(float) * 8 * kFwPlane);
     static bool attr = false;
@@ -1033,9 +1080,23 @@ static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
   else if (px1)
     raster_fwd_kernel<<<grid, 256, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha, depth,
                                             normal, raw_normal, valid, t_final, n_contrib, L);
-  else
-    raster_fwd2_kernel<<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha, depth,
-                                             normal, raw_normal, valid, t_final, n_contrib, L);
+  else {
+#define VSX_FWD2(P, U)                                                                        \
+  raster_fwd2_kernel<P, U><<<grid, 256 / P, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha, \
+                                                     depth, normal, raw_normal, valid, t_final,  \
+                                                     n_contrib, L)
+    switch (fwd_px * 10 + fwd_u) {
+      case 21: VSX_FWD2(2, 1); break;
+      case 24: VSX_FWD2(2, 4); break;
+      case 26: VSX_FWD2(2, 6); break;
+      case 28: VSX_FWD2(2, 8); break;
+      case 41: VSX_FWD2(4, 1); break;
+      case 42: VSX_FWD2(4, 2); break;
+      case 22: VSX_FWD2(2, 2); break;
+      default: VSX_FWD2(2, 4); break;
+    }
+#undef VSX_FWD2
+  }
   VSX_LAUNCH_CHECK("raster_fwd");
   return VSX_OK;
 }
