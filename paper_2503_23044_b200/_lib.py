@@ -14,7 +14,9 @@ from pathlib import Path
 from .errors import raise_for_status
 from .geometry import VsxCamera
 
-LIB_PATH = Path(__file__).resolve().parent / "libvsx_b200.so"
+# VSX_LIB points at an alternative build of the same library (A/B timing of
+# compile-time variants, scripts/ab_build.sh); the default is the in-tree one.
+LIB_PATH = Path(os.environ.get("VSX_LIB") or Path(__file__).resolve().parent / "libvsx_b200.so")
 
 c_void_p = ctypes.c_void_p
 c_i32 = ctypes.c_int32
