@@ -33,6 +33,11 @@ from pathlib import Path
 
 import numpy as np
 
+# Expandable segments (set before torch initialises CUDA): the per-step
+# buffers vary in size with each view's intersection count, and with fixed
+# segments the cache kept growing (cudaMalloc) several steps past warm-up.
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
 ROOT = Path(__file__).resolve().parent
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
@@ -45,8 +50,8 @@ CFG2_LOD_BIAS = 2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["vsx", "reference"], default="vsx")
     ap.add_argument("--config", choices=["cfg2", "cfg1"], default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -142,13 +147,16 @@ class NvmlClockSampler:
             self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
         self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
         self.rows: list[tuple[float, int]] = []
+        self.cost: list[float] = []
         self.ev = threading.Event()
         self.th = threading.Thread(target=self._run, daemon=True)
 
     def _sample(self):
         nv = self.nv
+        t = time.perf_counter()
         self.rows.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
                           int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+        self.cost.append(time.perf_counter() - t)
 
     def _run(self):
         while True:
@@ -166,10 +174,21 @@ class NvmlClockSampler:
         sm = [r[0] for r in self.rows]
         reasons = sorted({n for _, bits in self.rows for n, b in self.REASONS if bits & b})
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.rows), "src": "nvml"}
+                "samples": len(self.rows), "src": "nvml",
+                "max_query_ms": round(1e3 * max(self.cost), 2)}
+
+
+class _NoClocks:
+    def start(self):
+        pass
+
+    def stop(self) -> dict:
+        return {"src": "disabled (VSX_NO_CLOCKS=1)"}
 
 
 def clock_sampler(gpu: int):
+    if os.environ.get("VSX_NO_CLOCKS") == "1":
+        return _NoClocks()
     try:
         return NvmlClockSampler(gpu)
     except Exception:
@@ -351,23 +370,61 @@ def run_vsx(args):
                     "rgb": r.rgb, "depth": r.depth, "normal": r.normal,
                     "live_pairs": r.live_pairs}
     clocks = clock_sampler(local)
-    for _ in range(args.warmup):
-        step(imgs, priors, nprior)
+    # warm-up runs the timed loop's exact code path (stage timer included):
+    # on a fresh box the first touch of a code page or a lazily loaded kernel
+    # module costs tens of ms, which must not land in the timed region
+    for i in range(args.warmup):
+        if i == args.warmup - 2:
+            clocks.start()
+        step(imgs, priors, nprior, GpuTimer())
+    torch.cuda.synchronize()
+    # head-room in the cache so a view with more intersections than any
+    # warm-up view does not map new device memory inside the timed region
+    _pad = torch.empty(int(0.25 * torch.cuda.memory_reserved()) + (256 << 20),
+                       dtype=torch.uint8, device="cuda")
+    del _pad
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks.start()
+    if args.warmup < 2:
+        clocks.start()
     timer = GpuTimer()
     launches0 = lib.vsx_launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    diag = os.environ.get("VSX_BENCH_DIAG") == "1"
+    if diag:
+        import gc
+        gc0 = [g["collections"] for g in gc.get_stats()]
+        m0 = torch.cuda.memory_stats()
     ev0.record()
     reps = []
+    marks = []
+    from paper_2503_23044_b200 import trainer as _trainer
+    tr_marks = []
     for _ in range(args.steps):
+        tr_marks.append(len(_trainer.TRACE_LOG))
         reps.append(step(imgs, priors, nprior, timer))
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        marks.append(e)
+    tr_marks.append(len(_trainer.TRACE_LOG))
     ev1.record()
     torch.cuda.synchronize()
+    if diag:
+        m1 = torch.cuda.memory_stats()
+        keys = ("num_device_alloc", "num_device_free", "num_alloc_retries", "num_sync_all_streams")
+        print("diag alloc", {k: m1.get(k, 0) - m0.get(k, 0) for k in keys},
+              "gc", [g["collections"] - c for g, c in zip(gc.get_stats(), gc0)],
+              "reserved GB", m1["reserved_bytes.all.current"] / 1e9, file=sys.stderr)
+    step_ms = [round(ev0.elapsed_time(marks[0]), 2)] + [
+        round(a.elapsed_time(b), 2) for a, b in zip(marks, marks[1:])]
+    if _trainer.TRACE_LOG:  # VSX_TRACE=1: host phase gaps of the slowest step
+        k = int(np.argmax(step_ms))
+        seg = _trainer.TRACE_LOG[tr_marks[k]:tr_marks[k + 1]]
+        print("trace step", k, step_ms[k], [(b[0], round(1e3 * (b[1] - a[1]), 2))
+                                           for a, b in zip(seg, seg[1:])], file=sys.stderr)
     clk = clocks.stop()
     launches = lib.vsx_launch_count() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -446,6 +503,7 @@ def run_vsx(args):
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk,
         "stages_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
+        "step_ms": step_ms,
         "per_step": {"gaussians": reps[-1]["gaussians"],
                      "intersections": reps[-1]["intersections"],
                      "live_pairs": reps[-1].get("live_pairs"),

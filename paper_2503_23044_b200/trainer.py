@@ -22,6 +22,7 @@ from types import SimpleNamespace
 import ctypes
 import json
 import time
+import os
 from dataclasses import dataclass, fields
 
 import numpy as np
@@ -409,6 +410,14 @@ def _mask_u8(v, shape) -> torch.Tensor:
 
 _COPY_STREAM = None
 _FRONT_STREAM = None
+# VSX_TRACE=1: host timestamps of the step's phases (diagnosing host stalls)
+_TRACE = os.environ.get("VSX_TRACE") == "1"
+TRACE_LOG: list = []
+
+
+def _tr(label):
+    if _TRACE:
+        TRACE_LOG.append((label, time.perf_counter()))
 
 
 def _front_stream() -> torch.cuda.Stream:
@@ -532,6 +541,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
 
     def front(vi):
         view = views[vi]
+        _tr(f"front{vi}")
         with torch.cuda.stream(fs):
             with _span(timer, "cull"):
                 active = ds.active(view)
@@ -548,6 +558,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             ev = torch.cuda.Event()
             ev.record(fs)
         fronts[vi] = (active, dec, P, Bn, ev)
+        _tr(f"front{vi}_done")
 
     def loss_desc(vi, extra=None):
         view = views[vi]
@@ -609,10 +620,12 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             # fused objective (K9 inside K5/K6): loss sums in the forward
             # epilogue, cotangents formed on the fly in the backward
             loss = loss_desc(vi)
+            _tr(f"raster{vi}")
             with _span(timer, "raster_fwd"):
                 R = D.raster_forward(P, Bn, views[vi], loss=loss)
             live += R.n_contrib.sum()
             backward(vi, active, dec, P, Bn, R, loss)
+            _tr(f"bwd{vi}_queued")
             # the next view's front end is issued after this view's back end
             # is queued, so it overlaps it on the GPU
             if vi + 1 < B:
@@ -661,7 +674,9 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         cnt = nrm_cnt.double()
         terms = torch.where(cnt > 0, nrm_sum / (3.0 * cnt.clamp_min(1)), torch.zeros_like(cnt))
         vals[4] = terms[have_n].mean()
+    _tr("read")
     host = torch.stack(vals).cpu().numpy()
+    _tr("read_done")
     state._inflight = None  # the previous step's buffers are idle now
     st_bits, rgb, depth, supervised, normal = int(host[0]), float(host[1]), float(host[2]), \
         int(host[3]), float(host[4])
@@ -672,6 +687,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         raise NumericalError(f"non-finite loss at step {state.step}: rgb={rgb:.4g} depth={depth:.4g}")
     with _span(timer, "adam"):
         state.adam()
+    _tr("adam_queued")
     # per-view buffers stay referenced until the next step's sync point (the
     # GPU may still be running Adam and this step's last kernels)
     state._inflight = hold
