@@ -307,6 +307,13 @@ int vsx_masked_l1(const float *x, const uint8_t *valid, const float *prior,
 int vsx_adam(float *param, const float *grad, float *m, float *v, int32_t n_seg,
              const int64_t *seg_begin, const double *lr, double beta1, double beta2, double eps,
              int32_t step, vsx_stream s);
+/* Same update, skipped on the device when *guard (device int32) is nonzero:
+ * the trainer queues it before its single host read, with guard = status bits
+ * | non-finite loss, so the non-finite check still precedes the update
+ * (trainer.py:317-321) without a host round trip in front of Adam. */
+int vsx_adam_guarded(float *param, const float *grad, float *m, float *v, int32_t n_seg,
+                     const int64_t *seg_begin, const double *lr, double beta1, double beta2,
+                     double eps, int32_t step, const int32_t *guard, vsx_stream s);
 
 /* ---- f1: depth-prior precompute (depth_prior.py:85-214) ------------------ */
 /* float64 device maps (H, W) row-major with uint8 validity. Replaces the

@@ -101,7 +101,9 @@ __global__ void __launch_bounds__(256) adam_kernel(float *__restrict__ p,
                                                    const float *__restrict__ g,
                                                    float *__restrict__ m, float *__restrict__ v,
                                                    AdamSegs segs, double b1, double b2, double eps,
-                                                   double bc1, double bc2) {
+                                                   double bc1, double bc2,
+                                                   const int32_t *__restrict__ guard) {
+  if (guard && *guard) return;  // non-finite step: parameters and moments untouched
   const int64_t total = segs.begin[segs.n];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -161,9 +163,9 @@ extern "C" int vsx_masked_l1(const float *x, const uint8_t *valid, const float *
   return VSX_OK;
 }
 
-extern "C" int vsx_adam(float *param, const float *grad, float *m, float *v, int32_t n_seg,
-                        const int64_t *seg_begin, const double *lr, double beta1, double beta2,
-                        double eps, int32_t step, vsx_stream s) {
+static int adam_impl(float *param, const float *grad, float *m, float *v, int32_t n_seg,
+                     const int64_t *seg_begin, const double *lr, double beta1, double beta2,
+                     double eps, int32_t step, const int32_t *guard, vsx_stream s) {
   VSX_REQUIRE(n_seg >= 1 && n_seg <= kMaxSeg, "adam: 1..16 segments");
   AdamSegs segs{};
   segs.n = n_seg;
@@ -177,7 +179,21 @@ extern "C" int vsx_adam(float *param, const float *grad, float *m, float *v, int
   const int t = step + 1;
   const double bc1 = 1.0 - pow(beta1, (double)t), bc2 = 1.0 - pow(beta2, (double)t);
   adam_kernel<<<persistent_grid(total), 256, 0, as_stream(s)>>>(param, grad, m, v, segs, beta1,
-                                                                beta2, eps, bc1, bc2);
+                                                                beta2, eps, bc1, bc2, guard);
   VSX_LAUNCH_CHECK("adam");
   return VSX_OK;
+}
+
+extern "C" int vsx_adam(float *param, const float *grad, float *m, float *v, int32_t n_seg,
+                        const int64_t *seg_begin, const double *lr, double beta1, double beta2,
+                        double eps, int32_t step, vsx_stream s) {
+  return adam_impl(param, grad, m, v, n_seg, seg_begin, lr, beta1, beta2, eps, step, nullptr, s);
+}
+
+extern "C" int vsx_adam_guarded(float *param, const float *grad, float *m, float *v,
+                                int32_t n_seg, const int64_t *seg_begin, const double *lr,
+                                double beta1, double beta2, double eps, int32_t step,
+                                const int32_t *guard, vsx_stream s) {
+  VSX_REQUIRE(guard, "adam_guarded: guard is required");
+  return adam_impl(param, grad, m, v, n_seg, seg_begin, lr, beta1, beta2, eps, step, guard, s);
 }

@@ -317,14 +317,20 @@ class TrainState:
                 "log_scales": cosine_lr(self.step, c.lr_scales, c),
                 "offsets": cosine_lr(self.step, c.lr_offsets, c)}
 
-    def adam(self) -> None:
-        """One fused Adam launch over every parameter group (K10)."""
+    def adam(self, guard: torch.Tensor | None = None) -> None:
+        """One fused Adam launch over every parameter group (K10); with a
+        device int32 ``guard`` the update is skipped on the device when it is
+        nonzero."""
         begins, order = self.flat.segments(["dec", "emb", "log_scales", "offsets"])
         lrs = self.lrs()
         nseg = len(order)
         seg = (ctypes.c_int64 * (nseg + 1))(*begins)
         lr = (ctypes.c_double * nseg)(*[lrs[g] for g in order])
         f = self.flat
+        if guard is not None:
+            call("vsx_adam_guarded", ptr(f.param), ptr(f.grad), ptr(f.m), ptr(f.v), nseg, seg,
+                 lr, self.cfg.beta1, self.cfg.beta2, ADAM_EPS, self.step, ptr(guard), stream())
+            return
         call("vsx_adam", ptr(f.param), ptr(f.grad), ptr(f.m), ptr(f.v), nseg, seg, lr,
              self.cfg.beta1, self.cfg.beta2, ADAM_EPS, self.step, stream())
 
@@ -674,8 +680,17 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
         cnt = nrm_cnt.double()
         terms = torch.where(cnt > 0, nrm_sum / (3.0 * cnt.clamp_min(1)), torch.zeros_like(cnt))
         vals[4] = terms[have_n].mean()
+    # the non-finite check precedes the update (trainer.py:317-321): Adam is
+    # queued before the host read and skips itself on the device when the
+    # status bits or the loss are bad, so no host round trip sits in front of
+    # it; the host then raises with the parameters untouched
+    vt = torch.stack(vals)
+    total_dev = vt[1] + w2 * vt[2] + wn * vt[4] + w3 * geo_val
+    guard = ((vt[0] != 0) | ~torch.isfinite(total_dev)).to(torch.int32)
+    with _span(timer, "adam"):
+        state.adam(guard)
     _tr("read")
-    host = torch.stack(vals).cpu().numpy()
+    host = vt.cpu().numpy()
     _tr("read_done")
     state._inflight = None  # the previous step's buffers are idle now
     st_bits, rgb, depth, supervised, normal = int(host[0]), float(host[1]), float(host[2]), \
@@ -685,9 +700,6 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     total = rgb + w2 * depth + wn * normal + w3 * geo_val
     if not np.isfinite(total):
         raise NumericalError(f"non-finite loss at step {state.step}: rgb={rgb:.4g} depth={depth:.4g}")
-    with _span(timer, "adam"):
-        state.adam()
-    _tr("adam_queued")
     # per-view buffers stay referenced until the next step's sync point (the
     # GPU may still be running Adam and this step's last kernels)
     state._inflight = hold

@@ -460,3 +460,31 @@ def test_train_step_with_empty_and_ragged_views_matches_oracle(train_small):
         ov = oval.detach().numpy()
         ok, worst, nbad = rel_close(got, ov, 1e-3, 1e-6)
         assert nbad / ov.size <= 2e-3, f"{name}: {nbad}/{ov.size} off, worst {worst:.3g}"
+
+
+@pytest.mark.parametrize("poison", ["image", "weight"])
+def test_non_finite_step_raises_and_leaves_parameters(train_small, poison):
+    """A non-finite loss (NaN target pixel) or decoder output (NaN weight)
+    raises NumericalError before any parameter moves (trainer.py:317-321):
+    the device-guarded Adam must skip the update it was queued for."""
+    from paper_2503_23044_b200.errors import NumericalError
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step
+    d = train_small
+    scene = golden_scene(d)
+    views = [golden_view(d, f"v{i}", i) for i in range(3)]
+    images = [np.array(d[f"img{i}"], dtype=np.float32) for i in range(3)]
+    state = TrainState(scene, TrainConfig(total_steps=8, batch_size=3, step2_start=8,
+                                          step3_start=8, growth_stop=0))
+    train_step(state, views, images)  # one clean step: moments are non-zero
+    if poison == "image":
+        images[1][3, 4, 0] = np.nan
+    else:
+        state.flat.view(state.flat.param, "dec/opacity_w1")[0, 0] = float("nan")
+    before = [t.clone() for t in (state.flat.param, state.flat.m, state.flat.v)]
+    step0 = state.step
+    with pytest.raises(NumericalError):
+        train_step(state, views, images)
+    torch.cuda.synchronize()
+    for a, b in zip(before, (state.flat.param, state.flat.m, state.flat.v)):
+        assert torch.equal(a.nan_to_num(), b.nan_to_num())
+    assert state.step == step0
