@@ -918,15 +918,10 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
       // chains overlap instead of serialising on one accumulator
       float d[4] = {0.f, 0.f, 0.f, 0.f}, e1[4] = {0.f, 0.f, 0.f, 0.f},
             e2[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-      for (int kk = 0; kk < kKS; ++kk) {
-        float (&D0)[4] = d;
-        float (&D1)[4] = e1;
-        float (&D2)[4] = e2;
-        const int ks = kr * kKS + kk;
+      // A fragment of k-step ks split hi/lo (3xTF32)
+      auto a_frag = [&](int ks, uint32_t (&hi)[4], uint32_t (&lo)[4]) {
         const float x0 = A[8 * ks], x1 = A[8 * kPlaneStride + 8 * ks], x2 = A[8 * ks + 4],
                     x3 = A[8 * kPlaneStride + 8 * ks + 4];
-        uint32_t hi[4], lo[4];
         hi[0] = tf32_bits(x0);
         hi[1] = tf32_bits(x1);
         hi[2] = tf32_bits(x2);
@@ -935,15 +930,28 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
         lo[1] = tf32_bits(x1 - __uint_as_float(hi[1]));
         lo[2] = tf32_bits(x2 - __uint_as_float(hi[2]));
         lo[3] = tf32_bits(x3 - __uint_as_float(hi[3]));
-        if (plane == 0) {
+      };
+      // warp-uniform plane branch outside the k loop: no predicated HMMAs
+      if (plane == 0) {
+#pragma unroll 4
+        for (int kk = 0; kk < kKS; ++kk) {
+          const int ks = kr * kKS + kk;
+          uint32_t hi[4], lo[4];
+          a_frag(ks, hi, lo);
           const float4 b = s_bw[ks][lane];
-          mma_m16n8k8_tf32(D1, lo, __float_as_uint(b.x), __float_as_uint(b.y));
-          mma_m16n8k8_tf32(D2, hi, __float_as_uint(b.z), __float_as_uint(b.w));
-          mma_m16n8k8_tf32(D0, hi, __float_as_uint(b.x), __float_as_uint(b.y));
-        } else {
+          mma_m16n8k8_tf32(e1, lo, __float_as_uint(b.x), __float_as_uint(b.y));
+          mma_m16n8k8_tf32(e2, hi, __float_as_uint(b.z), __float_as_uint(b.w));
+          mma_m16n8k8_tf32(d, hi, __float_as_uint(b.x), __float_as_uint(b.y));
+        }
+      } else {
+#pragma unroll 4
+        for (int kk = 0; kk < kKS; ++kk) {
+          const int ks = kr * kKS + kk;
+          uint32_t hi[4], lo[4];
+          a_frag(ks, hi, lo);
           const float2 b = s_bq[ks][lane];
-          mma_m16n8k8_tf32(D1, lo, __float_as_uint(b.x), __float_as_uint(b.y));
-          mma_m16n8k8_tf32(D0, hi, __float_as_uint(b.x), __float_as_uint(b.y));
+          mma_m16n8k8_tf32(e1, lo, __float_as_uint(b.x), __float_as_uint(b.y));
+          mma_m16n8k8_tf32(d, hi, __float_as_uint(b.x), __float_as_uint(b.y));
         }
       }
 #pragma unroll
