@@ -378,12 +378,11 @@ def run_vsx(args):
             clocks.start()
         step(imgs, priors, nprior, GpuTimer())
     torch.cuda.synchronize()
-    # head-room in the cache so a view with more intersections than any
-    # warm-up view does not map new device memory inside the timed region
-    _pad = torch.empty(int(0.25 * torch.cuda.memory_reserved()) + (256 << 20),
-                       dtype=torch.uint8, device="cuda")
-    del _pad
-    torch.cuda.synchronize()
+    # head-room in every stream's cache pool so a view with more
+    # intersections than any warm-up view does not map new device memory
+    # inside the timed region
+    from paper_2503_23044_b200.trainer import reserve_stream_pools
+    reserve_stream_pools(1 << 30)
     if world > 1:
         dist.barrier()
     if args.warmup < 2:
@@ -456,8 +455,9 @@ def run_vsx(args):
             h2d += sum(d.numel() * 4 + v.numel() for d, v in hpri)
         if hnrm:
             h2d += sum(nn.numel() * 4 + v.numel() for nn, v in hnrm)
-        step(himgs, hpri, hnrm)
-        torch.cuda.synchronize()
+        for _ in range(2):  # host-input path: its H2D staging buffers join the pools
+            step(himgs, hpri, hnrm)
+        reserve_stream_pools(1 << 30)
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)

@@ -421,6 +421,26 @@ _TRACE = os.environ.get("VSX_TRACE") == "1"
 TRACE_LOG: list = []
 
 
+def reserve_stream_pools(nbytes: int) -> None:
+    """Grow the caching allocator's pool of every pipeline stream by nbytes.
+
+    Blocks are cached per stream, so head-room reserved on one stream does
+    not serve another. Mapping new device memory inside a step can stall the
+    host for as long as the queued GPU work (tens of ms); a long-running
+    trainer (or a benchmark) calls this once after warm-up."""
+    cur = torch.cuda.current_stream()
+    streams = [cur]
+    if _pipeline_enabled():
+        streams += [_front_stream(), _tail_stream()]
+    if _COPY_STREAM is not None:
+        streams.append(_COPY_STREAM)
+    for st in streams:
+        with torch.cuda.stream(st):
+            pad = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+            del pad
+    torch.cuda.synchronize()
+
+
 def _tr(label):
     if _TRACE:
         TRACE_LOG.append((label, time.perf_counter()))
