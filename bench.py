@@ -58,8 +58,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU sharded step even at one rank (testing)")
-    ap.add_argument("--cpu-tiles", type=int, default=400,
-                    help="tiles per CPU-baseline sample (evenly spaced over the view)")
+    ap.add_argument("--cpu-tiles", type=int, default=2000,
+                    help="tiles composited in the cpu_baseline sample (evenly spaced over "
+                         "the view; ~10 s of host work at cfg2)")
+    ap.add_argument("--ref-tiles", type=int, default=300,
+                    help="tiles per --impl reference step (each of the W+K steps is one "
+                         "such sample, so the arm ends within a few minutes)")
     return ap.parse_args()
 
 
@@ -294,7 +298,7 @@ def run_reference(args):
     if args.config == "cfg1":
         tiles = None
     else:
-        tiles = args.cpu_tiles
+        tiles = args.ref_tiles
     vals = []
     for i in range(args.warmup + args.steps):
         s = cpu_sample(scene, views, tiles if tiles else 10**9, images)
