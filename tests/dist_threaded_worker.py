@@ -1,0 +1,100 @@
+"""Two ranks of the sharded CUDA step on ONE GPU, as two threads of one
+process over torch's in-process "threaded" process group.
+
+The collectives (all-to-all of splat records, reverse all-to-all of the 2D
+gradients, decoder all-reduce, replica checksum) run on the host between the
+threads, so no kernel ever waits on another rank's kernel (the pattern the
+B200 profiling guide forbids on one GPU). Compares both ranks' losses and the
+owner-merged parameters with the single-process ``train_step``. Prints one
+JSON line; run by tests/test_gpu_dist.py in a subprocess (it swaps the
+process-wide distributed world).
+"""
+import json
+import sys
+import threading
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+from torch.testing._internal.distributed.multi_threaded_pg import _install_threaded_pg
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent))
+sys.path.insert(0, str(HERE))
+from conftest import golden_scene, golden_view, load_golden  # noqa: E402
+
+from paper_2503_23044_b200.dist import CudaShardBackend, sharded_train_step  # noqa: E402
+from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step  # noqa: E402
+
+WORLD = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+STEPS = 2
+d = load_golden("train_small")
+views = [golden_view(d, f"v{i}", i) for i in range(3)]
+images = [d[f"img{i}"] for i in range(3)]
+priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
+cfg = dict(total_steps=8, batch_size=3, step2_start=0, step3_start=8, growth_stop=0)
+
+import faulthandler  # noqa: E402
+faulthandler.dump_traceback_later(150, exit=True)  # a hang prints every thread's stack
+torch.cuda.init()
+torch._C._distributed_c10d._set_thread_isolation_mode(True)  # per-thread group registry
+_install_threaded_pg()
+store = dist.HashStore()
+res, errs = {}, []
+
+
+def run(rank):
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("threaded", rank=rank, world_size=WORLD, store=store)
+        # one stream per rank, as one process per GPU would have: the sort /
+        # scan scratch buffers are keyed by stream
+        with torch.cuda.stream(torch.cuda.Stream()):
+            st = TrainState(golden_scene(d), TrainConfig(**cfg, workers=WORLD))
+            be = CudaShardBackend(st, rank, WORLD)
+            reps = [sharded_train_step(be, views, images, priors) for _ in range(STEPS)]
+            torch.cuda.synchronize()
+        res[rank] = dict(reps=reps, state=st)
+    except Exception as e:  # surfaced in the JSON line
+        import traceback
+        errs.append(f"rank {rank}: {e!r}\n{traceback.format_exc()}")
+        print(errs[-1], file=sys.stderr, flush=True)
+        import os
+        os._exit(3)  # the other rank would wait in its next collective forever
+
+
+threads = [threading.Thread(target=run, args=(r,)) for r in range(WORLD)]
+for t in threads:
+    t.start()
+for t in threads:
+    t.join()
+if errs:
+    print(json.dumps({"ok": False, "errors": errs}))
+    sys.exit(0)
+
+faulthandler.cancel_dump_traceback_later()
+ref = TrainState(golden_scene(d), TrainConfig(**cfg))
+ref_reps = [train_step(ref, views, images, priors) for _ in range(STEPS)]
+out = {"ok": True, "loss": [], "param_bad_frac": {}, "owned_disjoint": None}
+for s in range(STEPS):
+    for r in range(WORLD):
+        rb = res[r]["reps"][s]
+        out["loss"].append([s, r, rb["rgb"], ref_reps[s].rgb, rb["depth"], ref_reps[s].depth])
+owner = res[0]["state"].assignment.flat_owner()
+out["owned_disjoint"] = bool(np.array_equal(np.bincount(owner, minlength=WORLD) > 0,
+                                            np.ones(WORLD, bool)))
+for name in ["emb", "log_scales", "offsets"]:
+    want = ref.flat.view(ref.flat.param, name).cpu().numpy()
+    got = np.empty_like(want)
+    for r in range(WORLD):
+        st = res[r]["state"]
+        g = st.flat.view(st.flat.param, name).cpu().numpy()
+        got[owner == r] = g[owner == r]
+    bad = np.abs(got - want) > 1e-5 * np.maximum(np.abs(got), np.abs(want)) + 1e-7
+    out["param_bad_frac"][name] = float(bad.mean())
+for r in range(WORLD):  # the replicated decoder (anchor rows of other owners are stale)
+    st = res[r]["state"]
+    out[f"dec_checksum_r{r}"] = float(st.flat.view(st.flat.param, "dec/opacity_w1").sum())
+out["dec_checksum_ref"] = float(ref.flat.view(ref.flat.param, "dec/opacity_w1").sum())
+print(json.dumps(out))

@@ -57,3 +57,29 @@ def test_sharded_step_world1_matches_train_step(nccl_world1, train_small):
     pa, pb = a.flat.param.cpu().numpy(), b.flat.param.cpu().numpy()
     bad = np.abs(pa - pb) > 1e-5 * np.maximum(np.abs(pa), np.abs(pb)) + 1e-7
     assert bad.mean() < 1e-3, bad.sum()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_step_threaded_ranks_match_train_step(world):
+    """World size 2 and 4 on one GPU: threads of one process joined by
+    torch's in-process process group (host-side collectives, no cross-rank
+    kernel waits). Losses on every rank and the owner-merged anchor
+    parameters must match the single-process train_step; the replicated
+    decoder too. At world 4 with 3 views one rank renders nothing."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    here = Path(__file__).resolve().parent
+    p = subprocess.run([sys.executable, str(here / "dist_threaded_worker.py"), str(world)],
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    out = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["ok"], "\n".join(out.get("errors", []))[-3000:]
+    for s, r, rgb, ref_rgb, dep, ref_dep in out["loss"]:
+        assert rgb == pytest.approx(ref_rgb, rel=1e-6), (s, r)
+        assert dep == pytest.approx(ref_dep, rel=1e-5), (s, r)
+    for name, frac in out["param_bad_frac"].items():
+        assert frac < 1e-3, (name, frac)
+    for r in range(world):
+        assert out[f"dec_checksum_r{r}"] == pytest.approx(out["dec_checksum_ref"], rel=1e-5)
