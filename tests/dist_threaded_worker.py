@@ -40,6 +40,22 @@ faulthandler.dump_traceback_later(150, exit=True)  # a hang prints every thread'
 torch.cuda.init()
 torch._C._distributed_c10d._set_thread_isolation_mode(True)  # per-thread group registry
 _install_threaded_pg()
+
+
+def _device_synced(fn):
+    """The threaded group reduces on whichever rank thread arrives last, on
+    that thread's stream; a device-wide sync on both sides orders it after
+    every rank's producer kernels (NCCL does this with stream dependencies)."""
+    def call(*a, **k):
+        torch.cuda.synchronize()
+        r = fn(*a, **k)
+        torch.cuda.synchronize()
+        return r
+    return call
+
+
+for _name in ("all_reduce", "all_to_all_single", "all_gather", "broadcast", "barrier"):
+    setattr(dist, _name, _device_synced(getattr(dist, _name)))
 store = dist.HashStore()
 res, errs = {}, []
 
