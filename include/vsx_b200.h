@@ -283,6 +283,12 @@ int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t *active, i
                    const float *g_normal, float *g_emb, float *g_log_scale, float *g_offsets,
                    void *ws, size_t ws_bytes, vsx_stream s);
 
+/* Growth pressure (trainer.py:342-349, f3): grow_sum[active[r]] += sum over
+ * the n gaussians of anchor r of |g_means| (float64), grow_cnt[...] += n.
+ * g_means is the (n_active*n, 3) mean gradient of the decode batch. */
+int vsx_growth_accumulate(const float *g_means, const int32_t *active, int32_t n_active,
+                          int32_t n, double *grow_sum, double *grow_cnt, vsx_stream s);
+
 /* ---- K9: losses --------------------------------------------------------- */
 /* L1: loss_accum[0] += sum|r - g| (float64); grad = sign(r - g) * scale. */
 int vsx_l1_loss(const float *rendered, const float *target, int64_t n, float scale,

@@ -86,6 +86,7 @@ _SIGS = {
     "vsx_l1_loss": ([P, P, c_i64, c_f32, P, P, P], c_i32),
     "vsx_depth_loss": ([P, P, P, P, c_i64, P, P, P, P, P], c_i32),
     "vsx_adam": ([P, P, P, P, c_i32, P, P, c_f64, c_f64, c_f64, c_i32, P], c_i32),
+    "vsx_growth_accumulate": ([P, P, c_i32, c_i32, P, P, P], c_i32),
     "vsx_adam_guarded": ([P, P, P, P, c_i32, P, P, c_f64, c_f64, c_f64, c_i32, P, P], c_i32),
     "vsx_masked_l1": ([P, P, P, P, c_i64, c_i32, P, P, P, P, P], c_i32),
     "vsx_launch_count": ([], ctypes.c_uint64),

@@ -234,6 +234,27 @@ __device__ __forceinline__ void rot_vjp(float w, float x, float y, float z, cons
                   y * G[5] + x * G[6] + y * G[7]);
 }
 
+// Growth pressure (trainer.py:342-349): per active anchor r, the float64 sum
+// of |dL/dmu| over its n gaussians (batch order g = r*n + sl) and n counts,
+// added into the flat per-anchor accumulators. One thread per anchor; an
+// anchor occurs once per view, so the adds do not contend.
+__global__ void growth_accumulate_kernel(const float *__restrict__ g_means,
+                                         const int32_t *__restrict__ active, int32_t n_active,
+                                         int n, double *__restrict__ grow_sum,
+                                         double *__restrict__ grow_cnt) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_active) return;
+  const float *gm = g_means + (size_t)r * n * 3;
+  double acc = 0.0;
+  for (int sl = 0; sl < n; ++sl) {
+    const double x = gm[3 * sl], y = gm[3 * sl + 1], z = gm[3 * sl + 2];
+    acc += sqrt(x * x + y * y + z * z);
+  }
+  const int a = active[r];
+  atomicAdd(grow_sum + a, acc);
+  atomicAdd(grow_cnt + a, (double)n);
+}
+
 // Backward, part 1 (gaussian-parallel): per-gaussian cotangents -> head-output
 // cotangents g_o (feature-major, row = head output column) and the offsets
 // grads. A block owns floor(256 / n) whole anchors (n gaussians each, thread =
@@ -1261,5 +1282,16 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
                       n_active, ld, o2, st);
     if (rc) return rc;
   }
+  return VSX_OK;
+}
+
+extern "C" int vsx_growth_accumulate(const float *g_means, const int32_t *active,
+                                     int32_t n_active, int32_t n, double *grow_sum,
+                                     double *grow_cnt, vsx_stream s) {
+  VSX_REQUIRE(n >= 1 && n_active >= 0 && grow_sum && grow_cnt, "growth_accumulate: bad args");
+  if (n_active == 0) return VSX_OK;
+  growth_accumulate_kernel<<<grid_for(n_active, 256), 256, 0, as_stream(s)>>>(
+      g_means, active, n_active, n, grow_sum, grow_cnt);
+  VSX_LAUNCH_CHECK("growth_accumulate");
   return VSX_OK;
 }

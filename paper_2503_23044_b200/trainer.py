@@ -623,10 +623,9 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             with _span(timer, "project_bwd"):
                 gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P, gs, view)
                 # growth pressure: |dL/dmu| of every gaussian into its anchor
-                norms = torch.linalg.vector_norm(gg["means"].double(), dim=-1)
-                gidx = active.long().repeat_interleave(state.n)
-                state.grow_sum_flat.index_add_(0, gidx, norms)
-                state.grow_cnt_flat.index_add_(0, gidx, torch.ones_like(norms))
+                # (one fused kernel: float64 norms, per-anchor sum and count)
+                call("vsx_growth_accumulate", ptr(gg["means"]), ptr(active), int(active.numel()),
+                     state.n, ptr(state.grow_sum_flat), ptr(state.grow_cnt_flat), stream())
             with _span(timer, "decode_bwd"):
                 decoder_backward_into(params, state.dgrads, active, ds.centers, anchors.emb,
                                       anchors.log_scales, anchors.offsets, view, ds.lod_ref,
