@@ -189,6 +189,10 @@ int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t n, int32_t 
  * (lower_bound per tile; no atomics). */
 int vsx_tile_ranges(const uint32_t *sorted_tiles, int64_t n, int32_t num_tiles,
                     uint32_t *tile_offsets, vsx_stream s);
+/* *max_len = max(*max_len, longest tile list) (device u32, accumulates across
+ * calls: StepReport.max_tile_splats, trainer.py:373). */
+int vsx_tile_max_len(const uint32_t *tile_offsets, int32_t num_tiles, uint32_t *max_len,
+                     vsx_stream s);
 /* Tile-major alternative to phases 2-3 (the training path): with
  * tile_offsets = exclusive scan of vsx_bin_count's tile_counts (splat_tiles
  * may be NULL), every covered tile's next slot (atomic cursor, num_tiles
@@ -236,6 +240,9 @@ typedef struct vsx_loss_desc {
   const float *extra_rgb;
   const float *extra_normal;
   const float *extra_depth;
+  /* optional: += sum over the view's pixels of n_contrib (live (pixel, splat)
+   * pairs), reduced in the forward epilogue; NULL when not wanted. */
+  unsigned long long *live_pairs;
 } vsx_loss_desc;
 
 int vsx_raster_fwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,

@@ -44,7 +44,7 @@ class VsxLossDesc(ctypes.Structure):
                 ("prior_normal_valid", c_void_p), ("rgb_scale", c_f32),
                 ("depth_weight", c_f32), ("normal_weight", c_f32), ("sums", c_void_p),
                 ("counts", c_void_p), ("extra_rgb", c_void_p), ("extra_normal", c_void_p),
-                ("extra_depth", c_void_p)]
+                ("extra_depth", c_void_p), ("live_pairs", c_void_p)]
 
 
 class VsxNccGeom(ctypes.Structure):
@@ -65,6 +65,7 @@ _SIGS = {
     "vsx_sort_pairs_u64": ([P, P, P, P, c_i64, c_i32, c_i32, c_i32, P, c_size, P], c_i32),
     "vsx_sort_pairs_u32": ([P, P, P, P, c_i64, c_i32, c_i32, c_i32, P, c_size, P], c_i32),
     "vsx_tile_ranges": ([P, c_i64, c_i32, P, P], c_i32),
+    "vsx_tile_max_len": ([P, c_i32, P, P], c_i32),
     "vsx_sort_splats_ws_bytes": ([c_i64], c_size),
     "vsx_sort_splats_z": ([P, c_i64, P, P, c_size, P], c_i32),
     "vsx_sort_z_gid_ws_bytes": ([c_i64], c_size),

@@ -440,6 +440,24 @@ extern "C" int vsx_tile_ranges(const uint32_t *sorted_tiles, int64_t n, int32_t 
   return VSX_OK;
 }
 
+__global__ void tile_max_len_kernel(const uint32_t *__restrict__ tile_off, int T,
+                                    uint32_t *__restrict__ max_len) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t len = t < T ? tile_off[t + 1] - tile_off[t] : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+  if ((threadIdx.x & 31) == 0 && len) atomicMax(max_len, len);
+}
+
+extern "C" int vsx_tile_max_len(const uint32_t *tile_offsets, int32_t num_tiles,
+                                uint32_t *max_len, vsx_stream s) {
+  VSX_REQUIRE(num_tiles >= 1 && max_len, "tile_max_len: bad args");
+  tile_max_len_kernel<<<grid_for(num_tiles, 256), 256, 0, as_stream(s)>>>(tile_offsets,
+                                                                          num_tiles, max_len);
+  VSX_LAUNCH_CHECK("tile_max_len");
+  return VSX_OK;
+}
+
 extern "C" int vsx_bin_emit_tiles(const vsx_splat *rec, const double *radius, int32_t n,
                                   int32_t width, int32_t height, const uint32_t *tile_offsets,
                                   uint32_t *cursor, uint32_t *tile_list, vsx_stream s) {

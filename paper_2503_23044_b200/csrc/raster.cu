@@ -94,6 +94,12 @@ __device__ __forceinline__ void fwd_epilogue(const vsx_camera &cam, bool inside,
       }
     }
   }
+  if (L.live_pairs) {  // block-uniform
+    unsigned long long lp = inside ? (unsigned long long)nc : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lp += __shfl_xor_sync(0xffffffffu, lp, o);
+    if ((threadIdx.x & 31) == 0 && lp) atomicAdd(L.live_pairs, lp);
+  }
   if (L.gt_rgb) {  // block-uniform
     l_rgb = warp_sum_d(l_rgb);
     l_dep = warp_sum_d(l_dep);

@@ -543,7 +543,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     counts = torch.zeros((B, 2), dtype=torch.int32, device=dev)     # depth px, normal px
     rgb_acc, dep_sum, nrm_sum = sums[:, 0], sums[:, 1], sums[:, 2]
     dep_cnt, nrm_cnt = counts[:, 0], counts[:, 1]
-    tile_max = torch.zeros(B, dtype=torch.int64, device=dev)
+    tile_max = torch.zeros(1, dtype=torch.int32, device=dev)   # longest tile list (u32)
     live = torch.zeros((), dtype=torch.int64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     gaussians = 0
@@ -580,7 +580,8 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
                               view, status)
             with _span(timer, "bin_sort"):
                 Bn = D.bin_tiles(P, view.width, view.height)
-            tile_max[vi] = torch.diff(Bn.tile_offsets.long()).max()
+            call("vsx_tile_max_len", ptr(Bn.tile_offsets), Bn.tiles_x * Bn.tiles_y,
+                 ptr(tile_max), stream())
             ev = torch.cuda.Event()
             ev.record(fs)
         fronts[vi] = (active, dec, P, Bn, ev)
@@ -598,7 +599,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             normal_weight=(wn / len(have_n) / 3.0) if vi in have_n else 0.0,
             sums=sums[vi].data_ptr(), counts=counts[vi].data_ptr(),
             extra_rgb=ptr(ex_rgb).value, extra_normal=ptr(ex_nrm).value,
-            extra_depth=ptr(ex_dep).value)
+            extra_depth=ptr(ex_dep).value, live_pairs=live.data_ptr())
 
     def take_front(vi):
         nonlocal gaussians, isects
@@ -648,7 +649,6 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             _tr(f"raster{vi}")
             with _span(timer, "raster_fwd"):
                 R = D.raster_forward(P, Bn, views[vi], loss=loss)
-            live += R.n_contrib.sum()
             backward(vi, active, dec, P, Bn, R, loss)
             _tr(f"bwd{vi}_queued")
             # the next view's front end is issued after this view's back end
@@ -666,7 +666,6 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             loss = loss_desc(vi)
             with _span(timer, "raster_fwd"):
                 R = D.raster_forward(P, Bn, views[vi], loss=loss)
-            live += R.n_contrib.sum()
             fwd.append((active, dec, P, Bn, R))
             if vi + 1 < B:
                 front(vi + 1)
@@ -688,7 +687,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     # step; the non-finite check must precede Adam, trainer.py:317-321)
     hw = torch.tensor([v.height * v.width * 3 for v in views], dtype=torch.float64, device=dev)
     z = torch.zeros((), dtype=torch.float64, device=dev)
-    vals = [status[0].double(), (rgb_acc / hw).mean(), z, z, z, tile_max.max().double(),
+    vals = [status[0].double(), (rgb_acc / hw).mean(), z, z, z, tile_max[0].double(),
             live.double()]
     if have:
         cnt = dep_cnt.double()
