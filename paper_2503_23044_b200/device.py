@@ -240,9 +240,16 @@ def decoder_image(dec_abi, n: int) -> torch.Tensor:
 class Projected:
     rec: torch.Tensor        # (G',16) f32 view of vsx_splat records, sorted
     radius: torch.Tensor     # (G',) f64 sorted
-    zkey: torch.Tensor       # (G',) int64 (float64 z bits) sorted
+    zkey_or_thunk: object    # (G',) int64 (float64 z bits) sorted, or a thunk making it
     src: torch.Tensor        # (G',) int32 index into the decode batch
     count: int
+
+    @property
+    def zkey(self) -> torch.Tensor:
+        """Sorted z keys; gathered on first use (the training step never reads them)."""
+        if callable(self.zkey_or_thunk):
+            self.zkey_or_thunk = self.zkey_or_thunk()
+        return self.zkey_or_thunk
 
     @property
     def mean2d(self) -> torch.Tensor:
@@ -301,8 +308,8 @@ def gather_projected(rec, key, rad, order, n_kept: int) -> "Projected":
     rs = torch.empty((max(n_kept, 1), REC_F32), dtype=torch.float32, device="cuda")
     rr = torch.empty(max(n_kept, 1), dtype=torch.float64, device="cuda")
     call("vsx_gather_splats", ptr(rec), ptr(rad), ptr(order), n_kept, ptr(rs), ptr(rr), stream())
-    skey = key[order[:n_kept].long()]
-    return Projected(rs[:n_kept], rr[:n_kept], skey, order[:n_kept], n_kept)
+    src = order[:n_kept]
+    return Projected(rs[:n_kept], rr[:n_kept], lambda: key[src.long()], src, n_kept)
 
 
 # ------------------------------------------------------------------ binning
