@@ -246,6 +246,17 @@ def ncu_traffic(kernel: str):
         return None
 
 
+def ncu_limiter(kernel: str):
+    """The limiter the committed ncu capture shows for `kernel` (issue slots)."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        e = json.loads(p.read_text())[kernel]
+        return {"kind": "instruction issue", "ncu_issue_slots_busy": e["issue_slots_busy"],
+                "source": e["source"]}
+    except Exception:
+        return None
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -503,7 +514,8 @@ def run_vsx(args):
                      # the compositor is issue-bound, not HBM-bound: composited
                      # (pixel, splat) pairs per second of the dominant kernel
                      "live_pairs_per_launch": live_pairs / max(stage_n[dom], 1),
-                     "pairs_per_s": live_pairs / max(stage_n[dom], 1) / per_launch_s},
+                     "pairs_per_s": live_pairs / max(stage_n[dom], 1) / per_launch_s,
+                     "limiter": ncu_limiter(dom)},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk,
         "stages_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
