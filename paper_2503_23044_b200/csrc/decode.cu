@@ -278,47 +278,66 @@ __global__ void __launch_bounds__(256) decode_bwd_gauss_kernel(
   const int rows = 11 * n;
   const size_t ld = cache_ld(n_active);
   const int t = threadIdx.x;
-  stage_cache_tile(so, cache_o, ld, r0, na, rows, sp);
-  __syncthreads();
   const bool ok = t < na * n;
   const int ra = t / n, sl = t - ra * n;  // block-local anchor, slot
   const int r = r0 + ra;
   const size_t g = (size_t)r * n + sl;
+  // per-gaussian operands are loaded before the staging barrier so their
+  // latency overlaps the tile staging
+  float gop = 0.f, gcol[3] = {0.f, 0.f, 0.f}, sc[3] = {0.f, 0.f, 0.f},
+        gsc[3] = {0.f, 0.f, 0.f}, q4[4] = {0.f, 0.f, 0.f, 0.f}, gq[4] = {0.f, 0.f, 0.f, 0.f},
+        gnr[3] = {0.f, 0.f, 0.f}, gmu[3] = {0.f, 0.f, 0.f}, ls[3] = {0.f, 0.f, 0.f};
+  int a = 0;
+  if (ok) {
+    a = active[r];
+    gop = g_opacity[g];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      gcol[c] = g_color[3 * g + c];
+      sc[c] = dscale[3 * g + c];
+      gsc[c] = g_scale[3 * g + c];
+      gnr[c] = g_normal[3 * g + c];
+      gmu[c] = g_means[3 * g + c];
+      ls[c] = log_scale[3 * a + c];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      q4[c] = dquat[4 * g + c];
+      gq[c] = g_quat[4 * g + c];
+    }
+  }
+  stage_cache_tile(so, cache_o, ld, r0, na, rows, sp);
+  __syncthreads();
   const float smax = (float)max_scale, smin = (float)kMinScale;
   float go[11];
   if (ok) {
     {
       const float sg = sigmoidf_(so[sl * sp + ra]);
-      go[0] = g_opacity[g] * sg * (1.f - sg);
+      go[0] = gop * sg * (1.f - sg);
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const float sg = sigmoidf_(so[(n + 3 * sl + c) * sp + ra]);
-      go[1 + c] = g_color[3 * g + c] * sg * (1.f - sg);
+      go[1 + c] = gcol[c] * sg * (1.f - sg);
     }
     float o[7];
 #pragma unroll
     for (int c = 0; c < 7; ++c) o[c] = so[(4 * n + 7 * sl + c) * sp + ra];
     // scales: clamp(exp(o), 1e-6, max) — gradient passes inside [min, max]
-    float sc[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const float e = expf(o[c]);
-      sc[c] = dscale[3 * g + c];
       const bool pass = (e >= smin) && (e <= smax);
-      go[4 + c] = pass ? g_scale[3 * g + c] * e : 0.f;
+      go[4 + c] = pass ? gsc[c] * e : 0.f;
     }
     // quaternion: normalised (o[3:7] + (1,0,0,0)); normal = column argmin(s) of R(q)
-    const float qw = dquat[4 * g + 0], qx = dquat[4 * g + 1], qy = dquat[4 * g + 2],
-                qz = dquat[4 * g + 3];
-    float gq[4] = {g_quat[4 * g + 0], g_quat[4 * g + 1], g_quat[4 * g + 2], g_quat[4 * g + 3]};
+    const float qw = q4[0], qx = q4[1], qy = q4[2], qz = q4[3];
     const int ax = argmin3(sc[0], sc[1], sc[2]);
     float G[9];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {  // register selects: a dynamic index would spill G
-      const float gn = g_normal[3 * g + c];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) G[3 * c + k] = k == ax ? gn : 0.f;
+      for (int k = 0; k < 3; ++k) G[3 * c + k] = k == ax ? gnr[c] : 0.f;
     }
     rot_vjp(qw, qx, qy, qz, G, gq);
     const float rw = o[3] + 1.0f, rx = o[4], ry = o[5], rz = o[6];
@@ -335,11 +354,9 @@ __global__ void __launch_bounds__(256) decode_bwd_gauss_kernel(
     }
     // means = c + offset * l  (each (anchor, slot) appears once per view);
     // float32 is ample for a gradient (the forward keeps mu in float64)
-    const int a = active[r];
     float *goff = g_offsets + ((size_t)a * n + sl) * 3;
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-      atomicAdd(goff + c, g_means[3 * g + c] * expf(log_scale[3 * a + c]));
+    for (int c = 0; c < 3; ++c) atomicAdd(goff + c, gmu[c] * expf(ls[c]));
   }
   __syncthreads();  // the tile is reused for g_o
   if (ok) {

@@ -284,16 +284,32 @@ __global__ void __launch_bounds__(256) decode_gauss_kernel(
   const int rows = 11 * n;
   const size_t ld = cache_ld(n_active);
   const int t = threadIdx.x;
+  const bool live = t < na * n;
+  const int ra = t / n, sl = t - ra * n;
+  const int r = r0 + ra;
+  // per-gaussian global operands first (active -> offsets / centres /
+  // log_scale is a dependent chain), so their latency overlaps the staging
+  const int a = live ? active[r] : 0;
+  float off[3] = {0.f, 0.f, 0.f};
+  double cen[3] = {0.0, 0.0, 0.0};
+  float ls[3] = {0.f, 0.f, 0.f};
+  if (live) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      off[c] = offsets[((size_t)a * n + sl) * 3 + c];
+      cen[c] = centers[3 * a + c];
+      if (sl == 0) ls[c] = log_scale[3 * a + c];
+    }
+  }
   stage_cache_tile(so, cache_o, ld, r0, na, rows, sp);
-  for (int e = t; e < 3 * na; e += blockDim.x)
-    s_ls[e] = exp((double)log_scale[3 * active[r0 + e / 3] + e % 3]);
+  if (live && sl == 0) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) s_ls[3 * ra + c] = exp((double)ls[c]);
+  }
   __syncthreads();
   bool bad = false;
-  if (t < na * n) {
-    const int ra = t / n, sl = t - ra * n;
-    const int r = r0 + ra;
+  if (live) {
     const int64_t g = (int64_t)r * n + sl;
-    const int a = active[r];
     const float op = sigm(so[sl * sp + ra]);
     opacity[g] = op;
     bad |= !isfinite(op);
@@ -329,10 +345,9 @@ __global__ void __launch_bounds__(256) decode_gauss_kernel(
 #pragma unroll
     for (int c = 0; c < 3; ++c)  // register selects: a dynamic index would spill R
       normal[3 * g + c] = ax == 0 ? R[3 * c] : (ax == 1 ? R[3 * c + 1] : R[3 * c + 2]);
-    const float *off = offsets + ((size_t)a * n + sl) * 3;
-    const double m0 = dadd(centers[3 * a + 0], dmul((double)off[0], s_ls[3 * ra + 0]));
-    const double m1 = dadd(centers[3 * a + 1], dmul((double)off[1], s_ls[3 * ra + 1]));
-    const double m2 = dadd(centers[3 * a + 2], dmul((double)off[2], s_ls[3 * ra + 2]));
+    const double m0 = dadd(cen[0], dmul((double)off[0], s_ls[3 * ra + 0]));
+    const double m1 = dadd(cen[1], dmul((double)off[1], s_ls[3 * ra + 1]));
+    const double m2 = dadd(cen[2], dmul((double)off[2], s_ls[3 * ra + 2]));
     means[3 * g + 0] = m0;
     means[3 * g + 1] = m1;
     means[3 * g + 2] = m2;

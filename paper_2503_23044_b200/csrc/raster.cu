@@ -29,7 +29,10 @@
 
 namespace vsx {
 
-constexpr int kChunk = 256;
+#ifndef VSX_FWD_CHUNK
+#define VSX_FWD_CHUNK 256
+#endif
+constexpr int kChunk = VSX_FWD_CHUNK;
 constexpr int kBCMax = 32;  // largest backward splat chunk
 
 // Per-pixel finalize (renderer.py:282-301) + fused loss partial sums (K9),
@@ -139,10 +142,12 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(
   bool done = !inside;
   for (uint32_t cs = begin; cs < end; cs += kChunk) {
     if (__syncthreads_count(!done) == 0) break;
-    const uint32_t idx = cs + threadIdx.x;
-    if (idx < end) {
-      const vsx_splat sp = load_splat(rec, tile_list[idx]);
-      stage_splat(sp, ox, oy, s0[threadIdx.x], s1[threadIdx.x], s2[threadIdx.x], s3[threadIdx.x]);
+    for (int k = threadIdx.x; k < kChunk; k += blockDim.x) {
+      const uint32_t idx = cs + k;
+      if (idx < end) {
+        const vsx_splat sp = load_splat(rec, tile_list[idx]);
+        stage_splat(sp, ox, oy, s0[k], s1[k], s2[k], s3[k]);
+      }
     }
     __syncthreads();
     const int cnt = (int)min((uint32_t)kChunk, end - cs);
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(256 / PX) raster_fwd2_kernel(
   for (uint32_t cs = begin; cs < end; cs += kChunk) {
     if (__syncthreads_count(!all_done()) == 0) break;
 #pragma unroll
-    for (int h = 0; h < PX; ++h) {
+    for (int h = 0; h < kChunk / kThreads; ++h) {
       const int k = threadIdx.x + kThreads * h;
       const uint32_t idx = cs + k;
       if (idx < end) {
