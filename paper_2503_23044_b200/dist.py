@@ -171,19 +171,26 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     B = len(views)
     renderers = scheduler.assign(views, world) if scheduler is not None else None
+    renderers = np.asarray(renderers if renderers is not None
+                           else [renderer_of(v, world) for v in range(B)], dtype=np.int64)
     backend.begin_step(views)
-    payloads = [backend.forward_shard(v, views[v]) for v in range(B)]
-    plan, merged = exchange_splats(payloads, rank, world, group, renderers)
-    grads, timers = {}, {}
-    for v, (payload, seg) in merged.items():
-        t0 = _Stopwatch(payload.z.device)
-        grads[v] = backend.render(v, views[v], payload, images[v],
-                                  None if priors is None else priors[v],
-                                  None if normal_priors is None else normal_priors[v])
-        timers[v] = t0.stop()
-    back = return_grads(plan, grads, backend.grad_like(), group)
-    for v in range(B):
-        backend.backward_shard(v, views[v], back[v])
+    from .trainer import _pipeline_enabled
+    if hasattr(backend, "prepare") and _pipeline_enabled():
+        timers = _pipelined_views(backend, views, images, priors, normal_priors, group,
+                                  renderers, rank, world)
+    else:
+        payloads = [backend.forward_shard(v, views[v]) for v in range(B)]
+        plan, merged = exchange_splats(payloads, rank, world, group, renderers)
+        grads, timers = {}, {}
+        for v, (payload, seg) in merged.items():
+            t0 = _Stopwatch(payload.z.device)
+            grads[v] = backend.render(v, views[v], payload, images[v],
+                                      None if priors is None else priors[v],
+                                      None if normal_priors is None else normal_priors[v])
+            timers[v] = t0.stop()
+        back = return_grads(plan, grads, backend.grad_like(), group)
+        for v in range(B):
+            backend.backward_shard(v, views[v], back[v])
     dist.all_reduce(backend.decoder_grad(), op=dist.ReduceOp.SUM, group=group)
     losses = backend.loss_terms()              # (B, 5): rgb, depth, normal sums; counts
     dist.all_reduce(losses, op=dist.ReduceOp.SUM, group=group)
@@ -196,7 +203,7 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
         secs = secs.cuda()
     dist.all_reduce(secs, op=dist.ReduceOp.SUM, group=group)
     secs = secs.cpu().numpy()
-    per_rank = np.bincount(plan.renderers, weights=secs, minlength=world)
+    per_rank = np.bincount(renderers, weights=secs, minlength=world)
     if isinstance(report, dict):
         report["render_seconds"] = per_rank.tolist()
         report["imbalance"] = float(per_rank.max() / per_rank.mean()) if per_rank.sum() > 0 \
@@ -204,6 +211,120 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
     if scheduler is not None:
         scheduler.update(views, secs)
     return report
+
+
+def _shard_groups() -> int:
+    import os
+    return max(1, int(os.environ.get("VSX_SHARD_GROUPS", "2")))
+
+
+def _pipelined_views(backend, views, images, priors, normal_priors, group, renderers, rank,
+                     world) -> dict:
+    """The sharded step in K view groups, software-pipelined over three streams.
+
+    Group k's C1 exchange, compositing and reverse C1 run on the main stream;
+    meanwhile the high-priority front stream runs the (z, gid) merge + binning
+    of the next composited view and the shard forwards (cull, decode,
+    project) of group k+1, and the tail stream runs the shard backwards
+    (projection + decoder backward) of group k-1. Every rank issues the same
+    collectives in the same order (exchange(g0), return(g0), exchange(g1),
+    ...); the side work is rank-local, so ranks may interleave it
+    differently. Buffers stay referenced until the step's host sync.
+    """
+    from .trainer import _front_stream, _side_stream, _tail_stream, _tr
+    B = len(views)
+    K = min(_shard_groups(), B)
+    groups = [list(range(k * B // K, (k + 1) * B // K)) for k in range(K)]
+    groups = [g for g in groups if g]
+    main = torch.cuda.current_stream()
+    # prep (merge + bin) and the shard forwards both read counts back to the
+    # host; on separate streams neither read waits behind the other's kernels
+    fs, ts = _front_stream(), _tail_stream()
+    ss = _side_stream("shard_fwd", priority=-1)
+    for st in (fs, ts, ss):
+        st.wait_stream(main)
+    payloads, hold, timers = {}, [], {}
+
+    def fwd(v):
+        with torch.cuda.stream(ss):
+            payloads[v] = backend.forward_shard(v, views[v])
+
+    def bwd(v, g):
+        with torch.cuda.stream(ts):
+            backend.backward_shard(v, views[v], g)
+
+    _tr("step")
+    for v in groups[0]:
+        fwd(v)
+    _tr("fwd_g0")
+    pending_bwd: list = []
+    for k, gk in enumerate(groups):
+        main.wait_stream(ss)          # group k's payloads are complete
+        _tr(f"x{k}")
+        plan, merged = exchange_splats([payloads[v] for v in gk], rank, world, group,
+                                       renderers[gk])
+        _tr(f"x{k}_done")
+        hold.append((plan, merged, [payloads[v] for v in gk]))
+        fs.wait_stream(main)          # the merge reads the received rows
+        items = list(merged.items())  # (local index, (payload, seg))
+        side = [("f", v) for v in (groups[k + 1] if k + 1 < len(groups) else [])] + \
+            [("b", vg) for vg in pending_bwd]
+        pending_bwd = []
+        done = 0
+
+        def run_side(upto):
+            nonlocal done
+            while done < upto:
+                kind, x = side[done]
+                if kind == "f":
+                    fwd(x)
+                else:
+                    bwd(*x)
+                done += 1
+
+        prepared = {}
+
+        def prep(i):
+            li, (payload, _seg) = items[i]
+            with torch.cuda.stream(fs):
+                work = backend.prepare(gk[li], views[gk[li]], payload)
+                ev = torch.cuda.Event()
+                ev.record(fs)
+            prepared[i] = (work, ev)
+
+        grads = {}
+        if items:
+            prep(0)
+        for i, (li, (payload, _seg)) in enumerate(items):
+            v = gk[li]
+            work, ev = prepared.pop(i)
+            hold.append(work)
+            main.wait_event(ev)
+            t0 = _Stopwatch(payload.z.device)
+            grads[li] = backend.render_prepared(v, views[v], work, images[v],
+                                                None if priors is None else priors[v],
+                                                None if normal_priors is None
+                                                else normal_priors[v])
+            timers[v] = t0.stop()
+            _tr(f"r{v}")
+            if i + 1 < len(items):
+                prep(i + 1)
+            _tr(f"p{v}")
+            run_side((i + 1) * len(side) // len(items))
+            _tr(f"s{v}")
+        run_side(len(side))
+        back = return_grads(plan, grads, backend.grad_like(), group)
+        _tr(f"ret{k}")
+        hold.append((grads, back))
+        ts.wait_stream(main)          # the returned gradients
+        pending_bwd = [(v, back[li]) for li, v in enumerate(gk)]
+    for v, g in pending_bwd:
+        bwd(v, g)
+    _tr("bwd_last")
+    for st in (ts, fs, ss):
+        main.wait_stream(st)
+    backend._hold = hold              # released by the next step's begin_step
+    return timers
 
 
 class _Stopwatch:
@@ -264,6 +385,7 @@ class CudaShardBackend:
 
     def begin_step(self, views) -> None:
         st = self.state
+        self._hold = None             # the previous step's buffers (synced since)
         st.flat.grad.zero_()
         B = len(views)
         self.B = B
@@ -294,16 +416,25 @@ class CudaShardBackend:
         self.work[v] = (active, dec, P)
         return SplatPayload(P.rec, P.zkey.view(torch.float64), P.radius, gid)
 
+    def prepare(self, v: int, view, payload: SplatPayload):
+        """Merge the view's received splats in (z, gid) order and bin them."""
+        D = self.D
+        n = payload.count
+        order = D.sort_z_gid(payload.z, payload.gid)
+        P = D.Projected(payload.rec[order].contiguous(), payload.radius[order].contiguous(),
+                        lambda: payload.z[order].view(torch.int64), order.int(), n)
+        Bn = D.bin_tiles(P, view.width, view.height)
+        return P, Bn, order
+
     def render(self, v: int, view, payload: SplatPayload, image, prior, nprior) -> torch.Tensor:
+        return self.render_prepared(v, view, self.prepare(v, view, payload), image, prior, nprior)
+
+    def render_prepared(self, v: int, view, work, image, prior, nprior) -> torch.Tensor:
         from ._lib import VsxLossDesc, ptr
         D, st = self.D, self.state
         from .trainer import _mask_u8, _prior_arrays, _to_device_image, weight_schedule
-        n = payload.count
+        P, Bn, order = work
         H, W = view.height, view.width
-        order = D.sort_z_gid(payload.z, payload.gid)
-        P = D.Projected(payload.rec[order].contiguous(), payload.radius[order].contiguous(),
-                        payload.z[order].view(torch.int64), order.int(), n)
-        Bn = D.bin_tiles(P, W, H)
         w2, _ = weight_schedule(st.step, st.cfg)
         wn = float(getattr(st.cfg, "normal_weight", 0.0))
         gt = _to_device_image(image, (H, W, 3))

@@ -21,6 +21,7 @@ import contextlib
 from types import SimpleNamespace
 import ctypes
 import json
+import threading
 import time
 import os
 from dataclasses import dataclass, fields
@@ -414,8 +415,18 @@ def _mask_u8(v, shape) -> torch.Tensor:
     return t
 
 
-_COPY_STREAM = None
-_FRONT_STREAM = None
+# Side streams of the per-view pipeline, one set per host thread (a host
+# thread drives one device; the sort/scan scratch buffers are keyed by stream,
+# so threads must not share streams).
+_STREAMS = threading.local()
+
+
+def _side_stream(name: str, priority: int = 0) -> torch.cuda.Stream:
+    st = getattr(_STREAMS, name, None)
+    if st is None or st.device != torch.device("cuda", torch.cuda.current_device()):
+        st = torch.cuda.Stream(priority=priority)
+        setattr(_STREAMS, name, st)
+    return st
 # VSX_TRACE=1: host timestamps of the step's phases (diagnosing host stalls)
 _TRACE = os.environ.get("VSX_TRACE") == "1"
 TRACE_LOG: list = []
@@ -432,8 +443,8 @@ def reserve_stream_pools(nbytes: int) -> None:
     streams = [cur]
     if _pipeline_enabled():
         streams += [_front_stream(), _tail_stream()]
-    if _COPY_STREAM is not None:
-        streams.append(_COPY_STREAM)
+    if getattr(_STREAMS, "copy", None) is not None:
+        streams.append(_STREAMS.copy)
     for st in streams:
         with torch.cuda.stream(st):
             pad = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
@@ -447,20 +458,11 @@ def _tr(label):
 
 
 def _front_stream() -> torch.cuda.Stream:
-    global _FRONT_STREAM
-    if _FRONT_STREAM is None:
-        _FRONT_STREAM = torch.cuda.Stream(priority=-1)  # ahead of the compositor's CTAs
-    return _FRONT_STREAM
-
-
-_TAIL_STREAM = None
+    return _side_stream("front", priority=-1)  # ahead of the compositor's CTAs
 
 
 def _tail_stream() -> torch.cuda.Stream:
-    global _TAIL_STREAM
-    if _TAIL_STREAM is None:
-        _TAIL_STREAM = torch.cuda.Stream()
-    return _TAIL_STREAM
+    return _side_stream("tail")
 
 
 def _pipeline_enabled() -> bool:
@@ -479,11 +481,8 @@ class _InputStager:
     """
 
     def __init__(self, views, images, priors, have, normal_priors, have_n):
-        global _COPY_STREAM
-        if _COPY_STREAM is None:
-            _COPY_STREAM = torch.cuda.Stream()
         cur = torch.cuda.current_stream()
-        cs = _COPY_STREAM
+        cs = _side_stream("copy")
         cs.wait_stream(cur)
         self.items, self.events = [], []
         with torch.cuda.stream(cs):
