@@ -111,14 +111,20 @@ def exclusive_scan(counts: torch.Tensor, n: int) -> torch.Tensor:
     return out
 
 
-def select(flags: torch.Tensor) -> torch.Tensor:
-    """Ordered indices of non-zero u8 flags (one host sync for the count)."""
+def select_async(flags: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """Ordered indices of non-zero u8 flags, capacity-sized, and the device count."""
     n = int(flags.numel())
     idx = _u32(n)
     cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
     lib = _lib.load()
     wp, wb = workspace().get(lib.vsx_sort_ws_bytes(n))
     call("vsx_select", ptr(flags), n, ptr(idx), ptr(cnt), wp, wb, stream())
+    return idx, cnt
+
+
+def select(flags: torch.Tensor) -> torch.Tensor:
+    """Ordered indices of non-zero u8 flags (one host sync for the count)."""
+    idx, cnt = select_async(flags)
     return idx[: int(cnt.item())]
 
 
@@ -276,9 +282,21 @@ class Projected:
         return self.rec[:, 14]
 
 
-def project(means, opacity, color, scale, quat, normal, view: CameraView,
-            status: torch.Tensor) -> Projected:
-    """EWA projection + stable (z, batch-order) sort; batch must be gid-ascending."""
+@dataclass
+class ProjectLaunch:
+    """project_launch() output: unsorted records, the sort order, and the
+    device count of kept splats (read by the caller, possibly batched)."""
+    rec: torch.Tensor
+    key: torch.Tensor
+    rad: torch.Tensor
+    kept: torch.Tensor
+    order: torch.Tensor | None
+    g: int
+
+
+def project_launch(means, opacity, color, scale, quat, normal, view: CameraView,
+                   status: torch.Tensor) -> ProjectLaunch:
+    """K3 projection + (z, batch-order) sort, no host sync."""
     g = int(means.shape[0])
     rec = torch.empty((max(g, 1), REC_F32), dtype=torch.float32, device="cuda")
     key = torch.empty(max(g, 1), dtype=torch.int64, device="cuda")
@@ -287,12 +305,21 @@ def project(means, opacity, color, scale, quat, normal, view: CameraView,
     call("vsx_project_fwd", ptr(means), ptr(opacity), ptr(color), ptr(scale), ptr(quat),
          ptr(normal), g, view.to_abi(), ptr(rec), ptr(key), ptr(rad), ptr(kept), ptr(status),
          stream())
-    if g == 0:
-        e = torch.empty(0, device="cuda")
-        return Projected(rec[:0], rad[:0], key[:0], kept[:0], 0)
-    order = sort_splats_z(key[:g], g)
-    n_kept = int(kept.item())
-    return gather_projected(rec, key, rad, order, n_kept)
+    order = sort_splats_z(key[:g], g) if g else None
+    return ProjectLaunch(rec, key, rad, kept, order, g)
+
+
+def project_finish(pl: ProjectLaunch, n_kept: int) -> "Projected":
+    if pl.g == 0:
+        return Projected(pl.rec[:0], pl.rad[:0], pl.key[:0], pl.kept[:0], 0)
+    return gather_projected(pl.rec, pl.key, pl.rad, pl.order, n_kept)
+
+
+def project(means, opacity, color, scale, quat, normal, view: CameraView,
+            status: torch.Tensor) -> Projected:
+    """EWA projection + stable (z, batch-order) sort; batch must be gid-ascending."""
+    pl = project_launch(means, opacity, color, scale, quat, normal, view, status)
+    return project_finish(pl, int(pl.kept.item()) if pl.g else 0)
 
 
 def sort_splats_z(key: torch.Tensor, g: int) -> torch.Tensor:

@@ -215,7 +215,7 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
 
 def _shard_groups() -> int:
     import os
-    return max(1, int(os.environ.get("VSX_SHARD_GROUPS", "2")))
+    return max(1, int(os.environ.get("VSX_SHARD_GROUPS", "4")))
 
 
 def _pipelined_views(backend, views, images, priors, normal_priors, group, renderers, rank,
@@ -245,30 +245,57 @@ def _pipelined_views(backend, views, images, priors, normal_priors, group, rende
         st.wait_stream(main)
     payloads, hold, timers = {}, [], {}
 
-    def fwd(v):
-        with torch.cuda.stream(ss):
-            payloads[v] = backend.forward_shard(v, views[v])
+    def fwd_stepper(g):
+        """One stage of the batched shard forward of group g per call."""
+        gen = backend.forward_shards(g, views)
+
+        def step():
+            with torch.cuda.stream(ss):
+                try:
+                    next(gen)
+                except StopIteration as e:
+                    payloads.update(e.value)
+        return step
 
     def bwd(v, g):
         with torch.cuda.stream(ts):
             backend.backward_shard(v, views[v], g)
 
     _tr("step")
-    for v in groups[0]:
-        fwd(v)
+    first = fwd_stepper(groups[0])
+    for _ in range(3):
+        first()
     _tr("fwd_g0")
-    pending_bwd: list = []
-    for k, gk in enumerate(groups):
-        main.wait_stream(ss)          # group k's payloads are complete
+    def exchange(k):
+        # issued on the shard-forward stream: the NCCL ops wait for that
+        # stream's forwards only, not for the compositor work queued on main,
+        # and the count read-back syncs that stream only. It is issued before
+        # the previous group's reverse exchange, so it does not queue behind it
+        # on the communicator either.
+        gk = groups[k]
         _tr(f"x{k}")
-        plan, merged = exchange_splats([payloads[v] for v in gk], rank, world, group,
-                                       renderers[gk])
+        with torch.cuda.stream(ss):
+            plan, merged = exchange_splats([payloads[v] for v in gk], rank, world, group,
+                                           renderers[gk])
         _tr(f"x{k}_done")
         hold.append((plan, merged, [payloads[v] for v in gk]))
-        fs.wait_stream(main)          # the merge reads the received rows
+        return plan, merged
+
+    pending_bwd: list = []
+    nxt = exchange(0)
+    for k, gk in enumerate(groups):
+        plan, merged = nxt
+        fs.wait_stream(ss)            # the merge reads the received rows
         items = list(merged.items())  # (local index, (payload, seg))
-        side = [("f", v) for v in (groups[k + 1] if k + 1 < len(groups) else [])] + \
-            [("b", vg) for vg in pending_bwd]
+        # the next group's batched forward (three stages) spread between this
+        # group's compositor launches, the previous group's backwards between
+        bw = [("b", vg) for vg in pending_bwd]
+        if k + 1 < len(groups):
+            st_ = fwd_stepper(groups[k + 1])
+            h = len(bw) // 2
+            side = [("f", st_)] + bw[:h] + [("f", st_)] + bw[h:] + [("f", st_)]
+        else:
+            side = bw
         pending_bwd = []
         done = 0
 
@@ -277,7 +304,7 @@ def _pipelined_views(backend, views, images, priors, normal_priors, group, rende
             while done < upto:
                 kind, x = side[done]
                 if kind == "f":
-                    fwd(x)
+                    x()
                 else:
                     bwd(*x)
                 done += 1
@@ -313,6 +340,9 @@ def _pipelined_views(backend, views, images, priors, normal_priors, group, rende
             run_side((i + 1) * len(side) // len(items))
             _tr(f"s{v}")
         run_side(len(side))
+        if k + 1 < len(groups):
+            nxt = exchange(k + 1)
+        main.wait_stream(ss)          # order main after this rank's NCCL issue on ss
         back = return_grads(plan, grads, backend.grad_like(), group)
         _tr(f"ret{k}")
         hold.append((grads, back))
@@ -425,6 +455,40 @@ class CudaShardBackend:
                         lambda: payload.z[order].view(torch.int64), order.int(), n)
         Bn = D.bin_tiles(P, view.width, view.height)
         return P, Bn, order
+
+    def forward_shards(self, vs: list[int], views):
+        """forward_shard for a group of views with two host reads in total
+        (all selection counts, then all kept counts) instead of two per view.
+        A generator: each next() runs one stage, so a caller can interleave
+        the stages with other host work; returns {v: SplatPayload}."""
+        D, st = self.D, self.state
+        ds = st.dscene
+        an = st.anchors
+        sel = []
+        for v in vs:
+            sel.append(D.select_async(ds.cull(views[v]) & self.owned))
+        yield
+        counts = torch.cat([c for _, c in sel]).cpu().tolist() if sel else []
+        launched = []
+        for v, (idx, _), c in zip(vs, sel, counts):
+            active = idx[:c]
+            dec = D.decode(st.params.abi(), st.n, active, ds.centers, an.emb, an.log_scales,
+                           an.offsets, views[v], ds.lod_ref, ds.max_scale, self.status,
+                           keep_cache=True)
+            self.gaussians += dec.count
+            launched.append((active, dec, D.project_launch(
+                dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, views[v],
+                self.status)))
+        yield
+        kept = torch.cat([pl.kept for _, _, pl in launched]).cpu().tolist() if launched else []
+        out = {}
+        for v, (active, dec, pl), k in zip(vs, launched, kept):
+            P = D.project_finish(pl, k if pl.g else 0)
+            src = P.src.long()
+            gid = active.long()[src // st.n] * st.n + src % st.n
+            self.work[v] = (active, dec, P)
+            out[v] = SplatPayload(P.rec, P.zkey.view(torch.float64), P.radius, gid)
+        return out
 
     def render(self, v: int, view, payload: SplatPayload, image, prior, nprior) -> torch.Tensor:
         return self.render_prepared(v, view, self.prepare(v, view, payload), image, prior, nprior)
