@@ -493,24 +493,6 @@ __global__ void iota_kernel(uint32_t *__restrict__ v, int64_t n) {
 // After a stable sort by z, runs of equal z keep input order; reorder each
 // run by gid so the result is lexsort((gid, z)) (renderer.py:197). Runs are
 // almost always length 1, so one thread per run start suffices.
-__global__ void fix_ties_kernel(const uint64_t *__restrict__ keys, const int64_t *__restrict__ gid,
-                                uint32_t *__restrict__ order, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || (i > 0 && keys[i] == keys[i - 1])) return;
-  int64_t j = i + 1;
-  while (j < n && keys[j] == keys[i]) ++j;
-  for (int64_t a = i + 1; a < j; ++a) {
-    const uint32_t o = order[a];
-    const int64_t g = gid[o];
-    int64_t b = a - 1;
-    while (b >= i && gid[order[b]] > g) {
-      order[b + 1] = order[b];
-      --b;
-    }
-    order[b + 1] = o;
-  }
-}
-
 // 32-bit monotone proxy of a positive float64 z: round toward zero to float32
 // (order-preserving, never reverses two keys); ~0 marks culled entries.
 __global__ void z_proxy_kernel(const uint64_t *__restrict__ zkey, int64_t n,
@@ -535,6 +517,28 @@ __global__ void fix_proxy_runs_kernel(const uint32_t *__restrict__ k32,
     const uint64_t z = zkey[o];
     int64_t b = a - 1;
     while (b >= i && (zkey[order[b]] > z || (zkey[order[b]] == z && order[b] > o))) {
+      order[b + 1] = order[b];
+      --b;
+    }
+    order[b + 1] = o;
+  }
+}
+
+// Same fix-up, exact order (z, gid): the merge of C1-received splat rows.
+__global__ void fix_proxy_runs_zgid_kernel(const uint32_t *__restrict__ k32,
+                                           const uint64_t *__restrict__ zkey,
+                                           const int64_t *__restrict__ gid,
+                                           uint32_t *__restrict__ order, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || (i > 0 && k32[i] == k32[i - 1])) return;
+  int64_t j = i + 1;
+  while (j < n && k32[j] == k32[i]) ++j;
+  for (int64_t a = i + 1; a < j; ++a) {
+    const uint32_t o = order[a];
+    const uint64_t z = zkey[o];
+    const int64_t g = gid[o];
+    int64_t b = a - 1;
+    while (b >= i && (zkey[order[b]] > z || (zkey[order[b]] == z && gid[order[b]] > g))) {
       order[b + 1] = order[b];
       --b;
     }
@@ -576,27 +580,34 @@ extern "C" int vsx_sort_splats_z(const uint64_t *zkey, int64_t n, uint32_t *orde
 
 extern "C" int vsx_sort_z_gid(const double *z, const int64_t *gid, uint32_t *order, int64_t n,
                               void *ws, size_t ws_bytes, vsx_stream s) {
+  // positive float64 z: float32 round-toward-zero proxy, 4 radix passes, then
+  // runs of equal proxies re-sorted by the exact (z, gid) key. No host read
+  // (the 64-bit sort needed the varying-bit mask on the host).
   cudaStream_t st = as_stream(s);
   if (n <= 0) return VSX_OK;
-  const size_t extra = align256(sizeof(uint64_t) * n) + align256(sizeof(uint32_t) * n);
-  VSX_REQUIRE(ws_bytes >= extra + sort_ws_bytes(n), "sort_z_gid: workspace too small");
+  VSX_REQUIRE(ws_bytes >= vsx_sort_z_gid_ws_bytes(n), "sort_z_gid: workspace too small");
+  const uint64_t *zkey = reinterpret_cast<const uint64_t *>(z);
   char *p = static_cast<char *>(ws);
-  uint64_t *keys_out = reinterpret_cast<uint64_t *>(p);
-  p += align256(sizeof(uint64_t) * n);
+  uint32_t *k32 = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * n);
+  uint32_t *k32s = reinterpret_cast<uint32_t *>(p);
+  p += align256(sizeof(uint32_t) * n);
   uint32_t *iota = reinterpret_cast<uint32_t *>(p);
   p += align256(sizeof(uint32_t) * n);
+  z_proxy_kernel<<<grid_for(n, 256), 256, 0, st>>>(zkey, n, k32);
+  VSX_LAUNCH_CHECK("z_proxy");
   iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(iota, n);
   VSX_LAUNCH_CHECK("iota");
-  int rc = sort_pairs<uint64_t>(reinterpret_cast<const uint64_t *>(z), iota, keys_out, order, n,
-                                0, 64, VSX_SORT_SKIP_CONSTANT, p, ws_bytes - extra, st);
+  int rc = sort_pairs<uint32_t>(k32, iota, k32s, order, n, 0, 32, 0, p,
+                                ws_bytes - 3 * align256(sizeof(uint32_t) * n), st);
   if (rc) return rc;
-  fix_ties_kernel<<<grid_for(n, 256), 256, 0, st>>>(keys_out, gid, order, n);
-  VSX_LAUNCH_CHECK("fix_ties");
+  fix_proxy_runs_zgid_kernel<<<grid_for(n, 256), 256, 0, st>>>(k32s, zkey, gid, order, n);
+  VSX_LAUNCH_CHECK("fix_proxy_runs_zgid");
   return VSX_OK;
 }
 
 extern "C" size_t vsx_sort_z_gid_ws_bytes(int64_t n) {
-  return align256(sizeof(uint64_t) * n) + align256(sizeof(uint32_t) * n) + sort_ws_bytes(n);
+  return 3 * align256(sizeof(uint32_t) * n) + sort_ws_bytes(n);
 }
 
 extern "C" size_t vsx_scan_ws_bytes(int64_t n) { return sizeof(uint32_t) * (scan_ws_elems(n) + 1); }
