@@ -243,6 +243,10 @@ typedef struct vsx_loss_desc {
   /* optional: += sum over the view's pixels of n_contrib (live (pixel, splat)
    * pairs), reduced in the forward epilogue; NULL when not wanted. */
   unsigned long long *live_pairs;
+  /* optional schedule for vsx_raster_bwd_loss: CTA i composites tile
+   * tile_order[i] (a permutation of the tiles, e.g. longest list first so the
+   * heavy tiles do not form the kernel's tail); NULL = row-major. */
+  const uint32_t *tile_order;
 } vsx_loss_desc;
 
 int vsx_raster_fwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,

@@ -44,7 +44,8 @@ class VsxLossDesc(ctypes.Structure):
                 ("prior_normal_valid", c_void_p), ("rgb_scale", c_f32),
                 ("depth_weight", c_f32), ("normal_weight", c_f32), ("sums", c_void_p),
                 ("counts", c_void_p), ("extra_rgb", c_void_p), ("extra_normal", c_void_p),
-                ("extra_depth", c_void_p), ("live_pairs", c_void_p)]
+                ("extra_depth", c_void_p), ("live_pairs", c_void_p),
+                ("tile_order", c_void_p)]
 
 
 class VsxNccGeom(ctypes.Structure):

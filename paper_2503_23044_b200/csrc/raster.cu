@@ -751,12 +751,15 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   __shared__ int s_max;
   extern __shared__ float s_plane[];  // w plane [kBC][kPlaneStride], then q plane
   const int txn = gridDim.x;
-  const int tile = blockIdx.y * txn + blockIdx.x;
+  // optional heaviest-first schedule: CTA i takes tile_order[i]
+  const int lin = blockIdx.y * txn + blockIdx.x;
+  const int tile = a.L.tile_order ? (int)a.L.tile_order[lin] : lin;
+  const int bx = tile % txn, by = tile / txn;
   const int t = threadIdx.x;
   const int lx = t & 15, ly = t >> 4;
-  const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
+  const int px = bx * kTile + lx, py = by * kTile + ly;
   const bool inside = px < cam.width && py < cam.height;
-  const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
+  const double ox = (double)(bx * kTile), oy = (double)(by * kTile);
   const uint32_t begin = a.tile_off[tile];
   const float fx = (float)lx, fy = (float)ly;
   const int lane = t & 31, warp = t >> 5;

@@ -443,6 +443,11 @@ def raster_forward(P: Projected, B: Bins, view: CameraView, loss=None) -> Raster
     return Raster(rgb, alpha, depth, normal, raw, valid, tfin, nc)
 
 
+def _tile_order_enabled() -> bool:
+    import os
+    return os.environ.get("VSX_TILE_ORDER", "0") == "1"
+
+
 def raster_backward(P: Projected, B: Bins, view: CameraView, R: Raster, g_rgb=None, g_alpha=None,
                     g_depth=None, g_normal=None, g_raw=None, out: torch.Tensor | None = None,
                     loss=None):
@@ -450,6 +455,13 @@ def raster_backward(P: Projected, B: Bins, view: CameraView, R: Raster, g_rgb=No
     grad = out if out is not None else torch.zeros((max(P.count, 1), GRAD_F32),
                                                    dtype=torch.float32, device="cuda")
     if loss is not None:
+        order = None
+        if _tile_order_enabled() and B.tile_list.numel():
+            # heaviest tiles first: the long tiles start in the first wave
+            # instead of forming the kernel's tail
+            lens = B.tile_offsets[1:] - B.tile_offsets[:-1]
+            order = torch.argsort(lens, descending=True).to(torch.int32)
+            loss.tile_order = order.data_ptr()
         call("vsx_raster_bwd_loss", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list),
              view.to_abi(), ptr(R.rgb), ptr(R.alpha), ptr(R.depth), ptr(R.normal),
              ptr(R.raw_normal), ptr(R.t_final), ptr(R.n_contrib), loss, ptr(grad), stream())
