@@ -319,7 +319,8 @@ int vsx_masked_l1(const float *x, const uint8_t *valid, const float *prior,
                   uint32_t *counts, const float *scale, float *grad, vsx_stream s);
 
 /* ---- K10: fused Adam (trainer.py:220-247) ------------------------------- */
-/* One launch over n_seg contiguous segments; seg_begin (n_seg+1, host) are
+/* One launch over n_seg contiguous segments (16-byte aligned buffers, each
+ * segment starting on a multiple of 4 elements); seg_begin (n_seg+1, host) are
  * element offsets into the flat param/grad/m/v buffers, lr (n_seg, host). */
 int vsx_adam(float *param, const float *grad, float *m, float *v, int32_t n_seg,
              const int64_t *seg_begin, const double *lr, double beta1, double beta2, double eps,

@@ -97,6 +97,11 @@ struct AdamSegs {
   int n;
 };
 
+// One thread per 4 consecutive parameters (segments start on 16-byte
+// boundaries, so a float4 never straddles two learning-rate groups): three
+// float4 loads + one scalar-free update + three float4 stores. The moment
+// updates run in float32 (the parameters are float32; relative error ~1e-7
+// of a step); the bias corrections come in from the host in float64.
 __global__ void __launch_bounds__(256) adam_kernel(float *__restrict__ p,
                                                    const float *__restrict__ g,
                                                    float *__restrict__ m, float *__restrict__ v,
@@ -105,17 +110,46 @@ __global__ void __launch_bounds__(256) adam_kernel(float *__restrict__ p,
                                                    const int32_t *__restrict__ guard) {
   if (guard && *guard) return;  // non-finite step: parameters and moments untouched
   const int64_t total = segs.begin[segs.n];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t n4 = total >> 2;
+  const float fb1 = (float)b1, fb2 = (float)b2, c1 = (float)(1.0 - b1), c2 = (float)(1.0 - b2);
+  const float ibc1 = (float)(1.0 / bc1), ibc2 = (float)(1.0 / bc2), feps = (float)eps;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q << 2;
     int s = 0;
     while (s + 1 < segs.n && i >= segs.begin[s + 1]) ++s;
-    const double gi = g[i];
-    const double mi = b1 * (double)m[i] + (1.0 - b1) * gi;
-    const double vi = b2 * (double)v[i] + (1.0 - b2) * gi * gi;
-    m[i] = (float)mi;
-    v[i] = (float)vi;
-    const double step = -segs.lr[s] * (mi / bc1) / (sqrt(vi / bc2) + eps);
-    p[i] = (float)((double)p[i] + step);
+    const float lr = (float)segs.lr[s];
+    const float4 gi = reinterpret_cast<const float4 *>(g)[q];
+    float4 mi = reinterpret_cast<const float4 *>(m)[q];
+    float4 vi = reinterpret_cast<const float4 *>(v)[q];
+    float4 pi = reinterpret_cast<const float4 *>(p)[q];
+    auto upd = [&](float gg, float &mm, float &vv, float &pp) {
+      mm = fb1 * mm + c1 * gg;
+      vv = fb2 * vv + c2 * gg * gg;
+      pp = pp - lr * (mm * ibc1) / (sqrtf(vv * ibc2) + feps);
+    };
+    upd(gi.x, mi.x, vi.x, pi.x);
+    upd(gi.y, mi.y, vi.y, pi.y);
+    upd(gi.z, mi.z, vi.z, pi.z);
+    upd(gi.w, mi.w, vi.w, pi.w);
+    reinterpret_cast<float4 *>(m)[q] = mi;
+    reinterpret_cast<float4 *>(v)[q] = vi;
+    reinterpret_cast<float4 *>(p)[q] = pi;
+  }
+  // tail (total % 4) elements
+  const int64_t t0 = n4 << 2;
+  const int64_t i = t0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x == 0 && i < total) {
+    int s = 0;
+    while (s + 1 < segs.n && i >= segs.begin[s + 1]) ++s;
+    const float lr = (float)segs.lr[s];
+    float mm = m[i], vv = v[i];
+    const float gg = g[i];
+    mm = fb1 * mm + c1 * gg;
+    vv = fb2 * vv + c2 * gg * gg;
+    m[i] = mm;
+    v[i] = vv;
+    p[i] = p[i] - lr * (mm * ibc1) / (sqrtf(vv * ibc2) + feps);
   }
 }
 
@@ -166,12 +200,16 @@ extern "C" int vsx_masked_l1(const float *x, const uint8_t *valid, const float *
 static int adam_impl(float *param, const float *grad, float *m, float *v, int32_t n_seg,
                      const int64_t *seg_begin, const double *lr, double beta1, double beta2,
                      double eps, int32_t step, const int32_t *guard, vsx_stream s) {
+  VSX_REQUIRE(((reinterpret_cast<uintptr_t>(param) | reinterpret_cast<uintptr_t>(grad) |
+                reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0,
+              "adam: buffers must be 16-byte aligned");
   VSX_REQUIRE(n_seg >= 1 && n_seg <= kMaxSeg, "adam: 1..16 segments");
   AdamSegs segs{};
   segs.n = n_seg;
   for (int i = 0; i <= n_seg; ++i) segs.begin[i] = seg_begin[i];
   for (int i = 0; i < n_seg; ++i) {
     VSX_REQUIRE(seg_begin[i + 1] >= seg_begin[i], "adam: segments must be ascending");
+    VSX_REQUIRE(seg_begin[i] % 4 == 0, "adam: segment %d must start on a 16-byte boundary", i);
     segs.lr[i] = lr[i];
   }
   const int64_t total = seg_begin[n_seg];
