@@ -66,7 +66,21 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool keep = false;
   if (i < n) {
+    // every operand is loaded up front (one memory round trip instead of a
+    // second one behind the near-plane test)
     const double mu[3] = {means[3 * i + 0], means[3 * i + 1], means[3 * i + 2]};
+    const float sc[3] = {scale[3 * i + 0], scale[3 * i + 1], scale[3 * i + 2]};
+    float qv[4];
+    if ((reinterpret_cast<uintptr_t>(quat) & 15) == 0) {  // uniform branch
+      const float4 q4 = reinterpret_cast<const float4 *>(quat)[i];
+      qv[0] = q4.x, qv[1] = q4.y, qv[2] = q4.z, qv[3] = q4.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) qv[k] = quat[4 * i + k];
+    }
+    const float nrm[3] = {normal[3 * i + 0], normal[3 * i + 1], normal[3 * i + 2]};
+    const float col[3] = {color[3 * i + 0], color[3 * i + 1], color[3 * i + 2]};
+    const float op = opacity[i];
     double x, y, z;
     cam_transform(cam, mu[0], mu[1], mu[2], x, y, z);
     keep = z > kZNear;
@@ -75,7 +89,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
       radius[i] = 0.0;
     } else {
       ProjGeom g;
-      proj_geom(cam, mu, scale + 3 * i, quat + 4 * i, g);
+      proj_geom(cam, mu, sc, qv, g);
       if (!(g.det > 0.0)) {
         if (g.det <= 0.0) atomicOr(status, VSX_STATUS_NONPD);
       }
@@ -85,7 +99,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
       const double lam = mid + sqrt(fmax(disc, 0.0));
       radius[i] = 3.0 * sqrt(lam);
       // camera normal, flipped to face the camera (sign(n.mu) > 0 -> flip)
-      const double n0 = normal[3 * i + 0], n1 = normal[3 * i + 1], n2 = normal[3 * i + 2];
+      const double n0 = nrm[0], n1 = nrm[1], n2 = nrm[2];
       double nc[3];
 #pragma unroll
       for (int k = 0; k < 3; ++k) nc[k] = cam.r[3 * k + 0] * n0 + cam.r[3 * k + 1] * n1 + cam.r[3 * k + 2] * n2;
@@ -99,10 +113,10 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
       r.conic[0] = (float)(g.c * idet);
       r.conic[1] = (float)(-g.b * idet);
       r.conic[2] = (float)(g.a * idet);
-      r.opacity = opacity[i];
-      r.color[0] = color[3 * i + 0];
-      r.color[1] = color[3 * i + 1];
-      r.color[2] = color[3 * i + 2];
+      r.opacity = op;
+      r.color[0] = col[0];
+      r.color[1] = col[1];
+      r.color[2] = col[2];
       r.normal[0] = (float)nc[0];
       r.normal[1] = (float)nc[1];
       r.normal[2] = (float)nc[2];
