@@ -10,18 +10,27 @@
  * Reference interface each group replaces (paths relative to
  * /root/reference/pkg/src/voxsplat):
  *   vsx_cull / vsx_select          scene.py:239-259 active_mask (+ lod_for_distance :232-236)
- *   vsx_decode_fwd                 decoder.py:142-180 decode_inputs/_head_forward/decode_arrays,
+ *   vsx_decode_fwd(_tc)            decoder.py:142-180 decode_inputs/_head_forward/decode_arrays,
  *                                  decoder.py:210-250 decode_active (canonical order)
  *   vsx_project_fwd                renderer.py:144-204 project_splats (EWA + (z,gid) order)
- *   vsx_sort_pairs_u64/_u32        renderer.py:197 np.lexsort((gid, z)) (stable LSD radix)
- *   vsx_bin                        renderer.py:207-226 bin_splats
- *   vsx_raster_fwd                 renderer.py:242-301 _blend_padded + _finalize, :390-449 rasterize_view
- *   vsx_raster_bwd                 renderer.py:347-367 rasterize_backward (autograd of the blend)
+ *   vsx_sort_splats_z              renderer.py:197 np.lexsort((gid, z)) (float32 proxy radix
+ *                                  sort + exact run fix-up); vsx_sort_pairs_u64/_u32 generic
+ *   vsx_bin_count / vsx_bin_emit / vsx_tile_ranges
+ *                                  renderer.py:207-226 bin_splats
+ *   vsx_raster_fwd(_loss)          renderer.py:242-301 _blend_padded + _finalize, :390-449 rasterize_view
+ *   vsx_raster_bwd(_loss)          renderer.py:347-367 rasterize_backward (autograd of the blend)
  *   vsx_project_bwd                autograd of project_splats (trainer.py:330)
  *   vsx_decode_bwd                 decoder.py:267-292 decoder_backward (autograd of decode)
  *   vsx_l1_loss / vsx_depth_loss   losses.py:43-53 bl_rgb_loss, losses.py:65-84 e_depth_loss
- *   vsx_adam                       trainer.py:220-247 TrainState._adam + apply_*_grads
- *   vsx_exchange_*                 renderer.py:452-477 transfer_gaussians (real C1 payload packing)
+ *   vsx_adam / vsx_adam_guarded    trainer.py:220-247 TrainState._adam + apply_*_grads
+ *                                  (guarded: skipped on the device after a non-finite step,
+ *                                  trainer.py:317-321)
+ *   vsx_growth_accumulate          trainer.py:342-349 (growth pressure accumulators)
+ *   vsx_tile_max_len               trainer.py:373 StepReport.max_tile_splats
+ *   vsx_sort_z_gid                 C1 merge of received splat rows in (z, gid) order
+ *   vsx_tsdf_integrate             fusion.py:102-133 TSDF integration
+ *   (C1 payload exchange)          renderer.py:452-477 transfer_gaussians: the 64-byte splat
+ *                                  records are the payload; the all-to-all is NCCL (dist.py)
  *   vsx_prior_sample / vsx_apply_scale_shift / vsx_reprojection_error / vsx_enhance_finalize
  *                                  depth_prior.py:85-214 (fit_scale_shift, apply_scale_shift,
  *                                  reprojection_error, enhance)
