@@ -480,6 +480,11 @@ inline int decode_image_in_smem() {
 }
 
 __host__ __device__ inline int dbw_ks(int h, int n) { return (dec_head_w(h, n) + 7) / 8; }
+// staged floats per warp (decode_bwd_anchor_mma_kernel): g_o rows of the
+// widest head + 64 hidden rows, 16 anchors each at the padded strides
+__host__ __device__ inline int dbw_stage_floats(int n) {
+  return 8 * dbw_ks(2, n) * 24 + 64 * 20;
+}
 __host__ __device__ inline int dbw_ks_total(int n) { return dbw_ks(0, n) + dbw_ks(1, n) + dbw_ks(2, n); }
 __host__ __device__ inline size_t dbw_w2_floats(int n) { return (size_t)dbw_ks_total(n) * 8 * 32 * 4; }
 constexpr size_t kDbwW1Floats = (size_t)24 * 4 * 32 * 4;
@@ -551,6 +556,7 @@ __device__ __forceinline__ void split_trunc(float v, uint32_t &hi, uint32_t &lo)
 }
 
 constexpr int kDbwWarps = 8;
+constexpr int kDbwGoStride = 24, kDbwHStride = 20;  // staged row strides (floats)
 
 __global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kernel(
     int n, const float4 *__restrict__ img, const int32_t *__restrict__ active, int32_t n_active,
@@ -562,14 +568,22 @@ __global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kerne
   extern __shared__ __align__(16) float4 dimg[];
   const int kst = dbw_ks_total(n);
   const float4 *base = img;  // weight fragments read through L1 (shared with the compositor)
+  const int nimg = smem_img ? (int)(dbw_image_floats(n) / 4) : 0;
   if (smem_img) {
-    const int nimg = (int)(dbw_image_floats(n) / 4);
     for (int e = threadIdx.x; e < nimg; e += blockDim.x) dimg[e] = img[e];
     __syncthreads();
     base = dimg;
   }
   const float4 *w2i = base, *w1i = base + kst * 8 * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // per-warp staging of one head's g_o rows and hidden activations for the
+  // warp's 16 anchors: one round of coalesced loads per head instead of a
+  // dependent global load in front of every k-step (the kernel was 76%
+  // long-scoreboard stalls). Row strides 24 / 20 keep the fragment reads
+  // bank-conflict free.
+  const int go_rows = 8 * dbw_ks(2, n);
+  float *s_go = reinterpret_cast<float *>(dimg + nimg) + (size_t)warp * dbw_stage_floats(n);
+  float *s_h = s_go + go_rows * kDbwGoStride;
   const int g = lane >> 2, t = lane & 3;
   const size_t ld = cache_ld(n_active);
   const int n_tiles = (n_active + 15) / 16;
@@ -611,12 +625,25 @@ __global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kerne
       float c[8][4];
 #pragma unroll
       for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = c[q][2] = c[q][3] = 0.f;
+      __syncwarp();  // the previous head's tiles are consumed
+      {
+        const int col = lane & 15, rr = lane >> 4;
+        const bool okc = r0 + col < n_active;
+#pragma unroll 8
+        for (int row = rr; row < 8 * nks; row += 2)
+          s_go[row * kDbwGoStride + col] =
+              (okc && row < ow) ? g_o[(size_t)(oo + row) * ld + r0 + col] : 0.f;
+#pragma unroll 8
+        for (int k = rr; k < 64; k += 2)
+          s_h[k * kDbwHStride + col] = okc ? cache_h[(size_t)(h * 64 + k) * ld + r0 + col] : 0.f;
+      }
+      __syncwarp();
       for (int ks = 0; ks < nks; ++ks, ++ksg) {
         const int j0 = ks * 8 + t, j1 = j0 + 4;
-        const float a0 = (va && j0 < ow) ? g_o[(size_t)(oo + j0) * ld + ra] : 0.f;
-        const float a1 = (vb && j0 < ow) ? g_o[(size_t)(oo + j0) * ld + rb] : 0.f;
-        const float a2 = (va && j1 < ow) ? g_o[(size_t)(oo + j1) * ld + ra] : 0.f;
-        const float a3 = (vb && j1 < ow) ? g_o[(size_t)(oo + j1) * ld + rb] : 0.f;
+        const float a0 = s_go[j0 * kDbwGoStride + g];
+        const float a1 = s_go[j0 * kDbwGoStride + g + 8];
+        const float a2 = s_go[j1 * kDbwGoStride + g];
+        const float a3 = s_go[j1 * kDbwGoStride + g + 8];
         uint32_t ah[4], al[4];
         split_trunc(a0, ah[0], al[0]);
         split_trunc(a1, ah[1], al[1]);
@@ -629,10 +656,10 @@ __global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kerne
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
         const int k0 = h * 64 + nt * 8 + 2 * t;
-        const float *h0 = cache_h + (size_t)k0 * ld, *h1 = h0 + ld;
+        const float *h0 = s_h + (nt * 8 + 2 * t) * kDbwHStride, *h1 = h0 + kDbwHStride;
         float *p0 = g_pre_out + (size_t)k0 * ld, *p1 = p0 + ld;
         if (va) {
-          const float x0 = h0[ra], x1 = h1[ra];
+          const float x0 = h0[g], x1 = h1[g];
           c[nt][0] *= 1.f - x0 * x0;
           c[nt][1] *= 1.f - x1 * x1;
           p0[ra] = c[nt][0];
@@ -641,7 +668,7 @@ __global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kerne
           c[nt][0] = c[nt][1] = 0.f;
         }
         if (vb) {
-          const float x0 = h0[rb], x1 = h1[rb];
+          const float x0 = h0[g + 8], x1 = h1[g + 8];
           c[nt][2] *= 1.f - x0 * x0;
           c[nt][3] *= 1.f - x1 * x1;
           p0[rb] = c[nt][2];
@@ -1231,9 +1258,11 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
     const int smem_img = decode_image_in_smem();
     const size_t smem_full = sizeof(float) * dbw_image_floats(n);
     VSX_REQUIRE(smem_full <= 113 * 1024, "decode_bwd: n=%d too large for the mma weight image", n);
+    const size_t stage = sizeof(float) * (size_t)kDbwWarps * dbw_stage_floats(n);
     VSX_CUDA_TRY(cudaFuncSetAttribute(decode_bwd_anchor_mma_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full));
-    const size_t smem = smem_img ? smem_full : 0;
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(smem_full + stage)));
+    const size_t smem = (smem_img ? smem_full : 0) + stage;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
