@@ -277,15 +277,44 @@ __global__ void bin_emit_kernel(const vsx_splat *__restrict__ rec,
 // Per sorted splat: screen-space grads (mean2d 2, conic 3, opacity, color 3,
 // normal 3, plane_d) -> gaussian grads, float64 internally. Writes (=) into
 // the batch-order outputs at rec.src; culled gaussians keep the caller's zeros.
+// kBatch = false: thread per sorted splat r, scattering into batch index
+// rec[r].src (culled gaussians keep the caller's zeros). kBatch = true: thread
+// per batch gaussian i with its sorted rank inv[i] (-1 = culled -> zeros), so
+// the per-gaussian inputs and all six outputs are read / written in order and
+// only the 64-byte record and the 13-float gradient row are gathered.
+template <bool kBatch>
 __global__ void __launch_bounds__(128) project_bwd_kernel(
     const double *__restrict__ means, const float *__restrict__ scale,
     const float *__restrict__ quat, const float *__restrict__ normal,
     const vsx_splat *__restrict__ rec, const float *__restrict__ gs, int32_t n, vsx_camera cam,
     float *__restrict__ g_means, float *__restrict__ g_opacity, float *__restrict__ g_color,
-    float *__restrict__ g_scale, float *__restrict__ g_quat, float *__restrict__ g_normal) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const uint32_t i = rec[r].src;
+    float *__restrict__ g_scale, float *__restrict__ g_quat, float *__restrict__ g_normal,
+    const int32_t *__restrict__ inv, int32_t n_batch) {
+  int r;
+  uint32_t i;
+  if (kBatch) {
+    const int ib = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ib >= n_batch) return;
+    i = (uint32_t)ib;
+    r = inv[ib];
+    if (r < 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        g_means[3 * i + k] = 0.f;
+        g_color[3 * i + k] = 0.f;
+        g_scale[3 * i + k] = 0.f;
+        g_normal[3 * i + k] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) g_quat[4 * i + k] = 0.f;
+      g_opacity[i] = 0.f;
+      return;
+    }
+  } else {
+    r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    i = rec[r].src;
+  }
   const float *G = gs + (size_t)13 * r;
   const double mu[3] = {means[3 * i + 0], means[3 * i + 1], means[3 * i + 2]};
   const float *sc = scale + 3 * i;
@@ -388,6 +417,12 @@ __global__ void __launch_bounds__(128) project_bwd_kernel(
   g_color[3 * i + 0] = G[6];
   g_color[3 * i + 1] = G[7];
   g_color[3 * i + 2] = G[8];
+}
+
+__global__ void splat_rank_kernel(const vsx_splat *__restrict__ rec, int32_t n,
+                                  int32_t *__restrict__ inv) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) inv[rec[r].src] = r;
 }
 
 }  // namespace vsx
@@ -504,9 +539,30 @@ extern "C" int vsx_project_bwd(const double *means, const float *scale, const fl
                                float *g_means, float *g_opacity, float *g_color, float *g_scale,
                                float *g_quat, float *g_normal, vsx_stream s) {
   if (n_sorted <= 0) return VSX_OK;
-  project_bwd_kernel<<<grid_for(n_sorted, 128), 128, 0, as_stream(s)>>>(
+  project_bwd_kernel<false><<<grid_for(n_sorted, 128), 128, 0, as_stream(s)>>>(
       means, scale, quat, normal, rec_sorted, grad_splat, n_sorted, cam, g_means, g_opacity,
-      g_color, g_scale, g_quat, g_normal);
+      g_color, g_scale, g_quat, g_normal, nullptr, 0);
+  VSX_LAUNCH_CHECK("project_bwd");
+  return VSX_OK;
+}
+
+extern "C" int vsx_project_bwd_batch(const double *means, const float *scale, const float *quat,
+                                     const float *normal, const vsx_splat *rec_sorted,
+                                     const float *grad_splat, int32_t n_sorted, int32_t n_batch,
+                                     vsx_camera cam, float *g_means, float *g_opacity,
+                                     float *g_color, float *g_scale, float *g_quat,
+                                     float *g_normal, int32_t *inv_ws, vsx_stream s) {
+  VSX_REQUIRE(n_sorted >= 0 && n_batch >= n_sorted && inv_ws, "project_bwd_batch: bad args");
+  if (n_batch == 0) return VSX_OK;
+  cudaStream_t st = as_stream(s);
+  VSX_CUDA_TRY(cudaMemsetAsync(inv_ws, 0xFF, sizeof(int32_t) * n_batch, st));
+  if (n_sorted > 0) {
+    splat_rank_kernel<<<grid_for(n_sorted, 256), 256, 0, st>>>(rec_sorted, n_sorted, inv_ws);
+    VSX_LAUNCH_CHECK("splat_rank");
+  }
+  project_bwd_kernel<true><<<grid_for(n_batch, 128), 128, 0, st>>>(
+      means, scale, quat, normal, rec_sorted, grad_splat, n_sorted, cam, g_means, g_opacity,
+      g_color, g_scale, g_quat, g_normal, inv_ws, n_batch);
   VSX_LAUNCH_CHECK("project_bwd");
   return VSX_OK;
 }

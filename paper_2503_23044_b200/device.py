@@ -477,15 +477,17 @@ def project_backward(means, scale, quat, normal, P: Projected, grad_splat: torch
                      view: CameraView):
     g = int(means.shape[0])
     dev = "cuda"
-    gm = torch.zeros((g, 3), dtype=torch.float32, device=dev)
-    go = torch.zeros(g, dtype=torch.float32, device=dev)
-    gc = torch.zeros((g, 3), dtype=torch.float32, device=dev)
-    gs = torch.zeros((g, 3), dtype=torch.float32, device=dev)
-    gq = torch.zeros((g, 4), dtype=torch.float32, device=dev)
-    gn = torch.zeros((g, 3), dtype=torch.float32, device=dev)
-    call("vsx_project_bwd", ptr(means), ptr(scale), ptr(quat), ptr(normal), ptr(P.rec),
-         ptr(grad_splat), P.count, view.to_abi(), ptr(gm), ptr(go), ptr(gc), ptr(gs), ptr(gq),
-         ptr(gn), stream())
+    # batch-order kernel: every row written (zeros for culled gaussians)
+    gm = torch.empty((g, 3), dtype=torch.float32, device=dev)
+    go = torch.empty(g, dtype=torch.float32, device=dev)
+    gc = torch.empty((g, 3), dtype=torch.float32, device=dev)
+    gs = torch.empty((g, 3), dtype=torch.float32, device=dev)
+    gq = torch.empty((g, 4), dtype=torch.float32, device=dev)
+    gn = torch.empty((g, 3), dtype=torch.float32, device=dev)
+    inv = torch.empty(max(g, 1), dtype=torch.int32, device=dev)
+    call("vsx_project_bwd_batch", ptr(means), ptr(scale), ptr(quat), ptr(normal), ptr(P.rec),
+         ptr(grad_splat), P.count, g, view.to_abi(), ptr(gm), ptr(go), ptr(gc), ptr(gs),
+         ptr(gq), ptr(gn), ptr(inv), stream())
     return {"means": gm, "opacities": go, "colors": gc, "scales": gs, "quats": gq, "normals": gn}
 
 
