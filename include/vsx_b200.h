@@ -290,13 +290,14 @@ int vsx_project_bwd(const double *means, const float *scale, const float *quat,
                     vsx_stream s);
 /* Same gradients in batch order: thread per decoded gaussian with its sorted
  * rank (inv_ws: n_batch int32 scratch); writes every output row, zeros for
- * gaussians culled by the projection (no zero-initialised outputs needed). */
+ * gaussians culled by the projection (no zero-initialised outputs needed).
+ * src_sorted (optional) = the records' src field as a dense int32 array. */
 int vsx_project_bwd_batch(const double *means, const float *scale, const float *quat,
                           const float *normal, const vsx_splat *rec_sorted,
                           const float *grad_splat, int32_t n_sorted, int32_t n_batch,
                           vsx_camera cam, float *g_means, float *g_opacity, float *g_color,
-                          float *g_scale, float *g_quat, float *g_normal, int32_t *inv_ws,
-                          vsx_stream s);
+                          float *g_scale, float *g_quat, float *g_normal,
+                          const int32_t *src_sorted, int32_t *inv_ws, vsx_stream s);
 
 /* ---- K8: decode backward ------------------------------------------------ */
 /* Per-gaussian grads -> decoder weight grads (+=) and per-anchor grads (+=)

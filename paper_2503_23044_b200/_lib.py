@@ -85,8 +85,8 @@ _SIGS = {
     "vsx_raster_fwd": ([P, P, P, VsxCamera, P, P, P, P, P, P, P, P, P], c_i32),
     "vsx_raster_bwd": ([P, P, P, VsxCamera, P, P, P, P, P, P, P, P, P, P, P, P, P], c_i32),
     "vsx_project_bwd": ([P, P, P, P, P, P, c_i32, VsxCamera, P, P, P, P, P, P, P], c_i32),
-    "vsx_project_bwd_batch": ([P, P, P, P, P, P, c_i32, c_i32, VsxCamera, P, P, P, P, P, P, P, P],
-                              c_i32),
+    "vsx_project_bwd_batch": ([P, P, P, P, P, P, c_i32, c_i32, VsxCamera, P, P, P, P, P, P, P, P,
+                               P], c_i32),
     "vsx_l1_loss": ([P, P, c_i64, c_f32, P, P, P], c_i32),
     "vsx_depth_loss": ([P, P, P, P, c_i64, P, P, P, P, P], c_i32),
     "vsx_adam": ([P, P, P, P, c_i32, P, P, c_f64, c_f64, c_f64, c_i32, P], c_i32),

@@ -419,10 +419,11 @@ __global__ void __launch_bounds__(128) project_bwd_kernel(
   g_color[3 * i + 2] = G[8];
 }
 
-__global__ void splat_rank_kernel(const vsx_splat *__restrict__ rec, int32_t n,
+__global__ void splat_rank_kernel(const vsx_splat *__restrict__ rec,
+                                  const int32_t *__restrict__ src, int32_t n,
                                   int32_t *__restrict__ inv) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n) inv[rec[r].src] = r;
+  if (r < n) inv[src ? (uint32_t)src[r] : rec[r].src] = r;
 }
 
 }  // namespace vsx
@@ -551,13 +552,15 @@ extern "C" int vsx_project_bwd_batch(const double *means, const float *scale, co
                                      const float *grad_splat, int32_t n_sorted, int32_t n_batch,
                                      vsx_camera cam, float *g_means, float *g_opacity,
                                      float *g_color, float *g_scale, float *g_quat,
-                                     float *g_normal, int32_t *inv_ws, vsx_stream s) {
+                                     float *g_normal, const int32_t *src_sorted, int32_t *inv_ws,
+                                     vsx_stream s) {
   VSX_REQUIRE(n_sorted >= 0 && n_batch >= n_sorted && inv_ws, "project_bwd_batch: bad args");
   if (n_batch == 0) return VSX_OK;
   cudaStream_t st = as_stream(s);
   VSX_CUDA_TRY(cudaMemsetAsync(inv_ws, 0xFF, sizeof(int32_t) * n_batch, st));
   if (n_sorted > 0) {
-    splat_rank_kernel<<<grid_for(n_sorted, 256), 256, 0, st>>>(rec_sorted, n_sorted, inv_ws);
+    splat_rank_kernel<<<grid_for(n_sorted, 256), 256, 0, st>>>(rec_sorted, src_sorted, n_sorted,
+                                                                inv_ws);
     VSX_LAUNCH_CHECK("splat_rank");
   }
   project_bwd_kernel<true><<<grid_for(n_batch, 128), 128, 0, st>>>(

@@ -487,7 +487,7 @@ def project_backward(means, scale, quat, normal, P: Projected, grad_splat: torch
     inv = torch.empty(max(g, 1), dtype=torch.int32, device=dev)
     call("vsx_project_bwd_batch", ptr(means), ptr(scale), ptr(quat), ptr(normal), ptr(P.rec),
          ptr(grad_splat), P.count, g, view.to_abi(), ptr(gm), ptr(go), ptr(gc), ptr(gs),
-         ptr(gq), ptr(gn), ptr(inv), stream())
+         ptr(gq), ptr(gn), ptr(P.src if P.src.dtype == torch.int32 else None), ptr(inv), stream())
     return {"means": gm, "opacities": go, "colors": gc, "scales": gs, "quats": gq, "normals": gn}
 
 
