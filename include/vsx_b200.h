@@ -190,7 +190,8 @@ int vsx_gather_splats(const vsx_splat *rec, const double *radius, const uint32_t
  * instead and passes NULL). */
 int vsx_bin_count(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
                   int32_t height, uint32_t *splat_tiles, uint32_t *tile_counts, vsx_stream s);
-/* Phase 2: emit (tile, rank) pairs at exclusive-scan offsets of splat_tiles. */
+/* Phase 2: emit (tile, rank) pairs at exclusive-scan offsets of splat_tiles
+ * (splat_offsets has n+1 entries, the total last). */
 int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
                  int32_t height, const uint32_t *splat_offsets, uint32_t *isect_tile,
                  uint32_t *isect_rank, vsx_stream s);

@@ -238,6 +238,52 @@ __global__ void tile_ranges_kernel(const uint32_t *__restrict__ keys, int64_t n,
   tile_off[t] = (uint32_t)(t == T ? n : lo);
 }
 
+// Block-cooperative emission: a CTA owns 256 consecutive splats; their pair
+// offsets come from the global exclusive scan, so thread t emits pairs
+// t, t+256, ... of the CTA's range (consecutive threads -> consecutive
+// addresses, every lane busy), locating its splat by binary search over the
+// CTA's 257 local offsets in shared memory. Row-major tile order inside a
+// splat and splat order across pairs are the reference's (renderer.py:216-226).
+__global__ void __launch_bounds__(256) bin_emit_block_kernel(
+    const vsx_splat *__restrict__ rec, const double *__restrict__ radius, int32_t n, int txn,
+    int tyn, const uint32_t *__restrict__ offs, uint32_t *__restrict__ tiles,
+    uint32_t *__restrict__ ranks) {
+  __shared__ uint32_t s_off[257];
+  __shared__ int s_x0[256], s_y0[256], s_w[256];
+  __shared__ float s_iw[256];
+  const int t = threadIdx.x;
+  const int s0 = blockIdx.x * 256;
+  const int i = s0 + t;
+  int x0 = 0, x1 = -1, y0 = 0, y1 = -1;
+  bool ok = false;
+  if (i < n) ok = tile_rect(rec[i].mean2d[0], rec[i].mean2d[1], radius[i], txn, tyn, x0, x1, y0, y1);
+  const int w = ok ? x1 - x0 + 1 : 1;
+  const uint32_t base = offs[s0];
+  s_x0[t] = x0;
+  s_y0[t] = y0;
+  s_w[t] = w;
+  s_iw[t] = 1.0f / (float)w;
+  s_off[t] = offs[min(i, n)] - base;
+  if (t == 0) s_off[256] = offs[min(s0 + 256, n)] - base;
+  __syncthreads();
+  const uint32_t total = s_off[256];
+  for (uint32_t q = t; q < total; q += 256) {
+    int lo = 0, hi = 255;  // largest k with s_off[k] <= q
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_off[mid] <= q) lo = mid;
+      else hi = mid - 1;
+    }
+    const int k = lo;
+    const int e = (int)(q - s_off[k]);
+    // e / w via the float reciprocal: exact for e < 2^22 (see tile_row)
+    const int row = __float2int_rz(((float)e + 0.5f) * s_iw[k]);
+    const int col = e - row * s_w[k];
+    tiles[base + q] = (uint32_t)((s_y0[k] + row) * txn + s_x0[k] + col);
+    ranks[base + q] = (uint32_t)(s0 + k);
+  }
+}
+
 __global__ void bin_emit_kernel(const vsx_splat *__restrict__ rec,
                                 const double *__restrict__ radius, int32_t n, int txn, int tyn,
                                 const uint32_t *__restrict__ offs, uint32_t *__restrict__ tiles,
@@ -474,9 +520,17 @@ extern "C" int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t 
   VSX_REQUIRE(width > 0 && height > 0 && n >= 0, "bin_emit: bad arguments");
   if (n == 0) return VSX_OK;
   const int txn = (width + kTile - 1) / kTile, tyn = (height + kTile - 1) / kTile;
-  bin_emit_kernel<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(rec, radius, n, txn, tyn,
-                                                              splat_offsets, isect_tile,
-                                                              isect_rank);  // whole warps
+  static const bool warp_emit = [] {  // VSX_BIN_EMIT=warp: the warp-walk kernel (A/B)
+    const char *e = getenv("VSX_BIN_EMIT");
+    return e && e[0] == 'w';
+  }();
+  if (warp_emit)
+    bin_emit_kernel<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(rec, radius, n, txn, tyn,
+                                                                splat_offsets, isect_tile,
+                                                                isect_rank);  // whole warps
+  else
+    bin_emit_block_kernel<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(
+        rec, radius, n, txn, tyn, splat_offsets, isect_tile, isect_rank);
   VSX_LAUNCH_CHECK("bin_emit");
   return VSX_OK;
 }
