@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
     const float *__restrict__ quat, const float *__restrict__ normal, int32_t n, vsx_camera cam,
     vsx_splat *__restrict__ rec, uint64_t *__restrict__ zkey, double *__restrict__ radius,
     uint32_t *__restrict__ n_kept, int32_t *__restrict__ status) {
+  __shared__ float4 s_rec[4 * 256];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   bool keep = false;
   if (i < n) {
@@ -122,23 +123,41 @@ __global__ void __launch_bounds__(256) project_fwd_kernel(
       r.normal[2] = (float)nc[2];
       r.plane_d = (float)(nc[0] * x + nc[1] * y + nc[2] * z);
       r.src = (uint32_t)i;
-      rec[i] = r;
+      union {
+        vsx_splat s;
+        float4 v[4];
+      } u;
+      u.s = r;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s_rec[4 * threadIdx.x + k] = u.v[k];
       zkey[i] = (uint64_t)__double_as_longlong(z);
     }
   }
   const unsigned ball = __ballot_sync(0xffffffffu, keep);
   if ((threadIdx.x & 31) == 0 && ball) atomicAdd(n_kept, (uint32_t)__popc(ball));
+  // records leave through shared memory as one contiguous run per CTA
+  // (consecutive lanes, consecutive 16-byte pieces); the slots of culled
+  // gaussians carry stale bytes, never read (they sort behind n_kept)
+  __syncthreads();
+  const int64_t b0 = (int64_t)blockIdx.x * blockDim.x;
+  const int nb = (int)min((int64_t)blockDim.x, (int64_t)n - b0);
+  float4 *out4 = reinterpret_cast<float4 *>(rec) + 4 * b0;
+  for (int e = threadIdx.x; e < 4 * nb; e += blockDim.x) out4[e] = s_rec[e];
 }
 
 __global__ void gather_splats_kernel(const vsx_splat *__restrict__ rec,
                                      const double *__restrict__ radius,
                                      const uint32_t *__restrict__ order, int32_t n,
                                      vsx_splat *__restrict__ out, double *__restrict__ rout) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // four threads per 64-byte record, one 16-byte piece each: full-line
+  // gathers and fully coalesced stores
+  const int64_t tq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = tq >> 2;
+  const int part = (int)(tq & 3);
   if (i >= n) return;
   const uint32_t j = order[i];
-  out[i] = rec[j];
-  rout[i] = radius[j];
+  reinterpret_cast<float4 *>(out)[4 * i + part] = __ldg(reinterpret_cast<const float4 *>(rec) + 4 * (int64_t)j + part);
+  if (part == 0) rout[i] = radius[j];
 }
 
 // Tile rectangle of a splat (renderer.py:216-221), float64 floor semantics.
@@ -494,8 +513,8 @@ extern "C" int vsx_gather_splats(const vsx_splat *rec, const double *radius,
                                  const uint32_t *order, int32_t n, vsx_splat *rec_sorted,
                                  double *radius_sorted, vsx_stream s) {
   if (n <= 0) return VSX_OK;
-  gather_splats_kernel<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(rec, radius, order, n,
-                                                                   rec_sorted, radius_sorted);
+  gather_splats_kernel<<<grid_for((int64_t)4 * n, 256), 256, 0, as_stream(s)>>>(
+      rec, radius, order, n, rec_sorted, radius_sorted);
   VSX_LAUNCH_CHECK("gather_splats");
   return VSX_OK;
 }
