@@ -117,6 +117,13 @@ int vsx_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, void *ws, size_t 
  * flags & VSX_SORT_SKIP_CONSTANT: first reduce OR/AND of the keys and skip
  * 8-bit digits that are identical for every key (costs one host sync). */
 #define VSX_SORT_SKIP_CONSTANT 1
+/* flags & VSX_SORT_HIST_IN_WS: the per-pass digit histograms (pass p at
+ * u32 [256 p, 256 p + 256)) are already in the workspace at
+ * vsx_sort_hist_offset(n) (a producer such as vsx_bin_emit_hist built them);
+ * the sort skips its own histogram read. Passes are every 8 bits of
+ * [begin_bit, end_bit). */
+#define VSX_SORT_HIST_IN_WS 2
+size_t vsx_sort_hist_offset(int64_t n);
 int vsx_sort_pairs_u64(const uint64_t *keys_in, const uint32_t *vals_in, uint64_t *keys_out,
                        uint32_t *vals_out, int64_t n, int32_t begin_bit, int32_t end_bit,
                        int32_t flags, void *ws, size_t ws_bytes, vsx_stream s);
@@ -195,6 +202,13 @@ int vsx_bin_count(const vsx_splat *rec, const double *radius, int32_t n, int32_t
 int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
                  int32_t height, const uint32_t *splat_offsets, uint32_t *isect_tile,
                  uint32_t *isect_rank, vsx_stream s);
+/* Phase 2 with the tile-key digit histograms of both radix passes (bits
+ * [0, 8) and [8, 16)) accumulated on the fly into hist (2 x 256 u32, zeroed
+ * here): the following vsx_sort_pairs_u32(..., VSX_SORT_HIST_IN_WS) skips
+ * its histogram read of the 8-byte pairs. */
+int vsx_bin_emit_hist(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
+                      int32_t height, const uint32_t *splat_offsets, uint32_t *isect_tile,
+                      uint32_t *isect_rank, uint32_t *hist, vsx_stream s);
 /* Phase 3: CSR tile offsets (num_tiles+1) from the tile-sorted keys
  * (lower_bound per tile; no atomics). */
 int vsx_tile_ranges(const uint32_t *sorted_tiles, int64_t n, int32_t num_tiles,

@@ -82,6 +82,8 @@ _SIGS = {
     "vsx_gather_splats": ([P, P, P, c_i32, P, P, P], c_i32),
     "vsx_bin_count": ([P, P, c_i32, c_i32, c_i32, P, P, P], c_i32),
     "vsx_bin_emit": ([P, P, c_i32, c_i32, c_i32, P, P, P, P], c_i32),
+    "vsx_bin_emit_hist": ([P, P, c_i32, c_i32, c_i32, P, P, P, P, P], c_i32),
+    "vsx_sort_hist_offset": ([c_i64], ctypes.c_size_t),
     "vsx_raster_fwd": ([P, P, P, VsxCamera, P, P, P, P, P, P, P, P, P], c_i32),
     "vsx_raster_bwd": ([P, P, P, VsxCamera, P, P, P, P, P, P, P, P, P, P, P, P, P], c_i32),
     "vsx_project_bwd": ([P, P, P, P, P, P, c_i32, VsxCamera, P, P, P, P, P, P, P], c_i32),

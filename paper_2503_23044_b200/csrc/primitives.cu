@@ -464,12 +464,15 @@ static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout
   OsShifts sh{};
   sh.np = np;
   for (int p = 0; p < np; ++p) sh.s[p] = shifts[p];
-  // gh and the counters are contiguous: one memset clears both
-  VSX_CUDA_TRY(cudaMemsetAsync(w.gh, 0, sizeof(uint32_t) * 16 * 256, st));
   VSX_CUDA_TRY(cudaMemsetAsync(w.counter, 0, sizeof(uint32_t) * 16, st));
-  os_hist_kernel<K><<<(unsigned)std::min<int64_t>(grid_for(n, 256), 8 * 148), 256, 0, st>>>(
-      kin, n, sh, w.gh);
-  VSX_LAUNCH_CHECK("os_hist");
+  if (!(flags & VSX_SORT_HIST_IN_WS)) {
+    VSX_CUDA_TRY(cudaMemsetAsync(w.gh, 0, sizeof(uint32_t) * 16 * 256, st));
+    os_hist_kernel<K><<<(unsigned)std::min<int64_t>(grid_for(n, 256), 8 * 148), 256, 0, st>>>(
+        kin, n, sh, w.gh);
+    VSX_LAUNCH_CHECK("os_hist");
+  } else {
+    VSX_REQUIRE(!(flags & VSX_SORT_SKIP_CONSTANT), "sort: HIST_IN_WS excludes SKIP_CONSTANT");
+  }
   for (int p = 0; p < np; ++p) {
     const bool to_out = ((np - 1 - p) % 2) == 0;
     K *dk = to_out ? kout : alt_k;
@@ -660,6 +663,10 @@ extern "C" int vsx_sort_pairs_u64(const uint64_t *keys_in, const uint32_t *vals_
                                   size_t ws_bytes, vsx_stream s) {
   return sort_pairs<uint64_t>(keys_in, vals_in, keys_out, vals_out, n, begin_bit, end_bit, flags,
                               ws, ws_bytes, as_stream(s));
+}
+
+extern "C" size_t vsx_sort_hist_offset(int64_t n) {
+  return align256(sizeof(uint64_t) * n) + align256(sizeof(uint32_t) * n);
 }
 
 extern "C" int vsx_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_in,

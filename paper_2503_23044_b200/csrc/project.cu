@@ -266,8 +266,13 @@ __global__ void tile_ranges_kernel(const uint32_t *__restrict__ keys, int64_t n,
 __global__ void __launch_bounds__(256) bin_emit_block_kernel(
     const vsx_splat *__restrict__ rec, const double *__restrict__ radius, int32_t n, int txn,
     int tyn, const uint32_t *__restrict__ offs, uint32_t *__restrict__ tiles,
-    uint32_t *__restrict__ ranks) {
+    uint32_t *__restrict__ ranks, uint32_t *__restrict__ hist) {
   __shared__ uint32_t s_off[257];
+  __shared__ uint32_t s_h[2][256];  // digit histograms of the two radix passes
+  if (hist) {
+    s_h[0][threadIdx.x] = 0u;
+    s_h[1][threadIdx.x] = 0u;
+  }
   __shared__ int s_x0[256], s_y0[256], s_w[256];
   __shared__ float s_iw[256];
   const int t = threadIdx.x;
@@ -298,8 +303,23 @@ __global__ void __launch_bounds__(256) bin_emit_block_kernel(
     // e / w via the float reciprocal: exact for e < 2^22 (see tile_row)
     const int row = __float2int_rz(((float)e + 0.5f) * s_iw[k]);
     const int col = e - row * s_w[k];
-    tiles[base + q] = (uint32_t)((s_y0[k] + row) * txn + s_x0[k] + col);
+    const uint32_t tile = (uint32_t)((s_y0[k] + row) * txn + s_x0[k] + col);
+    tiles[base + q] = tile;
     ranks[base + q] = (uint32_t)(s0 + k);
+    if (hist) {
+      // low digit: consecutive tiles, few collisions; high digit: one tile row
+      // shares it, so the lanes of a warp aggregate first
+      atomicAdd(&s_h[0][tile & 255u], 1u);
+      const uint32_t hi = (tile >> 8) & 255u;
+      const unsigned peers = __match_any_sync(__activemask(), hi);
+      if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&s_h[1][hi], __popc(peers));
+    }
+  }
+  if (hist) {
+    __syncthreads();
+    const uint32_t a = s_h[0][threadIdx.x], b = s_h[1][threadIdx.x];
+    if (a) atomicAdd(hist + threadIdx.x, a);
+    if (b) atomicAdd(hist + 256 + threadIdx.x, b);
   }
 }
 
@@ -549,8 +569,24 @@ extern "C" int vsx_bin_emit(const vsx_splat *rec, const double *radius, int32_t 
                                                                 isect_rank);  // whole warps
   else
     bin_emit_block_kernel<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(
-        rec, radius, n, txn, tyn, splat_offsets, isect_tile, isect_rank);
+        rec, radius, n, txn, tyn, splat_offsets, isect_tile, isect_rank, nullptr);
   VSX_LAUNCH_CHECK("bin_emit");
+  return VSX_OK;
+}
+
+extern "C" int vsx_bin_emit_hist(const vsx_splat *rec, const double *radius, int32_t n,
+                                 int32_t width, int32_t height, const uint32_t *splat_offsets,
+                                 uint32_t *isect_tile, uint32_t *isect_rank, uint32_t *hist,
+                                 vsx_stream s) {
+  VSX_REQUIRE(width > 0 && height > 0 && n >= 0 && hist, "bin_emit_hist: bad arguments");
+  const int txn = (width + kTile - 1) / kTile, tyn = (height + kTile - 1) / kTile;
+  VSX_REQUIRE((int64_t)txn * tyn <= 65536, "bin_emit_hist: more than 2^16 tiles");
+  cudaStream_t st = as_stream(s);
+  VSX_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2 * 256, st));
+  if (n == 0) return VSX_OK;
+  bin_emit_block_kernel<<<grid_for(n, 256), 256, 0, st>>>(rec, radius, n, txn, tyn, splat_offsets,
+                                                          isect_tile, isect_rank, hist);
+  VSX_LAUNCH_CHECK("bin_emit_hist");
   return VSX_OK;
 }
 

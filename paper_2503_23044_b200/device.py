@@ -8,6 +8,7 @@ built library) every entry point raises.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -67,6 +68,7 @@ def _u32(n: int) -> torch.Tensor:
 # ------------------------------------------------------------------ primitives
 
 SORT_SKIP_CONSTANT = 1
+SORT_HIST_IN_WS = 2
 
 
 def sort_pairs_u64(keys: torch.Tensor, vals: torch.Tensor, n: int, skip_constant: bool = True):
@@ -397,10 +399,22 @@ def bin_tiles(P: Projected, width: int, height: int) -> Bins:
                     torch.empty(0, dtype=torch.int32, device="cuda"), txn, tyn)
     tiles = torch.empty(total, dtype=torch.int32, device="cuda")
     ranks = torch.empty(total, dtype=torch.int32, device="cuda")
-    call("vsx_bin_emit", ptr(P.rec), ptr(P.radius), n, width, height, ptr(soff), ptr(tiles),
-         ptr(ranks), stream())
     bits = max(1, math.ceil(math.log2(T))) if T > 1 else 1
-    skeys, lst = sort_pairs_u32(tiles, ranks, total, bits)
+    lib = _lib.load()
+    if T <= 65536:
+        # the emission builds the sort's digit histograms on the fly
+        wp, wb = workspace().get(lib.vsx_sort_ws_bytes(total))
+        hist = ctypes.c_void_p(wp.value + int(lib.vsx_sort_hist_offset(total)))
+        call("vsx_bin_emit_hist", ptr(P.rec), ptr(P.radius), n, width, height, ptr(soff),
+             ptr(tiles), ptr(ranks), hist, stream())
+        skeys = torch.empty_like(tiles)
+        lst = torch.empty_like(ranks)
+        call("vsx_sort_pairs_u32", ptr(tiles), ptr(ranks), ptr(skeys), ptr(lst), total, 0, bits,
+             SORT_HIST_IN_WS, wp, wb, stream())
+    else:
+        call("vsx_bin_emit", ptr(P.rec), ptr(P.radius), n, width, height, ptr(soff),
+             ptr(tiles), ptr(ranks), stream())
+        skeys, lst = sort_pairs_u32(tiles, ranks, total, bits)
     toff = torch.empty(T + 1, dtype=torch.int32, device="cuda")
     call("vsx_tile_ranges", ptr(skeys), total, T, ptr(toff), stream())
     return Bins(toff, lst, txn, tyn)
