@@ -15,11 +15,11 @@
  *   vsx_project_fwd                renderer.py:144-204 project_splats (EWA + (z,gid) order)
  *   vsx_sort_splats_z              renderer.py:197 np.lexsort((gid, z)) (float32 proxy radix
  *                                  sort + exact run fix-up); vsx_sort_pairs_u64/_u32 generic
- *   vsx_bin_count / vsx_bin_emit / vsx_tile_ranges
+ *   vsx_bin_count / vsx_bin_emit(_hist) / vsx_tile_ranges
  *                                  renderer.py:207-226 bin_splats
  *   vsx_raster_fwd(_loss)          renderer.py:242-301 _blend_padded + _finalize, :390-449 rasterize_view
  *   vsx_raster_bwd(_loss)          renderer.py:347-367 rasterize_backward (autograd of the blend)
- *   vsx_project_bwd                autograd of project_splats (trainer.py:330)
+ *   vsx_project_bwd(_batch)        autograd of project_splats (trainer.py:330)
  *   vsx_decode_bwd                 decoder.py:267-292 decoder_backward (autograd of decode)
  *   vsx_l1_loss / vsx_depth_loss   losses.py:43-53 bl_rgb_loss, losses.py:65-84 e_depth_loss
  *   vsx_adam / vsx_adam_guarded    trainer.py:220-247 TrainState._adam + apply_*_grads
