@@ -24,7 +24,11 @@
 // onto the tensor cores (mma.sync tf32, 3xTF32 split): the per-(pixel, splat)
 // cotangent dot s = F[p] . P[j] before phase 1, and phase 2's per-splat sums,
 // which are two [kBC x 256] x [256 x 8] GEMMs. Records are prefetched one
-// chunk ahead with cp.async. VSX_RASTER_BWD="NS,BC" with NS > 0 selects v2.
+// chunk ahead with cp.async. Each chunk costs two CTA barriers: the next
+// chunk is staged right after phase 2 (double-buffered), so the epilogue's
+// atomics overlap the next chunk's phases 0/1 (1545 -> 1507 us per 1080p
+// view; -DVSX_BWD_MERGED=0 restores the three-barrier schedule for A/B).
+// VSX_RASTER_BWD="NS,BC" with NS > 0 selects v2.
 #include "raster_common.cuh"
 
 namespace vsx {
@@ -255,6 +259,21 @@ __device__ __forceinline__ float falloff_alpha(const float4 &p0, const float4 &p
   return fminf(__fmul_rn(p1.y, ex2_ftz(fminf(p2, 0.f))), 0.99f);
 }
 
+__device__ __forceinline__ void copy_splat_async(vsx_splat *dst, const vsx_splat *src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * k),
+                 "l"(reinterpret_cast<const char *>(src) + 16 * k)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 template <int PX, int U>
 __global__ void __launch_bounds__(256 / PX) raster_fwd2_kernel(
     const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
@@ -365,21 +384,6 @@ __device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ void copy_splat_async(vsx_splat *dst, const vsx_splat *src) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * k),
-                 "l"(reinterpret_cast<const char *>(src) + 16 * k)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // tf32 by truncation: one LOP3 (cvt.rna.tf32 is a 4-instruction sequence on
@@ -719,6 +723,9 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
 // a_hi + a_lo. Warps split (m-tile, plane, k-range); the KSPLIT partial sums
 // meet in shared memory and one 8-lane group per splat forms its 13
 // gradients (same polynomials as v2) and issues the atomics.
+#ifndef VSX_BWD_MERGED
+#define VSX_BWD_MERGED 1
+#endif
 constexpr int kPlaneStride = kTilePixels + 4;  // 4 mod 32: conflict-free A fragments
 
 // pixel moment m of tile pixel p (x, y about the tile centre)
@@ -831,34 +838,45 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     const uint32_t cs2 = chunk_lo(cs);
     if (cs > begin && t < (int)(cs - cs2)) nr = a.tile_list[cs2 + t];
   }
-  for (uint32_t ce = stop; ce > begin; buf ^= 1) {
-    const uint32_t cs = chunk_lo(ce);
-    const int cnt = (int)(ce - cs);
+  // Stage chunk [cs_, cs_ + cnt_) into buffer sb from its in-flight copy and
+  // start the copy of the chunk after it.
+  auto stage = [&](int sb, uint32_t cs_, int cnt_) {
     cp_async_wait_all();
-    if (t < cnt) {
-      s_rank[buf][t] = rr;
-      const vsx_splat &sp = s_raw[buf][t];
-      stage_splat(sp, ox, oy, s0[buf][t], s1[buf][t], s2[buf][t], s3[buf][t]);
+    if (t < cnt_) {
+      s_rank[sb][t] = rr;
+      const vsx_splat &sp = s_raw[sb][t];
+      stage_splat(sp, ox, oy, s0[sb][t], s1[sb][t], s2[sb][t], s3[sb][t]);
       const float pv[8] = {sp.color[0], sp.color[1], sp.color[2], sp.normal[0],
                            sp.normal[1], sp.normal[2], sp.plane_d, 1.f};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float h0 = __uint_as_float(tf32_bits(pv[k])), h1 = __uint_as_float(tf32_bits(pv[k + 4]));
-        s_ph[buf][t][k] = make_float4(h0, h1, __uint_as_float(tf32_bits(pv[k] - h0)),
-                                      __uint_as_float(tf32_bits(pv[k + 4] - h1)));
+        s_ph[sb][t][k] = make_float4(h0, h1, __uint_as_float(tf32_bits(pv[k] - h0)),
+                                     __uint_as_float(tf32_bits(pv[k + 4] - h1)));
       }
     }
-    {
-      const uint32_t cs2 = chunk_lo(cs);
-      if (cs > begin && t < (int)(cs - cs2)) {
-        rr = nr;
-        copy_splat_async(&s_raw[buf ^ 1][t], a.rec + nr);
-      }
-      cp_async_commit();
-      const uint32_t cs3 = chunk_lo(cs2);
-      if (cs2 > begin && t < (int)(cs2 - cs3)) nr = a.tile_list[cs3 + t];
+    const uint32_t cs2 = chunk_lo(cs_);
+    if (cs_ > begin && t < (int)(cs_ - cs2)) {
+      rr = nr;
+      copy_splat_async(&s_raw[sb ^ 1][t], a.rec + nr);
     }
+    cp_async_commit();
+    const uint32_t cs3 = chunk_lo(cs2);
+    if (cs2 > begin && t < (int)(cs2 - cs3)) nr = a.tile_list[cs3 + t];
+  };
+#if VSX_BWD_MERGED
+  // Two barriers per chunk: the next chunk is staged (double-buffered) right
+  // after phase 2, so the epilogue's atomics overlap the next chunk's phase 0/1.
+  if (stop > begin) stage(0, chunk_lo(stop), (int)(stop - chunk_lo(stop)));
+  __syncthreads();
+#endif
+  for (uint32_t ce = stop; ce > begin; buf ^= 1) {
+    const uint32_t cs = chunk_lo(ce);
+    const int cnt = (int)(ce - cs);
+#if !VSX_BWD_MERGED
+    stage(buf, cs, cnt);
     __syncthreads();
+#endif
     // ---- phase 0: sk[j][p] = F[p] . P[j] for this warp's 32 pixels on the
     // tensor cores (3xTF32), written into the q plane that phase 1 overwrites
     // in place with q (same thread, same slot)
@@ -974,6 +992,9 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
       *reinterpret_cast<float2 *>(red) = make_float2(d[0], d[1]);
       *reinterpret_cast<float2 *>(red + 8 * 24) = make_float2(d[2], d[3]);
     }
+#if VSX_BWD_MERGED
+    if (cs > begin) stage(buf ^ 1, chunk_lo(cs), (int)(cs - chunk_lo(cs)));
+#endif
     __syncthreads();
     // ---- epilogue: 8 lanes per splat, lane part holds features 2part, 2part+1
     if (t < 8 * kBC) {
