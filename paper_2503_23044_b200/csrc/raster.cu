@@ -723,6 +723,10 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
 // a_hi + a_lo. Warps split (m-tile, plane, k-range); the KSPLIT partial sums
 // meet in shared memory and one 8-lane group per splat forms its 13
 // gradients (same polynomials as v2) and issues the atomics.
+#ifndef VSX_BWD_UB
+#define VSX_BWD_UB 4
+#endif
+constexpr int kUB = VSX_BWD_UB;  // phase-1 splats per alpha batch
 #ifndef VSX_BWD_MERGED
 #define VSX_BWD_MERGED 1
 #endif
@@ -904,20 +908,20 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
       wpl[j * kPlaneStride + t] = 0.f;
       qpl[j * kPlaneStride + t] = 0.f;
     }
-    // batches of 4: the alphas (the long dependent part) are independent
+    // batches of kUB: the alphas (the long dependent part) are independent
     // across splats; only T and S are carried, one FMUL / FFMA each
     int j = jlive - 1;
-    for (; j >= 3; j -= 4) {
-      float al[4], ee[4], aa[4], rm[4], sk[4];
+    for (; j >= kUB - 1; j -= kUB) {
+      float al[kUB], ee[kUB], aa[kUB], rm[kUB], sk[kUB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kUB; ++u) {
         const float4 p0 = s0[buf][j - u], p1 = s1[buf][j - u];
         al[u] = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, ee[u], aa[u]);
         rm[u] = rcp_ftz(1.f - al[u]);
         sk[u] = qpl[(j - u) * kPlaneStride + t];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kUB; ++u) {
         const float Tk = T * rm[u];
         const float w = al[u] * Tk;
         const float da = Tk * sk[u] - S * rm[u];
