@@ -727,6 +727,9 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
 #define VSX_BWD_UB 4
 #endif
 constexpr int kUB = VSX_BWD_UB;  // phase-1 splats per alpha batch
+#ifndef VSX_BWD_STAGE_WARP
+#define VSX_BWD_STAGE_WARP 7
+#endif
 #ifndef VSX_BWD_MERGED
 #define VSX_BWD_MERGED 1
 #endif
@@ -828,45 +831,49 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   // Record prefetch: the raw 64-byte records of chunk i+1 are copied
   // (cp.async) into s_raw while chunk i is processed, and the tile-list ranks
   // of chunk i+2 are loaded into a register, so neither dependent global load
-  // sits in front of a barrier. Thread t always owns slot t.
+  // sits in front of a barrier.
   auto chunk_lo = [&](uint32_t e) { return e > begin + kBC ? e - kBC : begin; };
+  // slot owner: thread t owns slot t - 32 * VSX_BWD_STAGE_WARP, a warp whose
+  // phase-2 role has two tensor-core products per k-step, not three, and
+  // which sits outside the epilogue's warps 0-3 (warp 0: 1503 us, 7: 1475 us)
+  const int sl = t - 32 * VSX_BWD_STAGE_WARP;
   uint32_t rr = 0;  // rank of slot t in the chunk whose copy is in flight
   uint32_t nr = 0;  // rank of slot t in the chunk after it
   {
     const uint32_t cs = chunk_lo(stop);
-    if (stop > begin && t < (int)(stop - cs)) {
-      rr = a.tile_list[cs + t];
-      copy_splat_async(&s_raw[0][t], a.rec + rr);
+    if (stop > begin && (unsigned)sl < (stop - cs)) {
+      rr = a.tile_list[cs + sl];
+      copy_splat_async(&s_raw[0][sl], a.rec + rr);
     }
     cp_async_commit();
     const uint32_t cs2 = chunk_lo(cs);
-    if (cs > begin && t < (int)(cs - cs2)) nr = a.tile_list[cs2 + t];
+    if (cs > begin && (unsigned)sl < (cs - cs2)) nr = a.tile_list[cs2 + sl];
   }
   // Stage chunk [cs_, cs_ + cnt_) into buffer sb from its in-flight copy and
   // start the copy of the chunk after it.
   auto stage = [&](int sb, uint32_t cs_, int cnt_) {
     cp_async_wait_all();
-    if (t < cnt_) {
-      s_rank[sb][t] = rr;
-      const vsx_splat &sp = s_raw[sb][t];
-      stage_splat(sp, ox, oy, s0[sb][t], s1[sb][t], s2[sb][t], s3[sb][t]);
+    if ((unsigned)sl < (unsigned)cnt_) {
+      s_rank[sb][sl] = rr;
+      const vsx_splat &sp = s_raw[sb][sl];
+      stage_splat(sp, ox, oy, s0[sb][sl], s1[sb][sl], s2[sb][sl], s3[sb][sl]);
       const float pv[8] = {sp.color[0], sp.color[1], sp.color[2], sp.normal[0],
                            sp.normal[1], sp.normal[2], sp.plane_d, 1.f};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float h0 = __uint_as_float(tf32_bits(pv[k])), h1 = __uint_as_float(tf32_bits(pv[k + 4]));
-        s_ph[sb][t][k] = make_float4(h0, h1, __uint_as_float(tf32_bits(pv[k] - h0)),
+        s_ph[sb][sl][k] = make_float4(h0, h1, __uint_as_float(tf32_bits(pv[k] - h0)),
                                      __uint_as_float(tf32_bits(pv[k + 4] - h1)));
       }
     }
     const uint32_t cs2 = chunk_lo(cs_);
-    if (cs_ > begin && t < (int)(cs_ - cs2)) {
+    if (cs_ > begin && (unsigned)sl < (cs_ - cs2)) {
       rr = nr;
-      copy_splat_async(&s_raw[sb ^ 1][t], a.rec + nr);
+      copy_splat_async(&s_raw[sb ^ 1][sl], a.rec + nr);
     }
     cp_async_commit();
     const uint32_t cs3 = chunk_lo(cs2);
-    if (cs2 > begin && t < (int)(cs2 - cs3)) nr = a.tile_list[cs3 + t];
+    if (cs2 > begin && (unsigned)sl < (cs2 - cs3)) nr = a.tile_list[cs3 + sl];
   };
 #if VSX_BWD_MERGED
   // Two barriers per chunk: the next chunk is staged (double-buffered) right
