@@ -727,6 +727,9 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
 #define VSX_BWD_UB 4
 #endif
 constexpr int kUB = VSX_BWD_UB;  // phase-1 splats per alpha batch
+#ifndef VSX_BWD_KR7
+#define VSX_BWD_KR7 5
+#endif
 #ifndef VSX_BWD_STAGE_WARP
 #define VSX_BWD_STAGE_WARP 7
 #endif
@@ -987,9 +990,18 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
           mma_m16n8k8_tf32(d, hi, __float_as_uint(b.x), __float_as_uint(b.y));
         }
       } else {
+        // q-plane k-ranges: the staging warp (kr = 3 at kBC = 16) takes 5 of
+        // the 32 k-steps, the other three 9 each (VSX_BWD_KR7 = 8 / 5 / 2:
+        // 1479 / 1467 / 1479 us per view)
+        int k0 = kr * kKS, kn = kKS;
+        if (kMT == 1 && VSX_BWD_KR7 != kKS) {
+          constexpr int q = (32 - VSX_BWD_KR7) / 3;
+          k0 = kr * q;
+          kn = kr == 3 ? 32 - 3 * q : q;
+        }
 #pragma unroll 4
-        for (int kk = 0; kk < kKS; ++kk) {
-          const int ks = kr * kKS + kk;
+        for (int kk = 0; kk < kn; ++kk) {
+          const int ks = k0 + kk;
           uint32_t hi[4], lo[4];
           a_frag(ks, hi, lo);
           const float2 b = s_bq[ks][lane];
