@@ -13,11 +13,25 @@ embeddings) on the device before timing. Inputs (>> L2 per step: 8 views x
 larger than the 126 MB L2, so no explicit flush is needed.
 
   python bench.py [--gpus N --steps K --warmup W]            # CUDA path
-  python bench.py --impl reference [--steps K --warmup W]    # CPU oracle arm
+  python bench.py --impl reference [--steps K --warmup W]    # reference CPU arm
 
-Under torchrun (N>1) every rank trains its own replica on its own 8 views
-(replicas, weak scaling) and rank 0 prints one JSON line with the max-over-
-ranks device time.
+N > 1 (torchrun, or `--gpus N` alone: bench.py then re-launches itself
+under torch.distributed.run with N ranks, and fails if fewer GPUs exist):
+the anchors are sharded over the ranks by the paper's Eq. 3 (i mod M,
+partition.py:43-52) and every step runs dist.sharded_train_step: each rank
+culls / decodes / projects its own anchors for all views, a C1 all-to-all
+moves the splat records to each view's renderer rank, the reverse C1 returns
+the 2D gradients, and a C2 all-reduce sums the decoder gradient. cfg2 is
+weak scaling (8 views per rank per step); cfg3 (1M anchors, 16 views at
+1080p) and cfg4 (2M anchors, 8 views at 3840x2160) keep the batch fixed
+(strong scaling). Rank 0 prints one JSON line with the max-over-ranks
+device time.
+
+The reference arm runs the UNMODIFIED reference (oracle/_ref, installed by
+oracle/build_ref.py from /root/reference/pkg) on the host cores: a bounded,
+intersection-scaled sample of the same workload per step
+(oracle/ref_bench.py), plus one full reference train_step at cfg1 with all
+threads and with one thread.
 """
 
 from __future__ import annotations
@@ -44,27 +58,34 @@ if str(ROOT) not in sys.path:
 
 METRIC = "RGB-D-N fwd+bwd train views/sec at 1/2/4/8 B200 vs CPU ref; raster HBM GB/s"
 CFG2_VOXEL = 1.119          # base voxel size giving ~200k anchors over 3 levels
-CFG2_LOD_BIAS = 2
+CFG3_VOXEL = 0.503          # ~1M anchors (synthetic._fit_voxel, precomputed)
+CFG4_VOXEL = 0.395          # ~2M anchors
+CFG_LOD_BIAS = 2
+CFG2_LOD_BIAS = CFG_LOD_BIAS
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["vsx", "reference"], default="vsx")
-    ap.add_argument("--config", choices=["cfg2", "cfg1"], default="cfg2")
+    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg3", "cfg4"], default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cfg1", action="store_true",
+                    help="skip the same-config cfg1 side measurement")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU sharded step even at one rank (testing)")
-    ap.add_argument("--cpu-tiles", type=int, default=2000,
-                    help="tiles composited in the cpu_baseline sample (evenly spaced over "
-                         "the view; ~10 s of host work at cfg2)")
-    ap.add_argument("--ref-tiles", type=int, default=300,
+    ap.add_argument("--cpu-tiles", type=int, default=40,
+                    help="tiles composited per reference sample in the cpu_baseline leg")
+    ap.add_argument("--ref-tiles", type=int, default=40,
                     help="tiles per --impl reference step (each of the W+K steps is one "
                          "such sample, so the arm ends within a few minutes)")
-    return ap.parse_args()
+    ap.add_argument("--ref-cfg1-threads", default="all,1",
+                    help="thread counts of the full reference cfg1 step in --impl reference "
+                         "('all' = os.cpu_count(); empty = skip)")
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -76,22 +97,48 @@ def dist_env():
 
 # ------------------------------------------------------------------ workload
 
-def workload(config: str):
-    from paper_2503_23044_b200.synthetic import cfg1_scene, city_scene
+CITY = {  # config -> (target anchors, base voxel, views per step, width, height, scaling)
+    "cfg2": (200_000, CFG2_VOXEL, 8, 1920, 1080, "weak"),
+    "cfg3": (1_000_000, CFG3_VOXEL, 16, 1920, 1080, "strong"),
+    "cfg4": (2_000_000, CFG4_VOXEL, 8, 3840, 2160, "strong"),
+}
+
+
+def workload(config: str, world: int = 1):
+    """(scene, views, config description, host images or None).
+
+    cfg2 is weak scaling: 8 views per rank per step. cfg3 / cfg4 keep their
+    batch (16 views at 1080p / 8 views at 4K) for every world size."""
+    from paper_2503_23044_b200.synthetic import cfg1_scene, city_scene, city_views
     if config == "cfg1":
         scene, views, images = cfg1_scene()
         return scene, views, {"workload": "cfg1: 10,198 anchors x 10 gaussians, 4 views 128x128",
                               "anchors": scene.total_voxels, "views_per_step": 4,
                               "resolution": "128x128", "loss": "rgb"}, images
-    scene, views = city_scene(target_anchors=200_000, base_voxel_size=CFG2_VOXEL)
-    scene.lod_bias = CFG2_LOD_BIAS
-    desc = {"workload": "cfg2: synthetic aerial city block, 200k anchors x 10 gaussians "
-                        "(K=3, LoD bias 2), 8 views/step at 1920x1080, RGB+depth+normal loss",
+    target, voxel, nv, W, H, scaling = CITY[config]
+    scene, views = city_scene(target_anchors=target, base_voxel_size=voxel, n_views=nv,
+                              width=W, height=H)
+    scene.lod_bias = CFG_LOD_BIAS
+    if scaling == "weak" and world > 1:
+        views = city_views(nv * world, W, H)
+    desc = {"workload": f"{config}: synthetic aerial city block, {target // 1000}k anchors x 10 "
+                        f"gaussians (K=3, LoD bias {CFG_LOD_BIAS}), {nv} views/step"
+                        f"{' per GPU' if scaling == 'weak' else ''} at {W}x{H}, RGB+depth+normal"
+                        " loss",
             "anchors": scene.total_voxels, "gaussians_total": scene.total_voxels * 10,
-            "views_per_step": len(views), "resolution": "1920x1080",
+            "views_per_step": len(views), "resolution": f"{W}x{H}",
             "loss": "L1 rgb + depth-prior L1 (Eq.9) + 0.5 normal-prior L1",
             "l2_flush": "inputs > L2 (per-step working set ~GBs)"}
     return scene, views, desc, None
+
+
+def config_of(args, world: int, desc: dict) -> dict:
+    """The JSON `config` object, identical for the CUDA and the reference arm."""
+    desc = dict(desc)
+    desc["parallelism"] = (f"anchor-sharded x{world} (Eq.3 i mod M), views rendered round-robin, "
+                           "C1 all-to-all + C2 decoder all-reduce (NCCL)") if world > 1 else "single"
+    desc["scaling"] = CITY.get(args.config, (0, 0, 0, 0, 0, "weak"))[5]
+    return desc
 
 
 def teacher_targets(scene, views):
@@ -267,7 +314,53 @@ def measured_peaks() -> dict:
 
 # ------------------------------------------------------------------ CPU baseline (oracle)
 
-def cpu_sample(scene, views, tiles: int, images=None) -> dict:
+def reference_available() -> bool:
+    from oracle.ref_bench import REF_DIR
+    return (REF_DIR / "voxsplat" / "__init__.py").exists()
+
+
+def reference_sampler(config: str, views, tiles: int, front_views: int):
+    """oracle/ref_bench.Cfg2Sampler on the same points / views as the CUDA arm."""
+    import torch
+    from oracle.ref_bench import Cfg2Sampler
+    from paper_2503_23044_b200.synthetic import city_points
+    torch.set_num_threads(os.cpu_count() or 1)
+    target, voxel, _nv, _W, _H, _ = CITY[config]
+    pts = city_points(n_points=max(600_000, int(7.5 * target)), seed=0)
+    return Cfg2Sampler(pts, voxel, 3, CFG_LOD_BIAS, 10, views, tiles, normal_weight=0.5,
+                       front_views=front_views)
+
+
+def _ref_sample_desc(s, r: dict, n: int) -> str:
+    return (f"UNMODIFIED reference (oracle/_ref voxsplat, float64) on the host cores, "
+            f"{n} samples of the workload: per sample the reference's rasterize_view buckets "
+            f"(_blend_padded + _finalize) fwd + autograd bwd on {r['tiles']} of "
+            f"{r['tiles_nonempty']} non-empty tiles of one view ({r['isect_sampled']} of "
+            f"{r['isect_total']} intersections, scaled by intersections), RGB + Eq.9 depth + "
+            f"normal-prior L1, + the view's transfer_gaussians/project_splats/bin_splats "
+            f"({r['front_s']:.1f} s) and projection+decode autograd ({r['proj_decode_bwd_s']:.1f}"
+            f" s) measured once per view at setup ({len(s.fronts)} views), + the reference Adam "
+            f"over all parameters per sample ({r['adam_s']:.2f} s); step = "
+            f"{len(s.views)} views + 1 Adam")
+
+
+def cpu_sample(config: str, views, tiles: int) -> dict:
+    """cpu_baseline of the CUDA arm: the reference on a bounded sample (one
+    front-end view, 2 tile samples, ~30 s), or the oracle port if the
+    reference is not installed."""
+    import torch
+    if config != "cfg1" and reference_available():
+        t0 = time.perf_counter()
+        s = reference_sampler(config, views, tiles, front_views=1)
+        rs = [s.sample() for _ in range(2)]
+        value = float(np.median([r["views_per_s"] for r in rs]))
+        return {"value": value, "unit": "views/s", "cores": torch.get_num_threads(),
+                "kind": "reference", "wall_s": time.perf_counter() - t0,
+                "sample": _ref_sample_desc(s, rs[-1], len(rs))}
+    return cpu_sample_port(*workload(config)[:2], tiles=2000)
+
+
+def cpu_sample_port(scene, views, tiles: int, images=None) -> dict:
     """Oracle (float64 CPU port) on ONE view of the workload, time-extrapolated.
 
     Full cull/decode/project/bin for the view, composite fwd+bwd on `tiles`
@@ -301,29 +394,64 @@ def cpu_sample(scene, views, tiles: int, images=None) -> dict:
                        f"Adam excluded; {wall:.1f}s measured")}
 
 
+def reference_cfg1(spec: str) -> dict:
+    """Full reference train_step at cfg1 (the CPU-runnable config) per thread count."""
+    from oracle.ref_bench import cfg1_step_seconds
+    out = {}
+    for tok in [t.strip() for t in spec.split(",") if t.strip()]:
+        n = (os.cpu_count() or 1) if tok == "all" else int(tok)
+        r = cfg1_step_seconds(n)
+        out[f"threads_{n}"] = {"views_per_s": r["views_per_s"], "step_s": r["seconds"],
+                               "threads": n}
+    return out
+
+
 def run_reference(args):
+    """--impl reference: the unmodified reference on the host cores (rank 0 only)."""
+    import torch
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    scene, views, desc, images = workload(args.config)
+    world = max(world, args.gpus)     # the CUDA arm's config at the same N
+    if not reference_available():
+        from oracle.build_ref import build
+        if not build():
+            print(json.dumps({"impl": "reference", "unavailable":
+                              "oracle/_ref not installed and /root/reference absent"}))
+            return
+    _scene, views, desc, _images = workload(args.config, world)
+    config = config_of(args, world, desc)
+    torch.set_num_threads(os.cpu_count() or 1)
+    cores = torch.get_num_threads()
+    t0 = time.perf_counter()
     if args.config == "cfg1":
-        tiles = None
+        from oracle.ref_bench import cfg1_step_seconds
+        runs = [cfg1_step_seconds(cores) for _ in range(max(1, min(args.steps, 3)))]
+        value = float(np.median([r["views_per_s"] for r in runs]))
+        sample = (f"UNMODIFIED reference train_step at cfg1 (full steps, {len(runs)} timed, no "
+                  "warm-up: CPU float64)")
     else:
-        tiles = args.ref_tiles
-    vals = []
-    for i in range(args.warmup + args.steps):
-        s = cpu_sample(scene, views, tiles if tiles else 10**9, images)
-        if i >= args.warmup:
-            vals.append(s)
-    value = float(np.median([s["value"] for s in vals]))
-    cb = dict(vals[-1])
-    cb["value"] = value
+        s = reference_sampler(args.config, views, args.ref_tiles, front_views=2)
+        rs = []
+        for i in range(args.warmup + args.steps):
+            r = s.sample()
+            if i >= args.warmup:
+                rs.append(r)
+        value = float(np.median([r["views_per_s"] for r in rs]))
+        sample = _ref_sample_desc(s, rs[-1], len(rs))
+    wall = time.perf_counter() - t0
+    cfg1 = reference_cfg1(args.ref_cfg1_threads) if args.ref_cfg1_threads else None
+    ms = len(views) / value * 1e3
     line = {"metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": desc, "impl": "reference", "cpu_baseline": cb,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": config["scaling"], "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": config, "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "views/s", "cores": cores,
+                             "kind": "reference", "sample": sample, "wall_s": wall},
             "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0,
+            "cfg1_full_step": cfg1}
     print(json.dumps(line), flush=True)
 
 
@@ -352,12 +480,8 @@ def run_vsx(args):
     from paper_2503_23044_b200 import _lib
     from paper_2503_23044_b200.trainer import GpuTimer, TrainConfig, TrainState, train_step
     lib = _lib.load()
-    scene, views, desc, images = workload(args.config)
-    cfg2 = args.config == "cfg2"
-    if world > 1 and cfg2:
-        # weak scaling: 8 views per rank per step, anchors sharded over the ranks
-        from paper_2503_23044_b200.synthetic import city_views
-        views = city_views(8 * world)
+    scene, views, desc, images = workload(args.config, world)
+    cfg2 = args.config != "cfg1"      # the city configs share cfg2's objective
     cfg = TrainConfig(total_steps=30000, batch_size=len(views), step2_start=0 if cfg2 else 30000,
                       step3_start=30000, growth_stop=0, normal_weight=0.5 if cfg2 else 0.0,
                       workers=world)
@@ -489,23 +613,22 @@ def run_vsx(args):
             ems = float(t.item())
         e2e = {"value": len(views) / (ems / 1e3), "unit": "views/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * 4 + 8}
+    cfg1 = None
+    if rank == 0 and world == 1 and args.config != "cfg1" and not args.no_cfg1:
+        cfg1 = cfg1_gpu(max(args.steps, 10))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sample(scene, views, args.cpu_tiles if cfg2 else 10**9, images)
+        cpu = cpu_sample(args.config, views, args.cpu_tiles)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    desc = dict(desc)
-    desc["parallelism"] = (f"anchor-sharded x{world} (Eq.3 i mod M), views rendered round-robin, "
-                           "C1 all-to-all + C2 decoder all-reduce (NCCL)") if world > 1 else "single"
-    if world > 1:
-        desc["views_per_step"] = len(views)
+    config = config_of(args, world, desc)
     line = {
         "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": desc,
+        "higher_is_better": True, "scaling": config["scaling"], "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": config,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(dom),
@@ -525,16 +648,70 @@ def run_vsx(args):
                      "live_pairs": reps[-1].get("live_pairs"),
                      "loss_total": reps[-1]["total"], "loss_rgb": reps[-1]["rgb"],
                      "loss_depth": reps[-1]["depth"], "loss_normal": reps[-1]["normal"]},
+        # same-config side measurement against the reference arm's cfg1_full_step
+        "cfg1_full_step": cfg1,
     }
     print(json.dumps(line), flush=True)
     if sharded:
         dist.destroy_process_group()
 
 
+def cfg1_gpu(steps: int) -> dict:
+    """cfg1 (the reference's CPU-runnable config) through train_step on the
+    device: views/s over `steps` timed steps after 3 warm-ups (CUDA events)."""
+    import torch
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step
+    scene, views, _desc, images = workload("cfg1")
+    st = TrainState(scene, TrainConfig(total_steps=30000, batch_size=4, step2_start=30000,
+                                       step3_start=30000, growth_stop=0))
+    imgs = [torch.as_tensor(np.asarray(im, np.float32)).cuda() for im in images]
+    for _ in range(3):
+        train_step(st, views, imgs)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        train_step(st, views, imgs)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"views_per_s": len(views) / (ms / 1e3), "ms_per_step": ms, "steps": steps,
+            "workload": "cfg1: 10,198 anchors x 10, 4 views 128x128, RGB L1 + Adam"}
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: N ranks via torch.distributed.run."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} requested but only {have} CUDA device(s) are visible",
+              file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+           str(_free_port()), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None and int(env_world) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={env_world} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and env_world is None:
+        sys.exit(relaunch(args.gpus))
     else:
         run_vsx(args)
 

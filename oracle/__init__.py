@@ -15,6 +15,6 @@ outputs to 1e-10; gradients to 1e-9 relative).
 
 from .pipeline import (  # noqa: F401
     Cam, adam_update, bin_tiles, cosine_lr, cull, decode, decoder_init, l1_loss,
-    depth_l1_loss, project, raster, raster_tile, OracleState, train_step,
+    depth_l1_loss, normal_l1_loss, project, raster, raster_tile, OracleState, train_step,
     render_view, leaf_gaussians, flatten_decoded, weight_schedule, SPLAT_KEYS,
 )

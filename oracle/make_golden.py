@@ -216,13 +216,67 @@ def make_cfg1():
     out["rows"] = rows
     for name, a in zip(("emb", "log_scales", "offsets"), lgrads):
         out[f"lgrad_{name}"] = a[rows]
-    reports = [trainer.train_step(state, views, images) for _ in range(2)]
+    reports = [trainer.train_step(state, views, images)]
+    # step-2 gradients (at the post-step-1 parameters): the post-step tests
+    # exclude elements whose gradient in either step is at the noise floor
+    _, dgrads2, lgrads2 = _reference_grads(trainer, renderer, losses, state, views, images)
+    out.update({f"grad2_{k}": a for k, a in dgrads2.items()})
+    for name, a in zip(("emb", "log_scales", "offsets"), lgrads2):
+        out[f"lgrad2_{name}"] = a[rows]
+    reports.append(trainer.train_step(state, views, images))
     out["report_rgb"] = np.array([r.rgb for r in reports])
     for k, t_ in state.replicas[0].tensors.items():
         out[f"post_{k}"] = t_.detach().numpy()
     for name, key in (("emb", "embeddings"), ("log_scales", "log_scales"),
                       ("offsets", "offsets")):
         out[f"post_lv_{name}"] = state.level_state[0][key].detach().numpy()[rows]
+    # The same two steps from float32-representable initial parameters: the
+    # device's exact inputs, so its gradients are compared without the
+    # input-rounding term (f32_*). The full post-step-1 parameters let the
+    # device compute its step-2 gradient at the reference's parameters.
+    state = trainer.make_state(scene, cfg)
+    prng = np.random.default_rng(17)
+    for s in range(2):
+        # every step starts from float32-representable parameters, as the
+        # device's do (a float64 post-step value rounded by the device could
+        # flip a near-tie decision and make the step-2 gradients incomparable)
+        with torch.no_grad():
+            for t_ in state.replicas[0].tensors.values():
+                t_.copy_(t_.float().double())
+            for key in ("embeddings", "log_scales", "offsets"):
+                lv = state.level_state[0][key]
+                lv.copy_(lv.float().double())
+        _, dg, lg = _reference_grads(trainer, renderer, losses, state, views, images)
+        pre = "f32_grad" if s == 0 else "f32_grad2"
+        out.update({f"{pre}_{k}": a for k, a in dg.items()})
+        for name, a in zip(("emb", "log_scales", "offsets"), lg):
+            out[f"f32_l{pre[4:]}_{name}"] = a[rows]
+        # noise floor: the same gradient with every parameter moved by one
+        # float32 ulp (random sign) -- the sensitivity of each gradient element
+        # to the rounding of its inputs, which no float32 pipeline can avoid
+        params = list(state.replicas[0].tensors.values()) + \
+            [state.level_state[0][k] for k in ("embeddings", "log_scales", "offsets")]
+        saved = [p_.detach().clone() for p_ in params]
+        with torch.no_grad():
+            for p_ in params:
+                sgn = torch.as_tensor(prng.choice([-1.0, 1.0], size=tuple(p_.shape)))
+                p_.copy_(p_ * (1.0 + sgn * 2.0 ** -23))
+        _, dgp, lgp = _reference_grads(trainer, renderer, losses, state, views, images)
+        with torch.no_grad():
+            for p_, v_ in zip(params, saved):
+                p_.copy_(v_)
+        out.update({f"f32p_{pre[4:]}_{k}": a for k, a in dgp.items()})
+        for name, a in zip(("emb", "log_scales", "offsets"), lgp):
+            out[f"f32p_l{pre[4:]}_{name}"] = a[rows]
+        rep = trainer.train_step(state, views, images)
+        out[f"f32_report_rgb{s}"] = np.array(rep.rgb)
+        tag = "f32_post1" if s == 0 else "f32_post"
+        for k, t_ in state.replicas[0].tensors.items():
+            out[f"{tag}_{k}"] = t_.detach().numpy()
+        for name, key in (("emb", "embeddings"), ("log_scales", "log_scales"),
+                          ("offsets", "offsets")):
+            a = state.level_state[0][key].detach().numpy()
+            out[f"{tag}_lv_{name}"] = a if s == 0 else a[rows]
     np.savez_compressed(OUT / "cfg1.npz", **out)
     print(f"cfg1 golden in {time.time() - t0:.0f}s")
 
@@ -496,6 +550,39 @@ def make_depth_prior():
     out["enh0_valid"] = enh.valid
     out["enh0_min_roundtrip"] = enh.min_roundtrip
     np.savez_compressed(OUT / "depth_prior.npz", **out)
+
+
+def make_normal_prior():
+    """The normal-prior L1 of the RGB-D-N objective has no reference function
+    (the reference supervises normals through the depth quotient and Eq. 10);
+    its contract is Eq. 9 applied per channel: the reference's own
+    loss_e_depth (losses.py:65-95) on each of the 3 normal channels, averaged.
+    Three views of random unit normals, render-valid and prior-valid masks."""
+    decoder, geometry, partition, renderer, scene_m, trainer, losses = _ref()
+    rng = np.random.default_rng(21)
+    H, W = 24, 32
+    out = {}
+    normals, rvalid, priors, pvalid = [], [], [], []
+    for i in range(3):
+        n = rng.normal(size=(H, W, 3))
+        n /= np.linalg.norm(n, axis=-1, keepdims=True)
+        p = rng.normal(size=(H, W, 3))
+        p /= np.linalg.norm(p, axis=-1, keepdims=True)
+        rv = rng.uniform(size=(H, W)) > 0.2
+        pv = rng.uniform(size=(H, W)) > (0.3 if i < 2 else 1.1)   # view 2: no prior pixel
+        normals.append(n), rvalid.append(rv), priors.append(p), pvalid.append(pv)
+        out.update({f"n{i}": n, "rv%d" % i: rv, f"p{i}": p, f"pv{i}": pv})
+    vals, grads, sup = [], np.zeros((3, H, W, 3)), 0
+    for c in range(3):
+        v, g, s_ = losses.loss_e_depth([n[..., c] for n in normals], rvalid,
+                                       [p[..., c] for p in priors], pvalid)
+        vals.append(v)
+        grads[..., c] = np.stack(g)
+        sup = s_
+    out["value"] = np.array(np.mean(vals))
+    out["grad"] = grads / 3.0
+    out["supervised"] = np.array(sup)
+    np.savez_compressed(OUT / "normal_prior.npz", **out)
 
 
 def make_geo_loss():

@@ -272,7 +272,8 @@ def _tile_pixels(tx: int, ty: int):
     return (tx * PATCH + du).astype(np.float64), (ty * PATCH + dv).astype(np.float64)
 
 
-def raster_tile(S: dict, idx: np.ndarray, tx: int, ty: int, cam: Cam) -> dict:
+def raster_tile(S: dict, idx: np.ndarray, tx: int, ty: int, cam: Cam,
+                jitter: torch.Generator | None = None) -> dict:
     """One 16x16 tile, all 256 pixels (ragged ones included).
 
     Blend = ``renderer.py:242-279``: power at integer pixel coordinates,
@@ -281,6 +282,11 @@ def raster_tile(S: dict, idx: np.ndarray, tx: int, ty: int, cam: Cam) -> dict:
     accumulated alpha / rgb / raw normal / plane offset, and
     denom = raw_normal . ((u - cx)/fx, (v - cy)/fy, 1).
     Finalize = ``renderer.py:282-301``.
+
+    ``jitter`` (tests only) multiplies the per-(splat, pixel) power, each
+    transmittance factor and each weight by independent (1 + 2^-23 u),
+    u ~ U(-1, 1): float32 rounding of every intermediate, so that
+    |g - g_jitter| estimates a gradient element's float32 floor.
     """
     pu_np, pv_np = _tile_pixels(tx, ty)
     pu, pv = torch.from_numpy(pu_np), torch.from_numpy(pv_np)
@@ -289,14 +295,20 @@ def raster_tile(S: dict, idx: np.ndarray, tx: int, ty: int, cam: Cam) -> dict:
     con = S["conic"][it]
     dx = pu.unsqueeze(0) - m[:, 0:1]
     dy = pv.unsqueeze(0) - m[:, 1:2]
-    power = -0.5 * (con[:, 0:1] * dx * dx + 2.0 * con[:, 1:2] * dx * dy
-                    + con[:, 2:3] * dy * dy)
+
+    def jit(x):
+        if jitter is None:
+            return x
+        u = torch.rand(x.shape, generator=jitter, dtype=F64) * 2.0 - 1.0
+        return x * (1.0 + 2.0 ** -23 * u)
+    power = jit(-0.5 * (con[:, 0:1] * dx * dx + 2.0 * con[:, 1:2] * dx * dy
+                        + con[:, 2:3] * dy * dy))
     alpha = S["opacity"][it].unsqueeze(-1) * torch.exp(torch.clamp(power, max=0.0))
     alpha = torch.clamp(alpha, max=ALPHA_CLAMP)
-    trans = torch.cumprod(1.0 - alpha, dim=0)
+    trans = torch.cumprod(jit(1.0 - alpha), dim=0)
     t_prev = torch.cat([torch.ones_like(trans[:1]), trans[:-1]], dim=0)
     live = (t_prev >= EARLY_STOP_T).to(F64).detach()
-    w = alpha * t_prev * live                                   # (L, 256)
+    w = jit(alpha * t_prev * live)                              # (L, 256)
     acc = w.sum(0)
     rgb = w.transpose(0, 1) @ S["color"][it]
     raw_n = w.transpose(0, 1) @ S["normal_cam"][it]
@@ -496,22 +508,52 @@ def render_view(st: OracleState, cam: Cam) -> dict:
     return img
 
 
+def normal_l1_loss(normals, rvalid, priors, pvalid):
+    """Normal-prior L1 of the RGB-D-N objective (the B200 build's "N" term).
+
+    The reference has no standalone normal loss: it supervises normals only
+    through the depth quotient (``renderer.py:276-278``) and Eq. 10
+    (``losses.py:196-287``); SURVEY.md §8(d) cfg2 asks for an "N" term. This
+    is its contract, written in the shape of Eq. 9 (``losses.py:65-84``): per
+    view the mean of |n_hat - n_prior| over the 3 channels of the pixels that
+    are depth-valid and prior-valid, then the mean over the views that have a
+    prior. Returns (loss, supervised pixel count).
+    """
+    terms, total = [], 0
+    for n, rv, p, pv in zip(normals, rvalid, priors, pvalid):
+        mask = (torch.as_tensor(np.asarray(pv, bool)) & torch.as_tensor(rv)).to(F64)
+        cnt = int(mask.sum())
+        total += cnt
+        if cnt == 0:
+            terms.append(torch.zeros((), dtype=F64))
+        else:
+            d = (n - torch.as_tensor(np.asarray(p, np.float64))).abs().sum(-1)
+            terms.append((d * mask).sum() / (3.0 * cnt))
+    return torch.stack(terms).mean(), total
+
+
 def train_step(st: OracleState, cams: list, images: list, priors: list | None = None,
-               tile_limit: int | None = None) -> dict:
+               tile_limit: int | None = None, normal_priors: list | None = None,
+               normal_weight: float = 0.0) -> dict:
     """One step over a batch of views (``trainer.py:258-376``, RGB + depth terms).
 
     ``priors`` (optional) is a list of (depth, valid) per view for the Eq. 9
-    term, weighted by the stage schedule. ``tile_limit`` renders only the
-    first N non-empty tiles per view (bounded CPU-baseline sample); it is
+    term, weighted by the stage schedule. ``normal_priors`` (optional,
+    (normals, valid) per view) add ``normal_weight`` x the normal-prior L1
+    (:func:`normal_l1_loss`). ``tile_limit`` renders only an evenly spaced
+    sample of N non-empty tiles per view (bounded CPU-baseline sample); it is
     None for parity runs.
     """
     B = len(cams)
     w2, _ = weight_schedule(st.step, st.total_steps, st.step2_start, st.step3_start)
     use_depth = priors is not None and w2 > 0 and any(p is not None for p in priors)
+    use_normal = normal_priors is not None and normal_weight > 0
     for p in [*st.weights.values(), st.emb, st.log_scales, st.offsets]:
         p.requires_grad_(True)
         p.grad = None
     have = [i for i in range(B) if use_depth and priors[i] is not None]
+    have_n = [i for i in range(B) if use_normal and normal_priors[i] is not None]
+    normal_terms = []
     rgb_terms, depth_terms, supervised, gaussians, max_tile = [], [], 0, 0, 0
     timing = {"t_fixed": 0.0, "t_tiles": 0.0, "tiles_done": 0, "tiles_nonempty": 0}
     for vi, cam in enumerate(cams):
@@ -526,17 +568,26 @@ def train_step(st: OracleState, cams: list, images: list, priors: list | None = 
         gt = torch.as_tensor(np.asarray(images[vi], np.float64))
         H, W = cam.height, cam.width
         dnorm, prior_d, prior_v = 0.0, None, None
-        if vi in have:
+        nnorm, prior_n, prior_nv = 0.0, None, None
+        full = None
+        if vi in have or vi in have_n:
             with torch.no_grad():
                 full = raster(leaves, offsets, lists, cam)
+        if vi in have:
             prior_d = torch.as_tensor(np.asarray(priors[vi][0], np.float64))
             prior_v = torch.as_tensor(np.asarray(priors[vi][1], bool))
             cnt = int((prior_v & full["valid"]).sum())
             supervised += cnt
             dnorm = (w2 / len(have) / cnt) if cnt else 0.0
+        if vi in have_n:
+            prior_n = torch.as_tensor(np.asarray(normal_priors[vi][0], np.float64))
+            prior_nv = torch.as_tensor(np.asarray(normal_priors[vi][1], bool))
+            ncnt = int((prior_nv & full["valid"]).sum())
+            nnorm = (normal_weight / len(have_n) / (3.0 * ncnt)) if ncnt else 0.0
         tx_n, ty_n = cam.tiles
         rgb_sum = torch.zeros((), dtype=F64)
         dep_sum = torch.zeros((), dtype=F64)
+        nrm_sum = torch.zeros((), dtype=F64)
         done = 0
         timing["tiles_nonempty"] += int((np.diff(offsets) > 0).sum())
         tt = time.perf_counter()
@@ -565,6 +616,11 @@ def train_step(st: OracleState, cams: list, images: list, priors: list | None = 
                 dd = ((out["depth"][ki] - prior_d[py, px]).abs() * msk).sum()
                 obj = obj + dnorm * dd
                 dep_sum = dep_sum + dd.detach()
+            if prior_n is not None and nnorm:
+                msk = (prior_nv[py, px] & out["valid"][ki]).to(F64)
+                nd = ((out["normal"][ki] - prior_n[py, px]).abs().sum(-1) * msk).sum()
+                obj = obj + nnorm * nd
+                nrm_sum = nrm_sum + nd.detach()
             if obj.requires_grad:
                 obj.backward()
         tb = time.perf_counter()
@@ -583,6 +639,8 @@ def train_step(st: OracleState, cams: list, images: list, priors: list | None = 
         rgb_terms.append(rgb_sum / (H * W * 3))
         if vi in have:
             depth_terms.append(dep_sum * (dnorm * len(have) / w2))
+        if vi in have_n:
+            normal_terms.append(nrm_sum * (nnorm * len(have_n) / normal_weight))
         grads = [leaves[k].grad if leaves[k].grad is not None else torch.zeros_like(leaves[k])
                  for k in SPLAT_KEYS]
         torch.autograd.backward([P[k] for k in SPLAT_KEYS], grads)
@@ -590,7 +648,8 @@ def train_step(st: OracleState, cams: list, images: list, priors: list | None = 
     st.last_timing = timing
     rgb = torch.stack(rgb_terms).mean()
     depth = torch.stack(depth_terms).mean() if depth_terms else torch.zeros((), dtype=F64)
-    total = rgb + w2 * depth
+    normal = torch.stack(normal_terms).mean() if normal_terms else torch.zeros((), dtype=F64)
+    total = rgb + w2 * depth + normal_weight * normal
     if not bool(torch.isfinite(total)):
         raise FloatingPointError(f"non-finite loss at step {st.step}")
     st.last_grads = {}
@@ -600,7 +659,7 @@ def train_step(st: OracleState, cams: list, images: list, priors: list | None = 
         m, v = st.moments[name]
         adam_update(p.data, g, m, v, st.step, st.lr_for(name), st.beta1, st.beta2)
     report = {"step": st.step, "total": float(total), "rgb": float(rgb),
-              "depth": float(depth), "w2": w2, "gaussians": gaussians,
+              "depth": float(depth), "normal": float(normal), "w2": w2, "gaussians": gaussians,
               "supervised_depth_px": supervised, "max_tile_splats": max_tile}
     st.step += 1
     for p in [*st.weights.values(), st.emb, st.log_scales, st.offsets]:

@@ -27,8 +27,9 @@ def _unpack(rec: torch.Tensor) -> dict:
 
 
 class OracleShardBackend:
-    def __init__(self, st, rank: int, world: int):
+    def __init__(self, st, rank: int, world: int, normal_weight: float = 0.0):
         self.st, self.rank, self.world = st, rank, world
+        self.normal_weight = float(normal_weight)
         levels = np.asarray(st.levels)
         idx_in_level = np.zeros(levels.shape[0], dtype=np.int64)
         for k in np.unique(levels):
@@ -40,11 +41,17 @@ class OracleShardBackend:
         st = self.st
         return [*st.weights.values(), st.emb, st.log_scales, st.offsets]
 
-    def begin_step(self, views) -> None:
+    def schedule(self):
+        st = self.st
+        w2, w3 = weight_schedule(st.step, st.total_steps, st.step2_start, st.step3_start)
+        return w2, w3, self.normal_weight
+
+    def begin_step(self, views, have=(), have_n=()) -> None:
         for p in self.leaves():
             p.requires_grad_(True)
             p.grad = None
         self.B = len(views)
+        self.have, self.have_n = list(have), list(have_n)
         self.hw = np.array([v.height * v.width * 3 for v in views], dtype=np.float64)
         self.sums = torch.zeros((self.B, 5), dtype=F64)
         self.work = {}
@@ -84,16 +91,26 @@ class OracleShardBackend:
         diff = (img["rgb"] - gt).abs().sum()
         obj = diff / (self.B * cam.height * cam.width * 3)
         self.sums[v, 0] += float(diff)
-        if prior is not None and w2 > 0:
+        if v in self.have:      # Eq. 9, mean over the views with a prior
             pd = torch.as_tensor(np.asarray(prior[0], np.float64))
             pv = torch.as_tensor(np.asarray(prior[1], bool))
             mask = (pv & img["valid"]).to(F64)
             cnt = int(mask.sum())
             dd = ((img["depth"] - pd).abs() * mask).sum()
             if cnt:
-                obj = obj + (w2 / self.B) * dd / cnt
+                obj = obj + (w2 / len(self.have)) * dd / cnt
             self.sums[v, 1] += float(dd)
             self.sums[v, 3] += cnt
+        if v in self.have_n:    # normal-prior L1 (pipeline.normal_l1_loss)
+            pn = torch.as_tensor(np.asarray(nprior[0], np.float64))
+            pnv = torch.as_tensor(np.asarray(nprior[1], bool))
+            mask = (pnv & img["valid"]).to(F64)
+            cnt = int(mask.sum())
+            nd = ((img["normal"] - pn).abs().sum(-1) * mask).sum()
+            if cnt:
+                obj = obj + (self.normal_weight / len(self.have_n)) * nd / (3.0 * cnt)
+            self.sums[v, 2] += float(nd)
+            self.sums[v, 4] += cnt
         g = torch.autograd.grad(obj, leaf, allow_unused=True)[0]
         g = torch.zeros_like(leaf) if g is None else g
         merged = torch.empty_like(g)
@@ -125,8 +142,11 @@ class OracleShardBackend:
         w2, _ = weight_schedule(st.step, st.total_steps, st.step2_start, st.step3_start)
         L = losses.numpy()
         rgb = float(np.mean(L[:, 0] / self.hw))
-        cnt = L[:, 3]
-        depth = float(np.mean(np.where(cnt > 0, L[:, 1] / np.maximum(cnt, 1), 0.0)))
+        cnt, ncnt = L[:, 3], L[:, 4]
+        dterm = np.where(cnt > 0, L[:, 1] / np.maximum(cnt, 1), 0.0)
+        nterm = np.where(ncnt > 0, L[:, 2] / (3.0 * np.maximum(ncnt, 1)), 0.0)
+        depth = float(np.mean(dterm[self.have])) if self.have else 0.0
+        normal = float(np.mean(nterm[self.have_n])) if self.have_n else 0.0
         for name, p in st.params().items():
             g = p.grad if p.grad is not None else torch.zeros_like(p)
             m, vv = st.moments[name]
@@ -135,8 +155,8 @@ class OracleShardBackend:
         for p in self.leaves():
             p.requires_grad_(False)
             p.grad = None
-        return {"total": rgb + w2 * depth, "rgb": rgb, "depth": depth,
-                "gaussians": self.gaussians}
+        return {"total": rgb + w2 * depth + self.normal_weight * normal, "rgb": rgb,
+                "depth": depth, "normal": normal, "gaussians": self.gaussians}
 
     def decoder_checksum(self) -> torch.Tensor:
         return torch.cat([w.detach().reshape(-1) for w in self.st.weights.values()]).view(

@@ -1061,7 +1061,363 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   }
 }
 
+// ------------------------------------------------ backward v4 (warp-specialised)
+//
+// v3's per-chunk CTA barriers were its largest stall (19% of issue stalls,
+// profiles/r02_raster_bwd_v3_ncu.txt): every warp waited at the end of phase 1
+// for the slowest pixel of the tile and again after phase 2. v4 splits the CTA
+// into two roles that run concurrently on double-buffered shared memory:
+//   8 pixel warps (thread = pixel): phase 0 (tensor-core cotangent dots) and
+//     phase 1 (the back-to-front recursion) of chunk i into plane buffer i&1;
+//   4 reduction warps: phase 2 (tensor-core per-splat sums) and the atomics
+//     epilogue of chunk i-1 from the other buffer, and the staging of the
+//     splat records two chunks ahead.
+// The roles meet only through named barriers (producer bar.arrive, consumer
+// bar.sync): REC_FULL[b] (records of buffer b staged), PLANE_FULL[b] (planes
+// written), PLANE_EMPTY[b] (planes consumed). The math of each phase is v3's,
+// so results are identical up to the fp32 summation order of phase 2.
+namespace ws {
+constexpr int kBC = 16;                  // splats per chunk (one MMA m-tile)
+constexpr int kPixWarps = 8;
+constexpr int kRedWarps = 4;
+constexpr int kThreads = 32 * (kPixWarps + kRedWarps);
+constexpr int kRedThreads = 32 * kRedWarps;
+constexpr int kPlane = kBC * kPlaneStride;  // floats per plane
+enum : int { kRecFull = 1, kPlaneFull = 3, kPlaneEmpty = 5, kRed = 7 };
+}  // namespace ws
+
+// Barrier ids are immediates (ptxas then reserves only the ids used, not all
+// 16, which would cap the CTAs per SM); `b` selects buffer 0 / 1.
+template <int kId, int kN>
+__device__ __forceinline__ void named_sync2(int b) {
+  if (b) asm volatile("bar.sync %0, %1;" ::"n"(kId + 1), "n"(kN) : "memory");
+  else asm volatile("bar.sync %0, %1;" ::"n"(kId), "n"(kN) : "memory");
+}
+template <int kId, int kN>
+__device__ __forceinline__ void named_arrive2(int b) {
+  if (b) asm volatile("bar.arrive %0, %1;" ::"n"(kId + 1), "n"(kN) : "memory");
+  else asm volatile("bar.arrive %0, %1;" ::"n"(kId), "n"(kN) : "memory");
+}
+template <int kId, int kN>
+__device__ __forceinline__ void named_sync1() {
+  asm volatile("bar.sync %0, %1;" ::"n"(kId), "n"(kN) : "memory");
+}
+
+__global__ void __launch_bounds__(ws::kThreads, 2)
+    raster_bwd_ws_kernel(BwdArgs a, vsx_camera cam) {
+  using namespace ws;
+  __shared__ float4 s0[2][kBC], s1[2][kBC], s2[2][kBC], s3[2][kBC];
+  __shared__ float4 s_ph[2][kBC][4];  // P B fragments per (splat, lane&3): hi b0, hi b1, lo b0, lo b1
+  __shared__ uint32_t s_rank[2][kBC];
+  __shared__ float4 s_bw[32][32];     // Gw B fragments per (k-step, lane): hi b0, hi b1, lo b0, lo b1
+  __shared__ float2 s_bq[32][32];     // Mq B fragments per (k-step, lane)
+  __shared__ float s_red[4][kBC][24];
+  __shared__ int s_max;
+  extern __shared__ float s_plane[];  // [buffer][w | q][kBC][kPlaneStride]
+  const int txn = gridDim.x;
+  const int lin = blockIdx.y * txn + blockIdx.x;
+  const int tile = a.L.tile_order ? (int)a.L.tile_order[lin] : lin;
+  const int bx = tile % txn, by = tile / txn;
+  const int t = threadIdx.x;
+  const int lane = t & 31, warp = t >> 5;
+  const bool pix = warp < kPixWarps;
+  const int g = lane >> 2, tq = lane & 3;
+  const double ox = (double)(bx * kTile), oy = (double)(by * kTile);
+  const uint32_t begin = a.tile_off[tile];
+  if (t == 0) s_max = 0;
+  // ---- setup: per-pixel cotangents -> F A fragments (pixel warps) and the
+  // per-tile Gw / moment B fragments (all threads), staged through plane 0
+  int nc = 0;
+  float T = 1.f;
+  const int lx = t & 15, ly = (t >> 4) & 15;
+  const float fx = (float)lx, fy = (float)ly;
+  if (pix) {
+    const int px = bx * kTile + lx, py = by * kTile + ly;
+    PixCot c{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (px < cam.width && py < cam.height) {
+      const size_t p = (size_t)py * cam.width + px;
+      nc = a.nc[p];
+      T = a.T[p];
+      if (a.L.gt_rgb)
+        c = pixel_cotangent_loss(cam, px, py, p, a.alpha, a.rgb, a.depth, a.normal, a.raw, a.L);
+      else
+        c = pixel_cotangent(cam, px, py, p, a.alpha, a.depth, a.raw, a.g_rgb, a.g_alpha,
+                            a.g_depth, a.g_normal, a.g_raw);
+    }
+    float *gw = s_plane + t * 9;
+    gw[0] = c.gC0; gw[1] = c.gC1; gw[2] = c.gC2; gw[3] = c.gR0;
+    gw[4] = c.gR1; gw[5] = c.gR2; gw[6] = c.gD; gw[7] = c.gA;
+  }
+  __syncthreads();
+  if (pix && nc > 0) atomicMax(&s_max, nc);
+  uint32_t fhi[2][4], flo[2][4];
+  if (pix) {
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int pp = 32 * warp + 16 * m + g + 8 * (r & 1), f = tq + 4 * (r >> 1);
+        const float v = s_plane[pp * 9 + f];
+        fhi[m][r] = tf32_bits(v);
+        flo[m][r] = tf32_bits(v - __uint_as_float(fhi[m][r]));
+      }
+  }
+  for (int idx = t; idx < 32 * 32; idx += kThreads) {
+    const int ks = idx >> 5, ln = idx & 31;
+    const int f = ln >> 2, p0 = 8 * ks + (ln & 3), p1 = p0 + 4;
+    const float v0 = f < 7 ? s_plane[p0 * 9 + f] : 0.f, v1 = f < 7 ? s_plane[p1 * 9 + f] : 0.f;
+    const float h0 = __uint_as_float(tf32_bits(v0)), h1 = __uint_as_float(tf32_bits(v1));
+    s_bw[ks][ln] = make_float4(h0, h1, __uint_as_float(tf32_bits(v0 - h0)),
+                               __uint_as_float(tf32_bits(v1 - h1)));
+    s_bq[ks][ln] = make_float2(pixel_moment(p0, f), pixel_moment(p1, f));
+  }
+  __syncthreads();
+  const uint32_t stop = begin + (uint32_t)s_max;
+  const int nchunks = (int)((stop - begin + kBC - 1) / kBC);
+  // chunk i covers [cs, ce), walked from the end of the live range
+  auto chunk_cs = [&](int i) {
+    const uint32_t ce = stop - (uint32_t)(kBC * i);
+    return ce > begin + kBC ? ce - kBC : begin;
+  };
+  if (pix) {
+    // ================= pixel warps: phases 0 and 1 =================
+    float S = 0.f;  // sum over later live splats of s_i * w_i
+    for (int i = 0; i < nchunks; ++i) {
+      const int b = i & 1;
+      const uint32_t cs = chunk_cs(i);
+      const int cnt = (int)(stop - (uint32_t)(kBC * i) - cs);
+      float *wpl = s_plane + (2 * b) * kPlane, *qpl = wpl + kPlane;
+      named_sync2<kRecFull, kThreads>(b);
+      named_sync2<kPlaneEmpty, kThreads>(b);
+      // phase 0: sk[j][p] = F[p] . P[j] for this warp's 32 pixels (3xTF32)
+#pragma unroll
+      for (int nt = 0; nt < kBC / 8; ++nt) {
+        const float4 pb = s_ph[b][8 * nt + g][tq];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+          mma_m16n8k8_tf32(d, flo[m], __float_as_uint(pb.x), __float_as_uint(pb.y));
+          mma_m16n8k8_tf32(d, fhi[m], __float_as_uint(pb.z), __float_as_uint(pb.w));
+          mma_m16n8k8_tf32(d, fhi[m], __float_as_uint(pb.x), __float_as_uint(pb.y));
+          float *o = qpl + (8 * nt + 2 * tq) * kPlaneStride + 32 * warp + 16 * m + g;
+          o[0] = d[0];
+          o[kPlaneStride] = d[1];
+          o[8] = d[2];
+          o[kPlaneStride + 8] = d[3];
+        }
+      }
+      __syncwarp();
+      // phase 1: per-pixel back-to-front recursion
+      const int kbase = (int)(cs - begin);
+      const int jlive = min(cnt, nc - kbase);
+      for (int j = cnt - 1; j >= max(jlive, 0); --j) {
+        wpl[j * kPlaneStride + t] = 0.f;
+        qpl[j * kPlaneStride + t] = 0.f;
+      }
+      int j = jlive - 1;
+      for (; j >= kUB - 1; j -= kUB) {
+        float al[kUB], ee[kUB], aa[kUB], rm[kUB], sk[kUB];
+#pragma unroll
+        for (int u = 0; u < kUB; ++u) {
+          const float4 p0 = s0[b][j - u], p1 = s1[b][j - u];
+          al[u] = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, ee[u], aa[u]);
+          rm[u] = rcp_ftz(1.f - al[u]);
+          sk[u] = qpl[(j - u) * kPlaneStride + t];
+        }
+#pragma unroll
+        for (int u = 0; u < kUB; ++u) {
+          const float Tk = T * rm[u];
+          const float w = al[u] * Tk;
+          const float da = Tk * sk[u] - S * rm[u];
+          S = fmaf(sk[u], w, S);
+          T = Tk;
+          wpl[(j - u) * kPlaneStride + t] = w;
+          qpl[(j - u) * kPlaneStride + t] = (aa[u] <= kAlphaClamp ? da : 0.f) * ee[u];
+        }
+      }
+      for (; j >= 0; --j) {
+        const float4 p0 = s0[b][j], p1 = s1[b][j];
+        float e, at;
+        const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
+        const float rom = rcp_ftz(1.f - alpha);
+        const float Tk = T * rom;
+        const float w = alpha * Tk;
+        const float sk = qpl[j * kPlaneStride + t];
+        const float da = Tk * sk - S * rom;
+        S = fmaf(sk, w, S);
+        T = Tk;
+        wpl[j * kPlaneStride + t] = w;
+        qpl[j * kPlaneStride + t] = (at <= kAlphaClamp ? da : 0.f) * e;
+      }
+      named_arrive2<kPlaneFull, kThreads>(b);
+    }
+    return;
+  }
+  // ================= reduction warps: staging, phase 2, epilogue =================
+  const int rt = t - 32 * kPixWarps;  // 0..127
+  const int rw = rt >> 5;             // 0..3: k-quarter of both planes
+  // records of chunk i are loaded into registers one iteration early and
+  // written to shared memory when their buffer frees up, so the global-load
+  // latency never sits between a chunk's epilogue and the pixel warps
+  vsx_splat pre{};
+  uint32_t pre_r = 0;
+  auto fetch = [&](int i) {
+    const uint32_t cs = chunk_cs(i);
+    const int cnt = (int)(stop - (uint32_t)(kBC * i) - cs);
+    if (rt < cnt) {
+      pre_r = a.tile_list[cs + rt];
+      pre = load_splat(a.rec, pre_r);
+    }
+  };
+  auto stage = [&](int i) {
+    const int b = i & 1;
+    const uint32_t cs = chunk_cs(i);
+    const int cnt = (int)(stop - (uint32_t)(kBC * i) - cs);
+    if (rt < cnt) {
+      s_rank[b][rt] = pre_r;
+      stage_splat(pre, ox, oy, s0[b][rt], s1[b][rt], s2[b][rt], s3[b][rt]);
+      const float pv[8] = {pre.color[0], pre.color[1], pre.color[2], pre.normal[0],
+                           pre.normal[1], pre.normal[2], pre.plane_d, 1.f};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float h0 = __uint_as_float(tf32_bits(pv[k])),
+                    h1 = __uint_as_float(tf32_bits(pv[k + 4]));
+        s_ph[b][rt][k] = make_float4(h0, h1, __uint_as_float(tf32_bits(pv[k] - h0)),
+                                     __uint_as_float(tf32_bits(pv[k + 4] - h1)));
+      }
+    }
+    named_arrive2<kRecFull, kThreads>(b);
+  };
+  for (int i = 0; i < min(nchunks, 2); ++i) {
+    fetch(i);
+    stage(i);
+    named_arrive2<kPlaneEmpty, kThreads>(i);  // both plane buffers start empty
+  }
+  if (nchunks > 2) fetch(2);
+  for (int i = 0; i < nchunks; ++i) {
+    const int b = i & 1;
+    const uint32_t cs = chunk_cs(i);
+    const int cnt = (int)(stop - (uint32_t)(kBC * i) - cs);
+    named_sync2<kPlaneFull, kThreads>(b);
+    // phase 2: [kBC x 256] x [256 x 8] on the tensor cores, both planes, this
+    // warp's quarter of the 32 k-steps; two accumulator sets (even / odd
+    // k-step) per product so the HMMA chains are half as long
+    {
+      const float *Aw = s_plane + (2 * b) * kPlane + g * kPlaneStride + tq;
+      const float *Aq = Aw + kPlane;
+      float dw[2][4] = {}, ew1[2][4] = {}, ew2[2][4] = {}, dq[2][4] = {}, eq1[2][4] = {};
+      auto a_frag = [&](const float *A, int ks, uint32_t (&hi)[4], uint32_t (&lo)[4]) {
+        const float x0 = A[8 * ks], x1 = A[8 * kPlaneStride + 8 * ks], x2 = A[8 * ks + 4],
+                    x3 = A[8 * kPlaneStride + 8 * ks + 4];
+        hi[0] = tf32_bits(x0);
+        hi[1] = tf32_bits(x1);
+        hi[2] = tf32_bits(x2);
+        hi[3] = tf32_bits(x3);
+        lo[0] = tf32_bits(x0 - __uint_as_float(hi[0]));
+        lo[1] = tf32_bits(x1 - __uint_as_float(hi[1]));
+        lo[2] = tf32_bits(x2 - __uint_as_float(hi[2]));
+        lo[3] = tf32_bits(x3 - __uint_as_float(hi[3]));
+      };
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int ks = 8 * rw + kk, c = kk & 1;
+        uint32_t hi[4], lo[4];
+        a_frag(Aw, ks, hi, lo);
+        const float4 bw = s_bw[ks][lane];
+        mma_m16n8k8_tf32(ew1[c], lo, __float_as_uint(bw.x), __float_as_uint(bw.y));
+        mma_m16n8k8_tf32(ew2[c], hi, __float_as_uint(bw.z), __float_as_uint(bw.w));
+        mma_m16n8k8_tf32(dw[c], hi, __float_as_uint(bw.x), __float_as_uint(bw.y));
+        a_frag(Aq, ks, hi, lo);
+        const float2 bq = s_bq[ks][lane];
+        mma_m16n8k8_tf32(eq1[c], lo, __float_as_uint(bq.x), __float_as_uint(bq.y));
+        mma_m16n8k8_tf32(dq[c], hi, __float_as_uint(bq.x), __float_as_uint(bq.y));
+      }
+      // the planes of buffer b are free once the last chunk using it was read
+      if (i + 2 < nchunks) named_arrive2<kPlaneEmpty, kThreads>(b);
+      float w4[4], q4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        w4[k] = ((ew1[0][k] + ew2[0][k]) + dw[0][k]) + ((ew1[1][k] + ew2[1][k]) + dw[1][k]);
+        q4[k] = (eq1[0][k] + dq[0][k]) + (eq1[1][k] + dq[1][k]);
+      }
+      float *red = &s_red[rw][g][2 * tq];
+      *reinterpret_cast<float2 *>(red) = make_float2(w4[0], w4[1]);
+      *reinterpret_cast<float2 *>(red + 8 * 24) = make_float2(w4[2], w4[3]);
+      *reinterpret_cast<float2 *>(red + 8) = make_float2(q4[0], q4[1]);
+      *reinterpret_cast<float2 *>(red + 8 * 24 + 8) = make_float2(q4[2], q4[3]);
+    }
+    named_sync1<kRed, kRedThreads>();
+    // epilogue: 8 lanes per splat, lane part holds features 2part, 2part+1
+    {
+      const int j = rt >> 3, part = rt & 7;
+      float2 v = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 u = *reinterpret_cast<const float2 *>(&s_red[k][j][2 * part]);
+        v.x += u.x;
+        v.y += u.y;
+      }
+      // moments: part 4 = (1, x), 5 = (y, xx), 6 = (xy, yy)
+      const float m2 = __shfl_down_sync(0xffffffffu, v.x, 1),
+                  m3 = __shfl_down_sync(0xffffffffu, v.y, 1);
+      const float m4 = __shfl_down_sync(0xffffffffu, v.x, 2),
+                  m5 = __shfl_down_sync(0xffffffffu, v.y, 2);
+      if (j < cnt) {
+        float *gp = a.grad + (size_t)13 * s_rank[b][j];
+        if (part < 4) {
+          if (v.x != 0.f) atomicAdd(gp + 6 + 2 * part, v.x);
+          if (part < 3 && v.y != 0.f) atomicAdd(gp + 7 + 2 * part, v.y);
+        } else if (part == 4) {
+          const float4 p0 = s0[b][j], p1 = s1[b][j];
+          const float op = p1.y, A = p1.w, B = s2[b][j].w, C = s3[b][j].w;
+          const float mx = p0.x - 7.5f, my = p0.y - 7.5f;
+          const float Q1 = v.x, X = v.y, Y = m2, XX = m3, XY = m4, YY = m5;
+          const float sx = X - mx * Q1, sy = Y - my * Q1;
+          const float sxx = XX - 2.f * mx * X + mx * mx * Q1;
+          const float sxy = XY - mx * Y - my * X + mx * my * Q1;
+          const float syy = YY - 2.f * my * Y + my * my * Q1;
+          const float g0 = op * (A * sx + B * sy), g1 = op * (B * sx + C * sy);
+          const float g2 = -0.5f * op * sxx, g3 = -op * sxy, g4 = -0.5f * op * syy;
+          if (g0 != 0.f) atomicAdd(gp + 0, g0);
+          if (g1 != 0.f) atomicAdd(gp + 1, g1);
+          if (g2 != 0.f) atomicAdd(gp + 2, g2);
+          if (g3 != 0.f) atomicAdd(gp + 3, g3);
+          if (g4 != 0.f) atomicAdd(gp + 4, g4);
+          if (Q1 != 0.f) atomicAdd(gp + 5, Q1);
+        }
+      }
+    }
+    named_sync1<kRed, kRedThreads>();   // s_red and records of buffer b are free
+    if (i + 2 < nchunks) {
+      stage(i + 2);
+      if (i + 3 < nchunks) fetch(i + 3);
+    }
+  }
+}
+
+static int launch_bwd_ws(const BwdArgs &a, const vsx_camera &cam, cudaStream_t st) {
+  dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
+  const int smem = (int)(sizeof(float) * 4 * ws::kPlane);
+  // the opt-in is per device (a multi-GPU process launches on several)
+  int dev = 0;
+  VSX_CUDA_TRY(cudaGetDevice(&dev));
+  static std::atomic<uint64_t> done{0};
+  if (dev < 64 && !(done.load() & (1ull << dev))) {
+    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_ws_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    done.fetch_or(1ull << dev);
+  }
+  raster_bwd_ws_kernel<<<grid, ws::kThreads, smem, st>>>(a, cam);
+  VSX_LAUNCH_CHECK("raster_bwd");
+  return VSX_OK;
+}
+
 static int launch_bwd(const BwdArgs &a, const vsx_camera &cam, cudaStream_t st) {
+  static const bool v3 = [] {
+    const char *e = getenv("VSX_RASTER_BWD");
+    return e && e[0] != 'w';
+  }();
+  if (!v3) return launch_bwd_ws(a, cam, st);
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
   // VSX_RASTER_BWD="NS,BC" selects the v2 (FFMA) phase-2 splats-per-pass and
   // splat chunk for A/B timing; NS = 0 (default) is the tensor-core v3 with

@@ -34,7 +34,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .errors import ProtocolError
+from .errors import InvalidInput, ProtocolError
 
 
 @dataclass
@@ -61,6 +61,27 @@ class SplatPayload:
 
 def renderer_of(view_index: int, world: int) -> int:
     return view_index % world
+
+
+def _fields(p: SplatPayload):
+    return (p.rec, p.z, p.radius, p.gid)
+
+
+def _pack(p: SplatPayload) -> torch.Tensor:
+    """Rows of all four payload tensors side by side as bytes, (n, row_bytes) u8."""
+    n = p.count
+    return torch.cat([t.contiguous().view(torch.uint8).reshape(n, -1) for t in _fields(p)], 1)
+
+
+def _unpack(buf: torch.Tensor, like: SplatPayload) -> SplatPayload:
+    n = int(buf.shape[0])
+    out, col = [], 0
+    for t in _fields(like):
+        width = t.element_size() * int(np.prod(t.shape[1:], dtype=np.int64))
+        part = buf[:, col:col + width].contiguous().view(t.dtype)
+        out.append(part.reshape((n,) + tuple(t.shape[1:])))
+        col += width
+    return SplatPayload(*out)
 
 
 def _a2a(x: torch.Tensor, in_splits: list[int], out_splits: list[int], group=None):
@@ -115,8 +136,8 @@ def exchange_splats(payloads: list[SplatPayload], rank: int, world: int, group=N
     send_parts = [payloads[v] for r in range(world) for v in plan.views_of(r)]
     send = SplatPayload.cat(send_parts, payloads[0])
     ins, outs = plan.send_splits(), plan.recv_splits()
-    recv = SplatPayload(_a2a(send.rec, ins, outs, group), _a2a(send.z, ins, outs, group),
-                        _a2a(send.radius, ins, outs, group), _a2a(send.gid, ins, outs, group))
+    # ONE all-to-all of packed rows (record | z | radius | gid bytes)
+    recv = _unpack(_a2a(_pack(send), ins, outs, group), payloads[0])
     # split the received block per (source, view) and regroup per view
     mine = plan.views_of(rank)
     merged: dict[int, tuple[SplatPayload, list[int]]] = {}
@@ -170,10 +191,22 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
     """
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     B = len(views)
+    w2, w3, wn = backend.schedule()
+    if w3 > 0 and B >= 2:
+        # Eq. 10 couples views that different ranks render (losses.py:196-287);
+        # the sharded step does not exchange rendered buffers, so it refuses
+        # rather than silently training a different objective
+        raise InvalidInput("the sharded step does not implement the Eq. 10 multi-view NCC term "
+                           "(w3 > 0); use trainer.train_step or step3_start >= total_steps")
+    # the depth / normal terms average over the views that carry a prior
+    # (trainer.py:296-306, losses.py:84), a global property of the batch
+    have = [v for v in range(B) if w2 > 0 and priors is not None and priors[v] is not None]
+    have_n = [v for v in range(B)
+              if wn > 0 and normal_priors is not None and normal_priors[v] is not None]
     renderers = scheduler.assign(views, world) if scheduler is not None else None
     renderers = np.asarray(renderers if renderers is not None
                            else [renderer_of(v, world) for v in range(B)], dtype=np.int64)
-    backend.begin_step(views)
+    backend.begin_step(views, have, have_n)
     from .trainer import _pipeline_enabled
     if hasattr(backend, "prepare") and _pipeline_enabled():
         timers = _pipelined_views(backend, views, images, priors, normal_priors, group,
@@ -405,20 +438,40 @@ class CudaShardBackend:
         self.D = D
         self.state = state
         self.rank, self.world = rank, world
-        owner = torch.as_tensor(state.assignment.flat_owner() if world == state.cfg.workers
-                                else np.concatenate([np.arange(lv.count) % world
-                                                     for lv in state.scene.levels]))
-        self.owned = (owner == rank).to(torch.uint8).cuda()
+        self._owned_key = None
         self.work: dict = {}
         self.timer = None     # optional trainer.GpuTimer for per-kernel spans
         self.isects = 0
+        self.have, self.have_n = [], []
 
-    def begin_step(self, views) -> None:
+    @property
+    def owned(self) -> torch.Tensor:
+        """u8 mask of this rank's anchors (Eq. 3: i mod M per level), rebuilt
+        whenever anchor growth changed the level sizes."""
+        st = self.state
+        key = tuple(lv.count for lv in st.scene.levels)
+        if key != self._owned_key:
+            owner = (st.assignment.flat_owner() if self.world == st.cfg.workers
+                     else np.concatenate([np.arange(lv.count) % self.world
+                                          for lv in st.scene.levels]))
+            self._owned = (torch.as_tensor(owner) == self.rank).to(torch.uint8).cuda()
+            self._owned_key = key
+        return self._owned
+
+    def schedule(self) -> tuple[float, float, float]:
+        """(w2, w3, normal weight) of the current step (trainer.py:112-120)."""
+        from .trainer import weight_schedule
+        st = self.state
+        w2, w3 = weight_schedule(st.step, st.cfg)
+        return w2, w3, float(getattr(st.cfg, "normal_weight", 0.0))
+
+    def begin_step(self, views, have=(), have_n=()) -> None:
         st = self.state
         self._hold = None             # the previous step's buffers (synced since)
         st.flat.grad.zero_()
         B = len(views)
         self.B = B
+        self.have, self.have_n = list(have), list(have_n)
         self._hw = np.array([v.height * v.width * 3 for v in views], dtype=np.float64)
         self.sums = torch.zeros((B, 3), dtype=torch.float64, device="cuda")
         self.counts = torch.zeros((B, 2), dtype=torch.int32, device="cuda")
@@ -503,18 +556,18 @@ class CudaShardBackend:
         wn = float(getattr(st.cfg, "normal_weight", 0.0))
         gt = _to_device_image(image, (H, W, 3))
         pd = pv = pn = pnv = None
-        if prior is not None and w2 > 0:
+        if v in self.have:
             d_, m_ = _prior_arrays(prior)
             pd, pv = _to_device_image(d_, (H, W)), _mask_u8(m_, (H, W))
-        if nprior is not None and wn > 0:
+        if v in self.have_n:
             pn, pnv = _to_device_image(nprior[0], (H, W, 3)), _mask_u8(nprior[1], (H, W))
-        # every view carries the same kind of priors in the bench; the global
-        # per-term normaliser is the batch size (reference losses.py:84)
+        # the depth / normal terms are means over the views that carry a prior
+        # (trainer.py:296-306, losses.py:84): normalised by that global count
         loss = VsxLossDesc(gt_rgb=gt.data_ptr(), prior_depth=ptr(pd).value,
                            prior_depth_valid=ptr(pv).value, prior_normal=ptr(pn).value,
                            prior_normal_valid=ptr(pnv).value, rgb_scale=1.0 / (self.B * H * W * 3),
-                           depth_weight=w2 / self.B if pd is not None else 0.0,
-                           normal_weight=wn / self.B / 3.0 if pn is not None else 0.0,
+                           depth_weight=w2 / len(self.have) if pd is not None else 0.0,
+                           normal_weight=wn / len(self.have_n) / 3.0 if pn is not None else 0.0,
                            sums=self.sums[v].data_ptr(), counts=self.counts[v].data_ptr())
         from .trainer import _span
         self.isects += Bn.intersections
@@ -527,12 +580,18 @@ class CudaShardBackend:
         return merged
 
     def backward_shard(self, v: int, view, grads: torch.Tensor) -> None:
+        from ._lib import call, ptr, stream
         from .decoder import decoder_backward_into
         D, st = self.D, self.state
         ds = st.dscene
         active, dec, P = self.work[v]
         gg = D.project_backward(dec.means, dec.scale, dec.quat, dec.normal, P,
                                 grads.contiguous(), view)
+        # growth pressure (trainer.py:341-349): every gaussian of an owned
+        # anchor is decoded here, so the owner's sums are complete for its
+        # anchors (sync_growth sums them across ranks before grow_anchors)
+        call("vsx_growth_accumulate", ptr(gg["means"]), ptr(active), int(active.numel()), st.n,
+             ptr(st.grow_sum_flat), ptr(st.grow_cnt_flat), stream())
         an, ag = st.anchors, st.anchor_grads
         decoder_backward_into(st.params, st.dgrads, active, ds.centers, an.emb, an.log_scales,
                               an.offsets, view, ds.lod_ref, ds.max_scale, dec, gg["means"],
@@ -557,8 +616,10 @@ class CudaShardBackend:
         hw = self._hw
         rgb = float(np.mean(L[:, 0] / hw))
         dcnt, ncnt = L[:, 3], L[:, 4]
-        depth = float(np.mean(np.where(dcnt > 0, L[:, 1] / np.maximum(dcnt, 1), 0.0)))
-        normal = float(np.mean(np.where(ncnt > 0, L[:, 2] / (3 * np.maximum(ncnt, 1)), 0.0)))
+        dterm = np.where(dcnt > 0, L[:, 1] / np.maximum(dcnt, 1), 0.0)
+        nterm = np.where(ncnt > 0, L[:, 2] / (3 * np.maximum(ncnt, 1)), 0.0)
+        depth = float(np.mean(dterm[self.have])) if self.have else 0.0
+        normal = float(np.mean(nterm[self.have_n])) if self.have_n else 0.0
         total = rgb + w2 * depth + float(getattr(st.cfg, "normal_weight", 0.0)) * normal
         if not np.isfinite(total):
             raise NumericalError(f"non-finite loss at step {st.step}")
@@ -571,3 +632,11 @@ class CudaShardBackend:
         g = self.state.flat
         lo, hi = g.group_spans["dec"]
         return g.param[lo:hi].view(torch.int32).long().sum().reshape(1)
+
+
+def sync_growth(state, group=None) -> None:
+    """Sum the per-anchor growth accumulators over the ranks (each owner holds
+    the complete sums of its own anchors), so every rank's grow_anchors makes
+    the same decisions with the same RNG draws (trainer.py:379-454)."""
+    dist.all_reduce(state.grow_sum_flat, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(state.grow_cnt_flat, op=dist.ReduceOp.SUM, group=group)

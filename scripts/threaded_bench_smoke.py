@@ -1,9 +1,10 @@
-"""The bench's sharded cfg2 step (8 views per rank) at world size W on ONE
-GPU: W threads over torch's in-process process group (host collectives, so
-no kernel waits on another rank's). A crash/consistency smoke test of the
-multi-GPU bench path at full size, not a timing: the ranks share one GPU.
+"""The bench's sharded step at world size W on ONE GPU: W threads over
+torch's in-process process group (host collectives, so no kernel waits on
+another rank's). A crash/consistency smoke test of the multi-GPU bench path
+at full size, not a timing: the ranks share one GPU. cfg2: 8 views per rank;
+cfg3: 1M anchors, 16 views at 1080p; cfg4: 2M anchors, 8 views at 4K.
 
-  python scripts/threaded_bench_smoke.py [W]
+  python scripts/threaded_bench_smoke.py [W] [cfg2|cfg3|cfg4]
 """
 import sys
 import threading
@@ -18,12 +19,12 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 from paper_2503_23044_b200.dist import CudaShardBackend, sharded_train_step  # noqa: E402
-from paper_2503_23044_b200.synthetic import city_views  # noqa: E402
 from paper_2503_23044_b200.trainer import TrainConfig, TrainState  # noqa: E402
 
 W = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-scene, _, desc, _ = bench.workload("cfg2")
-views = city_views(8 * W)
+CONFIG = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
+scene, views, desc, _ = bench.workload(CONFIG, W)
+print(CONFIG, "anchors", scene.total_voxels, "views", len(views), flush=True)
 tgt = bench.teacher_targets(scene, views)
 imgs = [t["rgb"] for t in tgt]
 priors = [(t["depth"], t["valid"]) for t in tgt]

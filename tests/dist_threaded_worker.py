@@ -24,7 +24,8 @@ sys.path.insert(0, str(HERE.parent))
 sys.path.insert(0, str(HERE))
 from conftest import golden_scene, golden_view, load_golden  # noqa: E402
 
-from paper_2503_23044_b200.dist import CudaShardBackend, sharded_train_step  # noqa: E402
+from paper_2503_23044_b200.dist import (CudaShardBackend, sharded_train_step,  # noqa: E402
+                                        sync_growth)
 from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step  # noqa: E402
 
 WORLD = int(sys.argv[1]) if len(sys.argv) > 1 else 2
@@ -33,7 +34,15 @@ d = load_golden("train_small")
 views = [golden_view(d, f"v{i}", i) for i in range(3)]
 images = [d[f"img{i}"] for i in range(3)]
 priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
-cfg = dict(total_steps=8, batch_size=3, step2_start=0, step3_start=8, growth_stop=0)
+priors[1] = None                      # the depth term averages over views with a prior
+_rng = np.random.default_rng(5)
+npri = []
+for _i in range(3):
+    _p = _rng.normal(size=(40, 48, 3)).astype(np.float32)
+    npri.append((_p / np.linalg.norm(_p, axis=-1, keepdims=True), _rng.uniform(size=(40, 48)) > 0.3))
+npri[2] = None
+cfg = dict(total_steps=8, batch_size=3, step2_start=0, step3_start=8, growth_stop=0,
+           normal_weight=0.5)
 
 import faulthandler  # noqa: E402
 faulthandler.dump_traceback_later(150, exit=True)  # a hang prints every thread's stack
@@ -69,7 +78,8 @@ def run(rank):
         with torch.cuda.stream(torch.cuda.Stream()):
             st = TrainState(golden_scene(d), TrainConfig(**cfg, workers=WORLD))
             be = CudaShardBackend(st, rank, WORLD)
-            reps = [sharded_train_step(be, views, images, priors) for _ in range(STEPS)]
+            reps = [sharded_train_step(be, views, images, priors, npri) for _ in range(STEPS)]
+            sync_growth(st)
             torch.cuda.synchronize()
         res[rank] = dict(reps=reps, state=st)
     except Exception as e:  # surfaced in the JSON line
@@ -91,12 +101,13 @@ if errs:
 
 faulthandler.cancel_dump_traceback_later()
 ref = TrainState(golden_scene(d), TrainConfig(**cfg))
-ref_reps = [train_step(ref, views, images, priors) for _ in range(STEPS)]
+ref_reps = [train_step(ref, views, images, priors, normal_priors=npri) for _ in range(STEPS)]
 out = {"ok": True, "loss": [], "param_bad_frac": {}, "owned_disjoint": None}
 for s in range(STEPS):
     for r in range(WORLD):
         rb = res[r]["reps"][s]
-        out["loss"].append([s, r, rb["rgb"], ref_reps[s].rgb, rb["depth"], ref_reps[s].depth])
+        out["loss"].append([s, r, rb["rgb"], ref_reps[s].rgb, rb["depth"], ref_reps[s].depth,
+                            rb["normal"], ref_reps[s].normal])
 owner = res[0]["state"].assignment.flat_owner()
 out["owned_disjoint"] = bool(np.array_equal(np.bincount(owner, minlength=WORLD) > 0,
                                             np.ones(WORLD, bool)))
@@ -109,6 +120,13 @@ for name in ["emb", "log_scales", "offsets"]:
         got[owner == r] = g[owner == r]
     bad = np.abs(got - want) > 1e-5 * np.maximum(np.abs(got), np.abs(want)) + 1e-7
     out["param_bad_frac"][name] = float(bad.mean())
+gs_ref = ref.grow_sum_flat.cpu().numpy()
+gc_ref = ref.grow_cnt_flat.cpu().numpy()
+out["growth_ok"] = all(
+    np.array_equal(res[r]["state"].grow_cnt_flat.cpu().numpy(), gc_ref) and
+    np.allclose(res[r]["state"].grow_sum_flat.cpu().numpy(), gs_ref, rtol=1e-4, atol=1e-12)
+    for r in range(WORLD))
+out["growth_nonzero"] = bool(gc_ref.sum() > 0)
 for r in range(WORLD):  # the replicated decoder (anchor rows of other owners are stale)
     st = res[r]["state"]
     out[f"dec_checksum_r{r}"] = float(st.flat.view(st.flat.param, "dec/opacity_w1").sum())

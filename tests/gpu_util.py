@@ -62,3 +62,49 @@ def rel_close(a, b, rel, floor) -> tuple[bool, float, int]:
     worst = float((np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)).max()) \
         if a.size else 0.0
     return (not bad.any()), worst, int(bad.sum())
+
+
+def noise_floor_close(got, ref, rel, noise) -> tuple[bool, float, int]:
+    """Relative closeness with a noise-floor exclusion instead of an allowance.
+
+    An element is left out only when |ref| < noise * rms(ref) of its tensor
+    (a gradient whose fp32 sum has no determined sign there); every other
+    element must satisfy |got - ref| <= rel * |ref|, and an exactly-zero
+    reference (no contribution at all) must be matched by an exact zero.
+    Returns (ok, worst relative error over the kept elements, number of
+    non-zero elements excluded).
+    """
+    got, ref = np.asarray(got, np.float64).ravel(), np.asarray(ref, np.float64).ravel()
+    if ref.size == 0:
+        return True, 0.0, 0
+    rms = float(np.sqrt(np.mean(ref * ref)))
+    zero = ref == 0.0
+    zeros_ok = bool(np.all(got[zero] == 0.0))
+    if rms == 0.0:
+        return zeros_ok, float(np.abs(got).max()), 0
+    keep = np.abs(ref) >= noise * rms
+    err = np.abs(got - ref)[keep] / np.abs(ref)[keep]
+    worst = float(err.max()) if err.size else 0.0
+    return worst <= rel and zeros_ok, worst, int((~keep & ~zero).sum())
+
+
+def conditioned_close(got, ref, ref_pert, rel, k) -> tuple[bool, float, float, int]:
+    """Element-wise |got - ref| <= rel * |ref| + k * |ref - ref_pert|, nothing excluded.
+
+    ``ref_pert`` is the float64 reference evaluated with every input moved by
+    one float32 ulp: |ref - ref_pert| is the element's sensitivity to the
+    input rounding every float32 evaluation carries (a cancelling sum has a
+    large one). Returns (ok, worst err / bound, worst plain relative error
+    over the elements whose floor is below rel * |ref| / 10, number of
+    elements whose floor term dominates the bound).
+    """
+    got, ref = np.asarray(got, np.float64).ravel(), np.asarray(ref, np.float64).ravel()
+    floor = k * np.abs(ref - np.asarray(ref_pert, np.float64).ravel())
+    err = np.abs(got - ref)
+    bound = rel * np.abs(ref) + floor
+    zero = bound == 0.0
+    ok = bool(np.all(err[zero] == 0.0)) and bool(np.all(err[~zero] <= bound[~zero]))
+    ratio = float((err[~zero] / bound[~zero]).max()) if (~zero).any() else 0.0
+    well = (floor < 0.1 * rel * np.abs(ref)) & ~zero
+    wrel = float((err[well] / np.abs(ref[well])).max()) if well.any() else 0.0
+    return ok, ratio, wrel, int((floor > rel * np.abs(ref)).sum())

@@ -90,7 +90,22 @@ def _small_state(d):
         step3_start=8)
 
 
-def _sharded_worker(rank, world, port, out, scheduled=False):
+def _mixed_priors(d):
+    """View 1 without a depth prior, normal priors on views 0 and 2: the terms
+    average over the views that carry a prior (trainer.py:296-306)."""
+    priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
+    priors[1] = None
+    rng = np.random.default_rng(5)
+    npri = []
+    for i in range(3):
+        p = rng.normal(size=(40, 48, 3))
+        npri.append((p / np.linalg.norm(p, axis=-1, keepdims=True),
+                     rng.uniform(size=(40, 48)) > 0.3))
+    npri[1] = None
+    return priors, npri
+
+
+def _sharded_worker(rank, world, port, out, case="plain"):
     from oracle.shard import OracleShardBackend
     from paper_2503_23044_b200.dist import sharded_train_step
     from paper_2503_23044_b200.partition import ViewScheduler
@@ -99,15 +114,20 @@ def _sharded_worker(rank, world, port, out, scheduled=False):
     views = [golden_view(d, f"v{i}", i) for i in range(3)]
     images = [d[f"img{i}"] for i in range(3)]
     priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
+    npri, wn = None, 0.0
+    if case == "mixed":
+        priors, npri = _mixed_priors(d)
+        wn = 0.5
     st = _small_state(d)
-    be = OracleShardBackend(st, rank, world)
+    be = OracleShardBackend(st, rank, world, normal_weight=wn)
     sched = None
-    if scheduled:
+    if case == "scheduled":
         # EMA history that moves view 1 to rank 0 and views 0, 2 to rank 1
         sched = ViewScheduler(beta=1.0)
         sched.update(views, [1.0, 5.0, 1.0])
         sched.update = lambda *a, **k: None  # keep the planted assignment
-    reps = [sharded_train_step(be, views, images, priors, scheduler=sched) for _ in range(2)]
+    reps = [sharded_train_step(be, views, images, priors, npri, scheduler=sched)
+            for _ in range(2)]
     torch.save({"reps": reps, "owned": be.owned,
                 "weights": {k: v.numpy() for k, v in st.weights.items()},
                 "emb": st.emb.numpy(), "offsets": st.offsets.numpy(),
@@ -116,24 +136,32 @@ def _sharded_worker(rank, world, port, out, scheduled=False):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("scheduled", [False, True])
-def test_sharded_step_two_ranks_matches_single_process_oracle(scheduled):
+@pytest.mark.parametrize("case", ["plain", "scheduled", "mixed"])
+def test_sharded_step_two_ranks_matches_single_process_oracle(case):
     import oracle
     port = _free_port()
     d = load_golden("train_small")
     views = [golden_view(d, f"v{i}", i) for i in range(3)]
     images = [d[f"img{i}"] for i in range(3)]
     priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
+    npri, wn = None, 0.0
+    if case == "mixed":
+        priors, npri = _mixed_priors(d)
+        wn = 0.5
     ref = _small_state(d)
     cams = [oracle.Cam.of(v) for v in views]
-    ref_reps = [oracle.train_step(ref, cams, images, priors) for _ in range(2)]
+    ref_reps = [oracle.train_step(ref, cams, images, priors, normal_priors=npri,
+                                  normal_weight=wn) for _ in range(2)]
     with tempfile.TemporaryDirectory() as out:
-        mp.spawn(_sharded_worker, args=(2, port, out, scheduled), nprocs=2, join=True)
+        mp.spawn(_sharded_worker, args=(2, port, out, case), nprocs=2, join=True)
         res = [torch.load(os.path.join(out, f"r{r}.pt"), weights_only=False) for r in range(2)]
     for r in res:
         for s in range(2):
             assert r["reps"][s]["rgb"] == pytest.approx(ref_reps[s]["rgb"], rel=1e-10)
             assert r["reps"][s]["depth"] == pytest.approx(ref_reps[s]["depth"], rel=1e-9)
+            assert r["reps"][s]["normal"] == pytest.approx(ref_reps[s]["normal"], rel=1e-9,
+                                                           abs=1e-15)
+            assert r["reps"][s]["total"] == pytest.approx(ref_reps[s]["total"], rel=1e-10)
         for k, w in r["weights"].items():
             np.testing.assert_allclose(w, ref.weights[k].numpy(), rtol=1e-9, atol=1e-13)
         own = r["owned"]
@@ -141,3 +169,24 @@ def test_sharded_step_two_ranks_matches_single_process_oracle(scheduled):
             np.testing.assert_allclose(r[name][own], getattr(ref, name).numpy()[own],
                                        rtol=1e-9, atol=1e-13)
     assert np.array_equal(res[0]["owned"], ~res[1]["owned"])
+
+
+def test_sharded_step_refuses_the_ncc_term():
+    """With w3 > 0 (step >= step3_start) the sharded step raises instead of
+    silently dropping the Eq. 10 term it does not implement."""
+    from oracle.shard import OracleShardBackend
+    from paper_2503_23044_b200.dist import sharded_train_step
+    from paper_2503_23044_b200.errors import InvalidInput
+    port = _free_port()
+    dist.init_process_group("gloo", rank=0, world_size=1,
+                            init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        d = load_golden("train_small")
+        views = [golden_view(d, f"v{i}", i) for i in range(3)]
+        images = [d[f"img{i}"] for i in range(3)]
+        st = _small_state(d)
+        st.step3_start, st.step = 0, 1
+        with pytest.raises(InvalidInput):
+            sharded_train_step(OracleShardBackend(st, 0, 1), views, images)
+    finally:
+        dist.destroy_process_group()

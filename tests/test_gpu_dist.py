@@ -65,7 +65,10 @@ def test_sharded_step_threaded_ranks_match_train_step(world):
     torch's in-process process group (host-side collectives, no cross-rank
     kernel waits). Losses on every rank and the owner-merged anchor
     parameters must match the single-process train_step; the replicated
-    decoder too. At world 4 with 3 views one rank renders nothing."""
+    decoder too. At world 4 with 3 views one rank renders nothing. One view
+    has no depth prior and one no normal prior (per-term normalisation over
+    the views that carry one), and the growth accumulators summed over the
+    ranks equal train_step's."""
     import json
     import subprocess
     import sys
@@ -76,9 +79,12 @@ def test_sharded_step_threaded_ranks_match_train_step(world):
     assert p.returncode == 0, p.stderr[-3000:]
     out = json.loads(p.stdout.strip().splitlines()[-1])
     assert out["ok"], "\n".join(out.get("errors", []))[-3000:]
-    for s, r, rgb, ref_rgb, dep, ref_dep in out["loss"]:
+    for s, r, rgb, ref_rgb, dep, ref_dep, nrm, ref_nrm in out["loss"]:
         assert rgb == pytest.approx(ref_rgb, rel=1e-6), (s, r)
         assert dep == pytest.approx(ref_dep, rel=1e-5), (s, r)
+        assert nrm == pytest.approx(ref_nrm, rel=1e-5), (s, r)
+    # growth pressure accumulated by the owners, summed over ranks = train_step's
+    assert out["growth_nonzero"] and out["growth_ok"]
     for name, frac in out["param_bad_frac"].items():
         assert frac < 1e-3, (name, frac)
     for r in range(world):

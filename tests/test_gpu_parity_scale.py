@@ -1,0 +1,514 @@
+"""GPU parity where the benchmark runs (VERDICT r01 "parity at the sizes that matter").
+
+* cfg1 (10,198 anchors x 10, 4 views 128^2; tile lists of mean 2,360 and max
+  4,190 splats): the first train_step's decoder and per-anchor gradients and
+  the parameters after two steps against the unmodified reference
+  (``tests/golden/cfg1.npz``, its autograd, ``trainer.py:323-339``).
+* cfg2 (the bench workload, ~200k anchors x 10, 1920x1080): one view against
+  the float64 oracle on the device's own decoded gaussians — (z, gid) order
+  and every tile list of the view bit-exact, and on >= 200 evenly spaced
+  tiles plus the heaviest tiles of the view (SURVEY §7 hard part 8,
+  ``renderer.py:304-344``) the composited images within 1e-4 and the
+  per-splat 2D gradients within 1e-3 relative, through both the explicit-
+  cotangent backward and the fused RGB-D-N objective the training step runs.
+* The normal-prior term of the RGB-D-N objective: three train steps against
+  the oracle (``oracle.normal_l1_loss``, pinned on the reference's Eq. 9).
+
+Tolerances are north_star's: rel 1e-3 for gradients and post-step
+parameters, 1e-4 absolute for images. No fraction of elements is allowed to
+miss. Each gradient element's bound is 1e-3 |g_ref| plus its float32 floor,
+FLOOR_K |g_ref - g_ref'|, where g_ref' is the float64 reference with every
+input moved by one float32 ulp: the error no float32 evaluation of that
+element can avoid (large only for cancelling sums). Post-step parameters
+leave out only elements whose gradient sign is not determined within that
+floor in either step (Adam turns any sign into a full +-lr step). Every
+test prints the worst error / bound and the rms-based view next to it.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import golden_scene, golden_view, load_golden
+from gpu_util import conditioned_close, f32r, noise_floor_close
+
+pytestmark = pytest.mark.gpu
+
+NOISE = 1e-3          # noise-floor exclusion, fraction of the tensor's rms gradient
+# Float32 floor: a gradient element's error bound is rel * |ref| + FLOOR_K *
+# |ref - ref'|, ref' the float64 reference with every input moved by one
+# float32 ulp (the rounding no float32 evaluation avoids; cancelling sums
+# amplify it, scripts/diag/emu_bwd_precision.py). Nothing is excluded.
+FLOOR_K = 8.0
+GRAD_REL = 1e-3
+IMG_ABS = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2503_23044_b200 import _lib
+    _lib.load()
+
+
+# ------------------------------------------------------------------ cfg1 vs the reference
+
+DEC_NAMES = [f"{h}_{p}" for h in ("opacity", "color", "cov") for p in ("w1", "b1", "w2", "b2")]
+LEVEL_NAMES = ("emb", "log_scales", "offsets")
+
+
+def _cfg1_state():
+    from paper_2503_23044_b200.synthetic import cfg1_scene
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState
+    scene, views, images = cfg1_scene()
+    state = TrainState(scene, TrainConfig(total_steps=100, batch_size=4, step2_start=100,
+                                          step3_start=100, growth_stop=0))
+    return state, views, images
+
+
+def _grads_of(state, rows):
+    g = {k: state.flat.view(state.flat.grad, f"dec/{k}").double().cpu().numpy()
+         for k in DEC_NAMES}
+    for k in LEVEL_NAMES:
+        g[k] = state.flat.view(state.flat.grad, k).double().cpu().numpy()[rows]
+    return g
+
+
+@pytest.fixture(scope="module")
+def cfg1_run(cfg1_golden):
+    """The device's own two-step trajectory at cfg1, plus its step-2 gradient
+    evaluated at the reference's post-step-1 parameters."""
+    from paper_2503_23044_b200.trainer import train_step
+    d = cfg1_golden
+    rows = d["rows"]
+    state, views, images = _cfg1_state()
+    grads, reps = [], []
+    for _ in range(2):
+        reps.append(train_step(state, views, images))
+        grads.append(_grads_of(state, rows))
+    post = {k: state.flat.view(state.flat.param, f"dec/{k}").double().cpu().numpy()
+            for k in DEC_NAMES}
+    for k in LEVEL_NAMES:
+        post[k] = state.flat.view(state.flat.param, k).double().cpu().numpy()[rows]
+    # step 2 at the reference's parameters (gradient parity without the
+    # trajectory drift of step 1's noise-floor elements)
+    st2, _, _ = _cfg1_state()
+    with torch.no_grad():
+        for k in DEC_NAMES:
+            st2.flat.view(st2.flat.param, f"dec/{k}").copy_(torch.as_tensor(d[f"f32_post1_{k}"]))
+        for k in LEVEL_NAMES:
+            st2.flat.view(st2.flat.param, k).copy_(torch.as_tensor(d[f"f32_post1_lv_{k}"]))
+    rep2 = train_step(st2, views, images)
+    return {"grads": [grads[0], _grads_of(st2, rows)], "post": post, "reps": reps,
+            "rep2": rep2, "state": state}
+
+
+def _ref_grad(d, step, k, pre="f32_"):
+    g = "grad" if step == 0 else "grad2"
+    return d[f"{pre}{g}_{k}"] if k in DEC_NAMES else d[f"{pre}l{g}_{k}"]
+
+
+@pytest.mark.parametrize("step", [0, 1])
+def test_cfg1_gradients_vs_reference(cfg1_run, cfg1_golden, step):
+    """Decoder (all 12 tensors) and per-anchor (512 sampled anchors x 65)
+    gradients of train_step vs the reference's autograd at cfg1, at the same
+    (float32-representable) parameters: step 1 from the initial state, step 2
+    at the reference's post-step-1 parameters."""
+    d = cfg1_golden
+    report = []
+    for k in DEC_NAMES + list(LEVEL_NAMES):
+        ref = _ref_grad(d, step, k)
+        got = cfg1_run["grads"][step][k]
+        ok, ratio, wrel, nfloor = conditioned_close(got, ref, _ref_grad(d, step, k, pre="f32p_"),
+                                                    GRAD_REL, FLOOR_K)
+        # informational: the rms-based exclusion (|g| < 1e-3 rms skipped)
+        _, wr, excl = noise_floor_close(got, ref, 1.0, NOISE)
+        report.append((k, ratio, wrel, nfloor, ref.size, wr, excl))
+        assert ok, (f"step {step} {k}: worst err/bound {ratio:.3g}, worst rel (well-"
+                    f"conditioned) {wrel:.3g}, {nfloor}/{ref.size} floor-dominated")
+    print(f"\ncfg1 step {step} gradients: (worst err/bound, worst rel where the floor is "
+          "< rel/10, floor-dominated / size, worst rel beyond 1e-3 rms, excluded by it)",
+          {k: (f"{r:.2f}", f"{w:.1e}", f"{n}/{sz}", f"{wr:.1e}", e)
+           for k, r, w, n, sz, wr, e in report})
+    rep = cfg1_run["reps"][0] if step == 0 else cfg1_run["rep2"]
+    assert rep.rgb == pytest.approx(float(d[f"f32_report_rgb{step}"]), rel=1e-5)
+
+
+def test_cfg1_post_step_parameters_vs_reference(cfg1_run, cfg1_golden):
+    """Parameters after two train steps vs the reference's (same float32
+    initial parameters), rel 1e-3 of the value with the group's Adam step
+    size as the floor of the scale (a parameter moves by ~lr per step).
+    Excluded: elements whose reference gradient in either step is not
+    determined in float32, |g| <= K |g - g'| (g' at one-ulp-perturbed
+    parameters) -- Adam maps such a gradient's arbitrary sign to a full
+    +-lr step; everything else is asserted."""
+    d = cfg1_golden
+    st = cfg1_run["state"]
+    lrs = st.lrs()
+    report = {}
+    for k in DEC_NAMES + list(LEVEL_NAMES):
+        ref = d[f"f32_post_{k}"] if k in DEC_NAMES else d[f"f32_post_lv_{k}"]
+        got = cfg1_run["post"][k]
+        keep = np.ones(ref.shape, bool)
+        for s in range(2):
+            g = _ref_grad(d, s, k)
+            keep &= np.abs(g) > FLOOR_K * np.abs(g - _ref_grad(d, s, k, pre="f32p_"))
+        lr = lrs["dec" if k in DEC_NAMES else k]
+        err = np.abs(got - ref)
+        tol = GRAD_REL * np.maximum(np.abs(ref), lr)
+        worst = float((err / np.maximum(np.abs(ref), lr))[keep].max())
+        report[k] = (f"{worst:.1e}", f"{(~keep).sum()}/{ref.size}")
+        assert (err <= tol)[keep].all(), f"{k}: worst {worst:.3g} ({(~keep).sum()} excluded)"
+    print("\ncfg1 post-step parameters: (worst rel, excluded / size)", report)
+    r = cfg1_run["reps"]
+    np.testing.assert_allclose([r[0].rgb, r[1].rgb], d["report_rgb"], rtol=1e-4)
+
+
+# ------------------------------------------------------------------ cfg2 sampled tiles vs oracle
+
+@pytest.fixture(scope="module")
+def cfg2_view():
+    return build_cfg2_view()
+
+
+def build_cfg2_view():
+    """One cfg2 view through the device front end, plus the oracle's projection
+    of the device's decoded gaussians (identical inputs)."""
+    import bench
+    from paper_2503_23044_b200 import device as D
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState
+    scene, views, _desc, _ = bench.workload("cfg2")
+    view = views[0]
+    st = TrainState(scene, TrainConfig(total_steps=100, step2_start=100, step3_start=100,
+                                       growth_stop=0))
+    ds = st.dscene
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    act = ds.active(view)
+    dec = D.decode(st.params.abi(), st.n, act, ds.centers, st.anchors.emb, st.anchors.log_scales,
+                   st.anchors.offsets, view, ds.lod_ref, ds.max_scale, status, keep_cache=False)
+    P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, view,
+                  status)
+    B = D.bin_tiles(P, view.width, view.height)
+    assert int(status.item()) == 0
+    g = {"means": torch.tensor(dec.means.cpu().numpy()),
+         **{k: torch.tensor(getattr(dec, a).cpu().numpy().astype(np.float64))
+            for k, a in (("opacities", "opacity"), ("colors", "color"), ("scales", "scale"),
+                         ("quats", "quat"), ("normals", "normal"))}}
+    a = act.long().cpu().numpy()
+    gid = (a[:, None] * st.n + np.arange(st.n)).reshape(-1)
+    with torch.no_grad():
+        Po = oracle.project(g, gid, oracle.Cam.of(view))
+    return {"view": view, "P": P, "B": B, "Po": Po, "gid": gid}
+
+
+def test_cfg2_order_and_full_view_tile_lists_bitexact(cfg2_view):
+    c = cfg2_view
+    P, B, Po, view = c["P"], c["B"], c["Po"], c["view"]
+    src = P.src.long().cpu().numpy()
+    np.testing.assert_array_equal(c["gid"][src], Po["gid"])
+    np.testing.assert_array_equal(P.zkey.cpu().numpy().view(np.float64), Po["zkey"])
+    off, lst = oracle.bin_tiles(Po["mean2d"].numpy(), Po["radius"], view.width, view.height)
+    np.testing.assert_array_equal(B.tile_offsets.long().cpu().numpy(), off)
+    np.testing.assert_array_equal(B.tile_list.long().cpu().numpy(), lst)
+    assert off[-1] > 1_000_000, "a 1080p cfg2 view has millions of intersections"
+
+
+def _sample_tiles(B, count=240, heaviest=16):
+    lens = np.diff(B.tile_offsets.long().cpu().numpy())
+    busy = np.flatnonzero(lens > 0)
+    pick = busy[np.linspace(0, busy.size - 1, count).round().astype(np.int64)]
+    heavy = np.argsort(lens, kind="stable")[-heaviest:]
+    return np.unique(np.concatenate([pick, heavy])), lens
+
+
+def _device_leaves(P) -> dict:
+    """The device's sorted splat records as float64 oracle leaves (the
+    compositor's exact inputs, so K5/K6 numerics are isolated)."""
+    rec = P.rec.cpu()
+    out = {"mean2d": rec.view(torch.float64)[:, 0:2].clone(),
+           "conic": rec[:, 4:7].double(), "opacity": rec[:, 7].double(),
+           "color": rec[:, 8:11].double(), "normal_cam": rec[:, 11:14].double(),
+           "plane_d": rec[:, 14].double()}
+    return {k: v.clone().requires_grad_(True) for k, v in out.items()}
+
+
+GRAD_COLS = (("mean2d", 0, 2), ("conic", 2, 5), ("opacity", 5, 6), ("color", 6, 9),
+             ("normal_cam", 9, 12), ("plane_d", 12, 13))
+
+
+def _tile_mask(view, tiles) -> np.ndarray:
+    m = np.zeros((view.height, view.width), bool)
+    txn = (view.width + 15) // 16
+    for t in tiles:
+        ty, tx = divmod(int(t), txn)
+        m[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = True
+    return m
+
+
+def _guard_ok(R, view) -> np.ndarray:
+    """Pixels whose validity decisions sit away from the 1e-4 alpha / 1e-6
+    denominator guards (the reference tests' exclusion, helpers.py:129-137)."""
+    a = R.alpha.cpu().numpy().astype(np.float64)
+    raw = R.raw_normal.cpu().numpy().astype(np.float64)
+    ys, xs = np.mgrid[0:view.height, 0:view.width]
+    den = raw[..., 0] * (xs - view.cx) / view.fx + raw[..., 1] * (ys - view.cy) / view.fy + raw[..., 2]
+    return (np.abs(a - 1e-4) > 1e-3) & (np.abs(den) > 1e-3) & \
+        (np.linalg.norm(raw, axis=-1) > 1e-3)
+
+
+def _oracle_tiles(leaves, B, tiles, view, jitter=None):
+    """oracle.raster_tile on each sampled tile; per-tile outputs + pixel coords."""
+    off = B.tile_offsets.long().cpu().numpy()
+    lst = B.tile_list.long().cpu().numpy()
+    cam = oracle.Cam.of(view)
+    txn = (view.width + 15) // 16
+    outs = []
+    for t in tiles:
+        ty, tx = divmod(int(t), txn)
+        out = oracle.raster_tile(leaves, lst[off[t]:off[t + 1]], tx, ty, cam, jitter=jitter)
+        pu, pv = oracle.pipeline._tile_pixels(tx, ty)
+        inside = np.flatnonzero((pu < view.width) & (pv < view.height))
+        outs.append((out, inside, pv[inside].astype(np.int64), pu[inside].astype(np.int64)))
+    return outs
+
+
+def _perturbed(leaves, seed=0) -> dict:
+    """The leaves moved by one float32 ulp (random sign): relative 2^-23 for
+    the record's float32 fields, 2^-23 x 16 px for the mean (the resolution
+    of the tile-local float32 offset the kernels use)."""
+    g = torch.Generator().manual_seed(seed)
+    out = {}
+    for k, v in leaves.items():
+        sgn = torch.randint(0, 2, v.shape, generator=g).double() * 2 - 1
+        d = v.detach()
+        out[k] = (d + sgn * 2.0 ** -23 * 16.0 if k == "mean2d" else
+                  d * (1 + sgn * 2.0 ** -23)).clone().requires_grad_(True)
+    return out
+
+
+def _oracle_grads(objective, leaves, jitter=None) -> dict:
+    obj = objective(leaves, jitter)
+    gs = torch.autograd.grad(obj, [leaves[k] for k, _, _ in GRAD_COLS], allow_unused=True)
+    return {k: (np.zeros(tuple(leaves[k].shape)) if g is None else g.numpy())
+            for (k, _, _), g in zip(GRAD_COLS, gs)}
+
+
+def _compare_splat_grads(dev, objective, leaves, touched, what):
+    """Per-splat gradients vs the float64 oracle with the per-element float32
+    floor: |got - ref| <= 1e-3 |ref| + K * max(|ref - ref(one-ulp-perturbed
+    leaves)|, |ref - ref(one-ulp jitter of every per-pair intermediate)|)."""
+    ref = _oracle_grads(objective, leaves)
+    refp = _oracle_grads(objective, _perturbed(leaves))
+    refj = _oracle_grads(objective, leaves, torch.Generator().manual_seed(1))
+    for k in refp:   # the larger deviation of the two per element, same sign as ref-refp
+        dj, dp = ref[k] - refj[k], ref[k] - refp[k]
+        refp[k] = np.where(np.abs(dj) > np.abs(dp), refj[k], refp[k])
+    rep = {}
+    for name, a, b in GRAD_COLS:
+        r = ref[name].reshape(dev.shape[0], -1)
+        rp = refp[name].reshape(dev.shape[0], -1)
+        got = dev[:, a:b]
+        # splats outside the sampled tiles get exactly zero on both sides
+        assert np.all(got[~touched] == 0), f"{what} {name}: gradient outside the sampled tiles"
+        ok, ratio, wrel, nfloor = conditioned_close(got[touched], r[touched], rp[touched],
+                                                    GRAD_REL, FLOOR_K)
+        rep[name] = (ratio, wrel, nfloor)
+        assert ok, f"{what} {name}: worst err/bound {ratio:.3g}, worst rel (well-conditioned) " \
+                   f"{wrel:.3g}, {nfloor} floor-dominated"
+    print(f"\ncfg2 {what} per-splat 2D gradients: (worst err/bound, worst rel where the "
+          "floor is < rel/10, floor-dominated count)",
+          {k: (f"{r_:.2f}", f"{w:.1e}", n) for k, (r_, w, n) in rep.items()})
+
+
+def test_cfg2_sampled_tiles_forward_and_backward_vs_oracle(cfg2_view):
+    """Images within 1e-4 and per-splat gradients within rel 1e-3 (+ the
+    float32 floor) on the sampled tiles, explicit random pixel cotangents
+    (helpers.py:134-137 style), heaviest tiles of the view included."""
+    from paper_2503_23044_b200 import device as D
+    c = cfg2_view
+    P, B, view = c["P"], c["B"], c["view"]
+    tiles, lens = _sample_tiles(B)
+    assert tiles.size >= 200 and lens[tiles].max() == lens.max()
+    R = D.raster_forward(P, B, view)
+    leaves = _device_leaves(P)
+    with torch.no_grad():
+        outs = _oracle_tiles(leaves, B, tiles, view)
+    # forward: every sampled tile's pixels
+    for k in ("rgb", "alpha", "raw_normal", "normal"):
+        img = getattr(R, k).cpu().numpy()
+        err = max(np.abs(img[py, px] - o[k].numpy()[ins]).max() for o, ins, py, px in outs)
+        assert err <= IMG_ABS, (k, err)
+    valid = R.valid.cpu().numpy().astype(bool)
+    guard = _guard_ok(R, view)
+    for o, ins, py, px in outs:
+        ov = o["valid"].numpy()[ins]
+        g = guard[py, px]
+        np.testing.assert_array_equal(valid[py, px][g], ov[g])
+    dep = R.depth.cpu().numpy()
+    derr = 0.0
+    for o, ins, py, px in outs:
+        od = o["depth"].numpy()[ins]
+        e = (np.abs(dep[py, px] - od) / np.maximum(1.0, np.abs(od)))[guard[py, px] & valid[py, px]]
+        derr = max(derr, float(e.max()) if e.size else 0.0)
+    assert derr <= IMG_ABS, ("depth (abs, relative above 1 m)", derr)
+    # backward: random cotangents on the sampled tiles' guard-safe pixels
+    H, W = view.height, view.width
+    rng = np.random.default_rng(3)
+    m = _tile_mask(view, tiles)
+    mg = m & guard
+    cot = {"rgb": rng.normal(size=(H, W, 3)) * m[..., None],
+           "alpha": rng.normal(size=(H, W)) * m,
+           "depth": rng.normal(size=(H, W)) * mg * 1e-2,
+           "normal": rng.normal(size=(H, W, 3)) * mg[..., None]}
+    cf = {k: f32r(v) for k, v in cot.items()}
+    dev = D.raster_backward(P, B, view, R, *[torch.as_tensor(cf[k], dtype=torch.float32).cuda()
+                                             for k in ("rgb", "alpha", "depth", "normal")])
+    dev = dev.double().cpu().numpy()
+
+    def objective(lv, jitter=None):
+        obj = 0.0
+        for o, ins, py, px in _oracle_tiles(lv, B, tiles, view, jitter):
+            ki = torch.from_numpy(ins)
+            for k in ("rgb", "alpha", "depth", "normal"):
+                obj = obj + (o[k][ki] * torch.from_numpy(cf[k][py, px])).sum()
+        return obj
+
+    _compare_splat_grads(dev, objective, leaves, _touched(B, tiles, P.count),
+                         "explicit cotangents")
+
+
+def _touched(B, tiles, count) -> np.ndarray:
+    touched = np.zeros(count, bool)
+    off = B.tile_offsets.long().cpu().numpy()
+    lst = B.tile_list.long().cpu().numpy()
+    for t in tiles:
+        touched[lst[off[t]:off[t + 1]]] = True
+    return touched
+
+
+def test_cfg2_sampled_tiles_fused_objective_vs_oracle(cfg2_view):
+    """The training step's fused RGB-D-N objective (vsx_raster_fwd_loss /
+    vsx_raster_bwd_loss): L1 rgb + depth-prior L1 + normal-prior L1 restricted
+    to the sampled tiles (targets equal the render elsewhere, so sign(0) = 0
+    there), loss sums and per-splat gradients vs the oracle."""
+    from paper_2503_23044_b200 import device as D
+    from paper_2503_23044_b200._lib import VsxLossDesc
+    c = cfg2_view
+    P, B, view = c["P"], c["B"], c["view"]
+    tiles, _ = _sample_tiles(B)
+    H, W = view.height, view.width
+    R0 = D.raster_forward(P, B, view)
+    guard = _guard_ok(R0, view)
+    m = _tile_mask(view, tiles)
+    rng = np.random.default_rng(8)
+
+    # targets differ from the render by at least 1% (the L1 cotangent is
+    # sign(render - target); a near-tie is the sign analogue of a guard pixel)
+    def away(x, lo, hi):
+        sgn = np.where(rng.uniform(size=x.shape) < 0.5, -1.0, 1.0)
+        return (x + sgn * rng.uniform(lo, hi, x.shape)).astype(np.float32)
+    rgb0 = R0.rgb.cpu().numpy()
+    gt = np.where(m[..., None], away(rgb0, 0.01, 0.5), rgb0)
+    d0 = R0.depth.cpu().numpy()
+    pdep = (d0 * (1.0 + away(np.zeros_like(d0), 0.01, 0.1))).astype(np.float32)
+    pv = (m & guard & (rng.uniform(size=(H, W)) > 0.2)).astype(np.uint8)
+    pn = away(R0.normal.cpu().numpy(), 0.01, 0.5)
+    pnv = (m & guard & (rng.uniform(size=(H, W)) > 0.3)).astype(np.uint8)
+    dt = {k: torch.as_tensor(v).cuda() for k, v in
+          (("gt", gt), ("pd", pdep), ("pv", pv), ("pn", pn), ("pnv", pnv))}
+    sums = torch.zeros(3, dtype=torch.float64, device="cuda")
+    counts = torch.zeros(2, dtype=torch.int32, device="cuda")
+    live = torch.zeros((), dtype=torch.int64, device="cuda")
+    wd, wn = 1.0, 0.5
+    loss = VsxLossDesc(gt_rgb=dt["gt"].data_ptr(), prior_depth=dt["pd"].data_ptr(),
+                       prior_depth_valid=dt["pv"].data_ptr(), prior_normal=dt["pn"].data_ptr(),
+                       prior_normal_valid=dt["pnv"].data_ptr(), rgb_scale=1.0 / (H * W * 3),
+                       depth_weight=wd, normal_weight=wn / 3.0, sums=sums.data_ptr(),
+                       counts=counts.data_ptr(), live_pairs=live.data_ptr())
+    R = D.raster_forward(P, B, view, loss=loss)
+    dev = D.raster_backward(P, B, view, R, loss=loss).double().cpu().numpy()
+    # oracle: the same objective on the sampled tiles
+    leaves = _device_leaves(P)
+    gt_t, pd_t = torch.from_numpy(gt.astype(np.float64)), torch.from_numpy(pdep.astype(np.float64))
+    pn_t = torch.from_numpy(pn.astype(np.float64))
+    pv_b, pnv_b = torch.from_numpy(pv.astype(bool)), torch.from_numpy(pnv.astype(bool))
+    stats = {}
+
+    def objective(lv, jitter=None):
+        outs = _oracle_tiles(lv, B, tiles, view, jitter)
+        cnt_d = sum(int((o["valid"][torch.from_numpy(ins)] & pv_b[py, px]).sum())
+                    for o, ins, py, px in outs)
+        cnt_n = sum(int((o["valid"][torch.from_numpy(ins)] & pnv_b[py, px]).sum())
+                    for o, ins, py, px in outs)
+        rgb_s = dep_s = nrm_s = 0.0
+        for o, ins, py, px in outs:
+            ki = torch.from_numpy(ins)
+            rgb_s = rgb_s + (o["rgb"][ki] - gt_t[py, px]).abs().sum()
+            md = (o["valid"][ki] & pv_b[py, px]).double()
+            dep_s = dep_s + ((o["depth"][ki] - pd_t[py, px]).abs() * md).sum()
+            mn = (o["valid"][ki] & pnv_b[py, px]).double()
+            nrm_s = nrm_s + ((o["normal"][ki] - pn_t[py, px]).abs().sum(-1) * mn).sum()
+        stats.setdefault("counts", [cnt_d, cnt_n])
+        stats.setdefault("sums", [float(rgb_s), float(dep_s), float(nrm_s)])
+        return rgb_s / (H * W * 3) + wd * dep_s / cnt_d + wn * nrm_s / (3.0 * cnt_n)
+
+    _compare_splat_grads(dev, objective, leaves, _touched(B, tiles, P.count), "fused objective")
+    np.testing.assert_array_equal(counts.cpu().numpy(), stats["counts"])
+    # outside the sampled tiles |rgb - gt| = 0 exactly, so the sums are the tiles'
+    np.testing.assert_allclose(sums.cpu().numpy(), stats["sums"], rtol=1e-5)
+
+
+# ------------------------------------------------------------------ normal-prior term
+
+def test_train_steps_with_normal_prior_match_oracle(train_small):
+    """train_step(normal_priors=...) with cfg.normal_weight > 0 (the bench's
+    objective: RGB + depth prior + normal prior) vs the oracle for 3 steps:
+    loss terms and every post-step parameter (noise-floor exclusion on the
+    oracle's gradients)."""
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step
+    d = train_small
+    scene = golden_scene(d)
+    views = [golden_view(d, f"v{i}", i) for i in range(3)]
+    images = [d[f"img{i}"] for i in range(3)]
+    priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
+    rng = np.random.default_rng(12)
+    npri = []
+    for i in range(3):
+        p = rng.normal(size=(40, 48, 3))
+        npri.append(((p / np.linalg.norm(p, axis=-1, keepdims=True)).astype(np.float32),
+                     rng.uniform(size=(40, 48)) > 0.3))
+    wn = 0.5
+    state = TrainState(scene, TrainConfig(total_steps=8, batch_size=3, step2_start=0,
+                                          step3_start=8, growth_stop=0, normal_weight=wn))
+    w = oracle.decoder_init(3, 0, float(np.log(0.125 * scene.base_voxel_size)))
+    ost = oracle.OracleState.create(
+        scene.flat_centers(), scene.flat_levels(), scene.lod_count, scene.lod_ref_distance,
+        scene.lod_bias, scene.base_voxel_size, 3, {k: f32r(v) for k, v in w.items()},
+        f32r(scene.flat("embeddings")), f32r(np.log(scene.flat("scales"))),
+        f32r(scene.flat("offsets")), total_steps=8, step2_start=0, step3_start=8)
+    cams = [oracle.Cam.of(v) for v in views]
+    keep_all = {k: np.ones(v.shape, bool) for k, v in ost.params().items()}
+    for s in range(3):
+        rep = train_step(state, views, images, priors, normal_priors=npri)
+        orep = oracle.train_step(ost, cams, images, priors, normal_priors=npri,
+                                 normal_weight=wn)
+        np.testing.assert_allclose([rep.total, rep.rgb, rep.depth, rep.normal],
+                                   [orep["total"], orep["rgb"], orep["depth"], orep["normal"]],
+                                   rtol=2e-4, atol=1e-7)
+        assert orep["normal"] > 0
+        for name, g in ost.last_grads.items():
+            g = g.numpy()
+            keep_all[name] &= np.abs(g) >= NOISE * np.sqrt(np.mean(g * g))
+        lrs = state.lrs()
+        for name, oval in ost.params().items():
+            got = state.flat.view(state.flat.param, name).double().cpu().numpy()
+            ov = oval.detach().numpy()
+            lr = lrs["dec" if name.startswith("dec/") else name]
+            err = np.abs(got - ov) / np.maximum(np.abs(ov), lr)
+            k = keep_all[name]
+            assert err[k].max() <= GRAD_REL, \
+                f"step {s} {name}: worst {err[k].max():.3g} ({(~k).sum()} at noise floor)"

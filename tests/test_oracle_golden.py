@@ -202,6 +202,11 @@ def test_oracle_cfg1_matches_reference(cfg1_golden):
         _grad_close(st.last_grads[name].numpy()[rows], d[f"lgrad_{name}"], rel=1e-7, floor=1e-14)
     rep = oracle.train_step(st, cams, images)
     assert rep["rgb"] == pytest.approx(float(d["report_rgb"][1]), rel=1e-9)
+    for k, t in st.weights.items():   # step-2 gradients (at the post-step-1 parameters)
+        _grad_close(st.last_grads[f"dec/{k}"].numpy(), d[f"grad2_{k}"], rel=1e-7, floor=1e-14)
+    for name in ("emb", "log_scales", "offsets"):
+        _grad_close(st.last_grads[name].numpy()[rows], d[f"lgrad2_{name}"], rel=1e-7,
+                    floor=1e-14)
     for k, t in st.weights.items():
         np.testing.assert_allclose(t.numpy(), d[f"post_{k}"], rtol=1e-7, atol=1e-12)
     for name in ("emb", "log_scales", "offsets"):
@@ -238,3 +243,59 @@ def test_oracle_empty_and_ragged_views_match_reference():
     for name, t_ in st.weights.items():
         np.testing.assert_allclose(t_.detach().numpy(), g[f"post_{name}"], rtol=1e-8,
                                    atol=1e-12)
+
+
+def test_oracle_normal_prior_term_is_reference_eq9_per_channel():
+    """The normal-prior L1 (no reference function) is pinned on the reference's
+    own Eq. 9 machinery: loss_e_depth (losses.py:65-95) per normal channel,
+    averaged (golden normal_prior, make_golden.make_normal_prior)."""
+    g = load_golden("normal_prior")
+    leaves = [torch.tensor(g[f"n{i}"], requires_grad=True) for i in range(3)]
+    val, sup = oracle.normal_l1_loss(leaves, [torch.as_tensor(g[f"rv{i}"]) for i in range(3)],
+                                     [g[f"p{i}"] for i in range(3)],
+                                     [g[f"pv{i}"] for i in range(3)])
+    assert sup == int(g["supervised"])
+    assert float(val) == pytest.approx(float(g["value"]), rel=1e-12)
+    grads = torch.autograd.grad(val, leaves, allow_unused=True)
+    for i in range(3):
+        got = np.zeros_like(g["grad"][i]) if grads[i] is None else grads[i].numpy()
+        np.testing.assert_allclose(got, g["grad"][i], rtol=1e-12, atol=1e-18)
+
+
+def test_oracle_train_step_normal_term_equals_full_view_autograd(train_small):
+    """oracle.train_step's tile-wise normal term (value and gradients) equals
+    normal_l1_loss on the whole-view render, differentiated in one autograd
+    call (the reference's train_step structure, trainer.py:270-339)."""
+    d = train_small
+    cams = [oracle.Cam.of(golden_view(d, f"v{i}", i)) for i in range(3)]
+    images = [d[f"img{i}"] for i in range(3)]
+    rng = np.random.default_rng(4)
+    npri = []
+    for i in range(3):
+        p = rng.normal(size=(40, 48, 3))
+        npri.append((p / np.linalg.norm(p, axis=-1, keepdims=True),
+                     rng.uniform(size=(40, 48)) > (0.3 if i != 1 else 1.1)))
+    wn = 0.5
+    st = _train_state(d, total_steps=8, step2_start=8, step3_start=8)
+    # one autograd call over the whole-view renders
+    for p in st.params().values():
+        p.requires_grad_(True)
+    rgbs, nrms, vals = [], [], []
+    for cam in cams:
+        P, _, _ = oracle.pipeline._view_splats(st, cam, grad=True)
+        off, lst = oracle.bin_tiles(P["mean2d"].detach().numpy(), P["radius"], cam.width,
+                                    cam.height)
+        img = oracle.raster(P, off, lst, cam)
+        rgbs.append(img["rgb"]), nrms.append(img["normal"]), vals.append(img["valid"])
+    nl, _ = oracle.normal_l1_loss(nrms, vals, [p for p, _ in npri], [v for _, v in npri])
+    total = oracle.l1_loss(rgbs, images) + wn * nl
+    names = list(st.params())
+    ref = torch.autograd.grad(total, [st.params()[k] for k in names], allow_unused=True)
+    for p in st.params().values():
+        p.requires_grad_(False)
+    rep = oracle.train_step(st, cams, images, normal_priors=npri, normal_weight=wn)
+    assert rep["normal"] == pytest.approx(float(nl), rel=1e-10)
+    assert rep["total"] == pytest.approx(float(total), rel=1e-10)
+    for k, r in zip(names, ref):
+        r = np.zeros(st.last_grads[k].shape) if r is None else r.numpy()
+        _grad_close(st.last_grads[k].numpy(), r, rel=1e-8, floor=1e-15)
