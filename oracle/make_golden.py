@@ -271,12 +271,13 @@ def make_cfg1():
         rep = trainer.train_step(state, views, images)
         out[f"f32_report_rgb{s}"] = np.array(rep.rgb)
         tag = "f32_post1" if s == 0 else "f32_post"
+        # copies: the next step updates the parameter tensors in place
         for k, t_ in state.replicas[0].tensors.items():
-            out[f"{tag}_{k}"] = t_.detach().numpy()
+            out[f"{tag}_{k}"] = t_.detach().numpy().copy()
         for name, key in (("emb", "embeddings"), ("log_scales", "log_scales"),
                           ("offsets", "offsets")):
             a = state.level_state[0][key].detach().numpy()
-            out[f"{tag}_lv_{name}"] = a if s == 0 else a[rows]
+            out[f"{tag}_lv_{name}"] = a.copy() if s == 0 else a[rows]
     np.savez_compressed(OUT / "cfg1.npz", **out)
     print(f"cfg1 golden in {time.time() - t0:.0f}s")
 
@@ -645,6 +646,60 @@ def make_geo_loss():
         out[f"strat{k}_out"] = L._stratified_centers(cu, cv, w, h, cnt,
                                                      np.random.default_rng(100 + k))
     np.savez_compressed(OUT / "geo_loss.npz", **out)
+
+
+def make_boundary():
+    """API-surface cases of the drop-in boundary: the reference's
+    rasterize_patch on rectangles that are not tile aligned (scene_small
+    'near' view, its own sorted splats; renderer.py:304-344), and its
+    train_step report fields of the simulated multi-worker schedule
+    (transfer_bytes, trainer.py:264-289) at workers = 2 and 3 on train_small."""
+    decoder, geometry, partition, renderer, scene_m, trainer, _ = _ref()
+    out = {}
+    rng = np.random.default_rng(0)
+    pts = scene_m.SparsePoints(positions=rng.uniform(-1, 1, size=(150, 3)))
+    scene = scene_m.build_hierarchy(pts, 0.5, 3, offsets_per_voxel=2, seed=0)
+    r, t = geometry.look_at(np.array([0.0, -3.0, 1.0]), np.zeros(3))
+    far = geometry.CameraView(0, 48, 48, 40.0, 40.0, 23.5, 23.5, r, t)
+    r2, t2 = geometry.look_at(np.array([0.3, -1.2, 0.6]), np.array([0.0, 0.2, 0.0]))
+    near = geometry.CameraView(1, 40, 36, 30.0, 30.0, 19.5, 17.5, r2, t2)
+    scene.set_lod_reference([far])
+    params = decoder.DecoderParams.init(2, seed=0, scale_bias=float(np.log(0.1)))
+    from voxsplat.decoder import decode_active
+    splats = renderer.project_splats(decode_active(params, scene, near), near)
+    rects = [(5, 3, 21, 13), (0, 0, 40, 36), (17, 20, 9, 16), (30, 1, 10, 7)]
+    for i, (x0, y0, w, h) in enumerate(rects):
+        rect = partition.PatchRect(near.view_id, i, x0, y0, w, h)
+        res = renderer.rasterize_patch(rect, splats, near)
+        out[f"rect{i}"] = np.array([x0, y0, w, h])
+        out[f"rect{i}_idx"] = renderer.splats_for_rect(splats, x0, y0, w, h)
+        for k, v in res.items():
+            out[f"rect{i}_{k}"] = v.detach().numpy()
+    # an explicit index subset (every other overlapping splat)
+    idx = renderer.splats_for_rect(splats, 5, 3, 21, 13)[::2]
+    res = renderer.rasterize_patch(partition.PatchRect(near.view_id, 9, 5, 3, 21, 13), splats,
+                                   near, indices=idx)
+    out["sub_idx"] = idx
+    for k, v in res.items():
+        out[f"sub_{k}"] = v.detach().numpy()
+    d = np.load(OUT / "train_small.npz")
+    tpts = scene_m.SparsePoints(positions=d["points"])
+    views = []
+    for i in range(3):
+        ang = 2 * np.pi * i / 3
+        rr, tt = geometry.look_at(np.array([1.6 * np.cos(ang), 1.6 * np.sin(ang), 1.4]),
+                                  np.zeros(3))
+        views.append(geometry.CameraView(i, 48, 40, 40.0, 40.0, 23.5, 19.5, rr, tt))
+    images = [d[f"img{i}"] for i in range(3)]
+    for workers in (2, 3):
+        sc = scene_m.build_hierarchy(tpts, 0.25, 2, offsets_per_voxel=3, seed=4, views=views)
+        cfg = trainer.TrainConfig(total_steps=8, batch_size=3, workers=workers, step2_start=8,
+                                  step3_start=8, growth_stop=0, log_every=0)
+        st = trainer.make_state(sc, cfg)
+        reps = [trainer.train_step(st, views, images) for _ in range(2)]
+        out[f"w{workers}_transfer"] = np.array([r_.transfer_bytes for r_ in reps])
+        out[f"w{workers}_rgb"] = np.array([r_.rgb for r_ in reps])
+    np.savez_compressed(OUT / "boundary.npz", **out)
 
 
 if __name__ == "__main__":

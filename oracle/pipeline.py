@@ -311,11 +311,11 @@ def raster_tile(S: dict, idx: np.ndarray, tx: int, ty: int, cam: Cam,
     w = jit(alpha * t_prev * live)                              # (L, 256)
     acc = w.sum(0)
     rgb = w.transpose(0, 1) @ S["color"][it]
-    raw_n = w.transpose(0, 1) @ S["normal_cam"][it]
-    dist = (w * S["plane_d"][it].unsqueeze(-1)).sum(0)
+    raw_n = jit(w.transpose(0, 1) @ S["normal_cam"][it])
+    dist = jit((w * S["plane_d"][it].unsqueeze(-1)).sum(0))
     rx = (pu - cam.cx) / cam.fx
     ry = (pv - cam.cy) / cam.fy
-    denom = raw_n[:, 0] * rx + raw_n[:, 1] * ry + raw_n[:, 2]
+    denom = jit(raw_n[:, 0] * rx + raw_n[:, 1] * ry + raw_n[:, 2])
     covered = acc >= ALPHA_VALID_MIN
     valid = covered & (denom.abs() >= DENOM_GUARD)
     depth = torch.where(valid, dist / torch.where(valid, denom, torch.ones_like(denom)),

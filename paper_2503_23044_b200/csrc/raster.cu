@@ -1,34 +1,32 @@
 // K5 / K6 — per-tile front-to-back RGB-D-N compositing and its backward.
 //
 // Forward restates voxsplat renderer.py:242-301 (_blend_padded + _finalize)
-// and :390-449 (rasterize_view): one CTA per 16x16 tile, one thread per pixel,
-// splat records staged through shared memory in chunks of 256, CTA-wide early
-// exit once every pixel's transmittance fell below 1e-4 (__syncthreads_count).
-// Semantics that differ from stock 3DGS and are kept exactly: every binned
-// splat contributes (no 1/255 skip, no per-pixel 3-sigma cut), power is
-// clamped at 0, alpha is clamped at 0.99, a splat is live iff T_prev >= 1e-4.
+// and :390-449 (rasterize_view): one CTA of 128 threads per 16x16 tile, two
+// horizontally adjacent pixels per thread, splat records staged through
+// shared memory in chunks of 256, CTA-wide early exit once every pixel's
+// transmittance fell below 1e-4 (__syncthreads_count). Semantics that differ
+// from stock 3DGS and are kept exactly: every binned splat contributes (no
+// 1/255 skip, no per-pixel 3-sigma cut), power is clamped at 0, alpha is
+// clamped at 0.99, a splat is live iff T_prev >= 1e-4.
 //
-// Backward walks each tile back to front from the per-pixel live count,
-// recovering T_k = T_{k+1} / (1 - alpha_k) from the stored final
-// transmittance (the stable direction; see SURVEY.md §7 backward note).
-// It is split per chunk of kBC splats into
+// Backward (raster_bwd_tc_kernel) walks each tile back to front from the
+// per-pixel live count, recovering T_k = T_{k+1} / (1 - alpha_k) from the
+// stored final transmittance (the stable direction; SURVEY.md §7 backward
+// note), in chunks of 16 splats:
+//   phase 0 (tensor cores): the per-(pixel, splat) cotangent dot
+//            s = F[p] . P[j], a [256 x 8] . [8 x 16] product (3xTF32);
 //   phase 1 (thread = pixel): the sequential back-to-front recursion, writing
-//            the two per-(pixel, splat) scalars w = alpha*T and
-//            q = dL/d(alpha_unclamped) * exp(power) to shared memory;
-//   phase 2 (warp = splats, lane = pixels): per-splat sums over the tile's 256
-//            pixels in registers, one warp reduction per splat and chunk, and
-//            13 float atomics per (splat, tile) into the per-splat gradient.
-// This replaces a 13-value warp reduction per (splat, warp) (round-1 v1, see
-// profiles/r01_raster_bwd_v1_ncu.txt), which made the backward LSU-bound.
-// v3 (raster_bwd_tc_kernel, the default) moves both dot-product-shaped parts
-// onto the tensor cores (mma.sync tf32, 3xTF32 split): the per-(pixel, splat)
-// cotangent dot s = F[p] . P[j] before phase 1, and phase 2's per-splat sums,
-// which are two [kBC x 256] x [256 x 8] GEMMs. Records are prefetched one
-// chunk ahead with cp.async. Each chunk costs two CTA barriers: the next
-// chunk is staged right after phase 2 (double-buffered), so the epilogue's
-// atomics overlap the next chunk's phases 0/1 (1545 -> 1507 us per 1080p
-// view; -DVSX_BWD_MERGED=0 restores the three-barrier schedule for A/B).
-// VSX_RASTER_BWD="NS,BC" with NS > 0 selects v2.
+//            w = alpha*T and q = dL/d(alpha_unclamped) * exp(power) to two
+//            shared-memory planes;
+//   phase 2 (tensor cores): the per-splat sums over the tile's 256 pixels,
+//            [16 x 256] . [256 x 8] GEMMs of the w plane against the colour /
+//            normal / plane cotangents and of the q plane against the pixel
+//            moments (1, x, y, x^2, xy, y^2), then 13 float atomics per
+//            (splat, tile) from closed-form polynomials of the moments.
+// Records are prefetched one chunk ahead with cp.async; the next chunk is
+// staged right after phase 2 (double-buffered), two CTA barriers per chunk.
+// The measured alternatives (pixel-per-thread forward, a tensor-core
+// forward, an FFMA phase 2, a warp-specialised backward) are in DESIGN.md §6.
 #include "raster_common.cuh"
 
 namespace vsx {
@@ -37,7 +35,6 @@ namespace vsx {
 #define VSX_FWD_CHUNK 256
 #endif
 constexpr int kChunk = VSX_FWD_CHUNK;
-constexpr int kBCMax = 32;  // largest backward splat chunk
 
 // Per-pixel finalize (renderer.py:282-301) + fused loss partial sums (K9),
 // shared by both forward kernels. Block-uniform in L.gt_rgb.
@@ -126,96 +123,11 @@ __device__ __forceinline__ void fwd_epilogue(const vsx_camera &cam, bool inside,
   }
 }
 
-__global__ void __launch_bounds__(256) raster_fwd_kernel(
-    const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
-    const uint32_t *__restrict__ tile_list, vsx_camera cam, float *__restrict__ out_rgb,
-    float *__restrict__ out_alpha, float *__restrict__ out_depth, float *__restrict__ out_normal,
-    float *__restrict__ out_raw, uint8_t *__restrict__ out_valid, float *__restrict__ out_T,
-    int32_t *__restrict__ out_nc, vsx_loss_desc L) {
-  __shared__ float4 s0[kChunk], s1[kChunk], s2[kChunk], s3[kChunk];
-  const int txn = gridDim.x;
-  const int tile = blockIdx.y * txn + blockIdx.x;
-  const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
-  const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
-  const bool inside = px < cam.width && py < cam.height;
-  const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
-  const uint32_t begin = tile_off[tile], end = tile_off[tile + 1];
-  const float fx = (float)lx, fy = (float)ly;
-  float T = 1.f, acc = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f, dist = 0.f;
-  int32_t nc = 0;
-  bool done = !inside;
-  for (uint32_t cs = begin; cs < end; cs += kChunk) {
-    if (__syncthreads_count(!done) == 0) break;
-    for (int k = threadIdx.x; k < kChunk; k += blockDim.x) {
-      const uint32_t idx = cs + k;
-      if (idx < end) {
-        const vsx_splat sp = load_splat(rec, tile_list[idx]);
-        stage_splat(sp, ox, oy, s0[k], s1[k], s2[k], s3[k]);
-      }
-    }
-    __syncthreads();
-    const int cnt = (int)min((uint32_t)kChunk, end - cs);
-    if (!done) {
-      // batches of 4 independent alphas, then the sequential blend; T only
-      // decreases, so "live" (T_prev >= 1e-4) holds for a prefix of the chunk
-      int j = 0, live = 0;
-      for (; j + 4 <= cnt && T >= kEarlyStopT; j += 4) {
-        float al[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 p0 = s0[j + u], p1 = s1[j + u];
-          float e, at;
-          al[u] = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (T >= kEarlyStopT) {
-            const float w = al[u] * T;
-            const float4 p2 = s2[j + u], p3 = s3[j + u];
-            const float pd = s1[j + u].z;
-            acc += w;
-            c0 = fmaf(w, p2.x, c0);
-            c1 = fmaf(w, p2.y, c1);
-            c2 = fmaf(w, p2.z, c2);
-            n0 = fmaf(w, p3.x, n0);
-            n1 = fmaf(w, p3.y, n1);
-            n2 = fmaf(w, p3.z, n2);
-            dist = fmaf(w, pd, dist);
-            T = __fmaf_rn(-al[u], T, T);
-            ++live;
-          }
-        }
-      }
-      for (; j < cnt && T >= kEarlyStopT; ++j) {
-        const float4 p0 = s0[j], p1 = s1[j];
-        float e, at;
-        const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
-        const float w = alpha * T;
-        const float4 p2 = s2[j], p3 = s3[j];
-        acc += w;
-        c0 = fmaf(w, p2.x, c0);
-        c1 = fmaf(w, p2.y, c1);
-        c2 = fmaf(w, p2.z, c2);
-        n0 = fmaf(w, p3.x, n0);
-        n1 = fmaf(w, p3.y, n1);
-        n2 = fmaf(w, p3.z, n2);
-        dist = fmaf(w, p1.z, dist);
-        T = __fmaf_rn(-alpha, T, T);
-        ++live;
-      }
-      nc = (int32_t)(cs - begin) + live;
-      done = T < kEarlyStopT;
-    }
-  }
-  fwd_epilogue(cam, inside, px, py, acc, c0, c1, c2, n0, n1, n2, dist, T, nc, out_rgb, out_alpha,
-               out_depth, out_normal, out_raw, out_valid, out_T, out_nc, L);
-}
-
 // Forward with two horizontally adjacent pixels per thread (128 threads per
 // tile). The staged splat parameters are read from shared memory once per
 // pixel pair and the dy products of the falloff are shared, halving the
-// LSU traffic per (pixel, splat) of raster_fwd_kernel (which is L1-bound).
-// Per-pixel arithmetic and its rounding are exactly raster_fwd_kernel's.
+// LSU traffic per (pixel, splat) of a pixel-per-thread kernel (which was
+// L1-bound, profiles/r01_raster_fwd_ncu.txt).
 struct FwdPix {
   float T = 1.f, acc = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f, dist = 0.f;
   int32_t live = 0;
@@ -392,156 +304,16 @@ __device__ __forceinline__ uint32_t tf32_bits(float x) {
   return __float_as_uint(x) & 0xffffe000u;
 }
 
-// ------------------------------------------------------ forward v2 (tensor)
-//
-// The blend sums rgb, raw normal, plane offset and alpha are an [px x splat] .
-// [splat x 8] product once the per-(pixel, splat) weights w = alpha*T are
-// known. Each warp owns 32 pixels and walks the staged chunk of 256 splats in
-// sub-chunks of 32: lanes run the sequential transmittance recursion and
-// write w into a warp-private shared plane (0 once the pixel is dead), then
-// the warp accumulates the 8 channels with mma.sync m16n8k8 tf32 (3xTF32)
-// into register accumulators. Staged per splat: the alpha parameters and the
-// channel vector (r, g, b, nx, ny, nz, plane_d, 1) pre-split hi/lo.
-constexpr int kFwSub = 32;                 // splats per warp sub-chunk
-constexpr int kFwPlane = kFwSub * 36;      // floats per warp plane ([splat][36])
-
-__global__ void __launch_bounds__(256, 3) raster_fwd_tc_kernel(
-    const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
-    const uint32_t *__restrict__ tile_list, vsx_camera cam, float *__restrict__ out_rgb,
-    float *__restrict__ out_alpha, float *__restrict__ out_depth, float *__restrict__ out_normal,
-    float *__restrict__ out_raw, uint8_t *__restrict__ out_valid, float *__restrict__ out_T,
-    int32_t *__restrict__ out_nc, vsx_loss_desc L) {
-  __shared__ float4 s0[kChunk];
-  __shared__ float2 s1[kChunk];
-  __shared__ float s_phi[kChunk * 8], s_plo[kChunk * 8];
-  extern __shared__ float s_w[];  // 8 warp planes of kFwPlane floats
-  const int txn = gridDim.x;
-  const int tile = blockIdx.y * txn + blockIdx.x;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int g = lane >> 2, tq = lane & 3;
-  // pixel of this thread: warp w owns pixels 32w .. 32w+31 (rows 2w, 2w+1)
-  const int lx = t & 15, ly = t >> 4;
-  const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
-  const bool inside = px < cam.width && py < cam.height;
-  const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
-  const uint32_t begin = tile_off[tile], end = tile_off[tile + 1];
-  const float fx = (float)lx, fy = (float)ly;
-  float *wpl = s_w + warp * kFwPlane;
-  float T = 1.f;
-  int32_t nc = 0;
-  bool done = !inside;
-  float acc[2][4];  // C fragments: m-tile m = pixels 16m..16m+15 of the warp, channels
-#pragma unroll
-  for (int m = 0; m < 2; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
-  for (uint32_t cs = begin; cs < end; cs += kChunk) {
-    if (__syncthreads_count(!done) == 0) break;
-    const uint32_t idx = cs + t;
-    if (idx < end) {
-      const vsx_splat sp = load_splat(rec, tile_list[idx]);
-      s0[t] = make_float4((float)(sp.mean2d[0] - ox), (float)(sp.mean2d[1] - oy),
-                          (-0.5f * kLog2e) * sp.conic[0], (-kLog2e) * sp.conic[1]);
-      s1[t] = make_float2((-0.5f * kLog2e) * sp.conic[2], sp.opacity);
-      const float pv[8] = {sp.color[0], sp.color[1], sp.color[2], sp.normal[0],
-                           sp.normal[1], sp.normal[2], sp.plane_d, 1.f};
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float hi = __uint_as_float(tf32_bits(pv[c]));
-        s_phi[t * 8 + c] = hi;
-        s_plo[t * 8 + c] = __uint_as_float(tf32_bits(pv[c] - hi));
-      }
-    }
-    __syncthreads();
-    const int cnt = (int)min((uint32_t)kChunk, end - cs);
-    for (int sb = 0; sb < cnt; sb += kFwSub) {
-      if (!__any_sync(0xffffffffu, !done)) break;  // warp-uniform
-      const int m = min(kFwSub, cnt - sb);
-      // ---- sequential weights of this sub-chunk (dead pixels write 0)
-      int j = 0;
-      for (; j + 4 <= m; j += 4) {
-        float al[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 p0 = s0[sb + j + u];
-          const float2 p1 = s1[sb + j + u];
-          float e, at;
-          al[u] = splat_alpha(p0, make_float4(p1.x, p1.y, 0.f, 0.f), fx - p0.x, fy - p0.y, e, at);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          float w = 0.f;
-          if (!done) {
-            if (T >= kEarlyStopT) {
-              w = al[u] * T;
-              T = __fmaf_rn(-al[u], T, T);
-              ++nc;
-            } else {
-              done = true;
-            }
-          }
-          wpl[(j + u) * 36 + lane] = w;
-        }
-      }
-      for (; j < m; ++j) {
-        const float4 p0 = s0[sb + j];
-        const float2 p1 = s1[sb + j];
-        float e, at;
-        const float alpha =
-            splat_alpha(p0, make_float4(p1.x, p1.y, 0.f, 0.f), fx - p0.x, fy - p0.y, e, at);
-        float w = 0.f;
-        if (!done) {
-          if (T >= kEarlyStopT) {
-            w = alpha * T;
-            T = __fmaf_rn(-alpha, T, T);
-            ++nc;
-          } else {
-            done = true;
-          }
-        }
-        wpl[j * 36 + lane] = w;
-      }
-      for (; j < kFwSub; ++j) wpl[j * 36 + lane] = 0.f;  // ragged last sub-chunk
-      __syncwarp();
-      // ---- channel sums on the tensor cores: C[px][ch] += W[px][j] . P[j][ch]
-#pragma unroll
-      for (int ks = 0; ks < kFwSub / 8; ++ks) {
-        const int jr = sb + ks * 8 + tq;  // staged splat row of b0 (b1: +4)
-        const bool ok0 = ks * 8 + tq < m, ok1 = ks * 8 + tq + 4 < m;
-        const uint32_t bh0 = ok0 ? __float_as_uint(s_phi[jr * 8 + g]) : 0u;
-        const uint32_t bl0 = ok0 ? __float_as_uint(s_plo[jr * 8 + g]) : 0u;
-        const uint32_t bh1 = ok1 ? __float_as_uint(s_phi[(jr + 4) * 8 + g]) : 0u;
-        const uint32_t bl1 = ok1 ? __float_as_uint(s_plo[(jr + 4) * 8 + g]) : 0u;
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const float *A = wpl + (ks * 8 + tq) * 36 + 16 * mt + g;
-          const float a0 = A[0], a1 = A[8], a2 = A[4 * 36], a3 = A[4 * 36 + 8];
-          const uint32_t ah[4] = {tf32_bits(a0), tf32_bits(a1), tf32_bits(a2), tf32_bits(a3)};
-          const uint32_t alo[4] = {tf32_bits(a0 - __uint_as_float(ah[0])),
-                                   tf32_bits(a1 - __uint_as_float(ah[1])),
-                                   tf32_bits(a2 - __uint_as_float(ah[2])),
-                                   tf32_bits(a3 - __uint_as_float(ah[3]))};
-          mma_m16n8k8_tf32(acc[mt], alo, bh0, bh1);
-          mma_m16n8k8_tf32(acc[mt], ah, bl0, bl1);
-          mma_m16n8k8_tf32(acc[mt], ah, bh0, bh1);
-        }
-      }
-      __syncwarp();
-    }
-  }
-  // ---- C fragments -> per-pixel channels through the warp's plane
-  __syncwarp();
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt) {
-    float *o = wpl + (16 * mt + g) * 9 + 2 * tq;
-    o[0] = acc[mt][0];
-    o[1] = acc[mt][1];
-    o[8 * 9] = acc[mt][2];
-    o[8 * 9 + 1] = acc[mt][3];
-  }
-  __syncwarp();
-  const float *ch = wpl + lane * 9;
-  fwd_epilogue(cam, inside, px, py, ch[7], ch[0], ch[1], ch[2], ch[3], ch[4], ch[5], ch[6], T, nc,
-               out_rgb, out_alpha, out_depth, out_normal, out_raw, out_valid, out_T, out_nc, L);
+// tf32 by rounding to nearest (ties away from zero): one IADD more. With hi
+// rounded, |x - hi| <= 2^-11 |x| and the rounded lo leaves < 2^-22 |x|: the
+// 3xTF32 product then carries float32-level error (truncation leaves up to
+// 2^-20, which cancelling per-splat sums amplify past the 1e-3 bar).
+__device__ __forceinline__ uint32_t tf32_rn(float x) {
+  return (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
 }
+#ifndef VSX_BWD_RN2
+#define VSX_BWD_RN2 1
+#endif
 
 struct BwdArgs {
   const vsx_splat *rec;
@@ -553,163 +325,6 @@ struct BwdArgs {
   const float *rgb, *normal;  // forward outputs (fused-loss mode)
   vsx_loss_desc L;            // L.gt_rgb != NULL: cotangents from the fused objective
 };
-
-// ---------------------------------------------------------------- backward v2
-
-template <int NS, int kBC>
-__global__ void __launch_bounds__(256, (kBC == 16 ? 4 : 3))
-    raster_bwd_kernel(BwdArgs a, vsx_camera cam) {
-  __shared__ float4 s0[kBC], s1[kBC], s2[kBC], s3[kBC];
-  __shared__ uint32_t s_rank[kBC];
-  extern __shared__ float2 s_wq[];                // (w, q) per (splat, pixel): [kBC][256]
-  __shared__ float4 s_ga[kTilePixels], s_gb[kTilePixels];  // pixel cotangents
-  __shared__ int s_max;
-  const int txn = gridDim.x;
-  const int tile = blockIdx.y * txn + blockIdx.x;
-  const int t = threadIdx.x;
-  const int lx = t & 15, ly = t >> 4;
-  const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
-  const bool inside = px < cam.width && py < cam.height;
-  const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
-  const uint32_t begin = a.tile_off[tile];
-  const float fx = (float)lx, fy = (float)ly;
-  const int lane = t & 31, warp = t >> 5;
-  if (t == 0) s_max = 0;
-  __syncthreads();
-  int nc = 0;
-  float T = 1.f;
-  PixCot c{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  if (inside) {
-    const size_t p = (size_t)py * cam.width + px;
-    nc = a.nc[p];
-    T = a.T[p];
-    if (a.L.gt_rgb)
-      c = pixel_cotangent_loss(cam, px, py, p, a.alpha, a.rgb, a.depth, a.normal, a.raw, a.L);
-    else
-      c = pixel_cotangent(cam, px, py, p, a.alpha, a.depth, a.raw, a.g_rgb, a.g_alpha, a.g_depth,
-                          a.g_normal, a.g_raw);
-    if (nc > 0) atomicMax(&s_max, nc);
-  }
-  s_ga[t] = make_float4(c.gA, c.gC0, c.gC1, c.gC2);
-  s_gb[t] = make_float4(c.gR0, c.gR1, c.gR2, c.gD);
-  __syncthreads();
-  const uint32_t stop = begin + (uint32_t)s_max;
-  float S = 0.f;  // sum over later live splats of s_i * w_i
-  for (uint32_t ce = stop; ce > begin;) {
-    const uint32_t cs = ce > begin + kBC ? ce - kBC : begin;
-    const int cnt = (int)(ce - cs);
-    if (t < cnt) {
-      const uint32_t r = a.tile_list[cs + t];
-      s_rank[t] = r;
-      stage_splat(a.rec[r], ox, oy, s0[t], s1[t], s2[t], s3[t]);
-    }
-    __syncthreads();
-    // ---- phase 1: per-pixel back-to-front recursion
-    const int kbase = (int)(cs - begin);
-    // live splats of this pixel in the chunk are j < nc - kbase
-    const int jlive = min(cnt, nc - kbase);
-    // dead (and, in a partial chunk, padding) rows carry zeros into phase 2
-    for (int j = kBC - 1; j >= max(jlive, 0); --j) s_wq[j * kTilePixels + t] = make_float2(0.f, 0.f);
-#pragma unroll 2
-    for (int j = jlive - 1; j >= 0; --j) {
-      float2 wq;
-      {
-        const float4 p0 = s0[j], p1 = s1[j];
-        const float4 p2 = s2[j], p3 = s3[j];
-        float e, at;
-        const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
-        const float rom = rcp_ftz(1.f - alpha);
-        const float Tk = T * rom;
-        const float w = alpha * Tk;
-        const float sk = c.gA + c.gC0 * p2.x + c.gC1 * p2.y + c.gC2 * p2.z + c.gR0 * p3.x +
-                         c.gR1 * p3.y + c.gR2 * p3.z + c.gD * p1.z;
-        const float da = Tk * sk - S * rom;
-        S = fmaf(sk, w, S);
-        T = Tk;
-        // power <= 0 for a positive-definite conic; where rounding makes it
-        // slightly positive the clamped branch's zero d/dpower differs from
-        // dat*e*op only by terms of order dx, dy ~ 0 (phase 2 multiplies them).
-        const float dat = at <= kAlphaClamp ? da : 0.f;
-        wq = make_float2(w, dat * e);
-      }
-      s_wq[j * kTilePixels + t] = wq;
-    }
-    __syncthreads();
-    // ---- phase 2: warp w owns splats j = w + 8s (s < 4); lanes stride the 256
-    // pixels. Per splat it accumulates 7 colour/normal/plane sums sum_p w*G(p)
-    // and 6 pixel moments of q about the tile centre (1, x, y, x^2, xy, y^2);
-    // the conic/mean/opacity gradients are polynomials of those moments.
-    for (int jb = warp; jb < cnt; jb += 8 * NS) {
-      float acc[NS][13];
-#pragma unroll
-      for (int s = 0; s < NS; ++s)
-#pragma unroll
-        for (int q = 0; q < 13; ++q) acc[s][q] = 0.f;
-      // pix = lane + 32 i: x = lane & 15 is fixed per lane, y = (lane >> 4) + 2 i
-      const float xc = (float)(lane & 15) - 7.5f, xx = xc * xc;
-#pragma unroll 2
-      for (int i = 0; i < kTilePixels / 32; ++i) {
-        const int pix = lane + 32 * i;
-        const float4 ga = s_ga[pix], gb = s_gb[pix];
-        const float yc = (float)((lane >> 4) + 2 * i) - 7.5f;
-        const float xy = xc * yc, yy = yc * yc;
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
-          const int j = jb + 8 * s;  // rows >= cnt are zero-padded by phase 1
-          {
-            const float2 wq = s_wq[j * kTilePixels + pix];
-            acc[s][0] = fmaf(wq.x, ga.y, acc[s][0]);
-            acc[s][1] = fmaf(wq.x, ga.z, acc[s][1]);
-            acc[s][2] = fmaf(wq.x, ga.w, acc[s][2]);
-            acc[s][3] = fmaf(wq.x, gb.x, acc[s][3]);
-            acc[s][4] = fmaf(wq.x, gb.y, acc[s][4]);
-            acc[s][5] = fmaf(wq.x, gb.z, acc[s][5]);
-            acc[s][6] = fmaf(wq.x, gb.w, acc[s][6]);
-            acc[s][7] += wq.y;
-            acc[s][8] = fmaf(wq.y, xc, acc[s][8]);
-            acc[s][9] = fmaf(wq.y, yc, acc[s][9]);
-            acc[s][10] = fmaf(wq.y, xx, acc[s][10]);
-            acc[s][11] = fmaf(wq.y, xy, acc[s][11]);
-            acc[s][12] = fmaf(wq.y, yy, acc[s][12]);
-          }
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const int j = jb + 8 * s;
-        if (j >= cnt) break;  // warp-uniform
-#pragma unroll
-        for (int q = 0; q < 13; ++q) acc[s][q] = warp_sum(acc[s][q]);
-        const float4 p0 = s0[j], p1 = s1[j];
-        const float op = p1.y, A = p1.w, B = s2[j].w, C = s3[j].w;
-        const float mx = p0.x - 7.5f, my = p0.y - 7.5f;
-        const float Q1 = acc[s][7];
-        const float sx = acc[s][8] - mx * Q1;                 // sum q dx
-        const float sy = acc[s][9] - my * Q1;                 // sum q dy
-        const float sxx = acc[s][10] - 2.f * mx * acc[s][8] + mx * mx * Q1;
-        const float sxy = acc[s][11] - mx * acc[s][9] - my * acc[s][8] + mx * my * Q1;
-        const float syy = acc[s][12] - 2.f * my * acc[s][9] + my * my * Q1;
-        float g[13];
-        g[0] = op * (A * sx + B * sy);
-        g[1] = op * (B * sx + C * sy);
-        g[2] = -0.5f * op * sxx;
-        g[3] = -op * sxy;
-        g[4] = -0.5f * op * syy;
-        g[5] = Q1;
-#pragma unroll
-        for (int q = 0; q < 7; ++q) g[6 + q] = acc[s][q];
-        if (lane < 13) {
-          float v = g[0];
-#pragma unroll
-          for (int q = 1; q < 13; ++q) v = (lane == q) ? g[q] : v;
-          if (v != 0.f) atomicAdd(a.grad + (size_t)13 * s_rank[j] + lane, v);
-        }
-      }
-    }
-    __syncthreads();
-    ce = cs;
-  }
-}
 
 // ------------------------------------------------------- backward v3 (tensor)
 //
@@ -811,17 +426,17 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     for (int r = 0; r < 4; ++r) {
       const int pix = 32 * warp + 16 * m + g + 8 * (r & 1), f = tq + 4 * (r >> 1);
       const float v = s_plane[pix * 9 + f];
-      fhi[m][r] = tf32_bits(v);
-      flo[m][r] = tf32_bits(v - __uint_as_float(fhi[m][r]));
+      fhi[m][r] = tf32_rn(v);
+      flo[m][r] = tf32_rn(v - __uint_as_float(fhi[m][r]));
     }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int idx = t + 256 * i, ks = idx >> 5, ln = idx & 31;
     const int f = ln >> 2, p0 = 8 * ks + (ln & 3), p1 = p0 + 4;
     const float v0 = f < 7 ? s_plane[p0 * 9 + f] : 0.f, v1 = f < 7 ? s_plane[p1 * 9 + f] : 0.f;
-    const float h0 = __uint_as_float(tf32_bits(v0)), h1 = __uint_as_float(tf32_bits(v1));
-    s_bw[ks][ln] = make_float4(h0, h1, __uint_as_float(tf32_bits(v0 - h0)),
-                               __uint_as_float(tf32_bits(v1 - h1)));
+    const float h0 = __uint_as_float(tf32_rn(v0)), h1 = __uint_as_float(tf32_rn(v1));
+    s_bw[ks][ln] = make_float4(h0, h1, __uint_as_float(tf32_rn(v0 - h0)),
+                               __uint_as_float(tf32_rn(v1 - h1)));
     s_bq[ks][ln] = make_float2(pixel_moment(p0, f), pixel_moment(p1, f));
   }
   __syncthreads();
@@ -864,9 +479,9 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
                            sp.normal[1], sp.normal[2], sp.plane_d, 1.f};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const float h0 = __uint_as_float(tf32_bits(pv[k])), h1 = __uint_as_float(tf32_bits(pv[k + 4]));
-        s_ph[sb][sl][k] = make_float4(h0, h1, __uint_as_float(tf32_bits(pv[k] - h0)),
-                                     __uint_as_float(tf32_bits(pv[k + 4] - h1)));
+        const float h0 = __uint_as_float(tf32_rn(pv[k])), h1 = __uint_as_float(tf32_rn(pv[k + 4]));
+        s_ph[sb][sl][k] = make_float4(h0, h1, __uint_as_float(tf32_rn(pv[k] - h0)),
+                                     __uint_as_float(tf32_rn(pv[k + 4] - h1)));
       }
     }
     const uint32_t cs2 = chunk_lo(cs_);
@@ -968,14 +583,23 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
       auto a_frag = [&](int ks, uint32_t (&hi)[4], uint32_t (&lo)[4]) {
         const float x0 = A[8 * ks], x1 = A[8 * kPlaneStride + 8 * ks], x2 = A[8 * ks + 4],
                     x3 = A[8 * kPlaneStride + 8 * ks + 4];
+#if VSX_BWD_RN2
+        hi[0] = tf32_rn(x0);
+        hi[1] = tf32_rn(x1);
+        hi[2] = tf32_rn(x2);
+        hi[3] = tf32_rn(x3);
+#else
         hi[0] = tf32_bits(x0);
         hi[1] = tf32_bits(x1);
         hi[2] = tf32_bits(x2);
         hi[3] = tf32_bits(x3);
-        lo[0] = tf32_bits(x0 - __uint_as_float(hi[0]));
-        lo[1] = tf32_bits(x1 - __uint_as_float(hi[1]));
-        lo[2] = tf32_bits(x2 - __uint_as_float(hi[2]));
-        lo[3] = tf32_bits(x3 - __uint_as_float(hi[3]));
+#endif
+        // lo is passed as its float32 bits: the tensor core reads the tf32
+        // part (truncation of a value already <= 2^-11 |x|)
+        lo[0] = __float_as_uint(x0 - __uint_as_float(hi[0]));
+        lo[1] = __float_as_uint(x1 - __uint_as_float(hi[1]));
+        lo[2] = __float_as_uint(x2 - __uint_as_float(hi[2]));
+        lo[3] = __float_as_uint(x3 - __uint_as_float(hi[3]));
       };
       // warp-uniform plane branch outside the k loop: no predicated HMMAs
       if (plane == 0) {
@@ -1061,404 +685,27 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   }
 }
 
-// ------------------------------------------------ backward v4 (warp-specialised)
-//
-// v3's per-chunk CTA barriers were its largest stall (19% of issue stalls,
-// profiles/r02_raster_bwd_v3_ncu.txt): every warp waited at the end of phase 1
-// for the slowest pixel of the tile and again after phase 2. v4 splits the CTA
-// into two roles that run concurrently on double-buffered shared memory:
-//   8 pixel warps (thread = pixel): phase 0 (tensor-core cotangent dots) and
-//     phase 1 (the back-to-front recursion) of chunk i into plane buffer i&1;
-//   4 reduction warps: phase 2 (tensor-core per-splat sums) and the atomics
-//     epilogue of chunk i-1 from the other buffer, and the staging of the
-//     splat records two chunks ahead.
-// The roles meet only through named barriers (producer bar.arrive, consumer
-// bar.sync): REC_FULL[b] (records of buffer b staged), PLANE_FULL[b] (planes
-// written), PLANE_EMPTY[b] (planes consumed). The math of each phase is v3's,
-// so results are identical up to the fp32 summation order of phase 2.
-namespace ws {
-constexpr int kBC = 16;                  // splats per chunk (one MMA m-tile)
-constexpr int kPixWarps = 8;
-constexpr int kRedWarps = 4;
-constexpr int kThreads = 32 * (kPixWarps + kRedWarps);
-constexpr int kRedThreads = 32 * kRedWarps;
-constexpr int kPlane = kBC * kPlaneStride;  // floats per plane
-enum : int { kRecFull = 1, kPlaneFull = 3, kPlaneEmpty = 5, kRed = 7 };
-}  // namespace ws
-
-// Barrier ids are immediates (ptxas then reserves only the ids used, not all
-// 16, which would cap the CTAs per SM); `b` selects buffer 0 / 1.
-template <int kId, int kN>
-__device__ __forceinline__ void named_sync2(int b) {
-  if (b) asm volatile("bar.sync %0, %1;" ::"n"(kId + 1), "n"(kN) : "memory");
-  else asm volatile("bar.sync %0, %1;" ::"n"(kId), "n"(kN) : "memory");
-}
-template <int kId, int kN>
-__device__ __forceinline__ void named_arrive2(int b) {
-  if (b) asm volatile("bar.arrive %0, %1;" ::"n"(kId + 1), "n"(kN) : "memory");
-  else asm volatile("bar.arrive %0, %1;" ::"n"(kId), "n"(kN) : "memory");
-}
-template <int kId, int kN>
-__device__ __forceinline__ void named_sync1() {
-  asm volatile("bar.sync %0, %1;" ::"n"(kId), "n"(kN) : "memory");
-}
-
-__global__ void __launch_bounds__(ws::kThreads, 2)
-    raster_bwd_ws_kernel(BwdArgs a, vsx_camera cam) {
-  using namespace ws;
-  __shared__ float4 s0[2][kBC], s1[2][kBC], s2[2][kBC], s3[2][kBC];
-  __shared__ float4 s_ph[2][kBC][4];  // P B fragments per (splat, lane&3): hi b0, hi b1, lo b0, lo b1
-  __shared__ uint32_t s_rank[2][kBC];
-  __shared__ float4 s_bw[32][32];     // Gw B fragments per (k-step, lane): hi b0, hi b1, lo b0, lo b1
-  __shared__ float2 s_bq[32][32];     // Mq B fragments per (k-step, lane)
-  __shared__ float s_red[4][kBC][24];
-  __shared__ int s_max;
-  extern __shared__ float s_plane[];  // [buffer][w | q][kBC][kPlaneStride]
-  const int txn = gridDim.x;
-  const int lin = blockIdx.y * txn + blockIdx.x;
-  const int tile = a.L.tile_order ? (int)a.L.tile_order[lin] : lin;
-  const int bx = tile % txn, by = tile / txn;
-  const int t = threadIdx.x;
-  const int lane = t & 31, warp = t >> 5;
-  const bool pix = warp < kPixWarps;
-  const int g = lane >> 2, tq = lane & 3;
-  const double ox = (double)(bx * kTile), oy = (double)(by * kTile);
-  const uint32_t begin = a.tile_off[tile];
-  if (t == 0) s_max = 0;
-  // ---- setup: per-pixel cotangents -> F A fragments (pixel warps) and the
-  // per-tile Gw / moment B fragments (all threads), staged through plane 0
-  int nc = 0;
-  float T = 1.f;
-  const int lx = t & 15, ly = (t >> 4) & 15;
-  const float fx = (float)lx, fy = (float)ly;
-  if (pix) {
-    const int px = bx * kTile + lx, py = by * kTile + ly;
-    PixCot c{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (px < cam.width && py < cam.height) {
-      const size_t p = (size_t)py * cam.width + px;
-      nc = a.nc[p];
-      T = a.T[p];
-      if (a.L.gt_rgb)
-        c = pixel_cotangent_loss(cam, px, py, p, a.alpha, a.rgb, a.depth, a.normal, a.raw, a.L);
-      else
-        c = pixel_cotangent(cam, px, py, p, a.alpha, a.depth, a.raw, a.g_rgb, a.g_alpha,
-                            a.g_depth, a.g_normal, a.g_raw);
-    }
-    float *gw = s_plane + t * 9;
-    gw[0] = c.gC0; gw[1] = c.gC1; gw[2] = c.gC2; gw[3] = c.gR0;
-    gw[4] = c.gR1; gw[5] = c.gR2; gw[6] = c.gD; gw[7] = c.gA;
-  }
-  __syncthreads();
-  if (pix && nc > 0) atomicMax(&s_max, nc);
-  uint32_t fhi[2][4], flo[2][4];
-  if (pix) {
-#pragma unroll
-    for (int m = 0; m < 2; ++m)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int pp = 32 * warp + 16 * m + g + 8 * (r & 1), f = tq + 4 * (r >> 1);
-        const float v = s_plane[pp * 9 + f];
-        fhi[m][r] = tf32_bits(v);
-        flo[m][r] = tf32_bits(v - __uint_as_float(fhi[m][r]));
-      }
-  }
-  for (int idx = t; idx < 32 * 32; idx += kThreads) {
-    const int ks = idx >> 5, ln = idx & 31;
-    const int f = ln >> 2, p0 = 8 * ks + (ln & 3), p1 = p0 + 4;
-    const float v0 = f < 7 ? s_plane[p0 * 9 + f] : 0.f, v1 = f < 7 ? s_plane[p1 * 9 + f] : 0.f;
-    const float h0 = __uint_as_float(tf32_bits(v0)), h1 = __uint_as_float(tf32_bits(v1));
-    s_bw[ks][ln] = make_float4(h0, h1, __uint_as_float(tf32_bits(v0 - h0)),
-                               __uint_as_float(tf32_bits(v1 - h1)));
-    s_bq[ks][ln] = make_float2(pixel_moment(p0, f), pixel_moment(p1, f));
-  }
-  __syncthreads();
-  const uint32_t stop = begin + (uint32_t)s_max;
-  const int nchunks = (int)((stop - begin + kBC - 1) / kBC);
-  // chunk i covers [cs, ce), walked from the end of the live range
-  auto chunk_cs = [&](int i) {
-    const uint32_t ce = stop - (uint32_t)(kBC * i);
-    return ce > begin + kBC ? ce - kBC : begin;
-  };
-  if (pix) {
-    // ================= pixel warps: phases 0 and 1 =================
-    float S = 0.f;  // sum over later live splats of s_i * w_i
-    for (int i = 0; i < nchunks; ++i) {
-      const int b = i & 1;
-      const uint32_t cs = chunk_cs(i);
-      const int cnt = (int)(stop - (uint32_t)(kBC * i) - cs);
-      float *wpl = s_plane + (2 * b) * kPlane, *qpl = wpl + kPlane;
-      named_sync2<kRecFull, kThreads>(b);
-      named_sync2<kPlaneEmpty, kThreads>(b);
-      // phase 0: sk[j][p] = F[p] . P[j] for this warp's 32 pixels (3xTF32)
-#pragma unroll
-      for (int nt = 0; nt < kBC / 8; ++nt) {
-        const float4 pb = s_ph[b][8 * nt + g][tq];
-#pragma unroll
-        for (int m = 0; m < 2; ++m) {
-          float d[4] = {0.f, 0.f, 0.f, 0.f};
-          mma_m16n8k8_tf32(d, flo[m], __float_as_uint(pb.x), __float_as_uint(pb.y));
-          mma_m16n8k8_tf32(d, fhi[m], __float_as_uint(pb.z), __float_as_uint(pb.w));
-          mma_m16n8k8_tf32(d, fhi[m], __float_as_uint(pb.x), __float_as_uint(pb.y));
-          float *o = qpl + (8 * nt + 2 * tq) * kPlaneStride + 32 * warp + 16 * m + g;
-          o[0] = d[0];
-          o[kPlaneStride] = d[1];
-          o[8] = d[2];
-          o[kPlaneStride + 8] = d[3];
-        }
-      }
-      __syncwarp();
-      // phase 1: per-pixel back-to-front recursion
-      const int kbase = (int)(cs - begin);
-      const int jlive = min(cnt, nc - kbase);
-      for (int j = cnt - 1; j >= max(jlive, 0); --j) {
-        wpl[j * kPlaneStride + t] = 0.f;
-        qpl[j * kPlaneStride + t] = 0.f;
-      }
-      int j = jlive - 1;
-      for (; j >= kUB - 1; j -= kUB) {
-        float al[kUB], ee[kUB], aa[kUB], rm[kUB], sk[kUB];
-#pragma unroll
-        for (int u = 0; u < kUB; ++u) {
-          const float4 p0 = s0[b][j - u], p1 = s1[b][j - u];
-          al[u] = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, ee[u], aa[u]);
-          rm[u] = rcp_ftz(1.f - al[u]);
-          sk[u] = qpl[(j - u) * kPlaneStride + t];
-        }
-#pragma unroll
-        for (int u = 0; u < kUB; ++u) {
-          const float Tk = T * rm[u];
-          const float w = al[u] * Tk;
-          const float da = Tk * sk[u] - S * rm[u];
-          S = fmaf(sk[u], w, S);
-          T = Tk;
-          wpl[(j - u) * kPlaneStride + t] = w;
-          qpl[(j - u) * kPlaneStride + t] = (aa[u] <= kAlphaClamp ? da : 0.f) * ee[u];
-        }
-      }
-      for (; j >= 0; --j) {
-        const float4 p0 = s0[b][j], p1 = s1[b][j];
-        float e, at;
-        const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
-        const float rom = rcp_ftz(1.f - alpha);
-        const float Tk = T * rom;
-        const float w = alpha * Tk;
-        const float sk = qpl[j * kPlaneStride + t];
-        const float da = Tk * sk - S * rom;
-        S = fmaf(sk, w, S);
-        T = Tk;
-        wpl[j * kPlaneStride + t] = w;
-        qpl[j * kPlaneStride + t] = (at <= kAlphaClamp ? da : 0.f) * e;
-      }
-      named_arrive2<kPlaneFull, kThreads>(b);
-    }
-    return;
-  }
-  // ================= reduction warps: staging, phase 2, epilogue =================
-  const int rt = t - 32 * kPixWarps;  // 0..127
-  const int rw = rt >> 5;             // 0..3: k-quarter of both planes
-  // records of chunk i are loaded into registers one iteration early and
-  // written to shared memory when their buffer frees up, so the global-load
-  // latency never sits between a chunk's epilogue and the pixel warps
-  vsx_splat pre{};
-  uint32_t pre_r = 0;
-  auto fetch = [&](int i) {
-    const uint32_t cs = chunk_cs(i);
-    const int cnt = (int)(stop - (uint32_t)(kBC * i) - cs);
-    if (rt < cnt) {
-      pre_r = a.tile_list[cs + rt];
-      pre = load_splat(a.rec, pre_r);
-    }
-  };
-  auto stage = [&](int i) {
-    const int b = i & 1;
-    const uint32_t cs = chunk_cs(i);
-    const int cnt = (int)(stop - (uint32_t)(kBC * i) - cs);
-    if (rt < cnt) {
-      s_rank[b][rt] = pre_r;
-      stage_splat(pre, ox, oy, s0[b][rt], s1[b][rt], s2[b][rt], s3[b][rt]);
-      const float pv[8] = {pre.color[0], pre.color[1], pre.color[2], pre.normal[0],
-                           pre.normal[1], pre.normal[2], pre.plane_d, 1.f};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float h0 = __uint_as_float(tf32_bits(pv[k])),
-                    h1 = __uint_as_float(tf32_bits(pv[k + 4]));
-        s_ph[b][rt][k] = make_float4(h0, h1, __uint_as_float(tf32_bits(pv[k] - h0)),
-                                     __uint_as_float(tf32_bits(pv[k + 4] - h1)));
-      }
-    }
-    named_arrive2<kRecFull, kThreads>(b);
-  };
-  for (int i = 0; i < min(nchunks, 2); ++i) {
-    fetch(i);
-    stage(i);
-    named_arrive2<kPlaneEmpty, kThreads>(i);  // both plane buffers start empty
-  }
-  if (nchunks > 2) fetch(2);
-  for (int i = 0; i < nchunks; ++i) {
-    const int b = i & 1;
-    const uint32_t cs = chunk_cs(i);
-    const int cnt = (int)(stop - (uint32_t)(kBC * i) - cs);
-    named_sync2<kPlaneFull, kThreads>(b);
-    // phase 2: [kBC x 256] x [256 x 8] on the tensor cores, both planes, this
-    // warp's quarter of the 32 k-steps; two accumulator sets (even / odd
-    // k-step) per product so the HMMA chains are half as long
-    {
-      const float *Aw = s_plane + (2 * b) * kPlane + g * kPlaneStride + tq;
-      const float *Aq = Aw + kPlane;
-      float dw[2][4] = {}, ew1[2][4] = {}, ew2[2][4] = {}, dq[2][4] = {}, eq1[2][4] = {};
-      auto a_frag = [&](const float *A, int ks, uint32_t (&hi)[4], uint32_t (&lo)[4]) {
-        const float x0 = A[8 * ks], x1 = A[8 * kPlaneStride + 8 * ks], x2 = A[8 * ks + 4],
-                    x3 = A[8 * kPlaneStride + 8 * ks + 4];
-        hi[0] = tf32_bits(x0);
-        hi[1] = tf32_bits(x1);
-        hi[2] = tf32_bits(x2);
-        hi[3] = tf32_bits(x3);
-        lo[0] = tf32_bits(x0 - __uint_as_float(hi[0]));
-        lo[1] = tf32_bits(x1 - __uint_as_float(hi[1]));
-        lo[2] = tf32_bits(x2 - __uint_as_float(hi[2]));
-        lo[3] = tf32_bits(x3 - __uint_as_float(hi[3]));
-      };
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const int ks = 8 * rw + kk, c = kk & 1;
-        uint32_t hi[4], lo[4];
-        a_frag(Aw, ks, hi, lo);
-        const float4 bw = s_bw[ks][lane];
-        mma_m16n8k8_tf32(ew1[c], lo, __float_as_uint(bw.x), __float_as_uint(bw.y));
-        mma_m16n8k8_tf32(ew2[c], hi, __float_as_uint(bw.z), __float_as_uint(bw.w));
-        mma_m16n8k8_tf32(dw[c], hi, __float_as_uint(bw.x), __float_as_uint(bw.y));
-        a_frag(Aq, ks, hi, lo);
-        const float2 bq = s_bq[ks][lane];
-        mma_m16n8k8_tf32(eq1[c], lo, __float_as_uint(bq.x), __float_as_uint(bq.y));
-        mma_m16n8k8_tf32(dq[c], hi, __float_as_uint(bq.x), __float_as_uint(bq.y));
-      }
-      // the planes of buffer b are free once the last chunk using it was read
-      if (i + 2 < nchunks) named_arrive2<kPlaneEmpty, kThreads>(b);
-      float w4[4], q4[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        w4[k] = ((ew1[0][k] + ew2[0][k]) + dw[0][k]) + ((ew1[1][k] + ew2[1][k]) + dw[1][k]);
-        q4[k] = (eq1[0][k] + dq[0][k]) + (eq1[1][k] + dq[1][k]);
-      }
-      float *red = &s_red[rw][g][2 * tq];
-      *reinterpret_cast<float2 *>(red) = make_float2(w4[0], w4[1]);
-      *reinterpret_cast<float2 *>(red + 8 * 24) = make_float2(w4[2], w4[3]);
-      *reinterpret_cast<float2 *>(red + 8) = make_float2(q4[0], q4[1]);
-      *reinterpret_cast<float2 *>(red + 8 * 24 + 8) = make_float2(q4[2], q4[3]);
-    }
-    named_sync1<kRed, kRedThreads>();
-    // epilogue: 8 lanes per splat, lane part holds features 2part, 2part+1
-    {
-      const int j = rt >> 3, part = rt & 7;
-      float2 v = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 u = *reinterpret_cast<const float2 *>(&s_red[k][j][2 * part]);
-        v.x += u.x;
-        v.y += u.y;
-      }
-      // moments: part 4 = (1, x), 5 = (y, xx), 6 = (xy, yy)
-      const float m2 = __shfl_down_sync(0xffffffffu, v.x, 1),
-                  m3 = __shfl_down_sync(0xffffffffu, v.y, 1);
-      const float m4 = __shfl_down_sync(0xffffffffu, v.x, 2),
-                  m5 = __shfl_down_sync(0xffffffffu, v.y, 2);
-      if (j < cnt) {
-        float *gp = a.grad + (size_t)13 * s_rank[b][j];
-        if (part < 4) {
-          if (v.x != 0.f) atomicAdd(gp + 6 + 2 * part, v.x);
-          if (part < 3 && v.y != 0.f) atomicAdd(gp + 7 + 2 * part, v.y);
-        } else if (part == 4) {
-          const float4 p0 = s0[b][j], p1 = s1[b][j];
-          const float op = p1.y, A = p1.w, B = s2[b][j].w, C = s3[b][j].w;
-          const float mx = p0.x - 7.5f, my = p0.y - 7.5f;
-          const float Q1 = v.x, X = v.y, Y = m2, XX = m3, XY = m4, YY = m5;
-          const float sx = X - mx * Q1, sy = Y - my * Q1;
-          const float sxx = XX - 2.f * mx * X + mx * mx * Q1;
-          const float sxy = XY - mx * Y - my * X + mx * my * Q1;
-          const float syy = YY - 2.f * my * Y + my * my * Q1;
-          const float g0 = op * (A * sx + B * sy), g1 = op * (B * sx + C * sy);
-          const float g2 = -0.5f * op * sxx, g3 = -op * sxy, g4 = -0.5f * op * syy;
-          if (g0 != 0.f) atomicAdd(gp + 0, g0);
-          if (g1 != 0.f) atomicAdd(gp + 1, g1);
-          if (g2 != 0.f) atomicAdd(gp + 2, g2);
-          if (g3 != 0.f) atomicAdd(gp + 3, g3);
-          if (g4 != 0.f) atomicAdd(gp + 4, g4);
-          if (Q1 != 0.f) atomicAdd(gp + 5, Q1);
-        }
-      }
-    }
-    named_sync1<kRed, kRedThreads>();   // s_red and records of buffer b are free
-    if (i + 2 < nchunks) {
-      stage(i + 2);
-      if (i + 3 < nchunks) fetch(i + 3);
-    }
-  }
-}
-
-static int launch_bwd_ws(const BwdArgs &a, const vsx_camera &cam, cudaStream_t st) {
-  dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
-  const int smem = (int)(sizeof(float) * 4 * ws::kPlane);
-  // the opt-in is per device (a multi-GPU process launches on several)
+// cudaFuncSetAttribute is per device: set it once per device the process
+// launches on (a multi-GPU process, or threaded ranks, use several).
+template <typename K>
+static int smem_opt_in(K kernel, int bytes, std::atomic<uint64_t> &done) {
   int dev = 0;
   VSX_CUDA_TRY(cudaGetDevice(&dev));
-  static std::atomic<uint64_t> done{0};
-  if (dev < 64 && !(done.load() & (1ull << dev))) {
-    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_ws_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    done.fetch_or(1ull << dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load() & bit)) {
+    VSX_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.fetch_or(bit);
   }
-  raster_bwd_ws_kernel<<<grid, ws::kThreads, smem, st>>>(a, cam);
-  VSX_LAUNCH_CHECK("raster_bwd");
   return VSX_OK;
 }
 
 static int launch_bwd(const BwdArgs &a, const vsx_camera &cam, cudaStream_t st) {
-  static const bool v3 = [] {
-    const char *e = getenv("VSX_RASTER_BWD");
-    return e && e[0] != 'w';
-  }();
-  if (!v3) return launch_bwd_ws(a, cam, st);
+  constexpr int kBC = 16;
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
-  // VSX_RASTER_BWD="NS,BC" selects the v2 (FFMA) phase-2 splats-per-pass and
-  // splat chunk for A/B timing; NS = 0 (default) is the tensor-core v3 with
-  // chunk BC (default 16).
-  static int ns = 0, bc = 16;
-  static bool attr = false;
-  if (!attr) {
-    if (const char *sel = getenv("VSX_RASTER_BWD")) sscanf(sel, "%d,%d", &ns, &bc);
-    const int p32 = (int)(sizeof(float) * 2 * 32 * kPlaneStride);
-    const int p16 = (int)(sizeof(float) * 2 * 16 * kPlaneStride);
-    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_tc_kernel<32>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, p32));
-    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_tc_kernel<16>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, p16));
-    const int s32 = (int)(sizeof(float2) * 32 * kTilePixels);
-    const int s16 = (int)(sizeof(float2) * 16 * kTilePixels);
-    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<1, 16>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, s16));
-    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<2, 16>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, s16));
-    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<1, 32>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
-    VSX_CUDA_TRY(cudaFuncSetAttribute(raster_bwd_kernel<2, 32>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
-    attr = true;
-  }
-  if (ns == 0) {
-    const int smem = (int)(sizeof(float) * 2 * bc * kPlaneStride);
-    if (bc == 16) raster_bwd_tc_kernel<16><<<grid, 256, smem, st>>>(a, cam);
-    else raster_bwd_tc_kernel<32><<<grid, 256, smem, st>>>(a, cam);
-    VSX_LAUNCH_CHECK("raster_bwd");
-    return VSX_OK;
-  }
-  const int smem = (int)(sizeof(float2) * bc * kTilePixels);
-  if (bc == 16) {
-    if (ns == 1) raster_bwd_kernel<1, 16><<<grid, 256, smem, st>>>(a, cam);
-    else raster_bwd_kernel<2, 16><<<grid, 256, smem, st>>>(a, cam);
-  } else {
-    if (ns == 1) raster_bwd_kernel<1, 32><<<grid, 256, smem, st>>>(a, cam);
-    else raster_bwd_kernel<2, 32><<<grid, 256, smem, st>>>(a, cam);
-  }
+  const int smem = (int)(sizeof(float) * 2 * kBC * kPlaneStride);
+  static std::atomic<uint64_t> done{0};
+  if (int rc = smem_opt_in(raster_bwd_tc_kernel<kBC>, smem, done)) return rc;
+  raster_bwd_tc_kernel<kBC><<<grid, 256, smem, st>>>(a, cam);
   VSX_LAUNCH_CHECK("raster_bwd");
   return VSX_OK;
 }
@@ -1470,55 +717,11 @@ static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
                       cudaStream_t st) {
   VSX_REQUIRE(cam.width > 0 && cam.height > 0 && t_final && n_contrib, "raster_fwd: bad args");
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
-  // VSX_RASTER_FWD=tc selects the tensor-core-accumulation forward (A/B: it
-  // measured 6.0 vs 5.7 ms/step on cfg2 — the forward is bound by the alpha
-  // recursion, not by the 8 accumulation FMAs it removes)
-  static const bool tc = [] {
-    const char *e = getenv("VSX_RASTER_FWD");
-    return e && e[0] == 't';
-  }();
-  // VSX_RASTER_FWD=1|2|4: pixels per thread (A/B)
-  static const int fwd_px = [] {
-    const char *e = getenv("VSX_RASTER_FWD");
-    return (e && (e[0] == '1' || e[0] == '4')) ? e[0] - '0' : 2;
-  }();
-  static const int fwd_u = [] {  // second digit: splats per alpha batch
-    const char *e = getenv("VSX_RASTER_FWD");
-    return (e && e[0] && e[1] >= '1' && e[1] <= '8') ? e[1] - '0' : 4;
-  }();
-  const bool px1 = fwd_px == 1;
-  if (tc) {
-    const int smem = (int)(sizeof(float) * 8 * kFwPlane);
-    static bool attr = false;
-    if (!attr) {
-      VSX_CUDA_TRY(cudaFuncSetAttribute(raster_fwd_tc_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
-    raster_fwd_tc_kernel<<<grid, 256, smem, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha,
-                                                  depth, normal, raw_normal, valid, t_final,
-                                                  n_contrib, L);
-  }
-  else if (px1)
-    raster_fwd_kernel<<<grid, 256, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha, depth,
-                                            normal, raw_normal, valid, t_final, n_contrib, L);
-  else {
-#define VSX_FWD2(P, U)                                                                        \
-  raster_fwd2_kernel<P, U><<<grid, 256 / P, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha, \
-                                                     depth, normal, raw_normal, valid, t_final,  \
-                                                     n_contrib, L)
-    switch (fwd_px * 10 + fwd_u) {
-      case 21: VSX_FWD2(2, 1); break;
-      case 24: VSX_FWD2(2, 4); break;
-      case 26: VSX_FWD2(2, 6); break;
-      case 28: VSX_FWD2(2, 8); break;
-      case 41: VSX_FWD2(4, 1); break;
-      case 42: VSX_FWD2(4, 2); break;
-      case 22: VSX_FWD2(2, 2); break;
-      default: VSX_FWD2(2, 4); break;
-    }
-#undef VSX_FWD2
-  }
+  // two horizontally adjacent pixels per thread, alpha batches of 4 splats
+  // (the measured optimum: DESIGN.md §3, scripts/ab_fwd.py)
+  raster_fwd2_kernel<2, 4><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha,
+                                                 depth, normal, raw_normal, valid, t_final,
+                                                 n_contrib, L);
   VSX_LAUNCH_CHECK("raster_fwd");
   return VSX_OK;
 }

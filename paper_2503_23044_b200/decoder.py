@@ -286,6 +286,54 @@ def decode_indices(params: DecoderParams, scene, active: torch.Tensor, view: Cam
     return batch
 
 
+def decode_inputs(centers: torch.Tensor, embeddings: torch.Tensor, cam_center,
+                  lod_ref: float) -> torch.Tensor:
+    """The (V, 36) decoder input block [emb | d/ref | (c - cam)/d], d clamped
+    at 1e-12 (``decoder.py:142-147``), on the device.
+
+    API compatibility only: the training path never materialises it (K2
+    assembles each row in registers from the anchor arrays)."""
+    require_cuda()
+    c = torch.as_tensor(centers, device="cuda", dtype=torch.float64)
+    rel = c - torch.as_tensor(np.asarray(cam_center, np.float64), device="cuda")
+    dist = torch.linalg.norm(rel, dim=-1, keepdim=True).clamp_min(1e-12)
+    emb = torch.as_tensor(embeddings, device="cuda")
+    return torch.cat([emb.double(), dist / lod_ref, rel / dist], dim=-1).to(emb.dtype)
+
+
+def decode_arrays(params: DecoderParams, centers, embeddings, scales, offsets,
+                  view: CameraView, lod_ref: float, max_scale: float) -> dict:
+    """Decode V voxels of explicit state into (V, n, ...) gaussian attributes
+    (``decoder.py:150-180``) through the K2 kernel.
+
+    ``scales`` is the voxel scale triple l_v (positive); the kernel takes log
+    scales, so it is passed as log(l_v) (differentiably when it requires
+    grad). Graph-connected when any input or weight requires grad, with the
+    K8 kernel as its backward."""
+    require_cuda()
+    c = torch.as_tensor(centers, device="cuda", dtype=torch.float64).reshape(-1, 3).contiguous()
+    v, n = int(c.shape[0]), params.n
+    f32 = lambda x: torch.as_tensor(x, device="cuda").float()  # noqa: E731
+    emb = f32(embeddings).reshape(v, -1).contiguous()
+    log_s = torch.log(f32(scales).reshape(v, 3)).contiguous()
+    off = f32(offsets).reshape(v, n, 3).contiguous()
+    active = torch.arange(v, dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    w = [params.tensors[k] for k in params.param_names(n)]
+    if torch.is_grad_enabled() and any(t.requires_grad for t in [emb, log_s, off, *w]):
+        meta = (params, active, c, view, float(lod_ref), float(max_scale), status)
+        outs = _DecodeFn.apply(meta, emb, log_s, off, *w)
+    else:
+        dec = _decode(params.abi(), n, active, c, emb, log_s, off, view, float(lod_ref),
+                      float(max_scale), status, keep_cache=False)
+        outs = (dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal)
+    check_status(status, "decode_arrays")
+    means, opac, col, scl, quat, nrm = outs
+    return {"means": means.reshape(v, n, 3), "opacities": opac.reshape(v, n),
+            "colors": col.reshape(v, n, 3), "scales": scl.reshape(v, n, 3),
+            "quats": quat.reshape(v, n, 4), "normals": nrm.reshape(v, n, 3)}
+
+
 def decode_level(params: DecoderParams, scene, level: int, indices: np.ndarray,
                  view: CameraView, max_scale: float | None = None, state=None,
                  keep_graph: bool = False) -> dict | None:

@@ -11,6 +11,7 @@ contract (``renderer.py:347-367``).
 
 from __future__ import annotations
 
+import copy
 import time
 from dataclasses import dataclass, field
 
@@ -244,15 +245,63 @@ def rasterize_view(splats: ProjectedSplats, view: CameraView,
 
 def rasterize_patch(patch: PatchRect, splats: ProjectedSplats, view: CameraView,
                     tasks: frozenset[str] = ALL_TASKS, indices: np.ndarray | None = None) -> dict:
-    """One pixel rectangle of the view; tile-aligned patches equal the stitched view."""
-    if indices is not None and indices.size > 1 and np.any(np.diff(indices) <= 0):
+    """Blend exactly the splats ``indices`` (default: ``splats_for_rect`` of
+    the rectangle) over every pixel of one pixel rectangle
+    (``renderer.py:304-344``); returns (h, w[, c]) tensors plus 'valid'.
+
+    Runs the K5 kernel on a virtual (w x h) image whose origin is the
+    rectangle's corner: the selected records are gathered in their (z, gid)
+    order with the mean shifted by (-x0, -y0), the principal point likewise,
+    and every 16x16 sub-tile lists all of them (the reference blends the
+    whole overlap set at every pixel of the patch, no per-tile cut). A
+    tile-aligned 16x16 patch with its bin list equals rasterize_view's tile.
+    Differentiable through the projected splats when they carry a graph.
+    """
+    splats.assert_sorted()
+    if indices is None:
+        indices = splats_for_rect(splats, patch.x0, patch.y0, patch.width, patch.height)
+    indices = np.asarray(indices, np.int64)
+    if indices.size > 1 and np.any(np.diff(indices) <= 0):
         raise ContractViolation("patch splat indices must be ascending")
-    targets, _ = rasterize_view(splats, view, tasks)
-    sl = (slice(patch.y0, patch.y0 + patch.height), slice(patch.x0, patch.x0 + patch.width))
-    out = {"valid": targets.valid[sl]}
-    for k in ("rgb", "depth", "normal", "alpha"):
-        if k in tasks or k == "alpha":
-            out[k] = getattr(targets, k)[sl]
+    w, h = int(patch.width), int(patch.height)
+    if w <= 0 or h <= 0:
+        raise InvalidInput("patch must have a positive size")
+    # the virtual view: same pose and focal lengths, origin at the corner (its
+    # principal point may lie outside the rectangle, so no re-validation)
+    sub_view = copy.copy(view)
+    sub_view.width, sub_view.height = w, h
+    sub_view.cx, sub_view.cy = view.cx - patch.x0, view.cy - patch.y0
+    n = int(indices.size)
+    if n == 0:
+        z = torch.zeros((h, w), dtype=torch.float32, device="cuda")
+        out = {"alpha": z.clone(), "valid": torch.zeros((h, w), dtype=torch.bool, device="cuda")}
+        for k, c in (("rgb", 3), ("depth", 0), ("normal", 3)):
+            if k in tasks:
+                out[k] = torch.zeros((h, w, c) if c else (h, w), device="cuda")
+        return out
+    idx = torch.as_tensor(indices, device="cuda")
+    P = splats._P
+    rec = P.rec[idx].clone()
+    rec.view(torch.float64)[:, 0:2] -= torch.tensor([float(patch.x0), float(patch.y0)],
+                                                    dtype=torch.float64, device="cuda")
+    sub = D.Projected(rec, P.radius[idx], P.zkey[idx], P.src[idx], n)
+    txn, tyn = (w + 15) // 16, (h + 15) // 16
+    T = txn * tyn
+    offs = (torch.arange(T + 1, device="cuda", dtype=torch.int64) * n).to(torch.int32)
+    lst = torch.arange(n, device="cuda", dtype=torch.int32).repeat(T)
+    B = D.Bins(offs, lst, txn, tyn)
+    box: list = []
+    if splats.feat is not None and torch.is_grad_enabled():
+        rgb, alpha, depth, normal, raw, valid = _RasterFn.apply(splats.feat[idx], sub, B, sub_view,
+                                                                box)
+    else:
+        R = D.raster_forward(sub, B, sub_view)
+        rgb, alpha, depth, normal, valid = R.rgb, R.alpha, R.depth, R.normal, R.valid
+    valid_b = valid.bool() if "depth" in tasks else (alpha.detach() >= ALPHA_VALID_MIN)
+    out = {"valid": valid_b, "alpha": alpha}
+    for k, t in (("rgb", rgb), ("depth", depth), ("normal", normal)):
+        if k in tasks:
+            out[k] = t
     return out
 
 

@@ -34,7 +34,7 @@ from ._lib import VsxLossDesc, call, ptr, stream
 from .decoder import AnchorState, DecoderParams, decoder_backward_into
 from .errors import InvalidInput, NumericalError
 from .geometry import CameraView
-from .partition import assign_voxels
+from .partition import PatchCostModel, assign_voxels, balance_report, schedule_patches
 
 ADAM_EPS = 1e-15
 
@@ -215,6 +215,9 @@ class TrainState:
         self.assignment = assign_voxels(scene, cfg.workers)
         self.dscene = D.device_scene_for(scene)
         self._image_cache: dict = {}
+        # per-patch EMA cost model of the simulated multi-worker schedule
+        # (trainer.py:264-268, 355-364); only consulted when cfg.workers > 1
+        self.cost_model = PatchCostModel()
         self._inflight = None
         # growth pressure (trainer.py:341-349): per anchor, sum and count of
         # the decoded-position gradient norms of its gaussians (flat, level-major)
@@ -549,6 +552,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     isects = 0
     anchors, agrads = state.anchors, state.anchor_grads
     stager = _InputStager(views, images, priors, have, normal_priors, have_n)
+    book = _WorkerBook(state, views) if cfg.workers > 1 else None
     main = torch.cuda.current_stream()
     # Three-stream software pipeline over the views: the front end of view v+1
     # (cull, decode, project + sort, binning: small, latency-bound kernels and
@@ -608,12 +612,16 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             main.wait_event(ev)
         gaussians += dec.count
         isects += Bn.intersections
+        if book is not None:
+            book.view_start(vi, active, Bn)
         return active, dec, P, Bn
 
     def backward(vi, active, dec, P, Bn, R, loss):
         view = views[vi]
         with _span(timer, "raster_bwd"):
             gs = D.raster_backward(P, Bn, view, R, loss=loss)
+        if book is not None:
+            book.view_end(vi)
         # projection + decoder backward of this view run on the tail stream,
         # overlapping the next view's compositor; they are the only writers
         # of the parameter gradients, so one stream keeps them ordered
@@ -723,11 +731,79 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     report = StepReport(
         step=state.step, total=total, rgb=rgb, depth=depth, geo=geo_val, w2=w2, w3=w3,
         lr=cosine_lr(state.step, cfg.lr_decoder, cfg), supervised_depth_px=supervised,
-        geo_pairs=geo_pairs, geo_patches=geo_patches, gaussians=gaussians, transfer_bytes=0,
-        imbalance=1.0, max_tile_splats=int(host[5]), seconds=time.perf_counter() - t0,
+        geo_pairs=geo_pairs, geo_patches=geo_patches, gaussians=gaussians,
+        transfer_bytes=book.transfer_bytes() if book is not None else 0,
+        imbalance=book.imbalance() if book is not None else 1.0,
+        max_tile_splats=int(host[5]), seconds=time.perf_counter() - t0,
         intersections=isects, normal=normal, live_pairs=int(host[6]))
     state.step += 1
     return report
+
+
+class _WorkerBook:
+    """The reference's simulated multi-worker bookkeeping of one step
+    (``trainer.py:264-268, 276-289, 352-364``), for cfg.workers > 1: the LPT
+    patch schedule from the EMA cost model, the bytes moved to each view's
+    renderer workers (foreign gaussians x 136 B, ``renderer.py:452-477``) and
+    the balance report, whose per-patch seconds are the view's measured
+    compositing time (CUDA events, read after the step's one sync) split by
+    tile-list length + 1. With one worker both fields are their constants
+    (0 bytes, imbalance 1.0), exactly as the reference's."""
+
+    def __init__(self, state, views):
+        self.state, self.views = state, views
+        W = state.cfg.workers
+        self.schedule = schedule_patches(views, W, state.cost_model)
+        self.patches_by_view: dict[int, list[int]] = {}
+        for j, pr in enumerate(self.schedule.patches):
+            self.patches_by_view.setdefault(pr.view_id, []).append(j)
+        self.owner = torch.as_tensor(state.assignment.flat_owner().astype(np.int64),
+                                     device="cuda")
+        self.counts = torch.zeros((len(views), W), dtype=torch.int64, device="cuda")
+        self.active_n = [0] * len(views)
+        self.tile_counts: list = [None] * len(views)
+        self.ev: dict = {}
+
+    def view_start(self, vi, active, Bn) -> None:
+        a = active.long()
+        self.active_n[vi] = int(a.numel())
+        if a.numel():
+            self.counts[vi] = torch.bincount(self.owner[a], minlength=self.counts.shape[1])
+        self.tile_counts[vi] = Bn.tile_offsets[1:].long() - Bn.tile_offsets[:-1].long()
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.ev[vi] = [e]
+
+    def view_end(self, vi) -> None:
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.ev[vi].append(e)
+
+    def _renderers(self, v) -> set:
+        return {int(self.schedule.workers[j]) for j in self.patches_by_view[v.view_id]}
+
+    def transfer_bytes(self) -> int:
+        n = self.state.n
+        counts = self.counts.cpu().numpy()
+        total = 0
+        for vi, v in enumerate(self.views):
+            g = self.active_n[vi] * n
+            for w in self._renderers(v):
+                total += (g - int(counts[vi, w]) * n) * 136   # BYTES_PER_GAUSSIAN
+        return int(total)
+
+    def imbalance(self) -> float:
+        measured = np.zeros(len(self.schedule.patches))
+        for vi, v in enumerate(self.views):
+            a, b = self.ev[vi]
+            secs = a.elapsed_time(b) / 1e3
+            weights = self.tile_counts[vi].cpu().numpy().astype(np.float64) + 1.0
+            share = weights / weights.sum()
+            for j, sh in zip(self.patches_by_view[v.view_id], share):
+                measured[j] = secs * sh
+        st = self.state
+        return balance_report(st.assignment, self.schedule, measured, epoch=st.step,
+                              cost_model=st.cost_model).imbalance
 
 
 OCTANT_SIGNS = np.array([[sx, sy, sz] for sx in (-1.0, 1.0)

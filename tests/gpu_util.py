@@ -88,18 +88,21 @@ def noise_floor_close(got, ref, rel, noise) -> tuple[bool, float, int]:
     return worst <= rel and zeros_ok, worst, int((~keep & ~zero).sum())
 
 
-def conditioned_close(got, ref, ref_pert, rel, k) -> tuple[bool, float, float, int]:
-    """Element-wise |got - ref| <= rel * |ref| + k * |ref - ref_pert|, nothing excluded.
+def conditioned_close(got, ref, ref_pert, rel, k, eps=0.0) -> tuple[bool, float, float, int]:
+    """Element-wise |got - ref| <= rel |ref| + k |ref - ref_pert| + eps rms(ref).
 
-    ``ref_pert`` is the float64 reference evaluated with every input moved by
-    one float32 ulp: |ref - ref_pert| is the element's sensitivity to the
-    input rounding every float32 evaluation carries (a cancelling sum has a
-    large one). Returns (ok, worst err / bound, worst plain relative error
-    over the elements whose floor is below rel * |ref| / 10, number of
-    elements whose floor term dominates the bound).
+    Nothing is excluded. ``ref_pert`` is the float64 reference evaluated with
+    every input (or intermediate) moved by one float32 ulp: |ref - ref_pert|
+    is the element's sensitivity to the rounding every float32 evaluation
+    carries (a cancelling sum has a large one). ``eps`` rms(ref) is the
+    absolute noise floor of float32 accumulation at the tensor's scale.
+    Returns (ok, worst err / bound, worst plain relative error over the
+    elements whose floors are below rel |ref| / 10, number of elements whose
+    floor terms dominate the bound).
     """
     got, ref = np.asarray(got, np.float64).ravel(), np.asarray(ref, np.float64).ravel()
-    floor = k * np.abs(ref - np.asarray(ref_pert, np.float64).ravel())
+    rms = float(np.sqrt(np.mean(ref * ref))) if ref.size else 0.0
+    floor = k * np.abs(ref - np.asarray(ref_pert, np.float64).ravel()) + eps * rms
     err = np.abs(got - ref)
     bound = rel * np.abs(ref) + floor
     zero = bound == 0.0
