@@ -827,8 +827,8 @@ __global__ void __launch_bounds__(kDfwWarps * 32, 1) decode_fwd_mma_kernel(
       for (int q = 0; q < 9; ++q) o[q][0] = o[q][1] = o[q][2] = o[q][3] = 0.f;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        const float v0 = tanhf(c[kk][0]), v1 = tanhf(c[kk][1]);
-        const float v2 = tanhf(c[kk][2]), v3 = tanhf(c[kk][3]);
+        const float v0 = tanh_fast(c[kk][0]), v1 = tanh_fast(c[kk][1]);
+        const float v2 = tanh_fast(c[kk][2]), v3 = tanh_fast(c[kk][3]);
         if (cache_h) {
           const int k0 = h * 64 + kk * 8 + 2 * t;
           float *h0 = cache_h + (size_t)k0 * ld, *h1 = h0 + ld;

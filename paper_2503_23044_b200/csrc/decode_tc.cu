@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
         umma::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          v[i] = tanhf(v[i]);
+          v[i] = tanh_fast(v[i]);
           if (valid && cache_h) cache_h[(size_t)(h * 64 + c + i) * ld + r] = v[i];
         }
 #pragma unroll
