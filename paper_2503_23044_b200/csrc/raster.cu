@@ -348,6 +348,12 @@ constexpr int kUB = VSX_BWD_UB;  // phase-1 splats per alpha batch
 #ifndef VSX_BWD_STAGE_WARP
 #define VSX_BWD_STAGE_WARP 7
 #endif
+#ifndef VSX_BWD_SORTPIX
+#define VSX_BWD_SORTPIX 1
+#endif
+#ifndef VSX_BWD_P0SKIP
+#define VSX_BWD_P0SKIP 1
+#endif
 #ifndef VSX_BWD_MERGED
 #define VSX_BWD_MERGED 1
 #endif
@@ -388,14 +394,51 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   const int tile = a.L.tile_order ? (int)a.L.tile_order[lin] : lin;
   const int bx = tile % txn, by = tile / txn;
   const int t = threadIdx.x;
-  const int lx = t & 15, ly = t >> 4;
+  const int lane = t & 31, warp = t >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+#if VSX_BWD_SORTPIX
+  // Slot t (thread, plane column) takes the pixel of rank t in descending
+  // live count (8-splat buckets): pixels that stop compositing at similar
+  // depths share a warp, so phase 1 runs fewer idle lanes and whole warps go
+  // quiet together. Phases 0 / 2 follow the slot order through the per-tile
+  // fragments (cotangents and pixel moments are staged per slot).
+  __shared__ uint32_t s_bin[256];
+  __shared__ uint32_t s_wsum[8];
+  __shared__ uint8_t s_perm[256];  // slot -> pixel (t = 16 y + x)
+  {
+    const int x0 = bx * kTile + (t & 15), y0 = by * kTile + (t >> 4);
+    const int nc0 = (x0 < cam.width && y0 < cam.height) ? a.nc[(size_t)y0 * cam.width + x0] : 0;
+    const uint32_t key = 255u - (uint32_t)min(nc0 >> 3, 255);
+    s_bin[t] = 0u;
+    __syncthreads();
+    const uint32_t r = atomicAdd(&s_bin[key], 1u);  // order inside a bucket is free
+    __syncthreads();
+    // exclusive scan of the 256 bucket counts
+    uint32_t v = s_bin[t], inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    uint32_t base = 0;
+    for (int w = 0; w < warp; ++w) base += s_wsum[w];
+    s_bin[t] = base + inc - v;
+    __syncthreads();
+    s_perm[s_bin[key] + r] = (uint8_t)t;
+    __syncthreads();
+  }
+  const int pix = s_perm[t];
+#else
+  const int pix = t;
+#endif
+  const int lx = pix & 15, ly = pix >> 4;
   const int px = bx * kTile + lx, py = by * kTile + ly;
   const bool inside = px < cam.width && py < cam.height;
   const double ox = (double)(bx * kTile), oy = (double)(by * kTile);
   const uint32_t begin = a.tile_off[tile];
   const float fx = (float)lx, fy = (float)ly;
-  const int lane = t & 31, warp = t >> 5;
-  const int g = lane >> 2, tq = lane & 3;
   if (t == 0) s_max = 0;
   int nc = 0;
   float T = 1.f;
@@ -437,7 +480,11 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     const float h0 = __uint_as_float(tf32_rn(v0)), h1 = __uint_as_float(tf32_rn(v1));
     s_bw[ks][ln] = make_float4(h0, h1, __uint_as_float(tf32_rn(v0 - h0)),
                                __uint_as_float(tf32_rn(v1 - h1)));
+#if VSX_BWD_SORTPIX
+    s_bq[ks][ln] = make_float2(pixel_moment(s_perm[p0], f), pixel_moment(s_perm[p1], f));
+#else
     s_bq[ks][ln] = make_float2(pixel_moment(p0, f), pixel_moment(p1, f));
+#endif
   }
   __syncthreads();
   const uint32_t stop = begin + (uint32_t)s_max;
@@ -506,9 +553,14 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     stage(buf, cs, cnt);
     __syncthreads();
 #endif
+    const int kbase = (int)(cs - begin);
+    const int jlive = min(cnt, nc - kbase);
     // ---- phase 0: sk[j][p] = F[p] . P[j] for this warp's 32 pixels on the
     // tensor cores (3xTF32), written into the q plane that phase 1 overwrites
-    // in place with q (same thread, same slot)
+    // in place with q (same thread, same slot). Skipped by a warp none of
+    // whose pixels is live in this chunk (with pixels sorted by live count,
+    // whole warps go quiet together): phase 1 then only writes its zeros.
+    if (!VSX_BWD_P0SKIP || __any_sync(0xffffffffu, jlive > 0))
 #pragma unroll
     for (int nt = 0; nt < kBC / 8; ++nt) {
       const float4 b = s_ph[buf][8 * nt + g][tq];
@@ -526,9 +578,7 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
       }
     }
     __syncwarp();
-    // ---- phase 1: per-pixel back-to-front recursion (as v2)
-    const int kbase = (int)(cs - begin);
-    const int jlive = min(cnt, nc - kbase);
+    // ---- phase 1: per-pixel back-to-front recursion
     for (int j = cnt - 1; j >= max(jlive, 0); --j) {
       wpl[j * kPlaneStride + t] = 0.f;
       qpl[j * kPlaneStride + t] = 0.f;
@@ -602,6 +652,8 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
         lo[3] = __float_as_uint(x3 - __uint_as_float(hi[3]));
       };
       // warp-uniform plane branch outside the k loop: no predicated HMMAs
+      // (skipping the k-ranges of quiet pixel warps here measured 1,469 ->
+      // 1,583 us: the branch costs more than the zero products it saves)
       if (plane == 0) {
 #pragma unroll 4
         for (int kk = 0; kk < kKS; ++kk) {

@@ -179,6 +179,26 @@ def return_grads(plan: ExchangePlan, grads: dict[int, torch.Tensor], like: torch
     return out
 
 
+class _StagedView:
+    """Indexable view of one input kind of an _InputStager (0 = image,
+    1 = depth prior, 2 = normal prior); indexing waits for the view's copy."""
+
+    def __init__(self, stager, kind):
+        self.stager, self.kind = stager, kind
+
+    def __getitem__(self, v):
+        gt, pd, pv, pn, pnv = self.stager.get(v)
+        if self.kind == 0:
+            return gt
+        if self.kind == 1:
+            return None if pd is None else (pd, pv)
+        return None if pn is None else (pn, pnv)
+
+
+def _StagedInputs(stager, B):
+    return _StagedView(stager, 0), _StagedView(stager, 1), _StagedView(stager, 2)
+
+
 def sharded_train_step(backend, views, images, priors=None, normal_priors=None, group=None,
                        scheduler=None):
     """One sharded step; returns the global loss terms (same on every rank).
@@ -207,7 +227,15 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
     renderers = np.asarray(renderers if renderers is not None
                            else [renderer_of(v, world) for v in range(B)], dtype=np.int64)
     backend.begin_step(views, have, have_n)
-    from .trainer import _pipeline_enabled
+    from .trainer import _InputStager, _pipeline_enabled, _prior_arrays
+    if hasattr(backend, "prepare"):
+        # the targets / priors of the views this rank renders go to the
+        # device up front on the copy stream (non-blocking from pinned host
+        # memory), each view's compositor waiting only for its own inputs
+        dpri = None if priors is None else [_prior_arrays(p) for p in priors]
+        stager = _InputStager(views, images, dpri, set(have), normal_priors, set(have_n),
+                              only={v for v in range(B) if int(renderers[v]) == rank})
+        images, priors, normal_priors = _StagedInputs(stager, B)
     if hasattr(backend, "prepare") and _pipeline_enabled():
         timers = _pipelined_views(backend, views, images, priors, normal_priors, group,
                                   renderers, rank, world)

@@ -483,13 +483,17 @@ class _InputStager:
     earlier ones. CUDA inputs pass through untouched.
     """
 
-    def __init__(self, views, images, priors, have, normal_priors, have_n):
+    def __init__(self, views, images, priors, have, normal_priors, have_n, only=None):
         cur = torch.cuda.current_stream()
         cs = _side_stream("copy")
         cs.wait_stream(cur)
         self.items, self.events = [], []
         with torch.cuda.stream(cs):
             for vi, view in enumerate(views):
+                if only is not None and vi not in only:   # rendered by another rank
+                    self.items.append((None,) * 5)
+                    self.events.append(None)
+                    continue
                 H, W = view.height, view.width
                 gt = _to_device_image(images[vi], (H, W, 3))
                 pd = pv = pn = pnv = None
@@ -508,7 +512,8 @@ class _InputStager:
                 self.events.append(ev)
 
     def get(self, vi):
-        torch.cuda.current_stream().wait_event(self.events[vi])
+        if self.events[vi] is not None:
+            torch.cuda.current_stream().wait_event(self.events[vi])
         return self.items[vi]
 
 

@@ -118,8 +118,15 @@ for name in ["emb", "log_scales", "offsets"]:
         st = res[r]["state"]
         g = st.flat.view(st.flat.param, name).cpu().numpy()
         got[owner == r] = g[owner == r]
-    bad = np.abs(got - want) > 1e-5 * np.maximum(np.abs(got), np.abs(want)) + 1e-7
+    diff = np.abs(got - want)
+    bad = diff > 1e-5 * np.maximum(np.abs(got), np.abs(want)) + 1e-7
     out["param_bad_frac"][name] = float(bad.mean())
+    # an element whose gradient sits at float32 summation noise (the ranks add
+    # the per-view contributions in another order) can take an Adam step of
+    # either sign; Adam's update is bounded by lr per step, so any element's
+    # divergence is bounded by 2 lr STEPS (lrs at step 0 are the largest)
+    lr0 = TrainState(golden_scene(d), TrainConfig(**cfg)).lrs()[name]
+    out.setdefault("param_adam_ratio", {})[name] = float(diff.max() / (2 * lr0 * STEPS))
 gs_ref = ref.grow_sum_flat.cpu().numpy()
 gc_ref = ref.grow_cnt_flat.cpu().numpy()
 out["growth_ok"] = all(
