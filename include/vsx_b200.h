@@ -229,6 +229,22 @@ int vsx_bin_emit_tiles(const vsx_splat *rec, const double *radius, int32_t n, in
                        uint32_t *tile_list, vsx_stream s);
 int vsx_tile_segsort(const uint32_t *tile_offsets, int32_t num_tiles, uint32_t *tile_list,
                      int32_t max_len, vsx_stream s);
+/* Row-column binning (the training path; width and height <= 4096 pixels,
+ * i.e. <= 256 tile rows and columns): two stable counting sorts with the
+ * tile rectangle expanded on the fly, replacing phases 1-3. vsx_bin_plan
+ * computes each splat's rectangle (renderer.py:216-221) into plan_ws and
+ * totals[0] = row entries (sum of rectangle heights), totals[1] = pairs
+ * (copied to `totals`, device or pinned host, when not NULL). After the
+ * caller reads them, vsx_bin_build (once per plan) writes tile_offsets (T+1)
+ * and tile_list (pairs) — bit for bit the sorted (tile, rank) lists of
+ * phases 1-3 — using a build workspace of vsx_bin_build_ws_bytes(row_entries). */
+size_t vsx_bin_plan_ws_bytes(int32_t n, int32_t width, int32_t height);
+size_t vsx_bin_build_ws_bytes(int32_t width, int32_t height, int64_t row_entries);
+int vsx_bin_plan(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
+                 int32_t height, void *plan_ws, size_t plan_bytes, uint64_t *totals, vsx_stream s);
+int vsx_bin_build(int32_t n, int32_t width, int32_t height, int64_t row_entries, int64_t pairs,
+                  void *plan_ws, size_t plan_bytes, void *build_ws, size_t build_bytes,
+                  uint32_t *tile_offsets, uint32_t *tile_list, vsx_stream s);
 
 /* ---- K5: compositing forward (renderer.py:242-301, 390-449) ----------- */
 /* tile_offsets (T+1) CSR over tile_list (sorted ranks). Outputs are HWC

@@ -115,6 +115,10 @@ _SIGS = {
     "vsx_tsdf_integrate": ([P, P, P, P, c_f64, c_f64, P, P, VsxCamera, P, P], c_i32),
     "vsx_bin_emit_tiles": ([P, P, c_i32, c_i32, c_i32, P, P, P, P], c_i32),
     "vsx_tile_segsort": ([P, c_i32, P, c_i32, P], c_i32),
+    "vsx_bin_plan_ws_bytes": ([c_i32, c_i32, c_i32], c_size),
+    "vsx_bin_build_ws_bytes": ([c_i32, c_i32, c_i64], c_size),
+    "vsx_bin_plan": ([P, P, c_i32, c_i32, c_i32, P, c_size, P, P], c_i32),
+    "vsx_bin_build": ([c_i32, c_i32, c_i32, c_i64, c_i64, P, c_size, P, c_size, P, P, P], c_i32),
 }
 
 EXPORTED = tuple(_SIGS)

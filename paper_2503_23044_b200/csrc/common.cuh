@@ -183,4 +183,20 @@ __device__ __forceinline__ int argmin3(T a, T b, T c) {
   return i;
 }
 
+// Tile rectangle of a splat (renderer.py:216-221), float64 floor semantics.
+__device__ __forceinline__ bool tile_rect(double u, double v, double r, int txn, int tyn, int &x0,
+                                          int &x1, int &y0, int &y1) {
+  // x / 16 == x * 0.0625 exactly (power of two), without the f64 divide
+  const double fx0 = fmax(floor(dmul(dsub(u, r), 0.0625)), 0.0);
+  const double fx1 = fmin(floor(dmul(dadd(u, r), 0.0625)), (double)(txn - 1));
+  const double fy0 = fmax(floor(dmul(dsub(v, r), 0.0625)), 0.0);
+  const double fy1 = fmin(floor(dmul(dadd(v, r), 0.0625)), (double)(tyn - 1));
+  if (!(fx1 >= fx0) || !(fy1 >= fy0)) return false;
+  x0 = (int)fx0;
+  x1 = (int)fx1;
+  y0 = (int)fy0;
+  y1 = (int)fy1;
+  return true;
+}
+
 }  // namespace vsx

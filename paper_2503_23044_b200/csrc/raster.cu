@@ -357,6 +357,9 @@ constexpr int kUB = VSX_BWD_UB;  // phase-1 splats per alpha batch
 #ifndef VSX_BWD_MERGED
 #define VSX_BWD_MERGED 1
 #endif
+#ifndef VSX_BWD_PREFIX
+#define VSX_BWD_PREFIX 1
+#endif
 constexpr int kPlaneStride = kTilePixels + 4;  // 4 mod 32: conflict-free A fragments
 
 // pixel moment m of tile pixel p (x, y about the tile centre)
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   // depths share a warp, so phase 1 runs fewer idle lanes and whole warps go
   // quiet together. Phases 0 / 2 follow the slot order through the per-tile
   // fragments (cotangents and pixel moments are staged per slot).
-  __shared__ uint32_t s_bin[256];
+  __shared__ uint32_t s_bin[257];  // after the scan: first slot of each key; [256] = 256
   __shared__ uint32_t s_wsum[8];
   __shared__ uint8_t s_perm[256];  // slot -> pixel (t = 16 y + x)
   {
@@ -425,6 +428,7 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     uint32_t base = 0;
     for (int w = 0; w < warp; ++w) base += s_wsum[w];
     s_bin[t] = base + inc - v;
+    if (t == 0) s_bin[256] = 256u;
     __syncthreads();
     s_perm[s_bin[key] + r] = (uint8_t)t;
     __syncthreads();
@@ -555,6 +559,15 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
 #endif
     const int kbase = (int)(cs - begin);
     const int jlive = min(cnt, nc - kbase);
+#if VSX_BWD_SORTPIX && VSX_BWD_PREFIX
+    // Live prefix: slots are in descending (live count >> 3) order, so every
+    // pixel with nc >> 3 < kbase >> 3 (nc <= kbase: dead in this chunk and all
+    // earlier ones) sits after the first s_bin[256 - (kbase >> 3)] slots.
+    // Phases 1 / 2 only touch the k-steps (8 slots) that cover the prefix.
+    const int nks = ((int)s_bin[256 - min(kbase >> 3, 255)] + 7) >> 3;
+#else
+    const int nks = 32;
+#endif
     // ---- phase 0: sk[j][p] = F[p] . P[j] for this warp's 32 pixels on the
     // tensor cores (3xTF32), written into the q plane that phase 1 overwrites
     // in place with q (same thread, same slot). Skipped by a warp none of
@@ -579,10 +592,11 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     }
     __syncwarp();
     // ---- phase 1: per-pixel back-to-front recursion
-    for (int j = cnt - 1; j >= max(jlive, 0); --j) {
-      wpl[j * kPlaneStride + t] = 0.f;
-      qpl[j * kPlaneStride + t] = 0.f;
-    }
+    if (t < 8 * nks)
+      for (int j = cnt - 1; j >= max(jlive, 0); --j) {
+        wpl[j * kPlaneStride + t] = 0.f;
+        qpl[j * kPlaneStride + t] = 0.f;
+      }
     // batches of kUB: the alphas (the long dependent part) are independent
     // across splats; only T and S are carried, one FMUL / FFMA each
     int j = jlive - 1;
@@ -655,9 +669,15 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
       // (skipping the k-ranges of quiet pixel warps here measured 1,469 ->
       // 1,583 us: the branch costs more than the zero products it saves)
       if (plane == 0) {
+        int k0 = kr * kKS, kn = kKS;
+        if (kMT == 1 && nks != 32) {
+          const int q = (nks + 3) >> 2;
+          k0 = kr * q;
+          kn = max(0, min(q, nks - k0));
+        }
 #pragma unroll 4
-        for (int kk = 0; kk < kKS; ++kk) {
-          const int ks = kr * kKS + kk;
+        for (int kk = 0; kk < kn; ++kk) {
+          const int ks = k0 + kk;
           uint32_t hi[4], lo[4];
           a_frag(ks, hi, lo);
           const float4 b = s_bw[ks][lane];
@@ -671,9 +691,13 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
         // 1479 / 1467 / 1479 us per view)
         int k0 = kr * kKS, kn = kKS;
         if (kMT == 1 && VSX_BWD_KR7 != kKS) {
-          constexpr int q = (32 - VSX_BWD_KR7) / 3;
+          const int q = (nks * (32 - VSX_BWD_KR7) / 32 + 2) / 3;
           k0 = kr * q;
-          kn = kr == 3 ? 32 - 3 * q : q;
+          kn = max(0, min(kr == 3 ? nks - 3 * q : q, nks - k0));
+        } else if (kMT == 1 && nks != 32) {
+          const int q = (nks + 3) >> 2;
+          k0 = kr * q;
+          kn = max(0, min(q, nks - k0));
         }
 #pragma unroll 4
         for (int kk = 0; kk < kn; ++kk) {

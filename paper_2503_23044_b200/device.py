@@ -358,13 +358,36 @@ class Bins:
 SEGSORT_CAP = 4096   # vsx_tile_segsort shared-memory capacity
 
 
-def _tile_major_binning() -> bool:
-    """VSX_BIN=tiles selects the tile-major binning (per-tile atomics + per-tile
-    bitonic sort). It is correct but measured 2.5x slower on cfg2 (same-tile
-    atomic contention of neighbouring splats, 78 barrier stages per tile), so
-    the default is the sort-based path (emit pairs + onesweep radix sort)."""
+def _binning() -> str:
+    """Binning variant: "rowcol" (default: row then column stable counting
+    sorts, vsx_bin_plan / vsx_bin_build; images up to 4096 px a side),
+    "sort" (emit (tile, rank) pairs + onesweep radix sort; any size) or
+    "tiles" (per-tile atomics + per-tile bitonic sort; measured 2.5x slower
+    than "sort" on cfg2, kept as an A/B reference)."""
     import os
-    return os.environ.get("VSX_BIN", "sort") == "tiles"
+    return os.environ.get("VSX_BIN", "rowcol")
+
+
+def _tile_major_binning() -> bool:
+    return _binning() == "tiles"
+
+
+def _bin_rowcol(P: Projected, width: int, height: int, txn: int, tyn: int) -> Bins:
+    lib = _lib.load()
+    n, T = P.count, txn * tyn
+    pb = int(lib.vsx_bin_plan_ws_bytes(n, width, height))
+    pw = torch.empty(pb, dtype=torch.uint8, device="cuda")
+    tot = torch.empty(2, dtype=torch.int64, device="cuda")
+    call("vsx_bin_plan", ptr(P.rec), ptr(P.radius), n, width, height, ptr(pw), pb, ptr(tot),
+         stream())
+    E, total = (int(x) for x in tot.cpu())   # the front end's one host read
+    bb = int(lib.vsx_bin_build_ws_bytes(width, height, E))
+    bw = torch.empty(max(bb, 1), dtype=torch.uint8, device="cuda")
+    toff = torch.empty(T + 1, dtype=torch.int32, device="cuda")
+    lst = torch.empty(max(total, 1), dtype=torch.int32, device="cuda")
+    call("vsx_bin_build", n, width, height, E, total, ptr(pw), pb, ptr(bw), bb, ptr(toff), ptr(lst),
+         stream())
+    return Bins(toff, lst[:total], txn, tyn)
 
 
 def bin_tiles(P: Projected, width: int, height: int) -> Bins:
@@ -374,6 +397,8 @@ def bin_tiles(P: Projected, width: int, height: int) -> Bins:
     if n == 0:
         return Bins(torch.zeros(T + 1, dtype=torch.int32, device="cuda"),
                     torch.empty(0, dtype=torch.int32, device="cuda"), txn, tyn)
+    if _binning() == "rowcol" and txn <= 256 and tyn <= 256:
+        return _bin_rowcol(P, width, height, txn, tyn)
     if _tile_major_binning():
         # per-tile counts -> CSR offsets -> atomic tile-major emission ->
         # per-tile sort of the ranks (one host read: total and longest list)

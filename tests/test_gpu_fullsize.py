@@ -63,6 +63,14 @@ def test_one_view_invariants(cfg2):
     same = tile_of[1:] == tile_of[:-1]
     assert bool((lst[1:][same] > lst[:-1][same]).all())
     assert bool(((lst >= 0) & (lst < P.count)).all())
+    # the row-column binning (default) equals the emit + radix sort path
+    import os
+    os.environ["VSX_BIN"] = "sort"
+    try:
+        B2 = D.bin_tiles(P, v.width, v.height)
+    finally:
+        del os.environ["VSX_BIN"]
+    assert torch.equal(B.tile_offsets, B2.tile_offsets) and torch.equal(B.tile_list, B2.tile_list)
     R = D.raster_forward(P, B, v)
     assert bool(torch.isfinite(R.rgb).all()) and bool(torch.isfinite(R.normal).all())
     assert bool(((R.alpha >= 0) & (R.alpha <= 1 + 1e-6)).all())

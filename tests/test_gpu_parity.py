@@ -170,6 +170,55 @@ def test_bin_lists_bitexact_random_large():
     np.testing.assert_array_equal(B.tile_list.cpu().numpy(), lst)
 
 
+def _bin_case(rng, n, W, H, r_hi=120.0, margin=80.0):
+    spl = {"mean2d": np.stack([rng.uniform(-margin, W + margin, n),
+                               rng.uniform(-margin, H + margin, n)], -1),
+           "radius": np.exp(rng.uniform(np.log(0.5), np.log(r_hi), n)),
+           "conic": np.ones((n, 3)), "color": np.zeros((n, 3)), "opacity": np.ones(n),
+           "normal_cam": np.zeros((n, 3)), "plane_d": np.zeros(n)}
+    return spl
+
+
+@pytest.mark.parametrize("variant", ["rowcol", "sort"])
+@pytest.mark.parametrize("case", ["ragged", "one_tile", "single", "offscreen", "cover_all",
+                                  "max_tiles", "dense_row"])
+def test_bin_variants_bitexact_vs_oracle(monkeypatch, variant, case):
+    """Both binning paths (row-column counting sorts, and emit + radix sort)
+    equal the oracle's (tile, rank) lists on the edge cases: image sizes not
+    a multiple of 16, a one-tile image, one splat, every splat off screen,
+    splats covering the whole image, 256 x 256 tiles (the row-column path's
+    limit), and one tile row holding most of the entries (a row split over
+    many column-pass chunks)."""
+    from paper_2503_23044_b200 import device as D
+    monkeypatch.setenv("VSX_BIN", variant)
+    import zlib
+    rng = np.random.default_rng(zlib.crc32(case.encode()))
+    if case == "ragged":
+        W, H, spl = 1000, 563, _bin_case(rng, 30000, 1000, 563)
+    elif case == "one_tile":
+        W, H, spl = 9, 13, _bin_case(rng, 500, 9, 13, r_hi=6.0, margin=4.0)
+    elif case == "single":
+        W, H, spl = 640, 480, _bin_case(rng, 1, 640, 480)
+        spl["mean2d"][0] = (320.0, 240.0)
+        spl["radius"][0] = 40.0
+    elif case == "offscreen":
+        W, H, spl = 640, 480, _bin_case(rng, 3000, 640, 480)
+        spl["mean2d"][:, 0] = rng.uniform(-5000.0, -200.0, 3000)
+    elif case == "cover_all":
+        W, H, spl = 500, 300, _bin_case(rng, 700, 500, 300)
+        spl["radius"][::7] = 4000.0
+    elif case == "max_tiles":
+        W, H, spl = 4096, 4096, _bin_case(rng, 60000, 4096, 4096, r_hi=200.0)
+    else:  # dense_row
+        W, H, spl = 1920, 1080, _bin_case(rng, 40000, 1920, 1080, r_hi=30.0)
+        spl["mean2d"][:, 1] = rng.uniform(500.0, 508.0, 40000)
+        spl["radius"][:] = np.minimum(spl["radius"], 3.5)
+    B = D.bin_tiles(records_from(spl), W, H)
+    off, lst = oracle.bin_tiles(spl["mean2d"], spl["radius"], W, H)
+    np.testing.assert_array_equal(B.tile_offsets.cpu().numpy(), off)
+    np.testing.assert_array_equal(B.tile_list.cpu().numpy(), lst)
+
+
 # ------------------------------------------------------------------ K5 compositing
 
 @pytest.mark.parametrize("tag", ["far", "near"])
