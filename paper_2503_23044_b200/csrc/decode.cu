@@ -757,9 +757,15 @@ __global__ void decoder_fwd_image_kernel(vsx_decoder W, float4 *__restrict__ img
   }
 }
 
-constexpr int kDfwWarps = 16;
+#ifndef VSX_DFW_WARPS
+#define VSX_DFW_WARPS 16
+#endif
+#ifndef VSX_DFW_MINB
+#define VSX_DFW_MINB 1
+#endif
+constexpr int kDfwWarps = VSX_DFW_WARPS;
 
-__global__ void __launch_bounds__(kDfwWarps * 32, 1) decode_fwd_mma_kernel(
+__global__ void __launch_bounds__(kDfwWarps * 32, VSX_DFW_MINB) decode_fwd_mma_kernel(
     vsx_decoder W, const float4 *__restrict__ img, const int32_t *__restrict__ active,
     int32_t n_active, const double *__restrict__ centers, const float *__restrict__ emb,
     vsx_camera cam, double lod_ref, float *__restrict__ cache_h, float *__restrict__ cache_o,
@@ -890,7 +896,7 @@ int decode_fwd_mma(vsx_decoder W, const float *img, const int32_t *active, int32
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = (n_active + 15) / 16;
-  const int grid = std::max(1, std::min(sms, (tiles + kDfwWarps - 1) / kDfwWarps));
+  const int grid = std::max(1, std::min(VSX_DFW_MINB * sms, (tiles + kDfwWarps - 1) / kDfwWarps));
   decode_fwd_mma_kernel<<<grid, kDfwWarps * 32, smem, st>>>(
       W, reinterpret_cast<const float4 *>(img), active, n_active, centers, emb, cam, lod_ref,
       cache_h, cache_o, smem_img);

@@ -200,7 +200,12 @@ class Decoded:
 
 def decode(dec_abi, n: int, active: torch.Tensor, centers: torch.Tensor, emb: torch.Tensor,
            log_scales: torch.Tensor, offsets: torch.Tensor, view: CameraView, lod_ref: float,
-           max_scale: float, status: torch.Tensor, keep_cache: bool) -> Decoded:
+           max_scale: float, status: torch.Tensor, keep_cache: bool,
+           img: torch.Tensor | None = None) -> Decoded:
+    """Decode the active anchors for one view. ``img`` is the decoder weight
+    image of the current weights (``decoder_image``), built once per
+    optimizer step by the callers that decode several views; None builds it
+    here."""
     na = int(active.numel())
     g = na * n
     dev = "cuda"
@@ -216,7 +221,8 @@ def decode(dec_abi, n: int, active: torch.Tensor, centers: torch.Tensor, emb: to
     # the tensor-core path always stages the raw head outputs in cache_o
     co = torch.empty((11 * n, ld), dtype=torch.float32, device=dev) if keep_cache or tc else None
     if tc:
-        img = decoder_image(dec_abi, n)
+        if img is None:
+            img = decoder_image(dec_abi, n)
         call("vsx_decode_fwd_tc", dec_abi, ptr(img), ptr(active), na, ptr(centers), ptr(emb),
              ptr(log_scales), ptr(offsets), view.to_abi(), lod_ref, max_scale, ptr(means),
              ptr(opac), ptr(col), ptr(scl), ptr(quat), ptr(nrm), ptr(ch), ptr(co), ptr(status),

@@ -506,6 +506,9 @@ class CudaShardBackend:
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.work.clear()
         self.gaussians = 0
+        # decoder weight image of this step's weights, shared by every view
+        self._dimg = (self.D.decoder_image(st.params.abi(), st.n)
+                      if self.D.use_tensor_cores(st.n) else None)
         self.isects = 0
 
     def grad_like(self) -> torch.Tensor:
@@ -518,7 +521,8 @@ class CudaShardBackend:
         active = D.select(mask & self.owned)
         an = st.anchors
         dec = D.decode(st.params.abi(), st.n, active, ds.centers, an.emb, an.log_scales,
-                       an.offsets, view, ds.lod_ref, ds.max_scale, self.status, keep_cache=True)
+                       an.offsets, view, ds.lod_ref, ds.max_scale, self.status, keep_cache=True,
+                       img=self._dimg)
         self.gaussians += dec.count
         P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, view,
                       self.status)
@@ -555,7 +559,7 @@ class CudaShardBackend:
             active = idx[:c]
             dec = D.decode(st.params.abi(), st.n, active, ds.centers, an.emb, an.log_scales,
                            an.offsets, views[v], ds.lod_ref, ds.max_scale, self.status,
-                           keep_cache=True)
+                           keep_cache=True, img=self._dimg)
             self.gaussians += dec.count
             launched.append((active, dec, D.project_launch(
                 dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, views[v],

@@ -568,6 +568,8 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     # allocator never recycles a side-stream block the main stream still reads.
     fs = _front_stream() if _pipeline_enabled() else main
     ts = _tail_stream() if _pipeline_enabled() else main
+    # the decoder weight image (3xTF32 fragments) once per step, not per view
+    dimg = D.decoder_image(params.abi(), params.n) if D.use_tensor_cores(params.n) else None
     fs.wait_stream(main)
     ts.wait_stream(main)
     hold = []
@@ -582,7 +584,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             with _span(timer, "decode_fwd"):
                 dec = D.decode(params.abi(), params.n, active, ds.centers, anchors.emb,
                                anchors.log_scales, anchors.offsets, view, ds.lod_ref,
-                               ds.max_scale, status, keep_cache=True)
+                               ds.max_scale, status, keep_cache=True, img=dimg)
             with _span(timer, "project_sort"):
                 P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal,
                               view, status)
