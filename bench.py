@@ -77,6 +77,9 @@ def parse(argv=None):
                     help="skip the same-config cfg1 side measurement")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU sharded step even at one rank (testing)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="TrainConfig.deterministic: fixed-order gradient / loss sums (a side "
+                         "measurement of the mode's cost; the headline runs the default)")
     ap.add_argument("--cpu-tiles", type=int, default=40,
                     help="tiles composited per reference sample in the cpu_baseline leg")
     ap.add_argument("--ref-tiles", type=int, default=40,
@@ -138,6 +141,8 @@ def config_of(args, world: int, desc: dict) -> dict:
     desc["parallelism"] = (f"anchor-sharded x{world} (Eq.3 i mod M), views rendered round-robin, "
                            "C1 all-to-all + C2 decoder all-reduce (NCCL)") if world > 1 else "single"
     desc["scaling"] = CITY.get(args.config, (0, 0, 0, 0, 0, "weak"))[5]
+    if getattr(args, "deterministic", False):
+        desc["sums"] = "fixed-order (TrainConfig.deterministic)"
     return desc
 
 
@@ -484,7 +489,7 @@ def run_vsx(args):
     cfg2 = args.config != "cfg1"      # the city configs share cfg2's objective
     cfg = TrainConfig(total_steps=30000, batch_size=len(views), step2_start=0 if cfg2 else 30000,
                       step3_start=30000, growth_stop=0, normal_weight=0.5 if cfg2 else 0.0,
-                      workers=world)
+                      workers=world, deterministic=bool(getattr(args, "deterministic", False)))
     if cfg2:
         tgt = teacher_targets(scene, views)
         imgs = [t["rgb"] for t in tgt]

@@ -15,10 +15,15 @@
  *   vsx_project_fwd                renderer.py:144-204 project_splats (EWA + (z,gid) order)
  *   vsx_sort_splats_z              renderer.py:197 np.lexsort((gid, z)) (float32 proxy radix
  *                                  sort + exact run fix-up); vsx_sort_pairs_u64/_u32 generic
- *   vsx_bin_count / vsx_bin_emit(_hist) / vsx_tile_ranges
- *                                  renderer.py:207-226 bin_splats
+ *   vsx_bin_plan / vsx_bin_build   renderer.py:207-226 bin_splats (row-column counting sorts;
+ *                                  vsx_bin_count / vsx_bin_emit(_hist) / vsx_tile_ranges +
+ *                                  vsx_sort_pairs_u32 for images over 4096 px a side)
  *   vsx_raster_fwd(_loss)          renderer.py:242-301 _blend_padded + _finalize, :390-449 rasterize_view
  *   vsx_raster_bwd(_loss)          renderer.py:347-367 rasterize_backward (autograd of the blend)
+ *   vsx_reduce_partials / vsx_raster_grad_reduce
+ *                                  deterministic mode: fixed-order loss sums and per-splat
+ *                                  gradient sums (the reference's sums are order-fixed,
+ *                                  trainer.py:9-13)
  *   vsx_project_bwd(_batch)        autograd of project_splats (trainer.py:330)
  *   vsx_decode_bwd                 decoder.py:267-292 decoder_backward (autograd of decode)
  *   vsx_l1_loss / vsx_depth_loss   losses.py:43-53 bl_rgb_loss, losses.py:65-84 e_depth_loss
@@ -287,6 +292,16 @@ typedef struct vsx_loss_desc {
    * tile_order[i] (a permutation of the tiles, e.g. longest list first so the
    * heavy tiles do not form the kernel's tail); NULL = row-major. */
   const uint32_t *tile_order;
+  /* optional deterministic mode (bitwise run-to-run reproducible sums):
+   * sum_partials (3 doubles per (tile, forward warp): T * 4 * 3) takes the
+   * forward's loss sums instead of float atomics, reduced in order by
+   * vsx_reduce_partials; isect_grad (13 floats per intersection) and
+   * tile_live (one u32 per tile) take the backward's per-(splat, tile)
+   * gradient sums instead of float atomics into grad_splat, reduced per
+   * splat in row-major tile order by vsx_raster_grad_reduce. NULL = atomics. */
+  double *sum_partials;
+  float *isect_grad;
+  uint32_t *tile_live;
 } vsx_loss_desc;
 
 int vsx_raster_fwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,
@@ -298,6 +313,18 @@ int vsx_raster_bwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,
                         const float *alpha, const float *depth, const float *normal,
                         const float *raw_normal, const float *t_final, const int32_t *n_contrib,
                         vsx_loss_desc loss, float *grad_splat, vsx_stream s);
+
+/* Deterministic-mode reductions. vsx_reduce_partials: sums[k] += the
+ * fixed-order sum over `slots` of partials[3 * slot + k], k < 3.
+ * vsx_raster_grad_reduce: per sorted splat r (n of them, radius the binning
+ * radius), grad_splat[13 r + f] += the sum over the tiles of its rectangle in
+ * row-major order of isect_grad[13 * pos + f], pos = r's position in the
+ * tile's list, for the positions the backward visited (< tile_live). */
+int vsx_reduce_partials(const double *partials, int64_t slots, double *sums, vsx_stream s);
+int vsx_raster_grad_reduce(const vsx_splat *rec, const double *radius, int32_t n, int32_t width,
+                           int32_t height, const uint32_t *tile_offsets,
+                           const uint32_t *tile_list, const uint32_t *tile_live,
+                           const float *isect_grad, float *grad_splat, vsx_stream s);
 
 /* ---- K6: compositing backward ------------------------------------------ */
 /* Pixel cotangents (any may be NULL = zero) -> per-splat gradients

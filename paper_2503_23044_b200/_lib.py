@@ -45,7 +45,8 @@ class VsxLossDesc(ctypes.Structure):
                 ("depth_weight", c_f32), ("normal_weight", c_f32), ("sums", c_void_p),
                 ("counts", c_void_p), ("extra_rgb", c_void_p), ("extra_normal", c_void_p),
                 ("extra_depth", c_void_p), ("live_pairs", c_void_p),
-                ("tile_order", c_void_p)]
+                ("tile_order", c_void_p), ("sum_partials", c_void_p), ("isect_grad", c_void_p),
+                ("tile_live", c_void_p)]
 
 
 class VsxNccGeom(ctypes.Structure):
@@ -115,6 +116,8 @@ _SIGS = {
     "vsx_tsdf_integrate": ([P, P, P, P, c_f64, c_f64, P, P, VsxCamera, P, P], c_i32),
     "vsx_bin_emit_tiles": ([P, P, c_i32, c_i32, c_i32, P, P, P, P], c_i32),
     "vsx_tile_segsort": ([P, c_i32, P, c_i32, P], c_i32),
+    "vsx_reduce_partials": ([P, c_i64, P, P], c_i32),
+    "vsx_raster_grad_reduce": ([P, P, c_i32, c_i32, c_i32, P, P, P, P, P, P], c_i32),
     "vsx_bin_plan_ws_bytes": ([c_i32, c_i32, c_i32], c_size),
     "vsx_bin_build_ws_bytes": ([c_i32, c_i32, c_i64], c_size),
     "vsx_bin_plan": ([P, P, c_i32, c_i32, c_i32, P, c_size, P, P], c_i32),

@@ -1070,18 +1070,30 @@ __global__ void __launch_bounds__(256, 2) decoder_wgrad_mma_kernel(
   }
 }
 
-// blockIdx.y = slice of the CTA partials (kWmSlices slices, 8-way atomics)
+// Two fixed-order stages (no float atomics, so the weight gradients are
+// bitwise reproducible): blockIdx.y = slice of the CTA partials summed into
+// slice_sum, then one thread per element adds the kWmSlices slice sums in
+// order into the gradient (each element has exactly one thread).
 constexpr int kWmSlices = 8;
 
-__global__ void decoder_wgrad_reduce_kernel(const float *__restrict__ partial, int ctas, int n,
-                                            vsx_decoder_grads dW) {
+__global__ void decoder_wgrad_slices_kernel(const float *__restrict__ partial, int ctas,
+                                            float *__restrict__ slice_sum) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (tile, lane, e)
   if (idx >= kWmTiles * 128) return;
   const int per = (ctas + kWmSlices - 1) / kWmSlices;
   const int c0 = blockIdx.y * per, c1 = min(ctas, c0 + per);
-  if (c0 >= c1) return;
   float sum = 0.f;
   for (int c = c0; c < c1; ++c) sum += partial[(size_t)c * kWmTiles * 128 + idx];
+  slice_sum[(size_t)blockIdx.y * kWmTiles * 128 + idx] = sum;
+}
+
+__global__ void decoder_wgrad_reduce_kernel(const float *__restrict__ slice_sum, int n,
+                                            vsx_decoder_grads dW) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (tile, lane, e)
+  if (idx >= kWmTiles * 128) return;
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < kWmSlices; ++k) sum += slice_sum[(size_t)k * kWmTiles * 128 + idx];
   const int tile = idx >> 7, lane = (idx >> 2) & 31, e = idx & 3;
   const int g = lane >> 2, tq = lane & 3;
   const int row_in = g + 8 * (e >> 1), col_in = 2 * tq + (e & 1);
@@ -1094,14 +1106,14 @@ __global__ void decoder_wgrad_reduce_kernel(const float *__restrict__ partial, i
     const int owh = h == 0 ? n : (h == 1 ? 3 * n : 7 * n);
     if (jh >= owh) return;
     const int col = nt * 8 + col_in;
-    if (nt < 8) atomicAdd(dW.w2[h] + (size_t)col * owh + jh, sum);
-    else if (col == 64) atomicAdd(dW.b2[h] + jh, sum);
+    if (nt < 8) dW.w2[h][(size_t)col * owh + jh] += sum;
+    else if (col == 64) dW.b2[h][jh] += sum;
   } else {
     const int tt = tile - 72, mt = tt / 24, nt = tt % 24;
     const int i = mt * 16 + row_in, col = nt * 8 + col_in;
     const int h = col / 64, hh = col % 64;
-    if (i < kInDim) atomicAdd(dW.w1[h] + (size_t)i * 64 + hh, sum);
-    else if (i == kInDim) atomicAdd(dW.b1[h] + hh, sum);
+    if (i < kInDim) dW.w1[h][(size_t)i * 64 + hh] += sum;
+    else if (i == kInDim) dW.b1[h][hh] += sum;
   }
 }
 
@@ -1222,8 +1234,8 @@ extern "C" int vsx_decode_fwd(vsx_decoder W, const int32_t *active, int32_t n_ac
 extern "C" size_t vsx_decode_bwd_ws_bytes(int32_t n, int32_t n_active) {
   // xs [37][ld] + g_pre [192][ld] + g_o [11n][ld] + the mma weight image
   return sizeof(float) * cache_ld(n_active) * (size_t)(kInDim + 1 + 192 + 11 * n) +
-         sizeof(float) * dbw_image_floats(n) + sizeof(float) * (size_t)kWmMaxCtas * kWmTiles * 128 +
-         256;
+         sizeof(float) * dbw_image_floats(n) +
+         sizeof(float) * (size_t)(kWmMaxCtas + kWmSlices) * kWmTiles * 128 + 256;
 }
 
 extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t *active,
@@ -1305,8 +1317,11 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
     decoder_wgrad_mma_kernel<<<ctas, 256, smem, st>>>(g_o, cache_h, g_pre, xs, n_active, ld, n,
                                                        partial);
     VSX_LAUNCH_CHECK("decoder_wgrad_mma");
-    decoder_wgrad_reduce_kernel<<<dim3((kWmTiles * 128 + 255) / 256, kWmSlices), 256, 0, st>>>(
-        partial, ctas, n, dW);
+    float *slice_sum = partial + (size_t)kWmMaxCtas * kWmTiles * 128;
+    decoder_wgrad_slices_kernel<<<dim3((kWmTiles * 128 + 255) / 256, kWmSlices), 256, 0, st>>>(
+        partial, ctas, slice_sum);
+    VSX_LAUNCH_CHECK("decoder_wgrad_slices");
+    decoder_wgrad_reduce_kernel<<<(kWmTiles * 128 + 255) / 256, 256, 0, st>>>(slice_sum, n, dW);
     VSX_LAUNCH_CHECK("decoder_wgrad_reduce");
     return VSX_OK;
   }

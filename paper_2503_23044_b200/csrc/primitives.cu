@@ -177,7 +177,14 @@ constexpr int kOsTile = kOsBlock * kOsItems;  // 4096 keys, 512 per warp
 // Smaller tiles for small sorts (kOsItemsSmall, below kOsSmallN keys) are
 // kept as an A/B switch.
 constexpr int kOsItemsSmall = 4;
-constexpr int64_t kOsSmallN = 0;  // disabled: 1024-key tiles measured 21.2 us per pass at 0.6 M keys, 4096-key 15.5 (the look-back chain grows with the tile count)
+#ifndef VSX_OS_WIN
+#define VSX_OS_WIN 8
+#endif
+constexpr int kOsWin = VSX_OS_WIN;  // look-back window (predecessor tiles per step)
+#ifndef VSX_OS_SMALL_ON
+#define VSX_OS_SMALL_ON 0
+#endif
+constexpr int64_t kOsSmallN = VSX_OS_SMALL_ON ? ((int64_t)1 << 21) : 0;  // disabled: 1024-key tiles measured 21.2 us per pass at 0.6 M keys, 4096-key 15.5 (the look-back chain grows with the tile count)
 __host__ __device__ inline int os_items(int64_t n) { return n <= kOsSmallN ? kOsItemsSmall : kOsItems; }
 constexpr int kOsWarps = kOsBlock / 32;
 constexpr uint32_t kOsAgg = 1u << 30, kOsPre = 2u << 30, kOsMask = kOsAgg - 1u;
@@ -334,21 +341,21 @@ __global__ void __launch_bounds__(kOsBlock) os_pass_kernel(
   const uint32_t gstart = block_exclusive_scan(gh[t], tot);
   s_lstart[t] = lstart;
   // ---- decoupled look-back over earlier tiles (per digit)
-  // A window of 8 predecessors is read per step (independent loads in
+  // A window of kOsWin predecessors is read per step (independent loads in
   // flight), consumed nearest-first up to the first inclusive prefix or the
   // first tile that has not published yet (re-read next step).
   uint32_t excl = 0;
   if (bid > 0) {
     int64_t p = (int64_t)bid - 1;
     while (true) {
-      uint32_t w[8];
+      uint32_t w[kOsWin];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < kOsWin; ++j)
         w[j] = p - j >= 0 ? ld_relaxed_u32(status + (size_t)(p - j) * 256 + t) : kOsPre;
       int used = 0;
       bool done = false;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < kOsWin; ++j) {
         if (!done && used == j && w[j] != 0u) {
           excl += w[j] & kOsMask;
           ++used;

@@ -38,6 +38,7 @@ constexpr int kChunk = VSX_FWD_CHUNK;
 
 // Per-pixel finalize (renderer.py:282-301) + fused loss partial sums (K9),
 // shared by both forward kernels. Block-uniform in L.gt_rgb.
+template <bool kDet>
 __device__ __forceinline__ void fwd_epilogue(const vsx_camera &cam, bool inside, int px, int py,
                                              float acc, float c0, float c1, float c2, float n0,
                                              float n1, float n2, float dist, float T, int32_t nc,
@@ -110,15 +111,23 @@ __device__ __forceinline__ void fwd_epilogue(const vsx_camera &cam, bool inside,
     l_nrm = warp_sum_d(l_nrm);
     const unsigned bd = __ballot_sync(0xffffffffu, c_dep), bn = __ballot_sync(0xffffffffu, c_nrm);
     if ((threadIdx.x & 31) == 0) {
-      if (l_rgb != 0.0) atomicAdd(L.sums + 0, l_rgb);
-      if (bd) {
-        atomicAdd(L.sums + 1, l_dep);
-        atomicAdd(L.counts + 0, (uint32_t)__popc(bd));
+      if (kDet) {
+        // deterministic mode: one slot per (tile, warp), reduced in order by
+        // vsx_reduce_partials (the counts are integers: atomics are exact)
+        const size_t slot = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * (blockDim.x / 32) +
+                            (threadIdx.x >> 5);
+        // += : a thread finalizes PX pixels, one epilogue call each, in order
+        // (the buffer is zeroed by the caller)
+        L.sum_partials[3 * slot + 0] += l_rgb;
+        L.sum_partials[3 * slot + 1] += l_dep;
+        L.sum_partials[3 * slot + 2] += l_nrm;
+      } else {
+        if (l_rgb != 0.0) atomicAdd(L.sums + 0, l_rgb);
+        if (bd) atomicAdd(L.sums + 1, l_dep);
+        if (bn) atomicAdd(L.sums + 2, l_nrm);
       }
-      if (bn) {
-        atomicAdd(L.sums + 2, l_nrm);
-        atomicAdd(L.counts + 1, (uint32_t)__popc(bn));
-      }
+      if (bd) atomicAdd(L.counts + 0, (uint32_t)__popc(bd));
+      if (bn) atomicAdd(L.counts + 1, (uint32_t)__popc(bn));
     }
   }
 }
@@ -186,7 +195,9 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-template <int PX, int U>
+// kDet: deterministic mode (vsx_loss_desc.sum_partials), a separate
+// instantiation so the default kernel's code is unchanged.
+template <int PX, int U, bool kDet>
 __global__ void __launch_bounds__(256 / PX) raster_fwd2_kernel(
     const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
     const uint32_t *__restrict__ tile_list, vsx_camera cam, float *__restrict__ out_rgb,
@@ -285,7 +296,7 @@ __global__ void __launch_bounds__(256 / PX) raster_fwd2_kernel(
   }
 #pragma unroll
   for (int i = 0; i < PX; ++i)
-    fwd_epilogue(cam, in[i], px + i, py, A[i].acc, A[i].c0, A[i].c1, A[i].c2, A[i].n0, A[i].n1,
+    fwd_epilogue<kDet>(cam, in[i], px + i, py, A[i].acc, A[i].c0, A[i].c1, A[i].c2, A[i].n0, A[i].n1,
                  A[i].n2, A[i].dist, A[i].T, nc[i], out_rgb, out_alpha, out_depth, out_normal,
                  out_raw, out_valid, out_T, out_nc, L);
 }
@@ -376,7 +387,7 @@ __device__ __forceinline__ float pixel_moment(int p, int m) {
   }
 }
 
-template <int kBC>
+template <int kBC, bool kDet>
 __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     raster_bwd_tc_kernel(BwdArgs a, vsx_camera cam) {
   constexpr int kMT = kBC / 16;          // m-tiles per chunk
@@ -414,8 +425,26 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     const uint32_t key = 255u - (uint32_t)min(nc0 >> 3, 255);
     s_bin[t] = 0u;
     __syncthreads();
-    const uint32_t r = atomicAdd(&s_bin[key], 1u);  // order inside a bucket is free
-    __syncthreads();
+    uint32_t r;
+    if (kDet) {
+      // deterministic mode: pixels keep their index order inside a bucket
+      // (the slot order is the phase-2 summation order): warps in turn, lanes
+      // ranked among equal keys
+      r = 0;
+      for (int w = 0; w < 8; ++w) {
+        if (warp == w) {
+          const unsigned peers = __match_any_sync(0xffffffffu, key);
+          const uint32_t base = s_bin[key];
+          __syncwarp();
+          if ((peers >> lane) == 1u) s_bin[key] = base + __popc(peers);
+          r = base + __popc(peers & ((1u << lane) - 1u));
+        }
+        __syncthreads();
+      }
+    } else {
+      r = atomicAdd(&s_bin[key], 1u);  // order inside a bucket is free
+      __syncthreads();
+    }
     // exclusive scan of the 256 bucket counts
     uint32_t v = s_bin[t], inc = v;
 #pragma unroll
@@ -492,6 +521,7 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   }
   __syncthreads();
   const uint32_t stop = begin + (uint32_t)s_max;
+  if (a.L.tile_live && t == 0) a.L.tile_live[tile] = (uint32_t)s_max;  // rows written below stop
   float S = 0.f;  // sum over later live splats of s_i * w_i
   float *wpl = s_plane, *qpl = s_plane + kBC * kPlaneStride;
   // phase-2 role of this warp
@@ -733,10 +763,18 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
       const float m2 = __shfl_down_sync(0xffffffffu, v.x, 1), m3 = __shfl_down_sync(0xffffffffu, v.y, 1);
       const float m4 = __shfl_down_sync(0xffffffffu, v.x, 2), m5 = __shfl_down_sync(0xffffffffu, v.y, 2);
       if (j < cnt) {
-        float* gp = a.grad + (size_t)13 * s_rank[buf][j];
+        // deterministic mode (L.isect_grad): this (splat, tile)'s 13 sums go
+        // to the intersection's row, reduced per splat in tile order later
+        float *row = kDet ? a.L.isect_grad + (size_t)13 * (cs + j) : nullptr;
+        float *gp = a.grad + (size_t)13 * s_rank[buf][j];
         if (part < 4) {
-          if (v.x != 0.f) atomicAdd(gp + 6 + 2 * part, v.x);
-          if (part < 3 && v.y != 0.f) atomicAdd(gp + 7 + 2 * part, v.y);
+          if (row) {
+            row[6 + 2 * part] = v.x;
+            if (part < 3) row[7 + 2 * part] = v.y;
+          } else {
+            if (v.x != 0.f) atomicAdd(gp + 6 + 2 * part, v.x);
+            if (part < 3 && v.y != 0.f) atomicAdd(gp + 7 + 2 * part, v.y);
+          }
         } else if (part == 4) {
           const float4 p0 = s0[buf][j], p1 = s1[buf][j];
           const float op = p1.y, A = p1.w, B = s2[buf][j].w, C = s3[buf][j].w;
@@ -746,14 +784,13 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
           const float sxx = XX - 2.f * mx * X + mx * mx * Q1;
           const float sxy = XY - mx * Y - my * X + mx * my * Q1;
           const float syy = YY - 2.f * my * Y + my * my * Q1;
-          const float g0 = op * (A * sx + B * sy), g1 = op * (B * sx + C * sy);
-          const float g2 = -0.5f * op * sxx, g3 = -op * sxy, g4 = -0.5f * op * syy;
-          if (g0 != 0.f) atomicAdd(gp + 0, g0);
-          if (g1 != 0.f) atomicAdd(gp + 1, g1);
-          if (g2 != 0.f) atomicAdd(gp + 2, g2);
-          if (g3 != 0.f) atomicAdd(gp + 3, g3);
-          if (g4 != 0.f) atomicAdd(gp + 4, g4);
-          if (Q1 != 0.f) atomicAdd(gp + 5, Q1);
+          const float g[6] = {op * (A * sx + B * sy), op * (B * sx + C * sy), -0.5f * op * sxx,
+                              -op * sxy, -0.5f * op * syy, Q1};
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            if (row) row[k] = g[k];
+            else if (g[k] != 0.f) atomicAdd(gp + k, g[k]);
+          }
         }
       }
     }
@@ -780,8 +817,14 @@ static int launch_bwd(const BwdArgs &a, const vsx_camera &cam, cudaStream_t st) 
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
   const int smem = (int)(sizeof(float) * 2 * kBC * kPlaneStride);
   static std::atomic<uint64_t> done{0};
-  if (int rc = smem_opt_in(raster_bwd_tc_kernel<kBC>, smem, done)) return rc;
-  raster_bwd_tc_kernel<kBC><<<grid, 256, smem, st>>>(a, cam);
+  if (a.L.isect_grad) {  // deterministic mode (separate instantiation)
+    static std::atomic<uint64_t> done_det{0};
+    if (int rc = smem_opt_in(raster_bwd_tc_kernel<kBC, true>, smem, done_det)) return rc;
+    raster_bwd_tc_kernel<kBC, true><<<grid, 256, smem, st>>>(a, cam);
+  } else {
+    if (int rc = smem_opt_in(raster_bwd_tc_kernel<kBC, false>, smem, done)) return rc;
+    raster_bwd_tc_kernel<kBC, false><<<grid, 256, smem, st>>>(a, cam);
+  }
   VSX_LAUNCH_CHECK("raster_bwd");
   return VSX_OK;
 }
@@ -795,9 +838,14 @@ static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
   dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
   // two horizontally adjacent pixels per thread, alpha batches of 4 splats
   // (the measured optimum: DESIGN.md §3, scripts/ab_fwd.py)
-  raster_fwd2_kernel<2, 4><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb, alpha,
-                                                 depth, normal, raw_normal, valid, t_final,
-                                                 n_contrib, L);
+  if (L.sum_partials)  // deterministic mode (L.gt_rgb set: the fused objective)
+    raster_fwd2_kernel<2, 4, true><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb,
+                                                         alpha, depth, normal, raw_normal, valid,
+                                                         t_final, n_contrib, L);
+  else
+    raster_fwd2_kernel<2, 4, false><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb,
+                                                          alpha, depth, normal, raw_normal, valid,
+                                                          t_final, n_contrib, L);
   VSX_LAUNCH_CHECK("raster_fwd");
   return VSX_OK;
 }
@@ -853,4 +901,104 @@ extern "C" int vsx_raster_bwd_loss(const vsx_splat *rec, const uint32_t *tile_of
   BwdArgs a{rec, tile_offsets, tile_list, alpha, depth, raw_normal, t_final, nullptr, nullptr,
             nullptr, nullptr, nullptr, n_contrib, grad_splat, rgb, normal, loss};
   return launch_bwd(a, cam, as_stream(s));
+}
+
+// ------------------------------------------------------ deterministic mode
+//
+// With vsx_loss_desc.isect_grad / tile_live / sum_partials set, the compositor
+// kernels write their per-(splat, tile) gradient sums and per-warp loss sums
+// to fixed slots instead of adding them with float atomics; these kernels
+// reduce the slots in a fixed order, so a step is bitwise reproducible (the
+// reference's sums are order-fixed by construction, trainer.py:9-13).
+
+namespace vsx {
+
+// One thread per sorted splat: its tiles in row-major order over the
+// rectangle (renderer.py:216-221), its position in each tile's ascending list
+// by binary search, the row counted when the backward visited it.
+__global__ void raster_grad_reduce_kernel(const vsx_splat *__restrict__ rec,
+                                          const double *__restrict__ radius, int32_t n, int txn,
+                                          int tyn, const uint32_t *__restrict__ toff,
+                                          const uint32_t *__restrict__ tl,
+                                          const uint32_t *__restrict__ tile_live,
+                                          const float *__restrict__ isect,
+                                          float *__restrict__ grad) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int x0, x1, y0, y1;
+  if (!tile_rect(rec[r].mean2d[0], rec[r].mean2d[1], radius[r], txn, tyn, x0, x1, y0, y1)) return;
+  float acc[13];
+#pragma unroll
+  for (int f = 0; f < 13; ++f) acc[f] = 0.f;
+  for (int y = y0; y <= y1; ++y)
+    for (int x = x0; x <= x1; ++x) {
+      const int t = y * txn + x;
+      const uint32_t b = toff[t];
+      uint32_t lo = b, hi = toff[t + 1];
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (tl[mid] < (uint32_t)r) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo - b < tile_live[t]) {
+        const float *row = isect + (size_t)13 * lo;
+#pragma unroll
+        for (int f = 0; f < 13; ++f) acc[f] += row[f];
+      }
+    }
+  float *g = grad + (size_t)13 * r;
+#pragma unroll
+  for (int f = 0; f < 13; ++f) g[f] += acc[f];
+}
+
+// One CTA: thread t sums slots t, t + 1024, ... in order, then a fixed tree.
+__global__ void __launch_bounds__(1024) reduce_partials_kernel(const double *__restrict__ part,
+                                                               int64_t slots,
+                                                               double *__restrict__ sums) {
+  __shared__ double s[3][1024];
+  const int t = threadIdx.x;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int64_t i = t; i < slots; i += 1024) {
+    a0 += part[3 * i + 0];
+    a1 += part[3 * i + 1];
+    a2 += part[3 * i + 2];
+  }
+  s[0][t] = a0;
+  s[1][t] = a1;
+  s[2][t] = a2;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if (t < w) {
+      s[0][t] += s[0][t + w];
+      s[1][t] += s[1][t + w];
+      s[2][t] += s[2][t + w];
+    }
+    __syncthreads();
+  }
+  if (t < 3) sums[t] += s[t][0];
+}
+
+}  // namespace vsx
+
+extern "C" int vsx_reduce_partials(const double *partials, int64_t slots, double *sums,
+                                   vsx_stream s) {
+  VSX_REQUIRE(slots >= 0 && sums && (partials || slots == 0), "reduce_partials: bad args");
+  reduce_partials_kernel<<<1, 1024, 0, as_stream(s)>>>(partials, slots, sums);
+  VSX_LAUNCH_CHECK("reduce_partials");
+  return VSX_OK;
+}
+
+extern "C" int vsx_raster_grad_reduce(const vsx_splat *rec, const double *radius, int32_t n,
+                                      int32_t width, int32_t height, const uint32_t *tile_offsets,
+                                      const uint32_t *tile_list, const uint32_t *tile_live,
+                                      const float *isect_grad, float *grad_splat, vsx_stream s) {
+  VSX_REQUIRE(n >= 0 && width > 0 && height > 0, "raster_grad_reduce: bad args");
+  if (n == 0) return VSX_OK;
+  VSX_REQUIRE(rec && radius && tile_offsets && tile_list && tile_live && isect_grad && grad_splat,
+              "raster_grad_reduce: null buffer");
+  const int txn = (width + kTile - 1) / kTile, tyn = (height + kTile - 1) / kTile;
+  raster_grad_reduce_kernel<<<grid_for(n, 128), 128, 0, as_stream(s)>>>(
+      rec, radius, n, txn, tyn, tile_offsets, tile_list, tile_live, isect_grad, grad_splat);
+  VSX_LAUNCH_CHECK("raster_grad_reduce");
+  return VSX_OK;
 }

@@ -24,6 +24,7 @@ EMBED_DIM = 32
 HIDDEN = 64
 REC_F32 = 16            # sizeof(vsx_splat) / 4
 GRAD_F32 = 13           # per-splat gradient record
+FWD_WARPS = 4           # warps per CTA of the compositor forward (raster_fwd2_kernel<2, 4>)
 STATUS_NONPD = 1
 STATUS_NONFINITE = 2
 
@@ -465,8 +466,11 @@ class Raster:
     n_contrib: torch.Tensor
 
 
-def raster_forward(P: Projected, B: Bins, view: CameraView, loss=None) -> Raster:
-    """K5; with a VsxLossDesc the fused objective's sums/counts are accumulated too."""
+def raster_forward(P: Projected, B: Bins, view: CameraView, loss=None,
+                   deterministic: bool = False) -> Raster:
+    """K5; with a VsxLossDesc the fused objective's sums/counts are accumulated
+    too (deterministic: per-(tile, warp) partial sums reduced in a fixed order
+    instead of float atomics)."""
     H, W = view.height, view.width
     dev = "cuda"
     rgb = torch.empty((H, W, 3), dtype=torch.float32, device=dev)
@@ -482,9 +486,18 @@ def raster_forward(P: Projected, B: Bins, view: CameraView, loss=None) -> Raster
              ptr(rgb), ptr(alpha), ptr(depth), ptr(normal), ptr(raw), ptr(valid), ptr(tfin),
              ptr(nc), stream())
     else:
+        part = None
+        if deterministic:
+            slots = B.tiles_x * B.tiles_y * FWD_WARPS
+            part = torch.zeros((slots, 3), dtype=torch.float64, device=dev)
+            loss.sum_partials = part.data_ptr()
         call("vsx_raster_fwd_loss", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list),
              view.to_abi(), ptr(rgb), ptr(alpha), ptr(depth), ptr(normal), ptr(raw), ptr(valid),
              ptr(tfin), ptr(nc), loss, stream())
+        if part is not None:
+            loss.sum_partials = None
+            call("vsx_reduce_partials", ptr(part), int(part.shape[0]), ctypes.c_void_p(loss.sums),
+                 stream())
     return Raster(rgb, alpha, depth, normal, raw, valid, tfin, nc)
 
 
@@ -495,8 +508,10 @@ def _tile_order_enabled() -> bool:
 
 def raster_backward(P: Projected, B: Bins, view: CameraView, R: Raster, g_rgb=None, g_alpha=None,
                     g_depth=None, g_normal=None, g_raw=None, out: torch.Tensor | None = None,
-                    loss=None):
-    """K6 from explicit pixel cotangents, or (loss=VsxLossDesc) from the fused objective."""
+                    loss=None, deterministic: bool = False):
+    """K6 from explicit pixel cotangents, or (loss=VsxLossDesc) from the fused
+    objective (deterministic: per-intersection gradient rows reduced per
+    splat in tile order instead of float atomics)."""
     grad = out if out is not None else torch.zeros((max(P.count, 1), GRAD_F32),
                                                    dtype=torch.float32, device="cuda")
     if loss is not None:
@@ -507,9 +522,19 @@ def raster_backward(P: Projected, B: Bins, view: CameraView, R: Raster, g_rgb=No
             lens = B.tile_offsets[1:] - B.tile_offsets[:-1]
             order = torch.argsort(lens, descending=True).to(torch.int32)
             loss.tile_order = order.data_ptr()
+        rows = live = None
+        if deterministic and B.intersections:
+            rows = torch.empty((B.intersections, GRAD_F32), dtype=torch.float32, device="cuda")
+            live = torch.empty(B.tiles_x * B.tiles_y, dtype=torch.int32, device="cuda")
+            loss.isect_grad, loss.tile_live = rows.data_ptr(), live.data_ptr()
         call("vsx_raster_bwd_loss", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list),
              view.to_abi(), ptr(R.rgb), ptr(R.alpha), ptr(R.depth), ptr(R.normal),
              ptr(R.raw_normal), ptr(R.t_final), ptr(R.n_contrib), loss, ptr(grad), stream())
+        if rows is not None:
+            loss.isect_grad = loss.tile_live = None
+            call("vsx_raster_grad_reduce", ptr(P.rec), ptr(P.radius), P.count, view.width,
+                 view.height, ptr(B.tile_offsets), ptr(B.tile_list), ptr(live), ptr(rows),
+                 ptr(grad), stream())
         return grad[: P.count]
     call("vsx_raster_bwd", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list), view.to_abi(),
          ptr(R.rgb), ptr(R.alpha), ptr(R.depth), ptr(R.raw_normal), ptr(R.t_final),

@@ -252,7 +252,7 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
         back = return_grads(plan, grads, backend.grad_like(), group)
         for v in range(B):
             backend.backward_shard(v, views[v], back[v])
-    dist.all_reduce(backend.decoder_grad(), op=dist.ReduceOp.SUM, group=group)
+    _c2_sum(backend.decoder_grad(), group, ordered=bool(getattr(backend, "deterministic", False)))
     losses = backend.loss_terms()              # (B, 5): rgb, depth, normal sums; counts
     dist.all_reduce(losses, op=dist.ReduceOp.SUM, group=group)
     report = backend.finish_step(losses)
@@ -272,6 +272,22 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
     if scheduler is not None:
         scheduler.update(views, secs)
     return report
+
+
+def _c2_sum(t: torch.Tensor, group, ordered: bool) -> None:
+    """C2: the decoder gradient summed over the ranks, in place. ``ordered``
+    (deterministic mode): an all-gather and a sum in rank
+    order, so the result does not depend on the collective's reduction
+    order; otherwise one all-reduce SUM."""
+    if not ordered:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, t.contiguous(), group=group)
+    acc = parts[0].clone()
+    for p in parts[1:]:
+        acc += p
+    t.copy_(acc)
 
 
 def _shard_groups() -> int:
@@ -511,6 +527,10 @@ class CudaShardBackend:
                       if self.D.use_tensor_cores(st.n) else None)
         self.isects = 0
 
+    @property
+    def deterministic(self) -> bool:
+        return bool(getattr(self.state.cfg, "deterministic", False))
+
     def grad_like(self) -> torch.Tensor:
         return torch.zeros((0, self.D.GRAD_F32), dtype=torch.float32, device="cuda")
 
@@ -604,9 +624,10 @@ class CudaShardBackend:
         from .trainer import _span
         self.isects += Bn.intersections
         with _span(self.timer, "raster_fwd"):
-            R = D.raster_forward(P, Bn, view, loss=loss)
+            det = bool(getattr(st.cfg, "deterministic", False))
+            R = D.raster_forward(P, Bn, view, loss=loss, deterministic=det)
         with _span(self.timer, "raster_bwd"):
-            gs = D.raster_backward(P, Bn, view, R, loss=loss)
+            gs = D.raster_backward(P, Bn, view, R, loss=loss, deterministic=det)
         merged = torch.empty_like(gs)
         merged[order] = gs
         return merged

@@ -64,6 +64,12 @@ class TrainConfig:
     init_scale_fraction: float = 0.125
     # extension: weight of the normal-prior L1 (0 = reference objective)
     normal_weight: float = 0.0
+    # bitwise run-to-run reproducible sums: the compositor's per-splat
+    # gradients and the loss sums are reduced in a fixed order instead of by
+    # float atomics (vsx_raster_grad_reduce / vsx_reduce_partials), and the
+    # sharded step's decoder all-reduce becomes an all-gather + ordered sum.
+    # The Eq. 10 NCC term keeps its atomics.
+    deterministic: bool = False
     log_every: int = 10
     eval_every: int = 0
     checkpoint_every: int = 0
@@ -626,7 +632,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     def backward(vi, active, dec, P, Bn, R, loss):
         view = views[vi]
         with _span(timer, "raster_bwd"):
-            gs = D.raster_backward(P, Bn, view, R, loss=loss)
+            gs = D.raster_backward(P, Bn, view, R, loss=loss, deterministic=cfg.deterministic)
         if book is not None:
             book.view_end(vi)
         # projection + decoder backward of this view run on the tail stream,
@@ -662,7 +668,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             loss = loss_desc(vi)
             _tr(f"raster{vi}")
             with _span(timer, "raster_fwd"):
-                R = D.raster_forward(P, Bn, views[vi], loss=loss)
+                R = D.raster_forward(P, Bn, views[vi], loss=loss, deterministic=cfg.deterministic)
             backward(vi, active, dec, P, Bn, R, loss)
             _tr(f"bwd{vi}_queued")
             # the next view's front end is issued after this view's back end
@@ -679,7 +685,7 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             active, dec, P, Bn = take_front(vi)
             loss = loss_desc(vi)
             with _span(timer, "raster_fwd"):
-                R = D.raster_forward(P, Bn, views[vi], loss=loss)
+                R = D.raster_forward(P, Bn, views[vi], loss=loss, deterministic=cfg.deterministic)
             fwd.append((active, dec, P, Bn, R))
             if vi + 1 < B:
                 front(vi + 1)

@@ -73,6 +73,38 @@ def test_exchange_round_trip_two_ranks():
             assert torch.load(os.path.join(out, f"r{r}.pt"))["ok"]
 
 
+def _c2_worker(rank, world, port, out):
+    from paper_2503_23044_b200.dist import _c2_sum
+    _init(rank, world, port)
+    # values whose float32 sum depends on the order
+    base = torch.tensor([1e8, 1.0, -1e8, 3.25, 1e-3], dtype=torch.float32)
+    mine = base * (rank + 1) + torch.tensor([0.5, -0.75, 0.125, 2.0, 1e-4]) * rank
+    ordered = mine.clone()
+    _c2_sum(ordered, None, ordered=True)
+    reduced = mine.clone()
+    _c2_sum(reduced, None, ordered=False)
+    torch.save({"ordered": ordered, "reduced": reduced, "mine": mine},
+               os.path.join(out, f"r{rank}.pt"))
+    dist.destroy_process_group()
+
+
+def test_ordered_c2_is_the_rank_order_sum():
+    """Deterministic mode's C2: every rank gets the sum accumulated in rank
+    order (((g0 + g1) + g2) in float32), whatever the collective's own
+    reduction order; the plain all-reduce agrees up to rounding."""
+    port = _free_port()
+    world = 3
+    with tempfile.TemporaryDirectory() as out:
+        mp.spawn(_c2_worker, args=(world, port, out), nprocs=world, join=True)
+        res = [torch.load(os.path.join(out, f"r{r}.pt")) for r in range(world)]
+    expect = res[0]["mine"].clone()
+    for r in range(1, world):
+        expect += res[r]["mine"]
+    for r in range(world):
+        assert torch.equal(res[r]["ordered"], expect)
+        assert torch.allclose(res[r]["reduced"], expect, rtol=1e-6, atol=1e-2)
+
+
 def _small_state(d):
     import oracle
     K = int(d["lod_count"])
