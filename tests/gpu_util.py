@@ -64,6 +64,17 @@ def rel_close(a, b, rel, floor) -> tuple[bool, float, int]:
     return (not bad.any()), worst, int(bad.sum())
 
 
+def adam_worst_bound(lr: float, steps: int) -> float:
+    """Largest gap two Adam trajectories (beta1 0.9, beta2 0.999, same start)
+    can open in ``steps`` steps: each bias-corrected step moves a parameter
+    by at most ~1.5 lr (exactly lr at step 1; |m_hat / sqrt(v_hat)| stays
+    below 1.5 for these betas), so 2 x 1.5 lr per step. Post-step parameter
+    tests bound their worst element by this, on top of the element-wise check:
+    an element whose gradient sits at the float32 noise floor may take an
+    Adam step of the other sign, but never more than this."""
+    return 3.0 * lr * steps
+
+
 def noise_floor_close(got, ref, rel, noise) -> tuple[bool, float, int]:
     """Relative closeness with a noise-floor exclusion instead of an allowance.
 
