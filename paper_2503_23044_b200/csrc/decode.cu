@@ -555,6 +555,13 @@ __device__ __forceinline__ void split_trunc(float v, uint32_t &hi, uint32_t &lo)
   lo = __float_as_uint(v - __uint_as_float(hi));
 }
 
+// 16-byte global -> shared copy, zero-filled beyond `bytes` (cp.async.cg)
+__device__ __forceinline__ void cp_async16(float *dst, const float *src, int bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes)
+               : "memory");
+}
+
 constexpr int kDbwWarps = 8;
 constexpr int kDbwGoStride = 24, kDbwHStride = 20;  // staged row strides (floats)
 
@@ -627,15 +634,23 @@ __global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kerne
       for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = c[q][2] = c[q][3] = 0.f;
       __syncwarp();  // the previous head's tiles are consumed
       {
-        const int col = lane & 15, rr = lane >> 4;
-        const bool okc = r0 + col < n_active;
-#pragma unroll 8
-        for (int row = rr; row < 8 * nks; row += 2)
-          s_go[row * kDbwGoStride + col] =
-              (okc && row < ow) ? g_o[(size_t)(oo + row) * ld + r0 + col] : 0.f;
-#pragma unroll 8
-        for (int k = rr; k < 64; k += 2)
-          s_h[k * kDbwHStride + col] = okc ? cache_h[(size_t)(h * 64 + k) * ld + r0 + col] : 0.f;
+        // every 16-byte piece of the head's g_o rows and hidden rows in flight
+        // at once (cp.async, zero-filled past the last anchor / row): one
+        // memory latency per head instead of one per unrolled load batch
+        const int valid = min(16, n_active - r0);
+        for (int c = lane; c < 8 * nks * 4; c += 32) {
+          const int row = c >> 2, q = c & 3;
+          const int bytes = row < ow ? 4 * max(0, min(4, valid - 4 * q)) : 0;
+          cp_async16(s_go + row * kDbwGoStride + 4 * q,
+                     g_o + (size_t)(oo + min(row, ow - 1)) * ld + r0 + 4 * q, bytes);
+        }
+        for (int c = lane; c < 64 * 4; c += 32) {
+          const int k = c >> 2, q = c & 3;
+          cp_async16(s_h + k * kDbwHStride + 4 * q,
+                     cache_h + (size_t)(h * 64 + k) * ld + r0 + 4 * q,
+                     4 * max(0, min(4, valid - 4 * q)));
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
       }
       __syncwarp();
       for (int ks = 0; ks < nks; ++ks, ++ksg) {
