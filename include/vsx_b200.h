@@ -302,6 +302,13 @@ typedef struct vsx_loss_desc {
   double *sum_partials;
   float *isect_grad;
   uint32_t *tile_live;
+  /* optional band (the sharded step's split of a view over ranks when the
+   * batch has fewer views than ranks): composite only tile rows
+   * [tile_row0, tile_row0 + tile_rows); tile_rows = 0 = all rows. Outputs
+   * outside the band are not written; the loss counts and sums cover the
+   * band only. Not combined with tile_order. */
+  int32_t tile_row0;
+  int32_t tile_rows;
 } vsx_loss_desc;
 
 int vsx_raster_fwd_loss(const vsx_splat *rec, const uint32_t *tile_offsets,

@@ -46,7 +46,7 @@ class VsxLossDesc(ctypes.Structure):
                 ("counts", c_void_p), ("extra_rgb", c_void_p), ("extra_normal", c_void_p),
                 ("extra_depth", c_void_p), ("live_pairs", c_void_p),
                 ("tile_order", c_void_p), ("sum_partials", c_void_p), ("isect_grad", c_void_p),
-                ("tile_live", c_void_p)]
+                ("tile_live", c_void_p), ("tile_row0", c_i32), ("tile_rows", c_i32)]
 
 
 class VsxNccGeom(ctypes.Structure):

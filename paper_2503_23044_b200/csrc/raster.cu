@@ -207,10 +207,11 @@ __global__ void __launch_bounds__(256 / PX) raster_fwd2_kernel(
   constexpr int kThreads = 256 / PX, kRowThreads = kTile / PX;
   __shared__ float4 s0[kChunk], s1[kChunk], s2[kChunk], s3[kChunk];
   const int txn = gridDim.x;
-  const int tile = blockIdx.y * txn + blockIdx.x;
+  const int by = (int)blockIdx.y + L.tile_row0;  // tile row (a band: rows from tile_row0)
+  const int tile = by * txn + blockIdx.x;
   const int lx = PX * (threadIdx.x % kRowThreads), ly = threadIdx.x / kRowThreads;
-  const int px = blockIdx.x * kTile + lx, py = blockIdx.y * kTile + ly;
-  const double ox = (double)(blockIdx.x * kTile), oy = (double)(blockIdx.y * kTile);
+  const int px = blockIdx.x * kTile + lx, py = by * kTile + ly;
+  const double ox = (double)(blockIdx.x * kTile), oy = (double)(by * kTile);
   const uint32_t begin = tile_off[tile], end = tile_off[tile + 1];
   const float fy = (float)ly;
   float fx[PX];
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   extern __shared__ float s_plane[];  // w plane [kBC][kPlaneStride], then q plane
   const int txn = gridDim.x;
   // optional heaviest-first schedule: CTA i takes tile_order[i]
-  const int lin = blockIdx.y * txn + blockIdx.x;
+  const int lin = ((int)blockIdx.y + a.L.tile_row0) * txn + blockIdx.x;  // tile_row0: a band
   const int tile = a.L.tile_order ? (int)a.L.tile_order[lin] : lin;
   const int bx = tile % txn, by = tile / txn;
   const int t = threadIdx.x;
@@ -812,9 +813,23 @@ static int smem_opt_in(K kernel, int bytes, std::atomic<uint64_t> &done) {
   return VSX_OK;
 }
 
+// The tile rows a launch composites: all, or the band [tile_row0, tile_row0 +
+// tile_rows) of vsx_loss_desc (a renderer rank's share of a view).
+static int band_rows(const vsx_loss_desc &L, const vsx_camera &cam, int &rows) {
+  const int tyn = (cam.height + kTile - 1) / kTile;
+  rows = L.tile_rows > 0 ? L.tile_rows : tyn;
+  VSX_REQUIRE(L.tile_row0 >= 0 && L.tile_row0 + rows <= tyn && (L.tile_rows == 0 || L.tile_rows > 0),
+              "raster: tile band [%d, %d) outside the %d tile rows", L.tile_row0,
+              L.tile_row0 + rows, tyn);
+  VSX_REQUIRE(L.tile_rows == 0 || L.tile_order == nullptr, "raster: tile_order with a band");
+  return VSX_OK;
+}
+
 static int launch_bwd(const BwdArgs &a, const vsx_camera &cam, cudaStream_t st) {
   constexpr int kBC = 16;
-  dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
+  int rows = 0;
+  if (int rc = band_rows(a.L, cam, rows)) return rc;
+  dim3 grid((cam.width + kTile - 1) / kTile, rows);
   const int smem = (int)(sizeof(float) * 2 * kBC * kPlaneStride);
   static std::atomic<uint64_t> done{0};
   if (a.L.isect_grad) {  // deterministic mode (separate instantiation)
@@ -835,7 +850,9 @@ static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
                       float *t_final, int32_t *n_contrib, const vsx_loss_desc &L,
                       cudaStream_t st) {
   VSX_REQUIRE(cam.width > 0 && cam.height > 0 && t_final && n_contrib, "raster_fwd: bad args");
-  dim3 grid((cam.width + kTile - 1) / kTile, (cam.height + kTile - 1) / kTile);
+  int rows = 0;
+  if (int rc = band_rows(L, cam, rows)) return rc;
+  dim3 grid((cam.width + kTile - 1) / kTile, rows);
   // two horizontally adjacent pixels per thread, alpha batches of 4 splats
   // (the measured optimum: DESIGN.md §3, scripts/ab_fwd.py)
   if (L.sum_partials)  // deterministic mode (L.gt_rgb set: the fused objective)

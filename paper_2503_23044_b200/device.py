@@ -525,7 +525,8 @@ def raster_backward(P: Projected, B: Bins, view: CameraView, R: Raster, g_rgb=No
         rows = live = None
         if deterministic and B.intersections:
             rows = torch.empty((B.intersections, GRAD_F32), dtype=torch.float32, device="cuda")
-            live = torch.empty(B.tiles_x * B.tiles_y, dtype=torch.int32, device="cuda")
+            # zeros: a band launch leaves the other tiles' live counts unset
+            live = torch.zeros(B.tiles_x * B.tiles_y, dtype=torch.int32, device="cuda")
             loss.isect_grad, loss.tile_live = rows.data_ptr(), live.data_ptr()
         call("vsx_raster_bwd_loss", ptr(P.rec), ptr(B.tile_offsets), ptr(B.tile_list),
              view.to_abi(), ptr(R.rgb), ptr(R.alpha), ptr(R.depth), ptr(R.normal),

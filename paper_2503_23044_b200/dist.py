@@ -223,9 +223,26 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
     have = [v for v in range(B) if w2 > 0 and priors is not None and priors[v] is not None]
     have_n = [v for v in range(B)
               if wn > 0 and normal_priors is not None and normal_priors[v] is not None]
-    renderers = scheduler.assign(views, world) if scheduler is not None else None
-    renderers = np.asarray(renderers if renderers is not None
-                           else [renderer_of(v, world) for v in range(B)], dtype=np.int64)
+    banded = B < world
+    if banded:
+        # fewer views than ranks: every view is split into tile-row bands, one
+        # work item each, dealt round-robin over the ranks (SURVEY §8(e) step
+        # 2: "tile bands of a view when B < M"; the reference's patch work
+        # items, partition.py:71-81)
+        if not hasattr(backend, "band_forward"):
+            raise InvalidInput("a batch with fewer views than ranks needs tile bands "
+                               "(CudaShardBackend)")
+        S = -(-world // B)
+        bands = {v: backend.band_rows(views[v], S) for v in range(B)}
+        items = [(v, b) for v in range(B) for b in range(len(bands[v]))]
+        item_rend = np.arange(len(items), dtype=np.int64) % world
+        renderers = np.asarray([renderer_of(v, world) for v in range(B)], dtype=np.int64)
+        mine = {v for (v, _), r in zip(items, item_rend) if int(r) == rank}
+    else:
+        renderers = scheduler.assign(views, world) if scheduler is not None else None
+        renderers = np.asarray(renderers if renderers is not None
+                               else [renderer_of(v, world) for v in range(B)], dtype=np.int64)
+        mine = {v for v in range(B) if int(renderers[v]) == rank}
     backend.begin_step(views, have, have_n)
     from .trainer import _InputStager, _pipeline_enabled, _prior_arrays
     if hasattr(backend, "prepare"):
@@ -234,9 +251,12 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
         # memory), each view's compositor waiting only for its own inputs
         dpri = None if priors is None else [_prior_arrays(p) for p in priors]
         stager = _InputStager(views, images, dpri, set(have), normal_priors, set(have_n),
-                              only={v for v in range(B) if int(renderers[v]) == rank})
+                              only=mine)
         images, priors, normal_priors = _StagedInputs(stager, B)
-    if hasattr(backend, "prepare") and _pipeline_enabled():
+    if banded:
+        timers = _banded_views(backend, views, images, priors, normal_priors, group, rank, world,
+                               bands, items, item_rend)
+    elif hasattr(backend, "prepare") and _pipeline_enabled():
         timers = _pipelined_views(backend, views, images, priors, normal_priors, group,
                                   renderers, rank, world)
     else:
@@ -269,9 +289,62 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
         report["render_seconds"] = per_rank.tolist()
         report["imbalance"] = float(per_rank.max() / per_rank.mean()) if per_rank.sum() > 0 \
             else 1.0
-    if scheduler is not None:
+    if scheduler is not None and not banded:
         scheduler.update(views, secs)
     return report
+
+
+def _banded_views(backend, views, images, priors, normal_priors, group, rank, world, bands,
+                  items, item_rend) -> dict:
+    """The sharded step with views split into tile-row bands (B < M).
+
+    Owners run their shard's front end once per view; C1 sends every band's
+    renderer the rows whose tile rectangle reaches its rows (a splat spanning
+    two bands goes to both). Each renderer merges, bins over the whole view
+    (the band's tile lists are the full view's) and composites only its rows.
+    The depth / normal terms are means over a view's valid pixels, so every
+    band's forward runs first, the per-band counts are summed per view over
+    the ranks, and the backward normalises by the view's total. The reverse
+    C1 returns each band's gradients; the owner adds a splat's bands
+    together (distinct indices per band) before its projection / decoder
+    backward.
+    """
+    B = len(views)
+    payloads = [backend.forward_shard(v, views[v]) for v in range(B)]
+    item_payloads, index = [], []
+    for v, b in items:
+        sub, idx = backend.band_payload(payloads[v], views[v], bands[v][b])
+        item_payloads.append(sub)
+        index.append(idx)
+    plan, merged = exchange_splats(item_payloads, rank, world, group, item_rend)
+    backend.begin_bands(len(items))
+    for it, (payload, _seg) in merged.items():
+        v, b = items[it]
+        work = backend.prepare(it, views[v], payload)
+        backend.band_forward(it, v, views[v], work, images[v],
+                             None if priors is None else priors[v],
+                             None if normal_priors is None else normal_priors[v], bands[v][b])
+    local = backend.icounts.clone()
+    tot = local.clone()
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=group)
+    item_view = torch.tensor([v for v, _ in items], dtype=torch.int64, device=tot.device)
+    vt = torch.zeros((B, 2), dtype=tot.dtype, device=tot.device).index_add_(0, item_view, tot)
+    for it in merged:
+        backend.icounts[it].copy_(vt[items[it][0]])
+    grads = {it: backend.band_backward(it) for it in merged}
+    like = backend.grad_like()
+    back = return_grads(plan, grads, like, group)
+    for v in range(B):
+        g = torch.zeros((payloads[v].count, like.shape[1]), dtype=like.dtype, device=like.device)
+        for it, (vv, _b) in enumerate(items):
+            if vv == v and back[it] is not None and back[it].numel():
+                g.index_add_(0, index[it], back[it])
+        backend.backward_shard(v, views[v], g)
+    # this rank's share of each view's loss sums / counts (summed over ranks
+    # with the other loss terms)
+    backend.sums.index_add_(0, item_view, backend.isums)
+    backend.counts.index_add_(0, item_view, local)
+    return {}
 
 
 def _c2_sum(t: torch.Tensor, group, ordered: bool) -> None:
@@ -598,11 +671,11 @@ class CudaShardBackend:
     def render(self, v: int, view, payload: SplatPayload, image, prior, nprior) -> torch.Tensor:
         return self.render_prepared(v, view, self.prepare(v, view, payload), image, prior, nprior)
 
-    def render_prepared(self, v: int, view, work, image, prior, nprior) -> torch.Tensor:
+    def _loss(self, v: int, view, image, prior, nprior, sums, counts, band=(0, 0)):
+        """The fused objective of view v (or of its tile-row band) -> (desc, buffers)."""
         from ._lib import VsxLossDesc, ptr
-        D, st = self.D, self.state
         from .trainer import _mask_u8, _prior_arrays, _to_device_image, weight_schedule
-        P, Bn, order = work
+        st = self.state
         H, W = view.height, view.width
         w2, _ = weight_schedule(st.step, st.cfg)
         wn = float(getattr(st.cfg, "normal_weight", 0.0))
@@ -620,14 +693,72 @@ class CudaShardBackend:
                            prior_normal_valid=ptr(pnv).value, rgb_scale=1.0 / (self.B * H * W * 3),
                            depth_weight=w2 / len(self.have) if pd is not None else 0.0,
                            normal_weight=wn / len(self.have_n) / 3.0 if pn is not None else 0.0,
-                           sums=self.sums[v].data_ptr(), counts=self.counts[v].data_ptr())
+                           sums=sums.data_ptr(), counts=counts.data_ptr(),
+                           tile_row0=int(band[0]), tile_rows=int(band[1]))
+        return loss, (gt, pd, pv, pn, pnv)
+
+    def render_prepared(self, v: int, view, work, image, prior, nprior) -> torch.Tensor:
+        D, st = self.D, self.state
+        P, Bn, order = work
+        loss, keep = self._loss(v, view, image, prior, nprior, self.sums[v], self.counts[v])
         from .trainer import _span
         self.isects += Bn.intersections
+        det = bool(getattr(st.cfg, "deterministic", False))
         with _span(self.timer, "raster_fwd"):
-            det = bool(getattr(st.cfg, "deterministic", False))
             R = D.raster_forward(P, Bn, view, loss=loss, deterministic=det)
         with _span(self.timer, "raster_bwd"):
             gs = D.raster_backward(P, Bn, view, R, loss=loss, deterministic=det)
+        merged = torch.empty_like(gs)
+        merged[order] = gs
+        return merged
+
+    # ---- tile-row bands (a view split over renderer ranks when B < M)
+
+    @staticmethod
+    def band_rows(view, S: int) -> list[tuple[int, int]]:
+        """S contiguous tile-row bands (row0, rows) of the view, sizes within one."""
+        tyn = (view.height + 15) // 16
+        S = max(1, min(S, tyn))
+        cuts = [tyn * b // S for b in range(S + 1)]
+        return [(cuts[b], cuts[b + 1] - cuts[b]) for b in range(S)]
+
+    def band_payload(self, payload: SplatPayload, view, band):
+        """The payload rows whose tile rectangle (renderer.py:216-221, float64
+        floor as vsx_bin_*) reaches the band's tile rows, and their indices."""
+        tyn = (view.height + 15) // 16
+        if payload.count == 0:
+            idx = torch.zeros(0, dtype=torch.int64, device=payload.z.device)
+        else:
+            yv = payload.rec.view(torch.float64)[:, 1]
+            r = payload.radius
+            y0 = torch.clamp(torch.floor((yv - r) * 0.0625), min=0.0)
+            y1 = torch.clamp(torch.floor((yv + r) * 0.0625), max=float(tyn - 1))
+            lo, hi = float(band[0]), float(band[0] + band[1] - 1)
+            idx = torch.nonzero((y1 >= y0) & (y0 <= hi) & (y1 >= lo)).flatten()
+        sub = SplatPayload(payload.rec[idx], payload.z[idx], payload.radius[idx],
+                           payload.gid[idx])
+        return sub, idx
+
+    def begin_bands(self, n_items: int) -> None:
+        self.isums = torch.zeros((n_items, 3), dtype=torch.float64, device="cuda")
+        self.icounts = torch.zeros((n_items, 2), dtype=torch.int32, device="cuda")
+        self.pending = {}
+
+    def band_forward(self, it: int, v: int, view, work, image, prior, nprior, band) -> None:
+        D, st = self.D, self.state
+        P, Bn, order = work
+        loss, keep = self._loss(v, view, image, prior, nprior, self.isums[it], self.icounts[it],
+                                band)
+        self.isects += Bn.intersections
+        det = bool(getattr(st.cfg, "deterministic", False))
+        R = D.raster_forward(P, Bn, view, loss=loss, deterministic=det)
+        self.pending[it] = (work, view, loss, keep, R)
+
+    def band_backward(self, it: int) -> torch.Tensor:
+        D, st = self.D, self.state
+        (P, Bn, order), view, loss, keep, R = self.pending.pop(it)
+        det = bool(getattr(st.cfg, "deterministic", False))
+        gs = D.raster_backward(P, Bn, view, R, loss=loss, deterministic=det)
         merged = torch.empty_like(gs)
         merged[order] = gs
         return merged

@@ -29,6 +29,7 @@ from paper_2503_23044_b200.dist import (CudaShardBackend, sharded_train_step,  #
 from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step  # noqa: E402
 
 WORLD = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+NV = int(sys.argv[2]) if len(sys.argv) > 2 else 3   # views; < WORLD splits views into bands
 STEPS = 2
 d = load_golden("train_small")
 views = [golden_view(d, f"v{i}", i) for i in range(3)]
@@ -41,7 +42,12 @@ for _i in range(3):
     _p = _rng.normal(size=(40, 48, 3)).astype(np.float32)
     npri.append((_p / np.linalg.norm(_p, axis=-1, keepdims=True), _rng.uniform(size=(40, 48)) > 0.3))
 npri[2] = None
-cfg = dict(total_steps=8, batch_size=3, step2_start=0, step3_start=8, growth_stop=0,
+if NV < 3:
+    # keep a view with a normal prior but no depth prior among the first NV
+    views, images = views[:NV], images[:NV]
+    priors = [priors[0], None][:NV]
+    npri = [None, npri[1]][:NV]
+cfg = dict(total_steps=8, batch_size=NV, step2_start=0, step3_start=8, growth_stop=0,
            normal_weight=0.5)
 
 import faulthandler  # noqa: E402

@@ -157,3 +157,60 @@ def test_step_report_transfer_bytes_match_reference(train_small, workers):
             assert 0 < rep.transfer_bytes <= rep.gaussians * 136 * workers
         assert rep.rgb == pytest.approx(float(g[f"w{workers}_rgb"][s]), rel=2e-4)
         assert np.isfinite(rep.imbalance) and 1.0 <= rep.imbalance <= workers
+
+
+def test_tile_row_bands_compose_the_view():
+    """vsx_loss_desc.tile_row0 / tile_rows (the sharded step's bands when a
+    batch has fewer views than ranks): every band's pixels equal the
+    full-view render bit for bit, the bands' loss sums / counts add up to the
+    view's, and the bands' per-splat gradients (each normalised by the
+    view's counts) sum to the full view's."""
+    import bench
+    from paper_2503_23044_b200 import device as D
+    from paper_2503_23044_b200._lib import VsxLossDesc
+    from paper_2503_23044_b200.dist import CudaShardBackend
+    from paper_2503_23044_b200.trainer import TrainConfig, TrainState
+    scene, views, _desc, _ = bench.workload("cfg1")
+    v = views[0]
+    st = TrainState(scene, TrainConfig(total_steps=100, step2_start=0, step3_start=100,
+                                       growth_stop=0))
+    ds = st.dscene
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    act = ds.active(v)
+    dec = D.decode(st.params.abi(), st.n, act, ds.centers, st.anchors.emb, st.anchors.log_scales,
+                   st.anchors.offsets, v, ds.lod_ref, ds.max_scale, status, keep_cache=False)
+    P = D.project(dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, v, status)
+    B = D.bin_tiles(P, v.width, v.height)
+    H, W = v.height, v.width
+    g = torch.Generator(device="cuda").manual_seed(1)
+    gt = torch.rand((H, W, 3), device="cuda", generator=g)
+
+    def run(band, counts=None):
+        sums = torch.zeros(3, dtype=torch.float64, device="cuda")
+        cnt = torch.zeros(2, dtype=torch.int32, device="cuda")
+        loss = VsxLossDesc(gt_rgb=gt.data_ptr(), rgb_scale=1.0 / (H * W * 3),
+                           sums=sums.data_ptr(), counts=cnt.data_ptr(),
+                           tile_row0=band[0], tile_rows=band[1])
+        R = D.raster_forward(P, B, v, loss=loss)
+        if counts is not None:
+            cnt.copy_(counts)
+        gs = D.raster_backward(P, B, v, R, loss=loss)
+        torch.cuda.synchronize()
+        return R, sums, cnt, gs
+
+    R0, s0, c0, g0 = run((0, 0))
+    bands = CudaShardBackend.band_rows(v, 3)
+    assert len(bands) == 3 and sum(r for _, r in bands) == (H + 15) // 16
+    tot = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gsum = torch.zeros_like(g0)
+    for r0, nr in bands:
+        Rb, sb, cb, gb = run((r0, nr), counts=c0)
+        y0, y1 = 16 * r0, min(H, 16 * (r0 + nr))
+        assert torch.equal(Rb.rgb[y0:y1], R0.rgb[y0:y1])
+        assert torch.equal(Rb.t_final[y0:y1], R0.t_final[y0:y1])
+        tot += sb
+        gsum += gb
+    assert torch.allclose(tot, s0, rtol=1e-12, atol=0)
+    rms = g0.double().pow(2).mean().sqrt()
+    assert float((gsum.double() - g0.double()).abs().max()) <= 1e-5 * float(rms) + 1e-4 * \
+        float(g0.double().abs().max())

@@ -59,8 +59,8 @@ def test_sharded_step_world1_matches_train_step(nccl_world1, train_small):
     assert bad.mean() < 1e-3, bad.sum()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_step_threaded_ranks_match_train_step(world):
+@pytest.mark.parametrize("world,nv", [(2, 3), (4, 3), (4, 2), (3, 2)])
+def test_sharded_step_threaded_ranks_match_train_step(world, nv):
     """World size 2 and 4 on one GPU: threads of one process joined by
     torch's in-process process group (host-side collectives, no cross-rank
     kernel waits). Losses on every rank and the owner-merged anchor
@@ -68,13 +68,18 @@ def test_sharded_step_threaded_ranks_match_train_step(world):
     decoder too. At world 4 with 3 views one rank renders nothing. One view
     has no depth prior and one no normal prior (per-term normalisation over
     the views that carry one), and the growth accumulators summed over the
-    ranks equal train_step's."""
+    ranks equal train_step's. With fewer views than ranks (4 ranks / 2
+    views, 3 ranks / 2 views) every view is split into tile-row bands
+    rendered on different ranks: the per-view valid-pixel counts are summed
+    over the bands before the backward, and owners add each splat's band
+    gradients."""
     import json
     import subprocess
     import sys
     from pathlib import Path
     here = Path(__file__).resolve().parent
-    p = subprocess.run([sys.executable, str(here / "dist_threaded_worker.py"), str(world)],
+    p = subprocess.run([sys.executable, str(here / "dist_threaded_worker.py"), str(world),
+                        str(nv)],
                        capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
     out = json.loads(p.stdout.strip().splitlines()[-1])
