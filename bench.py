@@ -592,32 +592,74 @@ def run_vsx(args):
     e2e = None
     if not args.no_e2e:
         himgs = [t.cpu().pin_memory() for t in imgs]
-        hpri = [(d.cpu().pin_memory(), v.cpu().pin_memory()) for d, v in priors] if priors else None
-        hnrm = [(nn.cpu().pin_memory(), v.cpu().pin_memory()) for nn, v in nprior] if nprior else None
+        # masks travel as uint8 (one byte each, the kernels' type), so the copy
+        # is a plain DMA with no cast on either side
+        hpri = [(d.cpu().pin_memory(), v.cpu().to(torch.uint8).pin_memory())
+                for d, v in priors] if priors else None
+        hnrm = [(nn.cpu().pin_memory(), v.cpu().to(torch.uint8).pin_memory())
+                for nn, v in nprior] if nprior else None
         h2d = sum(t.numel() * t.element_size() for t in himgs)
         if hpri:
             h2d += sum(d.numel() * 4 + v.numel() for d, v in hpri)
         if hnrm:
             h2d += sum(nn.numel() * 4 + v.numel() for nn, v in hnrm)
-        for _ in range(2):  # host-input path: its H2D staging buffers join the pools
-            step(himgs, hpri, hnrm)
+        prefetch = world == 1 and not args.sharded and os.environ.get("VSX_BENCH_E2E_DEVICE") != "1"
+        # host-input path: its H2D staging buffers (two batches in flight when
+        # prefetching) join the pools before the timed region
+        if prefetch:
+            from paper_2503_23044_b200.trainer import StagedInputs
+            nxt = StagedInputs(views, himgs, hpri, hnrm)
+            for _ in range(3):
+                cur, nxt = nxt, StagedInputs(views, himgs, hpri, hnrm)
+                step(cur, None, None)
+            del nxt
+        else:
+            for _ in range(2):
+                step(himgs, hpri, hnrm)
         reserve_stream_pools(1 << 30)
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            step(himgs, hpri, hnrm)
-        e1.record()
+        if os.environ.get("VSX_BENCH_DIAG") == "1":
+            em0 = torch.cuda.memory_stats()
+        if prefetch:
+            # double-buffered input pipeline: step k+1's H2D copies are issued
+            # (trainer.StagedInputs) before step k runs, so they overlap its
+            # compute; every step's inputs are still copied inside the region
+            from paper_2503_23044_b200.trainer import StagedInputs
+            e0.record()
+            nxt = StagedInputs(views, himgs, hpri, hnrm)
+            for k in range(args.steps):
+                cur = nxt
+                if k + 1 < args.steps:
+                    nxt = StagedInputs(views, himgs, hpri, hnrm)
+                step(cur, None, None)
+            e1.record()
+        else:
+            e0.record()
+            if os.environ.get("VSX_BENCH_E2E_DEVICE") == "1":   # diagnostic: device inputs
+                for _ in range(args.steps):
+                    step(imgs, priors, nprior)
+            else:
+                for _ in range(args.steps):
+                    step(himgs, hpri, hnrm)
+            e1.record()
         torch.cuda.synchronize()
+        if os.environ.get("VSX_BENCH_DIAG") == "1":
+            em1 = torch.cuda.memory_stats()
+            print("diag e2e alloc", {k: em1.get(k, 0) - em0.get(k, 0) for k in (
+                "num_device_alloc", "num_device_free", "num_alloc_retries",
+                "num_sync_all_streams")}, file=sys.stderr)
         ems = e0.elapsed_time(e1) / args.steps
         if world > 1:
             t = torch.tensor([ems], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": len(views) / (ems / 1e3), "unit": "views/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * 4 + 8}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * 4 + 8,
+               "input_pipeline": "next step's H2D issued before the current step (StagedInputs)"
+               if prefetch else "each step's H2D issued at its start"}
     cfg1 = None
     if rank == 0 and world == 1 and args.config != "cfg1" and not args.no_cfg1:
         cfg1 = cfg1_gpu(max(args.steps, 10))

@@ -489,10 +489,14 @@ class _InputStager:
     earlier ones. CUDA inputs pass through untouched.
     """
 
-    def __init__(self, views, images, priors, have, normal_priors, have_n, only=None):
+    def __init__(self, views, images, priors, have, normal_priors, have_n, only=None,
+                 prefetch=False):
         cur = torch.cuda.current_stream()
         cs = _side_stream("copy")
-        cs.wait_stream(cur)
+        if not prefetch:
+            # (a prefetch depends on nothing but host memory and fresh blocks:
+            # it may run under the current step's compute)
+            cs.wait_stream(cur)
         self.items, self.events = [], []
         with torch.cuda.stream(cs):
             for vi, view in enumerate(views):
@@ -523,6 +527,34 @@ class _InputStager:
         return self.items[vi]
 
 
+class StagedInputs:
+    """A batch's targets and priors already on their way to the device.
+
+    The host->device copies (pinned host memory, the copy stream) are issued
+    when this is built, so building step k+1's inputs before calling
+    ``train_step`` for step k overlaps them with step k's compute — the
+    double-buffered input pipeline of a training loop. Pass it as
+    ``train_step``'s ``images``; its ``enhanced`` / ``normal_priors`` are
+    used (priors the step's schedule leaves unused are ignored).
+    """
+
+    def __init__(self, views: list[CameraView], images: list, enhanced: list | None = None,
+                 normal_priors: list | None = None):
+        B = len(views)
+        if B == 0 or len(images) != B:
+            raise InvalidInput("views and images must be equal length and non-empty")
+        self.views, self.images = views, images
+        self.enhanced, self.normal_priors = enhanced, normal_priors
+        priors = [_prior_arrays(e) for e in enhanced] if enhanced is not None else None
+        have = [i for i in range(B) if priors is not None and priors[i] is not None]
+        have_n = [i for i in range(B) if normal_priors is not None and normal_priors[i] is not None]
+        self.stager = _InputStager(views, images, priors, have, normal_priors, have_n,
+                                   prefetch=True)
+
+    def __len__(self) -> int:
+        return len(self.images)
+
+
 def train_step(state: TrainState, views: list[CameraView], images: list,
                enhanced: list | None = None, keep: list | None = None,
                normal_priors: list | None = None, timer: GpuTimer | None = None) -> StepReport:
@@ -538,6 +570,11 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     cfg = state.cfg
     t0 = time.perf_counter()
     B = len(views)
+    staged = images if isinstance(images, StagedInputs) else None
+    if staged is not None:
+        if len(staged.views) != B:
+            raise InvalidInput("StagedInputs built for another batch")
+        images, enhanced, normal_priors = staged.images, staged.enhanced, staged.normal_priors
     if B == 0 or len(images) != B:
         raise InvalidInput("views and images must be equal length and non-empty")
     w2, w3 = weight_schedule(state.step, cfg)
@@ -562,7 +599,8 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     gaussians = 0
     isects = 0
     anchors, agrads = state.anchors, state.anchor_grads
-    stager = _InputStager(views, images, priors, have, normal_priors, have_n)
+    stager = staged.stager if staged is not None else \
+        _InputStager(views, images, priors, have, normal_priors, have_n)
     book = _WorkerBook(state, views) if cfg.workers > 1 else None
     main = torch.cuda.current_stream()
     # Three-stream software pipeline over the views: the front end of view v+1
@@ -606,6 +644,10 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
     def loss_desc(vi, extra=None):
         view = views[vi]
         gt, pd, pv, pn, pnv = stager.get(vi)
+        if vi not in have:          # a prefetched prior the schedule does not use
+            pd = pv = None
+        if vi not in have_n:
+            pn = pnv = None
         ex_rgb, ex_nrm, ex_dep = extra if extra is not None else (None, None, None)
         return VsxLossDesc(
             gt_rgb=gt.data_ptr(), prior_depth=ptr(pd).value, prior_depth_valid=ptr(pv).value,

@@ -166,3 +166,23 @@ def test_deterministic_sharded_world1_matches_train_step(train_small):
             dist.destroy_process_group()
     torch.cuda.synchronize()
     assert torch.equal(a.flat.param, b.flat.param)
+
+
+def test_prefetched_inputs_give_the_same_steps(train_small):
+    """trainer.StagedInputs (the next step's targets / priors copied to the
+    device while the current step runs) is the same computation: with
+    fixed-order sums, two steps fed by prefetched inputs equal two steps fed
+    by host arrays bit for bit."""
+    from paper_2503_23044_b200.trainer import StagedInputs, TrainConfig, TrainState, train_step
+    d = train_small
+    views, images, priors, npri = _inputs(d)
+    a, _ = _run(d, True)
+    b = TrainState(golden_scene(d), TrainConfig(**_cfg(True)))
+    nxt = StagedInputs(views, images, priors, npri)
+    for k in range(2):
+        cur = nxt
+        if k == 0:
+            nxt = StagedInputs(views, images, priors, npri)
+        train_step(b, views, cur)
+    torch.cuda.synchronize()
+    assert torch.equal(a.flat.param, b.flat.param)
