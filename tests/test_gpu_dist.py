@@ -39,24 +39,27 @@ def test_sort_z_gid_is_lexsort():
 
 
 def test_sharded_step_world1_matches_train_step(nccl_world1, train_small):
+    """World size 1 (NCCL self-exchange) against train_step: losses to float
+    rounding of the report and, with fixed-order sums
+    (TrainConfig.deterministic), parameters bit for bit."""
     from paper_2503_23044_b200.dist import CudaShardBackend, sharded_train_step
     from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step
     d = train_small
     views = [golden_view(d, f"v{i}", i) for i in range(3)]
     images = [d[f"img{i}"] for i in range(3)]
     priors = [(d[f"prior{i}"], d[f"pvalid{i}"]) for i in range(3)]
-    cfg = dict(total_steps=8, batch_size=3, step2_start=0, step3_start=8, growth_stop=0)
+    cfg = dict(total_steps=8, batch_size=3, step2_start=0, step3_start=8, growth_stop=0,
+               deterministic=True)
     a = TrainState(golden_scene(d), TrainConfig(**cfg))
     b = TrainState(golden_scene(d), TrainConfig(**cfg))
     be = CudaShardBackend(b, 0, 1)
     for _ in range(2):
         ra = train_step(a, views, images, priors)
         rb = sharded_train_step(be, views, images, priors)
-        assert rb["rgb"] == pytest.approx(ra.rgb, rel=1e-6)
-        assert rb["depth"] == pytest.approx(ra.depth, rel=1e-5)
-    pa, pb = a.flat.param.cpu().numpy(), b.flat.param.cpu().numpy()
-    bad = np.abs(pa - pb) > 1e-5 * np.maximum(np.abs(pa), np.abs(pb)) + 1e-7
-    assert bad.mean() < 1e-3, bad.sum()
+        assert rb["rgb"] == pytest.approx(ra.rgb, rel=1e-15)
+        assert rb["depth"] == pytest.approx(ra.depth, rel=1e-15)
+    torch.cuda.synchronize()
+    assert torch.equal(a.flat.param, b.flat.param)
 
 
 @pytest.mark.parametrize("world,nv", [(2, 3), (4, 3), (4, 2), (3, 2)])
