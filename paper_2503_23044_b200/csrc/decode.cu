@@ -1212,8 +1212,9 @@ static int launch_wgrad(const float *A, int a_rows, bool ones_row, const float *
   return VSX_OK;
 }
 
-int decoder_wgrad_tc(const float *g_o, const float *cache_h, const float *g_pre, const float *xs,
-                     int64_t K, size_t ld, int n, vsx_decoder_grads dW, cudaStream_t st);
+int decoder_wgrad_tc2(const float *g_o, const float *cache_h, const float *g_pre, const float *xs,
+                      int64_t K, size_t ld, int n, vsx_decoder_grads dW, float *partial,
+                      size_t partial_floats, cudaStream_t st);
 
 }  // namespace vsx
 
@@ -1314,13 +1315,19 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
         g_emb, g_log_scale, xs, g_pre);
     VSX_LAUNCH_CHECK("decode_bwd_anchor");
   }
-  static const int wg_impl = [] {
-    const char *e = getenv("VSX_WGRAD");  // "tc" = tcgen05 version (A/B)
-    return (e && e[0] == 't') ? 1 : 0;
+  // weight gradients: the pipelined tcgen05 kernel (TMEM accumulators, one
+  // fixed-order reduction) by default; VSX_WGRAD=mma selects the mma.sync
+  // K-split kernel (A/B, and the path for 11 n > 128 outputs)
+  static const bool wg_mma = [] {
+    const char *e = getenv("VSX_WGRAD");
+    return e && e[0] == 'm';
   }();
-  if (use_tc && wg_impl == 0 && wm_supported(n)) {  // mma.sync K-split + reduction
-    float *partial = reinterpret_cast<float *>(
-        reinterpret_cast<char *>(g_o + (size_t)11 * n * ld) + sizeof(float) * dbw_image_floats(n));
+  float *partial = reinterpret_cast<float *>(
+      reinterpret_cast<char *>(g_o + (size_t)11 * n * ld) + sizeof(float) * dbw_image_floats(n));
+  if (use_tc && !wg_mma && 11 * n <= 128)
+    return decoder_wgrad_tc2(g_o, cache_h, g_pre, xs, n_active, ld, n, dW, partial,
+                             (size_t)(kWmMaxCtas + kWmSlices) * kWmTiles * 128, st);
+  if (use_tc && wm_supported(n)) {  // mma.sync K-split + reduction
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1340,8 +1347,6 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
     VSX_LAUNCH_CHECK("decoder_wgrad_reduce");
     return VSX_OK;
   }
-  if (use_tc && 11 * n <= 128)  // tensor-core weight gradients (decode_tc.cu)
-    return decoder_wgrad_tc(g_o, cache_h, g_pre, xs, n_active, ld, n, dW, st);
   // dW1_h = X^T Gpre_h (+ db1 via the ones row of X)
   WgradOut o1{};
   for (int h = 0; h < 3; ++h) {

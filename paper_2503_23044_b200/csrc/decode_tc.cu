@@ -367,9 +367,10 @@ __global__ void __launch_bounds__(256) decode_gauss_kernel(
 //              -> dW2_h[n][j] (diagonal head blocks) and db2 (ones column)
 //   C2[m][i] = sum_r dPre[r][m] * [X | 1][r][i] M = 192 hidden (two 128 tiles), N = 37 (pad 48)
 //              -> dW1_h[i][m] and db1 (ones column)
-// Each CTA accumulates its K-chunks in TMEM and adds its partial result to
-// the global gradients with one atomicAdd per element at the end. Stages are
-// double-buffered: 8 warps split/stage chunk i+1 while the MMAs of chunk i run.
+// Each persistent CTA accumulates its K-chunks in TMEM (304 of 512 columns)
+// and writes its partial sums to a slot of its own; one reduction kernel
+// folds the slots in CTA order into the gradients (no float atomics, so the
+// result is bitwise reproducible).
 
 constexpr int kWgKc = 16;    // anchors per stage (2 MMA k-steps)
 constexpr int kWgN1 = 208;   // 192 hidden + ones row, padded to 16
@@ -379,101 +380,143 @@ struct WgSmem {
   float *a1_hi, *a1_lo, *b1_hi, *b1_lo, *a2_hi, *a2_lo, *b2_hi, *b2_lo;
 };
 
-constexpr int kWgStageFloats = 2 * kWgKc * (128 + kWgN1 + 256 + kWgN2);
+// The raw fp32 operand rows of K-chunks arrive by cp.async (16-byte pieces
+// straight into the K-major core-matrix layout, eight threads per 128-byte
+// column) two chunks ahead of the tensor core (three raw stages); the MMA
+// reads the raw words as the "hi" tf32 operand (the tensor core keeps the
+// top 19 bits: truncation), and one pass per chunk writes lo = x - trunc(x)
+// into a double-buffered lo plane (3xTF32, the same split as the mma.sync
+// kernel). Padding rows and the ones row of [H | 1] are written once. One
+// mbarrier per raw stage orders its refill after the MMAs that read it.
+__device__ __forceinline__ void wg_cp16(float *dst_base, uint32_t off, const float *src,
+                                        int bytes) {
+  const uint32_t d = umma::smem_addr(reinterpret_cast<char *>(dst_base) + off);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes)
+               : "memory");
+}
 
-inline size_t wg_smem_bytes() { return sizeof(float) * (size_t)2 * kWgStageFloats; }
+struct WgOp {
+  float *hi, *lo;
+  const float *src;
+  int rows_valid;
+};
 
-// Stage rows [0, rows) of a feature-major [rows_valid x K] matrix, anchors
-// [k0, k0 + 32), into a hi/lo K-major tile of `rows` rows. Rows >= rows_valid
-// read `ones_row` (1.0 when == that row index) or zero.
-__device__ __forceinline__ void wg_stage(float *hi, float *lo, const float *__restrict__ src,
-                                         int rows, int rows_valid, int ones_row, int64_t K,
+__device__ __forceinline__ void wg_issue(const WgSmem &s, const float *g_o, const float *cache_h,
+                                         const float *g_pre, const float *xs, int nout, int64_t K,
                                          size_t ld, int64_t k0) {
-  const int quads = rows * (kWgKc / 4);
-  constexpr int kU = 8;  // float4 loads in flight per thread
-  for (int base = threadIdx.x; base < quads; base += kU * blockDim.x) {
-    float4 v[kU];
+  const WgOp ops[4] = {{s.a1_hi, s.a1_lo, g_o, nout},
+                       {s.b1_hi, s.b1_lo, cache_h, 192},
+                       {s.a2_hi, s.a2_lo, g_pre, 192},
+                       {s.b2_hi, s.b2_lo, xs, kInDim + 1}};
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int e = base + u * blockDim.x;
-      const int r = e / (kWgKc / 4), q = e % (kWgKc / 4);
+  for (int o = 0; o < 4; ++o) {
+    // piece e -> (8-row group, 16-byte column q, row in group): 8 consecutive
+    // threads fill one contiguous 128-byte core-matrix column
+    const int pieces = ((ops[o].rows_valid + 7) / 8) * 8 * (kWgKc / 4);
+    for (int e = threadIdx.x; e < pieces; e += blockDim.x) {
+      const int r = (e / (8 * (kWgKc / 4))) * 8 + (e & 7), q = (e >> 3) % (kWgKc / 4);
+      if (r >= ops[o].rows_valid) continue;
       const int64_t k = k0 + 4 * q;
-      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e < quads && r < rows_valid) {
-        const float *p = src + (size_t)r * ld + k;
-        if (k + 3 < K) {  // rows are 16-byte aligned (ld % 4 == 0)
-          v[u] = __ldg(reinterpret_cast<const float4 *>(p));
-        } else {
-          v[u].x = (k + 0 < K) ? p[0] : 0.f;
-          v[u].y = (k + 1 < K) ? p[1] : 0.f;
-          v[u].z = (k + 2 < K) ? p[2] : 0.f;
-          v[u].w = (k + 3 < K) ? p[3] : 0.f;
-        }
-      } else if (e < quads && r == ones_row) {
-        v[u] = make_float4(k < K ? 1.f : 0.f, k + 1 < K ? 1.f : 0.f, k + 2 < K ? 1.f : 0.f,
-                           k + 3 < K ? 1.f : 0.f);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int e = base + u * blockDim.x;
-      if (e < quads) {
-        const int r = e / (kWgKc / 4), q = e % (kWgKc / 4);
-        st_split4(hi, lo, umma::kmajor_offset(r, 4 * q, kWgKc), v[u].x, v[u].y, v[u].z, v[u].w);
-      }
+      const int64_t rem = K - k;
+      const int bytes = rem <= 0 ? 0 : (rem >= 4 ? 16 : (int)(4 * rem));
+      wg_cp16(ops[o].hi, umma::kmajor_offset(r, 4 * q, kWgKc),
+              ops[o].src + (size_t)r * ld + (bytes > 0 ? k : 0), bytes);
     }
   }
 }
 
-__device__ __forceinline__ WgSmem wg_carve(float *base) {
+__device__ __forceinline__ void wg_lo_pass(const WgSmem &s, int nout) {
+  const WgOp ops[4] = {{s.a1_hi, s.a1_lo, nullptr, nout},
+                       {s.b1_hi, s.b1_lo, nullptr, 192},
+                       {s.a2_hi, s.a2_lo, nullptr, 192},
+                       {s.b2_hi, s.b2_lo, nullptr, kInDim + 1}};
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const int pieces = ((ops[o].rows_valid + 7) / 8) * 8 * (kWgKc / 4);
+    for (int e = threadIdx.x; e < pieces; e += blockDim.x) {
+      const int r = (e / (8 * (kWgKc / 4))) * 8 + (e & 7), q = (e >> 3) % (kWgKc / 4);
+      if (r >= ops[o].rows_valid) continue;
+      const uint32_t off = umma::kmajor_offset(r, 4 * q, kWgKc);
+      const float4 x = *reinterpret_cast<const float4 *>(reinterpret_cast<const char *>(ops[o].hi) + off);
+      float4 l;
+      l.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
+      l.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
+      l.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
+      l.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
+      *reinterpret_cast<float4 *>(reinterpret_cast<char *>(ops[o].lo) + off) = l;
+    }
+  }
+}
+
+// Operand planes of one K-chunk (one plane: hi raw words or lo parts).
+constexpr int kWgPlaneFloats = kWgKc * (128 + kWgN1 + 256 + kWgN2);
+constexpr int kWgRaw = 3;  // raw-word stages in flight
+
+__device__ __forceinline__ WgSmem wg_planes(float *hi, float *lo) {
   WgSmem s;
-  s.a1_hi = base;
-  s.a1_lo = s.a1_hi + 128 * kWgKc;
-  s.b1_hi = s.a1_lo + 128 * kWgKc;
-  s.b1_lo = s.b1_hi + kWgN1 * kWgKc;
-  s.a2_hi = s.b1_lo + kWgN1 * kWgKc;
-  s.a2_lo = s.a2_hi + 256 * kWgKc;
-  s.b2_hi = s.a2_lo + 256 * kWgKc;
-  s.b2_lo = s.b2_hi + kWgN2 * kWgKc;
+  s.a1_hi = hi;
+  s.b1_hi = hi + 128 * kWgKc;
+  s.a2_hi = s.b1_hi + kWgN1 * kWgKc;
+  s.b2_hi = s.a2_hi + 256 * kWgKc;
+  s.a1_lo = lo;
+  s.b1_lo = lo + 128 * kWgKc;
+  s.a2_lo = s.b1_lo + kWgN1 * kWgKc;
+  s.b2_lo = s.a2_lo + 256 * kWgKc;
   return s;
 }
 
-__device__ __forceinline__ void wg_stage_all(const WgSmem &s, const float *g_o,
-                                             const float *cache_h, const float *g_pre,
-                                             const float *xs, int nout, int64_t K, size_t ld,
-                                             int64_t k0) {
-  wg_stage(s.a1_hi, s.a1_lo, g_o, 128, nout, -1, K, ld, k0);
-  wg_stage(s.b1_hi, s.b1_lo, cache_h, kWgN1, 192, 192, K, ld, k0);
-  wg_stage(s.a2_hi, s.a2_lo, g_pre, 256, 192, -1, K, ld, k0);
-  wg_stage(s.b2_hi, s.b2_lo, xs, kWgN2, kInDim + 1, -1, K, ld, k0);  // xs row 36 = ones
-}
+constexpr int kWgPartial = 128 * kWgN1 + 256 * kWgN2;  // floats per CTA partial
 
-__global__ void __launch_bounds__(256, 1) decoder_wgrad_tc_kernel(
+__global__ void __launch_bounds__(256, 1) decoder_wgrad_tc2_kernel(
     const float *__restrict__ g_o, const float *__restrict__ cache_h,
     const float *__restrict__ g_pre, const float *__restrict__ xs, int64_t K, size_t ld, int n,
-    vsx_decoder_grads dW) {
+    float *__restrict__ partial) {
   extern __shared__ __align__(1024) float wsm[];
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t mbar[kWgRaw];
   __shared__ uint32_t tslot;
-  const WgSmem sb[2] = {wg_carve(wsm), wg_carve(wsm + kWgStageFloats)};
+  float *raw = wsm, *lo = wsm + kWgRaw * kWgPlaneFloats;
   const int t = threadIdx.x, warp = t >> 5;
   const int nout = 11 * n;
+  // zero every plane once (padding rows, lo of the ones row), then the ones
+  // row of [H | 1] (row 192 of B1) in each raw stage
+  for (int e = t; e < (kWgRaw + 2) * kWgPlaneFloats; e += blockDim.x) wsm[e] = 0.f;
+  __syncthreads();
+  for (int b = 0; b < kWgRaw; ++b)
+    for (int k = t; k < kWgKc; k += blockDim.x)
+      *reinterpret_cast<float *>(reinterpret_cast<char *>(raw + b * kWgPlaneFloats +
+                                                          128 * kWgKc) +
+                                 umma::kmajor_offset(192, k, kWgKc)) = 1.f;
   if (warp == 0) umma::tmem_alloc(&tslot, 512);
-  if (t == 0) umma::mbar_init(&mbar, 1);
+  if (t == 0)
+    for (int b = 0; b < kWgRaw; ++b) umma::mbar_init(&mbar[b], 1);
+  __syncthreads();
   const int64_t nchunks = (K + kWgKc - 1) / kWgKc;
-  if ((int64_t)blockIdx.x < nchunks)
-    wg_stage_all(sb[0], g_o, cache_h, g_pre, xs, nout, K, ld, (int64_t)blockIdx.x * kWgKc);
-  umma::fence_async_smem();
+  const int64_t G = gridDim.x;
+  // prologue: this CTA's chunks 0 and 1 in flight (one cp.async group each)
+  for (int p = 0; p < kWgRaw - 1; ++p) {
+    const int64_t ch = (int64_t)blockIdx.x + p * G;
+    if (ch < nchunks)
+      wg_issue(wg_planes(raw + p * kWgPlaneFloats, lo), g_o, cache_h, g_pre, xs, nout, K, ld,
+               ch * kWgKc);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   umma::fence_before_sync();
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tbase = tslot;
   const uint32_t c1 = tbase, c2a = tbase + kWgN1, c2b = tbase + kWgN1 + kWgN2;
-  uint32_t phase = 0;
-  bool first = true;
-  int buf = 0;
-  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x, buf ^= 1) {
-    const WgSmem &s = sb[buf];
+  uint32_t phase[kWgRaw] = {0u, 0u, 0u};
+  int it = 0;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += G, ++it) {
+    const int rb = it % kWgRaw, lb = it & 1;
+    const WgSmem s = wg_planes(raw + rb * kWgPlaneFloats, lo + lb * kWgPlaneFloats);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // chunk ch landed
+    __syncthreads();
+    wg_lo_pass(s, nout);
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
     if (t == 0) {
       const uint32_t i1 = umma::idesc_tf32(128, kWgN1), i2 = umma::idesc_tf32(128, kWgN2);
       const uint32_t a1h = umma::smem_addr(s.a1_hi), a1l = umma::smem_addr(s.a1_lo);
@@ -483,7 +526,7 @@ __global__ void __launch_bounds__(256, 1) decoder_wgrad_tc_kernel(
       const uint32_t tile2 = 128 * kWgKc * 4;  // second 128-row tile of A2
       for (int st = 0; st < kWgKc / 8; ++st) {
         const uint32_t o = (uint32_t)st * 256;
-        const bool acc0 = !(first && st == 0);
+        const bool acc0 = !(it == 0 && st == 0);
         using umma::desc_kmajor;
         umma::mma_tf32(c1, desc_kmajor(a1h + o, kWgKc), desc_kmajor(b1h + o, kWgKc), i1, acc0);
         umma::mma_tf32(c1, desc_kmajor(a1l + o, kWgKc), desc_kmajor(b1h + o, kWgKc), i1, true);
@@ -498,78 +541,129 @@ __global__ void __launch_bounds__(256, 1) decoder_wgrad_tc_kernel(
                          true);
         }
       }
-      umma::commit(&mbar);
+      umma::commit(&mbar[rb]);
     }
-    // stage the next chunk into the other buffer while the MMAs run
-    const int64_t nx = ch + gridDim.x;
-    if (nx < nchunks) wg_stage_all(sb[buf ^ 1], g_o, cache_h, g_pre, xs, nout, K, ld, nx * kWgKc);
-    umma::mbar_wait(&mbar, phase);
-    phase ^= 1u;
-    umma::fence_async_smem();
-    umma::fence_before_sync();
-    __syncthreads();
+    // chunk ch + 2G goes to the raw stage chunk ch - G used: wait for its MMAs
+    // (issued last iteration; the lo plane it used is rewritten next time)
+    const int nb = (it + kWgRaw - 1) % kWgRaw;
+    if (it >= 1) {
+      umma::mbar_wait(&mbar[nb], phase[nb]);
+      phase[nb] ^= 1u;
+    }
     umma::fence_after_sync();
-    first = false;
+    if (ch + 2 * G < nchunks)
+      wg_issue(wg_planes(raw + nb * kWgPlaneFloats, lo), g_o, cache_h, g_pre, xs, nout, K, ld,
+               (ch + 2 * G) * kWgKc);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  if (!first && t < 128) {  // TMEM lanes 0-127 belong to warps 0-3
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (it > 0) {  // the last chunk's MMAs
+    const int lb = (it - 1) % kWgRaw;
+    umma::mbar_wait(&mbar[lb], phase[lb]);
+  }
+  umma::fence_after_sync();
+  // this CTA's sums to its partial slot (C1 [128][208] then C2 [256][48],
+  // row-major), folded over the CTAs in order by decoder_wgrad_tc2_reduce
+  if (t < 128) {
+    float *part = partial + (size_t)blockIdx.x * kWgPartial;
     const uint32_t lane = (uint32_t)(warp * 32) << 16;
-    // C1 row t = output j: head blocks of dW2 and db2
-    const int j = t;
-    int h = 2;
-    if (j < n) h = 0;
-    else if (j < 4 * n) h = 1;
-    const int oo = h == 0 ? 0 : (h == 1 ? n : 4 * n);
-    const int width = (h == 0 ? 1 : (h == 1 ? 3 : 7)) * n;
     for (int c = 0; c < kWgN1; c += 16) {
       float v[16];
-      umma::tmem_ld16(c1 + lane + (uint32_t)c, v);
-      umma::tmem_ld_wait();
-      if (j >= nout) continue;
+      if (it > 0) {
+        umma::tmem_ld16(c1 + lane + (uint32_t)c, v);
+        umma::tmem_ld_wait();
+      } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int col = c + i;
-        if (col >= h * 64 && col < h * 64 + 64)
-          atomicAdd(dW.w2[h] + (size_t)(col - h * 64) * width + (j - oo), v[i]);
-        else if (col == 192)
-          atomicAdd(dW.b2[h] + (j - oo), v[i]);
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
       }
+      float4 *dst = reinterpret_cast<float4 *>(part + (size_t)t * kWgN1 + c);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
-    // C2 rows = hidden m (two tiles): dW1_h[i][m] and db1 (ones column 36)
-    for (int mt = 0; mt < 2; ++mt) {
-      const int m = mt * 128 + t;
+    for (int mt = 0; mt < 2; ++mt)
       for (int c = 0; c < kWgN2; c += 16) {
         float v[16];
-        umma::tmem_ld16((mt ? c2b : c2a) + lane + (uint32_t)c, v);
-        umma::tmem_ld_wait();
-        if (m >= 192) continue;
-        const int hh = m / 64, mm = m % 64;
+        if (it > 0) {
+          umma::tmem_ld16((mt ? c2b : c2a) + lane + (uint32_t)c, v);
+          umma::tmem_ld_wait();
+        } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = c + i;
-          if (col < kInDim) atomicAdd(dW.w1[hh] + (size_t)col * 64 + mm, v[i]);
-          else if (col == kInDim) atomicAdd(dW.b1[hh] + mm, v[i]);
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
         }
+        float4 *dst = reinterpret_cast<float4 *>(part + 128 * kWgN1 +
+                                                 (size_t)(mt * 128 + t) * kWgN2 + c);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
-    }
   }
   umma::fence_before_sync();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tbase, 512);
 }
 
-int decoder_wgrad_tc(const float *g_o, const float *cache_h, const float *g_pre, const float *xs,
-                     int64_t K, size_t ld, int n, vsx_decoder_grads dW, cudaStream_t st) {
+// Element e of the partials summed over the CTAs in order (deterministic),
+// added into the gradient it maps to (one thread per element, no atomics).
+__global__ void decoder_wgrad_tc2_reduce(const float *__restrict__ partial, int ctas, int n,
+                                         vsx_decoder_grads dW) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= kWgPartial) return;
+  const int nout = 11 * n;
+  int h = 0, col = 0, j = 0;
+  bool w1 = false;
+  if (e < 128 * kWgN1) {
+    j = e / kWgN1;
+    col = e % kWgN1;
+    if (j >= nout || col > 192) return;
+  } else {
+    const int f = e - 128 * kWgN1;
+    j = f / kWgN2;        // hidden unit m
+    col = f % kWgN2;      // input i (36 = bias)
+    if (j >= 192 || col > kInDim) return;
+    w1 = true;
+  }
+  // 8 independent loads in flight, summed in CTA order
+  float sum = 0.f;
+  int c = 0;
+  for (; c + 8 <= ctas; c += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = partial[(size_t)(c + u) * kWgPartial + e];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) sum += v[u];
+  }
+  for (; c < ctas; ++c) sum += partial[(size_t)c * kWgPartial + e];
+  if (w1) {
+    const int hh = j / 64, mm = j % 64;
+    if (col < kInDim) dW.w1[hh][(size_t)col * 64 + mm] += sum;
+    else dW.b1[hh][mm] += sum;
+  } else {
+    h = j < n ? 0 : (j < 4 * n ? 1 : 2);
+    const int oo = h == 0 ? 0 : (h == 1 ? n : 4 * n);
+    const int width = (h == 0 ? 1 : (h == 1 ? 3 : 7)) * n;
+    if (col == 192) dW.b2[h][j - oo] += sum;
+    else if (col >= h * 64 && col < h * 64 + 64) dW.w2[h][(size_t)(col - h * 64) * width + (j - oo)] += sum;
+  }
+}
+
+int decoder_wgrad_tc2(const float *g_o, const float *cache_h, const float *g_pre, const float *xs,
+                      int64_t K, size_t ld, int n, vsx_decoder_grads dW, float *partial,
+                      size_t partial_floats, cudaStream_t st) {
   if (K == 0) return VSX_OK;
-  const size_t smem = wg_smem_bytes();
-  VSX_CUDA_TRY(cudaFuncSetAttribute(decoder_wgrad_tc_kernel,
+  const size_t smem = sizeof(float) * (size_t)(kWgRaw + 2) * kWgPlaneFloats;
+  VSX_CUDA_TRY(cudaFuncSetAttribute(decoder_wgrad_tc2_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t chunks = (K + kWgKc - 1) / kWgKc;
-  decoder_wgrad_tc_kernel<<<(int)std::min<int64_t>(chunks, sms), 256, smem, st>>>(
-      g_o, cache_h, g_pre, xs, K, ld, n, dW);
-  VSX_LAUNCH_CHECK("decoder_wgrad_tc");
+  const int ctas = (int)std::min<int64_t>(std::min<int64_t>(chunks, sms),
+                                          (int64_t)(partial_floats / kWgPartial));
+  VSX_REQUIRE(ctas >= 1, "decoder_wgrad_tc2: partial buffer too small");
+  decoder_wgrad_tc2_kernel<<<ctas, 256, smem, st>>>(g_o, cache_h, g_pre, xs, K, ld, n, partial);
+  VSX_LAUNCH_CHECK("decoder_wgrad_tc2");
+  decoder_wgrad_tc2_reduce<<<(kWgPartial + 255) / 256, 256, 0, st>>>(partial, ctas, n, dW);
+  VSX_LAUNCH_CHECK("decoder_wgrad_tc2_reduce");
   return VSX_OK;
 }
 
