@@ -27,6 +27,8 @@
 // staged right after phase 2 (double-buffered), two CTA barriers per chunk.
 // The measured alternatives (pixel-per-thread forward, a tensor-core
 // forward, an FFMA phase 2, a warp-specialised backward) are in DESIGN.md §6.
+#include <cuda_fp16.h>
+
 #include "raster_common.cuh"
 
 namespace vsx {
@@ -372,6 +374,17 @@ constexpr int kUB = VSX_BWD_UB;  // phase-1 splats per alpha batch
 #ifndef VSX_BWD_PREFIX
 #define VSX_BWD_PREFIX 1
 #endif
+#ifndef VSX_BWD_EPI_HI
+#define VSX_BWD_EPI_HI 1
+#endif
+// 4 CTAs per SM (56 KB of shared memory, 64 registers): the per-tile B
+// fragments of phase 2 are kept raw and split per k-step (cotangents) or as
+// exact half2 (pixel moments), the partial-sum rows are 18 floats, the
+// prologue's sort scratch lives in the not yet used q plane.
+#ifndef VSX_BWD_OCC4
+#define VSX_BWD_OCC4 1
+#endif
+constexpr int kRedStride = VSX_BWD_OCC4 ? 18 : 24;
 constexpr int kPlaneStride = kTilePixels + 4;  // 4 mod 32: conflict-free A fragments
 
 // pixel moment m of tile pixel p (x, y about the tile centre)
@@ -389,7 +402,7 @@ __device__ __forceinline__ float pixel_moment(int p, int m) {
 }
 
 template <int kBC, bool kDet>
-__global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
+__global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
     raster_bwd_tc_kernel(BwdArgs a, vsx_camera cam) {
   constexpr int kMT = kBC / 16;          // m-tiles per chunk
   constexpr int kSplit = 8 / (2 * kMT);  // k-range split across warps
@@ -397,9 +410,14 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   __shared__ float4 s0[2][kBC], s1[2][kBC], s2[2][kBC], s3[2][kBC];
   __shared__ float4 s_ph[2][kBC][4];  // P B fragments per (splat, lane&3): hi b0, hi b1, lo b0, lo b1
   __shared__ uint32_t s_rank[2][kBC];
+#if VSX_BWD_OCC4
+  __shared__ float2 s_bw[32][32];   // Gw B fragment values per (k-step, lane): b0, b1 (split per use)
+  __shared__ __half2 s_bq[32][32];  // Mq B fragments per (k-step, lane): exact in half
+#else
   __shared__ float4 s_bw[32][32];  // Gw B fragments per (k-step, lane): hi b0, hi b1, lo b0, lo b1
   __shared__ float2 s_bq[32][32];  // Mq B fragments per (k-step, lane)
-  __shared__ float s_red[kSplit][kBC][24];
+#endif
+  __shared__ float s_red[kSplit][kBC][kRedStride];
   __shared__ __align__(16) vsx_splat s_raw[2][kBC];
   __shared__ int s_max;
   extern __shared__ float s_plane[];  // w plane [kBC][kPlaneStride], then q plane
@@ -417,9 +435,16 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
   // depths share a warp, so phase 1 runs fewer idle lanes and whole warps go
   // quiet together. Phases 0 / 2 follow the slot order through the per-tile
   // fragments (cotangents and pixel moments are staged per slot).
+#if VSX_BWD_OCC4
+  // sort scratch in the q plane (first written by phase 0 of the first chunk)
+  uint32_t *s_bin = reinterpret_cast<uint32_t *>(s_plane + kBC * kPlaneStride);
+  uint8_t *s_perm = reinterpret_cast<uint8_t *>(s_plane + kBC * kPlaneStride + 260);
+  __shared__ uint16_t s_lp[257];  // first slot of each key ([256] = 256): the live prefix
+#else
   __shared__ uint32_t s_bin[257];  // after the scan: first slot of each key; [256] = 256
-  __shared__ uint32_t s_wsum[8];
   __shared__ uint8_t s_perm[256];  // slot -> pixel (t = 16 y + x)
+#endif
+  __shared__ uint32_t s_wsum[8];
   {
     const int x0 = bx * kTile + (t & 15), y0 = by * kTile + (t >> 4);
     const int nc0 = (x0 < cam.width && y0 < cam.height) ? a.nc[(size_t)y0 * cam.width + x0] : 0;
@@ -459,6 +484,10 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     for (int w = 0; w < warp; ++w) base += s_wsum[w];
     s_bin[t] = base + inc - v;
     if (t == 0) s_bin[256] = 256u;
+#if VSX_BWD_OCC4
+    s_lp[t] = (uint16_t)(base + inc - v);
+    if (t == 0) s_lp[256] = 256;
+#endif
     __syncthreads();
     s_perm[s_bin[key] + r] = (uint8_t)t;
     __syncthreads();
@@ -512,10 +541,19 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     const int f = ln >> 2, p0 = 8 * ks + (ln & 3), p1 = p0 + 4;
     const float v0 = f < 7 ? s_plane[p0 * 9 + f] : 0.f, v1 = f < 7 ? s_plane[p1 * 9 + f] : 0.f;
     const float h0 = __uint_as_float(tf32_rn(v0)), h1 = __uint_as_float(tf32_rn(v1));
+#if VSX_BWD_OCC4
+    (void)h0;
+    (void)h1;
+    s_bw[ks][ln] = make_float2(v0, v1);
+    s_bq[ks][ln] = __floats2half2_rn(pixel_moment(s_perm[p0], f), pixel_moment(s_perm[p1], f));
+#else
     s_bw[ks][ln] = make_float4(h0, h1, __uint_as_float(tf32_rn(v0 - h0)),
                                __uint_as_float(tf32_rn(v1 - h1)));
+#endif
 #if VSX_BWD_SORTPIX
+#if !VSX_BWD_OCC4
     s_bq[ks][ln] = make_float2(pixel_moment(s_perm[p0], f), pixel_moment(s_perm[p1], f));
+#endif
 #else
     s_bq[ks][ln] = make_float2(pixel_moment(p0, f), pixel_moment(p1, f));
 #endif
@@ -595,7 +633,11 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
     // pixel with nc >> 3 < kbase >> 3 (nc <= kbase: dead in this chunk and all
     // earlier ones) sits after the first s_bin[256 - (kbase >> 3)] slots.
     // Phases 1 / 2 only touch the k-steps (8 slots) that cover the prefix.
+#if VSX_BWD_OCC4
+    const int nks = ((int)s_lp[256 - min(kbase >> 3, 255)] + 7) >> 3;
+#else
     const int nks = ((int)s_bin[256 - min(kbase >> 3, 255)] + 7) >> 3;
+#endif
 #else
     const int nks = 32;
 #endif
@@ -711,10 +753,20 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
           const int ks = k0 + kk;
           uint32_t hi[4], lo[4];
           a_frag(ks, hi, lo);
+#if VSX_BWD_OCC4
+          const float2 rb = s_bw[ks][lane];
+          const uint32_t bh0 = tf32_rn(rb.x), bh1 = tf32_rn(rb.y);
+          const uint32_t bl0 = tf32_rn(rb.x - __uint_as_float(bh0));
+          const uint32_t bl1 = tf32_rn(rb.y - __uint_as_float(bh1));
+          mma_m16n8k8_tf32(e1, lo, bh0, bh1);
+          mma_m16n8k8_tf32(e2, hi, bl0, bl1);
+          mma_m16n8k8_tf32(d, hi, bh0, bh1);
+#else
           const float4 b = s_bw[ks][lane];
           mma_m16n8k8_tf32(e1, lo, __float_as_uint(b.x), __float_as_uint(b.y));
           mma_m16n8k8_tf32(e2, hi, __float_as_uint(b.z), __float_as_uint(b.w));
           mma_m16n8k8_tf32(d, hi, __float_as_uint(b.x), __float_as_uint(b.y));
+#endif
         }
       } else {
         // q-plane k-ranges: the staging warp (kr = 3 at kBC = 16) takes 5 of
@@ -735,7 +787,11 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
           const int ks = k0 + kk;
           uint32_t hi[4], lo[4];
           a_frag(ks, hi, lo);
+#if VSX_BWD_OCC4
+          const float2 b = __half22float2(s_bq[ks][lane]);
+#else
           const float2 b = s_bq[ks][lane];
+#endif
           mma_m16n8k8_tf32(e1, lo, __float_as_uint(b.x), __float_as_uint(b.y));
           mma_m16n8k8_tf32(d, hi, __float_as_uint(b.x), __float_as_uint(b.y));
         }
@@ -744,15 +800,20 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? 3 : 2))
       for (int k = 0; k < 4; ++k) d[k] = (e1[k] + e2[k]) + d[k];
       float *red = &s_red[kr][16 * mt + g][8 * plane + 2 * tq];
       *reinterpret_cast<float2 *>(red) = make_float2(d[0], d[1]);
-      *reinterpret_cast<float2 *>(red + 8 * 24) = make_float2(d[2], d[3]);
+      *reinterpret_cast<float2 *>(red + 8 * kRedStride) = make_float2(d[2], d[3]);
     }
 #if VSX_BWD_MERGED
     if (cs > begin) stage(buf ^ 1, chunk_lo(cs), (int)(cs - chunk_lo(cs)));
 #endif
     __syncthreads();
-    // ---- epilogue: 8 lanes per splat, lane part holds features 2part, 2part+1
-    if (t < 8 * kBC) {
-      const int j = t >> 3, part = t & 7;
+    // ---- epilogue: 8 lanes per splat, lane part holds features 2part, 2part+1.
+    // It runs on the LAST 8 kBC threads (warps 4-7 at kBC = 16): with pixels
+    // sorted by live count those warps hold the shortest-lived pixels, so the
+    // epilogue stays off the critical path (warp 0's phase 1 of the next
+    // chunk) instead of delaying it.
+    const int te = VSX_BWD_EPI_HI ? t - (256 - 8 * kBC) : t;
+    if (te >= 0 && te < 8 * kBC) {
+      const int j = te >> 3, part = te & 7;
       float2 v = *reinterpret_cast<const float2 *>(&s_red[0][j][2 * part]);
 #pragma unroll
       for (int k = 1; k < kSplit; ++k) {
