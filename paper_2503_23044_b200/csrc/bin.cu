@@ -207,28 +207,40 @@ __device__ __forceinline__ void warp_diff_to_counts(uint32_t *d, int lane) {
   }
 }
 
+// A CTA takes kRectSub consecutive row-pass chunks of kBinSplats splats:
+// one row histogram per chunk (the row pass's CTA granularity), one pair
+// histogram for all of them.
+constexpr int kRectSub = 4;
+
 __global__ void __launch_bounds__(256) bin_rect_kernel(const vsx_splat *__restrict__ rec,
                                                        const double *__restrict__ radius,
-                                                       int32_t n, int txn, int tyn, BinWs w) {
-  __shared__ uint32_t h[257], hp[257];
+                                                       int32_t n, int txn, int tyn, BinWs w,
+                                                       int chunks) {
+  __shared__ uint32_t h[kRectSub][257], hp[257];
   const int t = threadIdx.x;
-  h[t] = 0u;
+#pragma unroll
+  for (int c = 0; c < kRectSub; ++c) h[c][t] = 0u;
   hp[t] = 0u;
-  if (t == 0) h[256] = hp[256] = 0u;
+  if (t < kRectSub) h[t][256] = 0u;
+  if (t == 0) hp[256] = 0u;
   __syncthreads();
   unsigned long long rows = 0, pairs = 0;
-  for (int k = 0; k < kBinSplats / 256; ++k) {
-    const int i = blockIdx.x * kBinSplats + k * 256 + t;
-    if (i >= n) break;
-    int x0 = 0, x1 = -1, y0 = 1, y1 = 0;
-    if (tile_rect(rec[i].mean2d[0], rec[i].mean2d[1], radius[i], txn, tyn, x0, x1, y0, y1)) {
-      diff_add(h, y0, y1);
-      diff_add(hp, y0, y1, (uint32_t)(x1 - x0 + 1));
-      rows += (unsigned long long)(y1 - y0 + 1);
-      pairs += (unsigned long long)(y1 - y0 + 1) * (unsigned long long)(x1 - x0 + 1);
-      w.rect[i] = make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
-    } else {
-      w.rect[i] = make_uint2(0u, 1u);  // y0 = 1 > y1 = 0: no rows
+  for (int c = 0; c < kRectSub; ++c) {
+    const int chunk = blockIdx.x * kRectSub + c;
+#pragma unroll
+    for (int k = 0; k < kBinSplats / 256; ++k) {
+      const int i = chunk * kBinSplats + k * 256 + t;
+      if (i >= n) break;
+      int x0 = 0, x1 = -1, y0 = 1, y1 = 0;
+      if (tile_rect(rec[i].mean2d[0], rec[i].mean2d[1], radius[i], txn, tyn, x0, x1, y0, y1)) {
+        diff_add(h[c], y0, y1);
+        diff_add(hp, y0, y1, (uint32_t)(x1 - x0 + 1));
+        rows += (unsigned long long)(y1 - y0 + 1);
+        pairs += (unsigned long long)(y1 - y0 + 1) * (unsigned long long)(x1 - x0 + 1);
+        w.rect[i] = make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
+      } else {
+        w.rect[i] = make_uint2(0u, 1u);  // y0 = 1 > y1 = 0: no rows
+      }
     }
   }
 #pragma unroll
@@ -241,11 +253,16 @@ __global__ void __launch_bounds__(256) bin_rect_kernel(const vsx_splat *__restri
     if (pairs) atomicAdd(&w.totals[1], pairs);
   }
   __syncthreads();
-  if (t < 32) warp_diff_to_counts(h, t);
-  else if (t < 64) warp_diff_to_counts(hp, t - 32);
+  const int warp = t >> 5;
+  if (warp < kRectSub) warp_diff_to_counts(h[warp], t & 31);
+  else if (warp == kRectSub) warp_diff_to_counts(hp, t & 31);
   __syncthreads();
   if (t < tyn) {
-    w.mrow[(size_t)blockIdx.x * tyn + t] = h[t];
+#pragma unroll
+    for (int c = 0; c < kRectSub; ++c) {
+      const int chunk = blockIdx.x * kRectSub + c;
+      if (chunk < chunks) w.mrow[(size_t)chunk * tyn + t] = h[c][t];
+    }
     if (hp[t]) atomicAdd(&w.rowpairs[t], hp[t]);
   }
 }
@@ -551,7 +568,9 @@ extern "C" int vsx_bin_plan(const vsx_splat *rec, const double *radius, int32_t 
                                reinterpret_cast<char *>(w.rowstart) -
                                    reinterpret_cast<char *>(w.totals), st));
   if (n > 0) {
-    bin_rect_kernel<<<(int)rect_ctas(n), 256, 0, st>>>(rec, radius, n, txn, tyn, w);
+    const int chunks = (int)rect_ctas(n);
+    bin_rect_kernel<<<(chunks + kRectSub - 1) / kRectSub, 256, 0, st>>>(rec, radius, n, txn, tyn, w,
+                                                                       chunks);
     VSX_LAUNCH_CHECK("bin_rect");
   }
   if (totals) VSX_CUDA_TRY(cudaMemcpyAsync(totals, w.totals, 16, cudaMemcpyDefault, st));
