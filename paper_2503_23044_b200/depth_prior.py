@@ -109,7 +109,8 @@ def fit_scale_shift(depth, view: CameraView, points, valid=None) -> ScaleShiftFi
     raw = torch.empty(n, dtype=torch.float64, device="cuda")
     z = torch.empty(n, dtype=torch.float64, device="cuda")
     ok = torch.empty(n, dtype=torch.uint8, device="cuda")
-    call("vsx_prior_sample", ptr(pts), n, view.to_abi(), ptr(depth_t), ptr(_u8(valid_t)),
+    valid_u8 = _u8(valid_t)   # bound: a temporary would be freed before the kernel reads it
+    call("vsx_prior_sample", ptr(pts), n, view.to_abi(), ptr(depth_t), ptr(valid_u8),
          ptr(raw), ptr(z), ptr(ok), stream())
     projected = int((ok >= 1).sum()) if n else 0
     if projected < MIN_FIT_SAMPLES:
@@ -162,9 +163,11 @@ def reprojection_error(src: AlignedDepthMap, view_src: CameraView, ref: AlignedD
     _check_map(ref, view_ref, "reference")
     acc = out is not None
     err = out if acc else torch.empty(src.values.shape, dtype=torch.float64, device="cuda")
-    call("vsx_reprojection_error", ptr(src.values), ptr(_u8(src.valid)), view_src.to_abi(),
-         ptr(ref.values), ptr(_u8(ref.valid)), view_ref.to_abi(), ptr(err), 1 if acc else 0,
-         stream())
+    # the uint8 masks are bound to names: two temporaries made inside the
+    # argument list would share one recycled block before the kernel runs
+    sv, rv = _u8(src.valid), _u8(ref.valid)
+    call("vsx_reprojection_error", ptr(src.values), ptr(sv), view_src.to_abi(),
+         ptr(ref.values), ptr(rv), view_ref.to_abi(), ptr(err), 1 if acc else 0, stream())
     return err
 
 
@@ -197,7 +200,8 @@ def enhance(src: AlignedDepthMap, view_src: CameraView,
         reprojection_error(src, view_src, ref, view_ref, out=emin)
     vals = torch.empty_like(src.values)
     ov = torch.empty(src.values.shape, dtype=torch.uint8, device="cuda")
-    call("vsx_enhance_finalize", ptr(src.values), ptr(_u8(src.valid)), ptr(emin), float(tau),
+    sv = _u8(src.valid)
+    call("vsx_enhance_finalize", ptr(src.values), ptr(sv), ptr(emin), float(tau),
          src.values.numel(), ptr(vals), ptr(ov), stream())
     return EnhancedDepthMap(values=vals, valid=ov.bool(), min_roundtrip=emin, tau=float(tau))
 

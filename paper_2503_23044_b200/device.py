@@ -101,7 +101,8 @@ def sort_z_gid(z: torch.Tensor, gid: torch.Tensor) -> torch.Tensor:
         return order[:0].long()
     lib = _lib.load()
     wp, wb = workspace().get(lib.vsx_sort_z_gid_ws_bytes(n))
-    call("vsx_sort_z_gid", ptr(z.contiguous()), ptr(gid.contiguous()), ptr(order), n, wp, wb,
+    z, gid = z.contiguous(), gid.contiguous()   # bound for the kernel's lifetime
+    call("vsx_sort_z_gid", ptr(z), ptr(gid), ptr(order), n, wp, wb,
          stream())
     return order.long()
 

@@ -212,18 +212,17 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     B = len(views)
     w2, w3, wn = backend.schedule()
-    if w3 > 0 and B >= 2:
-        # Eq. 10 couples views that different ranks render (losses.py:196-287);
-        # the sharded step does not exchange rendered buffers, so it refuses
-        # rather than silently training a different objective
-        raise InvalidInput("the sharded step does not implement the Eq. 10 multi-view NCC term "
-                           "(w3 > 0); use trainer.train_step or step3_start >= total_steps")
+    use_geo = w3 > 0 and B >= 2
+    if use_geo and not hasattr(backend, "band_forward"):
+        # Eq. 10 couples views that different ranks render (losses.py:196-287)
+        raise InvalidInput("the Eq. 10 multi-view NCC term (w3 > 0) needs the two-phase "
+                           "sharded step (CudaShardBackend)")
     # the depth / normal terms average over the views that carry a prior
     # (trainer.py:296-306, losses.py:84), a global property of the batch
     have = [v for v in range(B) if w2 > 0 and priors is not None and priors[v] is not None]
     have_n = [v for v in range(B)
               if wn > 0 and normal_priors is not None and normal_priors[v] is not None]
-    banded = B < world
+    banded = B < world or use_geo
     if banded:
         # fewer views than ranks: every view is split into tile-row bands, one
         # work item each, dealt round-robin over the ranks (SURVEY §8(e) step
@@ -232,10 +231,17 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
         if not hasattr(backend, "band_forward"):
             raise InvalidInput("a batch with fewer views than ranks needs tile bands "
                                "(CudaShardBackend)")
-        S = -(-world // B)
-        bands = {v: backend.band_rows(views[v], S) for v in range(B)}
-        items = [(v, b) for v in range(B) for b in range(len(bands[v]))]
-        item_rend = np.arange(len(items), dtype=np.int64) % world
+        if B < world:
+            S = -(-world // B)
+            bands = {v: backend.band_rows(views[v], S) for v in range(B)}
+            items = [(v, b) for v in range(B) for b in range(len(bands[v]))]
+            item_rend = np.arange(len(items), dtype=np.int64) % world
+        else:
+            # whole views (one band each) on their round-robin renderers: the
+            # two-phase path only for the NCC term's exchange of renders
+            bands = {v: [(0, (views[v].height + 15) // 16)] for v in range(B)}
+            items = [(v, 0) for v in range(B)]
+            item_rend = np.asarray([renderer_of(v, world) for v in range(B)], dtype=np.int64)
         renderers = np.asarray([renderer_of(v, world) for v in range(B)], dtype=np.int64)
         mine = {v for (v, _), r in zip(items, item_rend) if int(r) == rank}
     else:
@@ -255,7 +261,7 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
         images, priors, normal_priors = _StagedInputs(stager, B)
     if banded:
         timers = _banded_views(backend, views, images, priors, normal_priors, group, rank, world,
-                               bands, items, item_rend)
+                               bands, items, item_rend, use_geo)
     elif hasattr(backend, "prepare") and _pipeline_enabled():
         timers = _pipelined_views(backend, views, images, priors, normal_priors, group,
                                   renderers, rank, world)
@@ -295,7 +301,7 @@ def sharded_train_step(backend, views, images, priors=None, normal_priors=None, 
 
 
 def _banded_views(backend, views, images, priors, normal_priors, group, rank, world, bands,
-                  items, item_rend) -> dict:
+                  items, item_rend, use_geo=False) -> dict:
     """The sharded step with views split into tile-row bands (B < M).
 
     Owners run their shard's front end once per view; C1 sends every band's
@@ -324,6 +330,10 @@ def _banded_views(backend, views, images, priors, normal_priors, group, rank, wo
         backend.band_forward(it, v, views[v], work, images[v],
                              None if priors is None else priors[v],
                              None if normal_priors is None else normal_priors[v], bands[v][b])
+    geo = None
+    if use_geo:
+        geo = _exchange_renders_and_geo(backend, views, items, item_rend, bands, rank, group)
+        backend.geo = geo
     local = backend.icounts.clone()
     tot = local.clone()
     dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=group)
@@ -331,7 +341,8 @@ def _banded_views(backend, views, images, priors, normal_priors, group, rank, wo
     vt = torch.zeros((B, 2), dtype=tot.dtype, device=tot.device).index_add_(0, item_view, tot)
     for it in merged:
         backend.icounts[it].copy_(vt[items[it][0]])
-    grads = {it: backend.band_backward(it) for it in merged}
+    grads = {it: backend.band_backward(it, None if geo is None else geo[2].get(items[it][0]))
+             for it in merged}
     like = backend.grad_like()
     back = return_grads(plan, grads, like, group)
     for v in range(B):
@@ -345,6 +356,44 @@ def _banded_views(backend, views, images, priors, normal_priors, group, rank, wo
     backend.sums.index_add_(0, item_view, backend.isums)
     backend.counts.index_add_(0, item_view, local)
     return {}
+
+
+def _exchange_renders_and_geo(backend, views, items, item_rend, bands, rank, group):
+    """All views' renders on every rank (each rank contributes the rows it
+    composited, one all-reduce SUM), then the Eq. 10 value and cotangents,
+    identical on every rank. Returns (value, stats, cot)."""
+    from types import SimpleNamespace
+    from .losses import geo_loss_cotangents
+    dev = "cuda"
+    full = []
+    for v, view in enumerate(views):
+        H, W = view.height, view.width
+        full.append(torch.zeros((H, W, 9), dtype=torch.float32, device=dev))
+    for it, (_work, view, _loss, _keep, R) in backend.pending.items():
+        v, b = items[it]
+        r0, nr = bands[v][b]
+        y0, y1 = 16 * r0, min(view.height, 16 * (r0 + nr))
+        f = full[v]
+        f[y0:y1, :, 0:3] = R.rgb[y0:y1]
+        f[y0:y1, :, 3:6] = R.normal[y0:y1]
+        f[y0:y1, :, 6] = R.depth[y0:y1]
+        f[y0:y1, :, 7] = R.alpha[y0:y1]
+        f[y0:y1, :, 8] = R.valid[y0:y1].float()
+    flat = torch.cat([f.reshape(-1) for f in full])
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    tg, off = [], 0
+    for v, view in enumerate(views):
+        n = view.height * view.width * 9
+        f = flat[off:off + n].view(view.height, view.width, 9)
+        off += n
+        tg.append(SimpleNamespace(rgb=f[..., 0:3].contiguous(), normal=f[..., 3:6].contiguous(),
+                                  depth=f[..., 6].contiguous(), alpha=f[..., 7].contiguous(),
+                                  valid=f[..., 8] > 0.5))
+    st = backend.state
+    _w2, w3, _wn = backend.schedule()
+    g_loss, gstats, cot = geo_loss_cotangents(tg, views, st.rng, patch_count=st.cfg.geo_patches,
+                                              half=st.cfg.geo_patch_half, upstream=w3)
+    return float(g_loss), gstats, cot
 
 
 def _c2_sum(t: torch.Tensor, group, ordered: bool) -> None:
@@ -595,6 +644,7 @@ class CudaShardBackend:
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.work.clear()
         self.gaussians = 0
+        self.geo = None
         # decoder weight image of this step's weights, shared by every view
         self._dimg = (self.D.decoder_image(st.params.abi(), st.n)
                       if self.D.use_tensor_cores(st.n) else None)
@@ -754,9 +804,17 @@ class CudaShardBackend:
         R = D.raster_forward(P, Bn, view, loss=loss, deterministic=det)
         self.pending[it] = (work, view, loss, keep, R)
 
-    def band_backward(self, it: int) -> torch.Tensor:
+    def band_backward(self, it: int, extra=None) -> torch.Tensor:
+        """The band's backward; ``extra`` = the view's NCC cotangents (rgb,
+        normal, depth images) or None."""
+        from ._lib import ptr
         D, st = self.D, self.state
         (P, Bn, order), view, loss, keep, R = self.pending.pop(it)
+        if extra is not None:
+            ex_rgb, ex_nrm, ex_dep = extra
+            loss.extra_rgb, loss.extra_normal = ptr(ex_rgb).value, ptr(ex_nrm).value
+            loss.extra_depth = ptr(ex_dep).value
+            keep = (keep, extra)
         det = bool(getattr(st.cfg, "deterministic", False))
         gs = D.raster_backward(P, Bn, view, R, loss=loss, deterministic=det)
         merged = torch.empty_like(gs)
@@ -804,13 +862,19 @@ class CudaShardBackend:
         nterm = np.where(ncnt > 0, L[:, 2] / (3 * np.maximum(ncnt, 1)), 0.0)
         depth = float(np.mean(dterm[self.have])) if self.have else 0.0
         normal = float(np.mean(nterm[self.have_n])) if self.have_n else 0.0
-        total = rgb + w2 * depth + float(getattr(st.cfg, "normal_weight", 0.0)) * normal
+        w3 = weight_schedule(st.step, st.cfg)[1]
+        geo = self.geo[0] if self.geo is not None else 0.0
+        total = rgb + w2 * depth + float(getattr(st.cfg, "normal_weight", 0.0)) * normal + \
+            w3 * geo
         if not np.isfinite(total):
             raise NumericalError(f"non-finite loss at step {st.step}")
         st.adam()
         st.step += 1
-        return {"total": total, "rgb": rgb, "depth": depth, "normal": normal,
-                "gaussians": self.gaussians}
+        out = {"total": total, "rgb": rgb, "depth": depth, "normal": normal, "geo": geo,
+               "gaussians": self.gaussians}
+        if self.geo is not None:
+            out["geo_pairs"], out["geo_patches"] = self.geo[1].pairs_used, self.geo[1].patches_used
+        return out
 
     def decoder_checksum(self) -> torch.Tensor:
         g = self.state.flat

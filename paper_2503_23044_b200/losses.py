@@ -211,10 +211,15 @@ def geo_loss_cotangents(targets: list, views: list, rng: np.random.Generator,
                "g_dep": torch.empty(P, dtype=torch.float64, device=dev),
                "sum": torch.zeros(1, dtype=torch.float64, device=dev),
                "used": torch.zeros(1, dtype=torch.int32, device=dev)}
+        # operands bound to names: a temporary made inside the call's argument
+        # list would be freed (and its block reused by the next temporary)
+        # before the kernel reads it
         srgb = src.rgb.detach().float().contiguous()
-        call("vsx_ncc_patches", ptr(srgb), ptr(src.normal.detach().float().contiguous()),
-             ptr(src.depth.detach().float().contiguous()), w, h,
-             ptr(ref.rgb.detach().float().contiguous()), vr.width, vr.height, _ncc_geom(vs, vr),
+        snrm = src.normal.detach().float().contiguous()
+        sdep = src.depth.detach().float().contiguous()
+        rrgb = ref.rgb.detach().float().contiguous()
+        call("vsx_ncc_patches", ptr(srgb), ptr(snrm), ptr(sdep), w, h,
+             ptr(rrgb), vr.width, vr.height, _ncc_geom(vs, vr),
              ptr(cen), P, half, ptr(rec["term"]), ptr(rec["status"]), ptr(rec["g_patch"]),
              ptr(rec["g_n"]), ptr(rec["g_dep"]), ptr(rec["sum"]), ptr(rec["used"]),
              ptr(pairs_used), stream())

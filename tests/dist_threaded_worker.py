@@ -30,6 +30,7 @@ from paper_2503_23044_b200.trainer import TrainConfig, TrainState, train_step  #
 
 WORLD = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 NV = int(sys.argv[2]) if len(sys.argv) > 2 else 3   # views; < WORLD splits views into bands
+GEO = len(sys.argv) > 3 and sys.argv[3] == "geo"    # Eq. 10 NCC term from step 1 on
 STEPS = 2
 d = load_golden("train_small")
 views = [golden_view(d, f"v{i}", i) for i in range(3)]
@@ -47,8 +48,8 @@ if NV < 3:
     views, images = views[:NV], images[:NV]
     priors = [priors[0], None][:NV]
     npri = [None, npri[1]][:NV]
-cfg = dict(total_steps=8, batch_size=NV, step2_start=0, step3_start=8, growth_stop=0,
-           normal_weight=0.5)
+cfg = dict(total_steps=8, batch_size=NV, step2_start=0, step3_start=0 if GEO else 8,
+           growth_stop=0, normal_weight=0.5)
 
 import faulthandler  # noqa: E402
 faulthandler.dump_traceback_later(150, exit=True)  # a hang prints every thread's stack
@@ -114,6 +115,8 @@ for s in range(STEPS):
         rb = res[r]["reps"][s]
         out["loss"].append([s, r, rb["rgb"], ref_reps[s].rgb, rb["depth"], ref_reps[s].depth,
                             rb["normal"], ref_reps[s].normal])
+        out.setdefault("geo", []).append([s, r, rb.get("geo", 0.0), ref_reps[s].geo,
+                                          rb.get("geo_pairs", 0), ref_reps[s].geo_pairs])
 owner = res[0]["state"].assignment.flat_owner()
 out["owned_disjoint"] = bool(np.array_equal(np.bincount(owner, minlength=WORLD) > 0,
                                             np.ones(WORLD, bool)))

@@ -62,8 +62,9 @@ def test_sharded_step_world1_matches_train_step(nccl_world1, train_small):
     assert torch.equal(a.flat.param, b.flat.param)
 
 
-@pytest.mark.parametrize("world,nv", [(2, 3), (4, 3), (4, 2), (3, 2)])
-def test_sharded_step_threaded_ranks_match_train_step(world, nv):
+@pytest.mark.parametrize("world,nv,geo", [(2, 3, False), (4, 3, False), (4, 2, False),
+                                         (3, 2, False), (2, 3, True), (4, 2, True)])
+def test_sharded_step_threaded_ranks_match_train_step(world, nv, geo):
     """World size 2 and 4 on one GPU: threads of one process joined by
     torch's in-process process group (host-side collectives, no cross-rank
     kernel waits). Losses on every rank and the owner-merged anchor
@@ -75,14 +76,16 @@ def test_sharded_step_threaded_ranks_match_train_step(world, nv):
     views, 3 ranks / 2 views) every view is split into tile-row bands
     rendered on different ranks: the per-view valid-pixel counts are summed
     over the bands before the backward, and owners add each splat's band
-    gradients."""
+    gradients. With the Eq. 10 NCC term (w3 > 0 from step 1) every rank
+    receives all renders and evaluates the term with the same RNG draws:
+    the term's value and pair count match train_step's on every rank."""
     import json
     import subprocess
     import sys
     from pathlib import Path
     here = Path(__file__).resolve().parent
     p = subprocess.run([sys.executable, str(here / "dist_threaded_worker.py"), str(world),
-                        str(nv)],
+                        str(nv)] + (["geo"] if geo else []),
                        capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
     out = json.loads(p.stdout.strip().splitlines()[-1])
@@ -91,6 +94,11 @@ def test_sharded_step_threaded_ranks_match_train_step(world, nv):
         assert rgb == pytest.approx(ref_rgb, rel=1e-6), (s, r)
         assert dep == pytest.approx(ref_dep, rel=1e-5), (s, r)
         assert nrm == pytest.approx(ref_nrm, rel=1e-5), (s, r)
+    for s, r, g, ref_g, gp, ref_gp in out["geo"]:
+        assert gp == ref_gp, (s, r)
+        assert g == pytest.approx(ref_g, rel=1e-5, abs=1e-9), (s, r)
+    if geo:
+        assert any(g > 0 for _, _, g, _, _, _ in out["geo"])
     # growth pressure accumulated by the owners, summed over ranks = train_step's
     assert out["growth_nonzero"] and out["growth_ok"]
     # element-wise: within 1e-5 rel, except near-zero-gradient Adam sign flips
