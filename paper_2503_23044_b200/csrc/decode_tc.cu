@@ -358,6 +358,174 @@ __global__ void __launch_bounds__(256) decode_gauss_kernel(
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(status, VSX_STATUS_NONFINITE);
 }
 
+// Resident-weight version (the default forward): W1 of all three heads
+// ([192 x 40], one N = 192 MMA chain for the first layer) and W2 ([NP x 64])
+// stay in shared memory for the CTA's lifetime, so a tile never copies
+// weights; the hidden layer is fed to the second GEMM in two K halves of 32
+// (the half tile is 32 KB, which keeps everything in 200 KB), and both
+// warpgroups share every epilogue (thread row = tid % 128, columns split).
+// TMEM: first-layer accumulators in columns [0, 192), second-layer head h at
+// 192 + row0[h].
+constexpr int kTcKH = 32;  // hidden columns per second-layer K half
+
+__global__ void __launch_bounds__(256, 1) decode_fwd_tc2_kernel(
+    vsx_decoder W, const float *__restrict__ img, const int32_t *__restrict__ active,
+    int32_t n_active, const double *__restrict__ centers, const float *__restrict__ emb,
+    vsx_camera cam, double lod_ref, float *__restrict__ cache_h, float *__restrict__ cache_o) {
+  extern __shared__ __align__(1024) float tsm[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tslot;
+  __shared__ float s_b2[11 * 13];
+  const int n = W.n;
+  const TcDims dims = tc_dims(n);
+  float *x_hi = tsm, *x_lo = x_hi + kTcRows * kTcK1;
+  float *w1_hi = x_lo + kTcRows * kTcK1, *w1_lo = w1_hi + 192 * kTcK1;
+  float *h_hi = w1_lo + 192 * kTcK1, *h_lo = h_hi + kTcRows * kTcKH;
+  float *w2_hi = h_lo + kTcRows * kTcKH, *w2_lo = w2_hi + dims.np_total * kTcK2;
+  const int tid = threadIdx.x, t = tid & 127, wg = tid >> 7, warp = (tid >> 5) & 3;
+  {
+    // W1: the image holds (hi, lo) per head; the N = 192 operand wants the
+    // three hi tiles back to back, then the three lo tiles
+    const int tile4 = 64 * kTcK1 / 4;
+    for (int i = tid; i < 3 * 2 * tile4; i += 256) {
+      const int h = i / (2 * tile4), part = (i / tile4) & 1, e = i % tile4;
+      float4 *dst = reinterpret_cast<float4 *>(part ? w1_lo : w1_hi) + h * tile4 + e;
+      *dst = reinterpret_cast<const float4 *>(img)[i];
+    }
+    const float4 *src = reinterpret_cast<const float4 *>(img + 3 * 2 * 64 * kTcK1);
+    float4 *dst = reinterpret_cast<float4 *>(w2_hi);
+    const int n4 = 2 * dims.np_total * kTcK2 / 4;
+    for (int i = tid; i < n4; i += 256) dst[i] = src[i];
+  }
+  for (int j = tid; j < 11 * n; j += 256)
+    s_b2[j] = j < n ? W.b2[0][j] : (j < 4 * n ? W.b2[1][j - n] : W.b2[2][j - 4 * n]);
+  if (tid < 32) umma::tmem_alloc(&tslot, 512);
+  if (tid == 0) umma::mbar_init(&mbar, 1);
+  umma::fence_async_smem();
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tbase = tslot;
+  const uint32_t lane = (uint32_t)(warp * 32) << 16;
+  const uint32_t d1 = tbase, d2 = tbase + 192;
+  uint32_t phase = 0;
+  const int n_tiles = (n_active + kTcRows - 1) / kTcRows;
+  const size_t ld = cache_ld(n_active);
+  auto sync_mma = [&]() {  // smem writes -> tensor core, all threads
+    umma::fence_async_smem();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+  };
+  auto wait_mma = [&]() {
+    umma::mbar_wait(&mbar, phase);
+    phase ^= 1u;
+    umma::fence_after_sync();
+  };
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int r = tile * kTcRows + t;
+    const bool valid = r < n_active;
+    // ---- input block (decoder.py:142-147) + bias column, split into X
+    if (wg == 0) {
+      float x[kTcK1];
+#pragma unroll
+      for (int i = 0; i < kTcK1; ++i) x[i] = 0.f;
+      if (valid) {
+        const int a = active[r];
+        const double rx = dsub(centers[3 * a + 0], cam.center[0]);
+        const double ry = dsub(centers[3 * a + 1], cam.center[1]);
+        const double rz = dsub(centers[3 * a + 2], cam.center[2]);
+        const double dd = fmax(sqrt(dadd(dadd(dmul(rx, rx), dmul(ry, ry)), dmul(rz, rz))), 1e-12);
+        const float4 *e4 = reinterpret_cast<const float4 *>(emb + (size_t)a * kEmbed);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = e4[q];
+          x[4 * q] = v.x;
+          x[4 * q + 1] = v.y;
+          x[4 * q + 2] = v.z;
+          x[4 * q + 3] = v.w;
+        }
+        x[32] = (float)ddiv(dd, lod_ref);
+        x[33] = (float)ddiv(rx, dd);
+        x[34] = (float)ddiv(ry, dd);
+        x[35] = (float)ddiv(rz, dd);
+        x[36] = 1.f;
+      }
+#pragma unroll
+      for (int q = 0; q < kTcK1 / 4; ++q)
+        st_split4(x_hi, x_lo, umma::kmajor_offset(t, 4 * q, kTcK1), x[4 * q], x[4 * q + 1],
+                  x[4 * q + 2], x[4 * q + 3]);
+    }
+    sync_mma();
+    if (tid == 0) {  // first layer of all three heads: N = 192
+      mma3(d1, x_hi, x_lo, w1_hi, w1_lo, kTcK1, umma::idesc_tf32(128, 192));
+      umma::commit(&mbar);
+    }
+    wait_mma();
+    for (int h = 0; h < 3; ++h) {
+      for (int kh = 0; kh < 2; ++kh) {
+        // hidden columns 32 kh .. 32 kh + 31 of head h: warpgroup wg takes 16
+        const int c0 = kTcKH * kh + 16 * wg;
+        float v[16];
+        umma::tmem_ld16(d1 + lane + (uint32_t)(64 * h + c0), v);
+        umma::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          v[i] = tanh_fast(v[i]);
+          if (valid && cache_h) cache_h[(size_t)(h * 64 + c0 + i) * ld + r] = v[i];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          st_split4(h_hi, h_lo, umma::kmajor_offset(t, 16 * wg + 4 * q, kTcKH), v[4 * q],
+                    v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        sync_mma();
+        if (tid == 0) {
+          const uint32_t ah = umma::smem_addr(h_hi), al = umma::smem_addr(h_lo);
+          const uint32_t boff = (uint32_t)(dims.row0[h] * kTcK2 * 4) + (uint32_t)kh * 4 * 256;
+          const uint32_t bh = umma::smem_addr(w2_hi) + boff, bl = umma::smem_addr(w2_lo) + boff;
+          const uint32_t id = umma::idesc_tf32(128, dims.np[h]);
+          const uint32_t dd2 = d2 + (uint32_t)dims.row0[h];
+          for (int st = 0; st < kTcKH / 8; ++st) {
+            const uint32_t oa = (uint32_t)st * 256;
+            using umma::desc_kmajor;
+            const bool acc = kh > 0 || st > 0;
+            umma::mma_tf32(dd2, desc_kmajor(ah + oa, kTcKH), desc_kmajor(bh + oa, kTcK2), id, acc);
+            umma::mma_tf32(dd2, desc_kmajor(al + oa, kTcKH), desc_kmajor(bh + oa, kTcK2), id, true);
+            umma::mma_tf32(dd2, desc_kmajor(ah + oa, kTcKH), desc_kmajor(bl + oa, kTcK2), id, true);
+          }
+          umma::commit(&mbar);
+        }
+        wait_mma();  // the half tile is rewritten next
+      }
+      // raw head outputs (+ b2) -> cache_o
+      const int width = (h == 0 ? 1 : (h == 1 ? 3 : 7)) * n;
+      const int oo = h == 0 ? 0 : (h == 1 ? n : 4 * n);
+      for (int c = 16 * wg; c < dims.np[h]; c += 32) {
+        float v[16];
+        umma::tmem_ld16(d2 + lane + (uint32_t)(dims.row0[h] + c), v);
+        umma::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int j = c + i;
+          if (valid && j < width) cache_o[(size_t)(oo + j) * ld + r] = v[i] + s_b2[oo + j];
+        }
+      }
+    }
+    umma::fence_before_sync();
+    __syncthreads();  // TMEM columns are rewritten by the next tile
+    umma::fence_after_sync();
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (tid < 32) umma::tmem_dealloc(tbase, 512);
+}
+
+size_t tc2_smem_bytes(int n) {
+  const TcDims d = tc_dims(n);
+  return sizeof(float) * ((size_t)2 * kTcRows * kTcK1 + 2 * 192 * kTcK1 + 2 * kTcRows * kTcKH +
+                          (size_t)2 * d.np_total * kTcK2);
+}
+
 // ---------------------------------------------------------------- weight gradients
 //
 // All decoder weight gradients of one view as two K-split tcgen05 GEMMs over
@@ -715,14 +883,31 @@ extern "C" int vsx_decode_fwd_tc(vsx_decoder W, const float *img, const int32_t 
   if (n_active == 0) return VSX_OK;
   // VSX_DECODE_FWD=tcgen05 selects the tcgen05 MLP (A/B); default is the
   // warp-per-16-anchors mma.sync kernel (falls back for large n)
-  static const bool use_tcgen05 = [] {
+  // VSX_DECODE_FWD: "tc2" = resident-weight tcgen05 MLP, "tcgen05" = the
+  // per-tile-copy tcgen05 MLP (A/B); default: the warp-per-16-anchors mma.sync
+  static const int fwd_impl = [] {
     const char *e = getenv("VSX_DECODE_FWD");
-    return e && e[0] == 't';
+    if (!e) return 0;
+    if (e[0] == 't' && e[1] == 'c' && e[2] == '2') return 2;
+    return e[0] == 't' ? 1 : 0;
   }();
   int rc = 1;
-  if (!use_tcgen05)
+  if (fwd_impl == 2 && tc2_smem_bytes(W.n) <= 227 * 1024) {
+    const size_t smem = tc2_smem_bytes(W.n);
+    VSX_CUDA_TRY(cudaFuncSetAttribute(decode_fwd_tc2_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = (n_active + kTcRows - 1) / kTcRows;
+    decode_fwd_tc2_kernel<<<std::min(tiles, sms), 256, smem, as_stream(s)>>>(
+        W, img, active, n_active, centers, emb, cam, lod_ref, cache_h, cache_o);
+    VSX_LAUNCH_CHECK("decode_fwd_tc2");
+    rc = 0;
+  } else if (fwd_impl == 0) {
     rc = decode_fwd_mma(W, img + mma_image_offset(W.n), active, n_active, centers, emb, cam,
                         lod_ref, cache_h, cache_o, as_stream(s));
+  }
   if (rc < 0) return rc;
   if (rc == 1) {
     const size_t smem = tc_smem_bytes(W.n);
