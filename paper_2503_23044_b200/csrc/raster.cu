@@ -304,6 +304,132 @@ __global__ void __launch_bounds__(256 / PX) raster_fwd2_kernel(
                  out_raw, out_valid, out_T, out_nc, L);
 }
 
+// Packed-pair forward: the same algorithm as raster_fwd2_kernel<2, U> with
+// the two pixels of a thread held as float2 lanes and advanced with the
+// sm_100 paired FP32 instructions (FFMA2 / FMUL2 / FADD2; the staged splat
+// value is the broadcast operand). Every lane performs the scalar kernel's
+// operations with the same roundings (fma / mul / add are each correctly
+// rounded), so alpha and T agree bit for bit with the backward's recompute.
+// The kernel was issue-bound at 84% with 26 instructions per (pixel, splat)
+// (profiles/r02_raster_final_ncu.txt); pairing removes about a third.
+#ifndef VSX_FWD_PACKED
+#define VSX_FWD_PACKED 1
+#endif
+__device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
+
+struct FwdPair {
+  float2 T = {1.f, 1.f}, acc = {0.f, 0.f}, c0 = {0.f, 0.f}, c1 = {0.f, 0.f}, c2 = {0.f, 0.f},
+         n0 = {0.f, 0.f}, n1 = {0.f, 0.f}, n2 = {0.f, 0.f}, dist = {0.f, 0.f};
+  // 1 + the chunk index of the last splat blended while live (T only
+  // decreases, so the live splats are a prefix): one select per lane
+  int32_t nl0 = 0, nl1 = 0;
+  __device__ __forceinline__ void blend_if_live(float2 al, const float4 &p2, const float4 &p3,
+                                                float pd, int32_t idx1) {
+    const bool l0 = T.x >= kEarlyStopT, l1 = T.y >= kEarlyStopT;
+    const float2 m = make_float2(l0 ? al.x : 0.f, l1 ? al.y : 0.f);
+    const float2 w = __fmul2_rn(m, T);
+    acc = __fadd2_rn(acc, w);
+    c0 = __ffma2_rn(w, bc2(p2.x), c0);
+    c1 = __ffma2_rn(w, bc2(p2.y), c1);
+    c2 = __ffma2_rn(w, bc2(p2.z), c2);
+    n0 = __ffma2_rn(w, bc2(p3.x), n0);
+    n1 = __ffma2_rn(w, bc2(p3.y), n1);
+    n2 = __ffma2_rn(w, bc2(p3.z), n2);
+    dist = __ffma2_rn(w, bc2(pd), dist);
+    T = __ffma2_rn(make_float2(-m.x, -m.y), T, T);
+    nl0 = l0 ? idx1 : nl0;
+    nl1 = l1 ? idx1 : nl1;
+  }
+};
+
+__device__ __forceinline__ float2 falloff_alpha2(const float4 &p0, const float4 &p1, float2 fx,
+                                                 float cy, float cyy) {
+  const float2 dx = __fadd2_rn(fx, bc2(-p0.x));
+  const float2 q = __ffma2_rn(bc2(p0.z), dx, bc2(cy));
+  const float2 p = __ffma2_rn(q, dx, bc2(cyy));
+  const float2 e = make_float2(ex2_ftz(fminf(p.x, 0.f)), ex2_ftz(fminf(p.y, 0.f)));
+  const float2 a = __fmul2_rn(bc2(p1.y), e);
+  return make_float2(fminf(a.x, 0.99f), fminf(a.y, 0.99f));
+}
+
+#ifndef VSX_FWD_PK_MINB
+#define VSX_FWD_PK_MINB 1
+#endif
+template <int U, bool kDet>
+__global__ void __launch_bounds__(128, VSX_FWD_PK_MINB) raster_fwd_pk_kernel(
+    const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
+    const uint32_t *__restrict__ tile_list, vsx_camera cam, float *__restrict__ out_rgb,
+    float *__restrict__ out_alpha, float *__restrict__ out_depth, float *__restrict__ out_normal,
+    float *__restrict__ out_raw, uint8_t *__restrict__ out_valid, float *__restrict__ out_T,
+    int32_t *__restrict__ out_nc, vsx_loss_desc L) {
+  constexpr int kThreads = 128, kRowThreads = kTile / 2;
+  __shared__ float4 s0[kChunk], s1[kChunk], s2[kChunk], s3[kChunk];
+  const int txn = gridDim.x;
+  const int by = (int)blockIdx.y + L.tile_row0;
+  const int tile = by * txn + blockIdx.x;
+  const int lx = 2 * (threadIdx.x % kRowThreads), ly = threadIdx.x / kRowThreads;
+  const int px = blockIdx.x * kTile + lx, py = by * kTile + ly;
+  const double ox = (double)(blockIdx.x * kTile), oy = (double)(by * kTile);
+  const uint32_t begin = tile_off[tile], end = tile_off[tile + 1];
+  const float fy = (float)ly;
+  const float2 fx = make_float2((float)lx, (float)(lx + 1));
+  const bool in0 = px < cam.width && py < cam.height, in1 = px + 1 < cam.width && py < cam.height;
+  bool done0 = !in0, done1 = !in1;
+  int32_t nc0 = 0, nc1 = 0;
+  FwdPair A;
+  for (uint32_t cs = begin; cs < end; cs += kChunk) {
+    if (__syncthreads_count(!(done0 && done1)) == 0) break;
+#pragma unroll
+    for (int h = 0; h < kChunk / kThreads; ++h) {
+      const int k = threadIdx.x + kThreads * h;
+      const uint32_t idx = cs + k;
+      if (idx < end) {
+        const vsx_splat sp = load_splat(rec, tile_list[idx]);
+        stage_splat(sp, ox, oy, s0[k], s1[k], s2[k], s3[k]);
+      }
+    }
+    __syncthreads();
+    const int cnt = (int)min((uint32_t)kChunk, end - cs);
+    if (!(done0 && done1)) {
+      A.nl0 = A.nl1 = 0;
+      int j = 0;
+      for (; j + U <= cnt && fmaxf(A.T.x, A.T.y) >= kEarlyStopT; j += U) {
+        float2 al[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float4 p0 = s0[j + u], p1 = s1[j + u];
+          const float dy = fy - p0.y;
+          const float cy = __fmul_rn(p0.w, dy), cyy = __fmul_rn(__fmul_rn(p1.x, dy), dy);
+          al[u] = falloff_alpha2(p0, p1, fx, cy, cyy);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          A.blend_if_live(al[u], s2[j + u], s3[j + u], s1[j + u].z, j + u + 1);
+      }
+      for (; j < cnt && fmaxf(A.T.x, A.T.y) >= kEarlyStopT; ++j) {
+        const float4 p0 = s0[j], p1 = s1[j];
+        const float dy = fy - p0.y;
+        const float cy = __fmul_rn(p0.w, dy), cyy = __fmul_rn(__fmul_rn(p1.x, dy), dy);
+        A.blend_if_live(falloff_alpha2(p0, p1, fx, cy, cyy), s2[j], s3[j], p1.z, j + 1);
+      }
+      if (!done0) {
+        nc0 = (int32_t)(cs - begin) + A.nl0;
+        done0 = A.T.x < kEarlyStopT;
+      }
+      if (!done1) {
+        nc1 = (int32_t)(cs - begin) + A.nl1;
+        done1 = A.T.y < kEarlyStopT;
+      }
+    }
+  }
+  fwd_epilogue<kDet>(cam, in0, px, py, A.acc.x, A.c0.x, A.c1.x, A.c2.x, A.n0.x, A.n1.x, A.n2.x,
+                     A.dist.x, A.T.x, nc0, out_rgb, out_alpha, out_depth, out_normal, out_raw,
+                     out_valid, out_T, out_nc, L);
+  fwd_epilogue<kDet>(cam, in1, px + 1, py, A.acc.y, A.c0.y, A.c1.y, A.c2.y, A.n0.y, A.n1.y,
+                     A.n2.y, A.dist.y, A.T.y, nc1, out_rgb, out_alpha, out_depth, out_normal,
+                     out_raw, out_valid, out_T, out_nc, L);
+}
+
 __device__ __forceinline__ void mma_m16n8k8_tf32(float (&d)[4], const uint32_t (&a)[4],
                                                  uint32_t b0, uint32_t b1) {
   asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
@@ -401,13 +527,106 @@ __device__ __forceinline__ float pixel_moment(int p, int m) {
   }
 }
 
+// Phase 1 on splat pairs: the alphas of splats 2i and 2i + 1 are evaluated
+// as the two lanes of paired FP32 instructions (FFMA2 / FMUL2 / FADD2) from
+// the pair-interleaved staging sP; the T / S recursion stays sequential
+// (T_2i+1 first, back to front). Per lane the operations and roundings are
+// the scalar ones (splat_alpha), so alpha and T agree bit for bit with the
+// forward. Writes w and q of rows [0, jlive) of this thread's plane column.
+#ifndef VSX_BWD_PK
+#define VSX_BWD_PK 1
+#endif
+__device__ __forceinline__ void pair_alpha(const float4 (&P)[3], float fx, float fy, float2 &al,
+                                           float2 &e, float2 &at) {
+  const float2 dx = __fadd2_rn(bc2(fx), make_float2(P[0].x, P[0].y));
+  const float2 dy = __fadd2_rn(bc2(fy), make_float2(P[0].z, P[0].w));
+  const float2 cy = __fmul2_rn(make_float2(P[1].z, P[1].w), dy);
+  const float2 cyy = __fmul2_rn(__fmul2_rn(make_float2(P[2].x, P[2].y), dy), dy);
+  const float2 q = __ffma2_rn(make_float2(P[1].x, P[1].y), dx, cy);
+  const float2 p = __ffma2_rn(q, dx, cyy);
+  e = make_float2(ex2_ftz(fminf(p.x, 0.f)), ex2_ftz(fminf(p.y, 0.f)));
+  at = __fmul2_rn(make_float2(P[2].z, P[2].w), e);
+  al = make_float2(fminf(at.x, 0.99f), fminf(at.y, 0.99f));
+}
+
+__device__ __forceinline__ void bwd_phase1_pairs(const float4 (*__restrict__ sP)[3],
+                                                 float *__restrict__ wpl, float *__restrict__ qpl,
+                                                 int t, int jlive, float fx, float fy, float &T,
+                                                 float &S) {
+  int j = jlive - 1;
+  if (j >= 0 && !(j & 1)) {  // an even top row: lane .x of its pair, alone
+    const float *pp = reinterpret_cast<const float *>(&sP[j >> 1][0]);
+    const float dx = fx + pp[0], dy = fy + pp[2];
+    const float q = __fmaf_rn(pp[4], dx, __fmul_rn(pp[6], dy));
+    const float p2 = __fmaf_rn(q, dx, __fmul_rn(__fmul_rn(pp[8], dy), dy));
+    const float e = ex2_ftz(fminf(p2, 0.f));
+    const float at = __fmul_rn(pp[10], e);
+    const float alpha = fminf(at, 0.99f);
+    const float rom = rcp_ftz(1.f - alpha);
+    const float Tk = T * rom;
+    const float w = alpha * Tk;
+    const float sk = qpl[j * kPlaneStride + t];
+    const float da = Tk * sk - S * rom;
+    S = fmaf(sk, w, S);
+    T = Tk;
+    wpl[j * kPlaneStride + t] = w;
+    qpl[j * kPlaneStride + t] = (at <= kAlphaClamp ? da : 0.f) * e;
+    --j;
+  }
+  // j odd (or -1): pairs (j - 1, j), two per batch
+  auto pair_step = [&](int i, float2 al, float2 e, float2 at, float2 sk) {
+    const float2 om = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-al.x, -al.y));
+    const float2 rm = make_float2(rcp_ftz(om.x), rcp_ftz(om.y));
+    const float Thi = T * rm.y;
+    const float Tlo = Thi * rm.x;
+    const float2 Tk = make_float2(Tlo, Thi);
+    const float2 w = __fmul2_rn(al, Tk);
+    const float S1 = fmaf(sk.y, w.y, S);
+    const float2 srm = __fmul2_rn(make_float2(S1, S), rm);
+    const float2 da = __ffma2_rn(Tk, sk, make_float2(-srm.x, -srm.y));
+    S = fmaf(sk.x, w.x, S1);
+    T = Tlo;
+    const float2 q = __fmul2_rn(make_float2(at.x <= kAlphaClamp ? da.x : 0.f,
+                                            at.y <= kAlphaClamp ? da.y : 0.f), e);
+    wpl[(2 * i + 1) * kPlaneStride + t] = w.y;
+    qpl[(2 * i + 1) * kPlaneStride + t] = q.y;
+    wpl[2 * i * kPlaneStride + t] = w.x;
+    qpl[2 * i * kPlaneStride + t] = q.x;
+  };
+  for (; j >= 3; j -= 4) {
+    const int i0 = j >> 1, i1 = i0 - 1;
+    float2 al0, e0, at0, al1, e1, at1;
+    pair_alpha(sP[i0], fx, fy, al0, e0, at0);
+    pair_alpha(sP[i1], fx, fy, al1, e1, at1);
+    const float2 sk0 = make_float2(qpl[2 * i0 * kPlaneStride + t], qpl[(2 * i0 + 1) * kPlaneStride + t]);
+    const float2 sk1 = make_float2(qpl[2 * i1 * kPlaneStride + t], qpl[(2 * i1 + 1) * kPlaneStride + t]);
+    pair_step(i0, al0, e0, at0, sk0);
+    pair_step(i1, al1, e1, at1, sk1);
+  }
+  if (j >= 1) {
+    const int i0 = j >> 1;
+    float2 al0, e0, at0;
+    pair_alpha(sP[i0], fx, fy, al0, e0, at0);
+    const float2 sk0 = make_float2(qpl[2 * i0 * kPlaneStride + t], qpl[(2 * i0 + 1) * kPlaneStride + t]);
+    pair_step(i0, al0, e0, at0, sk0);
+  }
+}
+
 template <int kBC, bool kDet>
 __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
     raster_bwd_tc_kernel(BwdArgs a, vsx_camera cam) {
   constexpr int kMT = kBC / 16;          // m-tiles per chunk
   constexpr int kSplit = 8 / (2 * kMT);  // k-range split across warps
   constexpr int kKS = 32 / kSplit;       // k-steps (8 pixels) per warp
+#if VSX_BWD_PK
+  // phase-1 operands of splat pair (2i, 2i + 1), lane .x / .y of each float2:
+  // (-mx, -my), (A2, B2), (C2, opacity) as in stage_splat; the epilogue's
+  // unscaled conic (A, B, C) per splat
+  __shared__ float4 sP[2][kBC / 2][3];
+  __shared__ float4 sC[2][kBC];
+#else
   __shared__ float4 s0[2][kBC], s1[2][kBC], s2[2][kBC], s3[2][kBC];
+#endif
   __shared__ float4 s_ph[2][kBC][4];  // P B fragments per (splat, lane&3): hi b0, hi b1, lo b0, lo b1
   __shared__ uint32_t s_rank[2][kBC];
 #if VSX_BWD_OCC4
@@ -594,7 +813,22 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
     if ((unsigned)sl < (unsigned)cnt_) {
       s_rank[sb][sl] = rr;
       const vsx_splat &sp = s_raw[sb][sl];
+#if VSX_BWD_PK
+      {
+        float4 p0, p1, p2, p3;
+        stage_splat(sp, ox, oy, p0, p1, p2, p3);
+        float *pp = reinterpret_cast<float *>(&sP[sb][sl >> 1][0]) + (sl & 1);
+        pp[0] = -p0.x;
+        pp[2] = -p0.y;
+        pp[4] = p0.z;
+        pp[6] = p0.w;
+        pp[8] = p1.x;
+        pp[10] = p1.y;
+        sC[sb][sl] = make_float4(p1.w, p2.w, p3.w, 0.f);
+      }
+#else
       stage_splat(sp, ox, oy, s0[sb][sl], s1[sb][sl], s2[sb][sl], s3[sb][sl]);
+#endif
       const float pv[8] = {sp.color[0], sp.color[1], sp.color[2], sp.normal[0],
                            sp.normal[1], sp.normal[2], sp.plane_d, 1.f};
 #pragma unroll
@@ -670,6 +904,9 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
         wpl[j * kPlaneStride + t] = 0.f;
         qpl[j * kPlaneStride + t] = 0.f;
       }
+#if VSX_BWD_PK
+    bwd_phase1_pairs(sP[buf], wpl, qpl, t, jlive, fx, fy, T, S);
+#else
     // batches of kUB: the alphas (the long dependent part) are independent
     // across splats; only T and S are carried, one FMUL / FFMA each
     int j = jlive - 1;
@@ -708,6 +945,7 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
       wpl[j * kPlaneStride + t] = w;
       qpl[j * kPlaneStride + t] = dat * e;
     }
+#endif
     __syncthreads();
     // ---- phase 2: tensor-core sums over this warp's k-range
     {
@@ -838,9 +1076,16 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
             if (part < 3 && v.y != 0.f) atomicAdd(gp + 7 + 2 * part, v.y);
           }
         } else if (part == 4) {
+#if VSX_BWD_PK
+          const float *pp = reinterpret_cast<const float *>(&sP[buf][j >> 1][0]) + (j & 1);
+          const float4 cc = sC[buf][j];
+          const float op = pp[10], A = cc.x, B = cc.y, C = cc.z;
+          const float mx = -pp[0] - 7.5f, my = -pp[2] - 7.5f;
+#else
           const float4 p0 = s0[buf][j], p1 = s1[buf][j];
           const float op = p1.y, A = p1.w, B = s2[buf][j].w, C = s3[buf][j].w;
           const float mx = p0.x - 7.5f, my = p0.y - 7.5f;
+#endif
           const float Q1 = v.x, X = v.y, Y = m2, XX = m3, XY = m4, YY = m5;
           const float sx = X - mx * Q1, sy = Y - my * Q1;
           const float sxx = XX - 2.f * mx * X + mx * mx * Q1;
@@ -916,6 +1161,18 @@ static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
   dim3 grid((cam.width + kTile - 1) / kTile, rows);
   // two horizontally adjacent pixels per thread, alpha batches of 4 splats
   // (the measured optimum: DESIGN.md §3, scripts/ab_fwd.py)
+#if VSX_FWD_PACKED
+  if (L.sum_partials)
+    raster_fwd_pk_kernel<4, true><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb,
+                                                        alpha, depth, normal, raw_normal, valid,
+                                                        t_final, n_contrib, L);
+  else
+    raster_fwd_pk_kernel<4, false><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb,
+                                                         alpha, depth, normal, raw_normal, valid,
+                                                         t_final, n_contrib, L);
+  VSX_LAUNCH_CHECK("raster_fwd");
+  return VSX_OK;
+#endif
   if (L.sum_partials)  // deterministic mode (L.gt_rgb set: the fused objective)
     raster_fwd2_kernel<2, 4, true><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb,
                                                          alpha, depth, normal, raw_normal, valid,
