@@ -2,7 +2,8 @@
 //
 // Forward restates voxsplat renderer.py:242-301 (_blend_padded + _finalize)
 // and :390-449 (rasterize_view): one CTA of 128 threads per 16x16 tile, two
-// horizontally adjacent pixels per thread, splat records staged through
+// horizontally adjacent pixels per thread as float2 lanes of paired FP32
+// instructions (FFMA2 / FMUL2 / FADD2), splat records staged through
 // shared memory in chunks of 256, CTA-wide early exit once every pixel's
 // transmittance fell below 1e-4 (__syncthreads_count). Semantics that differ
 // from stock 3DGS and are kept exactly: every binned splat contributes (no
@@ -17,7 +18,8 @@
 //            s = F[p] . P[j], a [256 x 8] . [8 x 16] product (3xTF32);
 //   phase 1 (thread = pixel): the sequential back-to-front recursion, writing
 //            w = alpha*T and q = dL/d(alpha_unclamped) * exp(power) to two
-//            shared-memory planes;
+//            shared-memory planes; the alphas of a splat pair are the lanes
+//            of paired FP32 instructions;
 //   phase 2 (tensor cores): the per-splat sums over the tile's 256 pixels,
 //            [16 x 256] . [256 x 8] GEMMs of the w plane against the colour /
 //            normal / plane cotangents and of the q plane against the pixel
@@ -134,54 +136,6 @@ __device__ __forceinline__ void fwd_epilogue(const vsx_camera &cam, bool inside,
   }
 }
 
-// Forward with two horizontally adjacent pixels per thread (128 threads per
-// tile). The staged splat parameters are read from shared memory once per
-// pixel pair and the dy products of the falloff are shared, halving the
-// LSU traffic per (pixel, splat) of a pixel-per-thread kernel (which was
-// L1-bound, profiles/r01_raster_fwd_ncu.txt).
-struct FwdPix {
-  float T = 1.f, acc = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f, dist = 0.f;
-  int32_t live = 0;
-  // Branch-free live test: a dead pixel (T < 1e-4) blends with alpha 0, which
-  // leaves every accumulator and T bit-identical (all staged values are finite).
-  __device__ __forceinline__ void blend_if_live(float al, const float4 &p2, const float4 &p3,
-                                                float pd) {
-    const bool lv = T >= kEarlyStopT;
-    const float m = lv ? al : 0.f;
-    const float w = m * T;
-    acc += w;
-    c0 = fmaf(w, p2.x, c0);
-    c1 = fmaf(w, p2.y, c1);
-    c2 = fmaf(w, p2.z, c2);
-    n0 = fmaf(w, p3.x, n0);
-    n1 = fmaf(w, p3.y, n1);
-    n2 = fmaf(w, p3.z, n2);
-    dist = fmaf(w, pd, dist);
-    T = __fmaf_rn(-m, T, T);
-    live += lv ? 1 : 0;
-  }
-  __device__ __forceinline__ void blend(float al, const float4 &p2, const float4 &p3, float pd) {
-    const float w = al * T;
-    acc += w;
-    c0 = fmaf(w, p2.x, c0);
-    c1 = fmaf(w, p2.y, c1);
-    c2 = fmaf(w, p2.z, c2);
-    n0 = fmaf(w, p3.x, n0);
-    n1 = fmaf(w, p3.y, n1);
-    n2 = fmaf(w, p3.z, n2);
-    dist = fmaf(w, pd, dist);
-    T = __fmaf_rn(-al, T, T);
-    ++live;
-  }
-};
-
-__device__ __forceinline__ float falloff_alpha(const float4 &p0, const float4 &p1, float dx,
-                                               float cy, float cyy) {
-  const float q = __fmaf_rn(p0.z, dx, cy);
-  const float p2 = __fmaf_rn(q, dx, cyy);
-  return fminf(__fmul_rn(p1.y, ex2_ftz(fminf(p2, 0.f))), 0.99f);
-}
-
 __device__ __forceinline__ void copy_splat_async(vsx_splat *dst, const vsx_splat *src) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
 #pragma unroll
@@ -197,124 +151,18 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// kDet: deterministic mode (vsx_loss_desc.sum_partials), a separate
-// instantiation so the default kernel's code is unchanged.
-template <int PX, int U, bool kDet>
-__global__ void __launch_bounds__(256 / PX) raster_fwd2_kernel(
-    const vsx_splat *__restrict__ rec, const uint32_t *__restrict__ tile_off,
-    const uint32_t *__restrict__ tile_list, vsx_camera cam, float *__restrict__ out_rgb,
-    float *__restrict__ out_alpha, float *__restrict__ out_depth, float *__restrict__ out_normal,
-    float *__restrict__ out_raw, uint8_t *__restrict__ out_valid, float *__restrict__ out_T,
-    int32_t *__restrict__ out_nc, vsx_loss_desc L) {
-  constexpr int kThreads = 256 / PX, kRowThreads = kTile / PX;
-  __shared__ float4 s0[kChunk], s1[kChunk], s2[kChunk], s3[kChunk];
-  const int txn = gridDim.x;
-  const int by = (int)blockIdx.y + L.tile_row0;  // tile row (a band: rows from tile_row0)
-  const int tile = by * txn + blockIdx.x;
-  const int lx = PX * (threadIdx.x % kRowThreads), ly = threadIdx.x / kRowThreads;
-  const int px = blockIdx.x * kTile + lx, py = by * kTile + ly;
-  const double ox = (double)(blockIdx.x * kTile), oy = (double)(by * kTile);
-  const uint32_t begin = tile_off[tile], end = tile_off[tile + 1];
-  const float fy = (float)ly;
-  float fx[PX];
-  bool in[PX], done[PX];
-  int32_t nc[PX];
-  FwdPix A[PX];
-#pragma unroll
-  for (int i = 0; i < PX; ++i) {
-    fx[i] = (float)(lx + i);
-    in[i] = px + i < cam.width && py < cam.height;
-    done[i] = !in[i];
-    nc[i] = 0;
-  }
-  auto all_done = [&] {
-    bool d = true;
-#pragma unroll
-    for (int i = 0; i < PX; ++i) d = d && done[i];
-    return d;
-  };
-  auto any_live = [&] {
-    bool l = false;
-#pragma unroll
-    for (int i = 0; i < PX; ++i) l = l || A[i].T >= kEarlyStopT;
-    return l;
-  };
-  for (uint32_t cs = begin; cs < end; cs += kChunk) {
-    if (__syncthreads_count(!all_done()) == 0) break;
-#pragma unroll
-    for (int h = 0; h < kChunk / kThreads; ++h) {
-      const int k = threadIdx.x + kThreads * h;
-      const uint32_t idx = cs + k;
-      if (idx < end) {
-        const vsx_splat sp = load_splat(rec, tile_list[idx]);
-        stage_splat(sp, ox, oy, s0[k], s1[k], s2[k], s3[k]);
-      }
-    }
-    __syncthreads();
-    const int cnt = (int)min((uint32_t)kChunk, end - cs);
-    if (!all_done()) {
-#pragma unroll
-      for (int i = 0; i < PX; ++i) A[i].live = 0;
-      // T only decreases, so each pixel's "live" splats are a prefix of the chunk
-      // batches of U splats: all U * PX alphas first (independent), then the
-      // sequential blends
-      int j = 0;
-      for (; j + U <= cnt && any_live(); j += U) {
-        float al[U][PX];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const float4 p0 = s0[j + u], p1 = s1[j + u];
-          const float dy = fy - p0.y;
-          const float cy = __fmul_rn(p0.w, dy), cyy = __fmul_rn(__fmul_rn(p1.x, dy), dy);
-#pragma unroll
-          for (int i = 0; i < PX; ++i) al[u][i] = falloff_alpha(p0, p1, fx[i] - p0.x, cy, cyy);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const float4 p2 = s2[j + u], p3 = s3[j + u];
-          const float pd = s1[j + u].z;
-#pragma unroll
-          for (int i = 0; i < PX; ++i) A[i].blend_if_live(al[u][i], p2, p3, pd);
-        }
-      }
-      for (; j < cnt && any_live(); ++j) {
-        const float4 p0 = s0[j], p1 = s1[j];
-        const float dy = fy - p0.y;
-        const float cy = __fmul_rn(p0.w, dy), cyy = __fmul_rn(__fmul_rn(p1.x, dy), dy);
-        float al[PX];
-#pragma unroll
-        for (int i = 0; i < PX; ++i) al[i] = falloff_alpha(p0, p1, fx[i] - p0.x, cy, cyy);
-        const float4 p2 = s2[j], p3 = s3[j];
-#pragma unroll
-        for (int i = 0; i < PX; ++i)
-          if (A[i].T >= kEarlyStopT) A[i].blend(al[i], p2, p3, p1.z);
-      }
-#pragma unroll
-      for (int i = 0; i < PX; ++i)
-        if (!done[i]) {
-          nc[i] = (int32_t)(cs - begin) + A[i].live;
-          done[i] = A[i].T < kEarlyStopT;
-        }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < PX; ++i)
-    fwd_epilogue<kDet>(cam, in[i], px + i, py, A[i].acc, A[i].c0, A[i].c1, A[i].c2, A[i].n0, A[i].n1,
-                 A[i].n2, A[i].dist, A[i].T, nc[i], out_rgb, out_alpha, out_depth, out_normal,
-                 out_raw, out_valid, out_T, out_nc, L);
-}
-
-// Packed-pair forward: the same algorithm as raster_fwd2_kernel<2, U> with
-// the two pixels of a thread held as float2 lanes and advanced with the
+// Forward: one CTA of 128 threads per tile, two horizontally adjacent pixels
+// per thread held as the lanes of float2 registers and advanced with the
 // sm_100 paired FP32 instructions (FFMA2 / FMUL2 / FADD2; the staged splat
-// value is the broadcast operand). Every lane performs the scalar kernel's
-// operations with the same roundings (fma / mul / add are each correctly
-// rounded), so alpha and T agree bit for bit with the backward's recompute.
-// The kernel was issue-bound at 84% with 26 instructions per (pixel, splat)
-// (profiles/r02_raster_final_ncu.txt); pairing removes about a third.
-#ifndef VSX_FWD_PACKED
-#define VSX_FWD_PACKED 1
-#endif
+// value is the broadcast operand). Records are staged through shared memory
+// kChunk at a time; per staged splat the two pixels share its loads and the dy
+// terms of the falloff; the alphas of U splats are evaluated before the
+// serial transmittance chain. Every lane performs the scalar operations with
+// the same roundings (fma / mul / add are each correctly rounded), so alpha
+// and T agree bit for bit with the backward's recompute. The scalar
+// two-pixel kernel this replaced was issue-bound at 84% with 26 instructions
+// per (pixel, splat) (profiles/r02_raster_final_ncu.txt); pairing removes a
+// third of them (profiles/r02_raster_fwd_pk_ncu.txt).
 __device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
 
 struct FwdPair {
@@ -478,10 +326,6 @@ struct BwdArgs {
 // a_hi + a_lo. Warps split (m-tile, plane, k-range); the KSPLIT partial sums
 // meet in shared memory and one 8-lane group per splat forms its 13
 // gradients (same polynomials as v2) and issues the atomics.
-#ifndef VSX_BWD_UB
-#define VSX_BWD_UB 4
-#endif
-constexpr int kUB = VSX_BWD_UB;  // phase-1 splats per alpha batch
 #ifndef VSX_BWD_KR7
 #define VSX_BWD_KR7 5
 #endif
@@ -533,9 +377,6 @@ __device__ __forceinline__ float pixel_moment(int p, int m) {
 // (T_2i+1 first, back to front). Per lane the operations and roundings are
 // the scalar ones (splat_alpha), so alpha and T agree bit for bit with the
 // forward. Writes w and q of rows [0, jlive) of this thread's plane column.
-#ifndef VSX_BWD_PK
-#define VSX_BWD_PK 1
-#endif
 __device__ __forceinline__ void pair_alpha(const float4 (&P)[3], float fx, float fy, float2 &al,
                                            float2 &e, float2 &at) {
   const float2 dx = __fadd2_rn(bc2(fx), make_float2(P[0].x, P[0].y));
@@ -618,15 +459,11 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
   constexpr int kMT = kBC / 16;          // m-tiles per chunk
   constexpr int kSplit = 8 / (2 * kMT);  // k-range split across warps
   constexpr int kKS = 32 / kSplit;       // k-steps (8 pixels) per warp
-#if VSX_BWD_PK
   // phase-1 operands of splat pair (2i, 2i + 1), lane .x / .y of each float2:
   // (-mx, -my), (A2, B2), (C2, opacity) as in stage_splat; the epilogue's
   // unscaled conic (A, B, C) per splat
   __shared__ float4 sP[2][kBC / 2][3];
   __shared__ float4 sC[2][kBC];
-#else
-  __shared__ float4 s0[2][kBC], s1[2][kBC], s2[2][kBC], s3[2][kBC];
-#endif
   __shared__ float4 s_ph[2][kBC][4];  // P B fragments per (splat, lane&3): hi b0, hi b1, lo b0, lo b1
   __shared__ uint32_t s_rank[2][kBC];
 #if VSX_BWD_OCC4
@@ -813,7 +650,6 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
     if ((unsigned)sl < (unsigned)cnt_) {
       s_rank[sb][sl] = rr;
       const vsx_splat &sp = s_raw[sb][sl];
-#if VSX_BWD_PK
       {
         float4 p0, p1, p2, p3;
         stage_splat(sp, ox, oy, p0, p1, p2, p3);
@@ -826,9 +662,6 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
         pp[10] = p1.y;
         sC[sb][sl] = make_float4(p1.w, p2.w, p3.w, 0.f);
       }
-#else
-      stage_splat(sp, ox, oy, s0[sb][sl], s1[sb][sl], s2[sb][sl], s3[sb][sl]);
-#endif
       const float pv[8] = {sp.color[0], sp.color[1], sp.color[2], sp.normal[0],
                            sp.normal[1], sp.normal[2], sp.plane_d, 1.f};
 #pragma unroll
@@ -904,48 +737,7 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
         wpl[j * kPlaneStride + t] = 0.f;
         qpl[j * kPlaneStride + t] = 0.f;
       }
-#if VSX_BWD_PK
     bwd_phase1_pairs(sP[buf], wpl, qpl, t, jlive, fx, fy, T, S);
-#else
-    // batches of kUB: the alphas (the long dependent part) are independent
-    // across splats; only T and S are carried, one FMUL / FFMA each
-    int j = jlive - 1;
-    for (; j >= kUB - 1; j -= kUB) {
-      float al[kUB], ee[kUB], aa[kUB], rm[kUB], sk[kUB];
-#pragma unroll
-      for (int u = 0; u < kUB; ++u) {
-        const float4 p0 = s0[buf][j - u], p1 = s1[buf][j - u];
-        al[u] = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, ee[u], aa[u]);
-        rm[u] = rcp_ftz(1.f - al[u]);
-        sk[u] = qpl[(j - u) * kPlaneStride + t];
-      }
-#pragma unroll
-      for (int u = 0; u < kUB; ++u) {
-        const float Tk = T * rm[u];
-        const float w = al[u] * Tk;
-        const float da = Tk * sk[u] - S * rm[u];
-        S = fmaf(sk[u], w, S);
-        T = Tk;
-        wpl[(j - u) * kPlaneStride + t] = w;
-        qpl[(j - u) * kPlaneStride + t] = (aa[u] <= kAlphaClamp ? da : 0.f) * ee[u];
-      }
-    }
-    for (; j >= 0; --j) {
-      const float4 p0 = s0[buf][j], p1 = s1[buf][j];
-      float e, at;
-      const float alpha = splat_alpha(p0, p1, fx - p0.x, fy - p0.y, e, at);
-      const float rom = rcp_ftz(1.f - alpha);
-      const float Tk = T * rom;
-      const float w = alpha * Tk;
-      const float sk = qpl[j * kPlaneStride + t];
-      const float da = Tk * sk - S * rom;
-      S = fmaf(sk, w, S);
-      T = Tk;
-      const float dat = at <= kAlphaClamp ? da : 0.f;
-      wpl[j * kPlaneStride + t] = w;
-      qpl[j * kPlaneStride + t] = dat * e;
-    }
-#endif
     __syncthreads();
     // ---- phase 2: tensor-core sums over this warp's k-range
     {
@@ -1076,16 +868,10 @@ __global__ void __launch_bounds__(256, (kBC == 16 ? (VSX_BWD_OCC4 ? 4 : 3) : 2))
             if (part < 3 && v.y != 0.f) atomicAdd(gp + 7 + 2 * part, v.y);
           }
         } else if (part == 4) {
-#if VSX_BWD_PK
           const float *pp = reinterpret_cast<const float *>(&sP[buf][j >> 1][0]) + (j & 1);
           const float4 cc = sC[buf][j];
           const float op = pp[10], A = cc.x, B = cc.y, C = cc.z;
           const float mx = -pp[0] - 7.5f, my = -pp[2] - 7.5f;
-#else
-          const float4 p0 = s0[buf][j], p1 = s1[buf][j];
-          const float op = p1.y, A = p1.w, B = s2[buf][j].w, C = s3[buf][j].w;
-          const float mx = p0.x - 7.5f, my = p0.y - 7.5f;
-#endif
           const float Q1 = v.x, X = v.y, Y = m2, XX = m3, XY = m4, YY = m5;
           const float sx = X - mx * Q1, sy = Y - my * Q1;
           const float sxx = XX - 2.f * mx * X + mx * mx * Q1;
@@ -1161,8 +947,7 @@ static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
   dim3 grid((cam.width + kTile - 1) / kTile, rows);
   // two horizontally adjacent pixels per thread, alpha batches of 4 splats
   // (the measured optimum: DESIGN.md §3, scripts/ab_fwd.py)
-#if VSX_FWD_PACKED
-  if (L.sum_partials)
+  if (L.sum_partials)  // deterministic mode (a separate instantiation)
     raster_fwd_pk_kernel<4, true><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb,
                                                         alpha, depth, normal, raw_normal, valid,
                                                         t_final, n_contrib, L);
@@ -1170,17 +955,6 @@ static int launch_fwd(const vsx_splat *rec, const uint32_t *tile_offsets,
     raster_fwd_pk_kernel<4, false><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb,
                                                          alpha, depth, normal, raw_normal, valid,
                                                          t_final, n_contrib, L);
-  VSX_LAUNCH_CHECK("raster_fwd");
-  return VSX_OK;
-#endif
-  if (L.sum_partials)  // deterministic mode (L.gt_rgb set: the fused objective)
-    raster_fwd2_kernel<2, 4, true><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb,
-                                                         alpha, depth, normal, raw_normal, valid,
-                                                         t_final, n_contrib, L);
-  else
-    raster_fwd2_kernel<2, 4, false><<<grid, 128, 0, st>>>(rec, tile_offsets, tile_list, cam, rgb,
-                                                          alpha, depth, normal, raw_normal, valid,
-                                                          t_final, n_contrib, L);
   VSX_LAUNCH_CHECK("raster_fwd");
   return VSX_OK;
 }

@@ -24,7 +24,7 @@ EMBED_DIM = 32
 HIDDEN = 64
 REC_F32 = 16            # sizeof(vsx_splat) / 4
 GRAD_F32 = 13           # per-splat gradient record
-FWD_WARPS = 4           # warps per CTA of the compositor forward (raster_fwd2_kernel<2, 4>)
+FWD_WARPS = 4           # warps per CTA of the compositor forward (raster_fwd_pk_kernel<4>)
 STATUS_NONPD = 1
 STATUS_NONFINITE = 2
 
