@@ -36,6 +36,9 @@
  *   vsx_tsdf_integrate             fusion.py:102-133 TSDF integration
  *   (C1 payload exchange)          renderer.py:452-477 transfer_gaussians: the 64-byte splat
  *                                  records are the payload; the all-to-all is NCCL (dist.py)
+ *   vsx_pack_splat_rows / vsx_splat_rows_keys / vsx_gather_splat_rows
+ *                                  C1 payload rows (96 B: record | z | radius | gid) packed
+ *                                  for the all-to-all, and read back in (z, gid) order
  *   vsx_prior_sample / vsx_apply_scale_shift / vsx_reprojection_error / vsx_enhance_finalize
  *                                  depth_prior.py:85-214 (fit_scale_shift, apply_scale_shift,
  *                                  reprojection_error, enhance)
@@ -115,6 +118,11 @@ uint64_t vsx_launch_count(void);
 /* Workspace bytes needed by vsx_sort_pairs_* / vsx_select / vsx_scan for n items. */
 size_t vsx_sort_ws_bytes(int64_t n);
 size_t vsx_scan_ws_bytes(int64_t n);
+/* Row scatter of float32 rows: dst[idx[i] * width + k] = src[i * width + k]
+ * (idx a permutation of [0, n); the sharded step returns each merged view's
+ * splat gradients to the received row order with it). */
+int vsx_scatter_rows_f32(const float *src, const uint32_t *idx, int32_t n, int32_t width,
+                         float *dst, vsx_stream s);
 /* Exclusive scan of uint32 counts: out[i] = sum(in[0:i]); out[n] = total. */
 int vsx_scan_u32(const uint32_t *in, uint32_t *out, int64_t n, void *ws, size_t ws_bytes,
                  vsx_stream s);
@@ -195,6 +203,20 @@ int vsx_project_fwd(const double *means, const float *opacity, const float *colo
 /* Gather records/radius into sorted order: dst[i] = src[order[i]], i < n. */
 int vsx_gather_splats(const vsx_splat *rec, const double *radius, const uint32_t *order,
                       int32_t n, vsx_splat *rec_sorted, double *radius_sorted, vsx_stream s);
+/* C1 payload rows (the sharded step, dist.py): 96 bytes per splat = the
+ * 64-byte record, float64 z, float64 radius, int64 gid, 8 bytes of padding
+ * (16-byte aligned rows for the all-to-all buffer). Pack n rows into out. */
+#define VSX_SPLAT_ROW_BYTES 96
+int vsx_pack_splat_rows(const vsx_splat *rec, const double *z, const double *radius,
+                        const int64_t *gid, int32_t n, uint8_t *out, vsx_stream s);
+/* Sort keys of n received rows: row i is rows[rowmap[i]] (rowmap NULL: rows[i]). */
+int vsx_splat_rows_keys(const uint8_t *rows, const int32_t *rowmap, int32_t n, double *z,
+                        int64_t *gid, vsx_stream s);
+/* Records / radii in merge order: dst[i] = row(order[i]), row(j) = rows[rowmap[j]]
+ * (rowmap NULL: rows[j]). */
+int vsx_gather_splat_rows(const uint8_t *rows, const int32_t *rowmap, const uint32_t *order,
+                          int32_t n, vsx_splat *rec_sorted, double *radius_sorted,
+                          vsx_stream s);
 
 /* ---- K4: tile binning (renderer.py:207-226) --------------------------- */
 /* Phase 1: per-splat tile counts (+ per-tile histogram when tile_counts is

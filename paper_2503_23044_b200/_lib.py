@@ -81,6 +81,10 @@ _SIGS = {
                         c_f64, P, P, P, P, P, P, P, P, P, P, P, P, P, P, c_size, P], c_i32),
     "vsx_project_fwd": ([P, P, P, P, P, P, c_i32, VsxCamera, P, P, P, P, P, P], c_i32),
     "vsx_gather_splats": ([P, P, P, c_i32, P, P, P], c_i32),
+    "vsx_scatter_rows_f32": ([P, P, c_i32, c_i32, P, P], c_i32),
+    "vsx_pack_splat_rows": ([P, P, P, P, c_i32, P, P], c_i32),
+    "vsx_splat_rows_keys": ([P, P, c_i32, P, P, P], c_i32),
+    "vsx_gather_splat_rows": ([P, P, P, c_i32, P, P, P], c_i32),
     "vsx_bin_count": ([P, P, c_i32, c_i32, c_i32, P, P, P], c_i32),
     "vsx_bin_emit": ([P, P, c_i32, c_i32, c_i32, P, P, P, P], c_i32),
     "vsx_bin_emit_hist": ([P, P, c_i32, c_i32, c_i32, P, P, P, P, P], c_i32),

@@ -702,3 +702,26 @@ extern "C" int vsx_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_
   return sort_pairs<uint32_t>(keys_in, vals_in, keys_out, vals_out, n, begin_bit, end_bit, flags,
                               ws, ws_bytes, as_stream(s));
 }
+
+namespace vsx {
+__global__ void scatter_rows_f32_kernel(const float *__restrict__ src,
+                                        const uint32_t *__restrict__ idx, int32_t n, int width,
+                                        float *__restrict__ dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * width) return;
+  const int64_t i = e / width;
+  dst[(int64_t)idx[i] * width + (e - i * width)] = src[e];
+}
+
+}  // namespace vsx
+
+extern "C" int vsx_scatter_rows_f32(const float *src, const uint32_t *idx, int32_t n,
+                                    int32_t width, float *dst, vsx_stream s) {
+  VSX_REQUIRE(n >= 0 && width > 0, "scatter_rows_f32: bad arguments");
+  if (n == 0) return VSX_OK;
+  VSX_REQUIRE(src && idx && dst, "scatter_rows_f32: null pointer");
+  scatter_rows_f32_kernel<<<grid_for((int64_t)n * width, 256), 256, 0, as_stream(s)>>>(
+      src, idx, n, width, dst);
+  VSX_LAUNCH_CHECK("scatter_rows_f32");
+  return VSX_OK;
+}

@@ -523,6 +523,92 @@ extern "C" int vsx_gather_splats(const vsx_splat *rec, const double *radius,
   return VSX_OK;
 }
 
+namespace vsx {
+// C1 payload rows: 6 x 16-byte pieces per 96-byte row (record, then
+// (z, radius), then (gid, pad)); one thread per piece, coalesced stores.
+__global__ void pack_splat_rows_kernel(const vsx_splat *__restrict__ rec,
+                                       const double *__restrict__ z,
+                                       const double *__restrict__ radius,
+                                       const int64_t *__restrict__ gid, int32_t n,
+                                       uint8_t *__restrict__ out) {
+  const int64_t tq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = tq / 6;
+  const int part = (int)(tq - 6 * i);
+  if (i >= n) return;
+  longlong2 v;
+  if (part < 4) {
+    v = __ldg(reinterpret_cast<const longlong2 *>(rec) + 4 * i + part);
+  } else if (part == 4) {
+    v = make_longlong2(__double_as_longlong(z[i]), __double_as_longlong(radius[i]));
+  } else {
+    v = make_longlong2(gid[i], 0);
+  }
+  reinterpret_cast<longlong2 *>(out + i * VSX_SPLAT_ROW_BYTES)[part] = v;
+}
+
+__global__ void splat_rows_keys_kernel(const uint8_t *__restrict__ rows,
+                                       const int32_t *__restrict__ rowmap, int32_t n,
+                                       double *__restrict__ z, int64_t *__restrict__ gid) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t r = rowmap ? rowmap[i] : i;
+  const longlong2 *row = reinterpret_cast<const longlong2 *>(rows + r * VSX_SPLAT_ROW_BYTES);
+  z[i] = __longlong_as_double(row[4].x);
+  gid[i] = row[5].x;
+}
+
+__global__ void gather_splat_rows_kernel(const uint8_t *__restrict__ rows,
+                                         const int32_t *__restrict__ rowmap,
+                                         const uint32_t *__restrict__ order, int32_t n,
+                                         vsx_splat *__restrict__ out, double *__restrict__ rout) {
+  const int64_t tq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = tq >> 2;
+  const int part = (int)(tq & 3);
+  if (i >= n) return;
+  const uint32_t j = order[i];
+  const int64_t r = rowmap ? rowmap[j] : (int64_t)j;
+  const float4 *row = reinterpret_cast<const float4 *>(rows + r * VSX_SPLAT_ROW_BYTES);
+  reinterpret_cast<float4 *>(out)[4 * i + part] = __ldg(row + part);
+  if (part == 0) rout[i] = __longlong_as_double(reinterpret_cast<const longlong2 *>(row)[4].y);
+}
+
+}  // namespace vsx
+
+extern "C" int vsx_pack_splat_rows(const vsx_splat *rec, const double *z, const double *radius,
+                                   const int64_t *gid, int32_t n, uint8_t *out, vsx_stream s) {
+  VSX_REQUIRE(n >= 0, "pack_splat_rows: n < 0");
+  if (n == 0) return VSX_OK;
+  VSX_REQUIRE(rec && z && radius && gid && out, "pack_splat_rows: null pointer");
+  VSX_REQUIRE(((uintptr_t)out & 15) == 0, "pack_splat_rows: out not 16-byte aligned");
+  pack_splat_rows_kernel<<<grid_for((int64_t)6 * n, 256), 256, 0, as_stream(s)>>>(
+      rec, z, radius, gid, n, out);
+  VSX_LAUNCH_CHECK("pack_splat_rows");
+  return VSX_OK;
+}
+
+extern "C" int vsx_splat_rows_keys(const uint8_t *rows, const int32_t *rowmap, int32_t n,
+                                   double *z, int64_t *gid, vsx_stream s) {
+  VSX_REQUIRE(n >= 0, "splat_rows_keys: n < 0");
+  if (n == 0) return VSX_OK;
+  VSX_REQUIRE(rows && z && gid, "splat_rows_keys: null pointer");
+  splat_rows_keys_kernel<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(rows, rowmap, n, z, gid);
+  VSX_LAUNCH_CHECK("splat_rows_keys");
+  return VSX_OK;
+}
+
+extern "C" int vsx_gather_splat_rows(const uint8_t *rows, const int32_t *rowmap,
+                                     const uint32_t *order, int32_t n, vsx_splat *rec_sorted,
+                                     double *radius_sorted, vsx_stream s) {
+  VSX_REQUIRE(n >= 0, "gather_splat_rows: n < 0");
+  if (n == 0) return VSX_OK;
+  VSX_REQUIRE(rows && order && rec_sorted && radius_sorted, "gather_splat_rows: null pointer");
+  VSX_REQUIRE(((uintptr_t)rows & 15) == 0, "gather_splat_rows: rows not 16-byte aligned");
+  gather_splat_rows_kernel<<<grid_for((int64_t)4 * n, 256), 256, 0, as_stream(s)>>>(
+      rows, rowmap, order, n, rec_sorted, radius_sorted);
+  VSX_LAUNCH_CHECK("gather_splat_rows");
+  return VSX_OK;
+}
+
 extern "C" int vsx_bin_count(const vsx_splat *rec, const double *radius, int32_t n,
                              int32_t width, int32_t height, uint32_t *splat_tiles,
                              uint32_t *tile_counts, vsx_stream s) {

@@ -93,18 +93,19 @@ def sort_pairs_u32(keys: torch.Tensor, vals: torch.Tensor, n: int, bits: int,
     return ko, vo
 
 
-def sort_z_gid(z: torch.Tensor, gid: torch.Tensor) -> torch.Tensor:
-    """Permutation = lexsort((gid, z)) of positive float64 z (int64 on device)."""
+def sort_z_gid(z: torch.Tensor, gid: torch.Tensor, int32: bool = False) -> torch.Tensor:
+    """Permutation = lexsort((gid, z)) of positive float64 z (int64 on device,
+    or the kernel's int32 with ``int32=True``)."""
     n = int(z.numel())
     order = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
     if n == 0:
-        return order[:0].long()
+        return order[:0] if int32 else order[:0].long()
     lib = _lib.load()
     wp, wb = workspace().get(lib.vsx_sort_z_gid_ws_bytes(n))
     z, gid = z.contiguous(), gid.contiguous()   # bound for the kernel's lifetime
     call("vsx_sort_z_gid", ptr(z), ptr(gid), ptr(order), n, wp, wb,
          stream())
-    return order.long()
+    return order[:n] if int32 else order.long()
 
 
 def exclusive_scan(counts: torch.Tensor, n: int) -> torch.Tensor:

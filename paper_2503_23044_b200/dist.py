@@ -28,6 +28,7 @@ single-process oracle step.
 
 from __future__ import annotations
 
+from ctypes import c_void_p
 from dataclasses import dataclass
 
 import numpy as np
@@ -61,6 +62,51 @@ class SplatPayload:
 
 def renderer_of(view_index: int, world: int) -> int:
     return view_index % world
+
+
+ROW_BYTES = 96   # VSX_SPLAT_ROW_BYTES: record | z | radius | gid | pad
+
+
+@dataclass
+class PackedPayload:
+    """A renderer's received rows of one view, left in the all-to-all buffer:
+    row i of the view is ``rows[rowmap[i]]`` (``rowmap`` None: row ``base + i``);
+    z and gid are extracted for the (z, gid) merge sort."""
+
+    buf: torch.Tensor            # (N, ROW_BYTES) uint8 receive buffer
+    base: int                    # first row of the view when rowmap is None
+    rowmap: torch.Tensor | None  # (n,) int32 rows of buf, source-rank order
+    z: torch.Tensor              # (n,) float64
+    gid: torch.Tensor            # (n,) int64
+
+    @property
+    def count(self) -> int:
+        return int(self.z.shape[0])
+
+    def rows_ptr(self) -> int:
+        return self.buf.data_ptr() + (self.base if self.rowmap is None else 0) * ROW_BYTES
+
+
+def _cuda_rows(p: SplatPayload) -> bool:
+    return (p.rec.is_cuda and p.rec.dtype == torch.float32 and p.rec.dim() == 2
+            and p.rec.shape[1] == 16)
+
+
+def _pack_rows(parts: list[SplatPayload], total: int, device) -> torch.Tensor:
+    """The send buffer of the CUDA path: every part's rows packed in order by
+    vsx_pack_splat_rows (one pass, no intermediate concatenation)."""
+    from ._lib import call, ptr, stream
+    buf = torch.empty((max(total, 1), ROW_BYTES), dtype=torch.uint8, device=device)
+    off = 0
+    for p in parts:
+        n = p.count
+        if n:
+            rec, z = p.rec.contiguous(), p.z.contiguous()
+            rad, gid = p.radius.contiguous(), p.gid.contiguous()
+            call("vsx_pack_splat_rows", ptr(rec), ptr(z), ptr(rad), ptr(gid), n,
+                 c_void_p(buf.data_ptr() + off * ROW_BYTES), stream())
+        off += n
+    return buf[:total]
 
 
 def _fields(p: SplatPayload):
@@ -134,12 +180,14 @@ def exchange_splats(payloads: list[SplatPayload], rank: int, world: int, group=N
     dist.all_gather(gathered, mine_counts, group=group)
     plan = ExchangePlan(torch.stack(gathered).cpu().numpy(), rank, world, renderers)
     send_parts = [payloads[v] for r in range(world) for v in plan.views_of(r)]
-    send = SplatPayload.cat(send_parts, payloads[0])
     ins, outs = plan.send_splits(), plan.recv_splits()
+    mine = plan.views_of(rank)
+    if _cuda_rows(payloads[0]):
+        return plan, _exchange_rows(plan, send_parts, ins, outs, mine, dev, group)
+    send = SplatPayload.cat(send_parts, payloads[0])
     # ONE all-to-all of packed rows (record | z | radius | gid bytes)
     recv = _unpack(_a2a(_pack(send), ins, outs, group), payloads[0])
     # split the received block per (source, view) and regroup per view
-    mine = plan.views_of(rank)
     merged: dict[int, tuple[SplatPayload, list[int]]] = {}
     pieces: dict[int, list[SplatPayload]] = {v: [] for v in mine}
     off = 0
@@ -153,6 +201,40 @@ def exchange_splats(payloads: list[SplatPayload], rank: int, world: int, group=N
         seg = [0] + list(np.cumsum([int(plan.counts[q, v]) for q in range(world)]))
         merged[v] = (SplatPayload.cat(pieces[v], payloads[0]), seg)
     return plan, merged
+
+
+def _exchange_rows(plan: ExchangePlan, send_parts, ins, outs, mine, dev, group):
+    """C1 forward of the CUDA path: one all-to-all of 96-byte rows packed by
+    vsx_pack_splat_rows; each view's rows stay in the receive buffer (a row
+    map when they come from several sources) and only the sort keys are
+    extracted (vsx_splat_rows_keys)."""
+    from ._lib import call, ptr, stream
+    world = plan.world
+    recv = _a2a(_pack_rows(send_parts, sum(ins), dev), ins, outs, group)
+    starts: dict[int, list[tuple[int, int]]] = {v: [] for v in mine}
+    off = 0
+    for q in range(world):
+        for v in mine:
+            c = int(plan.counts[q, v])
+            starts[v].append((off, c))
+            off += c
+    merged = {}
+    for v in mine:
+        blocks = [(o, c) for o, c in starts[v] if c]
+        n = sum(c for _, c in blocks)
+        rowmap, base = None, (blocks[0][0] if blocks else 0)
+        if len(blocks) > 1:
+            rowmap = torch.cat([torch.arange(o, o + c, dtype=torch.int32, device=dev)
+                                for o, c in blocks])
+        z = torch.empty(max(n, 1), dtype=torch.float64, device=dev)[:n]
+        gid = torch.empty(max(n, 1), dtype=torch.int64, device=dev)[:n]
+        pl = PackedPayload(recv, base, rowmap, z, gid)
+        if n:
+            call("vsx_splat_rows_keys", c_void_p(pl.rows_ptr()), ptr(rowmap), n, ptr(z),
+                 ptr(gid), stream())
+        seg = [0] + list(np.cumsum([int(plan.counts[q, v]) for q in range(world)]))
+        merged[v] = (pl, seg)
+    return merged
 
 
 def return_grads(plan: ExchangePlan, grads: dict[int, torch.Tensor], like: torch.Tensor,
@@ -177,6 +259,19 @@ def return_grads(plan: ExchangePlan, grads: dict[int, torch.Tensor], like: torch
             out[v] = recv[off:off + c]
             off += c
     return out
+
+
+def _unsort_rows(gs: torch.Tensor, order: torch.Tensor) -> torch.Tensor:
+    """merged[order[i]] = gs[i]: sorted-splat gradient rows back to the
+    received row order (vsx_scatter_rows_f32)."""
+    from ._lib import call, ptr, stream
+    merged = torch.empty_like(gs)
+    n = int(order.numel())
+    if n:
+        o32 = order if order.dtype == torch.int32 else order.int()
+        g = gs.contiguous()
+        call("vsx_scatter_rows_f32", ptr(g), ptr(o32), n, int(gs.shape[1]), ptr(merged), stream())
+    return merged
 
 
 class _StagedView:
@@ -678,9 +773,21 @@ class CudaShardBackend:
         """Merge the view's received splats in (z, gid) order and bin them."""
         D = self.D
         n = payload.count
-        order = D.sort_z_gid(payload.z, payload.gid)
-        P = D.Projected(payload.rec[order].contiguous(), payload.radius[order].contiguous(),
-                        lambda: payload.z[order].view(torch.int64), order.int(), n)
+        order = D.sort_z_gid(payload.z, payload.gid, int32=True)
+        if isinstance(payload, PackedPayload):
+            from ._lib import call, ptr, stream
+            rs = torch.empty((max(n, 1), D.REC_F32), dtype=torch.float32, device="cuda")
+            rr = torch.empty(max(n, 1), dtype=torch.float64, device="cuda")
+            call("vsx_gather_splat_rows", c_void_p(payload.rows_ptr()), ptr(payload.rowmap),
+                 ptr(order), n, ptr(rs), ptr(rr), stream())
+            zk = payload.z.view(torch.int64)
+            P = D.Projected(rs[:n], rr[:n], lambda: zk[order.long()], order, n)
+            Bn = D.bin_tiles(P, view.width, view.height)
+            return P, Bn, order
+        # records and radii gathered in merge order by vsx_gather_splats (the
+        # eager row gather took ~15x longer)
+        P = D.gather_projected(payload.rec.contiguous(), payload.z.view(torch.int64),
+                               payload.radius.contiguous(), order, n)
         Bn = D.bin_tiles(P, view.width, view.height)
         return P, Bn, order
 
@@ -758,9 +865,7 @@ class CudaShardBackend:
             R = D.raster_forward(P, Bn, view, loss=loss, deterministic=det)
         with _span(self.timer, "raster_bwd"):
             gs = D.raster_backward(P, Bn, view, R, loss=loss, deterministic=det)
-        merged = torch.empty_like(gs)
-        merged[order] = gs
-        return merged
+        return _unsort_rows(gs, order)
 
     # ---- tile-row bands (a view split over renderer ranks when B < M)
 
@@ -817,9 +922,7 @@ class CudaShardBackend:
             keep = (keep, extra)
         det = bool(getattr(st.cfg, "deterministic", False))
         gs = D.raster_backward(P, Bn, view, R, loss=loss, deterministic=det)
-        merged = torch.empty_like(gs)
-        merged[order] = gs
-        return merged
+        return _unsort_rows(gs, order)
 
     def backward_shard(self, v: int, view, grads: torch.Tensor) -> None:
         from ._lib import call, ptr, stream

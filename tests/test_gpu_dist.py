@@ -38,6 +38,44 @@ def test_sort_z_gid_is_lexsort():
     np.testing.assert_array_equal(order, np.lexsort((gid, z)))
 
 
+def test_c1_rows_pack_keys_gather_roundtrip():
+    """The CUDA C1 row path: rows packed by vsx_pack_splat_rows, keys read
+    back through a row map (rows of one view from several sources), and the
+    records / radii gathered in (z, gid) order equal torch indexing."""
+    from ctypes import c_void_p
+    from paper_2503_23044_b200 import device as D
+    from paper_2503_23044_b200._lib import call, ptr, stream
+    from paper_2503_23044_b200.dist import ROW_BYTES, SplatPayload, _pack_rows
+    g = torch.Generator(device="cuda").manual_seed(5)
+    parts = []
+    for n in (1000, 0, 2500, 777):
+        rec = torch.randn((n, 16), device="cuda", generator=g)
+        z = torch.rand(n, device="cuda", generator=g, dtype=torch.float64).round(decimals=2) + 1
+        rad = torch.rand(n, device="cuda", generator=g, dtype=torch.float64) * 30
+        gid = torch.randperm(10 ** 6, device="cuda", generator=g)[:n]
+        parts.append(SplatPayload(rec, z, rad, gid))
+    total = sum(p.count for p in parts)
+    buf = _pack_rows(parts, total, "cuda")
+    assert buf.shape == (total, ROW_BYTES)
+    cat = SplatPayload.cat(parts, parts[0])
+    # the "view" takes part 3 then part 0 (two source blocks)
+    offs = np.cumsum([0] + [p.count for p in parts])
+    rowmap = torch.cat([torch.arange(offs[3], offs[4]), torch.arange(offs[0], offs[1])]).int().cuda()
+    n = int(rowmap.numel())
+    z = torch.empty(n, dtype=torch.float64, device="cuda")
+    gid = torch.empty(n, dtype=torch.int64, device="cuda")
+    call("vsx_splat_rows_keys", c_void_p(buf.data_ptr()), ptr(rowmap), n, ptr(z), ptr(gid), stream())
+    rl = rowmap.long()
+    assert torch.equal(z, cat.z[rl]) and torch.equal(gid, cat.gid[rl])
+    order = D.sort_z_gid(z, gid, int32=True)
+    rs = torch.empty((n, 16), device="cuda")
+    rr = torch.empty(n, dtype=torch.float64, device="cuda")
+    call("vsx_gather_splat_rows", c_void_p(buf.data_ptr()), ptr(rowmap), ptr(order), n, ptr(rs),
+         ptr(rr), stream())
+    src = rl[order.long()]
+    assert torch.equal(rs, cat.rec[src]) and torch.equal(rr, cat.radius[src])
+
+
 def test_sharded_step_world1_matches_train_step(nccl_world1, train_small):
     """World size 1 (NCCL self-exchange) against train_step: losses to float
     rounding of the report and, with fixed-order sums
