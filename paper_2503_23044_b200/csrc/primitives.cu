@@ -514,22 +514,80 @@ static int sort_pairs(const K *kin, const uint32_t *vin, K *kout, uint32_t *vout
   return VSX_OK;
 }
 
-__global__ void iota_kernel(uint32_t *__restrict__ v, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (uint32_t)i;
-}
-
-// After a stable sort by z, runs of equal z keep input order; reorder each
-// run by gid so the result is lexsort((gid, z)) (renderer.py:197). Runs are
-// almost always length 1, so one thread per run start suffices.
 // 32-bit monotone proxy of a positive float64 z: round toward zero to float32
 // (order-preserving, never reverses two keys); ~0 marks culled entries.
-__global__ void z_proxy_kernel(const uint64_t *__restrict__ zkey, int64_t n,
-                               uint32_t *__restrict__ k32) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t k = zkey[i];
-  k32[i] = (k == ~0ull) ? 0xFFFFFFFFu : __float_as_uint(__double2float_rz(__longlong_as_double((long long)k)));
+// Proxies + identity values + the four 8-bit digit histograms in one
+// pass (the sort then runs with VSX_SORT_HIST_IN_WS): 8 consecutive items
+// per thread, vector loads / stores, run-compressed shared-memory counts as
+// os_hist_kernel (the high digits come in long runs).
+#ifndef VSX_ZPROXY_PER
+#define VSX_ZPROXY_PER 8
+#endif
+__global__ void __launch_bounds__(256) z_proxy_hist_kernel(const uint64_t *__restrict__ zkey,
+                                                           int64_t n, uint32_t *__restrict__ k32,
+                                                           uint32_t *__restrict__ iota,
+                                                           uint32_t *__restrict__ gh) {
+  constexpr int kPer = VSX_ZPROXY_PER;
+  __shared__ uint32_t h[4][256];
+  for (int p = 0; p < 4; ++p) h[p][threadIdx.x] = 0u;
+  __syncthreads();
+  for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kPer; b0 < n;
+       b0 += (int64_t)gridDim.x * blockDim.x * kPer) {
+    const int m = (int)min((int64_t)kPer, n - b0);
+    uint32_t kk[kPer];
+    if (m == kPer) {
+      const ulonglong2 *z2 = reinterpret_cast<const ulonglong2 *>(zkey + b0);
+#pragma unroll
+      for (int j = 0; j < kPer / 2; ++j) {
+        const ulonglong2 v = z2[j];
+        kk[2 * j] = v.x == ~0ull ? 0xFFFFFFFFu
+                                 : __float_as_uint(__double2float_rz(__longlong_as_double((long long)v.x)));
+        kk[2 * j + 1] = v.y == ~0ull ? 0xFFFFFFFFu
+                                     : __float_as_uint(__double2float_rz(__longlong_as_double((long long)v.y)));
+      }
+      uint4 *k4 = reinterpret_cast<uint4 *>(k32 + b0);
+      uint4 *i4 = reinterpret_cast<uint4 *>(iota + b0);
+#pragma unroll
+      for (int j = 0; j < kPer / 4; ++j) {
+        k4[j] = make_uint4(kk[4 * j], kk[4 * j + 1], kk[4 * j + 2], kk[4 * j + 3]);
+        const uint32_t b = (uint32_t)b0 + 4 * j;
+        i4[j] = make_uint4(b, b + 1, b + 2, b + 3);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        kk[j] = 0u;
+        if (j < m) {
+          const uint64_t k = zkey[b0 + j];
+          kk[j] = k == ~0ull ? 0xFFFFFFFFu
+                             : __float_as_uint(__double2float_rz(__longlong_as_double((long long)k)));
+          k32[b0 + j] = kk[j];
+          iota[b0 + j] = (uint32_t)(b0 + j);
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      uint32_t cur = (kk[0] >> (8 * p)) & 255u, c = 1;
+#pragma unroll
+      for (int j = 1; j < kPer; ++j) {
+        if (j < m) {
+          const uint32_t d = (kk[j] >> (8 * p)) & 255u;
+          if (d == cur) {
+            ++c;
+          } else {
+            atomicAdd(&h[p][cur], c);
+            cur = d;
+            c = 1;
+          }
+        }
+      }
+      atomicAdd(&h[p][cur], c);
+    }
+  }
+  __syncthreads();
+  for (int p = 0; p < 4; ++p)
+    if (h[p][threadIdx.x]) atomicAdd(gh + 256 * p + threadIdx.x, h[p][threadIdx.x]);
 }
 
 // Runs of equal 32-bit proxies (float32 collisions) are re-sorted by the exact
@@ -579,6 +637,22 @@ __global__ void fix_proxy_runs_zgid_kernel(const uint32_t *__restrict__ k32,
 
 using namespace vsx;
 
+// float32 proxies + identity values + digit histograms in one kernel, then
+// the four onesweep passes on the proxies (histograms taken from the
+// workspace)
+static int proxy_and_sort(const uint64_t *zkey, int64_t n, uint32_t *k32, uint32_t *iota,
+                          uint32_t *k32s, uint32_t *order, char *sort_ws, size_t sort_ws_bytes,
+                          cudaStream_t st) {
+  uint32_t *gh = reinterpret_cast<uint32_t *>(sort_ws + vsx_sort_hist_offset(n));
+  VSX_CUDA_TRY(cudaMemsetAsync(gh, 0, sizeof(uint32_t) * 4 * 256, st));
+  const int64_t per_block = 256 * VSX_ZPROXY_PER;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + per_block - 1) / per_block, 8 * 148);
+  z_proxy_hist_kernel<<<blocks, 256, 0, st>>>(zkey, n, k32, iota, gh);
+  VSX_LAUNCH_CHECK("z_proxy_hist");
+  return sort_pairs<uint32_t>(k32, iota, k32s, order, n, 0, 32, VSX_SORT_HIST_IN_WS, sort_ws,
+                              sort_ws_bytes, st);
+}
+
 extern "C" size_t vsx_sort_splats_ws_bytes(int64_t n) {
   return 2 * align256(sizeof(uint32_t) * n) + align256(sizeof(uint32_t) * n) + sort_ws_bytes(n);
 }
@@ -595,12 +669,8 @@ extern "C" int vsx_sort_splats_z(const uint64_t *zkey, int64_t n, uint32_t *orde
   p += align256(sizeof(uint32_t) * n);
   uint32_t *iota = reinterpret_cast<uint32_t *>(p);
   p += align256(sizeof(uint32_t) * n);
-  z_proxy_kernel<<<grid_for(n, 256), 256, 0, st>>>(zkey, n, k32);
-  VSX_LAUNCH_CHECK("z_proxy");
-  iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(iota, n);
-  VSX_LAUNCH_CHECK("iota");
-  int rc = sort_pairs<uint32_t>(k32, iota, k32s, order, n, 0, 32, 0, p,
-                                ws_bytes - 3 * align256(sizeof(uint32_t) * n), st);
+  int rc = proxy_and_sort(zkey, n, k32, iota, k32s, order, p,
+                          ws_bytes - 3 * align256(sizeof(uint32_t) * n), st);
   if (rc) return rc;
   fix_proxy_runs_kernel<<<grid_for(n, 256), 256, 0, st>>>(k32s, zkey, order, n);
   VSX_LAUNCH_CHECK("fix_proxy_runs");
@@ -623,12 +693,8 @@ extern "C" int vsx_sort_z_gid(const double *z, const int64_t *gid, uint32_t *ord
   p += align256(sizeof(uint32_t) * n);
   uint32_t *iota = reinterpret_cast<uint32_t *>(p);
   p += align256(sizeof(uint32_t) * n);
-  z_proxy_kernel<<<grid_for(n, 256), 256, 0, st>>>(zkey, n, k32);
-  VSX_LAUNCH_CHECK("z_proxy");
-  iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(iota, n);
-  VSX_LAUNCH_CHECK("iota");
-  int rc = sort_pairs<uint32_t>(k32, iota, k32s, order, n, 0, 32, 0, p,
-                                ws_bytes - 3 * align256(sizeof(uint32_t) * n), st);
+  int rc = proxy_and_sort(zkey, n, k32, iota, k32s, order, p,
+                          ws_bytes - 3 * align256(sizeof(uint32_t) * n), st);
   if (rc) return rc;
   fix_proxy_runs_zgid_kernel<<<grid_for(n, 256), 256, 0, st>>>(k32s, zkey, gid, order, n);
   VSX_LAUNCH_CHECK("fix_proxy_runs_zgid");
