@@ -117,20 +117,6 @@ static int scan_impl(const uint32_t *in, uint32_t *out, int64_t n, uint32_t *ws,
 
 // ------------------------------------------------------------------ select
 
-__global__ void flags_to_u32_kernel(const uint8_t *__restrict__ f, uint32_t *__restrict__ o,
-                                    int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) o[i] = f[i] ? 1u : 0u;
-}
-
-__global__ void select_scatter_kernel(const uint8_t *__restrict__ f,
-                                      const uint32_t *__restrict__ pos, int64_t n,
-                                      int32_t *__restrict__ out, uint32_t *__restrict__ count) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && f[i]) out[pos[i]] = (int32_t)i;
-  if (i == 0) *count = pos[n];
-}
-
 // ------------------------------------------------------------------ radix sort
 
 template <typename K>
@@ -388,6 +374,87 @@ __global__ void __launch_bounds__(kOsBlock) os_pass_kernel(
     kout[pos] = kk;
     vout[pos] = ov[s];
   }
+}
+
+// Ordered stream compaction in one pass: 2048 flags per CTA (8 per thread),
+// CTA prefix by decoupled look-back over the earlier tiles (tile ids from a
+// ticket, so every predecessor is already running), indices written at
+// their global rank. Replaces flags -> u32, a two-level scan and a scatter.
+constexpr int kSelItems = 8, kSelTile = 256 * kSelItems;
+__global__ void __launch_bounds__(256) select_onepass_kernel(const uint8_t *__restrict__ f,
+                                                             int64_t n, int32_t *__restrict__ out,
+                                                             uint32_t *__restrict__ count,
+                                                             uint32_t *__restrict__ status,
+                                                             uint32_t *__restrict__ ticket) {
+  __shared__ uint32_t s_bid, s_excl, s_w[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (t == 0) s_bid = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t bid = s_bid;
+  const int64_t i0 = bid * kSelTile + (int64_t)t * kSelItems;
+  uint32_t bits = 0;
+  if (i0 + kSelItems <= n && (reinterpret_cast<uintptr_t>(f + i0) & 7) == 0) {
+    const uint64_t v = *reinterpret_cast<const uint64_t *>(f + i0);
+#pragma unroll
+    for (int k = 0; k < kSelItems; ++k) bits |= ((v >> (8 * k)) & 0xffu) ? (1u << k) : 0u;
+  } else {
+#pragma unroll
+    for (int k = 0; k < kSelItems; ++k)
+      if (i0 + k < n && f[i0 + k]) bits |= 1u << k;
+  }
+  const uint32_t c = __popc(bits);
+  uint32_t inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    // CTA total and per-warp bases, then the look-back: 32 predecessors per
+    // step, one per lane, consumed up to the nearest inclusive prefix
+    const uint32_t x = lane < 8 ? s_w[lane] : 0u;
+    uint32_t xi = x;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += y;
+    }
+    if (lane < 8) s_w[lane] = xi - x;
+    const uint32_t agg = __shfl_sync(0xffffffffu, xi, 7);
+    uint32_t *my = status + bid;
+    if (lane == 0) st_relaxed_u32(my, (bid == 0 ? kOsPre : kOsAgg) | agg);
+    uint32_t excl = 0;
+    if (bid > 0) {
+      int64_t p = bid - 1;
+      while (true) {
+        const int64_t q = p - lane;
+        const uint32_t w = q >= 0 ? ld_relaxed_u32(status + q) : kOsPre;  // before tile 0: prefix 0
+        const unsigned pre = __ballot_sync(0xffffffffu, (w & kOsPre) != 0u);
+        const unsigned zero = __ballot_sync(0xffffffffu, w == 0u);
+        const int lim = pre ? __ffs(pre) - 1 : 31;
+        const unsigned need = lim == 31 ? 0xffffffffu : ((1u << (lim + 1)) - 1u);
+        if (zero & need) continue;  // a predecessor has not published: re-read
+        uint32_t v = lane <= lim ? (w & kOsMask) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (pre) break;
+        p -= 32;
+      }
+      if (lane == 0) st_relaxed_u32(my, kOsPre | (excl + agg));
+    }
+    if (lane == 0) {
+      s_excl = excl;
+      if ((bid + 1) * kSelTile >= n) *count = excl + agg;
+    }
+  }
+  __syncthreads();
+  uint32_t pos = s_excl + s_w[warp] + inc - c;
+#pragma unroll
+  for (int k = 0; k < kSelItems; ++k)
+    if (bits & (1u << k)) out[pos++] = (int32_t)(i0 + k);
 }
 
 struct SortWs {
@@ -732,20 +799,15 @@ extern "C" int vsx_select(const uint8_t *flags, int64_t n, int32_t *out_idx,
     VSX_CUDA_TRY(cudaMemsetAsync(out_count, 0, sizeof(uint32_t), st));
     return VSX_OK;
   }
-  const size_t need = align256(sizeof(uint32_t) * (n + 1)) + align256(sizeof(uint32_t) * n) +
-                      vsx_scan_ws_bytes(n);
+  const int64_t nt = (n + kSelTile - 1) / kSelTile;
+  const size_t need = sizeof(uint32_t) * (nt + 1);
   VSX_REQUIRE(ws_bytes >= need, "select: workspace %zu < %zu", ws_bytes, need);
-  char *p = static_cast<char *>(ws);
-  uint32_t *pos = reinterpret_cast<uint32_t *>(p);
-  p += align256(sizeof(uint32_t) * (n + 1));
-  uint32_t *ones = reinterpret_cast<uint32_t *>(p);
-  p += align256(sizeof(uint32_t) * n);
-  flags_to_u32_kernel<<<grid_for(n, 256), 256, 0, st>>>(flags, ones, n);
-  VSX_LAUNCH_CHECK("flags_to_u32");
-  int rc = scan_impl(ones, pos, n, reinterpret_cast<uint32_t *>(p), st);
-  if (rc) return rc;
-  select_scatter_kernel<<<grid_for(n, 256), 256, 0, st>>>(flags, pos, n, out_idx, out_count);
-  VSX_LAUNCH_CHECK("select_scatter");
+  VSX_REQUIRE(n < ((int64_t)1 << 30), "select: n >= 2^30");
+  uint32_t *status = static_cast<uint32_t *>(ws);
+  VSX_CUDA_TRY(cudaMemsetAsync(status, 0, need, st));
+  select_onepass_kernel<<<(unsigned)nt, 256, 0, st>>>(flags, n, out_idx, out_count, status,
+                                                       status + nt);
+  VSX_LAUNCH_CHECK("select");
   return VSX_OK;
 }
 
