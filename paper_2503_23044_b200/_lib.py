@@ -167,6 +167,13 @@ def ptr(t) -> c_void_p:
     return c_void_p(t.data_ptr())
 
 
-def stream() -> c_void_p:
+def raw_stream() -> int:
+    """cudaStream_t of torch's current stream (the C calls, without the
+    Python-level device lookup of torch.cuda.current_stream(): ~15 us per call
+    on the host, which a many-view step pays several times per view)."""
     import torch
-    return c_void_p(torch.cuda.current_stream().cuda_stream)
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
+
+
+def stream() -> c_void_p:
+    return c_void_p(raw_stream())

@@ -55,7 +55,7 @@ _WORKSPACES: dict[int, Workspace] = {}
 
 
 def workspace() -> Workspace:
-    key = torch.cuda.current_stream().cuda_stream
+    key = _lib.raw_stream()
     ws = _WORKSPACES.get(key)
     if ws is None:
         ws = _WORKSPACES[key] = Workspace()
@@ -306,8 +306,11 @@ class ProjectLaunch:
 
 
 def project_launch(means, opacity, color, scale, quat, normal, view: CameraView,
-                   status: torch.Tensor) -> ProjectLaunch:
-    """K3 projection + (z, batch-order) sort, no host sync."""
+                   status: torch.Tensor, sort: bool = True) -> ProjectLaunch:
+    """K3 projection + (z, batch-order) sort, no host sync. ``sort=False``
+    (the sharded step's owners, whose rows the renderer merges in (z, gid)
+    order anyway): only the kept splats are compacted, in batch order, by
+    one vsx_select pass instead of the radix sort."""
     g = int(means.shape[0])
     rec = torch.empty((max(g, 1), REC_F32), dtype=torch.float32, device="cuda")
     key = torch.empty(max(g, 1), dtype=torch.int64, device="cuda")
@@ -316,7 +319,13 @@ def project_launch(means, opacity, color, scale, quat, normal, view: CameraView,
     call("vsx_project_fwd", ptr(means), ptr(opacity), ptr(color), ptr(scale), ptr(quat),
          ptr(normal), g, view.to_abi(), ptr(rec), ptr(key), ptr(rad), ptr(kept), ptr(status),
          stream())
-    order = sort_splats_z(key[:g], g) if g else None
+    if not g:
+        order = None
+    elif sort:
+        order = sort_splats_z(key[:g], g)
+    else:
+        # culled splats carry key ~0 (vsx_project_fwd)
+        order, _cnt = select_async((key[:g] != -1).view(torch.uint8))
     return ProjectLaunch(rec, key, rad, kept, order, g)
 
 

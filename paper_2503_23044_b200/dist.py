@@ -813,7 +813,7 @@ class CudaShardBackend:
             self.gaussians += dec.count
             launched.append((active, dec, D.project_launch(
                 dec.means, dec.opacity, dec.color, dec.scale, dec.quat, dec.normal, views[v],
-                self.status)))
+                self.status, sort=False)))
         yield
         kept = torch.cat([pl.kept for _, _, pl in launched]).cpu().tolist() if launched else []
         out = {}
