@@ -207,6 +207,10 @@ int vsx_gather_splats(const vsx_splat *rec, const double *radius, const uint32_t
  * 64-byte record, float64 z, float64 radius, int64 gid, 8 bytes of padding
  * (16-byte aligned rows for the all-to-all buffer). Pack n rows into out. */
 #define VSX_SPLAT_ROW_BYTES 96
+/* Owner-side payload keys: gid[i] = active[src[i] / n] * n + src[i] % n and
+ * z[i] = key[src[i]] for the n_kept kept splats (src: decode batch indices). */
+int vsx_payload_keys(const int32_t *active, const uint32_t *src, const uint64_t *key,
+                     int32_t n_kept, int32_t n, int64_t *gid, uint64_t *z, vsx_stream s);
 int vsx_pack_splat_rows(const vsx_splat *rec, const double *z, const double *radius,
                         const int64_t *gid, int32_t n, uint8_t *out, vsx_stream s);
 /* Sort keys of n received rows: row i is rows[rowmap[i]] (rowmap NULL: rows[i]). */

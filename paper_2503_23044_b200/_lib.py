@@ -82,6 +82,7 @@ _SIGS = {
     "vsx_project_fwd": ([P, P, P, P, P, P, c_i32, VsxCamera, P, P, P, P, P, P], c_i32),
     "vsx_gather_splats": ([P, P, P, c_i32, P, P, P], c_i32),
     "vsx_scatter_rows_f32": ([P, P, c_i32, c_i32, P, P], c_i32),
+    "vsx_payload_keys": ([P, P, P, c_i32, c_i32, P, P, P], c_i32),
     "vsx_pack_splat_rows": ([P, P, P, P, c_i32, P, P], c_i32),
     "vsx_splat_rows_keys": ([P, P, c_i32, P, P, P], c_i32),
     "vsx_gather_splat_rows": ([P, P, P, c_i32, P, P, P], c_i32),

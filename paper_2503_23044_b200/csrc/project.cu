@@ -572,7 +572,33 @@ __global__ void gather_splat_rows_kernel(const uint8_t *__restrict__ rows,
   if (part == 0) rout[i] = __longlong_as_double(reinterpret_cast<const longlong2 *>(row)[4].y);
 }
 
+// Owner-side payload keys of the sharded step: for kept splat i (decode
+// batch index src[i]) the global gaussian id active[src / n] * n + src % n
+// and its float64 z bits.
+__global__ void payload_keys_kernel(const int32_t *__restrict__ active,
+                                    const uint32_t *__restrict__ src,
+                                    const uint64_t *__restrict__ key, int32_t n_kept, int32_t n,
+                                    int64_t *__restrict__ gid, uint64_t *__restrict__ z) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_kept) return;
+  const uint32_t s = src[i];
+  gid[i] = (int64_t)active[s / (uint32_t)n] * n + (int64_t)(s % (uint32_t)n);
+  z[i] = key[s];
+}
+
 }  // namespace vsx
+
+extern "C" int vsx_payload_keys(const int32_t *active, const uint32_t *src, const uint64_t *key,
+                                int32_t n_kept, int32_t n, int64_t *gid, uint64_t *z,
+                                vsx_stream s) {
+  VSX_REQUIRE(n_kept >= 0 && n >= 1, "payload_keys: bad arguments");
+  if (n_kept == 0) return VSX_OK;
+  VSX_REQUIRE(active && src && key && gid && z, "payload_keys: null pointer");
+  payload_keys_kernel<<<grid_for(n_kept, 256), 256, 0, as_stream(s)>>>(active, src, key, n_kept,
+                                                                      n, gid, z);
+  VSX_LAUNCH_CHECK("payload_keys");
+  return VSX_OK;
+}
 
 extern "C" int vsx_pack_splat_rows(const vsx_splat *rec, const double *z, const double *radius,
                                    const int64_t *gid, int32_t n, uint8_t *out, vsx_stream s) {

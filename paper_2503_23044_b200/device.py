@@ -120,7 +120,7 @@ def select_async(flags: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
     """Ordered indices of non-zero u8 flags, capacity-sized, and the device count."""
     n = int(flags.numel())
     idx = _u32(n)
-    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int32, device="cuda")   # written by vsx_select
     lib = _lib.load()
     wp, wb = workspace().get(lib.vsx_sort_ws_bytes(n))
     call("vsx_select", ptr(flags), n, ptr(idx), ptr(cnt), wp, wb, stream())
@@ -315,7 +315,9 @@ def project_launch(means, opacity, color, scale, quat, normal, view: CameraView,
     rec = torch.empty((max(g, 1), REC_F32), dtype=torch.float32, device="cuda")
     key = torch.empty(max(g, 1), dtype=torch.int64, device="cuda")
     rad = torch.empty(max(g, 1), dtype=torch.float64, device="cuda")
-    kept = torch.zeros(1, dtype=torch.int32, device="cuda")
+    # sort=False: the kept count comes from the compaction, and the
+    # projection's own counter is scratch (not zeroed, never read)
+    kept = (torch.zeros if sort or not g else torch.empty)(1, dtype=torch.int32, device="cuda")
     call("vsx_project_fwd", ptr(means), ptr(opacity), ptr(color), ptr(scale), ptr(quat),
          ptr(normal), g, view.to_abi(), ptr(rec), ptr(key), ptr(rad), ptr(kept), ptr(status),
          stream())
@@ -325,7 +327,7 @@ def project_launch(means, opacity, color, scale, quat, normal, view: CameraView,
         order = sort_splats_z(key[:g], g)
     else:
         # culled splats carry key ~0 (vsx_project_fwd)
-        order, _cnt = select_async((key[:g] != -1).view(torch.uint8))
+        order, kept = select_async((key[:g] != -1).view(torch.uint8))
     return ProjectLaunch(rec, key, rad, kept, order, g)
 
 

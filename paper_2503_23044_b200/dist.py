@@ -817,12 +817,17 @@ class CudaShardBackend:
         yield
         kept = torch.cat([pl.kept for _, _, pl in launched]).cpu().tolist() if launched else []
         out = {}
+        from ._lib import call, ptr, stream
         for v, (active, dec, pl), k in zip(vs, launched, kept):
             P = D.project_finish(pl, k if pl.g else 0)
-            src = P.src.long()
-            gid = active.long()[src // st.n] * st.n + src % st.n
+            n = P.count
+            gid = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")[:n]
+            z = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")[:n]
+            if n:
+                call("vsx_payload_keys", ptr(active), ptr(P.src), ptr(pl.key), n, st.n,
+                     ptr(gid), ptr(z), stream())
             self.work[v] = (active, dec, P)
-            out[v] = SplatPayload(P.rec, P.zkey.view(torch.float64), P.radius, gid)
+            out[v] = SplatPayload(P.rec, z.view(torch.float64), P.radius, gid)
         return out
 
     def render(self, v: int, view, payload: SplatPayload, image, prior, nprior) -> torch.Tensor:
