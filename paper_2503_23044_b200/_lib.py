@@ -161,11 +161,11 @@ def call(name: str, *args) -> None:
         raise_for_status(rc, name, lib.vsx_last_error().decode(errors="replace"))
 
 
-def ptr(t) -> c_void_p:
-    """Device pointer of a tensor (None -> NULL)."""
-    if t is None:
-        return c_void_p(0)
-    return c_void_p(t.data_ptr())
+def ptr(t):
+    """Device pointer of a tensor as a plain int (None -> NULL): ctypes
+    converts ints for c_void_p arguments and struct fields faster than
+    c_void_p objects (a call passes up to 20 of them)."""
+    return None if t is None else t.data_ptr()
 
 
 def raw_stream() -> int:

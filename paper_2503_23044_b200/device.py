@@ -449,7 +449,7 @@ def bin_tiles(P: Projected, width: int, height: int) -> Bins:
     if T <= 65536:
         # the emission builds the sort's digit histograms on the fly
         wp, wb = workspace().get(lib.vsx_sort_ws_bytes(total))
-        hist = ctypes.c_void_p(wp.value + int(lib.vsx_sort_hist_offset(total)))
+        hist = wp + int(lib.vsx_sort_hist_offset(total))
         call("vsx_bin_emit_hist", ptr(P.rec), ptr(P.radius), n, width, height, ptr(soff),
              ptr(tiles), ptr(ranks), hist, stream())
         skeys = torch.empty_like(tiles)

@@ -850,9 +850,9 @@ class CudaShardBackend:
             pn, pnv = _to_device_image(nprior[0], (H, W, 3)), _mask_u8(nprior[1], (H, W))
         # the depth / normal terms are means over the views that carry a prior
         # (trainer.py:296-306, losses.py:84): normalised by that global count
-        loss = VsxLossDesc(gt_rgb=gt.data_ptr(), prior_depth=ptr(pd).value,
-                           prior_depth_valid=ptr(pv).value, prior_normal=ptr(pn).value,
-                           prior_normal_valid=ptr(pnv).value, rgb_scale=1.0 / (self.B * H * W * 3),
+        loss = VsxLossDesc(gt_rgb=gt.data_ptr(), prior_depth=ptr(pd),
+                           prior_depth_valid=ptr(pv), prior_normal=ptr(pn),
+                           prior_normal_valid=ptr(pnv), rgb_scale=1.0 / (self.B * H * W * 3),
                            depth_weight=w2 / len(self.have) if pd is not None else 0.0,
                            normal_weight=wn / len(self.have_n) / 3.0 if pn is not None else 0.0,
                            sums=sums.data_ptr(), counts=counts.data_ptr(),
@@ -922,8 +922,8 @@ class CudaShardBackend:
         (P, Bn, order), view, loss, keep, R = self.pending.pop(it)
         if extra is not None:
             ex_rgb, ex_nrm, ex_dep = extra
-            loss.extra_rgb, loss.extra_normal = ptr(ex_rgb).value, ptr(ex_nrm).value
-            loss.extra_depth = ptr(ex_dep).value
+            loss.extra_rgb, loss.extra_normal = ptr(ex_rgb), ptr(ex_nrm)
+            loss.extra_depth = ptr(ex_dep)
             keep = (keep, extra)
         det = bool(getattr(st.cfg, "deterministic", False))
         gs = D.raster_backward(P, Bn, view, R, loss=loss, deterministic=det)

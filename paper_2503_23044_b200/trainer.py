@@ -650,14 +650,14 @@ def train_step(state: TrainState, views: list[CameraView], images: list,
             pn = pnv = None
         ex_rgb, ex_nrm, ex_dep = extra if extra is not None else (None, None, None)
         return VsxLossDesc(
-            gt_rgb=gt.data_ptr(), prior_depth=ptr(pd).value, prior_depth_valid=ptr(pv).value,
-            prior_normal=ptr(pn).value, prior_normal_valid=ptr(pnv).value,
+            gt_rgb=gt.data_ptr(), prior_depth=ptr(pd), prior_depth_valid=ptr(pv),
+            prior_normal=ptr(pn), prior_normal_valid=ptr(pnv),
             rgb_scale=1.0 / (B * view.height * view.width * 3),
             depth_weight=(w2 / len(have)) if vi in have else 0.0,
             normal_weight=(wn / len(have_n) / 3.0) if vi in have_n else 0.0,
             sums=sums[vi].data_ptr(), counts=counts[vi].data_ptr(),
-            extra_rgb=ptr(ex_rgb).value, extra_normal=ptr(ex_nrm).value,
-            extra_depth=ptr(ex_dep).value, live_pairs=live.data_ptr())
+            extra_rgb=ptr(ex_rgb), extra_normal=ptr(ex_nrm),
+            extra_depth=ptr(ex_dep), live_pairs=live.data_ptr())
 
     def take_front(vi):
         nonlocal gaussians, isects
