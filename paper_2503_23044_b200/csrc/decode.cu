@@ -773,10 +773,10 @@ __global__ void decoder_fwd_image_kernel(vsx_decoder W, float4 *__restrict__ img
 }
 
 #ifndef VSX_DFW_WARPS
-#define VSX_DFW_WARPS 16
+#define VSX_DFW_WARPS 8
 #endif
 #ifndef VSX_DFW_MINB
-#define VSX_DFW_MINB 1
+#define VSX_DFW_MINB 2
 #endif
 constexpr int kDfwWarps = VSX_DFW_WARPS;
 
