@@ -562,10 +562,14 @@ __device__ __forceinline__ void cp_async16(float *dst, const float *src, int byt
                : "memory");
 }
 
-constexpr int kDbwWarps = 8;
+#ifndef VSX_DBW_WARPS
+#define VSX_DBW_WARPS 4
+#endif
+constexpr int kDbwWarps = VSX_DBW_WARPS;
+constexpr int kDbwCtas = 16 / kDbwWarps;  // CTAs per SM: 16 warps at the 128-register budget
 constexpr int kDbwGoStride = 24, kDbwHStride = 20;  // staged row strides (floats)
 
-__global__ void __launch_bounds__(kDbwWarps * 32, 2) decode_bwd_anchor_mma_kernel(
+__global__ void __launch_bounds__(kDbwWarps * 32, kDbwCtas) decode_bwd_anchor_mma_kernel(
     int n, const float4 *__restrict__ img, const int32_t *__restrict__ active, int32_t n_active,
     const double *__restrict__ centers, const float *__restrict__ emb,
     const float *__restrict__ log_scale, const float *__restrict__ offsets, vsx_camera cam,
@@ -1301,7 +1305,8 @@ extern "C" int vsx_decode_bwd(vsx_decoder W, vsx_decoder_grads dW, const int32_t
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int warps_needed = (n_active + 15) / 16;
-    const int grid = std::max(1, std::min(2 * sms, (warps_needed + kDbwWarps - 1) / kDbwWarps));
+    const int grid =
+        std::max(1, std::min(kDbwCtas * sms, (warps_needed + kDbwWarps - 1) / kDbwWarps));
     decode_bwd_anchor_mma_kernel<<<grid, kDbwWarps * 32, smem, st>>>(
         n, dimg, active, n_active, centers, emb, log_scale, offsets, cam, lod_ref, cache_h,
         g_means, g_o, g_emb, g_log_scale, xs, g_pre, smem_img);
