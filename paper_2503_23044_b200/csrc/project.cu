@@ -351,8 +351,11 @@ __global__ void bin_emit_kernel(const vsx_splat *__restrict__ rec,
 // per batch gaussian i with its sorted rank inv[i] (-1 = culled -> zeros), so
 // the per-gaussian inputs and all six outputs are read / written in order and
 // only the 64-byte record and the 13-float gradient row are gathered.
+#ifndef VSX_PBW_MINB
+#define VSX_PBW_MINB 6
+#endif
 template <bool kBatch>
-__global__ void __launch_bounds__(128) project_bwd_kernel(
+__global__ void __launch_bounds__(128, VSX_PBW_MINB) project_bwd_kernel(
     const double *__restrict__ means, const float *__restrict__ scale,
     const float *__restrict__ quat, const float *__restrict__ normal,
     const vsx_splat *__restrict__ rec, const float *__restrict__ gs, int32_t n, vsx_camera cam,
