@@ -262,7 +262,10 @@ __global__ void growth_accumulate_kernel(const float *__restrict__ g_means,
 // [11n x anchors] slice of the raw head outputs is staged through shared
 // memory in, and the g_o slice out, so the feature-major rows move as
 // contiguous runs instead of one scattered 4-byte access per (gaussian, row).
-__global__ void __launch_bounds__(256) decode_bwd_gauss_kernel(
+#ifndef VSX_DBG_MINB
+#define VSX_DBG_MINB 4
+#endif
+__global__ void __launch_bounds__(256, VSX_DBG_MINB) decode_bwd_gauss_kernel(
     int n, const int32_t *__restrict__ active, int32_t n_active,
     const float *__restrict__ log_scale, const float *__restrict__ offsets, double max_scale,
     const float *__restrict__ cache_o, const float *__restrict__ dscale,

@@ -270,7 +270,10 @@ __global__ void __launch_bounds__(256, 1) decode_fwd_tc_kernel(
 // floor(256 / n) whole anchors and stages their [11n x anchors] slice of the
 // feature-major cache_o through shared memory, so the raw outputs are read as
 // contiguous row runs instead of one scattered 4-byte load per (gaussian, row).
-__global__ void __launch_bounds__(256) decode_gauss_kernel(
+#ifndef VSX_DG_MINB
+#define VSX_DG_MINB 5
+#endif
+__global__ void __launch_bounds__(256, VSX_DG_MINB) decode_gauss_kernel(
     int n, const int32_t *__restrict__ active, int32_t n_active, const double *__restrict__ centers,
     const float *__restrict__ log_scale, const float *__restrict__ offsets, double max_scale,
     const float *__restrict__ cache_o, double *__restrict__ means, float *__restrict__ opacity,
