@@ -773,37 +773,51 @@ __global__ void __launch_bounds__(256, 1) decoder_wgrad_tc2_kernel(
   if (warp == 0) umma::tmem_dealloc(tbase, 512);
 }
 
-// Element e of the partials summed over the CTAs in order (deterministic),
-// added into the gradient it maps to (one thread per element, no atomics).
-__global__ void decoder_wgrad_tc2_reduce(const float *__restrict__ partial, int ctas, int n,
-                                         vsx_decoder_grads dW) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= kWgPartial) return;
+// Element e of the partials summed over the CTAs in a fixed order
+// (deterministic): four threads per element each sum a quarter of the CTAs
+// in order, the quarters are added in order, and the result goes into the
+// gradient it maps to (no atomics). 64 elements per 256-thread block.
+__global__ void __launch_bounds__(256) decoder_wgrad_tc2_reduce(const float *__restrict__ partial,
+                                                                int ctas, int n,
+                                                                vsx_decoder_grads dW) {
+  __shared__ float s_q[4][64];
+  const int el = threadIdx.x & 63, qi = threadIdx.x >> 6;
+  const int e = blockIdx.x * 64 + el;
   const int nout = 11 * n;
   int h = 0, col = 0, j = 0;
-  bool w1 = false;
-  if (e < 128 * kWgN1) {
-    j = e / kWgN1;
-    col = e % kWgN1;
-    if (j >= nout || col > 192) return;
-  } else {
-    const int f = e - 128 * kWgN1;
-    j = f / kWgN2;        // hidden unit m
-    col = f % kWgN2;      // input i (36 = bias)
-    if (j >= 192 || col > kInDim) return;
-    w1 = true;
+  bool w1 = false, valid = e < kWgPartial;
+  if (valid) {
+    if (e < 128 * kWgN1) {
+      j = e / kWgN1;
+      col = e % kWgN1;
+      valid = j < nout && col <= 192;
+    } else {
+      const int f = e - 128 * kWgN1;
+      j = f / kWgN2;        // hidden unit m
+      col = f % kWgN2;      // input i (36 = bias)
+      valid = j < 192 && col <= kInDim;
+      w1 = true;
+    }
   }
-  // 8 independent loads in flight, summed in CTA order
   float sum = 0.f;
-  int c = 0;
-  for (; c + 8 <= ctas; c += 8) {
-    float v[8];
+  if (valid) {
+    const int q = (ctas + 3) / 4;
+    const int c0 = qi * q, c1 = min(ctas, c0 + q);
+    int c = c0;
+    // 8 independent loads in flight, summed in CTA order
+    for (; c + 8 <= c1; c += 8) {
+      float v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = partial[(size_t)(c + u) * kWgPartial + e];
+      for (int u = 0; u < 8; ++u) v[u] = partial[(size_t)(c + u) * kWgPartial + e];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) sum += v[u];
+      for (int u = 0; u < 8; ++u) sum += v[u];
+    }
+    for (; c < c1; ++c) sum += partial[(size_t)c * kWgPartial + e];
   }
-  for (; c < ctas; ++c) sum += partial[(size_t)c * kWgPartial + e];
+  s_q[qi][el] = sum;
+  __syncthreads();
+  if (qi != 0 || !valid) return;
+  sum = ((s_q[0][el] + s_q[1][el]) + s_q[2][el]) + s_q[3][el];
   if (w1) {
     const int hh = j / 64, mm = j % 64;
     if (col < kInDim) dW.w1[hh][(size_t)col * 64 + mm] += sum;
@@ -833,7 +847,7 @@ int decoder_wgrad_tc2(const float *g_o, const float *cache_h, const float *g_pre
   VSX_REQUIRE(ctas >= 1, "decoder_wgrad_tc2: partial buffer too small");
   decoder_wgrad_tc2_kernel<<<ctas, 256, smem, st>>>(g_o, cache_h, g_pre, xs, K, ld, n, partial);
   VSX_LAUNCH_CHECK("decoder_wgrad_tc2");
-  decoder_wgrad_tc2_reduce<<<(kWgPartial + 255) / 256, 256, 0, st>>>(partial, ctas, n, dW);
+  decoder_wgrad_tc2_reduce<<<(kWgPartial + 63) / 64, 256, 0, st>>>(partial, ctas, n, dW);
   VSX_LAUNCH_CHECK("decoder_wgrad_tc2_reduce");
   return VSX_OK;
 }
